@@ -1,0 +1,455 @@
+"""CPU oracle for the 2:4 FFN hot path -- TEST INFRASTRUCTURE ONLY.
+
+This module restates, in plain numpy (float64, fixed accumulation order), the
+reference `sparse24` algorithms that the B200 path replaces.  It is the checker
+for the CUDA path: only `tests/`, `__graft_entry__.smoke()` and the
+`cpu_baseline` / `--impl reference` legs of `bench.py` may import it.  The
+product package (`paper_2404_01847_b200`) never imports it and has no CPU
+fallback.
+
+Parity is pinned (see tests/test_oracle_golden.py):
+  * the pattern table against the reference golden file (md5 313a02e7...);
+  * mask search, compress, FST forward/backward and masked decay against
+    golden vectors produced by the reference package itself
+    (tests/golden/make_golden.py, committed .npz fixtures).
+SwiGLU is NOT in the reference (`gated_ffn.py:47-50`); the `silu_gate` rows
+below are a restatement of GEGLU with silu substituted -- parity unpinned.
+
+Where the compiled reference kernels are available (oracle/_ref/_core*.so,
+built by oracle/Makefile from /root/reference/pkg/src/sparse24/_core.pyx),
+`ref_kernels()` returns that module so the CPU baseline can time the
+reference's own compiled loops.
+
+Reference citations are to /root/reference/pkg/src/sparse24/<file>:<line>.
+"""
+
+from __future__ import annotations
+
+import glob
+import importlib.util
+import itertools
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+try:  # scipy is the reference's erf (gated_ffn.py:23, _core_py.py:12)
+    from scipy.special import erf as _erf
+except Exception:  # pragma: no cover - scipy is present in this image
+    _erf = np.vectorize(math.erf)
+
+RSQRT2 = 0.7071067811865476  # _core.pyx:19, gated_ffn.py:43
+RSQRT2PI = 0.3989422804014327  # gated_ffn.py:44
+
+
+# ---------------------------------------------------------------------------
+# errors (matrix.py:11-16)
+
+
+class ShapeError(ValueError):
+    """Operand shapes violate an operation's preconditions (matrix.py:11)."""
+
+
+class FormatError(ValueError):
+    """A mask / compressed buffer violates its invariants (matrix.py:15)."""
+
+
+# ---------------------------------------------------------------------------
+# the 90 transposable 4x4 patterns (sparsity.py:203-222)
+
+
+def _row_choices():
+    # every 4-bit row with exactly two ones, as tuples
+    return [r for r in itertools.product((0, 1), repeat=4) if sum(r) == 2]
+
+
+def pattern_table() -> tuple[np.ndarray, np.ndarray]:
+    """(patterns (90,4,4) uint8, positions (90,8) int32).
+
+    Canonical order = ascending lexicographic order of the row-major 16-bit
+    tuples (sparsity.py:210-216); positions = kept flat indices ascending
+    (sparsity.py:203-205).
+    """
+    rows = _row_choices()
+    found = []
+    for r0, r1, r2, r3 in itertools.product(rows, repeat=4):
+        colsum = [r0[j] + r1[j] + r2[j] + r3[j] for j in range(4)]
+        if colsum == [2, 2, 2, 2]:
+            found.append(r0 + r1 + r2 + r3)
+    found.sort()
+    pats = np.array(found, dtype=np.uint8).reshape(-1, 4, 4)
+    pos = np.array([np.flatnonzero(p.reshape(16)) for p in pats], dtype=np.int32)
+    return pats, pos
+
+
+def pattern_text(pats: np.ndarray) -> str:
+    """Text form: one 16-char line per pattern (sparsity.py:180-182)."""
+    return "".join("".join(str(int(b)) for b in p.reshape(16)) + "\n" for p in pats)
+
+
+# ---------------------------------------------------------------------------
+# 4x4 block tiling (sparsity.py:65-79)
+
+
+def blocks16(arr: np.ndarray) -> np.ndarray:
+    r, c = arr.shape
+    if r % 4 or c % 4:
+        raise ShapeError(f"shape {arr.shape} not divisible into 4x4 blocks")
+    return np.ascontiguousarray(arr.reshape(r // 4, 4, c // 4, 4).swapaxes(1, 2).reshape(-1, 16))
+
+
+def unblocks16(b16: np.ndarray, shape) -> np.ndarray:
+    r, c = shape
+    return np.ascontiguousarray(b16.reshape(r // 4, c // 4, 4, 4).swapaxes(1, 2).reshape(r, c))
+
+
+# ---------------------------------------------------------------------------
+# transposable mask search (sparsity.py:258-271; kernel _core.pyx:83-110)
+
+
+def pattern_scores(absblocks: np.ndarray, positions: np.ndarray):
+    """score[b,t] = sum of |w| over the 8 kept positions, accumulated
+    strictly ascending in position (_core.pyx:102-105); best = first argmax
+    (strict '>' so ties keep the lowest pattern index, _core.pyx:106)."""
+    absblocks = np.asarray(absblocks, dtype=np.float64)
+    nb = absblocks.shape[0]
+    scores = np.empty((nb, positions.shape[0]), dtype=np.float64)
+    for t in range(positions.shape[0]):
+        acc = absblocks[:, positions[t, 0]].copy()
+        for p in positions[t, 1:]:
+            acc = acc + absblocks[:, p]
+        scores[:, t] = acc
+    # np.argmax returns the first maximum == sequential strict '>' scan
+    return scores, np.argmax(scores, axis=1).astype(np.int64)
+
+
+def search_pattern_idx(w: np.ndarray) -> np.ndarray:
+    """Per-block canonical pattern index, shape (rows/4, cols/4) uint8."""
+    arr = np.asarray(w, dtype=np.float64)  # sparsity.py:265 casts to f64
+    _, pos = pattern_table()
+    _, best = pattern_scores(np.abs(blocks16(arr)), pos)
+    r, c = arr.shape
+    return best.astype(np.uint8).reshape(r // 4, c // 4)
+
+
+def idx_to_bits(idx: np.ndarray) -> np.ndarray:
+    """Expand per-block pattern indices to the full 0/1 mask (sparsity.py:270-271)."""
+    pats, _ = pattern_table()
+    nbr, nbc = idx.shape
+    return unblocks16(pats.reshape(90, 16)[idx.reshape(-1)], (4 * nbr, 4 * nbc))
+
+
+def transposable_search_conv(w: np.ndarray) -> np.ndarray:
+    """Full mask bits (uint8, same shape as w)."""
+    return idx_to_bits(search_pattern_idx(w))
+
+
+def validate_transposable(bits: np.ndarray) -> None:
+    """TransposableMask.validate (sparsity.py:122-131)."""
+    bits = np.asarray(bits)
+    if bits.ndim != 2:
+        raise FormatError("mask must be 2-D")
+    b = blocks16(bits).reshape(-1, 4, 4)
+    if bits.size and bits.max() > 1:
+        raise FormatError("mask bits must be 0/1")
+    if not (b.sum(axis=(1, 2)) == 8).all():
+        raise FormatError("every 4x4 block must contain exactly 8 ones")
+    if not (b.sum(axis=2) == 2).all() or not (b.sum(axis=1) == 2).all():
+        raise FormatError("every block row and column must contain exactly 2 ones")
+
+
+# ---------------------------------------------------------------------------
+# packed 2:4 format (spmm.py:38-147, compress at :92-106)
+
+
+def compress_rowwise(values: np.ndarray, bits: np.ndarray):
+    """Row-wise groups of 4 (row-major group order): kept values (m, k/2) and
+    one meta nibble per group (m, k/4) = i0 | i1 << 2 with i0 < i1
+    (spmm.py:98-104).  `values` is copied verbatim (f64 here)."""
+    m, k = bits.shape
+    if k % 4:
+        raise ShapeError(f"cols={k} not divisible by 4 for row-wise groups")
+    g = np.asarray(bits, dtype=np.uint8).reshape(m, k // 4, 4)
+    if not (g.sum(axis=2) == 2).all() or (g.size and g.max() > 1):
+        raise FormatError("every group of 4 must contain exactly 2 ones")
+    i0 = np.argmax(g, axis=2)  # first set bit
+    i1 = 3 - np.argmax(g[:, :, ::-1], axis=2)  # last set bit
+    v = np.asarray(values).reshape(m, k // 4, 4)
+    r_ix = np.arange(m)[:, None]
+    c_ix = np.arange(k // 4)[None, :]
+    kept = np.stack([v[r_ix, c_ix, i0], v[r_ix, c_ix, i1]], axis=2).reshape(m, k // 2)
+    meta = (i0 | (i1 << 2)).astype(np.uint8)
+    return kept, meta
+
+
+def decompress_rowwise(kept: np.ndarray, meta: np.ndarray, k: int) -> np.ndarray:
+    """Inverse of compress_rowwise; rejects non-ascending meta (spmm.py:61-67)."""
+    m = kept.shape[0]
+    i0 = (meta & 3).astype(np.int64)
+    i1 = ((meta >> 2) & 3).astype(np.int64)
+    if not (i0 < i1).all():
+        raise FormatError("metadata indices must be distinct and ascending")
+    out = np.zeros((m, k // 4, 4), dtype=np.asarray(kept).dtype)
+    kv = np.asarray(kept).reshape(m, k // 4, 2)
+    r_ix = np.arange(m)[:, None]
+    c_ix = np.arange(k // 4)[None, :]
+    out[r_ix, c_ix, i0] = kv[:, :, 0]
+    out[r_ix, c_ix, i1] = kv[:, :, 1]
+    return out.reshape(m, k)
+
+
+# ---------------------------------------------------------------------------
+# gather plan + column-wise sparse product (gated_ffn.py:131-162, _core.pyx:63-80)
+
+
+def gather_plan(bits: np.ndarray, transposed_source: bool):
+    """(take, pos_t): flat source indices of kept entries per row of `bits`
+    (slots ascending), and their contraction positions transposed
+    (gated_ffn.py:142-157)."""
+    m, k = bits.shape
+    g = np.asarray(bits, dtype=np.int64).reshape(m, k // 4, 4)
+    i0 = np.argmax(g, axis=2)
+    i1 = 3 - np.argmax(g[:, :, ::-1], axis=2)
+    base = 4 * np.arange(k // 4, dtype=np.int64)[None, :]
+    cols = np.empty((m, k // 2), dtype=np.int64)
+    cols[:, 0::2] = i0 + base
+    cols[:, 1::2] = i1 + base
+    take = np.arange(m, dtype=np.int64)[:, None] * k + cols
+    if transposed_source:
+        take = (take % k) * m + take // k
+    return take, np.ascontiguousarray(cols.T)
+
+
+def spmm_colwise(a: np.ndarray, values: np.ndarray, pos: np.ndarray) -> np.ndarray:
+    """C = A @ B, B column-wise 2:4 as (values, absolute row positions) of
+    shape (s, n); each output cell accumulates over kept k ascending, no FMA
+    (_core.pyx:63-80, _core_py.py:41-48).  Output column-major."""
+    a = np.asarray(a, dtype=np.float64)
+    values = np.asarray(values, dtype=np.float64)
+    out = np.zeros((a.shape[0], values.shape[1]), dtype=np.float64, order="F")
+    for t in range(values.shape[0]):
+        out += a[:, pos[t, :]] * values[t : t + 1, :]
+    return out
+
+
+def plan_product(a: np.ndarray, w_source: np.ndarray, bits: np.ndarray, transposed_source: bool):
+    """a @ (masked weight).T via the gather plan (gated_ffn.py:159-162)."""
+    take, pos_t = gather_plan(bits, transposed_source)
+    vals = np.ascontiguousarray(w_source, dtype=np.float64).ravel()[take]
+    return spmm_colwise(a, vals.T, pos_t)
+
+
+# ---------------------------------------------------------------------------
+# activations (gated_ffn.py:58-70, _core.pyx:222-250)
+
+
+def gelu(x):
+    x = np.asarray(x, dtype=np.float64)
+    return 0.5 * x * (1.0 + _erf(x * RSQRT2))
+
+
+def gelu_grad(x):
+    x = np.asarray(x, dtype=np.float64)
+    return 0.5 * (1.0 + _erf(x * RSQRT2)) + x * (RSQRT2PI * np.exp(-0.5 * x * x))
+
+
+def silu(x):  # SwiGLU extension: NOT in the reference (parity unpinned)
+    x = np.asarray(x, dtype=np.float64)
+    return x / (1.0 + np.exp(-x))
+
+
+def silu_grad(x):  # SwiGLU extension: NOT in the reference (parity unpinned)
+    x = np.asarray(x, dtype=np.float64)
+    s = 1.0 / (1.0 + np.exp(-x))
+    return s * (1.0 + x * (1.0 - s))
+
+
+def gate(z1, z2, act: str = "geglu"):
+    """gate_gelu (_core.pyx:222-250): act(z1) * z2, column-major result."""
+    f = gelu if act == "geglu" else silu
+    return np.asfortranarray(f(z1) * np.asarray(z2, dtype=np.float64))
+
+
+# ---------------------------------------------------------------------------
+# fully sparse FFN layer (gated_ffn.py:273-373), mvue=False branch
+
+
+@dataclass
+class Layer:
+    """Mirror of FFNLayer (gated_ffn.py:77-128).  `act` is 'gelu', 'relu',
+    'geglu' or 'swiglu' (the last is the unpinned extension).  For gated
+    layers w_in = [u; v] (r_in = 2 d_ff) and bias_in = [b; c]."""
+
+    w_in: np.ndarray  # (r_in, d)
+    bias_in: np.ndarray  # (r_in,)
+    w2: np.ndarray  # (d, d_ff)
+    act: str
+
+    @property
+    def gated(self) -> bool:
+        return self.act in ("geglu", "swiglu")
+
+    @property
+    def d_ff(self) -> int:
+        return self.w2.shape[1]
+
+
+def _activate(layer: Layer, z: np.ndarray) -> np.ndarray:
+    r = layer.d_ff
+    if layer.gated:
+        return gate(z[:, :r], z[:, r:], layer.act)
+    if layer.act == "gelu":
+        return gelu(z)
+    return np.maximum(z, 0.0)
+
+
+def fst_forward(layer: Layer, x: np.ndarray, mask_in, mask_out, exact: bool = True):
+    """Returns dict(z, a, y).  masks None -> dense path (gated_ffn.py:286-289).
+    exact=True runs the reference's gather + ascending spmm route
+    (gated_ffn.py:293-297); exact=False uses BLAS on the masked dense weight,
+    equal to the exact route within 1e-12 (the reference's own check,
+    test_gated_ffn.py:173-179) and fast enough for large parity cases."""
+    x = np.asarray(x, dtype=np.float64)
+    w_in = np.asarray(layer.w_in, dtype=np.float64)
+    w2 = np.asarray(layer.w2, dtype=np.float64)
+    if mask_in is None:
+        z = x @ w_in.T + layer.bias_in
+        a = _activate(layer, z)
+        y = a @ w2.T
+    else:
+        if mask_in.shape != w_in.shape or mask_out.shape != w2.shape:
+            raise ShapeError("mask shapes do not match layer weights")
+        if exact:
+            z = plan_product(x, w_in, mask_in, False)
+            z += layer.bias_in
+            a = _activate(layer, z)
+            y = plan_product(a, w2, mask_out, False)
+        else:
+            z = x @ (w_in * mask_in).T + layer.bias_in
+            a = _activate(layer, z)
+            y = a @ (w2 * mask_out).T
+    return {"x": x, "z": z, "a": a, "y": y}
+
+
+def fst_backward(layer: Layer, fwd: dict, dy: np.ndarray, mask_in, mask_out, exact: bool = True):
+    """mvue=False backward (gated_ffn.py:304-373): dA via the transposed mask,
+    dense dW, activation backward, dX via the transposed mask.  Returns
+    dict(dx, dw_in, dbias_in, dw2, dz)."""
+    dy = np.asarray(dy, dtype=np.float64)
+    if dy.shape != fwd["y"].shape:
+        raise ShapeError(f"upstream shape {dy.shape} != output shape {fwd['y'].shape}")
+    w_in = np.asarray(layer.w_in, dtype=np.float64)
+    w2 = np.asarray(layer.w2, dtype=np.float64)
+    sparse = mask_in is not None
+    if sparse and exact:
+        da = plan_product(dy, w2, np.ascontiguousarray(mask_out.T), True)
+    elif sparse:
+        da = dy @ (w2 * mask_out)
+    else:
+        da = dy @ w2
+    dw2 = dy.T @ fwd["a"]
+    z = fwd["z"]
+    r = layer.d_ff
+    if layer.gated:
+        z1, z2 = z[:, :r], z[:, r:]
+        f, fp = (gelu, gelu_grad) if layer.act == "geglu" else (silu, silu_grad)
+        g1 = da * z2 * fp(z1)
+        g2 = da * f(z1)
+        dz = np.concatenate([g1, g2], axis=1)
+    elif layer.act == "gelu":
+        dz = da * gelu_grad(z)
+    else:
+        dz = da * (z > 0)
+    dbias = dz.sum(axis=0)
+    if sparse and exact:
+        dx = plan_product(dz, w_in, np.ascontiguousarray(mask_in.T), True)
+    elif sparse:
+        dx = dz @ (w_in * mask_in)
+    else:
+        dx = dz @ w_in
+    dw_in = dz.T @ fwd["x"]
+    return {"dx": dx, "dw_in": dw_in, "dbias_in": dbias, "dw2": dw2, "dz": dz, "da": da}
+
+
+# ---------------------------------------------------------------------------
+# optimizer pieces on the path (optim.py:105-114, trainer.py:111-119)
+
+
+def masked_decay_gradient(g, w, m, lambda_w: float):
+    g = np.asarray(g, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    m = np.asarray(m)
+    if not (g.shape == w.shape == m.shape):
+        raise ShapeError("gradient, weights and mask must have equal shapes")
+    return g + lambda_w * ((1 - m) * w)
+
+
+def switch_step(steps: int, dense_ft_fraction: float) -> int:
+    return math.ceil(steps * (1.0 - dense_ft_fraction))
+
+
+def flip_rate(m_prev, m_curr) -> float:  # optim.py:94-102
+    a = np.asarray(m_prev).ravel().astype(np.int64)
+    b = np.asarray(m_curr).ravel().astype(np.int64)
+    return float(np.abs(b - a).sum()) / a.size
+
+
+# ---------------------------------------------------------------------------
+# the reference's own compiled kernels (oracle/_ref), when built
+
+
+def ref_kernels():
+    """The reference's `_core` extension compiled by oracle/Makefile from
+    /root/reference/pkg/src/sparse24/_core.pyx, or None when not built."""
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref")
+    hits = glob.glob(os.path.join(here, "_core*.so"))
+    if not hits:
+        return None
+    spec = importlib.util.spec_from_file_location("_core", hits[0])
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+# ---------------------------------------------------------------------------
+# deterministic synthetic data (integer-only, bit-reproducible on any host)
+
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64(n: int, seed: int) -> np.ndarray:
+    """n outputs of splitmix64 starting from `seed` (uint64 arithmetic)."""
+    with np.errstate(over="ignore"):
+        x = (np.arange(1, n + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+             + np.uint64(seed & _M64))
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
+def det_normal(shape, seed: int, scale_log2: int = 0) -> np.ndarray:
+    """Approximately N(0, 2**scale_log2) float64 values built from an
+    Irwin-Hall sum of 12 integer uniforms: exact integer arithmetic plus a
+    power-of-two scale, so every host produces identical bits."""
+    n = int(np.prod(shape))
+    u = _splitmix64(12 * n, seed) >> np.uint64(44)  # 20-bit uniforms
+    s = u.reshape(n, 12).astype(np.int64).sum(axis=1) - 6 * (1 << 20)
+    return np.ldexp(s.astype(np.float64), scale_log2 - 20).reshape(shape)
+
+
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """Round float64 -> bf16 (round-to-nearest-even via f32), back to f64."""
+    f = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    lsb = (f >> np.uint64(16)) & np.uint64(1)
+    f = (f + np.uint64(0x7FFF) + lsb) & np.uint64(0xFFFF0000)
+    return f.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def bf16_bits(x: np.ndarray) -> np.ndarray:
+    """uint16 bf16 encoding of bf16-representable float64 values."""
+    return (np.asarray(x, dtype=np.float32).view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+
+
+def from_bf16_bits(b: np.ndarray) -> np.ndarray:
+    return (np.asarray(b, dtype=np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)

@@ -1,0 +1,189 @@
+"""Generate golden vectors from the REFERENCE package itself.
+
+Run in the build container (needs /root/reference):
+    python tests/golden/make_golden.py
+It copies /root/reference/pkg to /tmp/refpkg_golden, builds the reference's
+Cython core there (its own setup.py, -O3 -ffp-contract=off), imports
+`sparse24` from that copy and records inputs + reference outputs as .npz
+fixtures next to this script.  The fixtures are committed; the GPU box never
+needs /root/reference.
+
+Inputs are integer-generated (oracle.s24_oracle.det_normal) and rounded to
+bf16 or fp32 where stated, so they are bit-reproducible everywhere.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.abspath(os.path.join(HERE, "..", ".."))
+sys.path.insert(0, REPO)
+from oracle import s24_oracle as o  # noqa: E402
+
+REF = "/root/reference/pkg"
+BUILD = "/tmp/refpkg_golden"
+
+
+def import_reference():
+    if not os.path.isdir(os.path.join(BUILD, "src")):
+        shutil.copytree(REF, BUILD)
+        subprocess.run([sys.executable, "setup.py", "build_ext", "--inplace"], cwd=BUILD,
+                       check=True, capture_output=True)
+    sys.path.insert(0, os.path.join(BUILD, "src"))
+    import sparse24  # noqa: F401
+
+    assert sparse24.BACKEND == "cython", sparse24.BACKEND
+    return sparse24
+
+
+def ref_search(s24, w):
+    """Reference mask, per-block idx and both compressed orientations."""
+    from sparse24.matrix import Direction
+    from sparse24.sparsity import Mask24, SparseEstimate, _blocks_16
+    from sparse24.spmm import compress
+
+    table = s24.enumerate_patterns()
+    mask = s24.transposable_search_conv(w)
+    blocks = _blocks_16(mask.bits).reshape(-1, 16)
+    idx = np.array([table.index_of(b.reshape(4, 4)) for b in blocks], dtype=np.uint8)
+    r, c = w.shape
+    idx = idx.reshape(r // 4, c // 4)
+    fwd = compress(SparseEstimate(w * mask.bits, Mask24(mask.bits, Direction.ROW_WISE)))
+    wt, mt = np.ascontiguousarray(w.T), np.ascontiguousarray(mask.bits.T)
+    bwd = compress(SparseEstimate(wt * mt, Mask24(mt, Direction.ROW_WISE)))
+    return dict(
+        bits=mask.bits,
+        idx=idx,
+        fwd_values=fwd.values.reshape(r, c // 2),
+        fwd_meta=fwd.meta.reshape(r, c // 4),
+        bwd_values=bwd.values.reshape(c, r // 2),
+        bwd_meta=bwd.meta.reshape(c, r // 4),
+    )
+
+
+def mask_corpora():
+    """name -> (input float64 array, storage dtype tag)."""
+    out = {}
+    # reference acceptance corpus style: 1000 Gaussian 16x16 blocks in f64
+    out["gauss_f64"] = (o.det_normal((1000 * 16, 16), seed=2024), "f64")
+    # bf16 N(0, 2^-6 ~ 0.0156): ~0.3% exact top-2 ties
+    out["gauss_bf16"] = (o.round_bf16(o.det_normal((512, 512), seed=7, scale_log2=-6)), "bf16")
+    # small-integer blocks: heavy ties (sparsity corpora, verify.py:193-214)
+    ints = (o._splitmix64(256 * 256, 11) % np.uint64(5)).astype(np.float64) - 2.0
+    out["int_ties"] = (ints.reshape(256, 256), "bf16")
+    # all-equal, all-zero, dominant-pattern KATs (test_sparsity.py:129-165),
+    # stuck-greedy block (test_sparsity.py:170-182), huge exponent spans
+    pats, _ = o.pattern_table()
+    kat = np.zeros((16, 64))
+    kat[0:4, 0:4] = 1.0
+    kat[0:4, 4:8] = 0.0
+    kat[0:4, 8:12] = np.where(pats[37] > 0, 10.0, 1.0)
+    kat[0:4, 12:16] = np.where(pats[5] > 0, 50.0, 1.0)
+    kat[0:4, 16:20] = [[10, 10, 0.01, 0.3], [10, 10, 0.01, 0.3],
+                       [0.02, 0.02, 10, 0.3], [0.4, 0.4, 10, 9]]
+    kat[0:4, 20:24] = -1.0  # sign must not matter
+    kat[4:8, :] = o.round_bf16(o.det_normal((4, 64), seed=3))
+    # blocks mixing 2^60 and 2^-60 magnitudes: exponent span > 42 so the
+    # reference's ascending f64 sum rounds (the GPU slow path must match)
+    span = o.det_normal((8, 64), seed=5)
+    span *= np.where((np.arange(8 * 64).reshape(8, 64) % 3) == 0, 2.0 ** 60, 2.0 ** -60)
+    kat[8:16, :] = o.round_bf16(span)
+    out["kats"] = (o.round_bf16(kat), "bf16")
+    # fp32 weights at the C1 (CPU-oracle) shape, d=768 d_ff=3072
+    out["c1_w1_f32"] = (o.det_normal((3072, 768), seed=101, scale_log2=-5).astype(np.float32).astype(np.float64), "f32")
+    # bf16 weights at the C2 shape (GPT-2 medium FFN, w1 4096x1024)
+    out["c2_w1_bf16"] = (o.round_bf16(o.det_normal((4096, 1024), seed=202, scale_log2=-5)), "bf16")
+    return out
+
+
+def fst_cases():
+    """Small FFN layers (bf16-representable values) for fwd/bwd goldens."""
+    cases = {}
+    for act, d, d_ff, n in (("gelu", 32, 64, 48), ("geglu", 32, 64, 48), ("relu", 16, 32, 24)):
+        seed = {"gelu": 1, "geglu": 2, "relu": 3}[act]
+        r_in = 2 * d_ff if act == "geglu" else d_ff
+        cases[act] = dict(
+            x=o.round_bf16(o.det_normal((n, d), seed=seed * 10 + 1)),
+            w_in=o.round_bf16(o.det_normal((r_in, d), seed=seed * 10 + 2, scale_log2=-2)),
+            bias_in=o.round_bf16(o.det_normal((r_in,), seed=seed * 10 + 3, scale_log2=-3)),
+            w2=o.round_bf16(o.det_normal((d, d_ff), seed=seed * 10 + 4, scale_log2=-3)),
+            dy=o.round_bf16(o.det_normal((n, d), seed=seed * 10 + 5, scale_log2=-4)),
+        )
+    return cases
+
+
+def main():
+    s24 = import_reference()
+    from sparse24.gated_ffn import Activation, FFNLayer, FFNMasks, fst_backward, fst_forward, geglu_forward
+    from sparse24.optim import masked_decay_gradient
+
+    table = s24.enumerate_patterns()
+    text = table.to_text()
+    md5 = hashlib.md5(text.encode()).hexdigest()
+    assert md5 == "313a02e787e3fa096f2727e789833468", md5
+    with open(os.path.join(HERE, "patterns.txt"), "w") as f:
+        f.write(text)
+
+    arrays = {}
+    for name, (w, tag) in mask_corpora().items():
+        res = ref_search(s24, w)
+        arrays[f"{name}.idx"] = res["idx"]
+        # large corpora are regenerated bit-exactly by tests from
+        # mask_corpora() (integer-only generator); small ones store
+        # inputs plus both compressed orientations
+        if w.size <= 512 * 512 and name != "gauss_f64":
+            arrays[f"{name}.w_bf16"] = o.bf16_bits(w)
+            arrays[f"{name}.fwd_meta"] = res["fwd_meta"]
+            arrays[f"{name}.bwd_meta"] = res["bwd_meta"]
+            arrays[f"{name}.fwd_values"] = o.bf16_bits(res["fwd_values"])
+            arrays[f"{name}.bwd_values"] = o.bf16_bits(res["bwd_values"])
+        print(f"{name}: {w.shape} tag={tag}")
+    np.savez_compressed(os.path.join(HERE, "mask_golden.npz"), **arrays)
+
+    fst = {}
+    for act, c in fst_cases().items():
+        if act == "geglu":
+            r = c["w2"].shape[1]
+            layer = FFNLayer.gated(u=c["w_in"][:r], v=c["w_in"][r:], b=c["bias_in"][:r],
+                                   c=c["bias_in"][r:], w2=c["w2"])
+        else:
+            layer = FFNLayer.plain(w1=c["w_in"], b=c["bias_in"], w2=c["w2"],
+                                   activation=Activation(act))
+        masks = FFNMasks(w_in=s24.transposable_search_conv(layer.w_in()),
+                         w_out=s24.transposable_search_conv(layer.w2))
+        f = fst_forward(layer, c["x"], masks)
+        g = fst_backward(f, c["dy"], rng_seed=0, mvue=False)
+        dw_in = np.concatenate([g.d_u, g.d_v]) if act == "geglu" else g.d_w1
+        dbias = np.concatenate([g.d_b, g.d_c]) if act == "geglu" else g.d_b
+        decayed = masked_decay_gradient(dw_in, layer.w_in(), masks.w_in.bits, 6e-5)
+        # dense path (masks=None): the dense fine-tune switch target
+        fd = fst_forward(layer, c["x"], None)
+        gd = fst_backward(fd, c["dy"], rng_seed=0, mvue=False)
+        for k, v in c.items():
+            fst[f"{act}.{k}"] = v
+        fst.update({
+            f"{act}.mask_in": masks.w_in.bits, f"{act}.mask_out": masks.w_out.bits,
+            f"{act}.z": np.asarray(f.z), f"{act}.a": np.asarray(f.a), f"{act}.y": np.asarray(f.y),
+            f"{act}.dx": np.asarray(g.d_x), f"{act}.dw_in": dw_in, f"{act}.dbias_in": dbias,
+            f"{act}.dw2": np.asarray(g.d_w2), f"{act}.dw_in_decayed": decayed,
+            f"{act}.dense_y": np.asarray(fd.y), f"{act}.dense_dx": np.asarray(gd.d_x),
+        })
+        print(f"fst {act}: y {f.y.shape}")
+    # standalone GEGLU gate (gated_ffn.py:208-224) on bf16-valued operands
+    c = fst_cases()["geglu"]
+    r = c["w2"].shape[1]
+    gg = geglu_forward(c["x"], c["w_in"][:r], c["w_in"][r:], c["bias_in"][:r], c["bias_in"][r:])
+    fst["geglu_forward.out"] = gg.to_array()
+    np.savez_compressed(os.path.join(HERE, "fst_golden.npz"), **fst)
+    print("wrote", os.listdir(HERE))
+
+
+if __name__ == "__main__":
+    main()

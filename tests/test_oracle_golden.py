@@ -1,0 +1,122 @@
+"""Pin the CPU oracle (oracle/s24_oracle.py) against golden vectors that the
+reference package itself produced (tests/golden/make_golden.py).  CPU only."""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from oracle import s24_oracle as o
+from make_golden import fst_cases, mask_corpora
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_pattern_table_matches_reference_golden():
+    pats, pos = o.pattern_table()
+    text = o.pattern_text(pats)
+    assert len(pats) == 90
+    assert hashlib.md5(text.encode()).hexdigest() == "313a02e787e3fa096f2727e789833468"
+    assert text == open(os.path.join(GOLDEN, "patterns.txt")).read()
+    # every row / column sums to two; closed under transpose
+    assert (pats.sum(axis=1) == 2).all() and (pats.sum(axis=2) == 2).all()
+    flat = {tuple(p.reshape(16)) for p in pats}
+    assert all(tuple(p.T.reshape(16)) in flat for p in pats)
+    assert list(pos[0]) == [2, 3, 6, 7, 8, 9, 12, 13]
+
+
+@pytest.fixture(scope="module")
+def corpora():
+    return mask_corpora()
+
+
+@pytest.mark.parametrize("name", ["gauss_f64", "gauss_bf16", "int_ties", "kats", "c1_w1_f32", "c2_w1_bf16"])
+def test_search_idx_bit_exact(name, corpora, mask_golden):
+    w, _ = corpora[name]
+    idx = o.search_pattern_idx(w)
+    assert idx.dtype == np.uint8
+    np.testing.assert_array_equal(idx, mask_golden[f"{name}.idx"])
+    bits = o.idx_to_bits(idx)
+    o.validate_transposable(bits)
+    o.validate_transposable(bits.T)
+
+
+@pytest.mark.parametrize("name", ["gauss_bf16", "int_ties", "kats"])
+def test_compress_both_orientations_bit_exact(name, corpora, mask_golden):
+    w, _ = corpora[name]
+    np.testing.assert_array_equal(o.bf16_bits(w), mask_golden[f"{name}.w_bf16"])
+    bits = o.idx_to_bits(mask_golden[f"{name}.idx"])
+    kv, meta = o.compress_rowwise(w, bits)
+    np.testing.assert_array_equal(meta, mask_golden[f"{name}.fwd_meta"])
+    np.testing.assert_array_equal(o.bf16_bits(kv), mask_golden[f"{name}.fwd_values"])
+    kvt, metat = o.compress_rowwise(np.ascontiguousarray(w.T), np.ascontiguousarray(bits.T))
+    np.testing.assert_array_equal(metat, mask_golden[f"{name}.bwd_meta"])
+    np.testing.assert_array_equal(o.bf16_bits(kvt), mask_golden[f"{name}.bwd_values"])
+    # round trip
+    np.testing.assert_array_equal(o.decompress_rowwise(kv, meta, w.shape[1]), w * bits)
+
+
+def test_kat_specifics(mask_golden):
+    idx = mask_golden["kats.idx"]
+    assert idx[0, 0] == 0  # all-equal block -> pattern 0 (first max)
+    assert idx[0, 1] == 0  # all-zero block -> pattern 0
+    assert idx[0, 2] == 37  # dominant pattern 37 (test_sparsity.py:129-134)
+    assert idx[0, 3] == 5
+    assert idx[0, 5] == 0  # sign does not matter
+
+
+def test_meta_nibble_kat():
+    # group [0, 5, 0, -3] -> values (5, -3), meta 1 | 3 << 2 = 13 (test_spmm.py:25-29)
+    kv, meta = o.compress_rowwise(np.array([[0.0, 5.0, 0.0, -3.0]]), np.array([[0, 1, 0, 1]]))
+    assert list(kv[0]) == [5.0, -3.0] and meta[0, 0] == 13
+    with pytest.raises(o.FormatError):
+        o.decompress_rowwise(np.zeros((1, 2)), np.array([[2 | (1 << 2)]], dtype=np.uint8), 4)
+
+
+@pytest.mark.parametrize("act", ["gelu", "geglu", "relu"])
+def test_fst_forward_backward_matches_reference(act, fst_golden):
+    c = fst_cases()[act]
+    g = {k.split(".", 1)[1]: v for k, v in fst_golden.items() if k.startswith(act + ".")}
+    for k in ("x", "w_in", "bias_in", "w2", "dy"):
+        np.testing.assert_array_equal(c[k], g[k])
+    layer = o.Layer(c["w_in"], c["bias_in"], c["w2"], act)
+    mi, mo = g["mask_in"], g["mask_out"]
+    np.testing.assert_array_equal(mi, o.transposable_search_conv(c["w_in"]))
+    for exact in (True, False):
+        f = o.fst_forward(layer, c["x"], mi, mo, exact=exact)
+        b = o.fst_backward(layer, f, c["dy"], mi, mo, exact=exact)
+        tol = 0 if exact else 1e-12
+        for ours, ref in ((f["z"], g["z"]), (f["a"], g["a"]), (f["y"], g["y"]), (b["dx"], g["dx"]),
+                          (b["dw_in"], g["dw_in"]), (b["dbias_in"], g["dbias_in"]), (b["dw2"], g["dw2"])):
+            np.testing.assert_allclose(ours, ref, rtol=tol, atol=1e-13 if exact else 1e-12)
+    dec = o.masked_decay_gradient(b["dw_in"], c["w_in"], mi, 6e-5)
+    np.testing.assert_allclose(dec, g["dw_in_decayed"], rtol=1e-12, atol=1e-14)
+    fd = o.fst_forward(layer, c["x"], None, None)
+    bd = o.fst_backward(layer, fd, c["dy"], None, None)
+    np.testing.assert_allclose(fd["y"], g["dense_y"], rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(bd["dx"], g["dense_dx"], rtol=1e-12, atol=1e-13)
+
+
+def test_geglu_gate(fst_golden):
+    c = fst_cases()["geglu"]
+    r = c["w2"].shape[1]
+    z = c["x"] @ c["w_in"].T + c["bias_in"]
+    out = o.gate(z[:, :r], z[:, r:])
+    np.testing.assert_allclose(out, fst_golden["geglu_forward.out"], rtol=1e-12, atol=1e-13)
+
+
+def test_switch_step_kat():
+    assert o.switch_step(60000, 1 / 6) == 50000  # test_trainer.py:68-71
+
+
+def test_ref_kernels_agree_with_restatement():
+    k = o.ref_kernels()
+    if k is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(5)
+    _, pos = o.pattern_table()
+    blocks = np.abs(rng.standard_normal((300, 16)))
+    s1, b1 = k.pattern_scores(blocks, pos)
+    s2, b2 = o.pattern_scores(blocks, pos)
+    assert s1.tobytes() == s2.tobytes() and (b1 == b2).all()
