@@ -1,0 +1,152 @@
+/*
+ * sparse24_b200.h -- C ABI of the B200 (sm_100a) 2:4-sparse FFN hot path.
+ *
+ * This is the drop-in boundary for the reference package `sparse24`
+ * (/root/reference/pkg/src/sparse24).  The reference selects its kernel
+ * module at import time (backend.py:13-36) and calls it through
+ * `kernels.<fn>` from sparsity.py / spmm.py / gated_ffn.py / optim.py; each
+ * entry point below names the reference interface it replaces.
+ *
+ * Conventions:
+ *   - plain pointers to DEVICE memory + sizes; no torch / C++ types;
+ *   - the caller allocates every output and workspace; nothing is retained;
+ *   - every call is asynchronous on the caller's cudaStream_t (passed as
+ *     void*; NULL = legacy default stream) and CUDA-graph capturable;
+ *   - return an int status; s24_last_error_string() describes the last
+ *     failure of the calling thread.  The Python layer maps
+ *     S24_ERR_SHAPE -> ShapeError, S24_ERR_FORMAT -> FormatError (both
+ *     ValueError subclasses, matrix.py:11-16), others -> RuntimeError.
+ *
+ * Data layouts
+ *   W       row-major (rows x cols), dtype S24_BF16 / S24_F32 / S24_F64.
+ *   idx     uint8 (rows/4 x cols/4): canonical pattern index (0..89) of
+ *           every aligned 4x4 block (sparsity.py:208-217 ordering).
+ *   vals    bf16 row-major (m x k/2): the two kept values of every row-wise
+ *           group of four, ascending (Compressed24.values, spmm.py:38-106).
+ *           "fwd" = groups along W's rows (m=rows, k=cols); "bwd" = groups
+ *           along W's columns, i.e. the compressed W^T (m=cols, k=rows).
+ *   E       the same metadata nibbles (i0 | i1<<2, spmm.py:98-104) arranged
+ *           for the sm_100 sparse tensor core: one 2048-byte tile per
+ *           (128-row m tile, 128-column k tile), tiles ordered
+ *           [m/128][k/128]; inside a tile byte 16*L + 4*c + 2*h holds the
+ *           16-bit word of lane L, column c, half h, bits 4g..4g+3 of which
+ *           are the nibble of row m = (L%8) + 16*(L/16) + 8*h and group
+ *           k/4 = 8*c + 4*((L/8)%2) + g.  Requires m, k multiples of 128.
+ *   feature-major activations: a logical (tokens x features) matrix stored
+ *           as features x tokens row-major (the reference's column-major
+ *           FST outputs, gated_ffn.py:162 / _core.pyx:67-69).
+ */
+#ifndef SPARSE24_B200_H
+#define SPARSE24_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define S24_ABI_VERSION 1
+
+/* status codes */
+#define S24_OK 0
+#define S24_ERR_SHAPE 1       /* -> ShapeError  (matrix.py:11) */
+#define S24_ERR_FORMAT 2      /* -> FormatError (matrix.py:15) */
+#define S24_ERR_UNSUPPORTED 3 /* dtype / arch / layout not supported */
+#define S24_ERR_CUDA 4        /* CUDA runtime / launch failure */
+#define S24_ERR_ARG 5         /* null pointer or bad enum */
+
+/* element types */
+#define S24_BF16 0
+#define S24_F32 1
+#define S24_F64 2
+
+/* activations (gated_ffn.py:47-50; SWIGLU is an extension, not in the reference) */
+#define S24_ACT_RELU 0
+#define S24_ACT_GELU 1
+#define S24_ACT_GEGLU 2
+#define S24_ACT_SWIGLU 3
+
+/* sparse GEMM epilogues */
+#define S24_EPI_STORE 0      /* D = acc (+ bias[m])                        */
+#define S24_EPI_GELU_AUX 1   /* D = acc + bias[m]; AUX = gelu(D)  (fwd GEMM1) */
+
+const char* s24_last_error_string(void);
+int s24_abi_version(void);
+/* S24_OK when the current device is sm_100 and the kernels are loadable. */
+int s24_device_check(void);
+
+/* ---- K1: transposable mask search ------------------------------------------
+ * Replaces transposable_search_conv (sparsity.py:258-271) and its kernel
+ * kernels.pattern_scores (_core.pyx:83-110): per 4x4 block the pattern with
+ * the largest retained |w| sum, ties -> lowest canonical index; bit-exact
+ * with the reference's ascending float64 accumulation for every input.
+ * rows, cols: multiples of 4 (else S24_ERR_SHAPE). */
+int s24_transposable_search(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* idx, void* stream);
+
+/* K1 fused: search + compress both orientations in one pass over W.
+ * Replaces transposable_search_conv + compress (spmm.py:92-106) +
+ * FFNMasks.plans/_GatherPlan (gated_ffn.py:131-188).  Any of fwd_vals,
+ * fwd_e, bwd_vals, bwd_e may be NULL; E outputs need rows, cols % 128 == 0. */
+int s24_search_compress(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* idx, uint16_t* fwd_vals,
+                        uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e, void* stream);
+
+/* ---- K2: per-step prune / compress with a cached mask ----------------------
+ * Replaces _GatherPlan.product's gather `w.ravel()[take]` (gated_ffn.py:159-162)
+ * for both orientations (in_fwd/in_bwd, out_fwd/out_bwd). */
+int s24_prune_compress(const void* w, int dtype, int64_t rows, int64_t cols, const uint8_t* idx,
+                       uint16_t* fwd_vals, uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e, void* stream);
+
+/* ---- format conversions (parity export / TransposableMask API) ------------ */
+/* idx -> full 0/1 mask, uint8 rows x cols (TransposableMask.bits, sparsity.py:270-271) */
+int s24_idx_to_bits(const uint8_t* idx, int64_t rows, int64_t cols, uint8_t* bits, void* stream);
+/* 0/1 mask -> idx; blocks that are not one of the 90 patterns get idx 255 and
+ * are counted into *bad_count (device int32, caller zeroes it); the caller
+ * raises FormatError when nonzero (TransposableMask.validate, sparsity.py:122-131). */
+int s24_bits_to_idx(const uint8_t* bits, int64_t rows, int64_t cols, uint8_t* idx, int32_t* bad_count,
+                    void* stream);
+/* reference-layout metadata, one nibble per uint8 (Compressed24.meta,
+ * spmm.py:98-104): fwd (rows x cols/4), bwd (cols x rows/4); either may be NULL */
+int s24_meta_flat(const uint8_t* idx, int64_t rows, int64_t cols, uint8_t* fwd_meta, uint8_t* bwd_meta,
+                  void* stream);
+/* E tiles (m x k logical) -> reference-layout nibbles (m x k/4) */
+int s24_e_to_flat(const uint8_t* e, int64_t m, int64_t k, uint8_t* meta, void* stream);
+
+/* ---- K3/K4: 2:4-sparse tcgen05 GEMM ----------------------------------------
+ * D[m, n] = sum_k A[m, k] * B[n, k] with A 2:4-sparse (vals m x k/2 + E tiles).
+ * Replaces kernels.spmm_colwise (_core.pyx:63-80) as driven by
+ * _GatherPlan.product for in_fwd / out_fwd / out_bwd / in_bwd
+ * (gated_ffn.py:294, :297, :329, :352).  B: b_mn = 0 -> stored n x k (ldb >= k),
+ * b_mn = 1 -> stored k x n (ldb >= n).  D bf16 m x n (ldd).  bias (bf16, m) may be
+ * NULL.  m % 128 == 0, k % 128 == 0, n % 32 == 0. */
+int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b, int b_mn,
+             int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias, int epilogue, uint16_t* aux,
+             int64_t ldaux, void* stream);
+
+/* ---- K5: dense tcgen05 dW GEMM with fused masked decay ---------------------
+ * D[m, n] (fp32, ldd) = sum_k A[m, k] B[n, k] + lambda_w * (1 - M[m, n]) * W[m, n]
+ * Replaces _grad_weight(mvue=False) (gated_ffn.py:367-371) followed by
+ * masked_decay_gradient (optim.py:105-114, applied at trainer.py:439-441).
+ * a_mn = 0 -> A stored m x k, 1 -> k x m; b_mn likewise (n x k / k x n).
+ * idx/w may be NULL (no decay).  m % 128 == 0, n % 256 == 0 (or % 128), k % 64 == 0. */
+int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int b_mn, int64_t ldb, int64_t m,
+                int64_t n, int64_t k, float* d, int64_t ldd, const void* w, int w_dtype, const uint8_t* idx,
+                float lambda_w, void* stream);
+
+/* ---- K6/K7: fused (gated) activation, feature-major --------------------------
+ * fwd: A[j, t] = act(Z[j, t]) * Z[r + j, t] (gated) or act(Z[j, t]) (plain);
+ * replaces kernels.gate_gelu (_core.pyx:222-250) / _activate (gated_ffn.py:264-270).
+ * bwd: dZ and the bias gradient sums dbias[j] = sum_t dZ[j, t] (fp32, r_in);
+ * replaces the activation block of fst_backward (gated_ffn.py:336-348). */
+int s24_act_fwd(const uint16_t* z, int64_t ldz, int64_t r, int64_t n, int act, uint16_t* a, int64_t lda,
+                void* stream);
+int s24_act_bwd(const uint16_t* z, int64_t ldz, const uint16_t* da, int64_t ldda, int64_t r, int64_t n, int act,
+                uint16_t* dz, int64_t lddz, float* dbias, void* stream);
+
+/* ---- standalone masked decay on an fp32 gradient (optim.py:105-114) -------- */
+int s24_masked_decay(float* g, const void* w, int w_dtype, const uint8_t* idx, int64_t rows, int64_t cols,
+                     float lambda_w, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSE24_B200_H */

@@ -1,0 +1,193 @@
+// K6 / K7: fused (gated) activation forward and backward on feature-major
+// activations (features x tokens, tokens contiguous).
+//
+// Reference: kernels.gate_gelu (_core.pyx:222-250) computes
+// gelu(z1) * z2 with z1 = Z[:, :r], z2 = Z[:, r:] of the column-major Z; the
+// paper's point is to walk that layout along its
+// contiguous axis.  Here the contiguous axis is tokens: one 16-byte vector of
+// z1 and of z2 (the same 8 tokens, rows j and r + j) produce one 16-byte
+// vector of A, so every byte is read once and fully coalesced.
+// The backward (gated_ffn.py:336-348) is one CTA per feature row: it streams
+// dA, z1, z2 along tokens, writes dZ1 / dZ2 and reduces the bias gradients
+// (d_b = sum_t dZ1, d_c = sum_t dZ2) in registers + shared memory, so the
+// bias reduction costs no extra pass.
+#include "s24_common.cuh"
+
+namespace s24 {
+
+constexpr float kRsqrt2 = 0.70710678118654752f;
+constexpr float kRsqrt2Pi = 0.39894228040143268f;
+
+__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.0f + erff(x * kRsqrt2)); }
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  return 0.5f * (1.0f + erff(x * kRsqrt2)) + x * (kRsqrt2Pi * __expf(-0.5f * x * x));
+}
+__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float silu_grad_f(float x) {
+  const float s = 1.0f / (1.0f + __expf(-x));
+  return s * (1.0f + x * (1.0f - s));
+}
+
+template <int kAct>
+__device__ __forceinline__ float act_f(float x) {
+  if constexpr (kAct == S24_ACT_RELU) return fmaxf(x, 0.0f);
+  else if constexpr (kAct == S24_ACT_SWIGLU) return silu_f(x);
+  else return gelu_f(x);
+}
+template <int kAct>
+__device__ __forceinline__ float act_grad_f(float x) {
+  if constexpr (kAct == S24_ACT_RELU) return x > 0.0f ? 1.0f : 0.0f;
+  else if constexpr (kAct == S24_ACT_SWIGLU) return silu_grad_f(x);
+  else return gelu_grad_f(x);
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                    pack_bf16x2(f[6], f[7]));
+}
+
+template <int kAct, bool kGated>
+__global__ void __launch_bounds__(256) act_fwd_kernel(const uint16_t* __restrict__ z, int64_t ldz, int64_t r,
+                                                      int64_t n, uint16_t* __restrict__ a, int64_t lda) {
+  const int64_t vpr = n / 8;  // vectors per row
+  const int64_t total = r * vpr;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = v / vpr, t = (v % vpr) * 8;
+    float x[8], o[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(z + j * ldz + t)), x);
+    if constexpr (kGated) {
+      float g[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(z + (j + r) * ldz + t)), g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = act_f<kAct>(x[i]) * g[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = act_f<kAct>(x[i]);
+    }
+    *reinterpret_cast<uint4*>(a + j * lda + t) = pack8(o);
+  }
+}
+
+template <int kAct, bool kGated>
+__global__ void __launch_bounds__(256) act_bwd_kernel(const uint16_t* __restrict__ z, int64_t ldz,
+                                                      const uint16_t* __restrict__ da, int64_t ldda, int64_t r,
+                                                      int64_t n, uint16_t* __restrict__ dz, int64_t lddz,
+                                                      float* __restrict__ dbias) {
+  __shared__ float s_red[2][8];
+  const int64_t j = blockIdx.x;
+  float acc1 = 0.0f, acc2 = 0.0f;
+  for (int64_t t = threadIdx.x * 8; t < n; t += 256 * 8) {
+    float x[8], d[8], o1[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(z + j * ldz + t)), x);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(da + j * ldda + t)), d);
+    if constexpr (kGated) {
+      float g[8], o2[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(z + (j + r) * ldz + t)), g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        o1[i] = d[i] * g[i] * act_grad_f<kAct>(x[i]);  // dZ1 = dA * z2 * act'(z1)
+        o2[i] = d[i] * act_f<kAct>(x[i]);              // dZ2 = dA * act(z1)
+        acc1 += o1[i];
+        acc2 += o2[i];
+      }
+      *reinterpret_cast<uint4*>(dz + (j + r) * lddz + t) = pack8(o2);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        o1[i] = d[i] * act_grad_f<kAct>(x[i]);
+        acc1 += o1[i];
+      }
+    }
+    *reinterpret_cast<uint4*>(dz + j * lddz + t) = pack8(o1);
+  }
+  if (dbias == nullptr) return;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    acc1 += __shfl_xor_sync(0xffffffffu, acc1, off);
+    acc2 += __shfl_xor_sync(0xffffffffu, acc2, off);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_red[0][warp] = acc1;
+    s_red[1][warp] = acc2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b1 = 0.0f, b2 = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      b1 += s_red[0][w];
+      b2 += s_red[1][w];
+    }
+    dbias[j] = b1;
+    if (kGated) dbias[j + r] = b2;
+  }
+}
+
+}  // namespace s24
+
+using namespace s24;
+
+static int check_act(const void* z, int64_t ldz, const void* o, int64_t ldo, int64_t r, int64_t n, int act) {
+  S24_REQUIRE(z && o, S24_ERR_ARG, "NULL pointer");
+  S24_REQUIRE(act >= S24_ACT_RELU && act <= S24_ACT_SWIGLU, S24_ERR_ARG, "unknown activation %d", act);
+  S24_REQUIRE(r >= 0 && n >= 0 && ldz >= n && ldo >= n, S24_ERR_SHAPE, "bad activation shape");
+  S24_REQUIRE(n % 8 == 0 && ldz % 8 == 0 && ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(z) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(o) & 15) == 0,
+              S24_ERR_UNSUPPORTED, "activation rows must be 16-byte aligned (tokens %% 8 == 0)");
+  return S24_OK;
+}
+
+template <int kAct, bool kGated>
+static void launch_fwd(const uint16_t* z, int64_t ldz, int64_t r, int64_t n, uint16_t* a, int64_t lda,
+                       cudaStream_t st) {
+  int64_t blocks = (r * (n / 8) + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  act_fwd_kernel<kAct, kGated><<<static_cast<unsigned>(blocks), 256, 0, st>>>(z, ldz, r, n, a, lda);
+}
+
+extern "C" int s24_act_fwd(const uint16_t* z, int64_t ldz, int64_t r, int64_t n, int act, uint16_t* a, int64_t lda,
+                           void* stream) {
+  if (int rc = check_act(z, ldz, a, lda, r, n, act)) return rc;
+  if (r == 0 || n == 0) return S24_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (act) {
+    case S24_ACT_RELU: launch_fwd<S24_ACT_RELU, false>(z, ldz, r, n, a, lda, st); break;
+    case S24_ACT_GELU: launch_fwd<S24_ACT_GELU, false>(z, ldz, r, n, a, lda, st); break;
+    case S24_ACT_GEGLU: launch_fwd<S24_ACT_GEGLU, true>(z, ldz, r, n, a, lda, st); break;
+    default: launch_fwd<S24_ACT_SWIGLU, true>(z, ldz, r, n, a, lda, st); break;
+  }
+  return s24_check_launch("act_fwd");
+}
+
+extern "C" int s24_act_bwd(const uint16_t* z, int64_t ldz, const uint16_t* da, int64_t ldda, int64_t r, int64_t n,
+                           int act, uint16_t* dz, int64_t lddz, float* dbias, void* stream) {
+  if (int rc = check_act(z, ldz, dz, lddz, r, n, act)) return rc;
+  if (int rc = check_act(da, ldda, dz, lddz, r, n, act)) return rc;
+  if (r == 0) return S24_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const unsigned grid = static_cast<unsigned>(r);
+  switch (act) {
+    case S24_ACT_RELU:
+      act_bwd_kernel<S24_ACT_RELU, false><<<grid, 256, 0, st>>>(z, ldz, da, ldda, r, n, dz, lddz, dbias);
+      break;
+    case S24_ACT_GELU:
+      act_bwd_kernel<S24_ACT_GELU, false><<<grid, 256, 0, st>>>(z, ldz, da, ldda, r, n, dz, lddz, dbias);
+      break;
+    case S24_ACT_GEGLU:
+      act_bwd_kernel<S24_ACT_GEGLU, true><<<grid, 256, 0, st>>>(z, ldz, da, ldda, r, n, dz, lddz, dbias);
+      break;
+    default:
+      act_bwd_kernel<S24_ACT_SWIGLU, true><<<grid, 256, 0, st>>>(z, ldz, da, ldda, r, n, dz, lddz, dbias);
+      break;
+  }
+  return s24_check_launch("act_bwd");
+}

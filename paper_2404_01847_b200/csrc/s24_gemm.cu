@@ -1,0 +1,477 @@
+// K3/K4 (2:4-sparse) and K5 (dense dW) GEMMs on the 5th-generation tensor
+// cores: tcgen05.mma[.sp] issued by one thread, operands staged in shared
+// memory by TMA (128-byte swizzle), fp32 accumulators in TMEM, metadata for the
+// sparse A operand copied smem -> TMEM with tcgen05.cp.
+//
+// D[m, n] = sum_k A[m, k] * B[n, k]
+//   sparse (K3/K4): A = compressed W (m x k/2 bf16, K-major) + E tiles,
+//                   B = activations (n tokens), D bf16 (+bias, +fused GELU).
+//                   Replaces kernels.spmm_colwise (_core.pyx:63-80) as used by
+//                   _GatherPlan.product (gated_ffn.py:159-162).
+//   dense  (K5):    A, B = activation / gradient panels (K = tokens),
+//                   D fp32 = dW + lambda (1 - M) W  (masked decay epilogue).
+//                   Replaces _grad_weight(mvue=False) (gated_ffn.py:367-371)
+//                   + masked_decay_gradient (optim.py:105-114).
+//
+// CTA layout (256 threads, one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      MMA issuer (one elected lane) + tcgen05.cp of the metadata
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns -> registers ->
+//               bias / GELU / decay -> global stores
+// Pipelines: kStages smem slots (full/empty mbarriers) and two TMEM
+// accumulators (tmem_full/tmem_empty) so the epilogue of tile i overlaps the
+// main loop of tile i+1.
+#include <cstdio>
+#include <mutex>
+
+#include "s24_common.cuh"
+#include "s24_patterns.h"
+
+namespace s24 {
+
+constexpr int kBM = 128;
+constexpr int kGemmThreads = 256;
+constexpr int kGroupM = 8;  // M tiles per raster group (L2 reuse of the B panel)
+
+enum Epi : int { kEpiStore = 0, kEpiGeluAux = 1, kEpiDw = 2 };
+
+struct EpiParams {
+  void* d;
+  int64_t ldd;
+  const uint16_t* bias;
+  uint16_t* aux;
+  int64_t ldaux;
+  const void* w;
+  int w_dtype;
+  const uint8_t* idx;
+  float lam;
+};
+
+struct GemmShape {
+  int m, n, k;  // k logical
+  const uint8_t* e;
+};
+
+__constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
+
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages>
+struct Cfg {
+  static constexpr int BK = kSparse ? 128 : 64;  // logical K per stage
+  static constexpr int kMmaK = kSparse ? 32 : 16;
+  static constexpr int kMmasPerStage = BK / kMmaK;  // 4
+  static constexpr int A_BYTES = kBM * 64 * 2;      // 16 KB either major
+  static constexpr int B_BYTES = kBN * BK * 2;
+  static constexpr int E_BYTES = kSparse ? 2048 : 0;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + E_BYTES;
+  static constexpr int ACC_COLS = kBN;
+  static constexpr int E_COL = 2 * kBN;
+  static constexpr int USED_COLS = 2 * kBN + (kSparse ? 4 : 0);
+  static constexpr int TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64 : USED_COLS <= 128 ? 128
+                                 : USED_COLS <= 256 ? 256 : 512;
+  static constexpr int SMEM_BYTES = kStages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t IDESC = make_idesc_bf16(kBM, kBN, kAMN, kBMN, kSparse);
+  static_assert(USED_COLS <= 512, "TMEM overflow");
+  static_assert(kBN % 32 == 0 && kBN >= 32 && kBN <= 256, "bad BN");
+};
+
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
+  const int per_group = kGroupM * num_n;
+  const int group = tile / per_group;
+  const int first_m = group * kGroupM;
+  const int gm = min(num_m - first_m, kGroupM);
+  const int in_group = tile % per_group;
+  mb = first_m + in_group % gm;
+  nb = in_group / gm;
+}
+
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kEpi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape shp,
+                EpiParams ep) {
+  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_m = shp.m / kBM;
+  const int num_n = (shp.n + kBN - 1) / kBN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = shp.k / C::BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int m0 = mb * kBM, n0 = nb * kBN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sA = smem + stage * C::STAGE_BYTES;
+          uint8_t* sB = sA + C::A_BYTES;
+          mbar_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          if constexpr (kSparse) {
+            tma_load_2d(sA, &tmA, &full_bar[stage], kb * 64, m0);  // 64 physical = 128 logical
+            uint8_t* sE = sB + C::B_BYTES;
+            bulk_load(sE, shp.e + (static_cast<int64_t>(mb) * (shp.k / 128) + kb) * 2048, 2048, &full_bar[stage]);
+          } else if constexpr (kAMN) {
+            tma_load_2d(sA, &tmA, &full_bar[stage], m0, kb * 64);
+            tma_load_2d(sA + 8192, &tmA, &full_bar[stage], m0 + 64, kb * 64);
+          } else {
+            tma_load_2d(sA, &tmA, &full_bar[stage], kb * 64, m0);
+          }
+          if constexpr (kBMN) {
+#pragma unroll
+            for (int i = 0; i < kBN / 64; ++i)
+              tma_load_2d(sB + i * (C::BK * 128), &tmB, &full_bar[stage], n0 + 64 * i, kb * C::BK);
+          } else {
+#pragma unroll
+            for (int i = 0; i < C::BK / 64; ++i)
+              tma_load_2d(sB + i * (kBN * 128), &tmB, &full_bar[stage], kb * C::BK + 64 * i, n0);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t b_addr = a_addr + C::A_BYTES;
+          if constexpr (kSparse) {
+            // metadata: 128 rows x 16 B (no swizzle, 8-row core matrices 128 B apart)
+            tmem_cp_128x128b(tmem_base + C::E_COL, make_sdesc(b_addr + C::B_BYTES, 2048, 128, 0));
+          }
+#pragma unroll
+          for (int j = 0; j < C::kMmasPerStage; ++j) {
+            uint64_t adesc, bdesc;
+            if constexpr (kAMN) {
+              adesc = make_sdesc(a_addr + j * (C::kMmaK * 128), 8192, 1024, 2);
+            } else {
+              adesc = make_sdesc(a_addr + j * 32, 16, 1024, 2);
+            }
+            if constexpr (kBMN) {
+              bdesc = make_sdesc(b_addr + j * (C::kMmaK * 128), C::BK * 128, 1024, 2);
+            } else if constexpr (kSparse) {
+              bdesc = make_sdesc(b_addr + (j >> 1) * (kBN * 128) + (j & 1) * 64, 16, 1024, 2);
+            } else {
+              bdesc = make_sdesc(b_addr + j * 32, 16, 1024, 2);
+            }
+            const uint32_t accum = (kb | j) != 0 ? 1u : 0u;
+            if constexpr (kSparse) {
+              mma_sp_bf16(d_tmem, adesc, bdesc, tmem_base + C::E_COL + j, C::IDESC, accum);
+            } else {
+              mma_bf16(d_tmem, adesc, bdesc, C::IDESC, accum);
+            }
+          }
+          mma_commit(&empty_bar[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue =====================
+    const int q = warp & 3;  // TMEM lane quarter
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int m = mb * kBM + 32 * q + lane;
+      const int n_base = nb * kBN;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      float bias_v = 0.0f;
+      if constexpr (kEpi != kEpiDw) {
+        if (ep.bias != nullptr) bias_v = bf16_to_f32(ep.bias[m]);
+      }
+#pragma unroll 1
+      for (int cc = 0; cc < kBN / 32; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + 32 * cc, r);
+        tmem_ld_wait();
+        const int n0 = n_base + 32 * cc;
+        if (n0 >= shp.n) continue;
+        if constexpr (kEpi == kEpiDw) {
+          float* out = static_cast<float*>(ep.d) + static_cast<int64_t>(m) * ep.ldd + n0;
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if (ep.idx != nullptr) {
+            const uint2 ib = *reinterpret_cast<const uint2*>(ep.idx + static_cast<int64_t>(m >> 2) * (shp.n >> 2) + (n0 >> 2));
+            const uint32_t iw[2] = {ib.x, ib.y};
+            float wv[32];
+            if (ep.w_dtype == S24_BF16) {
+              const uint4* wp = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(ep.w) +
+                                                               static_cast<int64_t>(m) * shp.n + n0);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const uint4 x = __ldg(wp + u);
+                const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  wv[8 * u + 2 * h] = __uint_as_float(xs[h] << 16);
+                  wv[8 * u + 2 * h + 1] = __uint_as_float(xs[h] & 0xFFFF0000u);
+                }
+              }
+            } else {
+              const float4* wp = reinterpret_cast<const float4*>(static_cast<const float*>(ep.w) +
+                                                                 static_cast<int64_t>(m) * shp.n + n0);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const float4 x = __ldg(wp + u);
+                wv[4 * u] = x.x;
+                wv[4 * u + 1] = x.y;
+                wv[4 * u + 2] = x.z;
+                wv[4 * u + 3] = x.w;
+              }
+            }
+#pragma unroll
+            for (int blk = 0; blk < 8; ++blk) {
+              const uint32_t pidx = (iw[blk >> 2] >> (8 * (blk & 3))) & 0xFF;
+              const uint32_t rowmask = (c_gemm_pat_bits[min(pidx, 89u)] >> (4 * (m & 3))) & 0xF;
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                if (!((rowmask >> c) & 1)) v[4 * blk + c] += ep.lam * wv[4 * blk + c];
+            }
+          }
+          float4* o4 = reinterpret_cast<float4*>(out);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) o4[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+        } else {
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) + bias_v;
+          uint4* o4 = reinterpret_cast<uint4*>(static_cast<uint16_t*>(ep.d) + static_cast<int64_t>(m) * ep.ldd + n0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            o4[u] = make_uint4(pack_bf16x2(v[8 * u], v[8 * u + 1]), pack_bf16x2(v[8 * u + 2], v[8 * u + 3]),
+                               pack_bf16x2(v[8 * u + 4], v[8 * u + 5]), pack_bf16x2(v[8 * u + 6], v[8 * u + 7]));
+          if constexpr (kEpi == kEpiGeluAux) {
+            float g[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) g[i] = 0.5f * v[i] * (1.0f + erff(v[i] * 0.70710678118654752f));
+            uint4* a4 = reinterpret_cast<uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              a4[u] = make_uint4(pack_bf16x2(g[8 * u], g[8 * u + 1]), pack_bf16x2(g[8 * u + 2], g[8 * u + 3]),
+                                 pack_bf16x2(g[8 * u + 4], g[8 * u + 5]), pack_bf16x2(g[8 * u + 6], g[8 * u + 7]));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, C::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map: inner (contiguous) extent, outer extent, row pitch in elements.
+static int make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch_elems,
+                    uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn enc = get_encode_fn();
+  S24_REQUIRE(enc != nullptr, S24_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  S24_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && (pitch_elems * 2) % 16 == 0, S24_ERR_UNSUPPORTED,
+              "TMA operands need 16-byte aligned base and row pitch");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch_elems * 2)};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  S24_REQUIRE(r == CUDA_SUCCESS, S24_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return S24_OK;
+}
+
+static int num_sms() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kEpi>
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& shp, const EpiParams& ep,
+                       cudaStream_t st) {
+  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages>;
+  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kEpi>;
+  static bool attr_done = false;  // per template instance
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    attr_done = true;
+  }
+  const int tiles = (shp.m / kBM) * ((shp.n + kBN - 1) / kBN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  if (grid <= 0) return S24_OK;
+  kern<<<grid, kGemmThreads, C::SMEM_BYTES, st>>>(ma, mb, shp, ep);
+  return s24_check_launch("gemm");
+}
+
+}  // namespace s24
+
+using namespace s24;
+
+extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b,
+                        int b_mn, int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias,
+                        int epilogue, uint16_t* aux, int64_t ldaux, void* stream) {
+  S24_REQUIRE(a_vals && a_e && b && d, S24_ERR_ARG, "NULL operand");
+  S24_REQUIRE(m % 128 == 0 && k % 128 == 0 && n % 32 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
+              "sparse GEMM needs m %% 128 == 0, k %% 128 == 0, n %% 32 == 0 (got m=%lld k=%lld n=%lld)",
+              (long long)m, (long long)k, (long long)n);
+  S24_REQUIRE(ldd >= n && ldd % 8 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0, S24_ERR_UNSUPPORTED,
+              "output rows must be 16-byte aligned");
+  S24_REQUIRE(epilogue == S24_EPI_STORE || epilogue == S24_EPI_GELU_AUX, S24_ERR_ARG, "bad epilogue");
+  if (epilogue == S24_EPI_GELU_AUX)
+    S24_REQUIRE(aux != nullptr && ldaux >= n && ldaux % 8 == 0, S24_ERR_ARG, "GELU epilogue needs aux output");
+  S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
+  CUtensorMap ma, mb;
+  if (int rc = make_map(&ma, a_vals, k / 2, m, k / 2, 64, 128)) return rc;
+  constexpr int BN = 128;
+  if (b_mn) {
+    S24_REQUIRE(ldb >= n, S24_ERR_SHAPE, "ldb < n");
+    if (int rc = make_map(&mb, b, n, k, ldb, 64, 128)) return rc;
+  } else {
+    S24_REQUIRE(ldb >= k, S24_ERR_SHAPE, "ldb < k");
+    if (int rc = make_map(&mb, b, k, n, ldb, 64, BN)) return rc;
+  }
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), a_e};
+  EpiParams ep{d, ldd, bias, aux, ldaux, nullptr, 0, nullptr, 0.0f};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (b_mn) {
+    if (epilogue == S24_EPI_STORE) return launch_gemm<true, false, true, BN, 4, kEpiStore>(ma, mb, shp, ep, st);
+    return launch_gemm<true, false, true, BN, 4, kEpiGeluAux>(ma, mb, shp, ep, st);
+  }
+  if (epilogue == S24_EPI_STORE) return launch_gemm<true, false, false, BN, 4, kEpiStore>(ma, mb, shp, ep, st);
+  return launch_gemm<true, false, false, BN, 4, kEpiGeluAux>(ma, mb, shp, ep, st);
+}
+
+extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int b_mn, int64_t ldb,
+                           int64_t m, int64_t n, int64_t k, float* d, int64_t ldd, const void* w, int w_dtype,
+                           const uint8_t* idx, float lambda_w, void* stream) {
+  S24_REQUIRE(a && b && d, S24_ERR_ARG, "NULL operand");
+  S24_REQUIRE(m % 128 == 0 && n % 128 == 0 && k % 64 == 0 && m > 0 && n > 0 && k > 0, S24_ERR_SHAPE,
+              "dW GEMM needs m %% 128 == 0, n %% 128 == 0, k %% 64 == 0 (got m=%lld n=%lld k=%lld)", (long long)m,
+              (long long)n, (long long)k);
+  S24_REQUIRE(ldd >= n && ldd % 4 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0, S24_ERR_UNSUPPORTED,
+              "dW rows must be 16-byte aligned");
+  if (idx != nullptr) {
+    S24_REQUIRE(w != nullptr && (w_dtype == S24_BF16 || w_dtype == S24_F32), S24_ERR_UNSUPPORTED,
+                "masked decay needs bf16 or fp32 weights");
+  }
+  S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
+  CUtensorMap ma, mb;
+  if (a_mn) {
+    S24_REQUIRE(lda >= m, S24_ERR_SHAPE, "lda < m");
+    if (int rc = make_map(&ma, a, m, k, lda, 64, 64)) return rc;
+  } else {
+    S24_REQUIRE(lda >= k, S24_ERR_SHAPE, "lda < k");
+    if (int rc = make_map(&ma, a, k, m, lda, 64, 128)) return rc;
+  }
+  const bool wide = n % 256 == 0;
+  const int BN = wide ? 256 : 128;
+  if (b_mn) {
+    S24_REQUIRE(ldb >= n, S24_ERR_SHAPE, "ldb < n");
+    if (int rc = make_map(&mb, b, n, k, ldb, 64, 64)) return rc;
+  } else {
+    S24_REQUIRE(ldb >= k, S24_ERR_SHAPE, "ldb < k");
+    if (int rc = make_map(&mb, b, k, n, ldb, 64, BN)) return rc;
+  }
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), nullptr};
+  EpiParams ep{d, ldd, nullptr, nullptr, 0, w, w_dtype, idx, lambda_w};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define S24_DW(AMN, BMN, BNV) return launch_gemm<false, AMN, BMN, BNV, 4, kEpiDw>(ma, mb, shp, ep, st)
+  if (wide) {
+    if (a_mn && b_mn) S24_DW(true, true, 256);
+    if (a_mn) S24_DW(true, false, 256);
+    if (b_mn) S24_DW(false, true, 256);
+    S24_DW(false, false, 256);
+  }
+  if (a_mn && b_mn) S24_DW(true, true, 128);
+  if (a_mn) S24_DW(true, false, 128);
+  if (b_mn) S24_DW(false, true, 128);
+  S24_DW(false, false, 128);
+#undef S24_DW
+}

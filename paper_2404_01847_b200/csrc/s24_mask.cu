@@ -1,0 +1,577 @@
+// K1 (transposable mask search, optionally fused with compression) and
+// K2 (per-step prune/compress from a cached mask), plus the small format
+// conversion kernels.
+//
+// Reference: transposable_search_conv (sparsity.py:258-271) scores all 90
+// canonical patterns per 4x4 block by summing |w| over the 8 kept positions in
+// ascending order in float64 (_core.pyx:98-109) and keeps the first maximum.
+// Bit-exactness on the GPU:
+//   * fast path (bf16 input, block exponent span <= 13): every |w| becomes an
+//     exact integer (mantissa << (exp - emin)); the reference's float64 sums
+//     are then exact too (<= 24 significant bits), so integer sums give the
+//     identical scores in any order.  The canonical index is packed into the
+//     low 7 bits (score << 7 | 127 - t) so one integer max implements
+//     "largest score, lowest index on ties".
+//   * slow path (larger spans, fp32/fp64 inputs): float64 adds in exactly the
+//     reference's order (row 0 pair, row 1 pair, ...), with the row-0/row-1
+//     prefix shared across patterns; strict '>' in canonical order.
+//
+// One CTA = one 128 x 128 tile of W, 8 warps; lane t of warp w owns the four
+// horizontally adjacent blocks of rows 16w + 4(t/8) .. +3, columns
+// 16(t%8) .. +15.  Loads are 16-byte and coalesced (8 lanes cover a 256-byte
+// row segment).  Outputs (fwd values: 16-byte stores; idx: 4-byte stores;
+// fwd/bwd metadata tiles and the transposed kept values: staged in shared
+// memory, then written as contiguous lines).
+#include "s24_common.cuh"
+#include "s24_patterns.h"
+
+namespace s24 {
+
+__constant__ uint16_t c_pat_bits[90] = S24_PATTERN_BITS;
+
+// exactly-two-bit 4-bit mask -> nibble i0 | i1 << 2 (i0 < i1)
+__device__ __forceinline__ uint32_t nib_of_mask(uint32_t m4) {
+  const uint32_t i0 = __ffs(m4) - 1;
+  const uint32_t i1 = 31 - __clz(m4);
+  return i0 | (i1 << 2);
+}
+
+// transposed 4-bit column masks of a 16-bit pattern mask (bit r of col c)
+__device__ __forceinline__ uint32_t col_mask(uint32_t bits16, int c) {
+  return ((bits16 >> c) & 1u) | (((bits16 >> (4 + c)) & 1u) << 1) | (((bits16 >> (8 + c)) & 1u) << 2) |
+         (((bits16 >> (12 + c)) & 1u) << 3);
+}
+
+// ---------------------------------------------------------------------------
+// per-block search
+
+// float64 path in the reference's exact accumulation order.  a: |w| row-major.
+__device__ __noinline__ int search_block_f64(const double (&a)[16]) {
+  constexpr uint16_t kRows[90] = S24_PATTERN_ROWS;
+  constexpr int kLo[6] = S24_PAIR_LO;
+  constexpr int kHi[6] = S24_PAIR_HI;
+  double best = 0.0;
+  int best_t = 0;
+  double s01 = 0.0;
+#pragma unroll
+  for (int t = 0; t < 90; ++t) {
+    const int p0 = kRows[t] & 15, p1 = (kRows[t] >> 4) & 15, p2 = (kRows[t] >> 8) & 15, p3 = kRows[t] >> 12;
+    if (t == 0 || (kRows[t] & 0xFF) != (kRows[t - 1] & 0xFF)) {
+      s01 = __dadd_rn(__dadd_rn(__dadd_rn(a[kLo[p0]], a[kHi[p0]]), a[4 + kLo[p1]]), a[4 + kHi[p1]]);
+    }
+    double s = __dadd_rn(__dadd_rn(s01, a[8 + kLo[p2]]), a[8 + kHi[p2]]);
+    s = __dadd_rn(__dadd_rn(s, a[12 + kLo[p3]]), a[12 + kHi[p3]]);
+    if (t == 0 || s > best) {
+      best = s;
+      best_t = t;
+    }
+  }
+  return best_t;
+}
+
+// bf16 input: integer fast path with the float64 fallback.  h: raw bf16 bits.
+__device__ __forceinline__ int search_block_bf16(const uint16_t (&h)[16]) {
+  uint32_t man[16];
+  int ee[16];
+  int emin = 1 << 20, emax = -1;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t mag = h[i] & 0x7FFFu;
+    const int e = static_cast<int>(mag >> 7);
+    man[i] = (mag & 0x7Fu) | (e ? 0x80u : 0u);
+    ee[i] = e ? e : 1;
+    if (man[i]) {
+      emin = min(emin, ee[i]);
+      emax = max(emax, ee[i]);
+    }
+  }
+  if (emax < 0) return 0;  // all-zero block: every score ties -> pattern 0
+  if (emax - emin > 13 || emax == 0xFF) {
+    double a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = static_cast<double>(bf16_to_f32(h[i] & 0x7FFFu));
+    return search_block_f64(a);
+  }
+  int v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = static_cast<int>(man[i] << (ee[i] - emin + 7));
+  constexpr uint16_t kRows[90] = S24_PATTERN_ROWS;
+  constexpr int kLo[6] = S24_PAIR_LO;
+  constexpr int kHi[6] = S24_PAIR_HI;
+  int rp[4][6];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int p = 0; p < 6; ++p) rp[r][p] = v[4 * r + kLo[p]] + v[4 * r + kHi[p]];
+  int key = 0;
+#pragma unroll
+  for (int t = 0; t < 90; ++t) {
+    const int p0 = kRows[t] & 15, p1 = (kRows[t] >> 4) & 15, p2 = (kRows[t] >> 8) & 15, p3 = kRows[t] >> 12;
+    const int k = (rp[0][p0] + rp[1][p1]) + (rp[2][p2] + rp[3][p3]) + (127 - t);
+    key = max(key, k);
+  }
+  return 127 - (key & 127);
+}
+
+template <int kDType>
+struct Elem;
+template <>
+struct Elem<S24_BF16> {
+  using T = uint16_t;
+  static constexpr int kVec = 8;  // elements per 16-byte load
+};
+template <>
+struct Elem<S24_F32> {
+  using T = float;
+  static constexpr int kVec = 4;
+};
+template <>
+struct Elem<S24_F64> {
+  using T = double;
+  static constexpr int kVec = 2;
+};
+
+template <typename T>
+__device__ __forceinline__ uint16_t to_bf16_bits(T x);
+template <>
+__device__ __forceinline__ uint16_t to_bf16_bits<uint16_t>(uint16_t x) {
+  return x;
+}
+template <>
+__device__ __forceinline__ uint16_t to_bf16_bits<float>(float x) {
+  return f32_to_bf16(x);
+}
+template <>
+__device__ __forceinline__ uint16_t to_bf16_bits<double>(double x) {
+  return __bfloat16_as_ushort(__double2bfloat16(x));
+}
+
+// ---------------------------------------------------------------------------
+// K1 / K2 tile kernel
+
+constexpr int kTile = 128;
+constexpr int kThreads = 256;
+
+struct MaskArgs {
+  const void* w;
+  int64_t rows, cols;
+  uint8_t* idx_out;        // K1: written
+  const uint8_t* idx_in;   // K2: read
+  uint16_t* fwd_vals;      // rows x cols/2
+  uint8_t* fwd_e;          // E tiles of W
+  uint16_t* bwd_vals;      // cols x rows/2
+  uint8_t* bwd_e;          // E tiles of W^T
+};
+
+// kNarrow: bf16 rows that are only 8-byte aligned (cols % 8 == 4) load 4 elements at a time
+template <int kDType, bool kSearch, bool kNarrow>
+__global__ void __launch_bounds__(kThreads) mask_tile_kernel(MaskArgs p) {
+  using T = typename Elem<kDType>::T;
+  constexpr int kVec = kNarrow ? 4 : Elem<kDType>::kVec;
+
+  __shared__ __align__(16) uint32_t s_fe[512];        // fwd E tile, 2048 B
+  __shared__ __align__(16) uint32_t s_be[512];        // bwd E tile, 2048 B
+  __shared__ __align__(16) uint32_t s_bv[128 * 32];   // bwd kept values, 128 x 64 bf16 (swizzled)
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tr = blockIdx.y, tc = blockIdx.x;  // tile row / col
+  const int br = 4 * warp + (lane >> 3);              // block-row within tile (0..31)
+  const int c0 = 16 * (lane & 7);                     // first column within tile
+  const int64_t grow0 = tr * kTile + 4 * br;
+  const int64_t gcol0 = tc * kTile + c0;
+  const bool want_fe = p.fwd_e != nullptr, want_be = p.bwd_e != nullptr, want_bv = p.bwd_vals != nullptr;
+
+  if (want_fe || want_be) {
+    for (int i = threadIdx.x; i < 512; i += kThreads) {
+      s_fe[i] = 0;
+      s_be[i] = 0;
+    }
+  }
+  if (want_fe || want_be || want_bv) __syncthreads();
+
+  const bool row_ok = grow0 < p.rows;
+  // ---- load 4 rows x 16 columns ----
+  T v[4][16];
+  const T* w = static_cast<const T*>(p.w);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int q = 0; q < 16 / kVec; ++q) {
+      const int64_t col = gcol0 + q * kVec;
+      if (row_ok && col < p.cols) {
+        if constexpr (kNarrow) {
+          const uint2 u = __ldg(reinterpret_cast<const uint2*>(w + (grow0 + i) * p.cols + col));
+          const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) v[i][q * kVec + j] = e[j];
+        } else {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(w + (grow0 + i) * p.cols + col));
+          const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) v[i][q * kVec + j] = e[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) v[i][q * kVec + j] = T(0);
+      }
+    }
+  }
+
+  // ---- per block: pattern ----
+  int pat[4];
+  uint32_t idx_word = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const bool ok = row_ok && (gcol0 + 4 * b) < p.cols;
+    int t = 0;
+    if constexpr (kSearch) {
+      if (ok) {
+        if constexpr (kDType == S24_BF16) {
+          uint16_t h[16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) h[4 * i + j] = v[i][4 * b + j];
+          t = search_block_bf16(h);
+        } else {
+          double a[16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a[4 * i + j] = fabs(static_cast<double>(v[i][4 * b + j]));
+          t = search_block_f64(a);
+        }
+      }
+    } else {
+      if (ok) t = p.idx_in[(grow0 / 4) * (p.cols / 4) + gcol0 / 4 + b];
+      if (t > 89) t = 0;  // validated upstream; never index out of the table
+    }
+    pat[b] = t;
+    idx_word |= static_cast<uint32_t>(t) << (8 * b);
+  }
+
+  // ---- idx ----
+  if (kSearch && row_ok) {
+    uint8_t* dst = p.idx_out + (grow0 / 4) * (p.cols / 4) + gcol0 / 4;
+    if (gcol0 + 16 <= p.cols && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+      *reinterpret_cast<uint32_t*>(dst) = idx_word;
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (gcol0 + 4 * b < p.cols) dst[b] = static_cast<uint8_t>(idx_word >> (8 * b));
+    }
+  }
+
+  // ---- fwd orientation: kept values along rows + E halfwords ----
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t packed[4];
+    uint32_t half = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t m4 = (c_pat_bits[pat[b]] >> (4 * i)) & 0xFu;
+      const uint32_t nib = nib_of_mask(m4);
+      const int i0 = nib & 3, i1 = nib >> 2;
+      uint16_t lo = 0, hi = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint16_t bits = to_bf16_bits<T>(v[i][4 * b + j]);
+        lo = (j == i0) ? bits : lo;
+        hi = (j == i1) ? bits : hi;
+      }
+      packed[b] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+      half |= nib << (4 * b);
+    }
+    if (p.fwd_vals != nullptr && row_ok) {
+      uint16_t* dst = p.fwd_vals + (grow0 + i) * (p.cols / 2) + gcol0 / 2;
+      if (gcol0 + 16 <= p.cols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      } else {
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (gcol0 + 4 * b < p.cols) reinterpret_cast<uint32_t*>(dst)[b] = packed[b];
+      }
+    }
+    if (want_fe) {
+      const int m = 4 * br + i;  // tile-local row
+      const int L = (m & 7) + 8 * ((c0 & 31) >> 4) + 16 * (m >> 4);
+      const int c = c0 >> 5, h = (m >> 3) & 1;
+      reinterpret_cast<uint16_t*>(s_fe)[L * 8 + c * 2 + h] = static_cast<uint16_t>(half);
+    }
+  }
+
+  // ---- bwd orientation (W^T): kept values along columns + E nibbles ----
+  if (want_bv || want_be) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t bits16 = c_pat_bits[pat[b]];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t nib = nib_of_mask(col_mask(bits16, j));
+        const int i0 = nib & 3, i1 = nib >> 2;
+        uint16_t lo = 0, hi = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint16_t bits = to_bf16_bits<T>(v[i][4 * b + j]);
+          lo = (i == i0) ? bits : lo;
+          hi = (i == i1) ? bits : hi;
+        }
+        const int mp = c0 + 4 * b + j;  // tile-local row of W^T
+        if (want_bv) {
+          s_bv[mp * 32 + ((br + 4 * (mp >> 4)) & 31)] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+        }
+        if (want_be) {
+          const int L = (mp & 7) + 16 * (mp >> 4) + 8 * (warp & 1);
+          const int c = warp >> 1, h = (mp >> 3) & 1;
+          atomicOr(&s_be[L * 4 + c], nib << (16 * h + 4 * (lane >> 3)));
+        }
+      }
+    }
+  }
+
+  if (want_fe || want_be || want_bv) __syncthreads();
+  const bool full_tile = (tr + 1) * kTile <= p.rows && (tc + 1) * kTile <= p.cols;
+  if (want_fe && full_tile) {
+    uint4* dst = reinterpret_cast<uint4*>(p.fwd_e + (tr * (p.cols / kTile) + tc) * 2048);
+    if (threadIdx.x < 128) dst[threadIdx.x] = reinterpret_cast<const uint4*>(s_fe)[threadIdx.x];
+  }
+  if (want_be && full_tile) {
+    uint4* dst = reinterpret_cast<uint4*>(p.bwd_e + (tc * (p.rows / kTile) + tr) * 2048);
+    if (threadIdx.x >= 128) dst[threadIdx.x - 128] = reinterpret_cast<const uint4*>(s_be)[threadIdx.x - 128];
+  }
+  if (want_bv) {
+    // W^T tile: 128 rows x 64 kept values; one warp streams one 128-byte row
+    const int64_t kcol = tr * (kTile / 2) + 2 * lane;  // kept-value column
+    for (int rr = warp; rr < kTile; rr += kThreads / 32) {
+      const int64_t grow_t = tc * kTile + rr;  // row of W^T = column of W
+      if (grow_t < p.cols && kcol < p.rows / 2) {
+        const uint32_t val = s_bv[rr * 32 + ((lane + 4 * (rr >> 4)) & 31)];
+        *reinterpret_cast<uint32_t*>(p.bwd_vals + grow_t * (p.rows / 2) + kcol) = val;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// small conversion kernels
+
+__global__ void idx_to_bits_kernel(const uint8_t* __restrict__ idx, int64_t rows, int64_t cols,
+                                   uint8_t* __restrict__ bits) {
+  const int64_t nb = (rows / 4) * (cols / 4);
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t bi = b / (cols / 4), bj = b % (cols / 4);
+    const uint32_t pb = c_pat_bits[min(static_cast<int>(idx[b]), 89)];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t m4 = (pb >> (4 * r)) & 0xF;
+      const uint32_t word = (m4 & 1) | ((m4 & 2) << 7) | ((m4 & 4) << 14) | ((m4 & 8) << 21);
+      *reinterpret_cast<uint32_t*>(bits + (4 * bi + r) * cols + 4 * bj) = word;
+    }
+  }
+}
+
+__global__ void bits_to_idx_kernel(const uint8_t* __restrict__ bits, int64_t rows, int64_t cols,
+                                   uint8_t* __restrict__ idx, int32_t* bad) {
+  const int64_t nb = (rows / 4) * (cols / 4);
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t bi = b / (cols / 4), bj = b % (cols / 4);
+    uint32_t m16 = 0;
+    bool ok = true;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint8_t x = bits[(4 * bi + r) * cols + 4 * bj + c];
+        ok = ok && x <= 1;
+        m16 |= static_cast<uint32_t>(x & 1) << (4 * r + c);
+      }
+    int found = 255;
+    if (ok) {
+      for (int t = 0; t < 90; ++t)
+        if (c_pat_bits[t] == m16) {
+          found = t;
+          break;
+        }
+    }
+    idx[b] = static_cast<uint8_t>(found);
+    if (found == 255) atomicAdd(bad, 1);
+  }
+}
+
+__global__ void meta_flat_kernel(const uint8_t* __restrict__ idx, int64_t rows, int64_t cols,
+                                 uint8_t* __restrict__ fwd, uint8_t* __restrict__ bwd) {
+  const int64_t nb = (rows / 4) * (cols / 4);
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t bi = b / (cols / 4), bj = b % (cols / 4);
+    const uint32_t pb = c_pat_bits[min(static_cast<int>(idx[b]), 89)];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (fwd) fwd[(4 * bi + r) * (cols / 4) + bj] = static_cast<uint8_t>(nib_of_mask((pb >> (4 * r)) & 0xF));
+      if (bwd) bwd[(4 * bj + r) * (rows / 4) + bi] = static_cast<uint8_t>(nib_of_mask(col_mask(pb, r)));
+    }
+  }
+}
+
+__global__ void e_to_flat_kernel(const uint8_t* __restrict__ e, int64_t m, int64_t k, uint8_t* __restrict__ meta) {
+  const int64_t ng = m * (k / 4);
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = g / (k / 4), grp = g % (k / 4);
+    const int64_t tile = (row / 128) * (k / 128) + (grp * 4) / 128;
+    const int mm = row % 128, kk = (grp * 4) % 128;
+    const int L = (mm & 7) + 8 * ((kk & 31) >> 4) + 16 * (mm >> 4);
+    const int c = kk >> 5, h = (mm >> 3) & 1, gsub = (kk & 15) >> 2;
+    const uint16_t word = *reinterpret_cast<const uint16_t*>(e + tile * 2048 + L * 16 + c * 4 + h * 2);
+    meta[g] = static_cast<uint8_t>((word >> (4 * gsub)) & 0xF);
+  }
+}
+
+__global__ void masked_decay_kernel(float* __restrict__ g, const void* __restrict__ w, int w_dtype,
+                                    const uint8_t* __restrict__ idx, int64_t rows, int64_t cols, float lam) {
+  const int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e % cols;
+    const uint32_t pb = c_pat_bits[min(static_cast<int>(idx[(r / 4) * (cols / 4) + c / 4]), 89)];
+    if ((pb >> (4 * (r & 3) + (c & 3))) & 1) continue;
+    float wv;
+    if (w_dtype == S24_BF16)
+      wv = bf16_to_f32(static_cast<const uint16_t*>(w)[e]);
+    else if (w_dtype == S24_F32)
+      wv = static_cast<const float*>(w)[e];
+    else
+      wv = static_cast<float>(static_cast<const double*>(w)[e]);
+    g[e] = g[e] + lam * wv;
+  }
+}
+
+}  // namespace s24
+
+using namespace s24;
+
+static int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 32) g = 148 * 32;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+static int check_w(const void* w, int dtype, int64_t rows, int64_t cols) {
+  S24_REQUIRE(w != nullptr, S24_ERR_ARG, "weight pointer is NULL");
+  S24_REQUIRE(dtype == S24_BF16 || dtype == S24_F32 || dtype == S24_F64, S24_ERR_UNSUPPORTED,
+              "unsupported weight dtype %d", dtype);
+  S24_REQUIRE(rows >= 0 && cols >= 0 && rows % 4 == 0 && cols % 4 == 0, S24_ERR_SHAPE,
+              "shape (%lld, %lld) not divisible into 4x4 blocks", (long long)rows, (long long)cols);
+  S24_REQUIRE((reinterpret_cast<uintptr_t>(w) & 15) == 0, S24_ERR_UNSUPPORTED,
+              "weight base pointer must be 16-byte aligned");
+  return S24_OK;
+}
+
+static int launch_mask(const MaskArgs& a, int dtype, bool search, cudaStream_t st) {
+  if (a.rows == 0 || a.cols == 0) return S24_OK;
+  dim3 grid(static_cast<unsigned>((a.cols + kTile - 1) / kTile), static_cast<unsigned>((a.rows + kTile - 1) / kTile));
+  const bool narrow = dtype == S24_BF16 && (a.cols % 8) != 0;
+  if (search) {
+    if (narrow) mask_tile_kernel<S24_BF16, true, true><<<grid, kThreads, 0, st>>>(a);
+    else if (dtype == S24_BF16) mask_tile_kernel<S24_BF16, true, false><<<grid, kThreads, 0, st>>>(a);
+    else if (dtype == S24_F32) mask_tile_kernel<S24_F32, true, false><<<grid, kThreads, 0, st>>>(a);
+    else mask_tile_kernel<S24_F64, true, false><<<grid, kThreads, 0, st>>>(a);
+  } else {
+    if (narrow) mask_tile_kernel<S24_BF16, false, true><<<grid, kThreads, 0, st>>>(a);
+    else if (dtype == S24_BF16) mask_tile_kernel<S24_BF16, false, false><<<grid, kThreads, 0, st>>>(a);
+    else if (dtype == S24_F32) mask_tile_kernel<S24_F32, false, false><<<grid, kThreads, 0, st>>>(a);
+    else mask_tile_kernel<S24_F64, false, false><<<grid, kThreads, 0, st>>>(a);
+  }
+  return s24_check_launch(search ? "mask_search" : "prune_compress");
+}
+
+extern "C" int s24_transposable_search(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* idx,
+                                       void* stream) {
+  if (int rc = check_w(w, dtype, rows, cols)) return rc;
+  S24_REQUIRE(idx != nullptr, S24_ERR_ARG, "idx pointer is NULL");
+  MaskArgs a{w, rows, cols, idx, nullptr, nullptr, nullptr, nullptr, nullptr};
+  return launch_mask(a, dtype, true, static_cast<cudaStream_t>(stream));
+}
+
+static int check_compress_outputs(int64_t rows, int64_t cols, const void* fwd_e, const void* bwd_e) {
+  if (fwd_e != nullptr || bwd_e != nullptr)
+    S24_REQUIRE(rows % 128 == 0 && cols % 128 == 0, S24_ERR_SHAPE,
+                "tensor-core metadata tiles need rows and cols divisible by 128, got (%lld, %lld)",
+                (long long)rows, (long long)cols);
+  return S24_OK;
+}
+
+extern "C" int s24_search_compress(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* idx,
+                                   uint16_t* fwd_vals, uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e,
+                                   void* stream) {
+  if (int rc = check_w(w, dtype, rows, cols)) return rc;
+  S24_REQUIRE(idx != nullptr, S24_ERR_ARG, "idx pointer is NULL");
+  if (int rc = check_compress_outputs(rows, cols, fwd_e, bwd_e)) return rc;
+  MaskArgs a{w, rows, cols, idx, nullptr, fwd_vals, fwd_e, bwd_vals, bwd_e};
+  return launch_mask(a, dtype, true, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int s24_prune_compress(const void* w, int dtype, int64_t rows, int64_t cols, const uint8_t* idx,
+                                  uint16_t* fwd_vals, uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e,
+                                  void* stream) {
+  if (int rc = check_w(w, dtype, rows, cols)) return rc;
+  S24_REQUIRE(idx != nullptr, S24_ERR_ARG, "idx pointer is NULL");
+  if (int rc = check_compress_outputs(rows, cols, fwd_e, bwd_e)) return rc;
+  MaskArgs a{w, rows, cols, nullptr, idx, fwd_vals, fwd_e, bwd_vals, bwd_e};
+  return launch_mask(a, dtype, false, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int s24_idx_to_bits(const uint8_t* idx, int64_t rows, int64_t cols, uint8_t* bits, void* stream) {
+  S24_REQUIRE(idx && bits, S24_ERR_ARG, "NULL pointer");
+  S24_REQUIRE(rows % 4 == 0 && cols % 4 == 0, S24_ERR_SHAPE, "shape (%lld, %lld) not divisible into 4x4 blocks",
+              (long long)rows, (long long)cols);
+  S24_REQUIRE((reinterpret_cast<uintptr_t>(bits) & 3) == 0, S24_ERR_UNSUPPORTED, "bits must be 4-byte aligned");
+  const int64_t nb = (rows / 4) * (cols / 4);
+  if (nb == 0) return S24_OK;
+  idx_to_bits_kernel<<<grid_for(nb, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(idx, rows, cols, bits);
+  return s24_check_launch("idx_to_bits");
+}
+
+extern "C" int s24_bits_to_idx(const uint8_t* bits, int64_t rows, int64_t cols, uint8_t* idx, int32_t* bad_count,
+                               void* stream) {
+  S24_REQUIRE(idx && bits && bad_count, S24_ERR_ARG, "NULL pointer");
+  S24_REQUIRE(rows % 4 == 0 && cols % 4 == 0, S24_ERR_SHAPE, "shape (%lld, %lld) not divisible into 4x4 blocks",
+              (long long)rows, (long long)cols);
+  const int64_t nb = (rows / 4) * (cols / 4);
+  if (nb == 0) return S24_OK;
+  bits_to_idx_kernel<<<grid_for(nb, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(bits, rows, cols, idx,
+                                                                                        bad_count);
+  return s24_check_launch("bits_to_idx");
+}
+
+extern "C" int s24_meta_flat(const uint8_t* idx, int64_t rows, int64_t cols, uint8_t* fwd_meta, uint8_t* bwd_meta,
+                             void* stream) {
+  S24_REQUIRE(idx != nullptr, S24_ERR_ARG, "NULL idx");
+  S24_REQUIRE(rows % 4 == 0 && cols % 4 == 0, S24_ERR_SHAPE, "shape (%lld, %lld) not divisible into 4x4 blocks",
+              (long long)rows, (long long)cols);
+  const int64_t nb = (rows / 4) * (cols / 4);
+  if (nb == 0) return S24_OK;
+  meta_flat_kernel<<<grid_for(nb, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(idx, rows, cols, fwd_meta,
+                                                                                     bwd_meta);
+  return s24_check_launch("meta_flat");
+}
+
+extern "C" int s24_e_to_flat(const uint8_t* e, int64_t m, int64_t k, uint8_t* meta, void* stream) {
+  S24_REQUIRE(e && meta, S24_ERR_ARG, "NULL pointer");
+  S24_REQUIRE(m % 128 == 0 && k % 128 == 0, S24_ERR_SHAPE, "E tiles need m, k divisible by 128");
+  const int64_t ng = m * (k / 4);
+  if (ng == 0) return S24_OK;
+  e_to_flat_kernel<<<grid_for(ng, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(e, m, k, meta);
+  return s24_check_launch("e_to_flat");
+}
+
+extern "C" int s24_masked_decay(float* g, const void* w, int w_dtype, const uint8_t* idx, int64_t rows,
+                                int64_t cols, float lambda_w, void* stream) {
+  S24_REQUIRE(g && w && idx, S24_ERR_ARG, "NULL pointer");
+  S24_REQUIRE(rows % 4 == 0 && cols % 4 == 0, S24_ERR_SHAPE, "shape (%lld, %lld) not divisible into 4x4 blocks",
+              (long long)rows, (long long)cols);
+  S24_REQUIRE(w_dtype == S24_BF16 || w_dtype == S24_F32 || w_dtype == S24_F64, S24_ERR_UNSUPPORTED, "bad dtype");
+  const int64_t n = rows * cols;
+  if (n == 0) return S24_OK;
+  masked_decay_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(g, w, w_dtype, idx, rows, cols,
+                                                                                       lambda_w);
+  return s24_check_launch("masked_decay");
+}

@@ -1,0 +1,177 @@
+"""Raw-tensor engine of the 2:4 FFN hot path (one FFN block fwd + bwd).
+
+Every function here is a thin sequence of C-ABI kernel launches on the
+current CUDA stream; the reference-facing API (gated_ffn.py) and the autograd
+module (module.py) are built on it.
+
+Layouts (see include/sparse24_b200.h):
+  x, dy            token-major  (N x d, row-major) -- the caller's tensors
+  zt, at, dat, dzt feature-major (features x N, row-major): the sparse GEMM
+                   writes D[m = feature, n = token], which is the reference's
+                   column-major FST output (gated_ffn.py:162, _core.pyx:67-69)
+  yt, dxt          feature-major (d x N); the API returns them as the
+                   column-major logical views y = yt.t(), dx = dxt.t()
+
+Reference call stack replaced:
+  forward : in_fwd.product -> +bias -> _activate -> out_fwd.product   (gated_ffn.py:293-297)
+  backward: out_bwd.product, _grad_weight x2, activation bwd, in_bwd.product (gated_ffn.py:327-356)
+  update  : masked_decay_gradient (optim.py:105-114) fused into the dW epilogue
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _capi as C
+from .matrix import ShapeError
+
+ACT_CODES = {"relu": C.ACT_RELU, "gelu": C.ACT_GELU, "geglu": C.ACT_GEGLU, "swiglu": C.ACT_SWIGLU}
+GATED = {"geglu", "swiglu"}
+
+
+@dataclass
+class CompressedOperand:
+    """Both 2:4 orientations of one weight under one transposable mask -- the
+    B200 counterpart of a pair of _GatherPlans (gated_ffn.py:131-188)."""
+
+    rows: int
+    cols: int
+    idx: torch.Tensor  # (rows/4, cols/4) pattern indices (the mask)
+    fwd_vals: torch.Tensor  # (rows, cols/2) bf16: A operand of W x (fwd)
+    fwd_e: torch.Tensor  # E tiles for fwd_vals
+    bwd_vals: torch.Tensor  # (cols, rows/2) bf16: A operand of W^T (bwd)
+    bwd_e: torch.Tensor  # E tiles for bwd_vals
+
+    @classmethod
+    def empty(cls, rows: int, cols: int, device) -> "CompressedOperand":
+        if rows % 128 or cols % 128:
+            raise ShapeError(
+                f"2:4 tensor-core operands need both weight dims divisible by 128, got ({rows}, {cols})")
+        e_bytes = (rows // 128) * (cols // 128) * 2048
+        u8 = dict(dtype=torch.uint8, device=device)
+        bf = dict(dtype=torch.bfloat16, device=device)
+        return cls(rows, cols, torch.empty((rows // 4, cols // 4), **u8),
+                   torch.empty((rows, cols // 2), **bf), torch.empty(e_bytes, **u8),
+                   torch.empty((cols, rows // 2), **bf), torch.empty(e_bytes, **u8))
+
+
+def search_compress(w: torch.Tensor, op: CompressedOperand) -> None:
+    """K1 fused: new mask + metadata + kept values (mask refresh step)."""
+    C.call("s24_search_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),
+           op.fwd_vals.data_ptr(), op.fwd_e.data_ptr(), op.bwd_vals.data_ptr(), op.bwd_e.data_ptr(),
+           C.stream_of(w))
+
+
+def compress_with_meta(w: torch.Tensor, op: CompressedOperand) -> None:
+    """K2 with metadata: (re)build E tiles and values from a given mask (op.idx)."""
+    C.call("s24_prune_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),
+           op.fwd_vals.data_ptr(), op.fwd_e.data_ptr(), op.bwd_vals.data_ptr(), op.bwd_e.data_ptr(),
+           C.stream_of(w))
+
+
+def compress_values(w: torch.Tensor, op: CompressedOperand) -> None:
+    """K2: per-step prune/compress of the current weight values (mask cached)."""
+    C.call("s24_prune_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),
+           op.fwd_vals.data_ptr(), None, op.bwd_vals.data_ptr(), None, C.stream_of(w))
+
+
+def spmm(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b_mn: bool, n: int,
+         out: torch.Tensor, bias: torch.Tensor | None = None, gelu_aux: torch.Tensor | None = None) -> None:
+    """out[m, n] (bf16, row-major) = W~[m, k] (2:4) . B[n, k]^T (+ bias[m]); optional aux = gelu(out)."""
+    ldb = b.stride(0)
+    C.call("s24_spmm", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), ldb, n,
+           out.data_ptr(), out.stride(0), C.ptr(bias), C.EPI_GELU_AUX if gelu_aux is not None else C.EPI_STORE,
+           C.ptr(gelu_aux), gelu_aux.stride(0) if gelu_aux is not None else 0, C.stream_of(out))
+
+
+def gemm_dw(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, m: int, n: int, k: int,
+            out: torch.Tensor, w: torch.Tensor | None = None, idx: torch.Tensor | None = None,
+            lam: float = 0.0) -> None:
+    """out[m, n] fp32 = sum_k A[m, k] B[n, k] + lam (1 - M) W  (dense tcgen05)."""
+    decay = idx is not None and lam != 0.0
+    C.call("s24_gemm_dw", a.data_ptr(), int(a_mn), a.stride(0), b.data_ptr(), int(b_mn), b.stride(0), m, n, k,
+           out.data_ptr(), out.stride(0), C.ptr(w) if decay else None, C.dtype_code(w) if decay else 0,
+           C.ptr(idx) if decay else None, float(lam if decay else 0.0), C.stream_of(out))
+
+
+def _token_operand(t: torch.Tensor) -> tuple[torch.Tensor, bool]:
+    """(storage, mn_major) for a logical (N x f) activation: row-major storage
+    is K-major for the sparse GEMM; a column-major view (feature-major
+    storage) is MN-major."""
+    if t.stride(1) == 1 and t.stride(0) >= t.shape[1] and t.stride(0) % 8 == 0:
+        return t, False
+    if t.stride(0) == 1 and t.stride(1) >= t.shape[0] and t.stride(1) % 8 == 0:
+        return t.t(), True
+    return t.contiguous(), False
+
+
+@dataclass
+class FwdState:
+    x: torch.Tensor  # (N, d) as given (bf16)
+    zt: torch.Tensor  # (r_in, N)
+    at: torch.Tensor  # (d_ff, N)
+    yt: torch.Tensor  # (d, N)
+
+
+def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor | None, w2: CompressedOperand,
+                act: str) -> FwdState:
+    n, d = x.shape
+    r_in = w_in.rows
+    d_ff = w2.cols
+    if w_in.cols != d or w2.rows != d or (r_in != (2 * d_ff if act in GATED else d_ff)):
+        raise ShapeError("layer weight shapes are inconsistent with the activation / input width")
+    if n % 64:
+        raise ShapeError(f"token count must be a multiple of 64 on the tensor-core path, got {n}")
+    dev = x.device
+    xs, x_mn = _token_operand(x)
+    zt = torch.empty((r_in, n), dtype=torch.bfloat16, device=dev)
+    at = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
+    if act == "gelu":
+        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, zt, bias_in, gelu_aux=at)
+    else:
+        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, zt, bias_in)
+        C.call("s24_act_fwd", zt.data_ptr(), n, d_ff, n, ACT_CODES[act], at.data_ptr(), n, C.stream_of(zt))
+    yt = torch.empty((d, n), dtype=torch.bfloat16, device=dev)
+    spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, at, True, n, yt)
+    return FwdState(x, zt, at, yt)
+
+
+@dataclass
+class Grads:
+    dxt: torch.Tensor  # (d, N) bf16
+    dw_in: torch.Tensor  # (r_in, d) fp32
+    dbias_in: torch.Tensor  # (r_in,) fp32
+    dw2: torch.Tensor  # (d, d_ff) fp32
+
+
+def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: CompressedOperand, act: str,
+                 w_in_dense: torch.Tensor | None = None, w2_dense: torch.Tensor | None = None,
+                 lam: float = 0.0, dw_in_out: torch.Tensor | None = None,
+                 dw2_out: torch.Tensor | None = None) -> Grads:
+    n, d = st.x.shape
+    r_in, d_ff = w_in.rows, w2.cols
+    if tuple(dy.shape) != (n, d):
+        raise ShapeError(f"upstream shape {tuple(dy.shape)} != output shape {(n, d)}")
+    dev = dy.device
+    dys, dy_mn = _token_operand(dy)
+    # dA^T = W2~^T . dY^T   (out_bwd: groups of W2 along d)
+    dat = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
+    spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dys, dy_mn, n, dat)
+    # activation backward + bias gradients
+    dzt = torch.empty((r_in, n), dtype=torch.bfloat16, device=dev)
+    dbias = torch.empty(r_in, dtype=torch.float32, device=dev)
+    C.call("s24_act_bwd", st.zt.data_ptr(), n, dat.data_ptr(), n, d_ff, n, ACT_CODES[act], dzt.data_ptr(), n,
+           dbias.data_ptr(), C.stream_of(dzt))
+    # dX^T = W_in~^T . dZ^T  (in_bwd: groups of W_in along r_in)
+    dxt = torch.empty((d, n), dtype=torch.bfloat16, device=dev)
+    spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dzt, True, n, dxt)
+    # dW2[d, d_ff] = dY^T A : A-op = dY (K = tokens), B-op = A^T (feature-major, K-major)
+    dw2 = dw2_out if dw2_out is not None else torch.empty((d, d_ff), dtype=torch.float32, device=dev)
+    gemm_dw(dys, not dy_mn, st.at, False, d, d_ff, n, dw2, w2_dense, w2.idx, lam)
+    # dW_in[r_in, d] = dZ^T X : A-op = dZ^T (K-major), B-op = X (token-major => MN-major)
+    xs, x_mn = _token_operand(st.x)
+    dw_in = dw_in_out if dw_in_out is not None else torch.empty((r_in, d), dtype=torch.float32, device=dev)
+    gemm_dw(dzt, False, xs, not x_mn, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam)
+    return Grads(dxt, dw_in, dbias, dw2)

@@ -1,0 +1,293 @@
+"""Gated activations and the fully sparse FFN layer on the B200 -- the
+reference API of sparse24.gated_ffn (gated_ffn.py:1-373) over CUDA tensors.
+
+Differences from the reference that are deliberate and visible:
+  * tensors are torch CUDA tensors; compute is bf16 with fp32 accumulation
+    (the reference is float64); tolerances are stated in tests/;
+  * z, a, y, d_x come back as column-major logical views of feature-major
+    storage -- the same storage order the reference's sparse route produces
+    (gated_ffn.py:162);
+  * weight gradients are fp32;
+  * mvue=True (the reference default, gated_ffn.py:308) needs the MVUE
+    sparse dW kernel, not built yet: it raises
+    NotImplementedError instead of silently computing the dense dW.
+  * Activation.SWIGLU is an extension (not in the reference enum).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from enum import Enum
+
+import torch
+
+from . import _capi as C
+from . import engine as E
+from .matrix import Layout, ShapeError
+from .sparsity import TransposableMask, transposable_search_conv
+
+__all__ = [
+    "Activation", "Traversal", "FFNLayer", "FFNMasks", "LayerGrads", "FstActivations",
+    "gelu", "gelu_grad", "geglu_forward", "geglu_backward", "fst_forward", "fst_backward",
+]
+
+
+class Activation(Enum):
+    RELU = "relu"
+    GELU = "gelu"
+    GEGLU = "geglu"
+    SWIGLU = "swiglu"  # extension
+
+
+class Traversal(Enum):
+    """Accepted for API compatibility: on the GPU the gate always streams the
+    contiguous (token) axis; values never depend on traversal (test_gated_ffn.py:96-103)."""
+
+    ROW_ORDER = "row_order"
+    COL_ORDER = "col_order"
+
+
+def gelu(x: torch.Tensor) -> torch.Tensor:
+    """Exact GELU (gated_ffn.py:58-62); elementwise helper in torch, not a hot path."""
+    return 0.5 * x * (1.0 + torch.erf(x * 0.7071067811865476))
+
+
+def gelu_grad(x: torch.Tensor) -> torch.Tensor:
+    return 0.5 * (1.0 + torch.erf(x * 0.7071067811865476)) + x * 0.3989422804014327 * torch.exp(-0.5 * x * x)
+
+
+@dataclass
+class FFNLayer:
+    """One FFN layer (gated_ffn.py:77-128).  The gated first weight is stored
+    concatenated as w_in = [u; v] (r_in = 2 d_ff) with bias_in = [b; c], which
+    is how the trainer lays it out (trainer.py:166) and what the single
+    transposable mask covers."""
+
+    w_in_cat: torch.Tensor  # (r_in, d)
+    bias_in_cat: torch.Tensor  # (r_in,)
+    w2: torch.Tensor  # (d, d_ff)
+    activation: Activation
+
+    def __post_init__(self) -> None:
+        d, d_ff = self.w2.shape
+        if d % 4 or d_ff % 4:
+            raise ShapeError(f"layer widths must be divisible by 4, got d={d}, d_ff={d_ff}")
+        r_in = 2 * d_ff if self.is_gated else d_ff
+        if tuple(self.w_in_cat.shape) != (r_in, d):
+            raise ShapeError(f"w_in shape {tuple(self.w_in_cat.shape)} != {(r_in, d)}")
+
+    @property
+    def is_gated(self) -> bool:
+        return self.activation in (Activation.GEGLU, Activation.SWIGLU)
+
+    @property
+    def d(self) -> int:
+        return self.w2.shape[0]
+
+    @property
+    def d_ff(self) -> int:
+        return self.w2.shape[1]
+
+    def w_in(self) -> torch.Tensor:
+        return self.w_in_cat
+
+    def bias_in(self) -> torch.Tensor:
+        return self.bias_in_cat
+
+    @property
+    def w1(self):
+        return None if self.is_gated else self.w_in_cat
+
+    @property
+    def u(self):
+        return self.w_in_cat[: self.d_ff] if self.is_gated else None
+
+    @property
+    def v(self):
+        return self.w_in_cat[self.d_ff:] if self.is_gated else None
+
+    @classmethod
+    def gated(cls, u, v, b, c, w2, activation: Activation = Activation.GEGLU) -> "FFNLayer":
+        return cls(torch.cat([u, v], 0).contiguous(), torch.cat([b, c]).contiguous(), w2, activation)
+
+    @classmethod
+    def plain(cls, w1, b, w2, activation: Activation = Activation.GELU) -> "FFNLayer":
+        return cls(w1.contiguous(), b.contiguous(), w2, activation)
+
+
+@dataclass
+class FFNMasks:
+    """Transposable masks for w_in and w2 (gated_ffn.py:165-188).  `plans()`
+    validates once and builds the tensor-core metadata (E tiles) for both
+    orientations; per-step values are recompressed from the current weights
+    on every forward (the reference re-gathers them the same way,
+    gated_ffn.py:159-162)."""
+
+    w_in: TransposableMask
+    w_out: TransposableMask
+    _ops: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def plans(self, layer: FFNLayer | None = None) -> dict:
+        if not self._ops:
+            self.w_in.validate()
+            self.w_out.validate()
+            if layer is None:
+                return self._ops
+            for name, mask, w in (("in", self.w_in, layer.w_in_cat), ("out", self.w_out, layer.w2)):
+                op = E.CompressedOperand.empty(mask.shape[0], mask.shape[1], w.device)
+                op.idx.copy_(mask.idx)
+                E.compress_with_meta(w, op)
+                self._ops[name] = op
+        return self._ops
+
+
+@dataclass
+class LayerGrads:
+    d_x: torch.Tensor
+    d_w2: torch.Tensor | None = None
+    d_b: torch.Tensor | None = None
+    d_w1: torch.Tensor | None = None
+    d_u: torch.Tensor | None = None
+    d_v: torch.Tensor | None = None
+    d_c: torch.Tensor | None = None
+
+
+@dataclass
+class FstActivations:
+    """Everything the backward needs from one forward (gated_ffn.py:251-261)."""
+
+    layer: FFNLayer
+    x: torch.Tensor
+    z: torch.Tensor  # (N, r_in) column-major view
+    a: torch.Tensor  # (N, d_ff) column-major view
+    y: torch.Tensor  # (N, d) column-major view
+    masks: FFNMasks | None
+    w_in_cat: torch.Tensor
+    state: E.FwdState | None = None
+
+
+def _as_bf16(t: torch.Tensor) -> torch.Tensor:
+    C.require_cuda(t)
+    return t if t.dtype == torch.bfloat16 else t.to(torch.bfloat16)
+
+
+def _dense_act(layer: FFNLayer, z: torch.Tensor) -> torch.Tensor:
+    r = layer.d_ff
+    if layer.activation is Activation.GEGLU:
+        return gelu(z[:, :r]) * z[:, r:]
+    if layer.activation is Activation.SWIGLU:
+        return torch.nn.functional.silu(z[:, :r]) * z[:, r:]
+    if layer.activation is Activation.GELU:
+        return gelu(z)
+    return torch.relu(z)
+
+
+def fst_forward(layer: FFNLayer, x: torch.Tensor, masks: FFNMasks | None,
+                traversal: Traversal = Traversal.COL_ORDER) -> FstActivations:
+    """Forward (gated_ffn.py:273-301).  masks=None is the dense path (dense
+    fine-tuning, gated_ffn.py:286-289): plain bf16 library GEMMs."""
+    x = _as_bf16(x)
+    if x.dim() != 2 or x.shape[1] != layer.d:
+        raise ShapeError(f"x shape {tuple(x.shape)} does not match layer width {layer.d}")
+    if masks is None:
+        z = torch.nn.functional.linear(x, layer.w_in_cat.to(torch.bfloat16), layer.bias_in_cat.to(torch.bfloat16))
+        a = _dense_act(layer, z)
+        y = torch.nn.functional.linear(a, layer.w2.to(torch.bfloat16))
+        return FstActivations(layer, x, z, a, y, None, layer.w_in_cat)
+    if masks.w_in.shape != tuple(layer.w_in_cat.shape) or masks.w_out.shape != tuple(layer.w2.shape):
+        raise ShapeError("mask shapes do not match layer weights")
+    ops = masks.plans(layer)
+    E.compress_values(layer.w_in_cat, ops["in"])
+    E.compress_values(layer.w2, ops["out"])
+    st = E.ffn_forward(x, ops["in"], _as_bf16(layer.bias_in_cat), ops["out"], layer.activation.value)
+    return FstActivations(layer, x, st.zt.t(), st.at.t(), st.yt.t(), masks, layer.w_in_cat, st)
+
+
+def fst_backward(bundle: FstActivations, upstream: torch.Tensor, rng_seed: int = 0, mvue: bool = True,
+                 decay_lambda: float = 0.0) -> LayerGrads:
+    """Backward (gated_ffn.py:304-364) with the straight-through weight
+    gradients reported against the dense weights.  `decay_lambda` (extension)
+    fuses masked_decay_gradient (optim.py:105-114) into the dW epilogue."""
+    layer = bundle.layer
+    up = _as_bf16(upstream)
+    if tuple(up.shape) != tuple(bundle.y.shape):
+        raise ShapeError(f"upstream shape {tuple(up.shape)} != output shape {tuple(bundle.y.shape)}")
+    if bundle.masks is None:
+        return _dense_backward(bundle, up)
+    if mvue:
+        raise NotImplementedError(
+            "MVUE-sparsified dW (fst_backward(mvue=True), gated_ffn.py:372-373) is the next kernel (K8) and is "
+            "not built yet; call fst_backward(..., mvue=False) for the dense dW path")
+    ops = bundle.masks.plans(layer)
+    g = E.ffn_backward(bundle.state, up, ops["in"], ops["out"], layer.activation.value,
+                       w_in_dense=layer.w_in_cat, w2_dense=layer.w2, lam=decay_lambda)
+    return _pack_grads(layer, g.dxt.t(), g.dw_in, g.dbias_in, g.dw2)
+
+
+def _pack_grads(layer, dx, dw_in, dbias, dw2) -> LayerGrads:
+    grads = LayerGrads(d_x=dx, d_w2=dw2)
+    if layer.is_gated:
+        r = layer.d_ff
+        grads.d_u, grads.d_v = dw_in[:r], dw_in[r:]
+        grads.d_b, grads.d_c = dbias[:r], dbias[r:]
+    else:
+        grads.d_w1, grads.d_b = dw_in, dbias
+    return grads
+
+
+def _dense_backward(bundle: FstActivations, up: torch.Tensor) -> LayerGrads:
+    layer = bundle.layer
+    with torch.enable_grad():
+        x = bundle.x.detach()
+        w_in = layer.w_in_cat.detach().to(torch.bfloat16).requires_grad_(True)
+        b_in = layer.bias_in_cat.detach().to(torch.bfloat16).requires_grad_(True)
+        w2 = layer.w2.detach().to(torch.bfloat16).requires_grad_(True)
+        xg = x.requires_grad_(True)
+        z = torch.nn.functional.linear(xg, w_in, b_in)
+        y = torch.nn.functional.linear(_dense_act(layer, z), w2)
+        dx, dw_in, db, dw2 = torch.autograd.grad(y, (xg, w_in, b_in, w2), up)
+    return _pack_grads(layer, dx, dw_in.float(), db.float(), dw2.float())
+
+
+def geglu_forward(x, u, v, b, c, traversal: Traversal = Traversal.COL_ORDER) -> torch.Tensor:
+    """gelu(x u^T + b) * (x v^T + c) (gated_ffn.py:208-224): dense GEMM, then the
+    fused gate kernel K6 on the feature-major intermediate.  Returns the
+    column-major (N x d_ff) logical view."""
+    x = _as_bf16(x)
+    w_cat = torch.cat([u, v], 0).to(torch.bfloat16)
+    b_cat = torch.cat([b, c]).to(torch.bfloat16)
+    if x.shape[1] != w_cat.shape[1]:
+        raise ShapeError(f"x cols {x.shape[1]} != weight cols {w_cat.shape[1]}")
+    n, r = x.shape[0], u.shape[0]
+    zt = torch.addmm(b_cat[:, None], w_cat, x.t()).contiguous()  # (2r, N) feature-major
+    at = torch.empty((r, n), dtype=torch.bfloat16, device=x.device)
+    C.call("s24_act_fwd", zt.data_ptr(), n, r, n, C.ACT_GEGLU, at.data_ptr(), n, C.stream_of(zt))
+    return at.t()
+
+
+def geglu_backward(x, u, v, b, c, upstream) -> LayerGrads:
+    """Analytic GEGLU gradients (gated_ffn.py:227-244) via K7 for the gate."""
+    x = _as_bf16(x)
+    up = _as_bf16(upstream)
+    w_cat = torch.cat([u, v], 0).to(torch.bfloat16)
+    b_cat = torch.cat([b, c]).to(torch.bfloat16)
+    n, r = x.shape[0], u.shape[0]
+    if tuple(up.shape) != (n, r):
+        raise ShapeError(f"upstream shape {tuple(up.shape)} != output shape {(n, r)}")
+    zt = torch.addmm(b_cat[:, None], w_cat, x.t()).contiguous()
+    dat = up.t().contiguous()
+    dzt = torch.empty_like(zt)
+    dbias = torch.empty(2 * r, dtype=torch.float32, device=x.device)
+    C.call("s24_act_bwd", zt.data_ptr(), n, dat.data_ptr(), n, r, n, C.ACT_GEGLU, dzt.data_ptr(), n,
+           dbias.data_ptr(), C.stream_of(zt))
+    dx = (dzt.t() @ w_cat)
+    dw = (dzt.float() @ x.float())
+    return LayerGrads(d_x=dx, d_u=dw[:r], d_v=dw[r:], d_b=dbias[:r], d_c=dbias[r:])
+
+
+def search_layer_masks(layer: FFNLayer) -> FFNMasks:
+    """Masks for both weights (trainer.py:212-219) via K1."""
+    return FFNMasks(w_in=transposable_search_conv(layer.w_in_cat), w_out=transposable_search_conv(layer.w2))
+
+
+LAYOUT_OF_OUTPUTS = Layout.COL_MAJOR

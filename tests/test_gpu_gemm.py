@@ -1,0 +1,109 @@
+"""K3/K4 (2:4 sparse tcgen05) and K5 (dense dW + masked decay) GEMMs vs a
+plain fp32 torch reference on the same bf16 operands.
+
+Tolerance: outputs are bf16 (sparse) or fp32 (dW) from fp32 accumulation;
+normwise relative error <= 1e-2 for bf16 outputs and <= 2e-3 for fp32 dW,
+plus an elementwise bound of 3 bf16 ulps of the row scale."""
+import numpy as np
+import pytest
+import torch
+
+from gpu_util import need_gpu, normwise_rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    need_gpu()
+
+
+def _operand(m, k, seed):
+    from paper_2404_01847_b200.engine import CompressedOperand, search_compress
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w = (torch.randn(m, k, generator=g, device="cuda") / k ** 0.5).bfloat16()
+    op = CompressedOperand.empty(m, k, "cuda")
+    search_compress(w, op)
+    from paper_2404_01847_b200 import TransposableMask
+    bits = TransposableMask(op.idx, (m, k)).bits
+    return w, op, bits
+
+
+@pytest.mark.parametrize("m,k,n", [(128, 128, 128), (256, 512, 384), (384, 256, 96), (1024, 1024, 512)])
+@pytest.mark.parametrize("b_mn", [False, True])
+def test_sparse_gemm_fwd_orientation(m, k, n, b_mn):
+    from paper_2404_01847_b200.engine import spmm
+
+    w, op, bits = _operand(m, k, 1 + m + k)
+    x = torch.randn(n, k, device="cuda").bfloat16()
+    b = x.t().contiguous() if b_mn else x
+    bias = torch.randn(m, device="cuda").bfloat16()
+    out = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    spmm(op.fwd_vals, op.fwd_e, m, k, b, b_mn, n, out, bias)
+    ref = (w.float() * bits.float()) @ x.float().t() + bias.float()[:, None]
+    assert normwise_rel(out.float().cpu(), ref.cpu()) < 1e-2
+
+
+@pytest.mark.parametrize("m,k,n", [(128, 256, 128), (512, 384, 256)])
+def test_sparse_gemm_bwd_orientation_and_gelu_epilogue(m, k, n):
+    """W^T operand from the same transposable mask; fused GELU aux output."""
+    from paper_2404_01847_b200.engine import spmm
+
+    w, op, bits = _operand(m, k, 7)
+    dy = torch.randn(n, m, device="cuda").bfloat16()
+    out = torch.empty((k, n), dtype=torch.bfloat16, device="cuda")
+    spmm(op.bwd_vals, op.bwd_e, k, m, dy, False, n, out)
+    ref = (w.float() * bits.float()).t() @ dy.float().t()
+    assert normwise_rel(out.float().cpu(), ref.cpu()) < 1e-2
+    x = torch.randn(n, k, device="cuda").bfloat16()
+    z = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    a = torch.empty_like(z)
+    spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, z, None, gelu_aux=a)
+    zr = (w.float() * bits.float()) @ x.float().t()
+    ar = torch.nn.functional.gelu(zr)
+    assert normwise_rel(z.float().cpu(), zr.cpu()) < 1e-2
+    assert normwise_rel(a.float().cpu(), ar.cpu()) < 1e-2
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("m,n,k", [(128, 128, 64), (256, 512, 320), (384, 256, 1024)])
+def test_dense_dw_gemm(m, n, k, a_mn, b_mn):
+    from paper_2404_01847_b200.engine import gemm_dw
+
+    a = torch.randn(m, k, device="cuda").bfloat16()
+    b = torch.randn(n, k, device="cuda").bfloat16()
+    out = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    gemm_dw(a.t().contiguous() if a_mn else a, a_mn, b.t().contiguous() if b_mn else b, b_mn, m, n, k, out)
+    ref = a.float() @ b.float().t()
+    assert normwise_rel(out.cpu(), ref.cpu()) < 2e-3
+
+
+def test_dense_dw_gemm_masked_decay_epilogue():
+    from paper_2404_01847_b200.engine import gemm_dw
+    from paper_2404_01847_b200 import transposable_search_conv
+
+    m, n, k = 256, 512, 256
+    w = torch.randn(m, n, device="cuda").bfloat16()
+    mask = transposable_search_conv(w)
+    a = torch.randn(m, k, device="cuda").bfloat16()
+    b = torch.randn(k, n, device="cuda").bfloat16()  # MN-major B
+    lam = 0.25
+    out = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    gemm_dw(a, False, b, True, m, n, k, out, w, mask.idx, lam)
+    ref = a.float() @ b.float() + lam * (1 - mask.bits.float()) * w.float()
+    assert normwise_rel(out.cpu(), ref.cpu()) < 2e-3
+    # kept entries carry no decay
+    plain = torch.empty_like(out)
+    gemm_dw(a, False, b, True, m, n, k, plain)
+    kept = mask.bits.bool()
+    assert torch.allclose(out[kept], plain[kept], rtol=0, atol=0)
+
+
+def test_shape_errors():
+    from paper_2404_01847_b200 import ShapeError
+    from paper_2404_01847_b200.engine import CompressedOperand
+
+    with pytest.raises(ShapeError):
+        CompressedOperand.empty(100, 128, "cuda")
