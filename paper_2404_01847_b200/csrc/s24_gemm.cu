@@ -23,6 +23,7 @@
 // accumulators (tmem_full/tmem_empty) so the epilogue of tile i overlaps the
 // main loop of tile i+1.
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "s24_common.cuh"
@@ -51,6 +52,7 @@ struct EpiParams {
 struct GemmShape {
   int m, n, k;  // k logical
   const uint8_t* e;
+  int dbg;  // debug variant bits (S24_GEMM_DEBUG env), 0 in production
 };
 
 __constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
@@ -203,7 +205,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
             const uint32_t accum = (kb | j) != 0 ? 1u : 0u;
             if constexpr (kSparse) {
-              mma_sp_bf16(d_tmem, adesc, bdesc, tmem_base + C::E_COL + j, C::IDESC, accum);
+              // MMA j's metadata sits in TMEM column E_COL + j; the instruction takes a
+              // 2-column-aligned address and selects the column with sparse_id2 (idesc[0:2))
+              const uint32_t e_addr = tmem_base + C::E_COL + (j & ~1);
+              mma_sp_bf16(d_tmem, adesc, bdesc, e_addr, C::IDESC | static_cast<uint32_t>(j & 1), accum);
             } else {
               mma_bf16(d_tmem, adesc, bdesc, C::IDESC, accum);
             }
@@ -417,7 +422,8 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     S24_REQUIRE(ldb >= k, S24_ERR_SHAPE, "ldb < k");
     if (int rc = make_map(&mb, b, k, n, ldb, 64, BN)) return rc;
   }
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), a_e};
+  static const int dbg = getenv("S24_GEMM_DEBUG") ? atoi(getenv("S24_GEMM_DEBUG")) : 0;
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), a_e, dbg};
   EpiParams ep{d, ldd, bias, aux, ldaux, nullptr, 0, nullptr, 0.0f};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (b_mn) {
@@ -459,7 +465,7 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
     S24_REQUIRE(ldb >= k, S24_ERR_SHAPE, "ldb < k");
     if (int rc = make_map(&mb, b, k, n, ldb, 64, BN)) return rc;
   }
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), nullptr};
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), nullptr, 0};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, w, w_dtype, idx, lambda_w};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define S24_DW(AMN, BMN, BNV) return launch_gemm<false, AMN, BMN, BNV, 4, kEpiDw>(ma, mb, shp, ep, st)
