@@ -27,6 +27,21 @@ import torch
 from . import _capi as C
 from .matrix import ShapeError
 
+class _NoTimer:
+    def __call__(self, name):
+        return self
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+# Optional per-launch timer hook (bench.py installs a CUDA-event timer to
+# attribute step time to kernels); the default is a no-op.
+TIMER = _NoTimer()
+
 ACT_CODES = {"relu": C.ACT_RELU, "gelu": C.ACT_GELU, "geglu": C.ACT_GEGLU, "swiglu": C.ACT_SWIGLU}
 GATED = {"geglu", "swiglu"}
 
@@ -59,9 +74,10 @@ class CompressedOperand:
 
 def search_compress(w: torch.Tensor, op: CompressedOperand) -> None:
     """K1 fused: new mask + metadata + kept values (mask refresh step)."""
-    C.call("s24_search_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),
-           op.fwd_vals.data_ptr(), op.fwd_e.data_ptr(), op.bwd_vals.data_ptr(), op.bwd_e.data_ptr(),
-           C.stream_of(w))
+    with TIMER("k1_search_compress"):
+        C.call("s24_search_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),
+               op.fwd_vals.data_ptr(), op.fwd_e.data_ptr(), op.bwd_vals.data_ptr(), op.bwd_e.data_ptr(),
+               C.stream_of(w))
 
 
 def compress_with_meta(w: torch.Tensor, op: CompressedOperand) -> None:
@@ -73,27 +89,31 @@ def compress_with_meta(w: torch.Tensor, op: CompressedOperand) -> None:
 
 def compress_values(w: torch.Tensor, op: CompressedOperand) -> None:
     """K2: per-step prune/compress of the current weight values (mask cached)."""
-    C.call("s24_prune_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),
-           op.fwd_vals.data_ptr(), None, op.bwd_vals.data_ptr(), None, C.stream_of(w))
+    with TIMER("k2_prune_compress"):
+        C.call("s24_prune_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),
+               op.fwd_vals.data_ptr(), None, op.bwd_vals.data_ptr(), None, C.stream_of(w))
 
 
 def spmm(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b_mn: bool, n: int,
-         out: torch.Tensor, bias: torch.Tensor | None = None, gelu_aux: torch.Tensor | None = None) -> None:
+         out: torch.Tensor, bias: torch.Tensor | None = None, gelu_aux: torch.Tensor | None = None,
+         tag: str = "k34_spmm") -> None:
     """out[m, n] (bf16, row-major) = W~[m, k] (2:4) . B[n, k]^T (+ bias[m]); optional aux = gelu(out)."""
     ldb = b.stride(0)
-    C.call("s24_spmm", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), ldb, n,
-           out.data_ptr(), out.stride(0), C.ptr(bias), C.EPI_GELU_AUX if gelu_aux is not None else C.EPI_STORE,
-           C.ptr(gelu_aux), gelu_aux.stride(0) if gelu_aux is not None else 0, C.stream_of(out))
+    with TIMER(tag):
+        C.call("s24_spmm", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), ldb, n,
+               out.data_ptr(), out.stride(0), C.ptr(bias), C.EPI_GELU_AUX if gelu_aux is not None else C.EPI_STORE,
+               C.ptr(gelu_aux), gelu_aux.stride(0) if gelu_aux is not None else 0, C.stream_of(out))
 
 
 def gemm_dw(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, m: int, n: int, k: int,
             out: torch.Tensor, w: torch.Tensor | None = None, idx: torch.Tensor | None = None,
-            lam: float = 0.0) -> None:
+            lam: float = 0.0, tag: str = "k5_gemm_dw") -> None:
     """out[m, n] fp32 = sum_k A[m, k] B[n, k] + lam (1 - M) W  (dense tcgen05)."""
     decay = idx is not None and lam != 0.0
-    C.call("s24_gemm_dw", a.data_ptr(), int(a_mn), a.stride(0), b.data_ptr(), int(b_mn), b.stride(0), m, n, k,
-           out.data_ptr(), out.stride(0), C.ptr(w) if decay else None, C.dtype_code(w) if decay else 0,
-           C.ptr(idx) if decay else None, float(lam if decay else 0.0), C.stream_of(out))
+    with TIMER(tag):
+        C.call("s24_gemm_dw", a.data_ptr(), int(a_mn), a.stride(0), b.data_ptr(), int(b_mn), b.stride(0), m, n,
+               k, out.data_ptr(), out.stride(0), C.ptr(w) if decay else None, C.dtype_code(w) if decay else 0,
+               C.ptr(idx) if decay else None, float(lam if decay else 0.0), C.stream_of(out))
 
 
 def _token_operand(t: torch.Tensor) -> tuple[torch.Tensor, bool]:
@@ -129,12 +149,13 @@ def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor 
     zt = torch.empty((r_in, n), dtype=torch.bfloat16, device=dev)
     at = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
     if act == "gelu":
-        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, zt, bias_in, gelu_aux=at)
+        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, zt, bias_in, gelu_aux=at, tag="k3_spmm_fwd_in")
     else:
-        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, zt, bias_in)
-        C.call("s24_act_fwd", zt.data_ptr(), n, d_ff, n, ACT_CODES[act], at.data_ptr(), n, C.stream_of(zt))
+        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, zt, bias_in, tag="k3_spmm_fwd_in")
+        with TIMER("k6_act_fwd"):
+            C.call("s24_act_fwd", zt.data_ptr(), n, d_ff, n, ACT_CODES[act], at.data_ptr(), n, C.stream_of(zt))
     yt = torch.empty((d, n), dtype=torch.bfloat16, device=dev)
-    spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, at, True, n, yt)
+    spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, at, True, n, yt, tag="k3_spmm_fwd_out")
     return FwdState(x, zt, at, yt)
 
 
@@ -158,20 +179,21 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     dys, dy_mn = _token_operand(dy)
     # dA^T = W2~^T . dY^T   (out_bwd: groups of W2 along d)
     dat = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
-    spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dys, dy_mn, n, dat)
+    spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dys, dy_mn, n, dat, tag="k4_spmm_bwd_out")
     # activation backward + bias gradients
     dzt = torch.empty((r_in, n), dtype=torch.bfloat16, device=dev)
     dbias = torch.empty(r_in, dtype=torch.float32, device=dev)
-    C.call("s24_act_bwd", st.zt.data_ptr(), n, dat.data_ptr(), n, d_ff, n, ACT_CODES[act], dzt.data_ptr(), n,
-           dbias.data_ptr(), C.stream_of(dzt))
+    with TIMER("k7_act_bwd"):
+        C.call("s24_act_bwd", st.zt.data_ptr(), n, dat.data_ptr(), n, d_ff, n, ACT_CODES[act], dzt.data_ptr(), n,
+               dbias.data_ptr(), C.stream_of(dzt))
     # dX^T = W_in~^T . dZ^T  (in_bwd: groups of W_in along r_in)
     dxt = torch.empty((d, n), dtype=torch.bfloat16, device=dev)
-    spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dzt, True, n, dxt)
+    spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dzt, True, n, dxt, tag="k4_spmm_bwd_in")
     # dW2[d, d_ff] = dY^T A : A-op = dY (K = tokens), B-op = A^T (feature-major, K-major)
     dw2 = dw2_out if dw2_out is not None else torch.empty((d, d_ff), dtype=torch.float32, device=dev)
-    gemm_dw(dys, not dy_mn, st.at, False, d, d_ff, n, dw2, w2_dense, w2.idx, lam)
+    gemm_dw(dys, not dy_mn, st.at, False, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")
     # dW_in[r_in, d] = dZ^T X : A-op = dZ^T (K-major), B-op = X (token-major => MN-major)
     xs, x_mn = _token_operand(st.x)
     dw_in = dw_in_out if dw_in_out is not None else torch.empty((r_in, d), dtype=torch.float32, device=dev)
-    gemm_dw(dzt, False, xs, not x_mn, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam)
+    gemm_dw(dzt, False, xs, not x_mn, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam, tag="k5_gemm_dw_in")
     return Grads(dxt, dw_in, dbias, dw2)
