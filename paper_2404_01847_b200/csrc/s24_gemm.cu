@@ -31,8 +31,8 @@
 
 namespace s24 {
 
-constexpr int kBM = 128;
-constexpr int kGemmThreads = 256;
+constexpr int kGemmThreads = 384;  // 4 control warps + 8 epilogue warps
+constexpr int kEpiWarps = 8;
 constexpr int kGroupM = 8;  // M tiles per raster group (L2 reuse of the B panel)
 
 enum Epi : int { kEpiStore = 0, kEpiGeluAux = 1, kEpiDw = 2 };
@@ -51,30 +51,36 @@ struct EpiParams {
 
 struct GemmShape {
   int m, n, k;  // k logical
-  const uint8_t* e;
-  int dbg;  // debug variant bits (S24_GEMM_DEBUG env), 0 in production
 };
 
 __constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
 
-template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages>
+// kCG = CTAs per MMA (1: M = 128, 2: CTA pair, M = 256, B split along N).
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG>
 struct Cfg {
   static constexpr int BK = kSparse ? 128 : 64;  // logical K per stage
   static constexpr int kMmaK = kSparse ? 32 : 16;
   static constexpr int kMmasPerStage = BK / kMmaK;  // 4
-  static constexpr int A_BYTES = kBM * 64 * 2;      // 16 KB either major
-  static constexpr int B_BYTES = kBN * BK * 2;
+  static constexpr int BN_CTA = kBN / kCG;          // B rows held by one CTA
+  static constexpr int B_CHUNKS = (BN_CTA + 63) / 64;  // MN-major 64-wide swizzle chunks
+  static constexpr int A_BYTES = 128 * 64 * 2;         // 16 KB either major
+  static constexpr int B_BOX_BYTES = kBMN ? BK * 128 : BN_CTA * 128;
+  static constexpr int B_BOXES = kBMN ? B_CHUNKS : BK / 64;
+  static constexpr int B_BYTES = B_BOXES * B_BOX_BYTES;
   static constexpr int E_BYTES = kSparse ? 2048 : 0;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + E_BYTES;
+  static constexpr int TX_BYTES = A_BYTES + (kBMN ? B_BYTES : BN_CTA * BK * 2) + E_BYTES;  // per CTA
   static constexpr int ACC_COLS = kBN;
   static constexpr int E_COL = 2 * kBN;
   static constexpr int USED_COLS = 2 * kBN + (kSparse ? 4 : 0);
   static constexpr int TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64 : USED_COLS <= 128 ? 128
                                  : USED_COLS <= 256 ? 256 : 512;
   static constexpr int SMEM_BYTES = kStages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr uint32_t IDESC = make_idesc_bf16(kBM, kBN, kAMN, kBMN, kSparse);
+  static constexpr uint32_t IDESC = make_idesc_bf16(128 * kCG, kBN, kAMN, kBMN, kSparse);
   static_assert(USED_COLS <= 512, "TMEM overflow");
   static_assert(kBN % 32 == 0 && kBN >= 32 && kBN <= 256, "bad BN");
+  static_assert(B_BOX_BYTES % 1024 == 0, "B boxes must stay 1024-byte aligned for the 128B swizzle");
+  static_assert(SMEM_BYTES <= 232448, "shared memory overflow");
 };
 
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
@@ -87,11 +93,11 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
   nb = in_group / gm;
 }
 
-template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kEpi>
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape shp,
-                EpiParams ep) {
-  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages>;
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmE, GemmShape shp, EpiParams ep) {
+  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
@@ -102,14 +108,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_m = shp.m / kBM;
+  const uint32_t rank = kCG == 2 ? cluster_rank() : 0;
+  const int num_m = shp.m / (128 * kCG);
   const int num_n = (shp.n + kBN - 1) / kBN;
   const int num_tiles = num_m * num_n;
   const int num_kb = shp.k / C::BK;
+  const int cluster_id = blockIdx.x / kCG, num_clusters = gridDim.x / kCG;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if constexpr (kSparse) tma_prefetch(&tmE);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -118,48 +127,49 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], kEpiWarps * kCG);
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 2) tmem_alloc_cg<kCG>(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kCG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (every CTA of the pair) =====================
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
-        const int m0 = mb * kBM, n0 = nb * kBN;
+        const int m0 = mb * 128 * kCG + 128 * rank;      // this CTA's A rows
+        const int nb0 = nb * kBN + C::BN_CTA * rank;      // this CTA's B rows (N split)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + C::A_BYTES;
-          mbar_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          if (rank == 0) mbar_expect_tx(&full_bar[stage], C::TX_BYTES * kCG);
           if constexpr (kSparse) {
-            tma_load_2d(sA, &tmA, &full_bar[stage], kb * 64, m0);  // 64 physical = 128 logical
-            uint8_t* sE = sB + C::B_BYTES;
-            bulk_load(sE, shp.e + (static_cast<int64_t>(mb) * (shp.k / 128) + kb) * 2048, 2048, &full_bar[stage]);
+            tma_load<kCG>(sA, &tmA, &full_bar[stage], kb * 64, m0);  // 64 physical = 128 logical
+            tma_load<kCG>(sB + C::B_BYTES, &tmE, &full_bar[stage], 0, (m0 / 128) * (shp.k / 128) + kb);
           } else if constexpr (kAMN) {
-            tma_load_2d(sA, &tmA, &full_bar[stage], m0, kb * 64);
-            tma_load_2d(sA + 8192, &tmA, &full_bar[stage], m0 + 64, kb * 64);
+            tma_load<kCG>(sA, &tmA, &full_bar[stage], m0, kb * 64);
+            tma_load<kCG>(sA + 8192, &tmA, &full_bar[stage], m0 + 64, kb * 64);
           } else {
-            tma_load_2d(sA, &tmA, &full_bar[stage], kb * 64, m0);
+            tma_load<kCG>(sA, &tmA, &full_bar[stage], kb * 64, m0);
           }
           if constexpr (kBMN) {
 #pragma unroll
-            for (int i = 0; i < kBN / 64; ++i)
-              tma_load_2d(sB + i * (C::BK * 128), &tmB, &full_bar[stage], n0 + 64 * i, kb * C::BK);
+            for (int i = 0; i < C::B_CHUNKS; ++i)
+              tma_load<kCG>(sB + i * C::B_BOX_BYTES, &tmB, &full_bar[stage], nb0 + 64 * i, kb * C::BK);
           } else {
 #pragma unroll
             for (int i = 0; i < C::BK / 64; ++i)
-              tma_load_2d(sB + i * (kBN * 128), &tmB, &full_bar[stage], kb * C::BK + 64 * i, n0);
+              tma_load<kCG>(sB + i * C::B_BOX_BYTES, &tmB, &full_bar[stage], kb * C::BK + 64 * i, nb0);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -169,13 +179,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (elect_one()) {
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (rank == 0 && elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
@@ -185,8 +195,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t a_addr = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t b_addr = a_addr + C::A_BYTES;
           if constexpr (kSparse) {
-            // metadata: 128 rows x 16 B (no swizzle, 8-row core matrices 128 B apart)
-            tmem_cp_128x128b(tmem_base + C::E_COL, make_sdesc(b_addr + C::B_BYTES, 2048, 128, 0));
+            // metadata: 128 rows x 16 B (no swizzle, 8-row core matrices 128 B apart) -> 4 TMEM columns
+            tmem_cp_128x128b_cg<kCG>(tmem_base + C::E_COL, make_sdesc(b_addr + C::B_BYTES, 2048, 128, 0));
           }
 #pragma unroll
           for (int j = 0; j < C::kMmasPerStage; ++j) {
@@ -197,9 +207,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               adesc = make_sdesc(a_addr + j * 32, 16, 1024, 2);
             }
             if constexpr (kBMN) {
-              bdesc = make_sdesc(b_addr + j * (C::kMmaK * 128), C::BK * 128, 1024, 2);
+              bdesc = make_sdesc(b_addr + j * (C::kMmaK * 128), C::B_BOX_BYTES, 1024, 2);
             } else if constexpr (kSparse) {
-              bdesc = make_sdesc(b_addr + (j >> 1) * (kBN * 128) + (j & 1) * 64, 16, 1024, 2);
+              bdesc = make_sdesc(b_addr + (j >> 1) * C::B_BOX_BYTES + (j & 1) * 64, 16, 1024, 2);
             } else {
               bdesc = make_sdesc(b_addr + j * 32, 16, 1024, 2);
             }
@@ -207,19 +217,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if constexpr (kSparse) {
               // MMA j's metadata sits in TMEM column E_COL + j; the instruction takes a
               // 2-column-aligned address and selects the column with sparse_id2 (idesc[0:2))
-              const uint32_t e_addr = tmem_base + C::E_COL + (j & ~1);
-              mma_sp_bf16(d_tmem, adesc, bdesc, e_addr, C::IDESC | static_cast<uint32_t>(j & 1), accum);
+              mma_sp_bf16_cg<kCG>(d_tmem, adesc, bdesc, tmem_base + C::E_COL + (j & ~1),
+                                  C::IDESC | static_cast<uint32_t>(j & 1), accum);
             } else {
-              mma_bf16(d_tmem, adesc, bdesc, C::IDESC, accum);
+              mma_bf16_cg<kCG>(d_tmem, adesc, bdesc, C::IDESC, accum);
             }
           }
-          mma_commit(&empty_bar[stage]);
+          mma_commit_cg<kCG>(&empty_bar[stage]);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull_bar[acc]);
+        mma_commit_cg<kCG>(&tfull_bar[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -227,14 +237,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue =====================
-    const int q = warp & 3;  // TMEM lane quarter
+    // ===================== epilogue (8 warps: lane quarter q, column half h) =====================
+    const int q = warp & 3, h = (warp - 4) >> 2;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
-      const int m = mb * kBM + 32 * q + lane;
+      const int m = mb * 128 * kCG + 128 * rank + 32 * q + lane;
       const int n_base = nb * kBN;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -243,7 +253,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (ep.bias != nullptr) bias_v = bf16_to_f32(ep.bias[m]);
       }
 #pragma unroll 1
-      for (int cc = 0; cc < kBN / 32; ++cc) {
+      for (int cc = h; cc < kBN / 32; cc += 2) {
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + 32 * cc, r);
         tmem_ld_wait();
@@ -255,7 +265,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           if (ep.idx != nullptr) {
-            const uint2 ib = *reinterpret_cast<const uint2*>(ep.idx + static_cast<int64_t>(m >> 2) * (shp.n >> 2) + (n0 >> 2));
+            const uint2 ib =
+                *reinterpret_cast<const uint2*>(ep.idx + static_cast<int64_t>(m >> 2) * (shp.n >> 2) + (n0 >> 2));
             const uint32_t iw[2] = {ib.x, ib.y};
             float wv[32];
             if (ep.w_dtype == S24_BF16) {
@@ -266,9 +277,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const uint4 x = __ldg(wp + u);
                 const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                  wv[8 * u + 2 * h] = __uint_as_float(xs[h] << 16);
-                  wv[8 * u + 2 * h + 1] = __uint_as_float(xs[h] & 0xFFFF0000u);
+                for (int t = 0; t < 4; ++t) {
+                  wv[8 * u + 2 * t] = __uint_as_float(xs[t] << 16);
+                  wv[8 * u + 2 * t + 1] = __uint_as_float(xs[t] & 0xFFFF0000u);
                 }
               }
             } else {
@@ -307,7 +318,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if constexpr (kEpi == kEpiGeluAux) {
             float g[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) g[i] = 0.5f * v[i] * (1.0f + erff(v[i] * 0.70710678118654752f));
+            for (int i = 0; i < 32; ++i) g[i] = gelu_fast(v[i]);
             uint4* a4 = reinterpret_cast<uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
@@ -318,7 +329,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (kCG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);
+        else mbar_arrive(&tempty_bar[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -327,9 +341,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kCG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem_base, C::TMEM_COLS);
+  if (warp == 2) tmem_dealloc_cg<kCG>(tmem_base, C::TMEM_COLS);
 }
 
 // ---------------------------------------------------------------------------
@@ -352,52 +367,76 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// 2-D bf16 tensor map: inner (contiguous) extent, outer extent, row pitch in elements.
+// 2-D tensor map: inner (contiguous) extent, outer extent, row pitch in elements.
 static int make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch_elems,
-                    uint32_t box_inner, uint32_t box_outer) {
+                    uint32_t box_inner, uint32_t box_outer, bool u64 = false) {
   EncodeTiledFn enc = get_encode_fn();
   S24_REQUIRE(enc != nullptr, S24_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  S24_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && (pitch_elems * 2) % 16 == 0, S24_ERR_UNSUPPORTED,
+  const int esz = u64 ? 8 : 2;
+  S24_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && (pitch_elems * esz) % 16 == 0, S24_ERR_UNSUPPORTED,
               "TMA operands need 16-byte aligned base and row pitch");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch_elems * 2)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch_elems * esz)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = enc(map, u64 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   u64 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   S24_REQUIRE(r == CUDA_SUCCESS, S24_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
   return S24_OK;
 }
 
 static int num_sms() {
-  int dev = 0, n = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
   return n;
 }
 
-template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kEpi>
-static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& shp, const EpiParams& ep,
-                       cudaStream_t st) {
-  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages>;
-  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kEpi>;
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi>
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& me, const GemmShape& shp,
+                       const EpiParams& ep, cudaStream_t st) {
+  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG>;
+  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi>;
   static bool attr_done = false;  // per template instance
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_done = true;
   }
-  const int tiles = (shp.m / kBM) * ((shp.n + kBN - 1) / kBN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  if (grid <= 0) return S24_OK;
-  kern<<<grid, kGemmThreads, C::SMEM_BYTES, st>>>(ma, mb, shp, ep);
+  const int tiles = (shp.m / (128 * kCG)) * ((shp.n + kBN - 1) / kBN);
+  const int clusters = tiles < num_sms() / kCG ? tiles : num_sms() / kCG;
+  if (clusters <= 0) return S24_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * kCG);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, shp, ep);
+  S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
   return s24_check_launch("gemm");
 }
 
 }  // namespace s24
 
 using namespace s24;
+
+static int cg_override() {
+  static const int v = getenv("S24_GEMM_CG") ? atoi(getenv("S24_GEMM_CG")) : 0;
+  return v;
+}
 
 extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b,
                         int b_mn, int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias,
@@ -412,26 +451,39 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   if (epilogue == S24_EPI_GELU_AUX)
     S24_REQUIRE(aux != nullptr && ldaux >= n && ldaux % 8 == 0, S24_ERR_ARG, "GELU epilogue needs aux output");
   S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
-  CUtensorMap ma, mb;
+  const bool pair = (m % 256 == 0) && cg_override() != 1;
+  constexpr int BN1 = 128, BN2 = 224;
+  CUtensorMap ma, mb, me;
   if (int rc = make_map(&ma, a_vals, k / 2, m, k / 2, 64, 128)) return rc;
-  constexpr int BN = 128;
+  if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, true)) return rc;
+  const int bn_cta = pair ? BN2 / 2 : BN1;
   if (b_mn) {
     S24_REQUIRE(ldb >= n, S24_ERR_SHAPE, "ldb < n");
     if (int rc = make_map(&mb, b, n, k, ldb, 64, 128)) return rc;
   } else {
     S24_REQUIRE(ldb >= k, S24_ERR_SHAPE, "ldb < k");
-    if (int rc = make_map(&mb, b, k, n, ldb, 64, BN)) return rc;
+    if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
-  static const int dbg = getenv("S24_GEMM_DEBUG") ? atoi(getenv("S24_GEMM_DEBUG")) : 0;
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), a_e, dbg};
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k)};
   EpiParams ep{d, ldd, bias, aux, ldaux, nullptr, 0, nullptr, 0.0f};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (b_mn) {
-    if (epilogue == S24_EPI_STORE) return launch_gemm<true, false, true, BN, 4, kEpiStore>(ma, mb, shp, ep, st);
-    return launch_gemm<true, false, true, BN, 4, kEpiGeluAux>(ma, mb, shp, ep, st);
+  const bool gelu = epilogue == S24_EPI_GELU_AUX;
+#define S24_SP(BMN, BNV, CG, EPI) return launch_gemm<true, false, BMN, BNV, 4, CG, EPI>(ma, mb, me, shp, ep, st)
+  if (pair) {
+    if (b_mn) {
+      if (gelu) S24_SP(true, BN2, 2, kEpiGeluAux);
+      S24_SP(true, BN2, 2, kEpiStore);
+    }
+    if (gelu) S24_SP(false, BN2, 2, kEpiGeluAux);
+    S24_SP(false, BN2, 2, kEpiStore);
   }
-  if (epilogue == S24_EPI_STORE) return launch_gemm<true, false, false, BN, 4, kEpiStore>(ma, mb, shp, ep, st);
-  return launch_gemm<true, false, false, BN, 4, kEpiGeluAux>(ma, mb, shp, ep, st);
+  if (b_mn) {
+    if (gelu) S24_SP(true, BN1, 1, kEpiGeluAux);
+    S24_SP(true, BN1, 1, kEpiStore);
+  }
+  if (gelu) S24_SP(false, BN1, 1, kEpiGeluAux);
+  S24_SP(false, BN1, 1, kEpiStore);
+#undef S24_SP
 }
 
 extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int b_mn, int64_t ldb,
@@ -448,7 +500,11 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
                 "masked decay needs bf16 or fp32 weights");
   }
   S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
-  CUtensorMap ma, mb;
+  const bool wide = n % 256 == 0;
+  const bool pair = wide && m % 256 == 0 && cg_override() != 1;
+  const int BN = wide ? 256 : 128;
+  const int bn_cta = pair ? BN / 2 : BN;
+  CUtensorMap ma, mb, me;
   if (a_mn) {
     S24_REQUIRE(lda >= m, S24_ERR_SHAPE, "lda < m");
     if (int rc = make_map(&ma, a, m, k, lda, 64, 64)) return rc;
@@ -456,28 +512,34 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
     S24_REQUIRE(lda >= k, S24_ERR_SHAPE, "lda < k");
     if (int rc = make_map(&ma, a, k, m, lda, 64, 128)) return rc;
   }
-  const bool wide = n % 256 == 0;
-  const int BN = wide ? 256 : 128;
   if (b_mn) {
     S24_REQUIRE(ldb >= n, S24_ERR_SHAPE, "ldb < n");
     if (int rc = make_map(&mb, b, n, k, ldb, 64, 64)) return rc;
   } else {
     S24_REQUIRE(ldb >= k, S24_ERR_SHAPE, "ldb < k");
-    if (int rc = make_map(&mb, b, k, n, ldb, 64, BN)) return rc;
+    if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), nullptr, 0};
+  me = mb;  // unused by the dense kernels
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k)};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, w, w_dtype, idx, lambda_w};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define S24_DW(AMN, BMN, BNV) return launch_gemm<false, AMN, BMN, BNV, 4, kEpiDw>(ma, mb, shp, ep, st)
-  if (wide) {
-    if (a_mn && b_mn) S24_DW(true, true, 256);
-    if (a_mn) S24_DW(true, false, 256);
-    if (b_mn) S24_DW(false, true, 256);
-    S24_DW(false, false, 256);
+#define S24_DW(AMN, BMN, BNV, CG) \
+  return launch_gemm<false, AMN, BMN, BNV, (CG == 2 ? 6 : 4), CG, kEpiDw>(ma, mb, me, shp, ep, st)
+  if (pair) {
+    if (a_mn && b_mn) S24_DW(true, true, 256, 2);
+    if (a_mn) S24_DW(true, false, 256, 2);
+    if (b_mn) S24_DW(false, true, 256, 2);
+    S24_DW(false, false, 256, 2);
   }
-  if (a_mn && b_mn) S24_DW(true, true, 128);
-  if (a_mn) S24_DW(true, false, 128);
-  if (b_mn) S24_DW(false, true, 128);
-  S24_DW(false, false, 128);
+  if (wide) {
+    if (a_mn && b_mn) S24_DW(true, true, 256, 1);
+    if (a_mn) S24_DW(true, false, 256, 1);
+    if (b_mn) S24_DW(false, true, 256, 1);
+    S24_DW(false, false, 256, 1);
+  }
+  if (a_mn && b_mn) S24_DW(true, true, 128, 1);
+  if (a_mn) S24_DW(true, false, 128, 1);
+  if (b_mn) S24_DW(false, true, 128, 1);
+  S24_DW(false, false, 128, 1);
 #undef S24_DW
 }
