@@ -56,6 +56,13 @@ struct GemmShape {
 __constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
 
 // kCG = CTAs per MMA (1: M = 128, 2: CTA pair, M = 256, B split along N).
+// Pipeline depth that fits next to the epilogue staging area.
+template <int kStageBytes>
+constexpr int stages_for() {
+  constexpr int budget = 232448 - 1024 - 256 - kEpiWarps * 4096;
+  return budget / kStageBytes > 6 ? 6 : budget / kStageBytes;
+}
+
 template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG>
 struct Cfg {
   static constexpr int BK = kSparse ? 128 : 64;  // logical K per stage
@@ -75,7 +82,9 @@ struct Cfg {
   static constexpr int USED_COLS = 2 * kBN + (kSparse ? 4 : 0);
   static constexpr int TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64 : USED_COLS <= 128 ? 128
                                  : USED_COLS <= 256 ? 256 : 512;
-  static constexpr int SMEM_BYTES = kStages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_OFF = kStages * STAGE_BYTES;          // per-warp 4 KB output staging
+  static constexpr int BAR_OFF = EPI_OFF + kEpiWarps * 4096;
+  static constexpr int SMEM_BYTES = BAR_OFF + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t IDESC = make_idesc_bf16(128 * kCG, kBN, kAMN, kBMN, kSparse);
   static_assert(USED_COLS <= 512, "TMEM overflow");
   static_assert(kBN % 32 == 0 && kBN >= 32 && kBN <= 256, "bad BN");
@@ -96,12 +105,13 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
 template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmE, GemmShape shp, EpiParams ep) {
+                const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmD,
+                const __grid_constant__ CUtensorMap tmX, GemmShape shp, EpiParams ep) {
   using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * C::STAGE_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -118,7 +128,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    tma_prefetch(&tmD);
     if constexpr (kSparse) tma_prefetch(&tmE);
+    if constexpr (kEpi == kEpiGeluAux) tma_prefetch(&tmX);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -238,13 +250,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== epilogue (8 warps: lane quarter q, column half h) =====================
+    // TMEM -> registers -> (bias / GELU / masked decay) -> swizzled smem staging -> TMA store
+    // (full-line writes; the staging buffer is recycled once the bulk store has read it).
     const int q = warp & 3, h = (warp - 4) >> 2;
-    int acc = 0;
+    uint8_t* stg = smem + C::EPI_OFF + (warp - 4) * 4096;
+    int acc = 0, sbuf = 0;
     uint32_t acc_phase = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
-      const int m = mb * 128 * kCG + 128 * rank + 32 * q + lane;
+      const int m_w = mb * 128 * kCG + 128 * rank + 32 * q;  // first row of this warp
+      const int m = m_w + lane;
       const int n_base = nb * kBN;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -259,11 +275,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tmem_ld_wait();
         const int n0 = n_base + 32 * cc;
         if (n0 >= shp.n) continue;
-        if constexpr (kEpi == kEpiDw) {
-          float* out = static_cast<float*>(ep.d) + static_cast<int64_t>(m) * ep.ldd + n0;
-          float v[32];
+        float v[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if constexpr (kEpi == kEpiDw) {
           if (ep.idx != nullptr) {
             const uint2 ib =
                 *reinterpret_cast<const uint2*>(ep.idx + static_cast<int64_t>(m >> 2) * (shp.n >> 2) + (n0 >> 2));
@@ -303,28 +318,54 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (!((rowmask >> c) & 1)) v[4 * blk + c] += ep.lam * wv[4 * blk + c];
             }
           }
-          float4* o4 = reinterpret_cast<float4*>(out);
+          // fp32 32x32 tile, 128B swizzle: 16-byte chunk c of row `lane` -> chunk c ^ (lane & 7)
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
 #pragma unroll
-          for (int u = 0; u < 8; ++u) o4[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-        } else {
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) + bias_v;
-          uint4* o4 = reinterpret_cast<uint4*>(static_cast<uint16_t*>(ep.d) + static_cast<int64_t>(m) * ep.ldd + n0);
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            o4[u] = make_uint4(pack_bf16x2(v[8 * u], v[8 * u + 1]), pack_bf16x2(v[8 * u + 2], v[8 * u + 3]),
-                               pack_bf16x2(v[8 * u + 4], v[8 * u + 5]), pack_bf16x2(v[8 * u + 6], v[8 * u + 7]));
-          if constexpr (kEpi == kEpiGeluAux) {
-            float g[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) g[i] = gelu_fast(v[i]);
-            uint4* a4 = reinterpret_cast<uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0);
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              a4[u] = make_uint4(pack_bf16x2(g[8 * u], g[8 * u + 1]), pack_bf16x2(g[8 * u + 2], g[8 * u + 3]),
-                                 pack_bf16x2(g[8 * u + 4], g[8 * u + 5]), pack_bf16x2(g[8 * u + 6], g[8 * u + 7]));
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmD, stg, n0, m_w);
+            bulk_commit();
           }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += bias_v;
+          // bf16 32x32 tile, 64B swizzle: chunk c of row `lane` -> chunk c ^ ((lane >> 1) & 3)
+          uint8_t* zb = stg + (kEpi == kEpiGeluAux ? 0 : sbuf * 2048);
+          if (lane == 0) {
+            if constexpr (kEpi == kEpiGeluAux) bulk_wait_read0();
+            else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          }
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4*>(zb + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+                make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
+                           pack_bf16x2(v[8 * c + 4], v[8 * c + 5]), pack_bf16x2(v[8 * c + 6], v[8 * c + 7]));
+          if constexpr (kEpi == kEpiGeluAux) {
+            uint8_t* ab = stg + 2048;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              float g[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) g[i] = gelu_fast(v[8 * c + i]);
+              *reinterpret_cast<uint4*>(ab + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]), pack_bf16x2(g[4], g[5]),
+                             pack_bf16x2(g[6], g[7]));
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmD, zb, n0, m_w);
+            if constexpr (kEpi == kEpiGeluAux) tma_store_2d(&tmX, stg + 2048, n0, m_w);
+            bulk_commit();
+          }
+          sbuf ^= 1;
         }
       }
       tc_fence_before();
@@ -338,6 +379,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait0();
   }
 
   tc_fence_before();
@@ -367,22 +409,28 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
+enum MapKind { kMapBf16Sw128 = 0, kMapBf16Sw64 = 1, kMapF32Sw128 = 2, kMapU64 = 3 };
+
 // 2-D tensor map: inner (contiguous) extent, outer extent, row pitch in elements.
 static int make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch_elems,
-                    uint32_t box_inner, uint32_t box_outer, bool u64 = false) {
+                    uint32_t box_inner, uint32_t box_outer, MapKind kind = kMapBf16Sw128) {
   EncodeTiledFn enc = get_encode_fn();
   S24_REQUIRE(enc != nullptr, S24_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const int esz = u64 ? 8 : 2;
+  const int esz = kind == kMapU64 ? 8 : kind == kMapF32Sw128 ? 4 : 2;
   S24_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && (pitch_elems * esz) % 16 == 0, S24_ERR_UNSUPPORTED,
               "TMA operands need 16-byte aligned base and row pitch");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch_elems * esz)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, u64 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   u64 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapDataType dt = kind == kMapU64 ? CU_TENSOR_MAP_DATA_TYPE_UINT64
+                                 : kind == kMapF32Sw128 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                        : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const CUtensorMapSwizzle sw = kind == kMapU64 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                : kind == kMapBf16Sw64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                       : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   S24_REQUIRE(r == CUDA_SUCCESS, S24_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
   return S24_OK;
 }
@@ -399,8 +447,8 @@ static int num_sms() {
 }
 
 template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi>
-static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& me, const GemmShape& shp,
-                       const EpiParams& ep, cudaStream_t st) {
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& me, const CUtensorMap& md,
+                       const CUtensorMap& mx, const GemmShape& shp, const EpiParams& ep, cudaStream_t st) {
   using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG>;
   auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi>;
   static bool attr_done = false;  // per template instance
@@ -424,7 +472,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, shp, ep);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, md, mx, shp, ep);
   S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
   return s24_check_launch("gemm");
 }
@@ -455,7 +503,14 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   constexpr int BN1 = 128, BN2 = 224;
   CUtensorMap ma, mb, me;
   if (int rc = make_map(&ma, a_vals, k / 2, m, k / 2, 64, 128)) return rc;
-  if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, true)) return rc;
+  if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, kMapU64)) return rc;
+  CUtensorMap md, mx;
+  if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapBf16Sw64)) return rc;
+  if (epilogue == S24_EPI_GELU_AUX) {
+    if (int rc = make_map(&mx, aux, n, m, ldaux, 32, 32, kMapBf16Sw64)) return rc;
+  } else {
+    mx = md;
+  }
   const int bn_cta = pair ? BN2 / 2 : BN1;
   if (b_mn) {
     S24_REQUIRE(ldb >= n, S24_ERR_SHAPE, "ldb < n");
@@ -468,7 +523,10 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   EpiParams ep{d, ldd, bias, aux, ldaux, nullptr, 0, nullptr, 0.0f};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool gelu = epilogue == S24_EPI_GELU_AUX;
-#define S24_SP(BMN, BNV, CG, EPI) return launch_gemm<true, false, BMN, BNV, 4, CG, EPI>(ma, mb, me, shp, ep, st)
+#define S24_SP(BMN, BNV, CG, EPI)                                                                       \
+  return launch_gemm<true, false, BMN, BNV,                                                              \
+                     stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, EPI>(ma, mb, me, md, mx, \
+                                                                                             shp, ep, st)
   if (pair) {
     if (b_mn) {
       if (gelu) S24_SP(true, BN2, 2, kEpiGeluAux);
@@ -520,11 +578,14 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
     if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
   me = mb;  // unused by the dense kernels
+  CUtensorMap md;
+  if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapF32Sw128)) return rc;
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k)};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, w, w_dtype, idx, lambda_w};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define S24_DW(AMN, BMN, BNV, CG) \
-  return launch_gemm<false, AMN, BMN, BNV, (CG == 2 ? 6 : 4), CG, kEpiDw>(ma, mb, me, shp, ep, st)
+#define S24_DW(AMN, BMN, BNV, CG)                                                                      \
+  return launch_gemm<false, AMN, BMN, BNV, stages_for<Cfg<false, AMN, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
+                     kEpiDw>(ma, mb, me, md, md, shp, ep, st)
   if (pair) {
     if (a_mn && b_mn) S24_DW(true, true, 256, 2);
     if (a_mn) S24_DW(true, false, 256, 2);
