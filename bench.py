@@ -238,8 +238,8 @@ class SparseStep:
         self.dbias = self.bucket[n_in:n_in + n_b]
         self.dw2 = self.bucket[n_in + n_b:].view(w2.shape)
         self.t = 0
-        # our kernel launches per step: K1 or K2 x2, fwd 2 (GELU fused) or 3, bwd 5
-        self.launches_per_step = 2 + (2 if act == "gelu" else 3) + 5
+        # our kernel launches per step: K1 or K2 x2, fwd 2 (GELU fused) or 3, bwd 4 (GELU' fused) or 5
+        self.launches_per_step = 2 + (2 if act == "gelu" else 3) + (4 if act == "gelu" else 5)
 
     def __call__(self, x, dy):
         E = self.E
@@ -249,7 +249,7 @@ class SparseStep:
         else:
             E.compress_values(self.w_in, self.op_in)
             E.compress_values(self.w2, self.op_out)
-        st = E.ffn_forward(x, self.op_in, self.bias, self.op_out, self.act)
+        st = E.ffn_forward(x, self.op_in, self.bias, self.op_out, self.act, fused=True)
         g = E.ffn_backward(st, dy, self.op_in, self.op_out, self.act, w_in_dense=self.w_in, w2_dense=self.w2,
                            lam=LAMBDA / self.world, dw_in_out=self.dw_in, dw2_out=self.dw2)
         self.dbias.copy_(g.dbias_in)

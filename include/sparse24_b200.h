@@ -67,8 +67,11 @@ extern "C" {
 #define S24_ACT_SWIGLU 3
 
 /* sparse GEMM epilogues */
-#define S24_EPI_STORE 0      /* D = acc (+ bias[m])                        */
-#define S24_EPI_GELU_AUX 1   /* D = acc + bias[m]; AUX = gelu(D)  (fwd GEMM1) */
+#define S24_EPI_STORE 0      /* D = acc (+ bias[m])                                        */
+#define S24_EPI_GELU_AUX 1   /* D = z = acc + bias[m]; AUX = gelu(z)          (API fwd GEMM1)  */
+#define S24_EPI_GELU_GRAD 2  /* D = gelu(z); AUX = gelu'(z), z = acc + bias[m] (train fwd GEMM1) */
+#define S24_EPI_DGELU 3      /* D = acc * AUX (AUX = gelu'(z) input); dbias[m] += sum_n D[m, n]
+                                (train bwd GEMM3: activation backward + bias gradient fused)    */
 
 const char* s24_last_error_string(void);
 int s24_abi_version(void);
@@ -117,10 +120,11 @@ int s24_e_to_flat(const uint8_t* e, int64_t m, int64_t k, uint8_t* meta, void* s
  * _GatherPlan.product for in_fwd / out_fwd / out_bwd / in_bwd
  * (gated_ffn.py:294, :297, :329, :352).  B: b_mn = 0 -> stored n x k (ldb >= k),
  * b_mn = 1 -> stored k x n (ldb >= n).  D bf16 m x n (ldd).  bias (bf16, m) may be
- * NULL.  m % 128 == 0, k % 128 == 0, n % 32 == 0. */
+ * NULL.  dbias (fp32, m, zeroed by the caller) is used by S24_EPI_DGELU only.
+ * m % 128 == 0, k % 128 == 0, n % 32 == 0. */
 int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b, int b_mn,
              int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias, int epilogue, uint16_t* aux,
-             int64_t ldaux, void* stream);
+             int64_t ldaux, float* dbias, void* stream);
 
 /* ---- K5: dense tcgen05 dW GEMM with fused masked decay ---------------------
  * D[m, n] (fp32, ldd) = sum_k A[m, k] B[n, k] + lambda_w * (1 - M[m, n]) * W[m, n]

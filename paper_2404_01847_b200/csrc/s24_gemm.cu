@@ -35,14 +35,17 @@ constexpr int kGemmThreads = 384;  // 4 control warps + 8 epilogue warps
 constexpr int kEpiWarps = 8;
 constexpr int kGroupM = 8;  // M tiles per raster group (L2 reuse of the B panel)
 
-enum Epi : int { kEpiStore = 0, kEpiGeluAux = 1, kEpiDw = 2 };
+// epilogues: plain store (+bias); Z and GELU(Z); GELU(Z) and GELU'(Z) (training forward);
+// dZ = acc * GELU'(Z) with bias-gradient row sums (training backward); dW fp32 + masked decay
+enum Epi : int { kEpiStore = 0, kEpiGeluAux = 1, kEpiDw = 2, kEpiGeluGrad = 3, kEpiDAct = 4 };
 
 struct EpiParams {
   void* d;
   int64_t ldd;
   const uint16_t* bias;
-  uint16_t* aux;
+  uint16_t* aux;     // second output (kEpiGeluAux, kEpiGeluGrad) or GELU'(Z) input (kEpiDAct)
   int64_t ldaux;
+  float* dbias;      // kEpiDAct: bias-gradient accumulator (zeroed by the caller)
   const void* w;
   int w_dtype;
   const uint8_t* idx;
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch(&tmB);
     tma_prefetch(&tmD);
     if constexpr (kSparse) tma_prefetch(&tmE);
-    if constexpr (kEpi == kEpiGeluAux) tma_prefetch(&tmX);
+    if constexpr (kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad) tma_prefetch(&tmX);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -264,8 +267,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int n_base = nb * kBN;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      float bias_v = 0.0f;
-      if constexpr (kEpi != kEpiDw) {
+      float bias_v = 0.0f;  // bias (forward epilogues) or running bias-gradient partial (kEpiDAct)
+      if constexpr (kEpi == kEpiStore || kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad) {
         if (ep.bias != nullptr) bias_v = bf16_to_f32(ep.bias[m]);
       }
 #pragma unroll 1
@@ -332,20 +335,63 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             bulk_commit();
           }
         } else {
+          constexpr bool kTwo = kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad;  // two bf16 outputs
+          if constexpr (kEpi == kEpiDAct) {
+            // dZ = dA * GELU'(Z): GELU'(Z) tile row from global (feature-major, bf16)
+            const uint4* gp = reinterpret_cast<const uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0);
+            float rs = 0.0f;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += bias_v;
+            for (int u = 0; u < 4; ++u) {
+              const uint4 x = __ldg(gp + u);
+              const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                v[8 * u + 2 * t] *= __uint_as_float(xs[t] << 16);
+                v[8 * u + 2 * t + 1] *= __uint_as_float(xs[t] & 0xFFFF0000u);
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) rs += v[i];
+            bias_v += rs;  // running bias-gradient partial of row m over this tile's chunks
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += bias_v;
+          }
           // bf16 32x32 tile, 64B swizzle: chunk c of row `lane` -> chunk c ^ ((lane >> 1) & 3)
-          uint8_t* zb = stg + (kEpi == kEpiGeluAux ? 0 : sbuf * 2048);
+          uint8_t* zb = stg + (kTwo ? 0 : sbuf * 2048);
           if (lane == 0) {
-            if constexpr (kEpi == kEpiGeluAux) bulk_wait_read0();
+            if constexpr (kTwo) bulk_wait_read0();
             else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           }
           __syncwarp();
+          if constexpr (kEpi == kEpiGeluGrad) {
+            // D = GELU(z), AUX = GELU'(z): one erf + one exp shared by both
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            *reinterpret_cast<uint4*>(zb + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
-                make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
-                           pack_bf16x2(v[8 * c + 4], v[8 * c + 5]), pack_bf16x2(v[8 * c + 6], v[8 * c + 7]));
+            for (int c = 0; c < 4; ++c) {
+              float g[8], gd[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float x = v[8 * c + i];
+                float e;
+                const float ef = erf_fast(x * 0.70710678118654752f, e);
+                const float cdf = 0.5f * (1.0f + ef);
+                g[i] = x * cdf;
+                gd[i] = fmaf(x * 0.39894228040143268f, e, cdf);
+              }
+              *reinterpret_cast<uint4*>(zb + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]), pack_bf16x2(g[4], g[5]),
+                             pack_bf16x2(g[6], g[7]));
+              *reinterpret_cast<uint4*>(stg + 2048 + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(pack_bf16x2(gd[0], gd[1]), pack_bf16x2(gd[2], gd[3]), pack_bf16x2(gd[4], gd[5]),
+                             pack_bf16x2(gd[6], gd[7]));
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              *reinterpret_cast<uint4*>(zb + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
+                             pack_bf16x2(v[8 * c + 4], v[8 * c + 5]), pack_bf16x2(v[8 * c + 6], v[8 * c + 7]));
+          }
           if constexpr (kEpi == kEpiGeluAux) {
             uint8_t* ab = stg + 2048;
 #pragma unroll
@@ -362,11 +408,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           __syncwarp();
           if (lane == 0) {
             tma_store_2d(&tmD, zb, n0, m_w);
-            if constexpr (kEpi == kEpiGeluAux) tma_store_2d(&tmX, stg + 2048, n0, m_w);
+            if constexpr (kTwo) tma_store_2d(&tmX, stg + 2048, n0, m_w);
             bulk_commit();
           }
           sbuf ^= 1;
         }
+      }
+      if constexpr (kEpi == kEpiDAct) {
+        if (ep.dbias != nullptr) atomicAdd(ep.dbias + m, bias_v);
       }
       tc_fence_before();
       __syncwarp();
@@ -488,16 +537,17 @@ static int cg_override() {
 
 extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b,
                         int b_mn, int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias,
-                        int epilogue, uint16_t* aux, int64_t ldaux, void* stream) {
+                        int epilogue, uint16_t* aux, int64_t ldaux, float* dbias, void* stream) {
   S24_REQUIRE(a_vals && a_e && b && d, S24_ERR_ARG, "NULL operand");
   S24_REQUIRE(m % 128 == 0 && k % 128 == 0 && n % 32 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
               "sparse GEMM needs m %% 128 == 0, k %% 128 == 0, n %% 32 == 0 (got m=%lld k=%lld n=%lld)",
               (long long)m, (long long)k, (long long)n);
   S24_REQUIRE(ldd >= n && ldd % 8 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0, S24_ERR_UNSUPPORTED,
               "output rows must be 16-byte aligned");
-  S24_REQUIRE(epilogue == S24_EPI_STORE || epilogue == S24_EPI_GELU_AUX, S24_ERR_ARG, "bad epilogue");
-  if (epilogue == S24_EPI_GELU_AUX)
-    S24_REQUIRE(aux != nullptr && ldaux >= n && ldaux % 8 == 0, S24_ERR_ARG, "GELU epilogue needs aux output");
+  S24_REQUIRE(epilogue >= S24_EPI_STORE && epilogue <= S24_EPI_DGELU, S24_ERR_ARG, "bad epilogue");
+  if (epilogue != S24_EPI_STORE)
+    S24_REQUIRE(aux != nullptr && ldaux >= n && ldaux % 8 == 0 && (reinterpret_cast<uintptr_t>(aux) & 15) == 0,
+                S24_ERR_ARG, "this epilogue needs a 16-byte aligned aux tensor");
   S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
   const bool pair = (m % 256 == 0) && cg_override() != 1;
   constexpr int BN1 = 128, BN2 = 224;
@@ -506,7 +556,7 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, kMapU64)) return rc;
   CUtensorMap md, mx;
   if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapBf16Sw64)) return rc;
-  if (epilogue == S24_EPI_GELU_AUX) {
+  if (epilogue == S24_EPI_GELU_AUX || epilogue == S24_EPI_GELU_GRAD) {
     if (int rc = make_map(&mx, aux, n, m, ldaux, 32, 32, kMapBf16Sw64)) return rc;
   } else {
     mx = md;
@@ -520,27 +570,26 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k)};
-  EpiParams ep{d, ldd, bias, aux, ldaux, nullptr, 0, nullptr, 0.0f};
+  EpiParams ep{d, ldd, bias, aux, ldaux, dbias, nullptr, 0, nullptr, 0.0f};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool gelu = epilogue == S24_EPI_GELU_AUX;
 #define S24_SP(BMN, BNV, CG, EPI)                                                                       \
   return launch_gemm<true, false, BMN, BNV,                                                              \
                      stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, EPI>(ma, mb, me, md, mx, \
                                                                                              shp, ep, st)
+#define S24_SP_EPI(BMN, BNV, CG)                                              \
+  switch (epilogue) {                                                           \
+    case S24_EPI_GELU_AUX: S24_SP(BMN, BNV, CG, kEpiGeluAux);                   \
+    case S24_EPI_GELU_GRAD: S24_SP(BMN, BNV, CG, kEpiGeluGrad);                 \
+    case S24_EPI_DGELU: S24_SP(BMN, BNV, CG, kEpiDAct);                         \
+    default: S24_SP(BMN, BNV, CG, kEpiStore);                                   \
+  }
   if (pair) {
-    if (b_mn) {
-      if (gelu) S24_SP(true, BN2, 2, kEpiGeluAux);
-      S24_SP(true, BN2, 2, kEpiStore);
-    }
-    if (gelu) S24_SP(false, BN2, 2, kEpiGeluAux);
-    S24_SP(false, BN2, 2, kEpiStore);
+    if (b_mn) S24_SP_EPI(true, BN2, 2);
+    S24_SP_EPI(false, BN2, 2);
   }
-  if (b_mn) {
-    if (gelu) S24_SP(true, BN1, 1, kEpiGeluAux);
-    S24_SP(true, BN1, 1, kEpiStore);
-  }
-  if (gelu) S24_SP(false, BN1, 1, kEpiGeluAux);
-  S24_SP(false, BN1, 1, kEpiStore);
+  if (b_mn) S24_SP_EPI(true, BN1, 1);
+  S24_SP_EPI(false, BN1, 1);
+#undef S24_SP_EPI
 #undef S24_SP
 }
 
@@ -581,7 +630,7 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   CUtensorMap md;
   if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapF32Sw128)) return rc;
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k)};
-  EpiParams ep{d, ldd, nullptr, nullptr, 0, w, w_dtype, idx, lambda_w};
+  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, w, w_dtype, idx, lambda_w};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define S24_DW(AMN, BMN, BNV, CG)                                                                      \
   return launch_gemm<false, AMN, BMN, BNV, stages_for<Cfg<false, AMN, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \

@@ -96,13 +96,19 @@ def compress_values(w: torch.Tensor, op: CompressedOperand) -> None:
 
 def spmm(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b_mn: bool, n: int,
          out: torch.Tensor, bias: torch.Tensor | None = None, gelu_aux: torch.Tensor | None = None,
-         tag: str = "k34_spmm") -> None:
-    """out[m, n] (bf16, row-major) = W~[m, k] (2:4) . B[n, k]^T (+ bias[m]); optional aux = gelu(out)."""
-    ldb = b.stride(0)
+         tag: str = "k34_spmm", epi: int | None = None, aux: torch.Tensor | None = None,
+         dbias: torch.Tensor | None = None) -> None:
+    """out[m, n] (bf16, row-major) = W~[m, k] (2:4) . B[n, k]^T with an epilogue:
+    EPI_STORE (+bias), EPI_GELU_AUX (out = z, gelu_aux = gelu(z)), EPI_GELU_GRAD
+    (out = gelu(z), aux = gelu'(z)), EPI_DGELU (out = acc * aux, dbias += row sums)."""
+    if epi is None:
+        epi = C.EPI_GELU_AUX if gelu_aux is not None else C.EPI_STORE
+    if gelu_aux is not None:
+        aux = gelu_aux
     with TIMER(tag):
-        C.call("s24_spmm", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), ldb, n,
-               out.data_ptr(), out.stride(0), C.ptr(bias), C.EPI_GELU_AUX if gelu_aux is not None else C.EPI_STORE,
-               C.ptr(gelu_aux), gelu_aux.stride(0) if gelu_aux is not None else 0, C.stream_of(out))
+        C.call("s24_spmm", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), b.stride(0), n,
+               out.data_ptr(), out.stride(0), C.ptr(bias), epi, C.ptr(aux), aux.stride(0) if aux is not None else 0,
+               C.ptr(dbias), C.stream_of(out))
 
 
 def gemm_dw(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, m: int, n: int, k: int,
@@ -130,13 +136,17 @@ def _token_operand(t: torch.Tensor) -> tuple[torch.Tensor, bool]:
 @dataclass
 class FwdState:
     x: torch.Tensor  # (N, d) as given (bf16)
-    zt: torch.Tensor  # (r_in, N)
+    zt: torch.Tensor | None  # (r_in, N) pre-activation (None on the fused training path)
     at: torch.Tensor  # (d_ff, N)
     yt: torch.Tensor  # (d, N)
+    gt: torch.Tensor | None = None  # (d_ff, N) GELU'(z), fused training path only
 
 
 def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor | None, w2: CompressedOperand,
-                act: str) -> FwdState:
+                act: str, fused: bool = False) -> FwdState:
+    """fused=True (GELU only): GEMM1's epilogue stores A = GELU(z) and
+    G = GELU'(z) instead of z, so the backward's GEMM3 epilogue applies the
+    activation derivative and reduces the bias gradient (no separate K7)."""
     n, d = x.shape
     r_in = w_in.rows
     d_ff = w2.cols
@@ -146,8 +156,15 @@ def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor 
         raise ShapeError(f"token count must be a multiple of 64 on the tensor-core path, got {n}")
     dev = x.device
     xs, x_mn = _token_operand(x)
-    zt = torch.empty((r_in, n), dtype=torch.bfloat16, device=dev)
     at = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
+    if fused and act == "gelu":
+        gt = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
+        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, at, bias_in, tag="k3_spmm_fwd_in",
+             epi=C.EPI_GELU_GRAD, aux=gt)
+        yt = torch.empty((d, n), dtype=torch.bfloat16, device=dev)
+        spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, at, True, n, yt, tag="k3_spmm_fwd_out")
+        return FwdState(x, None, at, yt, gt)
+    zt = torch.empty((r_in, n), dtype=torch.bfloat16, device=dev)
     if act == "gelu":
         spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, zt, bias_in, gelu_aux=at, tag="k3_spmm_fwd_in")
     else:
@@ -177,15 +194,21 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
         raise ShapeError(f"upstream shape {tuple(dy.shape)} != output shape {(n, d)}")
     dev = dy.device
     dys, dy_mn = _token_operand(dy)
-    # dA^T = W2~^T . dY^T   (out_bwd: groups of W2 along d)
-    dat = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
-    spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dys, dy_mn, n, dat, tag="k4_spmm_bwd_out")
-    # activation backward + bias gradients
     dzt = torch.empty((r_in, n), dtype=torch.bfloat16, device=dev)
-    dbias = torch.empty(r_in, dtype=torch.float32, device=dev)
-    with TIMER("k7_act_bwd"):
-        C.call("s24_act_bwd", st.zt.data_ptr(), n, dat.data_ptr(), n, d_ff, n, ACT_CODES[act], dzt.data_ptr(), n,
-               dbias.data_ptr(), C.stream_of(dzt))
+    if st.gt is not None:
+        # dZ^T = (W2~^T . dY^T) * GELU'(z) with the bias gradient reduced in the same epilogue
+        dbias = torch.zeros(r_in, dtype=torch.float32, device=dev)
+        spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dys, dy_mn, n, dzt, tag="k4_spmm_bwd_out", epi=C.EPI_DGELU,
+             aux=st.gt, dbias=dbias)
+    else:
+        # dA^T = W2~^T . dY^T   (out_bwd: groups of W2 along d)
+        dat = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
+        spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dys, dy_mn, n, dat, tag="k4_spmm_bwd_out")
+        # activation backward + bias gradients
+        dbias = torch.empty(r_in, dtype=torch.float32, device=dev)
+        with TIMER("k7_act_bwd"):
+            C.call("s24_act_bwd", st.zt.data_ptr(), n, dat.data_ptr(), n, d_ff, n, ACT_CODES[act], dzt.data_ptr(),
+                   n, dbias.data_ptr(), C.stream_of(dzt))
     # dX^T = W_in~^T . dZ^T  (in_bwd: groups of W_in along r_in)
     dxt = torch.empty((d, n), dtype=torch.bfloat16, device=dev)
     spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dzt, True, n, dxt, tag="k4_spmm_bwd_in")

@@ -28,7 +28,7 @@ class _SparseFFNFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w_in, bias_in, w2, mod):
         xb = x if x.dtype == torch.bfloat16 else x.to(torch.bfloat16)
-        st = E.ffn_forward(xb, mod.op_in, bias_in.to(torch.bfloat16), mod.op_out, mod.act)
+        st = E.ffn_forward(xb, mod.op_in, bias_in.to(torch.bfloat16), mod.op_out, mod.act, fused=True)
         ctx.mod = mod
         ctx.st = st
         ctx.save_for_backward(w_in, w2)

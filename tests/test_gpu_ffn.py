@@ -94,3 +94,55 @@ def test_dense_path_and_mvue_flag():
     fs = P.fst_forward(layer, to_dev_bf16(c["x"]), masks)
     with pytest.raises(NotImplementedError):
         P.fst_backward(fs, to_dev_bf16(c["dy"]))  # mvue=True default: K8 not built
+
+
+@pytest.mark.parametrize("d,d_ff,n", [(128, 256, 128), (256, 512, 192), (256, 768, 448)])
+def test_fused_training_path_vs_oracle(d, d_ff, n):
+    """GEMM1 epilogue -> GELU(z), GELU'(z); GEMM3 epilogue -> dZ and the bias
+    gradient (no separate activation-backward kernel)."""
+    from paper_2404_01847_b200 import engine as E
+
+    c = _case("gelu", d, d_ff, n, seed=7 * d + n)
+    w_in, b, w2 = to_dev_bf16(c["w_in"]), to_dev_bf16(c["bias_in"]), to_dev_bf16(c["w2"])
+    op_in, op_out = E.CompressedOperand.empty(d_ff, d, "cuda"), E.CompressedOperand.empty(d, d_ff, "cuda")
+    E.search_compress(w_in, op_in)
+    E.search_compress(w2, op_out)
+    st = E.ffn_forward(to_dev_bf16(c["x"]), op_in, b, op_out, "gelu", fused=True)
+    assert st.zt is None and st.gt is not None
+    g = E.ffn_backward(st, to_dev_bf16(c["dy"]), op_in, op_out, "gelu", w_in_dense=w_in, w2_dense=w2, lam=1e-2)
+    lo = o.Layer(c["w_in"], c["bias_in"], c["w2"], "gelu")
+    mi, mo = o.transposable_search_conv(c["w_in"]), o.transposable_search_conv(c["w2"])
+    fr = o.fst_forward(lo, c["x"], mi, mo, exact=False)
+    br = o.fst_backward(lo, fr, c["dy"], mi, mo, exact=False)
+    assert normwise_rel(st.at.t().float().cpu().numpy(), fr["a"]) < TOL
+    assert normwise_rel(st.gt.t().float().cpu().numpy(), o.gelu_grad(fr["z"])) < TOL
+    assert normwise_rel(st.yt.t().float().cpu().numpy(), fr["y"]) < TOL
+    assert normwise_rel(g.dxt.t().float().cpu().numpy(), br["dx"]) < TOL
+    assert normwise_rel(g.dbias_in.cpu().numpy(), br["dbias_in"]) < TOL
+    assert normwise_rel(g.dw_in.cpu().numpy(), o.masked_decay_gradient(br["dw_in"], c["w_in"], mi, 1e-2)) < TOL
+    assert normwise_rel(g.dw2.cpu().numpy(), o.masked_decay_gradient(br["dw2"], c["w2"], mo, 1e-2)) < TOL
+
+
+@pytest.mark.parametrize("act", ["gelu", "swiglu"])
+def test_sparse_ffn_module_autograd_vs_oracle(act):
+    from paper_2404_01847_b200.module import SparseFFN
+
+    d, d_ff, n = 128, 256, 128
+    c = _case(act, d, d_ff, n, seed=31)
+    mod = SparseFFN.from_weights(to_dev_bf16(c["w_in"]), to_dev_bf16(c["bias_in"]), to_dev_bf16(c["w2"]), act)
+    x = to_dev_bf16(c["x"])
+    y = mod(x)
+    y.backward(to_dev_bf16(c["dy"]))
+    lo = o.Layer(c["w_in"], c["bias_in"], c["w2"], "swiglu" if act == "swiglu" else "gelu")
+    mi, mo = o.transposable_search_conv(c["w_in"]), o.transposable_search_conv(c["w2"])
+    fr = o.fst_forward(lo, c["x"], mi, mo, exact=False)
+    br = o.fst_backward(lo, fr, c["dy"], mi, mo, exact=False)
+    assert normwise_rel(y.float().detach().cpu().numpy(), fr["y"]) < TOL
+    assert normwise_rel(mod.w_in.grad.cpu().numpy(), br["dw_in"]) < TOL
+    assert normwise_rel(mod.bias_in.grad.cpu().numpy(), br["dbias_in"]) < TOL
+    assert normwise_rel(mod.w2.grad.cpu().numpy(), br["dw2"]) < TOL
+    assert mod.mask_searches == 2
+    # refresh schedule: 40 training steps -> one more search
+    for _ in range(40):
+        mod(x)
+    assert mod.mask_searches == 4
