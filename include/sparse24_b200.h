@@ -32,9 +32,10 @@
  *           16-bit word of lane L, column c, half h, bits 4g..4g+3 of which
  *           are the nibble of row m = (L%8) + 16*(L/16) + 8*h and group
  *           k/4 = 8*c + 4*((L/8)%2) + g.  Requires m, k multiples of 128.
- *   feature-major activations: a logical (tokens x features) matrix stored
- *           as features x tokens row-major (the reference's column-major
- *           FST outputs, gated_ffn.py:162 / _core.pyx:67-69).
+ *   activations: token-major (tokens x features, row-major) on the hot path;
+ *           the sparse GEMM can also emit feature-major (features x tokens,
+ *           the storage order of the reference's column-major FST outputs,
+ *           gated_ffn.py:162 / _core.pyx:67-69).
  */
 #ifndef SPARSE24_B200_H
 #define SPARSE24_B200_H
@@ -119,12 +120,13 @@ int s24_e_to_flat(const uint8_t* e, int64_t m, int64_t k, uint8_t* meta, void* s
  * Replaces kernels.spmm_colwise (_core.pyx:63-80) as driven by
  * _GatherPlan.product for in_fwd / out_fwd / out_bwd / in_bwd
  * (gated_ffn.py:294, :297, :329, :352).  B: b_mn = 0 -> stored n x k (ldb >= k),
- * b_mn = 1 -> stored k x n (ldb >= n).  D bf16 m x n (ldd).  bias (bf16, m) may be
- * NULL.  dbias (fp32, m, zeroed by the caller) is used by S24_EPI_DGELU only.
- * m % 128 == 0, k % 128 == 0, n % 32 == 0. */
+ * b_mn = 1 -> stored k x n (ldb >= n).  D bf16: d_t = 0 -> stored m x n (feature-major,
+ * ldd >= n); d_t = 1 -> stored n x m (token-major, ldd >= m); AUX uses D's layout.
+ * bias (bf16, m) may be NULL.  dbias (fp32, m, zeroed by the caller) is used by
+ * S24_EPI_DGELU only.  m % 128 == 0, k % 128 == 0, n % 32 == 0. */
 int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b, int b_mn,
              int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias, int epilogue, uint16_t* aux,
-             int64_t ldaux, float* dbias, void* stream);
+             int64_t ldaux, float* dbias, int d_t, void* stream);
 
 /* ---- K5: dense tcgen05 dW GEMM with fused masked decay ---------------------
  * D[m, n] (fp32, ldd) = sum_k A[m, k] B[n, k] + lambda_w * (1 - M[m, n]) * W[m, n]
@@ -136,11 +138,13 @@ int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int
                 int64_t n, int64_t k, float* d, int64_t ldd, const void* w, int w_dtype, const uint8_t* idx,
                 float lambda_w, void* stream);
 
-/* ---- K6/K7: fused (gated) activation, feature-major --------------------------
- * fwd: A[j, t] = act(Z[j, t]) * Z[r + j, t] (gated) or act(Z[j, t]) (plain);
+/* ---- K6/K7: fused (gated) activation, token-major ----------------------------
+ * Z is n tokens x r_in (r_in = 2r gated, = r plain), row pitch ldz; A is n x r.
+ * fwd: A[t, j] = act(Z[t, j]) * Z[t, r + j] (gated) or act(Z[t, j]) (plain);
  * replaces kernels.gate_gelu (_core.pyx:222-250) / _activate (gated_ffn.py:264-270).
- * bwd: dZ and the bias gradient sums dbias[j] = sum_t dZ[j, t] (fp32, r_in);
- * replaces the activation block of fst_backward (gated_ffn.py:336-348). */
+ * bwd: dZ (n x r_in) and the bias gradient dbias[j] = sum_t dZ[t, j] (fp32, r_in,
+ * zeroed and accumulated by the call); replaces the activation block of
+ * fst_backward (gated_ffn.py:336-348). */
 int s24_act_fwd(const uint16_t* z, int64_t ldz, int64_t r, int64_t n, int act, uint16_t* a, int64_t lda,
                 void* stream);
 int s24_act_bwd(const uint16_t* z, int64_t ldz, const uint16_t* da, int64_t ldda, int64_t r, int64_t n, int act,

@@ -40,7 +40,7 @@ SIGNATURES = {
     "s24_bits_to_idx": [_P, _I64, _I64, _P, _P, _P],
     "s24_meta_flat": [_P, _I64, _I64, _P, _P, _P],
     "s24_e_to_flat": [_P, _I64, _I64, _P, _P],
-    "s24_spmm": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _I64, _P, _P],
+    "s24_spmm": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _I64, _P, _I, _P],
     "s24_gemm_dw": [_P, _I, _I64, _P, _I, _I64, _I64, _I64, _I64, _P, _I64, _P, _I, _P, _F, _P],
     "s24_act_fwd": [_P, _I64, _I64, _I64, _I, _P, _I64, _P],
     "s24_act_bwd": [_P, _I64, _P, _I64, _I64, _I64, _I, _P, _I64, _P, _P],

@@ -62,79 +62,72 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 template <int kAct, bool kGated>
 __global__ void __launch_bounds__(256) act_fwd_kernel(const uint16_t* __restrict__ z, int64_t ldz, int64_t r,
                                                       int64_t n, uint16_t* __restrict__ a, int64_t lda) {
-  const int64_t vpr = n / 8;  // vectors per row
-  const int64_t total = r * vpr;
+  // token-major: z row t = [z1 (r) | z2 (r)] (gated) or [z (r)]; a row t = act(z1) * z2
+  const int64_t vpr = r / 8;  // 16-byte vectors per output row
+  const int64_t total = n * vpr;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = v / vpr, t = (v % vpr) * 8;
+    const int64_t t = v / vpr, j = (v % vpr) * 8;
     float x[8], o[8];
-    unpack8(__ldg(reinterpret_cast<const uint4*>(z + j * ldz + t)), x);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(z + t * ldz + j)), x);
     if constexpr (kGated) {
       float g[8];
-      unpack8(__ldg(reinterpret_cast<const uint4*>(z + (j + r) * ldz + t)), g);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(z + t * ldz + r + j)), g);
 #pragma unroll
       for (int i = 0; i < 8; ++i) o[i] = act_f<kAct>(x[i]) * g[i];
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) o[i] = act_f<kAct>(x[i]);
     }
-    *reinterpret_cast<uint4*>(a + j * lda + t) = pack8(o);
+    *reinterpret_cast<uint4*>(a + t * lda + j) = pack8(o);
   }
 }
+
+constexpr int kBwdTokens = 128;  // tokens per CTA in the backward (bias partials per CTA)
 
 template <int kAct, bool kGated>
 __global__ void __launch_bounds__(256) act_bwd_kernel(const uint16_t* __restrict__ z, int64_t ldz,
                                                       const uint16_t* __restrict__ da, int64_t ldda, int64_t r,
                                                       int64_t n, uint16_t* __restrict__ dz, int64_t lddz,
                                                       float* __restrict__ dbias) {
-  __shared__ float s_red[2][8];
-  const int64_t j = blockIdx.x;
-  float acc1 = 0.0f, acc2 = 0.0f;
-#pragma unroll 4
-  for (int64_t t = threadIdx.x * 8; t < n; t += 256 * 8) {
+  // thread = 8 consecutive features, loops over kBwdTokens tokens; bias partial
+  // sums stay in registers and land with one atomic per feature per CTA
+  const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (j >= r) return;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.y) * kBwdTokens;
+  const int64_t t1 = min(n, t0 + kBwdTokens);
+  float s1[8], s2[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s1[i] = s2[i] = 0.0f;
+#pragma unroll 2
+  for (int64_t t = t0; t < t1; ++t) {
     float x[8], d[8], o1[8];
-    unpack8(__ldg(reinterpret_cast<const uint4*>(z + j * ldz + t)), x);
-    unpack8(__ldg(reinterpret_cast<const uint4*>(da + j * ldda + t)), d);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(z + t * ldz + j)), x);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(da + t * ldda + j)), d);
     if constexpr (kGated) {
       float g[8], o2[8];
-      unpack8(__ldg(reinterpret_cast<const uint4*>(z + (j + r) * ldz + t)), g);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(z + t * ldz + r + j)), g);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         o1[i] = d[i] * g[i] * act_grad_f<kAct>(x[i]);  // dZ1 = dA * z2 * act'(z1)
         o2[i] = d[i] * act_f<kAct>(x[i]);              // dZ2 = dA * act(z1)
-        acc1 += o1[i];
-        acc2 += o2[i];
+        s1[i] += o1[i];
+        s2[i] += o2[i];
       }
-      *reinterpret_cast<uint4*>(dz + (j + r) * lddz + t) = pack8(o2);
+      *reinterpret_cast<uint4*>(dz + t * lddz + r + j) = pack8(o2);
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         o1[i] = d[i] * act_grad_f<kAct>(x[i]);
-        acc1 += o1[i];
+        s1[i] += o1[i];
       }
     }
-    *reinterpret_cast<uint4*>(dz + j * lddz + t) = pack8(o1);
+    *reinterpret_cast<uint4*>(dz + t * lddz + j) = pack8(o1);
   }
   if (dbias == nullptr) return;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    acc1 += __shfl_xor_sync(0xffffffffu, acc1, off);
-    acc2 += __shfl_xor_sync(0xffffffffu, acc2, off);
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    s_red[0][warp] = acc1;
-    s_red[1][warp] = acc2;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float b1 = 0.0f, b2 = 0.0f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      b1 += s_red[0][w];
-      b2 += s_red[1][w];
-    }
-    dbias[j] = b1;
-    if (kGated) dbias[j + r] = b2;
+  for (int i = 0; i < 8; ++i) {
+    atomicAdd(dbias + j + i, s1[i]);
+    if (kGated) atomicAdd(dbias + r + j + i, s2[i]);
   }
 }
 
@@ -145,17 +138,18 @@ using namespace s24;
 static int check_act(const void* z, int64_t ldz, const void* o, int64_t ldo, int64_t r, int64_t n, int act) {
   S24_REQUIRE(z && o, S24_ERR_ARG, "NULL pointer");
   S24_REQUIRE(act >= S24_ACT_RELU && act <= S24_ACT_SWIGLU, S24_ERR_ARG, "unknown activation %d", act);
-  S24_REQUIRE(r >= 0 && n >= 0 && ldz >= n && ldo >= n, S24_ERR_SHAPE, "bad activation shape");
-  S24_REQUIRE(n % 8 == 0 && ldz % 8 == 0 && ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(z) & 15) == 0 &&
+  const int64_t r_in = (act == S24_ACT_GEGLU || act == S24_ACT_SWIGLU) ? 2 * r : r;
+  S24_REQUIRE(r >= 0 && n >= 0 && ldz >= r_in && ldo >= r, S24_ERR_SHAPE, "bad activation shape");
+  S24_REQUIRE(r % 8 == 0 && ldz % 8 == 0 && ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(z) & 15) == 0 &&
                   (reinterpret_cast<uintptr_t>(o) & 15) == 0,
-              S24_ERR_UNSUPPORTED, "activation rows must be 16-byte aligned (tokens %% 8 == 0)");
+              S24_ERR_UNSUPPORTED, "activation rows must be 16-byte aligned (features %% 8 == 0)");
   return S24_OK;
 }
 
 template <int kAct, bool kGated>
 static void launch_fwd(const uint16_t* z, int64_t ldz, int64_t r, int64_t n, uint16_t* a, int64_t lda,
                        cudaStream_t st) {
-  int64_t blocks = (r * (n / 8) + 255) / 256;
+  int64_t blocks = (n * (r / 8) + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   act_fwd_kernel<kAct, kGated><<<static_cast<unsigned>(blocks), 256, 0, st>>>(z, ldz, r, n, a, lda);
 }
@@ -177,10 +171,16 @@ extern "C" int s24_act_fwd(const uint16_t* z, int64_t ldz, int64_t r, int64_t n,
 extern "C" int s24_act_bwd(const uint16_t* z, int64_t ldz, const uint16_t* da, int64_t ldda, int64_t r, int64_t n,
                            int act, uint16_t* dz, int64_t lddz, float* dbias, void* stream) {
   if (int rc = check_act(z, ldz, dz, lddz, r, n, act)) return rc;
-  if (int rc = check_act(da, ldda, dz, lddz, r, n, act)) return rc;
-  if (r == 0) return S24_OK;
+  S24_REQUIRE(da != nullptr && ldda >= r && ldda % 8 == 0 && (reinterpret_cast<uintptr_t>(da) & 15) == 0,
+              S24_ERR_UNSUPPORTED, "dA rows must be 16-byte aligned");
+  if (r == 0 || n == 0) return S24_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const unsigned grid = static_cast<unsigned>(r);
+  const bool gated = act == S24_ACT_GEGLU || act == S24_ACT_SWIGLU;
+  if (dbias != nullptr) {
+    cudaError_t e = cudaMemsetAsync(dbias, 0, sizeof(float) * (gated ? 2 * r : r), st);
+    S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+  }
+  const dim3 grid(static_cast<unsigned>((r / 8 + 255) / 256), static_cast<unsigned>((n + kBwdTokens - 1) / kBwdTokens));
   switch (act) {
     case S24_ACT_RELU:
       act_bwd_kernel<S24_ACT_RELU, false><<<grid, 256, 0, st>>>(z, ldz, da, ldda, r, n, dz, lddz, dbias);

@@ -105,7 +105,7 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
   nb = in_group / gm;
 }
 
-template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi>
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmD,
@@ -336,20 +336,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         } else {
           constexpr bool kTwo = kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad;  // two bf16 outputs
+          float v2[32];
           if constexpr (kEpi == kEpiDAct) {
-            // dZ = dA * GELU'(Z): GELU'(Z) tile row from global (feature-major, bf16)
-            const uint4* gp = reinterpret_cast<const uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0);
-            float rs = 0.0f;
+            // dZ = dA * GELU'(z), GELU'(z) in the output's layout; row sums -> bias gradient
+            if constexpr (kOutT) {
+              const uint16_t* gp = ep.aux + static_cast<int64_t>(n0) * ep.ldaux + m;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const uint4 x = __ldg(gp + u);
-              const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+              for (int i = 0; i < 32; ++i) v[i] *= bf16_to_f32(__ldg(gp + static_cast<int64_t>(i) * ep.ldaux));
+            } else {
+              const uint4* gp = reinterpret_cast<const uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0);
 #pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                v[8 * u + 2 * t] *= __uint_as_float(xs[t] << 16);
-                v[8 * u + 2 * t + 1] *= __uint_as_float(xs[t] & 0xFFFF0000u);
+              for (int u = 0; u < 4; ++u) {
+                const uint4 x = __ldg(gp + u);
+                const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  v[8 * u + 2 * t] *= __uint_as_float(xs[t] << 16);
+                  v[8 * u + 2 * t + 1] *= __uint_as_float(xs[t] & 0xFFFF0000u);
+                }
               }
             }
+            float rs = 0.0f;
 #pragma unroll
             for (int i = 0; i < 32; ++i) rs += v[i];
             bias_v += rs;  // running bias-gradient partial of row m over this tile's chunks
@@ -357,58 +364,50 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += bias_v;
           }
-          // bf16 32x32 tile, 64B swizzle: chunk c of row `lane` -> chunk c ^ ((lane >> 1) & 3)
+          if constexpr (kEpi == kEpiGeluGrad) {
+            // D = GELU(z), AUX = GELU'(z): one erf + one exp shared by both
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float x = v[i];
+              float e;
+              const float ef = erf_fast(x * 0.70710678118654752f, e);
+              const float cdf = 0.5f * (1.0f + ef);
+              v[i] = x * cdf;
+              v2[i] = fmaf(x * 0.39894228040143268f, e, cdf);
+            }
+          } else if constexpr (kEpi == kEpiGeluAux) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v2[i] = gelu_fast(v[i]);
+          }
           uint8_t* zb = stg + (kTwo ? 0 : sbuf * 2048);
           if (lane == 0) {
             if constexpr (kTwo) bulk_wait_read0();
             else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           }
           __syncwarp();
-          if constexpr (kEpi == kEpiGeluGrad) {
-            // D = GELU(z), AUX = GELU'(z): one erf + one exp shared by both
+          // stage a 32 x 32 bf16 tile: feature-major -> 64B-swizzled rows of this lane;
+          // token-major (kOutT) -> transposed, row n holds the 32 features of this warp
+          auto stage = [&](uint8_t* buf, const float(&x)[32]) {
+            if constexpr (kOutT) {
+              uint16_t* b16 = reinterpret_cast<uint16_t*>(buf);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              float g[8], gd[8];
+              for (int i = 0; i < 32; ++i) b16[i * 32 + lane] = f32_to_bf16(x[i]);
+            } else {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const float x = v[8 * c + i];
-                float e;
-                const float ef = erf_fast(x * 0.70710678118654752f, e);
-                const float cdf = 0.5f * (1.0f + ef);
-                g[i] = x * cdf;
-                gd[i] = fmaf(x * 0.39894228040143268f, e, cdf);
-              }
-              *reinterpret_cast<uint4*>(zb + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
-                  make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]), pack_bf16x2(g[4], g[5]),
-                             pack_bf16x2(g[6], g[7]));
-              *reinterpret_cast<uint4*>(stg + 2048 + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
-                  make_uint4(pack_bf16x2(gd[0], gd[1]), pack_bf16x2(gd[2], gd[3]), pack_bf16x2(gd[4], gd[5]),
-                             pack_bf16x2(gd[6], gd[7]));
+              for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<uint4*>(buf + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+                    make_uint4(pack_bf16x2(x[8 * c], x[8 * c + 1]), pack_bf16x2(x[8 * c + 2], x[8 * c + 3]),
+                               pack_bf16x2(x[8 * c + 4], x[8 * c + 5]), pack_bf16x2(x[8 * c + 6], x[8 * c + 7]));
             }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              *reinterpret_cast<uint4*>(zb + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
-                  make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
-                             pack_bf16x2(v[8 * c + 4], v[8 * c + 5]), pack_bf16x2(v[8 * c + 6], v[8 * c + 7]));
-          }
-          if constexpr (kEpi == kEpiGeluAux) {
-            uint8_t* ab = stg + 2048;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              float g[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) g[i] = gelu_fast(v[8 * c + i]);
-              *reinterpret_cast<uint4*>(ab + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
-                  make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]), pack_bf16x2(g[4], g[5]),
-                             pack_bf16x2(g[6], g[7]));
-            }
-          }
+          };
+          stage(zb, v);
+          if constexpr (kTwo) stage(stg + 2048, v2);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmD, zb, n0, m_w);
-            if constexpr (kTwo) tma_store_2d(&tmX, stg + 2048, n0, m_w);
+            const int cx = kOutT ? m_w : n0, cy = kOutT ? n0 : m_w;
+            tma_store_2d(&tmD, zb, cx, cy);
+            if constexpr (kTwo) tma_store_2d(&tmX, stg + 2048, cx, cy);
             bulk_commit();
           }
           sbuf ^= 1;
@@ -458,7 +457,7 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-enum MapKind { kMapBf16Sw128 = 0, kMapBf16Sw64 = 1, kMapF32Sw128 = 2, kMapU64 = 3 };
+enum MapKind { kMapBf16Sw128 = 0, kMapBf16Sw64 = 1, kMapF32Sw128 = 2, kMapU64 = 3, kMapBf16Plain = 4 };
 
 // 2-D tensor map: inner (contiguous) extent, outer extent, row pitch in elements.
 static int make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch_elems,
@@ -475,7 +474,7 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t ou
   const CUtensorMapDataType dt = kind == kMapU64 ? CU_TENSOR_MAP_DATA_TYPE_UINT64
                                  : kind == kMapF32Sw128 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                         : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-  const CUtensorMapSwizzle sw = kind == kMapU64 ? CU_TENSOR_MAP_SWIZZLE_NONE
+  const CUtensorMapSwizzle sw = (kind == kMapU64 || kind == kMapBf16Plain) ? CU_TENSOR_MAP_SWIZZLE_NONE
                                 : kind == kMapBf16Sw64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                        : CU_TENSOR_MAP_SWIZZLE_128B;
   CUresult r = enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
@@ -495,11 +494,11 @@ static int num_sms() {
   return n;
 }
 
-template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi>
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT = false>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& me, const CUtensorMap& md,
                        const CUtensorMap& mx, const GemmShape& shp, const EpiParams& ep, cudaStream_t st) {
   using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG>;
-  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi>;
+  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi, kOutT>;
   static bool attr_done = false;  // per template instance
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -537,16 +536,17 @@ static int cg_override() {
 
 extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b,
                         int b_mn, int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias,
-                        int epilogue, uint16_t* aux, int64_t ldaux, float* dbias, void* stream) {
+                        int epilogue, uint16_t* aux, int64_t ldaux, float* dbias, int d_t, void* stream) {
   S24_REQUIRE(a_vals && a_e && b && d, S24_ERR_ARG, "NULL operand");
   S24_REQUIRE(m % 128 == 0 && k % 128 == 0 && n % 32 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
               "sparse GEMM needs m %% 128 == 0, k %% 128 == 0, n %% 32 == 0 (got m=%lld k=%lld n=%lld)",
               (long long)m, (long long)k, (long long)n);
-  S24_REQUIRE(ldd >= n && ldd % 8 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0, S24_ERR_UNSUPPORTED,
-              "output rows must be 16-byte aligned");
+  S24_REQUIRE(ldd >= (d_t ? m : n) && ldd % 8 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0,
+              S24_ERR_UNSUPPORTED, "output rows must be 16-byte aligned");
   S24_REQUIRE(epilogue >= S24_EPI_STORE && epilogue <= S24_EPI_DGELU, S24_ERR_ARG, "bad epilogue");
   if (epilogue != S24_EPI_STORE)
-    S24_REQUIRE(aux != nullptr && ldaux >= n && ldaux % 8 == 0 && (reinterpret_cast<uintptr_t>(aux) & 15) == 0,
+    S24_REQUIRE(aux != nullptr && ldaux >= (d_t ? m : n) && ldaux % 8 == 0 &&
+                    (reinterpret_cast<uintptr_t>(aux) & 15) == 0,
                 S24_ERR_ARG, "this epilogue needs a 16-byte aligned aux tensor");
   S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
   const bool pair = (m % 256 == 0) && cg_override() != 1;
@@ -555,9 +555,18 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   if (int rc = make_map(&ma, a_vals, k / 2, m, k / 2, 64, 128)) return rc;
   if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, kMapU64)) return rc;
   CUtensorMap md, mx;
-  if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapBf16Sw64)) return rc;
+  // D[m, n] feature-major (64B-swizzled staging) or D^T[n, m] token-major (d_t, transposed staging)
+  if (d_t) {
+    if (int rc = make_map(&md, d, m, n, ldd, 32, 32, kMapBf16Plain)) return rc;
+  } else {
+    if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapBf16Sw64)) return rc;
+  }
   if (epilogue == S24_EPI_GELU_AUX || epilogue == S24_EPI_GELU_GRAD) {
-    if (int rc = make_map(&mx, aux, n, m, ldaux, 32, 32, kMapBf16Sw64)) return rc;
+    if (d_t) {
+      if (int rc = make_map(&mx, aux, m, n, ldaux, 32, 32, kMapBf16Plain)) return rc;
+    } else {
+      if (int rc = make_map(&mx, aux, n, m, ldaux, 32, 32, kMapBf16Sw64)) return rc;
+    }
   } else {
     mx = md;
   }
@@ -572,10 +581,12 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k)};
   EpiParams ep{d, ldd, bias, aux, ldaux, dbias, nullptr, 0, nullptr, 0.0f};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define S24_SP(BMN, BNV, CG, EPI)                                                                       \
-  return launch_gemm<true, false, BMN, BNV,                                                              \
-                     stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, EPI>(ma, mb, me, md, mx, \
-                                                                                             shp, ep, st)
+#define S24_SP(BMN, BNV, CG, EPI)                                                                          \
+  if (d_t)                                                                                                  \
+    return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
+                       EPI, true>(ma, mb, me, md, mx, shp, ep, st);                                         \
+  return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG,   \
+                     EPI, false>(ma, mb, me, md, mx, shp, ep, st)
 #define S24_SP_EPI(BMN, BNV, CG)                                              \
   switch (epilogue) {                                                           \
     case S24_EPI_GELU_AUX: S24_SP(BMN, BNV, CG, kEpiGeluAux);                   \

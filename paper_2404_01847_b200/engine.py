@@ -97,10 +97,11 @@ def compress_values(w: torch.Tensor, op: CompressedOperand) -> None:
 def spmm(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b_mn: bool, n: int,
          out: torch.Tensor, bias: torch.Tensor | None = None, gelu_aux: torch.Tensor | None = None,
          tag: str = "k34_spmm", epi: int | None = None, aux: torch.Tensor | None = None,
-         dbias: torch.Tensor | None = None) -> None:
-    """out[m, n] (bf16, row-major) = W~[m, k] (2:4) . B[n, k]^T with an epilogue:
-    EPI_STORE (+bias), EPI_GELU_AUX (out = z, gelu_aux = gelu(z)), EPI_GELU_GRAD
-    (out = gelu(z), aux = gelu'(z)), EPI_DGELU (out = acc * aux, dbias += row sums)."""
+         dbias: torch.Tensor | None = None, out_t: bool = False) -> None:
+    """D[m, n] = W~[m, k] (2:4) . B[n, k]^T, stored as out[m, n] (feature-major)
+    or, with out_t, as out[n, m] (token-major); epilogues: EPI_STORE (+bias),
+    EPI_GELU_AUX (out = z, aux = gelu(z)), EPI_GELU_GRAD (out = gelu(z),
+    aux = gelu'(z)), EPI_DGELU (out = acc * aux, dbias += sums over tokens)."""
     if epi is None:
         epi = C.EPI_GELU_AUX if gelu_aux is not None else C.EPI_STORE
     if gelu_aux is not None:
@@ -108,7 +109,7 @@ def spmm(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b
     with TIMER(tag):
         C.call("s24_spmm", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), b.stride(0), n,
                out.data_ptr(), out.stride(0), C.ptr(bias), epi, C.ptr(aux), aux.stride(0) if aux is not None else 0,
-               C.ptr(dbias), C.stream_of(out))
+               C.ptr(dbias), int(out_t), C.stream_of(out))
 
 
 def gemm_dw(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, m: int, n: int, k: int,
@@ -122,29 +123,27 @@ def gemm_dw(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, m: int, n:
                C.ptr(idx) if decay else None, float(lam if decay else 0.0), C.stream_of(out))
 
 
-def _token_operand(t: torch.Tensor) -> tuple[torch.Tensor, bool]:
-    """(storage, mn_major) for a logical (N x f) activation: row-major storage
-    is K-major for the sparse GEMM; a column-major view (feature-major
-    storage) is MN-major."""
-    if t.stride(1) == 1 and t.stride(0) >= t.shape[1] and t.stride(0) % 8 == 0:
-        return t, False
-    if t.stride(0) == 1 and t.stride(1) >= t.shape[0] and t.stride(1) % 8 == 0:
-        return t.t(), True
-    return t.contiguous(), False
+def _rows(t: torch.Tensor) -> torch.Tensor:
+    """Row-major (token-major) storage with a 16-byte aligned pitch."""
+    if t.stride(1) == 1 and t.stride(0) >= t.shape[1] and t.stride(0) % 8 == 0 and t.data_ptr() % 16 == 0:
+        return t
+    return t.contiguous()
 
 
 @dataclass
 class FwdState:
-    x: torch.Tensor  # (N, d) as given (bf16)
-    zt: torch.Tensor | None  # (r_in, N) pre-activation (None on the fused training path)
-    at: torch.Tensor  # (d_ff, N)
-    yt: torch.Tensor  # (d, N)
-    gt: torch.Tensor | None = None  # (d_ff, N) GELU'(z), fused training path only
+    x: torch.Tensor  # (N, d) bf16, token-major
+    z: torch.Tensor | None  # (N, r_in) pre-activation (None on the fused training path)
+    a: torch.Tensor  # (N, d_ff)
+    y: torch.Tensor  # (N, d)
+    g: torch.Tensor | None = None  # (N, d_ff) GELU'(z), fused training path only
 
 
 def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor | None, w2: CompressedOperand,
                 act: str, fused: bool = False) -> FwdState:
-    """fused=True (GELU only): GEMM1's epilogue stores A = GELU(z) and
+    """Z = X W_in~^T + b -> A = act(Z) -> Y = A W2~^T (gated_ffn.py:293-297).
+
+    fused=True (GELU only): GEMM1's epilogue stores A = GELU(z) and
     G = GELU'(z) instead of z, so the backward's GEMM3 epilogue applies the
     activation derivative and reduces the bias gradient (no separate K7)."""
     n, d = x.shape
@@ -155,30 +154,30 @@ def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor 
     if n % 64:
         raise ShapeError(f"token count must be a multiple of 64 on the tensor-core path, got {n}")
     dev = x.device
-    xs, x_mn = _token_operand(x)
-    at = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
+    x = _rows(x)
+    a = torch.empty((n, d_ff), dtype=torch.bfloat16, device=dev)
+    y = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
     if fused and act == "gelu":
-        gt = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
-        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, at, bias_in, tag="k3_spmm_fwd_in",
-             epi=C.EPI_GELU_GRAD, aux=gt)
-        yt = torch.empty((d, n), dtype=torch.bfloat16, device=dev)
-        spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, at, True, n, yt, tag="k3_spmm_fwd_out")
-        return FwdState(x, None, at, yt, gt)
-    zt = torch.empty((r_in, n), dtype=torch.bfloat16, device=dev)
+        g = torch.empty((n, d_ff), dtype=torch.bfloat16, device=dev)
+        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, a, bias_in, tag="k3_spmm_fwd_in",
+             epi=C.EPI_GELU_GRAD, aux=g, out_t=True)
+        spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, a, False, n, y, tag="k3_spmm_fwd_out", out_t=True)
+        return FwdState(x, None, a, y, g)
+    z = torch.empty((n, r_in), dtype=torch.bfloat16, device=dev)
     if act == "gelu":
-        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, zt, bias_in, gelu_aux=at, tag="k3_spmm_fwd_in")
+        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, z, bias_in, gelu_aux=a, tag="k3_spmm_fwd_in",
+             out_t=True)
     else:
-        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, xs, x_mn, n, zt, bias_in, tag="k3_spmm_fwd_in")
+        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, z, bias_in, tag="k3_spmm_fwd_in", out_t=True)
         with TIMER("k6_act_fwd"):
-            C.call("s24_act_fwd", zt.data_ptr(), n, d_ff, n, ACT_CODES[act], at.data_ptr(), n, C.stream_of(zt))
-    yt = torch.empty((d, n), dtype=torch.bfloat16, device=dev)
-    spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, at, True, n, yt, tag="k3_spmm_fwd_out")
-    return FwdState(x, zt, at, yt)
+            C.call("s24_act_fwd", z.data_ptr(), r_in, d_ff, n, ACT_CODES[act], a.data_ptr(), d_ff, C.stream_of(z))
+    spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, a, False, n, y, tag="k3_spmm_fwd_out", out_t=True)
+    return FwdState(x, z, a, y)
 
 
 @dataclass
 class Grads:
-    dxt: torch.Tensor  # (d, N) bf16
+    dx: torch.Tensor  # (N, d) bf16
     dw_in: torch.Tensor  # (r_in, d) fp32
     dbias_in: torch.Tensor  # (r_in,) fp32
     dw2: torch.Tensor  # (d, d_ff) fp32
@@ -188,35 +187,33 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
                  w_in_dense: torch.Tensor | None = None, w2_dense: torch.Tensor | None = None,
                  lam: float = 0.0, dw_in_out: torch.Tensor | None = None,
                  dw2_out: torch.Tensor | None = None) -> Grads:
+    """dA = dY W2~ (out_bwd, W2's transposed orientation) -> dZ (activation
+    backward, bias gradient) -> dX = dZ W_in~ (in_bwd); dense dW2 = dY^T A and
+    dW_in = dZ^T X with the masked decay lam (1 - M) W fused (gated_ffn.py:327-356)."""
     n, d = st.x.shape
     r_in, d_ff = w_in.rows, w2.cols
     if tuple(dy.shape) != (n, d):
         raise ShapeError(f"upstream shape {tuple(dy.shape)} != output shape {(n, d)}")
     dev = dy.device
-    dys, dy_mn = _token_operand(dy)
-    dzt = torch.empty((r_in, n), dtype=torch.bfloat16, device=dev)
-    if st.gt is not None:
-        # dZ^T = (W2~^T . dY^T) * GELU'(z) with the bias gradient reduced in the same epilogue
+    dy = _rows(dy)
+    dz = torch.empty((n, r_in), dtype=torch.bfloat16, device=dev)
+    if st.g is not None:
+        # dZ = (dY W2~) * GELU'(z) with the bias gradient reduced in the same epilogue
         dbias = torch.zeros(r_in, dtype=torch.float32, device=dev)
-        spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dys, dy_mn, n, dzt, tag="k4_spmm_bwd_out", epi=C.EPI_DGELU,
-             aux=st.gt, dbias=dbias)
+        spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dy, False, n, dz, tag="k4_spmm_bwd_out", epi=C.EPI_DGELU,
+             aux=st.g, dbias=dbias, out_t=True)
     else:
-        # dA^T = W2~^T . dY^T   (out_bwd: groups of W2 along d)
-        dat = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
-        spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dys, dy_mn, n, dat, tag="k4_spmm_bwd_out")
-        # activation backward + bias gradients
+        da = torch.empty((n, d_ff), dtype=torch.bfloat16, device=dev)
+        spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dy, False, n, da, tag="k4_spmm_bwd_out", out_t=True)
         dbias = torch.empty(r_in, dtype=torch.float32, device=dev)
         with TIMER("k7_act_bwd"):
-            C.call("s24_act_bwd", st.zt.data_ptr(), n, dat.data_ptr(), n, d_ff, n, ACT_CODES[act], dzt.data_ptr(),
-                   n, dbias.data_ptr(), C.stream_of(dzt))
-    # dX^T = W_in~^T . dZ^T  (in_bwd: groups of W_in along r_in)
-    dxt = torch.empty((d, n), dtype=torch.bfloat16, device=dev)
-    spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dzt, True, n, dxt, tag="k4_spmm_bwd_in")
-    # dW2[d, d_ff] = dY^T A : A-op = dY (K = tokens), B-op = A^T (feature-major, K-major)
+            C.call("s24_act_bwd", st.z.data_ptr(), r_in, da.data_ptr(), d_ff, d_ff, n, ACT_CODES[act],
+                   dz.data_ptr(), r_in, dbias.data_ptr(), C.stream_of(dz))
+    dx = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
+    spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dz, False, n, dx, tag="k4_spmm_bwd_in", out_t=True)
+    # dW2[d, d_ff] = dY^T A and dW_in[r_in, d] = dZ^T X: K = tokens, both operands token-major (MN-major)
     dw2 = dw2_out if dw2_out is not None else torch.empty((d, d_ff), dtype=torch.float32, device=dev)
-    gemm_dw(dys, not dy_mn, st.at, False, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")
-    # dW_in[r_in, d] = dZ^T X : A-op = dZ^T (K-major), B-op = X (token-major => MN-major)
-    xs, x_mn = _token_operand(st.x)
+    gemm_dw(dy, True, st.a, True, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")
     dw_in = dw_in_out if dw_in_out is not None else torch.empty((r_in, d), dtype=torch.float32, device=dev)
-    gemm_dw(dzt, False, xs, not x_mn, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam, tag="k5_gemm_dw_in")
-    return Grads(dxt, dw_in, dbias, dw2)
+    gemm_dw(dz, True, st.x, True, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam, tag="k5_gemm_dw_in")
+    return Grads(dx, dw_in, dbias, dw2)

@@ -4,9 +4,9 @@ reference API of sparse24.gated_ffn (gated_ffn.py:1-373) over CUDA tensors.
 Differences from the reference that are deliberate and visible:
   * tensors are torch CUDA tensors; compute is bf16 with fp32 accumulation
     (the reference is float64); tolerances are stated in tests/;
-  * z, a, y, d_x come back as column-major logical views of feature-major
-    storage -- the same storage order the reference's sparse route produces
-    (gated_ffn.py:162);
+  * z, a, y, d_x are token-major (row-major N x features) torch tensors; the
+    reference's sparse route returns the same values in column-major numpy
+    arrays (gated_ffn.py:162);
   * weight gradients are fp32;
   * mvue=True (the reference default, gated_ffn.py:308) needs the MVUE
     sparse dW kernel, not built yet: it raises
@@ -158,9 +158,9 @@ class FstActivations:
 
     layer: FFNLayer
     x: torch.Tensor
-    z: torch.Tensor  # (N, r_in) column-major view
-    a: torch.Tensor  # (N, d_ff) column-major view
-    y: torch.Tensor  # (N, d) column-major view
+    z: torch.Tensor  # (N, r_in)
+    a: torch.Tensor  # (N, d_ff)
+    y: torch.Tensor  # (N, d)
     masks: FFNMasks | None
     w_in_cat: torch.Tensor
     state: E.FwdState | None = None
@@ -200,7 +200,7 @@ def fst_forward(layer: FFNLayer, x: torch.Tensor, masks: FFNMasks | None,
     E.compress_values(layer.w_in_cat, ops["in"])
     E.compress_values(layer.w2, ops["out"])
     st = E.ffn_forward(x, ops["in"], _as_bf16(layer.bias_in_cat), ops["out"], layer.activation.value)
-    return FstActivations(layer, x, st.zt.t(), st.at.t(), st.yt.t(), masks, layer.w_in_cat, st)
+    return FstActivations(layer, x, st.z, st.a, st.y, masks, layer.w_in_cat, st)
 
 
 def fst_backward(bundle: FstActivations, upstream: torch.Tensor, rng_seed: int = 0, mvue: bool = True,
@@ -221,7 +221,7 @@ def fst_backward(bundle: FstActivations, upstream: torch.Tensor, rng_seed: int =
     ops = bundle.masks.plans(layer)
     g = E.ffn_backward(bundle.state, up, ops["in"], ops["out"], layer.activation.value,
                        w_in_dense=layer.w_in_cat, w2_dense=layer.w2, lam=decay_lambda)
-    return _pack_grads(layer, g.dxt.t(), g.dw_in, g.dbias_in, g.dw2)
+    return _pack_grads(layer, g.dx, g.dw_in, g.dbias_in, g.dw2)
 
 
 def _pack_grads(layer, dx, dw_in, dbias, dw2) -> LayerGrads:
@@ -250,38 +250,37 @@ def _dense_backward(bundle: FstActivations, up: torch.Tensor) -> LayerGrads:
 
 
 def geglu_forward(x, u, v, b, c, traversal: Traversal = Traversal.COL_ORDER) -> torch.Tensor:
-    """gelu(x u^T + b) * (x v^T + c) (gated_ffn.py:208-224): dense GEMM, then the
-    fused gate kernel K6 on the feature-major intermediate.  Returns the
-    column-major (N x d_ff) logical view."""
+    """gelu(x u^T + b) * (x v^T + c) (gated_ffn.py:208-224): one dense GEMM on
+    the concatenated [u; v] (library GEMM: this standalone helper is not on the
+    sparse path), then the fused gate kernel K6.  Returns (N x d_ff)."""
     x = _as_bf16(x)
     w_cat = torch.cat([u, v], 0).to(torch.bfloat16)
     b_cat = torch.cat([b, c]).to(torch.bfloat16)
     if x.shape[1] != w_cat.shape[1]:
         raise ShapeError(f"x cols {x.shape[1]} != weight cols {w_cat.shape[1]}")
     n, r = x.shape[0], u.shape[0]
-    zt = torch.addmm(b_cat[:, None], w_cat, x.t()).contiguous()  # (2r, N) feature-major
-    at = torch.empty((r, n), dtype=torch.bfloat16, device=x.device)
-    C.call("s24_act_fwd", zt.data_ptr(), n, r, n, C.ACT_GEGLU, at.data_ptr(), n, C.stream_of(zt))
-    return at.t()
+    z = torch.nn.functional.linear(x, w_cat, b_cat).contiguous()  # (N, 2r) token-major
+    a = torch.empty((n, r), dtype=torch.bfloat16, device=x.device)
+    C.call("s24_act_fwd", z.data_ptr(), 2 * r, r, n, C.ACT_GEGLU, a.data_ptr(), r, C.stream_of(z))
+    return a
 
 
 def geglu_backward(x, u, v, b, c, upstream) -> LayerGrads:
-    """Analytic GEGLU gradients (gated_ffn.py:227-244) via K7 for the gate."""
+    """Analytic GEGLU gradients (gated_ffn.py:227-244), the gate part by K7."""
     x = _as_bf16(x)
-    up = _as_bf16(upstream)
+    up = _as_bf16(upstream).contiguous()
     w_cat = torch.cat([u, v], 0).to(torch.bfloat16)
     b_cat = torch.cat([b, c]).to(torch.bfloat16)
     n, r = x.shape[0], u.shape[0]
     if tuple(up.shape) != (n, r):
         raise ShapeError(f"upstream shape {tuple(up.shape)} != output shape {(n, r)}")
-    zt = torch.addmm(b_cat[:, None], w_cat, x.t()).contiguous()
-    dat = up.t().contiguous()
-    dzt = torch.empty_like(zt)
+    z = torch.nn.functional.linear(x, w_cat, b_cat).contiguous()
+    dz = torch.empty_like(z)
     dbias = torch.empty(2 * r, dtype=torch.float32, device=x.device)
-    C.call("s24_act_bwd", zt.data_ptr(), n, dat.data_ptr(), n, r, n, C.ACT_GEGLU, dzt.data_ptr(), n,
-           dbias.data_ptr(), C.stream_of(zt))
-    dx = (dzt.t() @ w_cat)
-    dw = (dzt.float() @ x.float())
+    C.call("s24_act_bwd", z.data_ptr(), 2 * r, up.data_ptr(), r, r, n, C.ACT_GEGLU, dz.data_ptr(), 2 * r,
+           dbias.data_ptr(), C.stream_of(z))
+    dx = dz @ w_cat
+    dw = dz.t().float() @ x.float()
     return LayerGrads(d_x=dx, d_u=dw[:r], d_v=dw[r:], d_b=dbias[:r], d_c=dbias[r:])
 
 

@@ -21,6 +21,7 @@ from __future__ import annotations
 import torch
 import torch.nn.functional as F
 
+from . import dp
 from . import engine as E
 
 
@@ -32,7 +33,7 @@ class _SparseFFNFn(torch.autograd.Function):
         ctx.mod = mod
         ctx.st = st
         ctx.save_for_backward(w_in, w2)
-        return st.yt.t()
+        return st.y
 
     @staticmethod
     def backward(ctx, dy):
@@ -41,7 +42,7 @@ class _SparseFFNFn(torch.autograd.Function):
         g = E.ffn_backward(ctx.st, dy.to(torch.bfloat16), mod.op_in, mod.op_out, mod.act, w_in_dense=w_in,
                            w2_dense=w2, lam=mod.decay_lambda)
         ctx.st = None
-        return g.dxt.t(), g.dw_in, g.dbias_in, g.dw2, None
+        return g.dx, g.dw_in, g.dbias_in, g.dw2, None
 
 
 class SparseFFN(torch.nn.Module):
@@ -108,13 +109,7 @@ class SparseFFN(torch.nn.Module):
     def allreduce_grads(self, group=None) -> None:
         """One NCCL all-reduce of the concatenated gradients (SUM: the
         per-rank loss is a per-rank sum/mean and the decay is pre-scaled)."""
-        grads = [p.grad for p in (self.w_in, self.bias_in, self.w2)]
-        flat = torch.cat([g.reshape(-1) for g in grads])
-        torch.distributed.all_reduce(flat, group=group)
-        off = 0
-        for g in grads:
-            g.copy_(flat[off:off + g.numel()].view_as(g))
-            off += g.numel()
+        dp.allreduce_grads([p.grad for p in (self.w_in, self.bias_in, self.w2)], group)
 
     @property
     def masks_idx(self):

@@ -107,3 +107,35 @@ def test_shape_errors():
 
     with pytest.raises(ShapeError):
         CompressedOperand.empty(100, 128, "cuda")
+
+
+@pytest.mark.parametrize("m,k,n", [(256, 256, 128), (512, 384, 448), (128, 256, 96)])
+@pytest.mark.parametrize("epi", ["store", "gelu_grad", "dgelu"])
+def test_sparse_gemm_token_major_output_and_epilogues(m, k, n, epi):
+    """out_t: D^T stored token-major (n x m); fused GELU/GELU' and dGELU+bias-grad epilogues."""
+    import paper_2404_01847_b200._capi as C
+    from paper_2404_01847_b200.engine import spmm
+
+    w, op, bits = _operand(m, k, 11 + m + n)
+    x = torch.randn(n, k, device="cuda").bfloat16()
+    ref = x.float() @ (w.float() * bits.float()).t()  # (n, m)
+    out = torch.empty((n, m), dtype=torch.bfloat16, device="cuda")
+    if epi == "store":
+        bias = torch.randn(m, device="cuda").bfloat16()
+        spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, bias, out_t=True)
+        assert normwise_rel(out.float().cpu(), (ref + bias.float()).cpu()) < 1e-2
+    elif epi == "gelu_grad":
+        g = torch.empty_like(out)
+        spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, None, epi=C.EPI_GELU_GRAD, aux=g, out_t=True)
+        zr = ref.double()
+        cdf = 0.5 * (1 + torch.erf(zr / 2 ** 0.5))
+        assert normwise_rel(out.float().cpu(), (zr * cdf).cpu()) < 1e-2
+        gd = cdf + zr * torch.exp(-0.5 * zr * zr) / (2 * torch.pi) ** 0.5
+        assert normwise_rel(g.float().cpu(), gd.cpu()) < 1e-2
+    else:
+        gin = torch.rand(n, m, device="cuda").bfloat16()
+        db = torch.zeros(m, dtype=torch.float32, device="cuda")
+        spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, None, epi=C.EPI_DGELU, aux=gin, dbias=db, out_t=True)
+        dz = ref * gin.float()
+        assert normwise_rel(out.float().cpu(), dz.cpu()) < 1e-2
+        assert normwise_rel(db.cpu(), dz.sum(0).cpu()) < 1e-3

@@ -147,3 +147,36 @@ def test_masked_decay_kernel():
     # kept weights untouched (test_optim.py:81-86)
     kept = m.bits.bool()
     assert torch.equal(out[kept], g[kept])
+
+
+def test_reference_backend_shim_pattern_scores_bit_exact(mask_golden):
+    """The reference-kernel-interface shim: pattern_scores(best) bit-exact on the
+    reference acceptance-style corpus, scores equal to the sequential f64 sums."""
+    from paper_2404_01847_b200 import reference_backend as rb
+
+    w = mask_corpora()["gauss_f64"][0]
+    absb = np.abs(o.blocks16(w))
+    _, pos = o.pattern_table()
+    scores, best = rb.pattern_scores(absb, pos)
+    s_ref, b_ref = o.pattern_scores(absb, pos)
+    assert scores.tobytes() == s_ref.tobytes()
+    np.testing.assert_array_equal(best, b_ref)
+    np.testing.assert_array_equal(best.reshape(-1), mask_golden["gauss_f64.idx"].reshape(-1))
+
+
+def test_reference_backend_shim_spmm_and_gate_toleranced():
+    from paper_2404_01847_b200 import reference_backend as rb
+
+    rng = np.random.default_rng(1)
+    w = o.round_bf16(rng.standard_normal((48, 40)))  # B^T (n x k) in the reference's column-wise spmm
+    bits = o.transposable_search_conv(w)
+    take, pos_t = o.gather_plan(bits, False)
+    vals = w.ravel()[take].T
+    a = o.round_bf16(rng.standard_normal((20, 40)))
+    got = rb.spmm_colwise(a, vals, pos_t)
+    ref = o.spmm_colwise(a, vals, pos_t)
+    assert got.flags["F_CONTIGUOUS"]
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-2
+    z1, z2 = rng.standard_normal((9, 12)), rng.standard_normal((9, 12))
+    g = rb.gate_gelu(z1, z2, False)
+    assert np.linalg.norm(g - o.gate(z1, z2)) / np.linalg.norm(o.gate(z1, z2)) < 1e-2
