@@ -121,7 +121,10 @@ int s24_e_to_flat(const uint8_t* e, int64_t m, int64_t k, uint8_t* meta, void* s
  * _GatherPlan.product for in_fwd / out_fwd / out_bwd / in_bwd
  * (gated_ffn.py:294, :297, :329, :352).  B: b_mn = 0 -> stored n x k (ldb >= k),
  * b_mn = 1 -> stored k x n (ldb >= n).  D bf16: d_t = 0 -> stored m x n (feature-major,
- * ldd >= n); d_t = 1 -> stored n x m (token-major, ldd >= m); AUX uses D's layout.
+ * ldd >= n); d_t = 1 -> stored n x m (token-major, ldd >= m).  AUX uses D's layout
+ * for S24_EPI_GELU_AUX; for S24_EPI_GELU_GRAD / S24_EPI_DGELU the GELU'(z) AUX is
+ * always m x n (feature-major, ldaux >= n): it is only read back row-wise by the
+ * DGELU epilogue.
  * bias (bf16, m) may be NULL.  dbias (fp32, m, zeroed by the caller) is used by
  * S24_EPI_DGELU only.  m % 128 == 0, k % 128 == 0, n % 32 == 0. */
 int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b, int b_mn,

@@ -339,11 +339,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           float v2[32];
           if constexpr (kEpi == kEpiDAct) {
             // dZ = dA * GELU'(z), GELU'(z) in the output's layout; row sums -> bias gradient
-            if constexpr (kOutT) {
-              const uint16_t* gp = ep.aux + static_cast<int64_t>(n0) * ep.ldaux + m;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= bf16_to_f32(__ldg(gp + static_cast<int64_t>(i) * ep.ldaux));
-            } else {
+            // GELU'(z) is stored feature-major (m x n) whatever D's layout: 64 contiguous bytes per row
+            {
               const uint4* gp = reinterpret_cast<const uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0);
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
@@ -387,8 +384,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           __syncwarp();
           // stage a 32 x 32 bf16 tile: feature-major -> 64B-swizzled rows of this lane;
           // token-major (kOutT) -> transposed, row n holds the 32 features of this warp
-          auto stage = [&](uint8_t* buf, const float(&x)[32]) {
-            if constexpr (kOutT) {
+          auto stage = [&](uint8_t* buf, const float(&x)[32], bool transposed) {
+            if (transposed) {
               uint16_t* b16 = reinterpret_cast<uint16_t*>(buf);
 #pragma unroll
               for (int i = 0; i < 32; ++i) b16[i * 32 + lane] = f32_to_bf16(x[i]);
@@ -400,14 +397,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                pack_bf16x2(x[8 * c + 4], x[8 * c + 5]), pack_bf16x2(x[8 * c + 6], x[8 * c + 7]));
             }
           };
-          stage(zb, v);
-          if constexpr (kTwo) stage(stg + 2048, v2);
+          // AUX of the training epilogue (GELU'(z)) is always feature-major; otherwise AUX follows D
+          constexpr bool kAuxT = kOutT && kEpi != kEpiGeluGrad;
+          stage(zb, v, kOutT);
+          if constexpr (kTwo) stage(stg + 2048, v2, kAuxT);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            const int cx = kOutT ? m_w : n0, cy = kOutT ? n0 : m_w;
-            tma_store_2d(&tmD, zb, cx, cy);
-            if constexpr (kTwo) tma_store_2d(&tmX, stg + 2048, cx, cy);
+            tma_store_2d(&tmD, zb, kOutT ? m_w : n0, kOutT ? n0 : m_w);
+            if constexpr (kTwo) tma_store_2d(&tmX, stg + 2048, kAuxT ? m_w : n0, kAuxT ? n0 : m_w);
             bulk_commit();
           }
           sbuf ^= 1;
@@ -545,7 +543,7 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
               S24_ERR_UNSUPPORTED, "output rows must be 16-byte aligned");
   S24_REQUIRE(epilogue >= S24_EPI_STORE && epilogue <= S24_EPI_DGELU, S24_ERR_ARG, "bad epilogue");
   if (epilogue != S24_EPI_STORE)
-    S24_REQUIRE(aux != nullptr && ldaux >= (d_t ? m : n) && ldaux % 8 == 0 &&
+    S24_REQUIRE(aux != nullptr && ldaux >= ((d_t && epilogue == S24_EPI_GELU_AUX) ? m : n) && ldaux % 8 == 0 &&
                     (reinterpret_cast<uintptr_t>(aux) & 15) == 0,
                 S24_ERR_ARG, "this epilogue needs a 16-byte aligned aux tensor");
   S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
@@ -561,8 +559,9 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   } else {
     if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapBf16Sw64)) return rc;
   }
+  const bool aux_t = d_t && epilogue == S24_EPI_GELU_AUX;  // GELU'(z) (GRAD / DGELU) stays m x n
   if (epilogue == S24_EPI_GELU_AUX || epilogue == S24_EPI_GELU_GRAD) {
-    if (d_t) {
+    if (aux_t) {
       if (int rc = make_map(&mx, aux, m, n, ldaux, 32, 32, kMapBf16Plain)) return rc;
     } else {
       if (int rc = make_map(&mx, aux, n, m, ldaux, 32, 32, kMapBf16Sw64)) return rc;

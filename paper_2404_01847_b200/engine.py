@@ -136,7 +136,7 @@ class FwdState:
     z: torch.Tensor | None  # (N, r_in) pre-activation (None on the fused training path)
     a: torch.Tensor  # (N, d_ff)
     y: torch.Tensor  # (N, d)
-    g: torch.Tensor | None = None  # (N, d_ff) GELU'(z), fused training path only
+    g: torch.Tensor | None = None  # (d_ff, N) GELU'(z), feature-major, fused training path only
 
 
 def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor | None, w2: CompressedOperand,
@@ -158,7 +158,7 @@ def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor 
     a = torch.empty((n, d_ff), dtype=torch.bfloat16, device=dev)
     y = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
     if fused and act == "gelu":
-        g = torch.empty((n, d_ff), dtype=torch.bfloat16, device=dev)
+        g = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)  # read row-wise by GEMM3's epilogue
         spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, a, bias_in, tag="k3_spmm_fwd_in",
              epi=C.EPI_GELU_GRAD, aux=g, out_t=True)
         spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, a, False, n, y, tag="k3_spmm_fwd_out", out_t=True)

@@ -125,8 +125,9 @@ def test_sparse_gemm_token_major_output_and_epilogues(m, k, n, epi):
         spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, bias, out_t=True)
         assert normwise_rel(out.float().cpu(), (ref + bias.float()).cpu()) < 1e-2
     elif epi == "gelu_grad":
-        g = torch.empty_like(out)
+        g = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")  # GELU'(z) stays feature-major
         spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, None, epi=C.EPI_GELU_GRAD, aux=g, out_t=True)
+        g = g.t()
         zr = ref.double()
         cdf = 0.5 * (1 + torch.erf(zr / 2 ** 0.5))
         assert normwise_rel(out.float().cpu(), (zr * cdf).cpu()) < 1e-2
@@ -135,7 +136,8 @@ def test_sparse_gemm_token_major_output_and_epilogues(m, k, n, epi):
     else:
         gin = torch.rand(n, m, device="cuda").bfloat16()
         db = torch.zeros(m, dtype=torch.float32, device="cuda")
-        spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, None, epi=C.EPI_DGELU, aux=gin, dbias=db, out_t=True)
+        gfm = gin.t().contiguous()  # feature-major GELU'(z) input
+        spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, None, epi=C.EPI_DGELU, aux=gfm, dbias=db, out_t=True)
         dz = ref * gin.float()
         assert normwise_rel(out.float().cpu(), dz.cpu()) < 1e-2
         assert normwise_rel(db.cpu(), dz.sum(0).cpu()) < 1e-3
