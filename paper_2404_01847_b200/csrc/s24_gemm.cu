@@ -54,6 +54,7 @@ struct EpiParams {
 
 struct GemmShape {
   int m, n, k;  // k logical
+  int ksplit;   // K chunks per output tile (dW split-K, reduced with TMA add); 1 = no split
 };
 
 __constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
@@ -124,8 +125,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t rank = kCG == 2 ? cluster_rank() : 0;
   const int num_m = shp.m / (128 * kCG);
   const int num_n = (shp.n + kBN - 1) / kBN;
-  const int num_tiles = num_m * num_n;
-  const int num_kb = shp.k / C::BK;
+  const int num_tiles = num_m * num_n * shp.ksplit;  // work units: (output tile, K chunk)
+  const int num_kb = shp.k / C::BK / shp.ksplit;        // k-blocks per unit
   const int cluster_id = blockIdx.x / kCG, num_clusters = gridDim.x / kCG;
 
   if (warp == 0 && lane == 0) {
@@ -160,10 +161,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, mb, nb);
+        tile_coords(tile / shp.ksplit, num_m, num_n, mb, nb);
+        const int kb_base = (tile % shp.ksplit) * num_kb;
         const int m0 = mb * 128 * kCG + 128 * rank;      // this CTA's A rows
         const int nb0 = nb * kBN + C::BN_CTA * rank;      // this CTA's B rows (N split)
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kbi = 0; kbi < num_kb; ++kbi) {
+          const int kb = kb_base + kbi;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + C::A_BYTES;
@@ -261,7 +264,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t acc_phase = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
       int mb, nb;
-      tile_coords(tile, num_m, num_n, mb, nb);
+      tile_coords(tile / shp.ksplit, num_m, num_n, mb, nb);
+      const bool first_chunk = (tile % shp.ksplit) == 0;
       const int m_w = mb * 128 * kCG + 128 * rank + 32 * q;  // first row of this warp
       const int m = m_w + lane;
       const int n_base = nb * kBN;
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         if constexpr (kEpi == kEpiDw) {
-          if (ep.idx != nullptr) {
+          if (ep.idx != nullptr && first_chunk) {  // the decay term is added by one K chunk only
             const uint2 ib =
                 *reinterpret_cast<const uint2*>(ep.idx + static_cast<int64_t>(m >> 2) * (shp.n >> 2) + (n0 >> 2));
             const uint32_t iw[2] = {ib.x, ib.y};
@@ -331,7 +335,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmD, stg, n0, m_w);
+            if (shp.ksplit > 1) tma_reduce_add_2d(&tmD, stg, n0, m_w);
+            else tma_store_2d(&tmD, stg, n0, m_w);
             bulk_commit();
           }
         } else {
@@ -503,7 +508,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_done = true;
   }
-  const int tiles = (shp.m / (128 * kCG)) * ((shp.n + kBN - 1) / kBN);
+  const int tiles = (shp.m / (128 * kCG)) * ((shp.n + kBN - 1) / kBN) * shp.ksplit;
   const int clusters = tiles < num_sms() / kCG ? tiles : num_sms() / kCG;
   if (clusters <= 0) return S24_OK;
   cudaLaunchConfig_t cfg = {};
@@ -577,7 +582,7 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     S24_REQUIRE(ldb >= k, S24_ERR_SHAPE, "ldb < k");
     if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k)};
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 1};
   EpiParams ep{d, ldd, bias, aux, ldaux, dbias, nullptr, 0, nullptr, 0.0f};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define S24_SP(BMN, BNV, CG, EPI)                                                                          \
@@ -639,9 +644,31 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   me = mb;  // unused by the dense kernels
   CUtensorMap md;
   if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapF32Sw128)) return rc;
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k)};
-  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, w, w_dtype, idx, lambda_w};
+  // split K so the (tile, K chunk) units fill whole waves of CTA pairs; chunks are
+  // reduced in fp32 with TMA add-reduce stores into the zeroed output
+  const int clusters = num_sms() / (pair ? 2 : 1);
+  const int tiles = static_cast<int>((m / (pair ? 256 : 128)) * (n / BN));
+  const int num_kb = static_cast<int>(k / 64);
+  int ksplit = 1;
+  if (!getenv("S24_DETERMINISTIC")) {
+    double best = static_cast<double>(tiles) / (((tiles + clusters - 1) / clusters) * clusters);
+    for (int s = 2; s <= 8 && best < 0.95; ++s) {
+      if (num_kb % s != 0 || num_kb / s < 8) continue;
+      const int units = tiles * s;
+      const double eff = static_cast<double>(units) / (((units + clusters - 1) / clusters) * clusters);
+      if (eff > best + 0.02) {
+        best = eff;
+        ksplit = s;
+      }
+    }
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (ksplit > 1) {
+    cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
+    S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+  }
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), ksplit};
+  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, w, w_dtype, idx, lambda_w};
 #define S24_DW(AMN, BMN, BNV, CG)                                                                      \
   return launch_gemm<false, AMN, BMN, BNV, stages_for<Cfg<false, AMN, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
                      kEpiDw>(ma, mb, me, md, md, shp, ep, st)
