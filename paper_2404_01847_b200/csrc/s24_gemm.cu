@@ -275,8 +275,46 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if constexpr (kEpi == kEpiStore || kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad) {
         if (ep.bias != nullptr) bias_v = bf16_to_f32(ep.bias[m]);
       }
+      // global inputs of the epilogue (GELU'(z) for dGELU; W + mask indices for the
+      // decay) are prefetched one chunk ahead so their latency hides behind the
+      // TMEM load and the math of the current chunk
+      constexpr bool kPre = kEpi == kEpiDAct || kEpi == kEpiDw;
+      constexpr int kPreVec = kEpi == kEpiDw ? 8 : 4;
+      uint4 pre[kPreVec];
+      uint2 pre_idx = make_uint2(0, 0);
+      const bool decay = kEpi == kEpiDw && ep.idx != nullptr && first_chunk;
+      auto prefetch = [&](int cc) {
+        const int n0p = n_base + 32 * cc;
+        if (cc >= kBN / 32 || n0p >= shp.n) return;
+        if constexpr (kEpi == kEpiDAct) {
+          const uint4* gp = reinterpret_cast<const uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0p);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) pre[u] = __ldg(gp + u);
+        } else if constexpr (kEpi == kEpiDw) {
+          if (!decay) return;
+          pre_idx = __ldg(reinterpret_cast<const uint2*>(ep.idx + static_cast<int64_t>(m >> 2) * (shp.n >> 2) +
+                                                         (n0p >> 2)));
+          if (ep.w_dtype == S24_BF16) {
+            const uint4* wp = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(ep.w) +
+                                                             static_cast<int64_t>(m) * shp.n + n0p);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pre[u] = __ldg(wp + u);
+          } else {
+            const uint4* wp = reinterpret_cast<const uint4*>(static_cast<const float*>(ep.w) +
+                                                             static_cast<int64_t>(m) * shp.n + n0p);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) pre[u] = __ldg(wp + u);
+          }
+        }
+      };
+      if constexpr (kPre) prefetch(h);
 #pragma unroll 1
       for (int cc = h; cc < kBN / 32; cc += 2) {
+        uint4 cur[kPreVec];
+        uint2 cur_idx = pre_idx;
+#pragma unroll
+        for (int u = 0; u < kPreVec; ++u) cur[u] = pre[u];
+        if constexpr (kPre) prefetch(cc + 2);
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + 32 * cc, r);
         tmem_ld_wait();
@@ -286,18 +324,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         if constexpr (kEpi == kEpiDw) {
-          if (ep.idx != nullptr && first_chunk) {  // the decay term is added by one K chunk only
-            const uint2 ib =
-                *reinterpret_cast<const uint2*>(ep.idx + static_cast<int64_t>(m >> 2) * (shp.n >> 2) + (n0 >> 2));
-            const uint32_t iw[2] = {ib.x, ib.y};
+          if (decay) {  // the decay term lam (1 - M) W is added by one K chunk only
+            const uint32_t iw[2] = {cur_idx.x, cur_idx.y};
             float wv[32];
             if (ep.w_dtype == S24_BF16) {
-              const uint4* wp = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(ep.w) +
-                                                               static_cast<int64_t>(m) * shp.n + n0);
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                const uint4 x = __ldg(wp + u);
-                const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+                const uint32_t xs[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                   wv[8 * u + 2 * t] = __uint_as_float(xs[t] << 16);
@@ -305,15 +338,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
               }
             } else {
-              const float4* wp = reinterpret_cast<const float4*>(static_cast<const float*>(ep.w) +
-                                                                 static_cast<int64_t>(m) * shp.n + n0);
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
-                const float4 x = __ldg(wp + u);
-                wv[4 * u] = x.x;
-                wv[4 * u + 1] = x.y;
-                wv[4 * u + 2] = x.z;
-                wv[4 * u + 3] = x.w;
+                wv[4 * u] = __uint_as_float(cur[u].x);
+                wv[4 * u + 1] = __uint_as_float(cur[u].y);
+                wv[4 * u + 2] = __uint_as_float(cur[u].z);
+                wv[4 * u + 3] = __uint_as_float(cur[u].w);
               }
             }
 #pragma unroll
@@ -344,13 +374,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           float v2[32];
           if constexpr (kEpi == kEpiDAct) {
             // dZ = dA * GELU'(z), GELU'(z) in the output's layout; row sums -> bias gradient
-            // GELU'(z) is stored feature-major (m x n) whatever D's layout: 64 contiguous bytes per row
+            // GELU'(z) is stored feature-major (m x n) whatever D's layout: 64 contiguous bytes
+            // per row, prefetched into cur[] one chunk ahead
             {
-              const uint4* gp = reinterpret_cast<const uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0);
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                const uint4 x = __ldg(gp + u);
-                const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+                const uint32_t xs[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                   v[8 * u + 2 * t] *= __uint_as_float(xs[t] << 16);
