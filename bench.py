@@ -229,7 +229,9 @@ class SparseStep:
         self.E, self.torch = E, torch
         self.w_in, self.bias, self.w2, self.act, self.world, self.pg = w_in, bias, w2, act, world, pg
         dev = w_in.device
-        self.op_in = E.CompressedOperand.empty(w_in.shape[0], w_in.shape[1], dev)
+        # gated layers: first weight compressed u/v-interleaved for the fused gate epilogues
+        self.op_in = E.CompressedOperand.empty(w_in.shape[0], w_in.shape[1], dev,
+                                               perm_ff=w2.shape[1] if act in E.GATED else 0)
         self.op_out = E.CompressedOperand.empty(w2.shape[0], w2.shape[1], dev)
         # one flat fp32 gradient bucket [dW_in | dbias_in | dW2] -> one all-reduce per step
         n_in, n_b, n_2 = w_in.numel(), w_in.shape[0], w2.numel()
@@ -238,8 +240,8 @@ class SparseStep:
         self.dbias = self.bucket[n_in:n_in + n_b]
         self.dw2 = self.bucket[n_in + n_b:].view(w2.shape)
         self.t = 0
-        # our kernel launches per step: K1 or K2 x2, fwd 2 (GELU fused) or 3, bwd 4 (GELU' fused) or 5
-        self.launches_per_step = 2 + (2 if act == "gelu" else 3) + (4 if act == "gelu" else 5)
+        # our kernel launches per step: K1 or K2 x2, fwd 2 sparse GEMMs, bwd 2 sparse + 2 dW GEMMs
+        self.launches_per_step = 2 + 2 + 4  # activations fused into the GEMM epilogues
 
     def __call__(self, x, dy):
         E = self.E

@@ -73,6 +73,13 @@ extern "C" {
 #define S24_EPI_GELU_GRAD 2  /* D = gelu(z); AUX = gelu'(z), z = acc + bias[m] (train fwd GEMM1) */
 #define S24_EPI_DGELU 3      /* D = acc * AUX (AUX = gelu'(z) input); dbias[m] += sum_n D[m, n]
                                 (train bwd GEMM3: activation backward + bias gradient fused)    */
+/* gated layers (GEGLU / SwiGLU), first weight compressed u/v-interleaved (gate_ff = d_ff, see
+ * s24_search_compress): GEMM1 writes A = act(u) * v (n x d_ff, token-major) and AUX = v act'(u),
+ * AUX2 = act(u) (d_ff x n, feature-major); GEMM3 (m = d_ff) reads AUX/AUX2 and writes
+ * dZ = [dA AUX | dA AUX2] in the interleaved order (n x 2 d_ff) plus dbias ([b; c] order). */
+#define S24_EPI_GEGLU_GRAD 4
+#define S24_EPI_SWIGLU_GRAD 5
+#define S24_EPI_DGATED 6
 
 const char* s24_last_error_string(void);
 int s24_abi_version(void);
@@ -90,15 +97,20 @@ int s24_transposable_search(const void* w, int dtype, int64_t rows, int64_t cols
 /* K1 fused: search + compress both orientations in one pass over W.
  * Replaces transposable_search_conv + compress (spmm.py:92-106) +
  * FFNMasks.plans/_GatherPlan (gated_ffn.py:131-188).  Any of fwd_vals,
- * fwd_e, bwd_vals, bwd_e may be NULL; E outputs need rows, cols % 128 == 0. */
+ * fwd_e, bwd_vals, bwd_e may be NULL; E outputs need rows, cols % 128 == 0.
+ * perm_ff > 0 (gated W_in = [u; v], rows = 2 perm_ff): every output (idx, values, E)
+ * is produced for the u/v-interleaved row order p -> (p%32 < 16 ? u row 16(p/32) + p%32
+ * : v row 16(p/32) + p%32 - 16); 4x4 blocks never straddle u/v, so the masks are the
+ * reference's masks with block rows permuted. */
 int s24_search_compress(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* idx, uint16_t* fwd_vals,
-                        uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e, void* stream);
+                        uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e, int64_t perm_ff, void* stream);
 
 /* ---- K2: per-step prune / compress with a cached mask ----------------------
  * Replaces _GatherPlan.product's gather `w.ravel()[take]` (gated_ffn.py:159-162)
  * for both orientations (in_fwd/in_bwd, out_fwd/out_bwd). */
 int s24_prune_compress(const void* w, int dtype, int64_t rows, int64_t cols, const uint8_t* idx,
-                       uint16_t* fwd_vals, uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e, void* stream);
+                       uint16_t* fwd_vals, uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e, int64_t perm_ff,
+                       void* stream);
 
 /* ---- format conversions (parity export / TransposableMask API) ------------ */
 /* idx -> full 0/1 mask, uint8 rows x cols (TransposableMask.bits, sparsity.py:270-271) */
@@ -126,20 +138,23 @@ int s24_e_to_flat(const uint8_t* e, int64_t m, int64_t k, uint8_t* meta, void* s
  * always m x n (feature-major, ldaux >= n): it is only read back row-wise by the
  * DGELU epilogue.
  * bias (bf16, m) may be NULL.  dbias (fp32, m, zeroed by the caller) is used by
- * S24_EPI_DGELU only.  m % 128 == 0, k % 128 == 0, n % 32 == 0. */
+ * S24_EPI_DGELU / S24_EPI_DGATED.  aux2 / gate_ff: gated epilogues only (gate_ff = d_ff).
+ * m % 128 == 0, k % 128 == 0, n % 32 == 0. */
 int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b, int b_mn,
              int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias, int epilogue, uint16_t* aux,
-             int64_t ldaux, float* dbias, int d_t, void* stream);
+             int64_t ldaux, uint16_t* aux2, float* dbias, int d_t, int64_t gate_ff, void* stream);
 
 /* ---- K5: dense tcgen05 dW GEMM with fused masked decay ---------------------
  * D[m, n] (fp32, ldd) = sum_k A[m, k] B[n, k] + lambda_w * (1 - M[m, n]) * W[m, n]
  * Replaces _grad_weight(mvue=False) (gated_ffn.py:367-371) followed by
  * masked_decay_gradient (optim.py:105-114, applied at trainer.py:439-441).
  * a_mn = 0 -> A stored m x k, 1 -> k x m; b_mn likewise (n x k / k x n).
- * idx/w may be NULL (no decay).  m % 128 == 0, n % 256 == 0 (or % 128), k % 64 == 0. */
+ * idx/w may be NULL (no decay).  gate_ff > 0: A's rows (m = 2 gate_ff) are in the gated
+ * u/v-interleaved order (idx too); D rows and the W rows read for the decay are in [u; v]
+ * order.  m % 128 == 0, n % 256 == 0 (or % 128), k % 64 == 0. */
 int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int b_mn, int64_t ldb, int64_t m,
                 int64_t n, int64_t k, float* d, int64_t ldd, const void* w, int w_dtype, const uint8_t* idx,
-                float lambda_w, void* stream);
+                float lambda_w, int64_t gate_ff, void* stream);
 
 /* ---- K6/K7: fused (gated) activation, token-major ----------------------------
  * Z is n tokens x r_in (r_in = 2r gated, = r plain), row pitch ldz; A is n x r.

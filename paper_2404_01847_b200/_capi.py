@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "libs24b200.so")
 S24_OK, S24_ERR_SHAPE, S24_ERR_FORMAT, S24_ERR_UNSUPPORTED, S24_ERR_CUDA, S24_ERR_ARG = range(6)
 S24_BF16, S24_F32, S24_F64 = 0, 1, 2
 ACT_RELU, ACT_GELU, ACT_GEGLU, ACT_SWIGLU = 0, 1, 2, 3
-EPI_STORE, EPI_GELU_AUX, EPI_GELU_GRAD, EPI_DGELU = 0, 1, 2, 3
+EPI_STORE, EPI_GELU_AUX, EPI_GELU_GRAD, EPI_DGELU, EPI_GEGLU_GRAD, EPI_SWIGLU_GRAD, EPI_DGATED = range(7)
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -34,14 +34,14 @@ SIGNATURES = {
     "s24_abi_version": [],
     "s24_device_check": [],
     "s24_transposable_search": [_P, _I, _I64, _I64, _P, _P],
-    "s24_search_compress": [_P, _I, _I64, _I64, _P, _P, _P, _P, _P, _P],
-    "s24_prune_compress": [_P, _I, _I64, _I64, _P, _P, _P, _P, _P, _P],
+    "s24_search_compress": [_P, _I, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P],
+    "s24_prune_compress": [_P, _I, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P],
     "s24_idx_to_bits": [_P, _I64, _I64, _P, _P],
     "s24_bits_to_idx": [_P, _I64, _I64, _P, _P, _P],
     "s24_meta_flat": [_P, _I64, _I64, _P, _P, _P],
     "s24_e_to_flat": [_P, _I64, _I64, _P, _P],
-    "s24_spmm": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _I64, _P, _I, _P],
-    "s24_gemm_dw": [_P, _I, _I64, _P, _I, _I64, _I64, _I64, _I64, _P, _I64, _P, _I, _P, _F, _P],
+    "s24_spmm": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _I64, _P, _P, _I, _I64, _P],
+    "s24_gemm_dw": [_P, _I, _I64, _P, _I, _I64, _I64, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _P],
     "s24_act_fwd": [_P, _I64, _I64, _I64, _I, _P, _I64, _P],
     "s24_act_bwd": [_P, _I64, _P, _I64, _I64, _I64, _I, _P, _I64, _P, _P],
     "s24_masked_decay": [_P, _P, _I, _P, _I64, _I64, _F, _P],

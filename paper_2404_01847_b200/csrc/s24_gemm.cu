@@ -37,7 +37,12 @@ constexpr int kGroupM = 8;  // M tiles per raster group (L2 reuse of the B panel
 
 // epilogues: plain store (+bias); Z and GELU(Z); GELU(Z) and GELU'(Z) (training forward);
 // dZ = acc * GELU'(Z) with bias-gradient row sums (training backward); dW fp32 + masked decay
-enum Epi : int { kEpiStore = 0, kEpiGeluAux = 1, kEpiDw = 2, kEpiGeluGrad = 3, kEpiDAct = 4 };
+// gated (GEGLU / SwiGLU) training epilogues on the u/v-interleaved first weight:
+// kEpiGatedGrad: A = act(u) * v (token-major) + AUX = v * act'(u), AUX2 = act(u) (feature-major)
+// kEpiDGated:    dZ_u = dA * AUX, dZ_v = dA * AUX2 into the interleaved token-major dZ, bias grads
+enum Epi : int {
+  kEpiStore = 0, kEpiGeluAux = 1, kEpiDw = 2, kEpiGeluGrad = 3, kEpiDAct = 4, kEpiGatedGrad = 5, kEpiDGated = 6
+};
 
 struct EpiParams {
   void* d;
@@ -45,7 +50,10 @@ struct EpiParams {
   const uint16_t* bias;
   uint16_t* aux;     // second output (kEpiGeluAux, kEpiGeluGrad) or GELU'(Z) input (kEpiDAct)
   int64_t ldaux;
-  float* dbias;      // kEpiDAct: bias-gradient accumulator (zeroed by the caller)
+  float* dbias;      // kEpiDAct / kEpiDGated: bias-gradient accumulator (zeroed by the caller)
+  uint16_t* aux2;    // kEpiGatedGrad output / kEpiDGated input (same pitch as aux)
+  int act;           // S24_ACT_GEGLU or S24_ACT_SWIGLU for the gated epilogues
+  int64_t gate_ff;   // d_ff of the u/v interleave (gated epilogues, dW row remap); 0 = none
   const void* w;
   int w_dtype;
   const uint8_t* idx;
@@ -58,6 +66,25 @@ struct GemmShape {
 };
 
 __constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
+
+// interleaved row p of the gated first weight -> row of [u; v] (see s24_mask.cu)
+__device__ __forceinline__ int gate_row_dev(int p, int64_t ff) {
+  return (p & 31) < 16 ? 16 * (p >> 5) + (p & 31) : static_cast<int>(ff) + 16 * (p >> 5) + (p & 31) - 16;
+}
+
+template <bool kSilu>
+__device__ __forceinline__ void gate_act(float u, float& a, float& da) {
+  if constexpr (kSilu) {
+    const float sg = 1.0f / (1.0f + __expf(-u));
+    a = u * sg;
+    da = sg * (1.0f + u * (1.0f - sg));
+  } else {
+    float e;
+    const float cdf = 0.5f * (1.0f + erf_fast(u * 0.70710678118654752f, e));
+    a = u * cdf;
+    da = fmaf(u * 0.39894228040143268f, e, cdf);
+  }
+}
 
 // kCG = CTAs per MMA (1: M = 128, 2: CTA pair, M = 256, B split along N).
 // Pipeline depth that fits next to the epilogue staging area.
@@ -110,7 +137,8 @@ template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmD,
-                const __grid_constant__ CUtensorMap tmX, GemmShape shp, EpiParams ep) {
+                const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, GemmShape shp,
+                EpiParams ep) {
   using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -134,7 +162,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch(&tmB);
     tma_prefetch(&tmD);
     if constexpr (kSparse) tma_prefetch(&tmE);
-    if constexpr (kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad) tma_prefetch(&tmX);
+    if constexpr (kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad || kEpi == kEpiGatedGrad) tma_prefetch(&tmX);
+    if constexpr (kEpi == kEpiGatedGrad) tma_prefetch(&tmY);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -271,37 +300,46 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int n_base = nb * kBN;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      float bias_v = 0.0f;  // bias (forward epilogues) or running bias-gradient partial (kEpiDAct)
+      float bias_v = 0.0f;   // bias (forward epilogues) or running bias-gradient partial (backward)
+      float bias_v2 = 0.0f;  // second bias-gradient partial (kEpiDGated: the v half)
       if constexpr (kEpi == kEpiStore || kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad) {
         if (ep.bias != nullptr) bias_v = bf16_to_f32(ep.bias[m]);
+      } else if constexpr (kEpi == kEpiGatedGrad) {
+        if (ep.bias != nullptr) bias_v = bf16_to_f32(ep.bias[gate_row_dev(m, ep.gate_ff)]);
       }
       // global inputs of the epilogue (GELU'(z) for dGELU; W + mask indices for the
       // decay) are prefetched one chunk ahead so their latency hides behind the
       // TMEM load and the math of the current chunk
-      constexpr bool kPre = kEpi == kEpiDAct || kEpi == kEpiDw;
-      constexpr int kPreVec = kEpi == kEpiDw ? 8 : 4;
+      constexpr bool kPre = kEpi == kEpiDAct || kEpi == kEpiDw || kEpi == kEpiDGated;
+      constexpr int kPreVec = (kEpi == kEpiDw || kEpi == kEpiDGated) ? 8 : 4;
+      const int w_row = (kEpi == kEpiDw && ep.gate_ff > 0) ? gate_row_dev(m, ep.gate_ff) : m;
       uint4 pre[kPreVec];
       uint2 pre_idx = make_uint2(0, 0);
       const bool decay = kEpi == kEpiDw && ep.idx != nullptr && first_chunk;
       auto prefetch = [&](int cc) {
         const int n0p = n_base + 32 * cc;
         if (cc >= kBN / 32 || n0p >= shp.n) return;
-        if constexpr (kEpi == kEpiDAct) {
+        if constexpr (kEpi == kEpiDAct || kEpi == kEpiDGated) {
           const uint4* gp = reinterpret_cast<const uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0p);
 #pragma unroll
           for (int u = 0; u < 4; ++u) pre[u] = __ldg(gp + u);
+          if constexpr (kEpi == kEpiDGated) {
+            const uint4* gp2 = reinterpret_cast<const uint4*>(ep.aux2 + static_cast<int64_t>(m) * ep.ldaux + n0p);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pre[4 + u] = __ldg(gp2 + u);
+          }
         } else if constexpr (kEpi == kEpiDw) {
           if (!decay) return;
           pre_idx = __ldg(reinterpret_cast<const uint2*>(ep.idx + static_cast<int64_t>(m >> 2) * (shp.n >> 2) +
                                                          (n0p >> 2)));
           if (ep.w_dtype == S24_BF16) {
             const uint4* wp = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(ep.w) +
-                                                             static_cast<int64_t>(m) * shp.n + n0p);
+                                                             static_cast<int64_t>(w_row) * shp.n + n0p);
 #pragma unroll
             for (int u = 0; u < 4; ++u) pre[u] = __ldg(wp + u);
           } else {
             const uint4* wp = reinterpret_cast<const uint4*>(static_cast<const float*>(ep.w) +
-                                                             static_cast<int64_t>(m) * shp.n + n0p);
+                                                             static_cast<int64_t>(w_row) * shp.n + n0p);
 #pragma unroll
             for (int u = 0; u < 8; ++u) pre[u] = __ldg(wp + u);
           }
@@ -365,8 +403,95 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            if (shp.ksplit > 1) tma_reduce_add_2d(&tmD, stg, n0, m_w);
-            else tma_store_2d(&tmD, stg, n0, m_w);
+            // two 16-row boxes: the gated first weight's rows go back to [u; v] order
+            const int y0 = ep.gate_ff > 0 ? gate_row_dev(m_w, ep.gate_ff) : m_w;
+            const int y1 = ep.gate_ff > 0 ? gate_row_dev(m_w + 16, ep.gate_ff) : m_w + 16;
+            if (shp.ksplit > 1) {
+              tma_reduce_add_2d(&tmD, stg, n0, y0);
+              tma_reduce_add_2d(&tmD, stg + 2048, n0, y1);
+            } else {
+              tma_store_2d(&tmD, stg, n0, y0);
+              tma_store_2d(&tmD, stg + 2048, n0, y1);
+            }
+            bulk_commit();
+          }
+        } else if constexpr (kEpi == kEpiGatedGrad) {
+          // rows: lanes 0-15 = u of features 16g+l, lanes 16-31 = the matching v rows.
+          // Swap half the tokens across the pair so every lane holds (u, v) of one
+          // feature for 16 tokens: lanes < 16 tokens 0..15, lanes >= 16 tokens 16..31.
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += bias_v;
+          const bool lo = lane < 16;
+          float uu[16], vv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float send = lo ? v[16 + i] : v[i];
+            const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+            uu[i] = lo ? v[i] : recv;
+            vv[i] = lo ? recv : v[16 + i];
+          }
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+          uint16_t* sa = reinterpret_cast<uint16_t*>(stg);          // A: [32 tokens][16 features]
+          uint16_t* s1 = reinterpret_cast<uint16_t*>(stg + 1024);   // AUX  v act'(u): [16 f][32 t]
+          uint16_t* s2 = reinterpret_cast<uint16_t*>(stg + 2048);   // AUX2 act(u):    [16 f][32 t]
+          const int f = lane & 15, t0 = lo ? 0 : 16;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float a, da;
+            if (ep.act == S24_ACT_SWIGLU) gate_act<true>(uu[i], a, da);
+            else gate_act<false>(uu[i], a, da);
+            sa[(t0 + i) * 16 + f] = f32_to_bf16(a * vv[i]);
+            s1[f * 32 + t0 + i] = f32_to_bf16(vv[i] * da);
+            s2[f * 32 + t0 + i] = f32_to_bf16(a);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int fg = m_w >> 1;  // first gate feature of this warp: 16 g, g = m_w / 32
+            tma_store_2d(&tmD, stg, fg, n0);
+            tma_store_2d(&tmX, stg + 1024, n0, fg);
+            tma_store_2d(&tmY, stg + 2048, n0, fg);
+            bulk_commit();
+          }
+        } else if constexpr (kEpi == kEpiDGated) {
+          // rows: gate features j; dZ_u = dA * v act'(u), dZ_v = dA * act(u) written into the
+          // interleaved token-major dZ: this warp's 32 features own the 64 columns [2 m_w, 2 m_w + 64)
+          float dz1[32], dz2[32];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t x1[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
+            const uint32_t x2[4] = {cur[4 + u].x, cur[4 + u].y, cur[4 + u].z, cur[4 + u].w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int i = 8 * u + 2 * t;
+              dz1[i] = v[i] * __uint_as_float(x1[t] << 16);
+              dz1[i + 1] = v[i + 1] * __uint_as_float(x1[t] & 0xFFFF0000u);
+              dz2[i] = v[i] * __uint_as_float(x2[t] << 16);
+              dz2[i + 1] = v[i + 1] * __uint_as_float(x2[t] & 0xFFFF0000u);
+            }
+          }
+          float r1 = 0.0f, r2 = 0.0f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            r1 += dz1[i];
+            r2 += dz2[i];
+          }
+          bias_v += r1;
+          bias_v2 += r2;
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+          uint16_t* sz = reinterpret_cast<uint16_t*>(stg);  // [32 tokens][64 interleaved columns]
+          const int c1 = lane < 16 ? lane : lane + 16;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            sz[i * 64 + c1] = f32_to_bf16(dz1[i]);
+            sz[i * 64 + c1 + 16] = f32_to_bf16(dz2[i]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmD, stg, 2 * m_w, n0);
             bulk_commit();
           }
         } else {
@@ -447,6 +572,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       if constexpr (kEpi == kEpiDAct) {
         if (ep.dbias != nullptr) atomicAdd(ep.dbias + m, bias_v);
+      } else if constexpr (kEpi == kEpiDGated) {
+        if (ep.dbias != nullptr) {  // [b; c] order: u half at j, v half at d_ff + j
+          atomicAdd(ep.dbias + m, bias_v);
+          atomicAdd(ep.dbias + ep.gate_ff + m, bias_v2);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -528,7 +658,8 @@ static int num_sms() {
 
 template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT = false>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& me, const CUtensorMap& md,
-                       const CUtensorMap& mx, const GemmShape& shp, const EpiParams& ep, cudaStream_t st) {
+                       const CUtensorMap& mx, const CUtensorMap& my, const GemmShape& shp, const EpiParams& ep,
+                       cudaStream_t st) {
   using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG>;
   auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi, kOutT>;
   static bool attr_done = false;  // per template instance
@@ -552,7 +683,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, md, mx, shp, ep);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, md, mx, my, shp, ep);
   S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
   return s24_check_launch("gemm");
 }
@@ -568,14 +699,27 @@ static int cg_override() {
 
 extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b,
                         int b_mn, int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias,
-                        int epilogue, uint16_t* aux, int64_t ldaux, float* dbias, int d_t, void* stream) {
+                        int epilogue, uint16_t* aux, int64_t ldaux, uint16_t* aux2, float* dbias, int d_t,
+                        int64_t gate_ff, void* stream) {
   S24_REQUIRE(a_vals && a_e && b && d, S24_ERR_ARG, "NULL operand");
   S24_REQUIRE(m % 128 == 0 && k % 128 == 0 && n % 32 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
               "sparse GEMM needs m %% 128 == 0, k %% 128 == 0, n %% 32 == 0 (got m=%lld k=%lld n=%lld)",
               (long long)m, (long long)k, (long long)n);
-  S24_REQUIRE(ldd >= (d_t ? m : n) && ldd % 8 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0,
+  S24_REQUIRE(epilogue >= S24_EPI_STORE && epilogue <= S24_EPI_DGATED, S24_ERR_ARG, "bad epilogue");
+  const bool gated_fwd = epilogue == S24_EPI_GEGLU_GRAD || epilogue == S24_EPI_SWIGLU_GRAD;
+  const bool gated_bwd = epilogue == S24_EPI_DGATED;
+  // logical width of the stored output: GEMM1 gated stores d_ff = m/2 gate features, GEMM3 gated
+  // stores the interleaved 2m columns of dZ
+  const int64_t d_cols = gated_fwd ? m / 2 : gated_bwd ? 2 * m : m;
+  S24_REQUIRE(ldd >= (d_t ? d_cols : n) && ldd % 8 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0,
               S24_ERR_UNSUPPORTED, "output rows must be 16-byte aligned");
-  S24_REQUIRE(epilogue >= S24_EPI_STORE && epilogue <= S24_EPI_DGELU, S24_ERR_ARG, "bad epilogue");
+  if (gated_fwd || gated_bwd) {
+    S24_REQUIRE(d_t == 1, S24_ERR_ARG, "gated epilogues store token-major outputs (d_t = 1)");
+    S24_REQUIRE(gate_ff == (gated_fwd ? m / 2 : m) && gate_ff % 16 == 0, S24_ERR_SHAPE,
+                "gated epilogue: gate_ff must be d_ff (%lld) and a multiple of 16", (long long)gate_ff);
+    S24_REQUIRE(aux2 != nullptr && (reinterpret_cast<uintptr_t>(aux2) & 15) == 0, S24_ERR_ARG,
+                "gated epilogues need a 16-byte aligned aux2 tensor");
+  }
   if (epilogue != S24_EPI_STORE)
     S24_REQUIRE(aux != nullptr && ldaux >= ((d_t && epilogue == S24_EPI_GELU_AUX) ? m : n) && ldaux % 8 == 0 &&
                     (reinterpret_cast<uintptr_t>(aux) & 15) == 0,
@@ -586,22 +730,33 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   CUtensorMap ma, mb, me;
   if (int rc = make_map(&ma, a_vals, k / 2, m, k / 2, 64, 128)) return rc;
   if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, kMapU64)) return rc;
-  CUtensorMap md, mx;
-  // D[m, n] feature-major (64B-swizzled staging) or D^T[n, m] token-major (d_t, transposed staging)
-  if (d_t) {
-    if (int rc = make_map(&md, d, m, n, ldd, 32, 32, kMapBf16Plain)) return rc;
+  CUtensorMap md, mx, my;
+  if (gated_fwd) {
+    // A: [n tokens][d_ff] boxes of 16 features x 32 tokens; AUX, AUX2: [d_ff][n] boxes of 32 x 16
+    if (int rc = make_map(&md, d, m / 2, n, ldd, 16, 32, kMapBf16Plain)) return rc;
+    if (int rc = make_map(&mx, aux, n, m / 2, ldaux, 32, 16, kMapBf16Plain)) return rc;
+    if (int rc = make_map(&my, aux2, n, m / 2, ldaux, 32, 16, kMapBf16Plain)) return rc;
+  } else if (gated_bwd) {
+    if (int rc = make_map(&md, d, 2 * m, n, ldd, 64, 32, kMapBf16Plain)) return rc;  // dZ interleaved
+    mx = my = md;
   } else {
-    if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapBf16Sw64)) return rc;
-  }
-  const bool aux_t = d_t && epilogue == S24_EPI_GELU_AUX;  // GELU'(z) (GRAD / DGELU) stays m x n
-  if (epilogue == S24_EPI_GELU_AUX || epilogue == S24_EPI_GELU_GRAD) {
-    if (aux_t) {
-      if (int rc = make_map(&mx, aux, m, n, ldaux, 32, 32, kMapBf16Plain)) return rc;
+    // D[m, n] feature-major (64B-swizzled staging) or D^T[n, m] token-major (d_t, transposed staging)
+    if (d_t) {
+      if (int rc = make_map(&md, d, m, n, ldd, 32, 32, kMapBf16Plain)) return rc;
     } else {
-      if (int rc = make_map(&mx, aux, n, m, ldaux, 32, 32, kMapBf16Sw64)) return rc;
+      if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapBf16Sw64)) return rc;
     }
-  } else {
-    mx = md;
+    const bool aux_t = d_t && epilogue == S24_EPI_GELU_AUX;  // GELU'(z) (GRAD / DGELU) stays m x n
+    if (epilogue == S24_EPI_GELU_AUX || epilogue == S24_EPI_GELU_GRAD) {
+      if (aux_t) {
+        if (int rc = make_map(&mx, aux, m, n, ldaux, 32, 32, kMapBf16Plain)) return rc;
+      } else {
+        if (int rc = make_map(&mx, aux, n, m, ldaux, 32, 32, kMapBf16Sw64)) return rc;
+      }
+    } else {
+      mx = md;
+    }
+    my = md;
   }
   const int bn_cta = pair ? BN2 / 2 : BN1;
   if (b_mn) {
@@ -612,19 +767,28 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 1};
-  EpiParams ep{d, ldd, bias, aux, ldaux, dbias, nullptr, 0, nullptr, 0.0f};
+  EpiParams ep{d,       ldd,
+               bias,    aux,
+               ldaux,   dbias,
+               aux2,    epilogue == S24_EPI_SWIGLU_GRAD ? S24_ACT_SWIGLU : S24_ACT_GEGLU,
+               gate_ff, nullptr,
+               0,       nullptr,
+               0.0f};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define S24_SP(BMN, BNV, CG, EPI)                                                                          \
   if (d_t)                                                                                                  \
     return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
-                       EPI, true>(ma, mb, me, md, mx, shp, ep, st);                                         \
+                       EPI, true>(ma, mb, me, md, mx, my, shp, ep, st);                                     \
   return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG,   \
-                     EPI, false>(ma, mb, me, md, mx, shp, ep, st)
+                     EPI, false>(ma, mb, me, md, mx, my, shp, ep, st)
 #define S24_SP_EPI(BMN, BNV, CG)                                              \
   switch (epilogue) {                                                           \
     case S24_EPI_GELU_AUX: S24_SP(BMN, BNV, CG, kEpiGeluAux);                   \
     case S24_EPI_GELU_GRAD: S24_SP(BMN, BNV, CG, kEpiGeluGrad);                 \
     case S24_EPI_DGELU: S24_SP(BMN, BNV, CG, kEpiDAct);                         \
+    case S24_EPI_GEGLU_GRAD:                                                    \
+    case S24_EPI_SWIGLU_GRAD: S24_SP(BMN, BNV, CG, kEpiGatedGrad);              \
+    case S24_EPI_DGATED: S24_SP(BMN, BNV, CG, kEpiDGated);                      \
     default: S24_SP(BMN, BNV, CG, kEpiStore);                                   \
   }
   if (pair) {
@@ -639,7 +803,9 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
 
 extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int b_mn, int64_t ldb,
                            int64_t m, int64_t n, int64_t k, float* d, int64_t ldd, const void* w, int w_dtype,
-                           const uint8_t* idx, float lambda_w, void* stream) {
+                           const uint8_t* idx, float lambda_w, int64_t gate_ff, void* stream) {
+  if (gate_ff > 0)
+    S24_REQUIRE(m == 2 * gate_ff && gate_ff % 16 == 0, S24_ERR_SHAPE, "gated dW: m must be 2 * d_ff");
   S24_REQUIRE(a && b && d, S24_ERR_ARG, "NULL operand");
   S24_REQUIRE(m % 128 == 0 && n % 128 == 0 && k % 64 == 0 && m > 0 && n > 0 && k > 0, S24_ERR_SHAPE,
               "dW GEMM needs m %% 128 == 0, n %% 128 == 0, k %% 64 == 0 (got m=%lld n=%lld k=%lld)", (long long)m,
@@ -672,7 +838,7 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   }
   me = mb;  // unused by the dense kernels
   CUtensorMap md;
-  if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapF32Sw128)) return rc;
+  if (int rc = make_map(&md, d, n, m, ldd, 32, 16, kMapF32Sw128)) return rc;  // 16-row store boxes
   // split K so the (tile, K chunk) units fill whole waves of CTA pairs; chunks are
   // reduced in fp32 with TMA add-reduce stores into the zeroed output
   const int clusters = num_sms() / (pair ? 2 : 1);
@@ -699,10 +865,10 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   }
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), ksplit};
-  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, w, w_dtype, idx, lambda_w};
+  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
 #define S24_DW(AMN, BMN, BNV, CG)                                                                      \
   return launch_gemm<false, AMN, BMN, BNV, stages_for<Cfg<false, AMN, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
-                     kEpiDw>(ma, mb, me, md, md, shp, ep, st)
+                     kEpiDw>(ma, mb, me, md, md, md, shp, ep, st)
   if (pair) {
     if (a_mn && b_mn) S24_DW(true, true, 256, 2);
     if (a_mn) S24_DW(true, false, 256, 2);

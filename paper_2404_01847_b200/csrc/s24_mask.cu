@@ -161,7 +161,18 @@ struct MaskArgs {
   uint8_t* fwd_e;          // E tiles of W
   uint16_t* bwd_vals;      // cols x rows/2
   uint8_t* bwd_e;          // E tiles of W^T
+  int64_t perm_ff;         // >0: gated u/v interleave (output row p reads input row gate_row(p))
 };
+
+// Gated first weight W_in = [u; v] (2 d_ff rows) is compressed in an interleaved
+// row order: output rows 32g..32g+15 are u rows 16g.., rows 32g+16..32g+31 the
+// matching v rows, so one 32-row epilogue warp of GEMM1 holds both halves of
+// 16 gate features.  4-row blocks never straddle u/v (16 % 4 == 0), so the
+// per-block masks are the reference's masks with block rows permuted.
+__host__ __device__ __forceinline__ int64_t gate_row(int64_t p, int64_t perm_ff) {
+  const int64_t g = p >> 5, t = p & 31;
+  return t < 16 ? 16 * g + t : perm_ff + 16 * g + (t - 16);
+}
 
 // kNarrow: bf16 rows that are only 8-byte aligned (cols % 8 == 4) load 4 elements at a time
 template <int kDType, bool kSearch, bool kNarrow>
@@ -193,6 +204,7 @@ __global__ void __launch_bounds__(kThreads) mask_tile_kernel(MaskArgs p) {
   // ---- load 4 rows x 16 columns ----
   T v[4][16];
   const T* w = static_cast<const T*>(p.w);
+  const int64_t in_row0 = p.perm_ff > 0 ? gate_row(grow0, p.perm_ff) : grow0;  // 4-row block stays contiguous
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
 #pragma unroll
@@ -200,12 +212,12 @@ __global__ void __launch_bounds__(kThreads) mask_tile_kernel(MaskArgs p) {
       const int64_t col = gcol0 + q * kVec;
       if (row_ok && col < p.cols) {
         if constexpr (kNarrow) {
-          const uint2 u = __ldg(reinterpret_cast<const uint2*>(w + (grow0 + i) * p.cols + col));
+          const uint2 u = __ldg(reinterpret_cast<const uint2*>(w + (in_row0 + i) * p.cols + col));
           const T* e = reinterpret_cast<const T*>(&u);
 #pragma unroll
           for (int j = 0; j < kVec; ++j) v[i][q * kVec + j] = e[j];
         } else {
-          const uint4 u = __ldg(reinterpret_cast<const uint4*>(w + (grow0 + i) * p.cols + col));
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(w + (in_row0 + i) * p.cols + col));
           const T* e = reinterpret_cast<const T*>(&u);
 #pragma unroll
           for (int j = 0; j < kVec; ++j) v[i][q * kVec + j] = e[j];
@@ -487,7 +499,7 @@ extern "C" int s24_transposable_search(const void* w, int dtype, int64_t rows, i
                                        void* stream) {
   if (int rc = check_w(w, dtype, rows, cols)) return rc;
   S24_REQUIRE(idx != nullptr, S24_ERR_ARG, "idx pointer is NULL");
-  MaskArgs a{w, rows, cols, idx, nullptr, nullptr, nullptr, nullptr, nullptr};
+  MaskArgs a{w, rows, cols, idx, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   return launch_mask(a, dtype, true, static_cast<cudaStream_t>(stream));
 }
 
@@ -499,23 +511,33 @@ static int check_compress_outputs(int64_t rows, int64_t cols, const void* fwd_e,
   return S24_OK;
 }
 
+static int check_perm(int64_t rows, int64_t perm_ff) {
+  if (perm_ff > 0)
+    S24_REQUIRE(rows == 2 * perm_ff && perm_ff % 16 == 0, S24_ERR_SHAPE,
+                "gated interleave needs rows == 2 * d_ff and d_ff %% 16 == 0 (rows=%lld d_ff=%lld)", (long long)rows,
+                (long long)perm_ff);
+  return S24_OK;
+}
+
 extern "C" int s24_search_compress(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* idx,
                                    uint16_t* fwd_vals, uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e,
-                                   void* stream) {
+                                   int64_t perm_ff, void* stream) {
+  if (int rc = check_perm(rows, perm_ff)) return rc;
   if (int rc = check_w(w, dtype, rows, cols)) return rc;
   S24_REQUIRE(idx != nullptr, S24_ERR_ARG, "idx pointer is NULL");
   if (int rc = check_compress_outputs(rows, cols, fwd_e, bwd_e)) return rc;
-  MaskArgs a{w, rows, cols, idx, nullptr, fwd_vals, fwd_e, bwd_vals, bwd_e};
+  MaskArgs a{w, rows, cols, idx, nullptr, fwd_vals, fwd_e, bwd_vals, bwd_e, perm_ff};
   return launch_mask(a, dtype, true, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int s24_prune_compress(const void* w, int dtype, int64_t rows, int64_t cols, const uint8_t* idx,
                                   uint16_t* fwd_vals, uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e,
-                                  void* stream) {
+                                  int64_t perm_ff, void* stream) {
+  if (int rc = check_perm(rows, perm_ff)) return rc;
   if (int rc = check_w(w, dtype, rows, cols)) return rc;
   S24_REQUIRE(idx != nullptr, S24_ERR_ARG, "idx pointer is NULL");
   if (int rc = check_compress_outputs(rows, cols, fwd_e, bwd_e)) return rc;
-  MaskArgs a{w, rows, cols, nullptr, idx, fwd_vals, fwd_e, bwd_vals, bwd_e};
+  MaskArgs a{w, rows, cols, nullptr, idx, fwd_vals, fwd_e, bwd_vals, bwd_e, perm_ff};
   return launch_mask(a, dtype, false, static_cast<cudaStream_t>(stream));
 }
 

@@ -58,18 +58,31 @@ class CompressedOperand:
     fwd_e: torch.Tensor  # E tiles for fwd_vals
     bwd_vals: torch.Tensor  # (cols, rows/2) bf16: A operand of W^T (bwd)
     bwd_e: torch.Tensor  # E tiles for bwd_vals
+    perm_ff: int = 0  # > 0: gated W_in = [u; v] stored u/v-interleaved (16-row groups), d_ff = perm_ff
 
     @classmethod
-    def empty(cls, rows: int, cols: int, device) -> "CompressedOperand":
+    def empty(cls, rows: int, cols: int, device, perm_ff: int = 0) -> "CompressedOperand":
         if rows % 128 or cols % 128:
             raise ShapeError(
                 f"2:4 tensor-core operands need both weight dims divisible by 128, got ({rows}, {cols})")
         e_bytes = (rows // 128) * (cols // 128) * 2048
         u8 = dict(dtype=torch.uint8, device=device)
         bf = dict(dtype=torch.bfloat16, device=device)
+        if perm_ff and (rows != 2 * perm_ff or perm_ff % 16):
+            raise ShapeError(f"gated interleave needs rows == 2 * d_ff and d_ff % 16 == 0, got {rows}, {perm_ff}")
         return cls(rows, cols, torch.empty((rows // 4, cols // 4), **u8),
                    torch.empty((rows, cols // 2), **bf), torch.empty(e_bytes, **u8),
-                   torch.empty((cols, rows // 2), **bf), torch.empty(e_bytes, **u8))
+                   torch.empty((cols, rows // 2), **bf), torch.empty(e_bytes, **u8), perm_ff)
+
+    def mask_idx(self) -> torch.Tensor:
+        """Pattern indices in the weight's own row order (undoing the gated interleave)."""
+        if not self.perm_ff:
+            return self.idx
+        p = torch.arange(0, self.rows, 4, device=self.idx.device)
+        orig = torch.where(p % 32 < 16, 16 * (p // 32) + p % 32, self.perm_ff + 16 * (p // 32) + p % 32 - 16)
+        out = torch.empty_like(self.idx)
+        out[orig // 4] = self.idx
+        return out
 
 
 def search_compress(w: torch.Tensor, op: CompressedOperand) -> None:
@@ -77,27 +90,28 @@ def search_compress(w: torch.Tensor, op: CompressedOperand) -> None:
     with TIMER("k1_search_compress"):
         C.call("s24_search_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),
                op.fwd_vals.data_ptr(), op.fwd_e.data_ptr(), op.bwd_vals.data_ptr(), op.bwd_e.data_ptr(),
-               C.stream_of(w))
+               op.perm_ff, C.stream_of(w))
 
 
 def compress_with_meta(w: torch.Tensor, op: CompressedOperand) -> None:
     """K2 with metadata: (re)build E tiles and values from a given mask (op.idx)."""
     C.call("s24_prune_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),
            op.fwd_vals.data_ptr(), op.fwd_e.data_ptr(), op.bwd_vals.data_ptr(), op.bwd_e.data_ptr(),
-           C.stream_of(w))
+           op.perm_ff, C.stream_of(w))
 
 
 def compress_values(w: torch.Tensor, op: CompressedOperand) -> None:
     """K2: per-step prune/compress of the current weight values (mask cached)."""
     with TIMER("k2_prune_compress"):
         C.call("s24_prune_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),
-               op.fwd_vals.data_ptr(), None, op.bwd_vals.data_ptr(), None, C.stream_of(w))
+               op.fwd_vals.data_ptr(), None, op.bwd_vals.data_ptr(), None, op.perm_ff, C.stream_of(w))
 
 
 def spmm(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b_mn: bool, n: int,
          out: torch.Tensor, bias: torch.Tensor | None = None, gelu_aux: torch.Tensor | None = None,
          tag: str = "k34_spmm", epi: int | None = None, aux: torch.Tensor | None = None,
-         dbias: torch.Tensor | None = None, out_t: bool = False) -> None:
+         dbias: torch.Tensor | None = None, out_t: bool = False, aux2: torch.Tensor | None = None,
+         gate_ff: int = 0) -> None:
     """D[m, n] = W~[m, k] (2:4) . B[n, k]^T, stored as out[m, n] (feature-major)
     or, with out_t, as out[n, m] (token-major); epilogues: EPI_STORE (+bias),
     EPI_GELU_AUX (out = z, aux = gelu(z)), EPI_GELU_GRAD (out = gelu(z),
@@ -109,18 +123,18 @@ def spmm(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b
     with TIMER(tag):
         C.call("s24_spmm", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), b.stride(0), n,
                out.data_ptr(), out.stride(0), C.ptr(bias), epi, C.ptr(aux), aux.stride(0) if aux is not None else 0,
-               C.ptr(dbias), int(out_t), C.stream_of(out))
+               C.ptr(aux2), C.ptr(dbias), int(out_t), gate_ff, C.stream_of(out))
 
 
 def gemm_dw(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, m: int, n: int, k: int,
             out: torch.Tensor, w: torch.Tensor | None = None, idx: torch.Tensor | None = None,
-            lam: float = 0.0, tag: str = "k5_gemm_dw") -> None:
+            lam: float = 0.0, tag: str = "k5_gemm_dw", gate_ff: int = 0) -> None:
     """out[m, n] fp32 = sum_k A[m, k] B[n, k] + lam (1 - M) W  (dense tcgen05)."""
     decay = idx is not None and lam != 0.0
     with TIMER(tag):
         C.call("s24_gemm_dw", a.data_ptr(), int(a_mn), a.stride(0), b.data_ptr(), int(b_mn), b.stride(0), m, n,
                k, out.data_ptr(), out.stride(0), C.ptr(w) if decay else None, C.dtype_code(w) if decay else 0,
-               C.ptr(idx) if decay else None, float(lam if decay else 0.0), C.stream_of(out))
+               C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, C.stream_of(out))
 
 
 def _rows(t: torch.Tensor) -> torch.Tensor:
@@ -136,7 +150,8 @@ class FwdState:
     z: torch.Tensor | None  # (N, r_in) pre-activation (None on the fused training path)
     a: torch.Tensor  # (N, d_ff)
     y: torch.Tensor  # (N, d)
-    g: torch.Tensor | None = None  # (d_ff, N) GELU'(z), feature-major, fused training path only
+    g: torch.Tensor | None = None  # (d_ff, N) GELU'(z) / gated v act'(u), feature-major, fused path only
+    g2: torch.Tensor | None = None  # (d_ff, N) gated act(u), fused gated path only
 
 
 def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor | None, w2: CompressedOperand,
@@ -157,6 +172,18 @@ def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor 
     x = _rows(x)
     a = torch.empty((n, d_ff), dtype=torch.bfloat16, device=dev)
     y = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
+    if fused and act in GATED:
+        if w_in.perm_ff != d_ff:
+            raise ShapeError("the fused gated path needs the first weight compressed u/v-interleaved (perm_ff = d_ff)")
+        g = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
+        g2 = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
+        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, a, bias_in, tag="k3_spmm_fwd_in",
+             epi=C.EPI_SWIGLU_GRAD if act == "swiglu" else C.EPI_GEGLU_GRAD, aux=g, aux2=g2, out_t=True,
+             gate_ff=d_ff)
+        spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, a, False, n, y, tag="k3_spmm_fwd_out", out_t=True)
+        return FwdState(x, None, a, y, g, g2)
+    if w_in.perm_ff:
+        raise ShapeError("an interleaved gated operand is only valid on the fused path")
     if fused and act == "gelu":
         g = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)  # read row-wise by GEMM3's epilogue
         spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, a, bias_in, tag="k3_spmm_fwd_in",
@@ -197,7 +224,13 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     dev = dy.device
     dy = _rows(dy)
     dz = torch.empty((n, r_in), dtype=torch.bfloat16, device=dev)
-    if st.g is not None:
+    gate_ff = w_in.perm_ff
+    if st.g2 is not None:
+        # gated: dZ_u = dA v act'(u), dZ_v = dA act(u) straight into the interleaved dZ, bias grads fused
+        dbias = torch.zeros(r_in, dtype=torch.float32, device=dev)
+        spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dy, False, n, dz, tag="k4_spmm_bwd_out", epi=C.EPI_DGATED,
+             aux=st.g, aux2=st.g2, dbias=dbias, out_t=True, gate_ff=d_ff)
+    elif st.g is not None:
         # dZ = (dY W2~) * GELU'(z) with the bias gradient reduced in the same epilogue
         dbias = torch.zeros(r_in, dtype=torch.float32, device=dev)
         spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dy, False, n, dz, tag="k4_spmm_bwd_out", epi=C.EPI_DGELU,
@@ -215,5 +248,6 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     dw2 = dw2_out if dw2_out is not None else torch.empty((d, d_ff), dtype=torch.float32, device=dev)
     gemm_dw(dy, True, st.a, True, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")
     dw_in = dw_in_out if dw_in_out is not None else torch.empty((r_in, d), dtype=torch.float32, device=dev)
-    gemm_dw(dz, True, st.x, True, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam, tag="k5_gemm_dw_in")
+    gemm_dw(dz, True, st.x, True, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam, tag="k5_gemm_dw_in",
+            gate_ff=gate_ff)
     return Grads(dx, dw_in, dbias, dw2)

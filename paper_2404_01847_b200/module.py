@@ -58,7 +58,7 @@ class SparseFFN(torch.nn.Module):
         self.refresh_period = refresh_period
         self.decay_lambda = decay_lambda
         self.sparse = True
-        self.op_in = E.CompressedOperand.empty(r_in, d, dev)
+        self.op_in = E.CompressedOperand.empty(r_in, d, dev, perm_ff=d_ff if act in E.GATED else 0)
         self.op_out = E.CompressedOperand.empty(d, d_ff, dev)
         self.steps_since_refresh = None  # None -> search on first use
         self.mask_searches = 0

@@ -146,3 +146,31 @@ def test_sparse_ffn_module_autograd_vs_oracle(act):
     for _ in range(40):
         mod(x)
     assert mod.mask_searches == 4
+
+
+@pytest.mark.parametrize("act", ["geglu", "swiglu"])
+@pytest.mark.parametrize("d,d_ff,n", [(128, 256, 128), (256, 384, 192)])
+def test_fused_gated_training_path_vs_oracle(act, d, d_ff, n):
+    """Gate computed in GEMM1's epilogue on the u/v-interleaved operand; the gated
+    backward + bias gradients in GEMM3's epilogue; dW_in returned in [u; v] order."""
+    from paper_2404_01847_b200 import engine as E
+
+    c = _case(act, d, d_ff, n, seed=3 * d + n)
+    w_in, b, w2 = to_dev_bf16(c["w_in"]), to_dev_bf16(c["bias_in"]), to_dev_bf16(c["w2"])
+    op_in = E.CompressedOperand.empty(2 * d_ff, d, "cuda", perm_ff=d_ff)
+    op_out = E.CompressedOperand.empty(d, d_ff, "cuda")
+    E.search_compress(w_in, op_in)
+    E.search_compress(w2, op_out)
+    st = E.ffn_forward(to_dev_bf16(c["x"]), op_in, b, op_out, act, fused=True)
+    g = E.ffn_backward(st, to_dev_bf16(c["dy"]), op_in, op_out, act, w_in_dense=w_in, w2_dense=w2, lam=1e-2)
+    lo = o.Layer(c["w_in"], c["bias_in"], c["w2"], act)
+    mi, mo = o.transposable_search_conv(c["w_in"]), o.transposable_search_conv(c["w2"])
+    np.testing.assert_array_equal(o.idx_to_bits(op_in.mask_idx().cpu().numpy()), mi)
+    fr = o.fst_forward(lo, c["x"], mi, mo, exact=False)
+    br = o.fst_backward(lo, fr, c["dy"], mi, mo, exact=False)
+    assert normwise_rel(st.a.float().cpu().numpy(), fr["a"]) < TOL
+    assert normwise_rel(st.y.float().cpu().numpy(), fr["y"]) < TOL
+    assert normwise_rel(g.dx.float().cpu().numpy(), br["dx"]) < TOL
+    assert normwise_rel(g.dbias_in.cpu().numpy(), br["dbias_in"]) < TOL
+    assert normwise_rel(g.dw_in.cpu().numpy(), o.masked_decay_gradient(br["dw_in"], c["w_in"], mi, 1e-2)) < TOL
+    assert normwise_rel(g.dw2.cpu().numpy(), o.masked_decay_gradient(br["dw2"], c["w2"], mo, 1e-2)) < TOL

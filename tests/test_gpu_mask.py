@@ -51,7 +51,7 @@ def test_compress_values_and_meta_bit_exact(name, corpora, mask_golden):
     fv = torch.empty((rows, cols // 2), dtype=torch.bfloat16, device="cuda")
     bv = torch.empty((cols, rows // 2), dtype=torch.bfloat16, device="cuda")
     C.call("s24_search_compress", wd.data_ptr(), C.S24_BF16, rows, cols, idx.data_ptr(), fv.data_ptr(), None,
-           bv.data_ptr(), None, C.stream_of(wd))
+           bv.data_ptr(), None, 0, C.stream_of(wd))
     np.testing.assert_array_equal(idx.cpu().numpy(), mask_golden[f"{name}.idx"])
     np.testing.assert_array_equal(bf16_bits_of(fv), mask_golden[f"{name}.fwd_values"])
     np.testing.assert_array_equal(bf16_bits_of(bv), mask_golden[f"{name}.bwd_values"])
@@ -62,7 +62,7 @@ def test_compress_values_and_meta_bit_exact(name, corpora, mask_golden):
     # K2 from the cached mask reproduces the same values
     fv2, bv2 = torch.zeros_like(fv), torch.zeros_like(bv)
     C.call("s24_prune_compress", wd.data_ptr(), C.S24_BF16, rows, cols, idx.data_ptr(), fv2.data_ptr(), None,
-           bv2.data_ptr(), None, C.stream_of(wd))
+           bv2.data_ptr(), None, 0, C.stream_of(wd))
     assert torch.equal(fv2.view(torch.int16), fv.view(torch.int16))
     assert torch.equal(bv2.view(torch.int16), bv.view(torch.int16))
 
@@ -180,3 +180,19 @@ def test_reference_backend_shim_spmm_and_gate_toleranced():
     z1, z2 = rng.standard_normal((9, 12)), rng.standard_normal((9, 12))
     g = rb.gate_gelu(z1, z2, False)
     assert np.linalg.norm(g - o.gate(z1, z2)) / np.linalg.norm(o.gate(z1, z2)) < 1e-2
+
+
+def test_gated_interleave_masks_are_reference_masks_permuted():
+    """u/v-interleaved compression of W_in = [u; v]: the mask (un-permuted) equals
+    the reference mask of [u; v]; the interleaved kept values are the rows' values."""
+    from paper_2404_01847_b200.engine import CompressedOperand, search_compress
+
+    d_ff, d = 256, 128
+    w = o.round_bf16(o.det_normal((2 * d_ff, d), seed=77))
+    op = CompressedOperand.empty(2 * d_ff, d, "cuda", perm_ff=d_ff)
+    search_compress(to_dev_bf16(w), op)
+    np.testing.assert_array_equal(op.mask_idx().cpu().numpy(), o.search_pattern_idx(w))
+    p = np.arange(2 * d_ff)
+    orig = np.where(p % 32 < 16, 16 * (p // 32) + p % 32, d_ff + 16 * (p // 32) + p % 32 - 16)
+    kv, _ = o.compress_rowwise(w[orig], o.transposable_search_conv(w)[orig])
+    np.testing.assert_array_equal(bf16_bits_of(op.fwd_vals), o.bf16_bits(kv))
