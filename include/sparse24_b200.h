@@ -156,6 +156,27 @@ int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int
                 int64_t n, int64_t k, float* d, int64_t ldd, const void* w, int w_dtype, const uint8_t* idx,
                 float lambda_w, int64_t gate_ff, void* stream);
 
+/* ---- K8: MVUE sparsification of an upstream gradient (next row 1 of SURVEY 8f) ----
+ * G is n tokens x f features (token-major, ldg); the sparsified matrix is G^T with
+ * groups of 4 consecutive tokens per feature -- mvue_slots_rowwise(G^T, seed)
+ * (sparsity.py:401-413) as used by _grad_weight(mvue=True) (gated_ffn.py:367-373).
+ * (state, inc) = numpy default_rng(seed).bit_generator.state after seeding
+ * (128-bit values split hi/lo).  Outputs the kept values g/pi (f x n/2 bf16) and
+ * E tiles of the f x n operand; `pairs` (optional, f x n/4) gets each group's kept
+ * pair index 0..5 (MVUE_PAIRS order).  gate_ff > 0: feature p of G is row
+ * gate_row(p) of [u; v] for the random-stream index.  n, f % 128 == 0. */
+int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int64_t f, uint64_t state_hi, uint64_t state_lo,
+                      uint64_t inc_hi, uint64_t inc_lo, int64_t gate_ff, uint16_t* vals, uint8_t* e,
+                      uint8_t* pairs, void* stream);
+
+/* sparse-A weight-gradient GEMM: D[m, n] fp32 = sum_k A~[m, k] B[n, k] + decay, with A~ an
+ * MVUE-compressed operand (vals m x k/2, E tiles; k = tokens).  Replaces
+ * kernels.spmm_rowwise (_core.pyx:44-60) in _grad_weight(mvue=True).  B layout and
+ * w / idx / lambda_w / gate_ff as s24_gemm_dw.  m % 128, k % 128, n % 256 == 0. */
+int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b, int b_mn,
+                int64_t ldb, int64_t n, float* d, int64_t ldd, const void* w, int w_dtype, const uint8_t* idx,
+                float lambda_w, int64_t gate_ff, void* stream);
+
 /* ---- K6/K7: fused (gated) activation, token-major ----------------------------
  * Z is n tokens x r_in (r_in = 2r gated, = r plain), row pitch ldz; A is n x r.
  * fwd: A[t, j] = act(Z[t, j]) * Z[t, r + j] (gated) or act(Z[t, j]) (plain);

@@ -453,3 +453,109 @@ def bf16_bits(x: np.ndarray) -> np.ndarray:
 
 def from_bf16_bits(b: np.ndarray) -> np.ndarray:
     return (np.asarray(b, dtype=np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+# ---------------------------------------------------------------------------
+# MVUE: unbiased stochastic 2:4 sparsification along rows (sparsity.py:285-413)
+# and the mvue=True weight gradient (gated_ffn.py:367-373).  Every array op is
+# the reference's sequence of IEEE float64 operations (sums over a group of 4
+# are sequential, as numpy reduces a (n, 4) C-contiguous array along axis 1).
+
+MVUE_PAIRS = np.array([(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)], dtype=np.int64)
+
+
+def mvue_inclusion_probs(groups: np.ndarray) -> np.ndarray:
+    """pi_i = min(1, c |x_i|) with sum(pi) = 2 per group (sparsity.py:290-324)."""
+    a = np.abs(np.asarray(groups, dtype=np.float64))
+    total = ((a[:, 0] + a[:, 1]) + a[:, 2]) + a[:, 3]
+    amax = a.max(axis=1)
+    fm = np.arange(4)[None, :] == a.argmax(axis=1)[:, None]
+    b = np.where(fm, 0.0, a)
+    rest = ((b[:, 0] + b[:, 1]) + b[:, 2]) + b[:, 3]
+    clamp = amax > rest
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+        plain = (2.0 * a) / total[:, None]
+        capped = a / rest[:, None]
+    capped = np.where(fm, 1.0, capped)
+    pi = np.where(clamp[:, None], capped, plain)
+    nnz = np.count_nonzero(a, axis=1)
+    pi[nnz == 1] = np.where(a[nnz == 1] > 0, 1.0, 1.0 / 3.0)
+    pi[nnz == 0] = 0.5
+    return pi
+
+
+def mvue_pair_probs(pi: np.ndarray) -> np.ndarray:
+    """Greedy transportation fill over the six pairs (sparsity.py:327-355)."""
+    pi = np.asarray(pi, dtype=np.float64)
+    r0, r1, r2, r3 = (pi[:, i].copy() for i in range(4))
+    s = 0.5 * (((pi[:, 0] + pi[:, 1]) + pi[:, 2]) + pi[:, 3])
+    p01 = np.maximum(np.minimum(np.minimum(np.minimum(r0, r1), s - r2), s - r3), 0.0)
+    r0 = r0 - p01
+    r1 = r1 - p01
+    s = s - p01
+    p02 = np.maximum(np.minimum(np.minimum(r0, r2), s - r3), 0.0)
+    r0 = r0 - p02
+    r2 = r2 - p02
+    s = s - p02
+    p03 = np.maximum(np.minimum(r0, r3), 0.0)
+    r3 = r3 - p03
+    s = s - p03
+    p12 = np.maximum(np.minimum(np.minimum(r1, r2), s - r3), 0.0)
+    r1 = r1 - p12
+    r2 = r2 - p12
+    p13 = np.maximum(np.minimum(r1, r3), 0.0)
+    r3 = r3 - p13
+    p23 = np.maximum(np.minimum(r2, r3), 0.0)
+    return np.stack([p01, p02, p03, p12, p13, p23], axis=1)
+
+
+def mvue_kept(groups: np.ndarray, rng_seed: int):
+    """(values (n, 2), kept pair indices (n, 2)) -- sparsity.py:358-376: one
+    numpy default_rng(seed).random() draw per group, in group order."""
+    groups = np.asarray(groups, dtype=np.float64)
+    pi = mvue_inclusion_probs(groups)
+    probs = mvue_pair_probs(pi)
+    u = np.random.default_rng(int(rng_seed) & 0xFFFF_FFFF_FFFF_FFFF).random(len(groups))
+    cum = np.cumsum(probs, axis=1)
+    draw = u * cum[:, -1]
+    idx = np.minimum(np.sum(cum <= draw[:, None], axis=1), 5)
+    kept = MVUE_PAIRS[idx]
+    rows = np.arange(len(groups))
+    values = np.stack([groups[rows, kept[:, s]] / pi[rows, kept[:, s]] for s in (0, 1)], axis=1)
+    return values, kept, idx
+
+
+def mvue_slots_rowwise(arr: np.ndarray, rng_seed: int):
+    """(values (m, k/2), absolute column positions (m, k/2)) -- sparsity.py:401-413."""
+    arr = np.ascontiguousarray(np.asarray(arr, dtype=np.float64))
+    m, k = arr.shape
+    if k % 4:
+        raise ShapeError(f"cols={k} not divisible by 4 for row-wise groups")
+    values, kept, _ = mvue_kept(arr.reshape(-1, 4), rng_seed)
+    pos = kept.reshape(m, k // 4, 2) + (4 * np.arange(k // 4, dtype=np.int64))[None, :, None]
+    return values.reshape(m, k // 2), pos.reshape(m, k // 2)
+
+
+def mvue_seed(rng_seed: int, salt: int) -> int:
+    """Per-product seed of _grad_weight (gated_ffn.py:372): (seed << 2) ^ salt."""
+    return (int(rng_seed) << 2) ^ salt
+
+
+def grad_weight_mvue(dz: np.ndarray, x: np.ndarray, rng_seed: int, salt: int) -> np.ndarray:
+    """dz^T @ x with dz^T MVUE-sparsified row-wise (gated_ffn.py:367-373), as
+    the dense product of the sparsified operand (equal to spmm_rowwise's
+    ascending-order result within float64 rounding)."""
+    dzt = np.ascontiguousarray(np.asarray(dz, dtype=np.float64).T)
+    vals, pos = mvue_slots_rowwise(dzt, mvue_seed(rng_seed, salt))
+    dense = np.zeros_like(dzt)
+    np.put_along_axis(dense, pos, vals, axis=1)
+    return dense @ np.asarray(x, dtype=np.float64)
+
+
+def fst_backward_mvue(layer: "Layer", fwd: dict, dy: np.ndarray, mask_in, mask_out, rng_seed: int = 0):
+    """fst_backward(mvue=True) (gated_ffn.py:304-364): as fst_backward but both
+    weight gradients through the MVUE-sparsified upstream gradients (salts 1, 2)."""
+    out = fst_backward(layer, fwd, dy, mask_in, mask_out, exact=False)
+    out["dw2"] = grad_weight_mvue(np.asarray(dy, dtype=np.float64), fwd["a"], rng_seed, 1)
+    out["dw_in"] = grad_weight_mvue(out["dz"], fwd["x"], rng_seed, 2)
+    return out

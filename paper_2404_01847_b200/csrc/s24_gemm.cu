@@ -94,7 +94,7 @@ constexpr int stages_for() {
   return budget / kStageBytes > 6 ? 6 : budget / kStageBytes;
 }
 
-template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG>
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kAcc = 2>
 struct Cfg {
   static constexpr int BK = kSparse ? 128 : 64;  // logical K per stage
   static constexpr int kMmaK = kSparse ? 32 : 16;
@@ -109,8 +109,8 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + E_BYTES;
   static constexpr int TX_BYTES = A_BYTES + (kBMN ? B_BYTES : BN_CTA * BK * 2) + E_BYTES;  // per CTA
   static constexpr int ACC_COLS = kBN;
-  static constexpr int E_COL = 2 * kBN;
-  static constexpr int USED_COLS = 2 * kBN + (kSparse ? 4 : 0);
+  static constexpr int E_COL = kAcc * kBN;  // kAcc TMEM accumulators (2: epilogue overlaps the next tile)
+  static constexpr int USED_COLS = kAcc * kBN + (kSparse ? 4 : 0);
   static constexpr int TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64 : USED_COLS <= 128 ? 128
                                  : USED_COLS <= 256 ? 256 : 512;
   static constexpr int EPI_OFF = kStages * STAGE_BYTES;          // per-warp 4 KB output staging
@@ -133,13 +133,13 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
   nb = in_group / gm;
 }
 
-template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT>
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT, int kAcc>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmD,
                 const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, GemmShape shp,
                 EpiParams ep) {
-  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG>;
+  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG, kAcc>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
         mma_commit_cg<kCG>(&tfull_bar[acc]);
-        if (++acc == 2) {
+        if (++acc == kAcc) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if constexpr (kCG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);
         else mbar_arrive(&tempty_bar[acc]);
       }
-      if (++acc == 2) {
+      if (++acc == kAcc) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -656,12 +656,13 @@ static int num_sms() {
   return n;
 }
 
-template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT = false>
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT = false,
+          int kAcc = 2>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& me, const CUtensorMap& md,
                        const CUtensorMap& mx, const CUtensorMap& my, const GemmShape& shp, const EpiParams& ep,
                        cudaStream_t st) {
-  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG>;
-  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi, kOutT>;
+  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG, kAcc>;
+  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi, kOutT, kAcc>;
   static bool attr_done = false;  // per template instance
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -886,4 +887,47 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   if (b_mn) S24_DW(false, true, 128, 1);
   S24_DW(false, false, 128, 1);
 #undef S24_DW
+}
+
+extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b,
+                           int b_mn, int64_t ldb, int64_t n, float* d, int64_t ldd, const void* w, int w_dtype,
+                           const uint8_t* idx, float lambda_w, int64_t gate_ff, void* stream) {
+  S24_REQUIRE(a_vals && a_e && b && d, S24_ERR_ARG, "NULL operand");
+  S24_REQUIRE(m % 128 == 0 && k % 128 == 0 && n % 256 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
+              "sparse dW GEMM needs m %% 128 == 0, k %% 128 == 0, n %% 256 == 0 (got m=%lld k=%lld n=%lld)",
+              (long long)m, (long long)k, (long long)n);
+  S24_REQUIRE(ldd >= n && ldd % 4 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0, S24_ERR_UNSUPPORTED,
+              "dW rows must be 16-byte aligned");
+  if (idx != nullptr)
+    S24_REQUIRE(w != nullptr && (w_dtype == S24_BF16 || w_dtype == S24_F32), S24_ERR_UNSUPPORTED,
+                "masked decay needs bf16 or fp32 weights");
+  if (gate_ff > 0) S24_REQUIRE(m == 2 * gate_ff && gate_ff % 16 == 0, S24_ERR_SHAPE, "gated dW: m must be 2 * d_ff");
+  S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
+  const bool pair = m % 256 == 0 && cg_override() != 1;
+  CUtensorMap ma, mb, me, md;
+  if (int rc = make_map(&ma, a_vals, k / 2, m, k / 2, 64, 128)) return rc;
+  if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, kMapU64)) return rc;
+  if (b_mn) {
+    S24_REQUIRE(ldb >= n, S24_ERR_SHAPE, "ldb < n");
+    if (int rc = make_map(&mb, b, n, k, ldb, 64, 128)) return rc;
+  } else {
+    S24_REQUIRE(ldb >= k, S24_ERR_SHAPE, "ldb < k");
+    if (int rc = make_map(&mb, b, k, n, ldb, 64, pair ? 128 : 256)) return rc;
+  }
+  if (int rc = make_map(&md, d, n, m, ldd, 32, 16, kMapF32Sw128)) return rc;
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 1};
+  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // BN = 256 with one TMEM accumulator (256 + 4 metadata columns): K = tokens is long, so the
+  // un-overlapped epilogue is a small share; the B half per CTA is exactly two 64-wide chunks
+#define S24_SDW(BMN, CG)                                                                                  \
+  return launch_gemm<true, false, BMN, 256, stages_for<Cfg<true, false, BMN, 256, 1, CG, 1>::STAGE_BYTES>(), \
+                     CG, kEpiDw, false, 1>(ma, mb, me, md, md, md, shp, ep, st)
+  if (pair) {
+    if (b_mn) S24_SDW(true, 2);
+    S24_SDW(false, 2);
+  }
+  if (b_mn) S24_SDW(true, 1);
+  S24_SDW(false, 1);
+#undef S24_SDW
 }

@@ -176,7 +176,7 @@ __host__ __device__ __forceinline__ int64_t gate_row(int64_t p, int64_t perm_ff)
 
 // kNarrow: bf16 rows that are only 8-byte aligned (cols % 8 == 4) load 4 elements at a time
 template <int kDType, bool kSearch, bool kNarrow>
-__global__ void __launch_bounds__(kThreads) mask_tile_kernel(MaskArgs p) {
+__global__ void __launch_bounds__(kThreads, 2) mask_tile_kernel(MaskArgs p) {
   using T = typename Elem<kDType>::T;
   constexpr int kVec = kNarrow ? 4 : Elem<kDType>::kVec;
 

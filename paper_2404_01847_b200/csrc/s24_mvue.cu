@@ -1,0 +1,238 @@
+// K8: MVUE (minimum-variance unbiased) 2:4 sparsification of an upstream
+// gradient along tokens, emitted directly as the sparse tensor-core operand of
+// the weight-gradient GEMM (kept values + E tiles).
+//
+// Reference: _grad_weight(mvue=True) (gated_ffn.py:367-373) ->
+// mvue_slots_rowwise(dz^T) (sparsity.py:401-413) -> _mvue_kept (:358-376):
+//   pi   = mvue_inclusion_probs(group)   (:290-324, water-filled, sum 2)
+//   p    = mvue_pair_probs(pi)           (:327-355, greedy transportation fill)
+//   u    = default_rng(seed).random(n)   (one draw per group, group order)
+//   pick = min(#{cumsum(p) <= u * sum(p)}, 5); kept values g / pi
+// Bit-exact reproduction: every float64 operation is issued explicitly in the
+// reference's order (sequential 4-term sums, mul-then-div, no FMA
+// contraction), and numpy's PCG64 (XSL-RR 128/64) stream is regenerated on the
+// device with O(log n) jump-ahead to each thread's first group.
+//
+// Layout: input G is token-major (n tokens x f features); the sparsified
+// matrix is G^T (f x n), groups of 4 consecutive tokens per feature, group
+// index i = row * (n / 4) + token / 4 (row = feature in the reference's order;
+// gate_ff > 0 maps the u/v-interleaved feature p back to its [u; v] row).
+// One CTA = 128 features x 128 tokens = one E tile; the tile is staged in smem
+// so each lane streams one feature column conflict-free.
+#include "s24_common.cuh"
+
+namespace s24 {
+
+struct U128 {
+  uint64_t hi, lo;
+};
+__device__ __forceinline__ U128 mul128(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo * b.lo;
+  r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+  return r;
+}
+__device__ __forceinline__ U128 add128(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1 : 0);
+  return r;
+}
+
+struct MvueRng {
+  U128 state;       // PCG64 state after seeding (numpy bit_generator.state)
+  U128 inc;         // increment (odd)
+  U128 mult[40];    // MULT^(2^i)
+  U128 plus[40];    // additive term of 2^i steps
+};
+
+constexpr uint64_t kPcgMultHi = 0x2360ED051FC65DA4ull, kPcgMultLo = 0x4385DF649FCCF645ull;
+
+__device__ __forceinline__ U128 pcg_advance(const MvueRng& rng, uint64_t delta) {
+  U128 am{0, 1}, ap{0, 0};
+  for (int i = 0; delta; ++i, delta >>= 1) {
+    if (delta & 1) {
+      am = mul128(am, rng.mult[i]);
+      ap = add128(mul128(ap, rng.mult[i]), rng.plus[i]);
+    }
+  }
+  return add128(mul128(am, rng.state), ap);
+}
+// one numpy Generator.random(): step, XSL-RR output, 53-bit double
+__device__ __forceinline__ double pcg_uniform(U128& st, const U128& inc) {
+  st = add128(mul128(st, U128{kPcgMultHi, kPcgMultLo}), inc);
+  const uint64_t x = st.hi ^ st.lo;
+  const unsigned rot = static_cast<unsigned>(st.hi >> 58);
+  const uint64_t out = (x >> rot) | (x << ((64u - rot) & 63u));
+  return __dmul_rn(static_cast<double>(out >> 11), 1.0 / 9007199254740992.0);
+}
+
+// exact reference arithmetic helpers (no contraction)
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// MVUE selection for one group: returns the pair index (0..5) and the two kept values
+__device__ __forceinline__ int mvue_group(const double (&g)[4], double u, double& v0, double& v1) {
+  double a[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) a[k] = fabs(g[k]);
+  const double total = dadd(dadd(dadd(a[0], a[1]), a[2]), a[3]);
+  int fm = 0;
+#pragma unroll
+  for (int k = 1; k < 4; ++k)
+    if (a[k] > a[fm]) fm = k;
+  const double amax = a[fm];
+  double b[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) b[k] = k == fm ? 0.0 : a[k];
+  const double rest = dadd(dadd(dadd(b[0], b[1]), b[2]), b[3]);
+  const bool clamp = amax > rest;
+  int nnz = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) nnz += a[k] != 0.0;
+  double pi[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double plain = ddiv(dmul(2.0, a[k]), total);
+    const double capped = k == fm ? 1.0 : ddiv(a[k], rest);
+    pi[k] = clamp ? capped : plain;
+    if (nnz == 1) pi[k] = a[k] > 0.0 ? 1.0 : 1.0 / 3.0;
+    if (nnz == 0) pi[k] = 0.5;
+  }
+  // greedy pair fill (sparsity.py:334-355)
+  double r0 = pi[0], r1 = pi[1], r2 = pi[2], r3 = pi[3];
+  double s = dmul(0.5, dadd(dadd(dadd(pi[0], pi[1]), pi[2]), pi[3]));
+  const double p01 = fmax(fmin(fmin(fmin(r0, r1), dsub(s, r2)), dsub(s, r3)), 0.0);
+  r0 = dsub(r0, p01);
+  r1 = dsub(r1, p01);
+  s = dsub(s, p01);
+  const double p02 = fmax(fmin(fmin(r0, r2), dsub(s, r3)), 0.0);
+  r0 = dsub(r0, p02);
+  r2 = dsub(r2, p02);
+  s = dsub(s, p02);
+  const double p03 = fmax(fmin(r0, r3), 0.0);
+  r3 = dsub(r3, p03);
+  s = dsub(s, p03);
+  const double p12 = fmax(fmin(fmin(r1, r2), dsub(s, r3)), 0.0);
+  r1 = dsub(r1, p12);
+  r2 = dsub(r2, p12);
+  const double p13 = fmax(fmin(r1, r3), 0.0);
+  r3 = dsub(r3, p13);
+  const double p23 = fmax(fmin(r2, r3), 0.0);
+  double c[6];
+  c[0] = p01;
+  c[1] = dadd(c[0], p02);
+  c[2] = dadd(c[1], p03);
+  c[3] = dadd(c[2], p12);
+  c[4] = dadd(c[3], p13);
+  c[5] = dadd(c[4], p23);
+  const double draw = dmul(u, c[5]);
+  int idx = 0;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) idx += c[j] <= draw;
+  idx = min(idx, 5);
+  constexpr int kI0[6] = {0, 0, 0, 1, 1, 2}, kI1[6] = {1, 2, 3, 2, 3, 3};
+  const int i0 = kI0[idx], i1 = kI1[idx];
+  v0 = ddiv(g[i0], pi[i0]);
+  v1 = ddiv(g[i1], pi[i1]);
+  return idx;
+}
+
+struct MvueArgs {
+  const uint16_t* g;  // n x f token-major (ldg)
+  int64_t ldg, n, f, gate_ff;
+  uint16_t* vals;     // f x n/2
+  uint8_t* e;         // E tiles [f/128][n/128]
+  uint8_t* pairs;     // optional f x n/4 pair indices (tests)
+};
+
+__global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid_constant__ MvueRng rng) {
+  __shared__ __align__(16) uint16_t s_g[128 * 136];  // [token][feature], row pitch 136 (272 B)
+  __shared__ __align__(16) uint32_t s_e[512];
+  const int tid = threadIdx.x;
+  const int64_t f0 = static_cast<int64_t>(blockIdx.y) * 128, t0 = static_cast<int64_t>(blockIdx.x) * 128;
+  for (int i = tid; i < 512; i += 256) s_e[i] = 0;
+  // coalesced tile load: 128 token rows x 256 bytes
+  for (int i = tid; i < 128 * 16; i += 256) {
+    const int tr = i >> 4, ch = i & 15;
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(p.g + (t0 + tr) * p.ldg + f0 + ch * 8));
+    *reinterpret_cast<uint4*>(&s_g[tr * 136 + ch * 8]) = x;
+  }
+  __syncthreads();
+  const int ml = tid & 127, half = tid >> 7;  // feature in tile, token half (64 tokens = 16 groups)
+  const int64_t feat = f0 + ml;
+  const int64_t row = p.gate_ff > 0 ? ((feat & 31) < 16 ? 16 * (feat >> 5) + (feat & 31)
+                                                         : p.gate_ff + 16 * (feat >> 5) + (feat & 31) - 16)
+                                    : feat;
+  const int64_t grp0 = t0 / 4 + 16 * half;
+  U128 st = pcg_advance(rng, static_cast<uint64_t>(row * (p.n / 4) + grp0));
+  uint32_t packed[16];
+  uint32_t halfwords[4] = {0, 0, 0, 0};
+#pragma unroll 1
+  for (int j = 0; j < 16; ++j) {
+    double gv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) gv[k] = static_cast<double>(bf16_to_f32(s_g[(64 * half + 4 * j + k) * 136 + ml]));
+    const double u = pcg_uniform(st, rng.inc);
+    double v0, v1;
+    const int idx = mvue_group(gv, u, v0, v1);
+    constexpr uint32_t kNib[6] = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE};  // i0 | i1 << 2
+    halfwords[j >> 2] |= kNib[idx] << (4 * (j & 3));
+    // f64 -> f32 -> bf16 (the rounding of the reference-side bf16 operand)
+    packed[j] = static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v0))) |
+                (static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v1))) << 16);
+    if (p.pairs) p.pairs[feat * (p.n / 4) + grp0 + j] = static_cast<uint8_t>(idx);
+  }
+  // kept values: 32 bf16 (64 B) of row feat
+  uint4* dst = reinterpret_cast<uint4*>(p.vals + feat * (p.n / 2) + t0 / 2 + 32 * half);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+  // metadata: halfword w covers tokens 64 half + 16 w .. +15 of row ml
+  if (p.e) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int kk = 64 * half + 16 * w;
+      const int L = (ml & 7) + 8 * ((kk & 31) >> 4) + 16 * (ml >> 4);
+      const int c = kk >> 5, h = (ml >> 3) & 1;
+      reinterpret_cast<uint16_t*>(s_e)[L * 8 + c * 2 + h] = static_cast<uint16_t>(halfwords[w]);
+    }
+    __syncthreads();
+    uint4* de = reinterpret_cast<uint4*>(p.e + (static_cast<int64_t>(blockIdx.y) * (p.n / 128) + blockIdx.x) * 2048);
+    if (tid < 128) de[tid] = reinterpret_cast<const uint4*>(s_e)[tid];
+  }
+}
+
+}  // namespace s24
+
+using namespace s24;
+
+extern "C" int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int64_t f, uint64_t state_hi,
+                                 uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t gate_ff,
+                                 uint16_t* vals, uint8_t* e, uint8_t* pairs, void* stream) {
+  S24_REQUIRE(g && vals, S24_ERR_ARG, "NULL pointer");
+  S24_REQUIRE(n % 128 == 0 && f % 128 == 0 && n > 0 && f > 0, S24_ERR_SHAPE,
+              "MVUE operand needs tokens and features divisible by 128 (got n=%lld f=%lld)", (long long)n,
+              (long long)f);
+  S24_REQUIRE(ldg >= f && ldg % 8 == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0, S24_ERR_UNSUPPORTED,
+              "gradient rows must be 16-byte aligned");
+  if (gate_ff > 0) S24_REQUIRE(f == 2 * gate_ff && gate_ff % 16 == 0, S24_ERR_SHAPE, "gated MVUE: f must be 2 d_ff");
+  MvueRng rng;
+  rng.state = U128{state_hi, state_lo};
+  rng.inc = U128{inc_hi, inc_lo};
+  unsigned __int128 m = (static_cast<unsigned __int128>(kPcgMultHi) << 64) | kPcgMultLo;
+  unsigned __int128 pl = (static_cast<unsigned __int128>(inc_hi) << 64) | inc_lo;
+  for (int i = 0; i < 40; ++i) {
+    rng.mult[i] = U128{static_cast<uint64_t>(m >> 64), static_cast<uint64_t>(m)};
+    rng.plus[i] = U128{static_cast<uint64_t>(pl >> 64), static_cast<uint64_t>(pl)};
+    pl = (m + 1) * pl;
+    m = m * m;
+  }
+  S24_REQUIRE(static_cast<double>(f) * static_cast<double>(n / 4) < 1099511627776.0, S24_ERR_SHAPE,
+              "MVUE stream index exceeds the 2^40 jump table");
+  MvueArgs a{g, ldg, n, f, gate_ff, vals, e, pairs};
+  dim3 grid(static_cast<unsigned>(n / 128), static_cast<unsigned>(f / 128));
+  mvue_tile_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, rng);
+  return s24_check_launch("mvue_compress");
+}

@@ -137,6 +137,49 @@ def gemm_dw(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, m: int, n:
                C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, C.stream_of(out))
 
 
+def mvue_seed(rng_seed: int, salt: int) -> int:
+    """Per-product seed of _grad_weight (gated_ffn.py:372): (seed << 2) ^ salt."""
+    return (int(rng_seed) << 2) ^ salt
+
+
+def pcg64_state(seed: int) -> tuple[int, int, int, int]:
+    """(state_hi, state_lo, inc_hi, inc_lo) of numpy default_rng(seed) after seeding
+    (sparsity.py:364) -- the device regenerates the same PCG64 stream."""
+    import numpy as np
+
+    st = np.random.default_rng(int(seed) & 0xFFFF_FFFF_FFFF_FFFF).bit_generator.state["state"]
+    s, i = int(st["state"]), int(st["inc"])
+    m64 = (1 << 64) - 1
+    return s >> 64, s & m64, i >> 64, i & m64
+
+
+def mvue_compress(g: torch.Tensor, seed: int, gate_ff: int = 0, want_pairs: bool = False):
+    """K8: MVUE-sparsify g^T (features x tokens) along tokens (sparsity.py:401-413)
+    into the tensor-core operand.  g: token-major (N x F) bf16.  Returns
+    (vals F x N/2, E tiles, pairs F x N/4 or None)."""
+    n, f = g.shape
+    dev = g.device
+    vals = torch.empty((f, n // 2), dtype=torch.bfloat16, device=dev)
+    e = torch.empty((f // 128) * (n // 128) * 2048, dtype=torch.uint8, device=dev)
+    pairs = torch.empty((f, n // 4), dtype=torch.uint8, device=dev) if want_pairs else None
+    sh, sl, ih, il = pcg64_state(seed)
+    with TIMER("k8_mvue"):
+        C.call("s24_mvue_compress", g.data_ptr(), g.stride(0), n, f, sh, sl, ih, il, gate_ff, vals.data_ptr(),
+               e.data_ptr(), C.ptr(pairs), C.stream_of(g))
+    return vals, e, pairs
+
+
+def spmm_dw(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b_mn: bool, n: int,
+            out: torch.Tensor, w: torch.Tensor | None = None, idx: torch.Tensor | None = None, lam: float = 0.0,
+            gate_ff: int = 0, tag: str = "k8_spmm_dw") -> None:
+    """out[m, n] fp32 = MVUE-sparse A~[m, k] . B[n, k]^T + lam (1 - M) W (2:4 tensor cores)."""
+    decay = idx is not None and lam != 0.0
+    with TIMER(tag):
+        C.call("s24_spmm_dw", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), b.stride(0), n,
+               out.data_ptr(), out.stride(0), C.ptr(w) if decay else None, C.dtype_code(w) if decay else 0,
+               C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, C.stream_of(out))
+
+
 def _rows(t: torch.Tensor) -> torch.Tensor:
     """Row-major (token-major) storage with a 16-byte aligned pitch."""
     if t.stride(1) == 1 and t.stride(0) >= t.shape[1] and t.stride(0) % 8 == 0 and t.data_ptr() % 16 == 0:
@@ -213,10 +256,13 @@ class Grads:
 def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: CompressedOperand, act: str,
                  w_in_dense: torch.Tensor | None = None, w2_dense: torch.Tensor | None = None,
                  lam: float = 0.0, dw_in_out: torch.Tensor | None = None,
-                 dw2_out: torch.Tensor | None = None) -> Grads:
+                 dw2_out: torch.Tensor | None = None, mvue: bool = False, rng_seed: int = 0) -> Grads:
     """dA = dY W2~ (out_bwd, W2's transposed orientation) -> dZ (activation
     backward, bias gradient) -> dX = dZ W_in~ (in_bwd); dense dW2 = dY^T A and
-    dW_in = dZ^T X with the masked decay lam (1 - M) W fused (gated_ffn.py:327-356)."""
+    dW_in = dZ^T X with the masked decay lam (1 - M) W fused (gated_ffn.py:327-356).
+    mvue=True: both weight gradients use the MVUE-sparsified upstream gradients
+    (dY^T with salt 1, dZ^T with salt 2, seeds (rng_seed << 2) ^ salt) on the
+    2:4 tensor cores (gated_ffn.py:367-373)."""
     n, d = st.x.shape
     r_in, d_ff = w_in.rows, w2.cols
     if tuple(dy.shape) != (n, d):
@@ -246,8 +292,14 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dz, False, n, dx, tag="k4_spmm_bwd_in", out_t=True)
     # dW2[d, d_ff] = dY^T A and dW_in[r_in, d] = dZ^T X: K = tokens, both operands token-major (MN-major)
     dw2 = dw2_out if dw2_out is not None else torch.empty((d, d_ff), dtype=torch.float32, device=dev)
-    gemm_dw(dy, True, st.a, True, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")
     dw_in = dw_in_out if dw_in_out is not None else torch.empty((r_in, d), dtype=torch.float32, device=dev)
-    gemm_dw(dz, True, st.x, True, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam, tag="k5_gemm_dw_in",
-            gate_ff=gate_ff)
+    if mvue:
+        v2, e2, _ = mvue_compress(dy, mvue_seed(rng_seed, 1))
+        spmm_dw(v2, e2, d, n, st.a, True, d_ff, dw2, w2_dense, w2.idx, lam, tag="k8_spmm_dw2")
+        v1, e1, _ = mvue_compress(dz, mvue_seed(rng_seed, 2), gate_ff)
+        spmm_dw(v1, e1, r_in, n, st.x, True, d, dw_in, w_in_dense, w_in.idx, lam, gate_ff, tag="k8_spmm_dw_in")
+    else:
+        gemm_dw(dy, True, st.a, True, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")
+        gemm_dw(dz, True, st.x, True, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam, tag="k5_gemm_dw_in",
+                gate_ff=gate_ff)
     return Grads(dx, dw_in, dbias, dw2)

@@ -8,9 +8,9 @@ Differences from the reference that are deliberate and visible:
     reference's sparse route returns the same values in column-major numpy
     arrays (gated_ffn.py:162);
   * weight gradients are fp32;
-  * mvue=True (the reference default, gated_ffn.py:308) needs the MVUE
-    sparse dW kernel, not built yet: it raises
-    NotImplementedError instead of silently computing the dense dW.
+  * mvue=True (the reference default, gated_ffn.py:308) runs K8: the MVUE
+    draw of the reference (same PCG64 stream, same float64 selection) on the
+    GPU's bf16 upstream gradients, then 2:4 tensor-core weight-gradient GEMMs;
   * Activation.SWIGLU is an extension (not in the reference enum).
 """
 
@@ -214,13 +214,10 @@ def fst_backward(bundle: FstActivations, upstream: torch.Tensor, rng_seed: int =
         raise ShapeError(f"upstream shape {tuple(up.shape)} != output shape {tuple(bundle.y.shape)}")
     if bundle.masks is None:
         return _dense_backward(bundle, up)
-    if mvue:
-        raise NotImplementedError(
-            "MVUE-sparsified dW (fst_backward(mvue=True), gated_ffn.py:372-373) is the next kernel (K8) and is "
-            "not built yet; call fst_backward(..., mvue=False) for the dense dW path")
     ops = bundle.masks.plans(layer)
     g = E.ffn_backward(bundle.state, up, ops["in"], ops["out"], layer.activation.value,
-                       w_in_dense=layer.w_in_cat, w2_dense=layer.w2, lam=decay_lambda)
+                       w_in_dense=layer.w_in_cat, w2_dense=layer.w2, lam=decay_lambda, mvue=mvue,
+                       rng_seed=rng_seed)
     return _pack_grads(layer, g.dx, g.dw_in, g.dbias_in, g.dw2)
 
 

@@ -182,7 +182,50 @@ def main():
     gg = geglu_forward(c["x"], c["w_in"][:r], c["w_in"][r:], c["bias_in"][:r], c["bias_in"][r:])
     fst["geglu_forward.out"] = gg.to_array()
     np.savez_compressed(os.path.join(HERE, "fst_golden.npz"), **fst)
+
+    # MVUE (sparsity.py:285-413) on bf16-valued inputs incl. zeros, single
+    # nonzeros and one dominant entry per group; fst_backward(mvue=True), the
+    # reference default (gated_ffn.py:308)
+    from sparse24.sparsity import mvue_inclusion_probs, mvue_pair_probs, mvue_slots_rowwise
+
+    mv = {}
+    for i, (shape, seed) in enumerate(mvue_cases()):
+        arr = mvue_input(shape, i)
+        vals, pos = mvue_slots_rowwise(arr, seed)
+        mv[f"case{i}.x"] = arr
+        mv[f"case{i}.seed"] = np.array(seed, dtype=np.uint64)
+        mv[f"case{i}.values"] = vals
+        mv[f"case{i}.pos"] = pos.astype(np.int32)
+        mv[f"case{i}.pi"] = mvue_inclusion_probs(arr.reshape(-1, 4))
+        mv[f"case{i}.pairs"] = mvue_pair_probs(mv[f"case{i}.pi"])
+    for act, c in fst_cases().items():
+        if act == "geglu":
+            r = c["w2"].shape[1]
+            layer = FFNLayer.gated(u=c["w_in"][:r], v=c["w_in"][r:], b=c["bias_in"][:r],
+                                   c=c["bias_in"][r:], w2=c["w2"])
+        else:
+            layer = FFNLayer.plain(w1=c["w_in"], b=c["bias_in"], w2=c["w2"], activation=Activation(act))
+        masks = FFNMasks(w_in=s24.transposable_search_conv(layer.w_in()),
+                         w_out=s24.transposable_search_conv(layer.w2))
+        f = fst_forward(layer, c["x"], masks)
+        for seed in (0, 12345):
+            g = fst_backward(f, c["dy"], rng_seed=seed, mvue=True)
+            mv[f"fst_{act}_{seed}.dw_in"] = np.concatenate([g.d_u, g.d_v]) if act == "geglu" else g.d_w1
+            mv[f"fst_{act}_{seed}.dw2"] = np.asarray(g.d_w2)
+    np.savez_compressed(os.path.join(HERE, "mvue_golden.npz"), **mv)
     print("wrote", os.listdir(HERE))
+
+
+def mvue_cases():
+    return [((16, 64), 0), ((32, 128), 7), ((8, 256), 2 ** 40 + 3), ((128, 64), (12345 << 2) ^ 2)]
+
+
+def mvue_input(shape, i):
+    a = o.det_normal(shape, seed=500 + i)
+    u = (o._splitmix64(int(np.prod(shape)), 900 + i) % np.uint64(10)).reshape(shape)
+    a = np.where(u < 2, 0.0, a)                       # zeros -> groups with < 2 nonzeros
+    a = np.where(u == 9, a * 2.0 ** 12, a)            # dominant entries -> clamped pi
+    return o.round_bf16(a)
 
 
 if __name__ == "__main__":

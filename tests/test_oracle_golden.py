@@ -120,3 +120,33 @@ def test_ref_kernels_agree_with_restatement():
     s1, b1 = k.pattern_scores(blocks, pos)
     s2, b2 = o.pattern_scores(blocks, pos)
     assert s1.tobytes() == s2.tobytes() and (b1 == b2).all()
+
+
+def test_mvue_oracle_bit_exact_vs_reference():
+    from make_golden import mvue_cases
+
+    g = dict(np.load(os.path.join(GOLDEN, "mvue_golden.npz")))
+    for i, (shape, seed) in enumerate(mvue_cases()):
+        x = g[f"case{i}.x"]
+        assert int(g[f"case{i}.seed"]) == seed
+        pi = o.mvue_inclusion_probs(x.reshape(-1, 4))
+        assert pi.tobytes() == g[f"case{i}.pi"].tobytes()
+        assert o.mvue_pair_probs(pi).tobytes() == g[f"case{i}.pairs"].tobytes()
+        vals, pos = o.mvue_slots_rowwise(x, seed)
+        assert vals.tobytes() == g[f"case{i}.values"].tobytes()
+        np.testing.assert_array_equal(pos, g[f"case{i}.pos"])
+        # every group keeps exactly two entries; unbiased marginals sum to 2
+        np.testing.assert_allclose(pi.sum(axis=1), 2.0, rtol=1e-12)
+
+
+@pytest.mark.parametrize("act", ["gelu", "geglu", "relu"])
+def test_fst_backward_mvue_matches_reference(act, fst_golden):
+    g = dict(np.load(os.path.join(GOLDEN, "mvue_golden.npz")))
+    c = fst_cases()[act]
+    fg = {k.split(".", 1)[1]: v for k, v in fst_golden.items() if k.startswith(act + ".")}
+    layer = o.Layer(c["w_in"], c["bias_in"], c["w2"], act)
+    f = o.fst_forward(layer, c["x"], fg["mask_in"], fg["mask_out"], exact=True)
+    for seed in (0, 12345):
+        b = o.fst_backward_mvue(layer, f, c["dy"], fg["mask_in"], fg["mask_out"], rng_seed=seed)
+        np.testing.assert_allclose(b["dw_in"], g[f"fst_{act}_{seed}.dw_in"], rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(b["dw2"], g[f"fst_{act}_{seed}.dw2"], rtol=1e-12, atol=1e-13)
