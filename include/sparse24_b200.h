@@ -172,7 +172,7 @@ int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int64_t f, uint
 /* sparse-A weight-gradient GEMM: D[m, n] fp32 = sum_k A~[m, k] B[n, k] + decay, with A~ an
  * MVUE-compressed operand (vals m x k/2, E tiles; k = tokens).  Replaces
  * kernels.spmm_rowwise (_core.pyx:44-60) in _grad_weight(mvue=True).  B layout and
- * w / idx / lambda_w / gate_ff as s24_gemm_dw.  m % 128, k % 128, n % 256 == 0. */
+ * w / idx / lambda_w / gate_ff as s24_gemm_dw.  m % 128, k % 128, n % 128 == 0. */
 int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b, int b_mn,
                 int64_t ldb, int64_t n, float* d, int64_t ldd, const void* w, int w_dtype, const uint8_t* idx,
                 float lambda_w, int64_t gate_ff, void* stream);

@@ -893,8 +893,8 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
                            int b_mn, int64_t ldb, int64_t n, float* d, int64_t ldd, const void* w, int w_dtype,
                            const uint8_t* idx, float lambda_w, int64_t gate_ff, void* stream) {
   S24_REQUIRE(a_vals && a_e && b && d, S24_ERR_ARG, "NULL operand");
-  S24_REQUIRE(m % 128 == 0 && k % 128 == 0 && n % 256 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
-              "sparse dW GEMM needs m %% 128 == 0, k %% 128 == 0, n %% 256 == 0 (got m=%lld k=%lld n=%lld)",
+  S24_REQUIRE(m % 128 == 0 && k % 128 == 0 && n % 128 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
+              "sparse dW GEMM needs m %% 128 == 0, k %% 128 == 0, n %% 128 == 0 (got m=%lld k=%lld n=%lld)",
               (long long)m, (long long)k, (long long)n);
   S24_REQUIRE(ldd >= n && ldd % 4 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0, S24_ERR_UNSUPPORTED,
               "dW rows must be 16-byte aligned");
@@ -904,6 +904,8 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
   if (gate_ff > 0) S24_REQUIRE(m == 2 * gate_ff && gate_ff % 16 == 0, S24_ERR_SHAPE, "gated dW: m must be 2 * d_ff");
   S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
   const bool pair = m % 256 == 0 && cg_override() != 1;
+  const bool wide = n % 256 == 0;
+  const int bn_cta = (wide ? 256 : 128) / (pair ? 2 : 1);
   CUtensorMap ma, mb, me, md;
   if (int rc = make_map(&ma, a_vals, k / 2, m, k / 2, 64, 128)) return rc;
   if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, kMapU64)) return rc;
@@ -912,7 +914,7 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
     if (int rc = make_map(&mb, b, n, k, ldb, 64, 128)) return rc;
   } else {
     S24_REQUIRE(ldb >= k, S24_ERR_SHAPE, "ldb < k");
-    if (int rc = make_map(&mb, b, k, n, ldb, 64, pair ? 128 : 256)) return rc;
+    if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
   if (int rc = make_map(&md, d, n, m, ldd, 32, 16, kMapF32Sw128)) return rc;
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 1};
@@ -920,14 +922,22 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // BN = 256 with one TMEM accumulator (256 + 4 metadata columns): K = tokens is long, so the
   // un-overlapped epilogue is a small share; the B half per CTA is exactly two 64-wide chunks
-#define S24_SDW(BMN, CG)                                                                                  \
-  return launch_gemm<true, false, BMN, 256, stages_for<Cfg<true, false, BMN, 256, 1, CG, 1>::STAGE_BYTES>(), \
-                     CG, kEpiDw, false, 1>(ma, mb, me, md, md, md, shp, ep, st)
-  if (pair) {
-    if (b_mn) S24_SDW(true, 2);
-    S24_SDW(false, 2);
+#define S24_SDW(BMN, BNV, CG, ACC)                                                                            \
+  return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG, ACC>::STAGE_BYTES>(), \
+                     CG, kEpiDw, false, ACC>(ma, mb, me, md, md, md, shp, ep, st)
+  if (wide) {
+    if (pair) {
+      if (b_mn) S24_SDW(true, 256, 2, 1);
+      S24_SDW(false, 256, 2, 1);
+    }
+    if (b_mn) S24_SDW(true, 256, 1, 1);
+    S24_SDW(false, 256, 1, 1);
   }
-  if (b_mn) S24_SDW(true, 1);
-  S24_SDW(false, 1);
+  if (pair) {
+    if (b_mn) S24_SDW(true, 128, 2, 2);
+    S24_SDW(false, 128, 2, 2);
+  }
+  if (b_mn) S24_SDW(true, 128, 1, 2);
+  S24_SDW(false, 128, 1, 2);
 #undef S24_SDW
 }

@@ -81,7 +81,7 @@ def test_fused_masked_decay_matches_oracle():
 def test_dense_path_and_mvue_flag():
     import paper_2404_01847_b200 as P
 
-    c = _case("gelu", 128, 256, 64, seed=5)
+    c = _case("gelu", 128, 256, 128, seed=5)
     layer = P.FFNLayer(to_dev_bf16(c["w_in"]), to_dev_bf16(c["bias_in"]), to_dev_bf16(c["w2"]), P.Activation.GELU)
     f = P.fst_forward(layer, to_dev_bf16(c["x"]), None)  # dense fine-tune path
     g = P.fst_backward(f, to_dev_bf16(c["dy"]))
