@@ -222,7 +222,7 @@ def make_problem(cfg, device, seed):
 class SparseStep:
     """One 2:4 FFN training step on the engine (the measured unit)."""
 
-    def __init__(self, w_in, bias, w2, act, world, pg=None):
+    def __init__(self, w_in, bias, w2, act, world, pg=None, mvue=False):
         import torch
         from paper_2404_01847_b200 import engine as E
 
@@ -240,8 +240,9 @@ class SparseStep:
         self.dbias = self.bucket[n_in:n_in + n_b]
         self.dw2 = self.bucket[n_in + n_b:].view(w2.shape)
         self.t = 0
+        self.mvue = mvue
         # our kernel launches per step: K1 or K2 x2, fwd 2 sparse GEMMs, bwd 2 sparse + 2 dW GEMMs
-        self.launches_per_step = 2 + 2 + 4  # activations fused into the GEMM epilogues
+        self.launches_per_step = 2 + 2 + 4 + (2 if mvue else 0)  # activations fused into the GEMM epilogues
 
     def __call__(self, x, dy):
         E = self.E
@@ -253,7 +254,8 @@ class SparseStep:
             E.compress_values(self.w2, self.op_out)
         st = E.ffn_forward(x, self.op_in, self.bias, self.op_out, self.act, fused=True)
         g = E.ffn_backward(st, dy, self.op_in, self.op_out, self.act, w_in_dense=self.w_in, w2_dense=self.w2,
-                           lam=LAMBDA / self.world, dw_in_out=self.dw_in, dw2_out=self.dw2)
+                           lam=LAMBDA / self.world, dw_in_out=self.dw_in, dw2_out=self.dw2, mvue=self.mvue,
+                           rng_seed=self.t)
         self.dbias.copy_(g.dbias_in)
         if self.world > 1:
             self.torch.distributed.all_reduce(self.bucket, group=self.pg)
@@ -357,6 +359,14 @@ def run_ours(a, cfg):
     ms_step = ms / a.steps
     value = n_tok * world / (ms_step / 1000.0)
 
+    # ---- variant: MVUE-sparsified dW (the reference default fst_backward(mvue=True)) ----
+    mstep = SparseStep(w_in, bias, w2, cfg["act"], world, pg, mvue=True)
+    mms, _ = time_loop(lambda: mstep(x, dy), max(10, a.steps // 2), a.warmup, dist if world > 1 else None)
+    mvue_line = {"tokens_per_s": n_tok * world / (mms / max(10, a.steps // 2) / 1000.0),
+                 "ms_per_step": mms / max(10, a.steps // 2),
+                 "note": "dW GEMMs on MVUE-sparsified dY^T / dZ^T (K8 + 2:4 tensor cores), gated_ffn.py:367-373"}
+    del mstep
+
     # ---- dense cuBLAS bf16 baseline on the same box ----
     dense = None
     if not a.no_dense:
@@ -455,6 +465,8 @@ def run_ours(a, cfg):
                        "tokens_per_rank": n_tok, "mask_refresh_every": REFRESH, "lambda_w": LAMBDA,
                        "parallelism": f"dp{world}", "l2": "per-step working set ~1 GB > 126 MB L2 (no flush)"},
             "dense_tokens_per_s": dense, "speedup_vs_dense": (value / dense) if dense else None,
+            "variants": {"mvue_dw": dict(mvue_line, speedup_vs_dense=(mvue_line["tokens_per_s"] / dense)
+                                         if dense else None)},
             "mask_search": mask_search,
             "roofline": roof,
             "kernels": per_kernel,
