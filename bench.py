@@ -254,8 +254,8 @@ class SparseStep:
             E.compress_values(self.w2, self.op_out)
         st = E.ffn_forward(x, self.op_in, self.bias, self.op_out, self.act, fused=True)
         g = E.ffn_backward(st, dy, self.op_in, self.op_out, self.act, w_in_dense=self.w_in, w2_dense=self.w2,
-                           lam=LAMBDA / self.world, dw_in_out=self.dw_in, dw2_out=self.dw2, mvue=self.mvue,
-                           rng_seed=self.t)
+                           lam=LAMBDA / self.world, dw_in_out=self.dw_in, dw2_out=self.dw2, mvue=bool(self.mvue),
+                           rng_seed=self.t, mvue_exact=self.mvue == "exact")
         self.dbias.copy_(g.dbias_in)
         if self.world > 1:
             self.torch.distributed.all_reduce(self.bucket, group=self.pg)
@@ -360,12 +360,17 @@ def run_ours(a, cfg):
     value = n_tok * world / (ms_step / 1000.0)
 
     # ---- variant: MVUE-sparsified dW (the reference default fst_backward(mvue=True)) ----
-    mstep = SparseStep(w_in, bias, w2, cfg["act"], world, pg, mvue=True)
-    mms, _ = time_loop(lambda: mstep(x, dy), max(10, a.steps // 2), a.warmup, dist if world > 1 else None)
-    mvue_line = {"tokens_per_s": n_tok * world / (mms / max(10, a.steps // 2) / 1000.0),
-                 "ms_per_step": mms / max(10, a.steps // 2),
-                 "note": "dW GEMMs on MVUE-sparsified dY^T / dZ^T (K8 + 2:4 tensor cores), gated_ffn.py:367-373"}
-    del mstep
+    variants = {}
+    for mode in ("fast", "exact"):
+        mstep = SparseStep(w_in, bias, w2, cfg["act"], world, pg, mvue=mode)
+        msteps = max(10, a.steps // 4)
+        mms, _ = time_loop(lambda: mstep(x, dy), msteps, a.warmup, dist if world > 1 else None)
+        variants[f"mvue_dw_{mode}"] = {
+            "tokens_per_s": n_tok * world / (mms / msteps / 1000.0), "ms_per_step": mms / msteps,
+            "note": ("dW GEMMs on MVUE-sparsified dY^T / dZ^T (K8 + 2:4 tensor cores), gated_ffn.py:367-373; "
+                     + ("float64 + numpy PCG64 stream, bit-identical draws" if mode == "exact"
+                        else "fp32 + counter RNG, unbiased"))}
+        del mstep
 
     # ---- dense cuBLAS bf16 baseline on the same box ----
     dense = None
@@ -465,8 +470,8 @@ def run_ours(a, cfg):
                        "tokens_per_rank": n_tok, "mask_refresh_every": REFRESH, "lambda_w": LAMBDA,
                        "parallelism": f"dp{world}", "l2": "per-step working set ~1 GB > 126 MB L2 (no flush)"},
             "dense_tokens_per_s": dense, "speedup_vs_dense": (value / dense) if dense else None,
-            "variants": {"mvue_dw": dict(mvue_line, speedup_vs_dense=(mvue_line["tokens_per_s"] / dense)
-                                         if dense else None)},
+            "variants": {k: dict(v, speedup_vs_dense=(v["tokens_per_s"] / dense) if dense else None)
+                         for k, v in variants.items()},
             "mask_search": mask_search,
             "roofline": roof,
             "kernels": per_kernel,

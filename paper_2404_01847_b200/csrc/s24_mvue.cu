@@ -140,6 +140,67 @@ __device__ __forceinline__ int mvue_group(const double (&g)[4], double u, double
   return idx;
 }
 
+// Throughput mode: the same estimator in fp32 (inclusion probabilities, greedy
+// pair fill, cumulative draw, g / pi) with a counter-based uniform per group.
+// Unbiased like the reference (E[value] = g) but not bit-identical to numpy's
+// stream; selected with exact=0.
+__device__ __forceinline__ int mvue_group_f32(const float (&g)[4], float u, float& v0, float& v1) {
+  float a[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) a[k] = fabsf(g[k]);
+  const float total = ((a[0] + a[1]) + a[2]) + a[3];
+  int fm = 0;
+#pragma unroll
+  for (int k = 1; k < 4; ++k)
+    if (a[k] > a[fm]) fm = k;
+  const float rest = total - a[fm];
+  const bool clamp = a[fm] > rest;
+  int nnz = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) nnz += a[k] != 0.0f;
+  const float sc = clamp ? __frcp_rn(rest) : 2.0f * __frcp_rn(total);
+  float pi[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    pi[k] = (clamp && k == fm) ? 1.0f : fminf(a[k] * sc, 1.0f);
+    if (nnz == 1) pi[k] = a[k] > 0.0f ? 1.0f : (1.0f / 3.0f);
+    if (nnz == 0) pi[k] = 0.5f;
+  }
+  float r0 = pi[0], r1 = pi[1], r2 = pi[2], r3 = pi[3];
+  float s = 0.5f * (((pi[0] + pi[1]) + pi[2]) + pi[3]);
+  const float p01 = fmaxf(fminf(fminf(fminf(r0, r1), s - r2), s - r3), 0.0f);
+  r0 -= p01; r1 -= p01; s -= p01;
+  const float p02 = fmaxf(fminf(fminf(r0, r2), s - r3), 0.0f);
+  r0 -= p02; r2 -= p02; s -= p02;
+  const float p03 = fmaxf(fminf(r0, r3), 0.0f);
+  r3 -= p03; s -= p03;
+  const float p12 = fmaxf(fminf(fminf(r1, r2), s - r3), 0.0f);
+  r1 -= p12; r2 -= p12;
+  const float p13 = fmaxf(fminf(r1, r3), 0.0f);
+  r3 -= p13;
+  const float p23 = fmaxf(fminf(r2, r3), 0.0f);
+  float c[6];
+  c[0] = p01; c[1] = c[0] + p02; c[2] = c[1] + p03; c[3] = c[2] + p12; c[4] = c[3] + p13; c[5] = c[4] + p23;
+  const float draw = u * c[5];
+  int idx = 0;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) idx += c[j] <= draw;
+  idx = min(idx, 5);
+  constexpr int kI0[6] = {0, 0, 0, 1, 1, 2}, kI1[6] = {1, 2, 3, 2, 3, 3};
+  const int i0 = kI0[idx], i1 = kI1[idx];
+  v0 = g[i0] / pi[i0];
+  v1 = g[i1] / pi[i1];
+  return idx;
+}
+
+__device__ __forceinline__ float counter_uniform(uint64_t key, uint64_t ctr) {
+  uint64_t x = key ^ (ctr * 0x9E3779B97F4A7C15ull);
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return static_cast<float>(x >> 40) * (1.0f / 16777216.0f);  // [0, 1) with 24 bits
+}
+
 struct MvueArgs {
   const uint16_t* g;  // n x f token-major (ldg)
   int64_t ldg, n, f, gate_ff;
@@ -148,6 +209,7 @@ struct MvueArgs {
   uint8_t* pairs;     // optional f x n/4 pair indices (tests)
 };
 
+template <bool kExact>
 __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid_constant__ MvueRng rng) {
   __shared__ __align__(16) uint16_t s_g[128 * 136];  // [token][feature], row pitch 136 (272 B)
   __shared__ __align__(16) uint32_t s_e[512];
@@ -167,17 +229,30 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
                                                          : p.gate_ff + 16 * (feat >> 5) + (feat & 31) - 16)
                                     : feat;
   const int64_t grp0 = t0 / 4 + 16 * half;
-  U128 st = pcg_advance(rng, static_cast<uint64_t>(row * (p.n / 4) + grp0));
+  const uint64_t stream0 = static_cast<uint64_t>(row * (p.n / 4) + grp0);
+  U128 st{0, 0};
+  if constexpr (kExact) st = pcg_advance(rng, stream0);
   uint32_t packed[16];
   uint32_t halfwords[4] = {0, 0, 0, 0};
 #pragma unroll 1
   for (int j = 0; j < 16; ++j) {
-    double gv[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) gv[k] = static_cast<double>(bf16_to_f32(s_g[(64 * half + 4 * j + k) * 136 + ml]));
-    const double u = pcg_uniform(st, rng.inc);
     double v0, v1;
-    const int idx = mvue_group(gv, u, v0, v1);
+    int idx;
+    if constexpr (kExact) {
+      double gv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gv[k] = static_cast<double>(bf16_to_f32(s_g[(64 * half + 4 * j + k) * 136 + ml]));
+      const double u = pcg_uniform(st, rng.inc);
+      idx = mvue_group(gv, u, v0, v1);
+    } else {
+      float gv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gv[k] = bf16_to_f32(s_g[(64 * half + 4 * j + k) * 136 + ml]);
+      float f0, f1;
+      idx = mvue_group_f32(gv, counter_uniform(rng.state.lo ^ rng.inc.hi, stream0 + j), f0, f1);
+      v0 = f0;
+      v1 = f1;
+    }
     constexpr uint32_t kNib[6] = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE};  // i0 | i1 << 2
     halfwords[j >> 2] |= kNib[idx] << (4 * (j & 3));
     // f64 -> f32 -> bf16 (the rounding of the reference-side bf16 operand)
@@ -210,7 +285,7 @@ using namespace s24;
 
 extern "C" int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int64_t f, uint64_t state_hi,
                                  uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t gate_ff,
-                                 uint16_t* vals, uint8_t* e, uint8_t* pairs, void* stream) {
+                                 uint16_t* vals, uint8_t* e, uint8_t* pairs, int exact, void* stream) {
   S24_REQUIRE(g && vals, S24_ERR_ARG, "NULL pointer");
   S24_REQUIRE(n % 128 == 0 && f % 128 == 0 && n > 0 && f > 0, S24_ERR_SHAPE,
               "MVUE operand needs tokens and features divisible by 128 (got n=%lld f=%lld)", (long long)n,
@@ -233,6 +308,7 @@ extern "C" int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int6
               "MVUE stream index exceeds the 2^40 jump table");
   MvueArgs a{g, ldg, n, f, gate_ff, vals, e, pairs};
   dim3 grid(static_cast<unsigned>(n / 128), static_cast<unsigned>(f / 128));
-  mvue_tile_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, rng);
+  if (exact) mvue_tile_kernel<true><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, rng);
+  else mvue_tile_kernel<false><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, rng);
   return s24_check_launch("mvue_compress");
 }

@@ -153,10 +153,11 @@ def pcg64_state(seed: int) -> tuple[int, int, int, int]:
     return s >> 64, s & m64, i >> 64, i & m64
 
 
-def mvue_compress(g: torch.Tensor, seed: int, gate_ff: int = 0, want_pairs: bool = False):
+def mvue_compress(g: torch.Tensor, seed: int, gate_ff: int = 0, want_pairs: bool = False, exact: bool = True):
     """K8: MVUE-sparsify g^T (features x tokens) along tokens (sparsity.py:401-413)
     into the tensor-core operand.  g: token-major (N x F) bf16.  Returns
-    (vals F x N/2, E tiles, pairs F x N/4 or None)."""
+    (vals F x N/2, E tiles, pairs F x N/4 or None).  exact=False: fp32 math and a
+    counter-based uniform (unbiased, not numpy's stream) for throughput."""
     n, f = g.shape
     dev = g.device
     vals = torch.empty((f, n // 2), dtype=torch.bfloat16, device=dev)
@@ -165,7 +166,7 @@ def mvue_compress(g: torch.Tensor, seed: int, gate_ff: int = 0, want_pairs: bool
     sh, sl, ih, il = pcg64_state(seed)
     with TIMER("k8_mvue"):
         C.call("s24_mvue_compress", g.data_ptr(), g.stride(0), n, f, sh, sl, ih, il, gate_ff, vals.data_ptr(),
-               e.data_ptr(), C.ptr(pairs), C.stream_of(g))
+               e.data_ptr(), C.ptr(pairs), int(exact), C.stream_of(g))
     return vals, e, pairs
 
 
@@ -256,7 +257,8 @@ class Grads:
 def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: CompressedOperand, act: str,
                  w_in_dense: torch.Tensor | None = None, w2_dense: torch.Tensor | None = None,
                  lam: float = 0.0, dw_in_out: torch.Tensor | None = None,
-                 dw2_out: torch.Tensor | None = None, mvue: bool = False, rng_seed: int = 0) -> Grads:
+                 dw2_out: torch.Tensor | None = None, mvue: bool = False, rng_seed: int = 0,
+                 mvue_exact: bool = True) -> Grads:
     """dA = dY W2~ (out_bwd, W2's transposed orientation) -> dZ (activation
     backward, bias gradient) -> dX = dZ W_in~ (in_bwd); dense dW2 = dY^T A and
     dW_in = dZ^T X with the masked decay lam (1 - M) W fused (gated_ffn.py:327-356).
@@ -294,9 +296,9 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     dw2 = dw2_out if dw2_out is not None else torch.empty((d, d_ff), dtype=torch.float32, device=dev)
     dw_in = dw_in_out if dw_in_out is not None else torch.empty((r_in, d), dtype=torch.float32, device=dev)
     if mvue:
-        v2, e2, _ = mvue_compress(dy, mvue_seed(rng_seed, 1))
+        v2, e2, _ = mvue_compress(dy, mvue_seed(rng_seed, 1), exact=mvue_exact)
         spmm_dw(v2, e2, d, n, st.a, True, d_ff, dw2, w2_dense, w2.idx, lam, tag="k8_spmm_dw2")
-        v1, e1, _ = mvue_compress(dz, mvue_seed(rng_seed, 2), gate_ff)
+        v1, e1, _ = mvue_compress(dz, mvue_seed(rng_seed, 2), gate_ff, exact=mvue_exact)
         spmm_dw(v1, e1, r_in, n, st.x, True, d, dw_in, w_in_dense, w_in.idx, lam, gate_ff, tag="k8_spmm_dw_in")
     else:
         gemm_dw(dy, True, st.a, True, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")

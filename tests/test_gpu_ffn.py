@@ -222,11 +222,16 @@ def test_mvue_sparse_dw_gemm_and_unbiasedness():
     ref = o.round_bf16(_mvue_dense(np.ascontiguousarray(gx.T), 99)) @ b
     assert normwise_rel(out.cpu().numpy(), ref) < 2e-3
     dense = gx.T @ b
+    for exact in (True, False):
+        _check_unbiased(E, gd, bd, f, n, dcols, out, dense, exact)
+
+
+def _check_unbiased(E, gd, bd, f, n, dcols, out, dense, exact):
     acc = np.zeros_like(dense)
     acc2 = np.zeros_like(dense)
     trials = 48
     for s in range(trials):
-        vals, e, _ = E.mvue_compress(gd, 1000 + s)
+        vals, e, _ = E.mvue_compress(gd, 1000 + s, exact=exact)
         E.spmm_dw(vals, e, f, n, bd, True, dcols, out)
         r = out.double().cpu().numpy()
         acc += r
