@@ -158,7 +158,7 @@ __device__ __forceinline__ int mvue_group_f32(const float (&g)[4], float u, floa
   int nnz = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) nnz += a[k] != 0.0f;
-  const float sc = clamp ? __frcp_rn(rest) : 2.0f * __frcp_rn(total);
+  const float sc = clamp ? __fdividef(1.0f, rest) : __fdividef(2.0f, total);
   float pi[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -188,8 +188,8 @@ __device__ __forceinline__ int mvue_group_f32(const float (&g)[4], float u, floa
   idx = min(idx, 5);
   constexpr int kI0[6] = {0, 0, 0, 1, 1, 2}, kI1[6] = {1, 2, 3, 2, 3, 3};
   const int i0 = kI0[idx], i1 = kI1[idx];
-  v0 = g[i0] / pi[i0];
-  v1 = g[i1] / pi[i1];
+  v0 = __fdividef(g[i0], pi[i0]);
+  v1 = __fdividef(g[i1], pi[i1]);
   return idx;
 }
 
@@ -232,9 +232,9 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
   const uint64_t stream0 = static_cast<uint64_t>(row * (p.n / 4) + grp0);
   U128 st{0, 0};
   if constexpr (kExact) st = pcg_advance(rng, stream0);
-  uint32_t packed[16];
   uint32_t halfwords[4] = {0, 0, 0, 0};
-#pragma unroll 1
+  uint32_t packed[16];
+#pragma unroll(kExact ? 1 : 16)
   for (int j = 0; j < 16; ++j) {
     double v0, v1;
     int idx;
@@ -260,10 +260,16 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
                 (static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v1))) << 16);
     if (p.pairs) p.pairs[feat * (p.n / 4) + grp0 + j] = static_cast<uint8_t>(idx);
   }
-  // kept values: 32 bf16 (64 B) of row feat
-  uint4* dst = reinterpret_cast<uint4*>(p.vals + feat * (p.n / 2) + t0 / 2 + 32 * half);
+  // kept values staged in the (now free) input tile, then streamed as whole 128-byte rows
+  __syncthreads();
+  uint32_t* s_v = reinterpret_cast<uint32_t*>(s_g);  // [feature][32 words + 1 pad]
 #pragma unroll
-  for (int q = 0; q < 4; ++q) dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+  for (int j = 0; j < 16; ++j) s_v[ml * 33 + 16 * half + j] = packed[j];
+  __syncthreads();
+  for (int rr = tid >> 5; rr < 128; rr += 8) {
+    const int lane = tid & 31;
+    reinterpret_cast<uint32_t*>(p.vals + (f0 + rr) * (p.n / 2) + t0 / 2)[lane] = s_v[rr * 33 + lane];
+  }
   // metadata: halfword w covers tokens 64 half + 16 w .. +15 of row ml
   if (p.e) {
 #pragma unroll
