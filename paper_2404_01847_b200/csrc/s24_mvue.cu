@@ -133,38 +133,34 @@ __device__ __forceinline__ int mvue_group(const double (&g)[4], double u, double
 #pragma unroll
   for (int j = 0; j < 6; ++j) idx += c[j] <= draw;
   idx = min(idx, 5);
-  constexpr int kI0[6] = {0, 0, 0, 1, 1, 2}, kI1[6] = {1, 2, 3, 2, 3, 3};
-  const int i0 = kI0[idx], i1 = kI1[idx];
-  v0 = ddiv(g[i0], pi[i0]);
-  v1 = ddiv(g[i1], pi[i1]);
+  // register selects, not indexed arrays (dynamic indexing would go to local memory)
+  const double g0 = idx < 3 ? g[0] : (idx < 5 ? g[1] : g[2]);
+  const double q0 = idx < 3 ? pi[0] : (idx < 5 ? pi[1] : pi[2]);
+  const bool s1 = idx == 0, s2 = idx == 1 || idx == 3;
+  const double g1 = s1 ? g[1] : (s2 ? g[2] : g[3]);
+  const double q1 = s1 ? pi[1] : (s2 ? pi[2] : pi[3]);
+  v0 = ddiv(g0, q0);
+  v1 = ddiv(g1, q1);
   return idx;
 }
 
 // Throughput mode: the same estimator in fp32 (inclusion probabilities, greedy
 // pair fill, cumulative draw, g / pi) with a counter-based uniform per group.
 // Unbiased like the reference (E[value] = g) but not bit-identical to numpy's
-// stream; selected with exact=0.
-__device__ __forceinline__ int mvue_group_f32(const float (&g)[4], float u, float& v0, float& v1) {
-  float a[4];
+// stream; selected with exact=0.  Branch-free: pi_k = min(a_k * inv, 1) covers
+// both the plain (2 a / total) and the clamped (1 for the max, a / rest) case.
+__device__ __forceinline__ uint32_t mvue_nibble_f32(const float (&g)[4], float u, float& v0, float& v1) {
+  const float a0 = fabsf(g[0]), a1 = fabsf(g[1]), a2 = fabsf(g[2]), a3 = fabsf(g[3]);
+  const float total = ((a0 + a1) + a2) + a3;
+  const float amax = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+  const float rest = total - amax;
+  const bool clamp = amax > rest;
+  const float inv = __frcp_rn(clamp ? rest : 0.5f * total);
+  float pi[4] = {fminf(a0 * inv, 1.0f), fminf(a1 * inv, 1.0f), fminf(a2 * inv, 1.0f), fminf(a3 * inv, 1.0f)};
+  if (rest == 0.0f) {  // at most one nonzero: it is kept, the zeros share 1 (or all 0.5)
+    const float z = total > 0.0f ? (1.0f / 3.0f) : 0.5f;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) a[k] = fabsf(g[k]);
-  const float total = ((a[0] + a[1]) + a[2]) + a[3];
-  int fm = 0;
-#pragma unroll
-  for (int k = 1; k < 4; ++k)
-    if (a[k] > a[fm]) fm = k;
-  const float rest = total - a[fm];
-  const bool clamp = a[fm] > rest;
-  int nnz = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) nnz += a[k] != 0.0f;
-  const float sc = clamp ? __fdividef(1.0f, rest) : __fdividef(2.0f, total);
-  float pi[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    pi[k] = (clamp && k == fm) ? 1.0f : fminf(a[k] * sc, 1.0f);
-    if (nnz == 1) pi[k] = a[k] > 0.0f ? 1.0f : (1.0f / 3.0f);
-    if (nnz == 0) pi[k] = 0.5f;
+    for (int k = 0; k < 4; ++k) pi[k] = (k == 0 ? a0 : k == 1 ? a1 : k == 2 ? a2 : a3) > 0.0f ? 1.0f : z;
   }
   float r0 = pi[0], r1 = pi[1], r2 = pi[2], r3 = pi[3];
   float s = 0.5f * (((pi[0] + pi[1]) + pi[2]) + pi[3]);
@@ -179,26 +175,32 @@ __device__ __forceinline__ int mvue_group_f32(const float (&g)[4], float u, floa
   const float p13 = fmaxf(fminf(r1, r3), 0.0f);
   r3 -= p13;
   const float p23 = fmaxf(fminf(r2, r3), 0.0f);
-  float c[6];
-  c[0] = p01; c[1] = c[0] + p02; c[2] = c[1] + p03; c[3] = c[2] + p12; c[4] = c[3] + p13; c[5] = c[4] + p23;
-  const float draw = u * c[5];
-  int idx = 0;
-#pragma unroll
-  for (int j = 0; j < 6; ++j) idx += c[j] <= draw;
-  idx = min(idx, 5);
-  constexpr int kI0[6] = {0, 0, 0, 1, 1, 2}, kI1[6] = {1, 2, 3, 2, 3, 3};
-  const int i0 = kI0[idx], i1 = kI1[idx];
-  v0 = __fdividef(g[i0], pi[i0]);
-  v1 = __fdividef(g[i1], pi[i1]);
-  return idx;
+  const float c0 = p01, c1 = c0 + p02, c2 = c1 + p03, c3 = c2 + p12, c4 = c3 + p13, c5 = c4 + p23;
+  const float draw = u * c5;
+  const int idx = min((c0 <= draw) + (c1 <= draw) + (c2 <= draw) + (c3 <= draw) + (c4 <= draw) + (c5 <= draw), 5);
+  const float g0 = idx < 3 ? g[0] : (idx < 5 ? g[1] : g[2]);
+  const float q0 = idx < 3 ? pi[0] : (idx < 5 ? pi[1] : pi[2]);
+  const bool s1 = idx == 0, s2 = idx == 1 || idx == 3;
+  const float g1 = s1 ? g[1] : (s2 ? g[2] : g[3]);
+  const float q1 = s1 ? pi[1] : (s2 ? pi[2] : pi[3]);
+  v0 = __fdividef(g0, q0);
+  v1 = __fdividef(g1, q1);
+  return static_cast<uint32_t>(idx);
 }
 
-__device__ __forceinline__ float counter_uniform(uint64_t key, uint64_t ctr) {
-  uint64_t x = key ^ (ctr * 0x9E3779B97F4A7C15ull);
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  x ^= x >> 31;
-  return static_cast<float>(x >> 40) * (1.0f / 16777216.0f);  // [0, 1) with 24 bits
+// murmur3 finaliser: a bijection on 32 bits, so distinct group counters under
+// one key never share a uniform
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+__device__ __forceinline__ float counter_uniform(uint32_t k1, uint32_t k2, uint32_t ctr) {
+  const uint32_t h = fmix32(fmix32(ctr ^ k1) + k2);
+  return static_cast<float>(h >> 8) * (1.0f / 16777216.0f);  // [0, 1) with 24 bits
 }
 
 struct MvueArgs {
@@ -216,11 +218,20 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
   const int tid = threadIdx.x;
   const int64_t f0 = static_cast<int64_t>(blockIdx.y) * 128, t0 = static_cast<int64_t>(blockIdx.x) * 128;
   for (int i = tid; i < 512; i += 256) s_e[i] = 0;
-  // coalesced tile load: 128 token rows x 256 bytes
-  for (int i = tid; i < 128 * 16; i += 256) {
-    const int tr = i >> 4, ch = i & 15;
-    const uint4 x = __ldg(reinterpret_cast<const uint4*>(p.g + (t0 + tr) * p.ldg + f0 + ch * 8));
-    *reinterpret_cast<uint4*>(&s_g[tr * 136 + ch * 8]) = x;
+  // coalesced tile load: 128 token rows x 256 bytes; all 8 loads of a thread are in
+  // flight before the first smem store (one DRAM latency per CTA, not eight)
+  {
+    uint4 buf[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int i = tid + 256 * q, tr = i >> 4, ch = i & 15;
+      buf[q] = __ldg(reinterpret_cast<const uint4*>(p.g + (t0 + tr) * p.ldg + f0 + ch * 8));
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int i = tid + 256 * q, tr = i >> 4, ch = i & 15;
+      *reinterpret_cast<uint4*>(&s_g[tr * 136 + ch * 8]) = buf[q];
+    }
   }
   __syncthreads();
   const int ml = tid & 127, half = tid >> 7;  // feature in tile, token half (64 tokens = 16 groups)
@@ -234,31 +245,38 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
   if constexpr (kExact) st = pcg_advance(rng, stream0);
   uint32_t halfwords[4] = {0, 0, 0, 0};
   uint32_t packed[16];
-#pragma unroll(kExact ? 1 : 16)
+  uint32_t pidx[4] = {0, 0, 0, 0};
+#pragma unroll
   for (int j = 0; j < 16; ++j) {
-    double v0, v1;
     int idx;
     if constexpr (kExact) {
       double gv[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) gv[k] = static_cast<double>(bf16_to_f32(s_g[(64 * half + 4 * j + k) * 136 + ml]));
       const double u = pcg_uniform(st, rng.inc);
+      double v0, v1;
       idx = mvue_group(gv, u, v0, v1);
+      // f64 -> f32 -> bf16 (the rounding of the reference-side bf16 operand)
+      packed[j] = static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v0))) |
+                  (static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v1))) << 16);
     } else {
       float gv[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) gv[k] = bf16_to_f32(s_g[(64 * half + 4 * j + k) * 136 + ml]);
       float f0, f1;
-      idx = mvue_group_f32(gv, counter_uniform(rng.state.lo ^ rng.inc.hi, stream0 + j), f0, f1);
-      v0 = f0;
-      v1 = f1;
+      const uint32_t k1 = static_cast<uint32_t>(rng.state.lo ^ (rng.state.lo >> 32)),
+                     k2 = static_cast<uint32_t>(rng.inc.hi ^ (rng.inc.hi >> 32));
+      idx = static_cast<int>(mvue_nibble_f32(gv, counter_uniform(k1, k2, static_cast<uint32_t>(stream0 + j)), f0, f1));
+      packed[j] = static_cast<uint32_t>(f32_to_bf16(f0)) | (static_cast<uint32_t>(f32_to_bf16(f1)) << 16);
     }
-    constexpr uint32_t kNib[6] = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE};  // i0 | i1 << 2
-    halfwords[j >> 2] |= kNib[idx] << (4 * (j & 3));
-    // f64 -> f32 -> bf16 (the rounding of the reference-side bf16 operand)
-    packed[j] = static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v0))) |
-                (static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v1))) << 16);
-    if (p.pairs) p.pairs[feat * (p.n / 4) + grp0 + j] = static_cast<uint8_t>(idx);
+    // nibble i0 | i1 << 2 of pair idx = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE}[idx]
+    const uint32_t nib = (0xED9C84u >> (4 * idx)) & 0xFu;
+    halfwords[j >> 2] |= nib << (4 * (j & 3));
+    pidx[j >> 2] |= static_cast<uint32_t>(idx) << (8 * (j & 3));
+  }
+  if (p.pairs) {
+    uint4* dp = reinterpret_cast<uint4*>(p.pairs + feat * (p.n / 4) + grp0);
+    *dp = make_uint4(pidx[0], pidx[1], pidx[2], pidx[3]);
   }
   // kept values staged in the (now free) input tile, then streamed as whole 128-byte rows
   __syncthreads();
@@ -312,6 +330,8 @@ extern "C" int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int6
   }
   S24_REQUIRE(static_cast<double>(f) * static_cast<double>(n / 4) < 1099511627776.0, S24_ERR_SHAPE,
               "MVUE stream index exceeds the 2^40 jump table");
+  S24_REQUIRE(exact || static_cast<double>(f) * static_cast<double>(n / 4) < 4294967296.0, S24_ERR_SHAPE,
+              "fast MVUE: group counter exceeds 2^32 (use exact mode or split the call)");
   MvueArgs a{g, ldg, n, f, gate_ff, vals, e, pairs};
   dim3 grid(static_cast<unsigned>(n / 128), static_cast<unsigned>(f / 128));
   if (exact) mvue_tile_kernel<true><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, rng);
