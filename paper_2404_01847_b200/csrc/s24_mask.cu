@@ -365,6 +365,83 @@ __global__ void __launch_bounds__(kThreads, 2) mask_tile_kernel(MaskArgs p) {
 }
 
 // ---------------------------------------------------------------------------
+// K2 fast path: the per-step prune of bf16 weights into both value orientations
+// (metadata cached from the last refresh).  Same outputs as mask_tile_kernel with
+// fwd_e = bwd_e = NULL, restructured for bandwidth: 512 threads per 128 x 128
+// tile, each owning 4 rows x 8 columns (two 4x4 blocks, one 16-byte load per
+// row), so a thread holds 16 data registers and 2-3 CTAs fit per SM.
+
+constexpr int kPruneThreads = 512;
+
+// PRMT selector picking elements i0 < i1 of a 4 x bf16 group held in two words
+__device__ __forceinline__ uint32_t pair_selector(uint32_t nib) {
+  const uint32_t i0 = nib & 3u, i1 = nib >> 2;
+  return (2 * i0) | ((2 * i0 + 1) << 4) | ((2 * i1) << 8) | ((2 * i1 + 1) << 12);
+}
+
+__global__ void __launch_bounds__(kPruneThreads, 2) prune_bf16_kernel(MaskArgs p) {
+  __shared__ uint32_t s_bv[128 * 32];  // W^T tile: 128 rows x 32 words (64 kept bf16)
+  __shared__ uint4 s_sel[90];          // per pattern: row selectors (x, y), column selectors (z, w)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tr = blockIdx.y, tc = blockIdx.x;
+  const int br = 2 * warp + (lane >> 4);  // block row in tile, 0..31
+  const int c0 = 8 * (lane & 15);         // first column in tile, 0..120
+  const int64_t grow0 = tr * kTile + 4 * br, gcol0 = tc * kTile + c0;
+  const int64_t in_row0 = p.perm_ff > 0 ? gate_row(grow0, p.perm_ff) : grow0;
+  const uint16_t* w = static_cast<const uint16_t*>(p.w);
+  uint4 v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const uint4*>(w + (in_row0 + i) * p.cols + gcol0));
+  const uint32_t t2 = *reinterpret_cast<const uint16_t*>(p.idx_in + (grow0 / 4) * (p.cols / 4) + gcol0 / 4);
+  if (threadIdx.x < 90) {
+    const uint32_t bits16 = c_pat_bits[threadIdx.x];
+    uint32_t r[4], c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      r[k] = pair_selector(nib_of_mask((bits16 >> (4 * k)) & 0xFu));
+      c[k] = pair_selector(nib_of_mask(col_mask(bits16, k)));
+    }
+    s_sel[threadIdx.x] = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+  }
+  __syncthreads();
+  uint32_t fw[4][2];
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    uint32_t t = (t2 >> (8 * b)) & 0xFFu;
+    const uint4 sel = s_sel[t > 89 ? 0 : t];
+    // fwd orientation: row i keeps 2 of its 4 elements (one byte permute)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t si = ((i < 2 ? sel.x : sel.y) >> (16 * (i & 1))) & 0xFFFFu;
+      fw[i][b] = __byte_perm((&v[i].x)[2 * b], (&v[i].x)[2 * b + 1], si);
+    }
+    // bwd orientation (W^T): transpose column j into two words, then keep 2 of 4.
+    // Word (mp, br) sits at mp * 32 + (br + 2 (mp / 8)) % 32: the 32 lanes of a
+    // warp (16 column strips x 2 block rows) hit 32 distinct banks.
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int wj = 2 * b + (j >> 1);
+      const uint32_t hsel = (j & 1) ? 0x7632u : 0x5410u;
+      const uint32_t col01 = __byte_perm((&v[0].x)[wj], (&v[1].x)[wj], hsel);
+      const uint32_t col23 = __byte_perm((&v[2].x)[wj], (&v[3].x)[wj], hsel);
+      const uint32_t sj = ((j < 2 ? sel.z : sel.w) >> (16 * (j & 1))) & 0xFFFFu;
+      const int mp = c0 + 4 * b + j;
+      s_bv[mp * 32 + ((br + 2 * (mp >> 3)) & 31)] = __byte_perm(col01, col23, sj);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    *reinterpret_cast<uint2*>(p.fwd_vals + (grow0 + i) * (p.cols / 2) + gcol0 / 2) = make_uint2(fw[i][0], fw[i][1]);
+  __syncthreads();
+  const int64_t kcol = tr * (kTile / 2) + 2 * lane;
+#pragma unroll 4
+  for (int rr = warp; rr < kTile; rr += kPruneThreads / 32) {
+    const uint32_t val = s_bv[rr * 32 + ((lane + 2 * (rr >> 3)) & 31)];
+    *reinterpret_cast<uint32_t*>(p.bwd_vals + (tc * kTile + rr) * (p.rows / 2) + kcol) = val;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // small conversion kernels
 
 __global__ void idx_to_bits_kernel(const uint8_t* __restrict__ idx, int64_t rows, int64_t cols,
@@ -487,6 +564,11 @@ static int launch_mask(const MaskArgs& a, int dtype, bool search, cudaStream_t s
     else if (dtype == S24_F32) mask_tile_kernel<S24_F32, true, false><<<grid, kThreads, 0, st>>>(a);
     else mask_tile_kernel<S24_F64, true, false><<<grid, kThreads, 0, st>>>(a);
   } else {
+    if (dtype == S24_BF16 && a.fwd_e == nullptr && a.bwd_e == nullptr && a.fwd_vals != nullptr &&
+        a.bwd_vals != nullptr && a.rows % kTile == 0 && a.cols % kTile == 0) {
+      prune_bf16_kernel<<<grid, kPruneThreads, 0, st>>>(a);
+      return s24_check_launch("prune_compress");
+    }
     if (narrow) mask_tile_kernel<S24_BF16, false, true><<<grid, kThreads, 0, st>>>(a);
     else if (dtype == S24_BF16) mask_tile_kernel<S24_BF16, false, false><<<grid, kThreads, 0, st>>>(a);
     else if (dtype == S24_F32) mask_tile_kernel<S24_F32, false, false><<<grid, kThreads, 0, st>>>(a);

@@ -196,3 +196,33 @@ def test_gated_interleave_masks_are_reference_masks_permuted():
     orig = np.where(p % 32 < 16, 16 * (p // 32) + p % 32, d_ff + 16 * (p // 32) + p % 32 - 16)
     kv, _ = o.compress_rowwise(w[orig], o.transposable_search_conv(w)[orig])
     np.testing.assert_array_equal(bf16_bits_of(op.fwd_vals), o.bf16_bits(kv))
+
+
+@pytest.mark.parametrize("shape,perm_ff", [((256, 384), 0), ((512, 128), 256), ((384, 1024), 0)])
+def test_k2_fast_prune_matches_oracle(shape, perm_ff):
+    """K2 bf16 fast path (tile-aligned shapes, no metadata): both value
+    orientations bit-equal to the oracle's compress of the cached mask, for the
+    plain and the u/v-interleaved (gated) row order."""
+    from paper_2404_01847_b200.engine import CompressedOperand, compress_values, search_compress
+
+    rows, cols = shape
+    w = o.round_bf16(o.det_normal(shape, seed=rows + 7 * cols))
+    wd = to_dev_bf16(w)
+    op = CompressedOperand.empty(rows, cols, "cuda", perm_ff=perm_ff)
+    search_compress(wd, op)
+    fv1, bv1 = op.fwd_vals.clone(), op.bwd_vals.clone()
+    w2 = o.round_bf16(o.det_normal(shape, seed=rows + 7 * cols + 1))  # new values, same (cached) mask
+    op.fwd_vals.zero_()
+    op.bwd_vals.zero_()
+    compress_values(to_dev_bf16(w2), op)
+    bits = o.idx_to_bits(op.mask_idx().cpu().numpy())
+    p = np.arange(rows)
+    order = p if perm_ff == 0 else np.where(p % 32 < 16, 16 * (p // 32) + p % 32, perm_ff + 16 * (p // 32) + p % 32 - 16)
+    kv, _ = o.compress_rowwise(w2[order], bits[order])
+    np.testing.assert_array_equal(bf16_bits_of(op.fwd_vals), o.bf16_bits(kv))
+    kb, _ = o.compress_rowwise(np.ascontiguousarray(w2[order].T), np.ascontiguousarray(bits[order].T))
+    np.testing.assert_array_equal(bf16_bits_of(op.bwd_vals), o.bf16_bits(kb))
+    # and K2 on the original values reproduces K1's fused compress
+    compress_values(wd, op)
+    assert torch.equal(op.fwd_vals.view(torch.int16), fv1.view(torch.int16))
+    assert torch.equal(op.bwd_vals.view(torch.int16), bv1.view(torch.int16))
