@@ -24,6 +24,7 @@
 // memory, then written as contiguous lines).
 #include "s24_common.cuh"
 #include "s24_patterns.h"
+#include "s24_search_tree.h"
 
 namespace s24 {
 
@@ -95,7 +96,6 @@ __device__ __forceinline__ int search_block_bf16(const uint16_t (&h)[16]) {
   int v[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = static_cast<int>(man[i] << (ee[i] - emin + 7));
-  constexpr uint16_t kRows[90] = S24_PATTERN_ROWS;
   constexpr int kLo[6] = S24_PAIR_LO;
   constexpr int kHi[6] = S24_PAIR_HI;
   int rp[4][6];
@@ -103,14 +103,7 @@ __device__ __forceinline__ int search_block_bf16(const uint16_t (&h)[16]) {
   for (int r = 0; r < 4; ++r)
 #pragma unroll
     for (int p = 0; p < 6; ++p) rp[r][p] = v[4 * r + kLo[p]] + v[4 * r + kHi[p]];
-  int key = 0;
-#pragma unroll
-  for (int t = 0; t < 90; ++t) {
-    const int p0 = kRows[t] & 15, p1 = (kRows[t] >> 4) & 15, p2 = (kRows[t] >> 8) & 15, p3 = kRows[t] >> 12;
-    const int k = (rp[0][p0] + rp[1][p1]) + (rp[2][p2] + rp[3][p3]) + (127 - t);
-    key = max(key, k);
-  }
-  return 127 - (key & 127);
+  return s24_search_tree(rp);
 }
 
 template <int kDType>
@@ -442,6 +435,185 @@ __global__ void __launch_bounds__(kPruneThreads, 2) prune_bf16_kernel(MaskArgs p
 }
 
 // ---------------------------------------------------------------------------
+// K1 fast path: bf16 search fused with compression for tile-aligned weights.
+// Same thread map as prune_bf16_kernel (4 rows x 8 columns = two 4x4 blocks per
+// thread); kept values via byte permutes, metadata nibbles from a per-pattern
+// table, E-tile bytes assembled without shared-memory atomics.
+
+// integer search on one block given as 4 rows x 2 words (bf16 pairs); falls back
+// to the float64 reference-order path for exponent spans > 13
+__device__ __forceinline__ int search_block_bf16w(const uint32_t (&wd)[8]) {
+  uint32_t h[16];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[4 * r + k] = (wd[2 * r + (k >> 1)] >> (16 * (k & 1))) & 0x7FFFu;
+  // magnitudes as exact f32; positive float bits order like the values, so the
+  // exponent range over nonzero entries comes from integer max / min(bits - 1)
+  float f[16];
+  uint32_t bmax = 0, bmin1 = 0xFFFFFFFFu;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t fb = h[i] << 16;
+    f[i] = __uint_as_float(fb);
+    bmax = max(bmax, fb);
+    bmin1 = min(bmin1, fb - 1u);
+  }
+  if (bmax == 0) return 0;  // all-zero block: every score ties -> pattern 0
+  const int emax = static_cast<int>(bmax >> 23), emin = static_cast<int>((bmin1 + 1u) >> 23);
+  // span > 13 (sums need > 24 bits), inf/nan, or tiny values (scale not representable):
+  // the float64 reference-order path
+  if (emax - emin > 13 || emax == 0xFF || emin < 8) {
+    double a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = static_cast<double>(f[i]);
+    return search_block_f64(a);
+  }
+  // |w| * 2^(134 - emin) is an integer < 2^21 (8-bit significand, span <= 13);
+  // adding 1.5 * 2^23 puts it in the low mantissa bits exactly, and the integer
+  // is pre-scaled by 128 for the tie-break bits: v = (bits - 0x4B400000) << 7
+  const float scale = __uint_as_float(static_cast<uint32_t>(261 - emin) << 23);
+  int v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    v[i] = static_cast<int>(__float_as_uint(__fmaf_rn(f[i], scale, 12582912.0f)) * 128u - (0x4B400000u << 7));
+  constexpr int kLo[6] = S24_PAIR_LO;
+  constexpr int kHi[6] = S24_PAIR_HI;
+  int rp[4][6];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) rp[r][q] = v[4 * r + kLo[q]] + v[4 * r + kHi[q]];
+  return s24_search_tree(rp);
+}
+
+__global__ void __launch_bounds__(kPruneThreads, 1) search_bf16_kernel(MaskArgs p) {
+  __shared__ uint32_t s_bv[128 * 32];
+  __shared__ __align__(16) uint32_t s_fe[512];
+  __shared__ __align__(16) uint32_t s_be[512];
+  __shared__ uint4 s_sel[90];
+  __shared__ uint32_t s_nib[90];  // fwd row nibbles (bits 0-15) | bwd column nibbles (bits 16-31)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tr = blockIdx.y, tc = blockIdx.x;
+  const int br = 2 * warp + (lane >> 4);
+  const int c0 = 8 * (lane & 15);
+  const int64_t grow0 = tr * kTile + 4 * br, gcol0 = tc * kTile + c0;
+  const int64_t in_row0 = p.perm_ff > 0 ? gate_row(grow0, p.perm_ff) : grow0;
+  const uint16_t* w = static_cast<const uint16_t*>(p.w);
+  uint4 v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const uint4*>(w + (in_row0 + i) * p.cols + gcol0));
+  if (threadIdx.x < 90) {
+    const uint32_t bits16 = c_pat_bits[threadIdx.x];
+    uint32_t r[4], c[4], nf = 0, nb = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t rn = nib_of_mask((bits16 >> (4 * k)) & 0xFu), cn = nib_of_mask(col_mask(bits16, k));
+      r[k] = pair_selector(rn);
+      c[k] = pair_selector(cn);
+      nf |= rn << (4 * k);
+      nb |= cn << (4 * k);
+    }
+    s_sel[threadIdx.x] = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+    s_nib[threadIdx.x] = nf | (nb << 16);
+  }
+  for (int i = threadIdx.x; i < 512; i += kPruneThreads) {
+    s_fe[i] = 0;
+    s_be[i] = 0;
+  }
+  int pat[2];
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    uint32_t wd[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      wd[2 * i] = (&v[i].x)[2 * b];
+      wd[2 * i + 1] = (&v[i].x)[2 * b + 1];
+    }
+    pat[b] = search_block_bf16w(wd);
+  }
+  *reinterpret_cast<uint16_t*>(p.idx_out + (grow0 / 4) * (p.cols / 4) + gcol0 / 4) =
+      static_cast<uint16_t>(pat[0] | (pat[1] << 8));
+  __syncthreads();  // tables ready
+  const uint32_t n0 = s_nib[pat[0]], n1 = s_nib[pat[1]];
+  // fwd E: row m = 4 br + i holds groups c0/4, c0/4 + 1 -> one byte of its halfword
+  if (p.fwd_e) {
+    uint8_t* fe = reinterpret_cast<uint8_t*>(s_fe);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int m = 4 * br + i;
+      const int L = (m & 7) + 8 * ((c0 & 31) >> 4) + 16 * (m >> 4);
+      const int c = c0 >> 5, h = (m >> 3) & 1;
+      fe[2 * (L * 8 + c * 2 + h) + ((c0 >> 3) & 1)] =
+          static_cast<uint8_t>(((n0 >> (4 * i)) & 0xFu) | (((n1 >> (4 * i)) & 0xFu) << 4));
+    }
+  }
+  // bwd E: W^T row mp = c0 + 4b + j, group br; block rows 2w (lane < 16) and 2w + 1
+  // (lane + 16) share one byte -> exchange the eight column nibbles once
+  if (p.bwd_e) {
+    const uint32_t mine = (n0 >> 16) | (n1 & 0xFFFF0000u);  // nibble 4b + j
+    const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, 16);
+    const uint32_t lo = lane < 16 ? mine : other, hi = lane < 16 ? other : mine;
+    uint8_t* be = reinterpret_cast<uint8_t*>(s_be);
+    const int brp = br & ~1;  // even block row of the pair
+    const int c = brp >> 3, byte_in_half = (brp >> 1) & 1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 4 * (lane >> 4) + q;  // lanes < 16: columns 0-3, lanes >= 16: columns 4-7
+      const int mp = c0 + k;
+      const int L = (mp & 7) + 16 * (mp >> 4) + 8 * ((brp >> 2) & 1);
+      const int h = (mp >> 3) & 1;
+      be[4 * (L * 4 + c) + 2 * h + byte_in_half] =
+          static_cast<uint8_t>(((lo >> (4 * k)) & 0xFu) | (((hi >> (4 * k)) & 0xFu) << 4));
+    }
+  }
+  uint32_t fw[4][2];
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    const uint4 sel = s_sel[pat[b]];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t si = ((i < 2 ? sel.x : sel.y) >> (16 * (i & 1))) & 0xFFFFu;
+      fw[i][b] = __byte_perm((&v[i].x)[2 * b], (&v[i].x)[2 * b + 1], si);
+    }
+    if (p.bwd_vals) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int wj = 2 * b + (j >> 1);
+        const uint32_t hsel = (j & 1) ? 0x7632u : 0x5410u;
+        const uint32_t col01 = __byte_perm((&v[0].x)[wj], (&v[1].x)[wj], hsel);
+        const uint32_t col23 = __byte_perm((&v[2].x)[wj], (&v[3].x)[wj], hsel);
+        const uint32_t sj = ((j < 2 ? sel.z : sel.w) >> (16 * (j & 1))) & 0xFFFFu;
+        const int mp = c0 + 4 * b + j;
+        s_bv[mp * 32 + ((br + 2 * (mp >> 3)) & 31)] = __byte_perm(col01, col23, sj);
+      }
+    }
+  }
+  if (p.fwd_vals) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      *reinterpret_cast<uint2*>(p.fwd_vals + (grow0 + i) * (p.cols / 2) + gcol0 / 2) = make_uint2(fw[i][0], fw[i][1]);
+  }
+  __syncthreads();
+  if (p.fwd_e && threadIdx.x < 128) {
+    uint4* dst = reinterpret_cast<uint4*>(p.fwd_e + (tr * (p.cols / kTile) + tc) * 2048);
+    dst[threadIdx.x] = reinterpret_cast<const uint4*>(s_fe)[threadIdx.x];
+  }
+  if (p.bwd_e && threadIdx.x >= 128 && threadIdx.x < 256) {
+    uint4* dst = reinterpret_cast<uint4*>(p.bwd_e + (tc * (p.rows / kTile) + tr) * 2048);
+    dst[threadIdx.x - 128] = reinterpret_cast<const uint4*>(s_be)[threadIdx.x - 128];
+  }
+  if (p.bwd_vals) {
+    const int64_t kcol = tr * (kTile / 2) + 2 * lane;
+#pragma unroll 4
+    for (int rr = warp; rr < kTile; rr += kPruneThreads / 32) {
+      const uint32_t val = s_bv[rr * 32 + ((lane + 2 * (rr >> 3)) & 31)];
+      *reinterpret_cast<uint32_t*>(p.bwd_vals + (tc * kTile + rr) * (p.rows / 2) + kcol) = val;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // small conversion kernels
 
 __global__ void idx_to_bits_kernel(const uint8_t* __restrict__ idx, int64_t rows, int64_t cols,
@@ -558,14 +730,19 @@ static int launch_mask(const MaskArgs& a, int dtype, bool search, cudaStream_t s
   if (a.rows == 0 || a.cols == 0) return S24_OK;
   dim3 grid(static_cast<unsigned>((a.cols + kTile - 1) / kTile), static_cast<unsigned>((a.rows + kTile - 1) / kTile));
   const bool narrow = dtype == S24_BF16 && (a.cols % 8) != 0;
+  const bool aligned = a.rows % kTile == 0 && a.cols % kTile == 0;
   if (search) {
+    if (dtype == S24_BF16 && aligned) {
+      search_bf16_kernel<<<grid, kPruneThreads, 0, st>>>(a);
+      return s24_check_launch("mask_search");
+    }
     if (narrow) mask_tile_kernel<S24_BF16, true, true><<<grid, kThreads, 0, st>>>(a);
     else if (dtype == S24_BF16) mask_tile_kernel<S24_BF16, true, false><<<grid, kThreads, 0, st>>>(a);
     else if (dtype == S24_F32) mask_tile_kernel<S24_F32, true, false><<<grid, kThreads, 0, st>>>(a);
     else mask_tile_kernel<S24_F64, true, false><<<grid, kThreads, 0, st>>>(a);
   } else {
     if (dtype == S24_BF16 && a.fwd_e == nullptr && a.bwd_e == nullptr && a.fwd_vals != nullptr &&
-        a.bwd_vals != nullptr && a.rows % kTile == 0 && a.cols % kTile == 0) {
+        a.bwd_vals != nullptr && aligned) {
       prune_bf16_kernel<<<grid, kPruneThreads, 0, st>>>(a);
       return s24_check_launch("prune_compress");
     }
