@@ -487,7 +487,7 @@ __device__ __forceinline__ int search_block_bf16w(const uint32_t (&wd)[8]) {
   return s24_search_tree(rp);
 }
 
-__global__ void __launch_bounds__(kPruneThreads, 1) search_bf16_kernel(MaskArgs p) {
+__global__ void __launch_bounds__(kPruneThreads, 2) search_bf16_kernel(MaskArgs p) {
   __shared__ uint32_t s_bv[128 * 32];
   __shared__ __align__(16) uint32_t s_fe[512];
   __shared__ __align__(16) uint32_t s_be[512];
