@@ -282,7 +282,9 @@ def dense_step_factory(w_in, bias, w2, act):
         return F.gelu(z[:, :d_ff]) * z[:, d_ff:]
 
     def step(x, dy):
-        y = F.linear(act_fn(F.linear(x, W1, B1)), W2)
+        # the same gradients as the 2:4 step (and fst_backward, gated_ffn.py:352): dX, dW_in, dbias, dW2
+        xg = x.detach().requires_grad_(True)
+        y = F.linear(act_fn(F.linear(xg, W1, B1)), W2)
         y.backward(dy)
         W1.grad = B1.grad = W2.grad = None
 
@@ -329,6 +331,18 @@ def load_peaks():
         return pk, "measured"
     except Exception:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def ncu_traffic(cfg_name, tag):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of kernel `tag` from the committed
+    ncu --set full capture of this configuration (profiles/ncu_traffic_<cfg>.json, written by
+    tools/ncu_traffic.py from tools/gpu_profile_round.sh), or None."""
+    p = os.path.join(HERE, "profiles", f"ncu_traffic_{cfg_name}.json")
+    try:
+        with open(p) as f:
+            return json.load(f)["kernels"][tag]["traffic_bytes"]
+    except Exception:
+        return None
 
 
 def run_ours(a, cfg):
@@ -406,7 +420,7 @@ def run_ours(a, cfg):
         # a 2:4 GEMM executes half the MACs: its tensor-pipe peak is 2x the dense peak
         peak = sustained * (2.0 if sparse else 1.0)
         roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": ncu_traffic(a.config, dom),
                 "note": ("dense-equivalent 2MNK / t vs 2x measured sustained dense bf16 peak (2:4 pipe)" if sparse
                          else "2MNK / t vs measured sustained dense bf16 peak") + f" ({peaks_src})"}
     else:

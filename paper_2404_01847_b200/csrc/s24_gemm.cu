@@ -33,7 +33,6 @@ namespace s24 {
 
 constexpr int kGemmThreads = 384;  // 4 control warps + 8 epilogue warps
 constexpr int kEpiWarps = 8;
-constexpr int kGroupM = 8;  // M tiles per raster group (L2 reuse of the B panel)
 
 // epilogues: plain store (+bias); Z and GELU(Z); GELU(Z) and GELU'(Z) (training forward);
 // dZ = acc * GELU'(Z) with bias-gradient row sums (training backward); dW fp32 + masked decay
@@ -63,6 +62,8 @@ struct EpiParams {
 struct GemmShape {
   int m, n, k;  // k logical
   int ksplit;   // K chunks per output tile (dW split-K, reduced with TMA add); 1 = no split
+  int group_m;  // M tiles per raster group: each group sweeps all N with its A panels L2-resident
+  int exp;      // experiment flags (timing studies only, results invalid): 1 skip B loads, 2 skip metadata cp, 4 every tile loads the B tile of n = 0
 };
 
 __constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
@@ -123,11 +124,11 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 232448, "shared memory overflow");
 };
 
-__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
-  const int per_group = kGroupM * num_n;
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group_m, int& mb, int& nb) {
+  const int per_group = group_m * num_n;
   const int group = tile / per_group;
-  const int first_m = group * kGroupM;
-  const int gm = min(num_m - first_m, kGroupM);
+  const int first_m = group * group_m;
+  const int gm = min(num_m - first_m, group_m);
   const int in_group = tile % per_group;
   mb = first_m + in_group % gm;
   nb = in_group / gm;
@@ -190,16 +191,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int mb, nb;
-        tile_coords(tile / shp.ksplit, num_m, num_n, mb, nb);
+        tile_coords(tile / shp.ksplit, num_m, num_n, shp.group_m, mb, nb);
         const int kb_base = (tile % shp.ksplit) * num_kb;
         const int m0 = mb * 128 * kCG + 128 * rank;      // this CTA's A rows
-        const int nb0 = nb * kBN + C::BN_CTA * rank;      // this CTA's B rows (N split)
+        const int nb0 = ((shp.exp & 4) ? 0 : nb * kBN) + C::BN_CTA * rank;  // this CTA's B rows (N split)
         for (int kbi = 0; kbi < num_kb; ++kbi) {
           const int kb = kb_base + kbi;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + C::A_BYTES;
-          if (rank == 0) mbar_expect_tx(&full_bar[stage], C::TX_BYTES * kCG);
+          const bool skip_b = shp.exp & 1;
+          if (rank == 0)
+            mbar_expect_tx(&full_bar[stage], (C::TX_BYTES - (skip_b ? C::TX_BYTES - C::A_BYTES - C::E_BYTES : 0)) * kCG);
           if constexpr (kSparse) {
             tma_load<kCG>(sA, &tmA, &full_bar[stage], kb * 64, m0);  // 64 physical = 128 logical
             tma_load<kCG>(sB + C::B_BYTES, &tmE, &full_bar[stage], 0, (m0 / 128) * (shp.k / 128) + kb);
@@ -209,7 +212,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           } else {
             tma_load<kCG>(sA, &tmA, &full_bar[stage], kb * 64, m0);
           }
-          if constexpr (kBMN) {
+          if (skip_b) {
+          } else if constexpr (kBMN) {
 #pragma unroll
             for (int i = 0; i < C::B_CHUNKS; ++i)
               tma_load<kCG>(sB + i * C::B_BOX_BYTES, &tmB, &full_bar[stage], nb0 + 64 * i, kb * C::BK);
@@ -241,7 +245,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t b_addr = a_addr + C::A_BYTES;
-          if constexpr (kSparse) {
+          if (kSparse && !(shp.exp & 2)) {
             // metadata: 128 rows x 16 B (no swizzle, 8-row core matrices 128 B apart) -> 4 TMEM columns
             tmem_cp_128x128b_cg<kCG>(tmem_base + C::E_COL, make_sdesc(b_addr + C::B_BYTES, 2048, 128, 0));
           }
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t acc_phase = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
       int mb, nb;
-      tile_coords(tile / shp.ksplit, num_m, num_n, mb, nb);
+      tile_coords(tile / shp.ksplit, num_m, num_n, shp.group_m, mb, nb);
       const bool first_chunk = (tile % shp.ksplit) == 0;
       const int m_w = mb * 128 * kCG + 128 * rank + 32 * q;  // first row of this warp
       const int m = m_w + lane;
@@ -656,6 +660,24 @@ static int num_sms() {
   return n;
 }
 
+// Raster group: the M tiles whose A panels (all of K) stay L2-resident while the
+// group sweeps every N tile, so the B operand streams from HBM num_m / group times.
+// Sparse GEMMs (A = compressed weight, 1.125 B per logical K per row incl. metadata)
+// take as many M tiles as fit a ~48 MB L2 budget; dense dW panels (K = tokens) are
+// far larger than L2, so they keep the wave-square default of 8.
+static int exp_flags() {
+  static const int v = getenv("S24_EXP") ? atoi(getenv("S24_EXP")) : 0;
+  return v;
+}
+
+static int pick_group_m(int num_m, double a_bytes_per_mtile) {
+  static const int env = getenv("S24_GROUP_M") ? atoi(getenv("S24_GROUP_M")) : 0;
+  int g = env > 0 ? env : 8;
+  (void)a_bytes_per_mtile;
+  if (g < 1) g = 1;
+  return g < num_m ? g : num_m;
+}
+
 template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT = false,
           int kAcc = 2>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& me, const CUtensorMap& md,
@@ -767,7 +789,9 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     S24_REQUIRE(ldb >= k, S24_ERR_SHAPE, "ldb < k");
     if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 1};
+  const int tile_m = pair ? 256 : 128;
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 1,
+                pick_group_m(static_cast<int>(m / tile_m), 1.125 * tile_m * static_cast<double>(k)), exp_flags()};
   EpiParams ep{d,       ldd,
                bias,    aux,
                ldaux,   dbias,
@@ -865,7 +889,10 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
     cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   }
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), ksplit};
+  const int tile_m = pair ? 256 : 128;
+  static const int env_dw = getenv("S24_GROUP_M_DW") ? atoi(getenv("S24_GROUP_M_DW")) : 8;
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), ksplit,
+                static_cast<int>(m / tile_m) < env_dw ? static_cast<int>(m / tile_m) : env_dw, exp_flags()};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
 #define S24_DW(AMN, BMN, BNV, CG)                                                                      \
   return launch_gemm<false, AMN, BMN, BNV, stages_for<Cfg<false, AMN, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
@@ -917,7 +944,7 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
     if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
   if (int rc = make_map(&md, d, n, m, ldd, 32, 16, kMapF32Sw128)) return rc;
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 1};
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 1, 8, 0};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // BN = 256 with one TMEM accumulator (256 + 4 metadata columns): K = tokens is long, so the
