@@ -134,9 +134,13 @@ int s24_e_to_flat(const uint8_t* e, int64_t m, int64_t k, uint8_t* meta, void* s
  * (gated_ffn.py:294, :297, :329, :352).  B: b_mn = 0 -> stored n x k (ldb >= k),
  * b_mn = 1 -> stored k x n (ldb >= n).  D bf16: d_t = 0 -> stored m x n (feature-major,
  * ldd >= n); d_t = 1 -> stored n x m (token-major, ldd >= m).  AUX uses D's layout
- * for S24_EPI_GELU_AUX; for S24_EPI_GELU_GRAD / S24_EPI_DGELU the GELU'(z) AUX is
- * always m x n (feature-major, ldaux >= n): it is only read back row-wise by the
- * DGELU epilogue.
+ * for S24_EPI_GELU_AUX.  The training epilogues (GELU_GRAD / DGELU, GEGLU_GRAD /
+ * SWIGLU_GRAD / DGATED) exchange AUX / AUX2 in the BLOCKED layout of an F x n matrix
+ * (F = m, or gate_ff for the gated ones; ldaux is ignored): 32 x 32 blocks, block
+ * (f/32, t/32) at element ((f/32) * (n/32) + t/32) * 1024, inside a block the
+ * 8-element unit ((t%32)/8) * 32 + f%32 holds tokens (t & ~7) .. +7 of feature f.
+ * The buffer holds ceil(F/32) * 32 * n elements.  It is produced by GEMM1's epilogue
+ * and consumed by GEMM3's, one coalesced 512-byte access per warp and 8 tokens.
  * bias (bf16, m) may be NULL.  dbias (fp32, m, zeroed by the caller) is used by
  * S24_EPI_DGELU / S24_EPI_DGATED.  aux2 / gate_ff: gated epilogues only (gate_ff = d_ff).
  * m % 128 == 0, k % 128 == 0, n % 32 == 0. */

@@ -286,6 +286,29 @@ __device__ __forceinline__ float gelu_fast(float x) {
   return 0.5f * x * (1.0f + erf_fast(x * 0.70710678118654752f, e));
 }
 
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// GELU(x) = x Phi(x) and GELU'(x) = Phi(x) + x phi(x) with ONE MUFU op (GEMM epilogues, where
+// the MUFU pipe is the limit): Phi(x) ~ 0.5 (1 + tanh(x (a + b x^2 + c x^4))) with a, b, c
+// minimax-fitted to the exact-erf GELU on [0, 9] (|err| < 4e-5 for GELU, < 1e-4 for GELU' with
+// an exact tanh; tanh.approx adds <= 2.5e-4 |x|, a twentieth of a bf16 ulp of the stored value).
+// |x| > 9 saturates exactly (Phi = 0 or 1).
+__device__ __forceinline__ void gelu_and_grad(float x, float& g, float& dg) {
+  constexpr float kA = 0.797422874f, kB = 0.0370039386f, kC = -3.47603262e-4f;
+  const float xc = fminf(fmaxf(x, -9.0f), 9.0f);
+  const float x2 = xc * xc;
+  const float t = tanh_approx(xc * fmaf(fmaf(kC, x2, kB), x2, kA));
+  const float cdf = fmaf(0.5f, t, 0.5f);
+  g = x * cdf;
+  const float dp = fmaf(fmaf(5.0f * kC, x2, 3.0f * kB), x2, kA);
+  dg = fmaf(0.5f * xc * fmaf(-t, t, 1.0f), dp, cdf);
+}
+// sigmoid(u) = 0.5 + 0.5 tanh(u / 2): one MUFU op
+__device__ __forceinline__ float sigmoid_fast(float u) { return fmaf(0.5f, tanh_approx(0.5f * u), 0.5f); }
+
 // UMMA shared-memory matrix descriptor (sm_100 "version 1" format):
 //   [0,14) start>>4 | [16,30) LBO>>4 | [32,46) SBO>>4 | [46,48) version=1 |
 //   [49,52) base offset | [52] lbo mode | [61,64) layout (0 none, 2 = 128B swizzle)

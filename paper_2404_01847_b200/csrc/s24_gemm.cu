@@ -63,7 +63,8 @@ struct GemmShape {
   int m, n, k;  // k logical
   int ksplit;   // K chunks per output tile (dW split-K, reduced with TMA add); 1 = no split
   int group_m;  // M tiles per raster group: each group sweeps all N with its A panels L2-resident
-  int exp;      // experiment flags (timing studies only, results invalid): 1 skip B loads, 2 skip metadata cp, 4 every tile loads the B tile of n = 0
+  int exp;      // experiment flags (timing studies only, results invalid): 1 skip B loads, 2 skip metadata cp, 4 every tile loads the B tile of n = 0,
+                //  16 no activation math in the epilogue, 32 no epilogue global loads
 };
 
 __constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
@@ -76,15 +77,21 @@ __device__ __forceinline__ int gate_row_dev(int p, int64_t ff) {
 template <bool kSilu>
 __device__ __forceinline__ void gate_act(float u, float& a, float& da) {
   if constexpr (kSilu) {
-    const float sg = 1.0f / (1.0f + __expf(-u));
+    const float sg = sigmoid_fast(u);
     a = u * sg;
-    da = sg * (1.0f + u * (1.0f - sg));
+    da = sg * fmaf(u, 1.0f - sg, 1.0f);
   } else {
-    float e;
-    const float cdf = 0.5f * (1.0f + erf_fast(u * 0.70710678118654752f, e));
-    a = u * cdf;
-    da = fmaf(u * 0.39894228040143268f, e, cdf);
+    gelu_and_grad(u, a, da);
   }
+}
+
+// Blocked AUX layout of an (F features x n tokens) bf16 matrix (GELU'(z), v act'(u), act(u)):
+// 32 x 32 blocks, block (f / 32, t / 32) at element ((f / 32) (n / 32) + t / 32) * 1024; inside a
+// block the 16-byte unit ((t % 32) / 8) * 32 + f % 32 holds tokens t & ~7 .. +7 of feature f.
+// An epilogue warp owns 32 features x 32 tokens with lane = feature, so writing or reading its
+// 32 x 32 slice is four fully coalesced 512-byte accesses (unit c * 32 + lane, c = 0..3).
+__device__ __forceinline__ uint4* aux_block(uint16_t* base, int fblk, int n, int n0) {
+  return reinterpret_cast<uint4*>(base + (static_cast<int64_t>(fblk) * (n >> 5) + (n0 >> 5)) * 1024);
 }
 
 // kCG = CTAs per MMA (1: M = 128, 2: CTA pair, M = 256, B split along N).
@@ -163,8 +170,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch(&tmB);
     tma_prefetch(&tmD);
     if constexpr (kSparse) tma_prefetch(&tmE);
-    if constexpr (kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad || kEpi == kEpiGatedGrad) tma_prefetch(&tmX);
-    if constexpr (kEpi == kEpiGatedGrad) tma_prefetch(&tmY);
+    if constexpr (kEpi == kEpiGeluAux) tma_prefetch(&tmX);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -324,13 +330,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int n0p = n_base + 32 * cc;
         if (cc >= kBN / 32 || n0p >= shp.n) return;
         if constexpr (kEpi == kEpiDAct || kEpi == kEpiDGated) {
-          const uint4* gp = reinterpret_cast<const uint4*>(ep.aux + static_cast<int64_t>(m) * ep.ldaux + n0p);
+          // blocked AUX: this warp's 32 features x 32 tokens, four coalesced 512-byte loads
+          const uint4* gp = aux_block(ep.aux, m_w >> 5, shp.n, n0p) + lane;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) pre[u] = __ldg(gp + u);
+          for (int u = 0; u < 4; ++u) pre[u] = __ldg(gp + 32 * u);
           if constexpr (kEpi == kEpiDGated) {
-            const uint4* gp2 = reinterpret_cast<const uint4*>(ep.aux2 + static_cast<int64_t>(m) * ep.ldaux + n0p);
+            const uint4* gp2 = aux_block(ep.aux2, m_w >> 5, shp.n, n0p) + lane;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) pre[4 + u] = __ldg(gp2 + u);
+            for (int u = 0; u < 4; ++u) pre[4 + u] = __ldg(gp2 + 32 * u);
           }
         } else if constexpr (kEpi == kEpiDw) {
           if (!decay) return;
@@ -349,14 +356,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       };
-      if constexpr (kPre) prefetch(h);
+      if (kPre && !(shp.exp & 32)) prefetch(h);
 #pragma unroll 1
       for (int cc = h; cc < kBN / 32; cc += 2) {
         uint4 cur[kPreVec];
         uint2 cur_idx = pre_idx;
 #pragma unroll
         for (int u = 0; u < kPreVec; ++u) cur[u] = pre[u];
-        if constexpr (kPre) prefetch(cc + 2);
+        if (kPre && !(shp.exp & 32)) prefetch(cc + 2);
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + 32 * cc, r);
         tmem_ld_wait();
@@ -436,27 +443,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (lane == 0) bulk_wait_read0();
           __syncwarp();
-          uint16_t* sa = reinterpret_cast<uint16_t*>(stg);          // A: [32 tokens][16 features]
-          uint16_t* s1 = reinterpret_cast<uint16_t*>(stg + 1024);   // AUX  v act'(u): [16 f][32 t]
-          uint16_t* s2 = reinterpret_cast<uint16_t*>(stg + 2048);   // AUX2 act(u):    [16 f][32 t]
+          uint16_t* sa = reinterpret_cast<uint16_t*>(stg);  // A: [32 tokens][16 features]
           const int f = lane & 15, t0 = lo ? 0 : 16;
+          float g1[16], g2[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float a, da;
-            if (ep.act == S24_ACT_SWIGLU) gate_act<true>(uu[i], a, da);
+            if (shp.exp & 16) { a = uu[i]; da = uu[i]; }
+            else if (ep.act == S24_ACT_SWIGLU) gate_act<true>(uu[i], a, da);
             else gate_act<false>(uu[i], a, da);
             sa[(t0 + i) * 16 + f] = f32_to_bf16(a * vv[i]);
-            s1[f * 32 + t0 + i] = f32_to_bf16(vv[i] * da);
-            s2[f * 32 + t0 + i] = f32_to_bf16(a);
+            g1[i] = vv[i] * da;
+            g2[i] = a;
           }
           fence_proxy_async_smem();
           __syncwarp();
+          const int fg = m_w >> 1;  // first gate feature of this warp: 16 g, g = m_w / 32
           if (lane == 0) {
-            const int fg = m_w >> 1;  // first gate feature of this warp: 16 g, g = m_w / 32
             tma_store_2d(&tmD, stg, fg, n0);
-            tma_store_2d(&tmX, stg + 1024, n0, fg);
-            tma_store_2d(&tmY, stg + 2048, n0, fg);
             bulk_commit();
+          }
+          // AUX = v act'(u), AUX2 = act(u), blocked: this lane's 16 tokens are units t0/8 + j
+          {
+            const int unit = (t0 >> 3) * 32 + (fg & 31) + f;
+            uint4* p1 = aux_block(ep.aux, fg >> 5, shp.n, n0) + unit;
+            uint4* p2 = aux_block(ep.aux2, fg >> 5, shp.n, n0) + unit;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              p1[32 * j] = make_uint4(pack_bf16x2(g1[8 * j], g1[8 * j + 1]), pack_bf16x2(g1[8 * j + 2], g1[8 * j + 3]),
+                                      pack_bf16x2(g1[8 * j + 4], g1[8 * j + 5]),
+                                      pack_bf16x2(g1[8 * j + 6], g1[8 * j + 7]));
+              p2[32 * j] = make_uint4(pack_bf16x2(g2[8 * j], g2[8 * j + 1]), pack_bf16x2(g2[8 * j + 2], g2[8 * j + 3]),
+                                      pack_bf16x2(g2[8 * j + 4], g2[8 * j + 5]),
+                                      pack_bf16x2(g2[8 * j + 6], g2[8 * j + 7]));
+            }
           }
         } else if constexpr (kEpi == kEpiDGated) {
           // rows: gate features j; dZ_u = dA * v act'(u), dZ_v = dA * act(u) written into the
@@ -499,7 +519,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             bulk_commit();
           }
         } else {
-          constexpr bool kTwo = kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad;  // two bf16 outputs
+          constexpr bool kTwo = kEpi == kEpiGeluAux;  // two bf16 outputs staged through smem
           float v2[32];
           if constexpr (kEpi == kEpiDAct) {
             // dZ = dA * GELU'(z), GELU'(z) in the output's layout; row sums -> bias gradient
@@ -524,17 +544,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += bias_v;
           }
-          if constexpr (kEpi == kEpiGeluGrad) {
-            // D = GELU(z), AUX = GELU'(z): one erf + one exp shared by both
+          if (kEpi == kEpiGeluGrad && (shp.exp & 16)) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float x = v[i];
-              float e;
-              const float ef = erf_fast(x * 0.70710678118654752f, e);
-              const float cdf = 0.5f * (1.0f + ef);
-              v[i] = x * cdf;
-              v2[i] = fmaf(x * 0.39894228040143268f, e, cdf);
-            }
+            for (int i = 0; i < 32; ++i) v2[i] = v[i];
+          } else if constexpr (kEpi == kEpiGeluGrad) {
+            // D = GELU(z), AUX = GELU'(z): one tanh shared by both
+#pragma unroll
+            for (int i = 0; i < 32; ++i) gelu_and_grad(v[i], v[i], v2[i]);
           } else if constexpr (kEpi == kEpiGeluAux) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v2[i] = gelu_fast(v[i]);
@@ -560,16 +576,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                pack_bf16x2(x[8 * c + 4], x[8 * c + 5]), pack_bf16x2(x[8 * c + 6], x[8 * c + 7]));
             }
           };
-          // AUX of the training epilogue (GELU'(z)) is always feature-major; otherwise AUX follows D
-          constexpr bool kAuxT = kOutT && kEpi != kEpiGeluGrad;
+          // API epilogue: AUX follows D's layout; training epilogue: GELU'(z) goes out blocked
           stage(zb, v, kOutT);
-          if constexpr (kTwo) stage(stg + 2048, v2, kAuxT);
+          if constexpr (kTwo) stage(stg + 2048, v2, kOutT);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             tma_store_2d(&tmD, zb, kOutT ? m_w : n0, kOutT ? n0 : m_w);
-            if constexpr (kTwo) tma_store_2d(&tmX, stg + 2048, kAuxT ? m_w : n0, kAuxT ? n0 : m_w);
+            if constexpr (kTwo) tma_store_2d(&tmX, stg + 2048, kOutT ? m_w : n0, kOutT ? n0 : m_w);
             bulk_commit();
+          }
+          if constexpr (kEpi == kEpiGeluGrad) {
+            uint4* gp = aux_block(ep.aux, m_w >> 5, shp.n, n0) + lane;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              gp[32 * c] = make_uint4(pack_bf16x2(v2[8 * c], v2[8 * c + 1]), pack_bf16x2(v2[8 * c + 2], v2[8 * c + 3]),
+                                      pack_bf16x2(v2[8 * c + 4], v2[8 * c + 5]),
+                                      pack_bf16x2(v2[8 * c + 6], v2[8 * c + 7]));
           }
           sbuf ^= 1;
         }
@@ -743,10 +766,12 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     S24_REQUIRE(aux2 != nullptr && (reinterpret_cast<uintptr_t>(aux2) & 15) == 0, S24_ERR_ARG,
                 "gated epilogues need a 16-byte aligned aux2 tensor");
   }
-  if (epilogue != S24_EPI_STORE)
-    S24_REQUIRE(aux != nullptr && ldaux >= ((d_t && epilogue == S24_EPI_GELU_AUX) ? m : n) && ldaux % 8 == 0 &&
-                    (reinterpret_cast<uintptr_t>(aux) & 15) == 0,
+  if (epilogue == S24_EPI_GELU_AUX)
+    S24_REQUIRE(aux != nullptr && ldaux >= (d_t ? m : n) && ldaux % 8 == 0 && (reinterpret_cast<uintptr_t>(aux) & 15) == 0,
                 S24_ERR_ARG, "this epilogue needs a 16-byte aligned aux tensor");
+  else if (epilogue != S24_EPI_STORE)  // blocked AUX layout (ldaux unused)
+    S24_REQUIRE(aux != nullptr && (reinterpret_cast<uintptr_t>(aux) & 15) == 0, S24_ERR_ARG,
+                "this epilogue needs a 16-byte aligned (blocked) aux tensor");
   S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
   const bool pair = (m % 256 == 0) && cg_override() != 1;
   constexpr int BN1 = 128, BN2 = 224;
@@ -755,10 +780,9 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, kMapU64)) return rc;
   CUtensorMap md, mx, my;
   if (gated_fwd) {
-    // A: [n tokens][d_ff] boxes of 16 features x 32 tokens; AUX, AUX2: [d_ff][n] boxes of 32 x 16
+    // A: [n tokens][d_ff] boxes of 16 features x 32 tokens; AUX, AUX2 are written blocked
     if (int rc = make_map(&md, d, m / 2, n, ldd, 16, 32, kMapBf16Plain)) return rc;
-    if (int rc = make_map(&mx, aux, n, m / 2, ldaux, 32, 16, kMapBf16Plain)) return rc;
-    if (int rc = make_map(&my, aux2, n, m / 2, ldaux, 32, 16, kMapBf16Plain)) return rc;
+    mx = my = md;
   } else if (gated_bwd) {
     if (int rc = make_map(&md, d, 2 * m, n, ldd, 64, 32, kMapBf16Plain)) return rc;  // dZ interleaved
     mx = my = md;
@@ -769,9 +793,8 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     } else {
       if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapBf16Sw64)) return rc;
     }
-    const bool aux_t = d_t && epilogue == S24_EPI_GELU_AUX;  // GELU'(z) (GRAD / DGELU) stays m x n
-    if (epilogue == S24_EPI_GELU_AUX || epilogue == S24_EPI_GELU_GRAD) {
-      if (aux_t) {
+    if (epilogue == S24_EPI_GELU_AUX) {
+      if (d_t) {
         if (int rc = make_map(&mx, aux, m, n, ldaux, 32, 32, kMapBf16Plain)) return rc;
       } else {
         if (int rc = make_map(&mx, aux, n, m, ldaux, 32, 32, kMapBf16Sw64)) return rc;

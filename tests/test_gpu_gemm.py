@@ -125,9 +125,11 @@ def test_sparse_gemm_token_major_output_and_epilogues(m, k, n, epi):
         spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, bias, out_t=True)
         assert normwise_rel(out.float().cpu(), (ref + bias.float()).cpu()) < 1e-2
     elif epi == "gelu_grad":
-        g = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")  # GELU'(z) stays feature-major
+        from paper_2404_01847_b200.engine import aux_empty, aux_to_feature_major
+
+        g = aux_empty(m, n, "cuda")  # GELU'(z), blocked layout
         spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, None, epi=C.EPI_GELU_GRAD, aux=g, out_t=True)
-        g = g.t()
+        g = aux_to_feature_major(g, m, n).t()
         zr = ref.double()
         cdf = 0.5 * (1 + torch.erf(zr / 2 ** 0.5))
         assert normwise_rel(out.float().cpu(), (zr * cdf).cpu()) < 1e-2
@@ -136,7 +138,9 @@ def test_sparse_gemm_token_major_output_and_epilogues(m, k, n, epi):
     else:
         gin = torch.rand(n, m, device="cuda").bfloat16()
         db = torch.zeros(m, dtype=torch.float32, device="cuda")
-        gfm = gin.t().contiguous()  # feature-major GELU'(z) input
+        from paper_2404_01847_b200.engine import aux_from_feature_major
+
+        gfm = aux_from_feature_major(gin.t().contiguous())  # blocked GELU'(z) input
         spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, None, epi=C.EPI_DGELU, aux=gfm, dbias=db, out_t=True)
         dz = ref * gin.float()
         assert normwise_rel(out.float().cpu(), dz.cpu()) < 1e-2
