@@ -135,12 +135,14 @@ int s24_e_to_flat(const uint8_t* e, int64_t m, int64_t k, uint8_t* meta, void* s
  * b_mn = 1 -> stored k x n (ldb >= n).  D bf16: d_t = 0 -> stored m x n (feature-major,
  * ldd >= n); d_t = 1 -> stored n x m (token-major, ldd >= m).  AUX uses D's layout
  * for S24_EPI_GELU_AUX.  The training epilogues (GELU_GRAD / DGELU, GEGLU_GRAD /
- * SWIGLU_GRAD / DGATED) exchange AUX / AUX2 in the BLOCKED layout of an F x n matrix
- * (F = m, or gate_ff for the gated ones; ldaux is ignored): 32 x 32 blocks, block
- * (f/32, t/32) at element ((f/32) * (n/32) + t/32) * 1024, inside a block the
- * 8-element unit ((t%32)/8) * 32 + f%32 holds tokens (t & ~7) .. +7 of feature f.
- * The buffer holds ceil(F/32) * 32 * n elements.  It is produced by GEMM1's epilogue
- * and consumed by GEMM3's, one coalesced 512-byte access per warp and 8 tokens.
+ * SWIGLU_GRAD / DGATED) need d_t = 1 and exchange AUX / AUX2 in the FRAGMENT layout of an
+ * F x n matrix (F = m, or gate_ff for the gated ones; ldaux is ignored): 16-feature x
+ * 32-token sub-blocks of 512 elements, sub-block (f/16, t/32) at element
+ * ((f/16) * (n/32) + t/32) * 512; inside, the 8-element unit 32*s + 4*r + p holds feature
+ * 8*s + r of the sub-block (s = (f%16)/8, r = f%8) at tokens 8*c + 2*p + k (element 2*c + k,
+ * c = 0..3, k = 0, 1) -- the register layout of a tcgen05.ld 16x256b, so the producing and
+ * consuming epilogues move it with coalesced 512-byte accesses.  The buffer holds
+ * ceil(F/16) * 16 * n elements.
  * bias (bf16, m) may be NULL.  dbias (fp32, m, zeroed by the caller) is used by
  * S24_EPI_DGELU / S24_EPI_DGATED.  aux2 / gate_ff: gated epilogues only (gate_ff = d_ff).
  * m % 128 == 0, k % 128 == 0, n % 32 == 0. */

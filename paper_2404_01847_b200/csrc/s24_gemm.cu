@@ -85,13 +85,14 @@ __device__ __forceinline__ void gate_act(float u, float& a, float& da) {
   }
 }
 
-// Blocked AUX layout of an (F features x n tokens) bf16 matrix (GELU'(z), v act'(u), act(u)):
-// 32 x 32 blocks, block (f / 32, t / 32) at element ((f / 32) (n / 32) + t / 32) * 1024; inside a
-// block the 16-byte unit ((t % 32) / 8) * 32 + f % 32 holds tokens t & ~7 .. +7 of feature f.
-// An epilogue warp owns 32 features x 32 tokens with lane = feature, so writing or reading its
-// 32 x 32 slice is four fully coalesced 512-byte accesses (unit c * 32 + lane, c = 0..3).
-__device__ __forceinline__ uint4* aux_block(uint16_t* base, int fblk, int n, int n0) {
-  return reinterpret_cast<uint4*>(base + (static_cast<int64_t>(fblk) * (n >> 5) + (n0 >> 5)) * 1024);
+// AUX layout exchanged between GEMM1's and GEMM3's fragment epilogues (GELU'(z), v act'(u),
+// act(u); an F x n bf16 matrix, F rounded up to 16): 16-feature x 32-token sub-blocks of 1 KB,
+// sub-block (f / 16, t / 32) at element ((f / 16) (n / 32) + t / 32) * 512.  Inside, 16-byte unit
+// 32 s + 4 r + p holds feature 8 s + r (s = (f % 16) / 8, r = f % 8) at tokens 8 c + 2 p + k
+// (c = 0..3, k = 0, 1, element 2 c + k): exactly what thread 4 r + p of a 16x256b TMEM load
+// holds, so each warp reads or writes a sub-block as two coalesced 512-byte accesses.
+__device__ __forceinline__ uint4* aux_frag(uint16_t* base, int f16blk, int n, int n0) {
+  return reinterpret_cast<uint4*>(base + (static_cast<int64_t>(f16blk) * (n >> 5) + (n0 >> 5)) * 512);
 }
 
 // kCG = CTAs per MMA (1: M = 128, 2: CTA pair, M = 256, B split along N).
@@ -148,6 +149,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, GemmShape shp,
                 EpiParams ep) {
   using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG, kAcc>;
+  // token-major training / plain-store epilogues run on the fragment path (tcgen05.ld 16x256b +
+  // stmatrix); the masked-decay dW epilogue and the API's z / GELU(z) epilogue on the row path
+  constexpr bool kFrag = kOutT && (kEpi == kEpiStore || kEpi == kEpiGeluGrad || kEpi == kEpiDAct ||
+                                   kEpi == kEpiGatedGrad || kEpi == kEpiDGated);
+  static_assert(kOutT || !(kEpi == kEpiGeluGrad || kEpi == kEpiDAct || kEpi == kEpiGatedGrad || kEpi == kEpiDGated),
+                "training epilogues store token-major outputs");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
@@ -294,53 +301,295 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue (8 warps: lane quarter q, column half h) =====================
-    // TMEM -> registers -> (bias / GELU / masked decay) -> swizzled smem staging -> TMA store
-    // (full-line writes; the staging buffer is recycled once the bulk store has read it).
-    const int q = warp & 3, h = (warp - 4) >> 2;
-    uint8_t* stg = smem + C::EPI_OFF + (warp - 4) * 4096;
-    int acc = 0, sbuf = 0;
-    uint32_t acc_phase = 0;
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-      int mb, nb;
-      tile_coords(tile / shp.ksplit, num_m, num_n, shp.group_m, mb, nb);
-      const bool first_chunk = (tile % shp.ksplit) == 0;
-      const int m_w = mb * 128 * kCG + 128 * rank + 32 * q;  // first row of this warp
-      const int m = m_w + lane;
-      const int n_base = nb * kBN;
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
-      float bias_v = 0.0f;   // bias (forward epilogues) or running bias-gradient partial (backward)
-      float bias_v2 = 0.0f;  // second bias-gradient partial (kEpiDGated: the v half)
-      if constexpr (kEpi == kEpiStore || kEpi == kEpiGeluAux || kEpi == kEpiGeluGrad) {
-        if (ep.bias != nullptr) bias_v = bf16_to_f32(ep.bias[m]);
-      } else if constexpr (kEpi == kEpiGatedGrad) {
-        if (ep.bias != nullptr) bias_v = bf16_to_f32(ep.bias[gate_row_dev(m, ep.gate_ff)]);
-      }
-      // global inputs of the epilogue (GELU'(z) for dGELU; W + mask indices for the
-      // decay) are prefetched one chunk ahead so their latency hides behind the
-      // TMEM load and the math of the current chunk
-      constexpr bool kPre = kEpi == kEpiDAct || kEpi == kEpiDw || kEpi == kEpiDGated;
-      constexpr int kPreVec = (kEpi == kEpiDw || kEpi == kEpiDGated) ? 8 : 4;
-      const int w_row = (kEpi == kEpiDw && ep.gate_ff > 0) ? gate_row_dev(m, ep.gate_ff) : m;
-      uint4 pre[kPreVec];
-      uint2 pre_idx = make_uint2(0, 0);
-      const bool decay = kEpi == kEpiDw && ep.idx != nullptr && first_chunk;
-      auto prefetch = [&](int cc) {
-        const int n0p = n_base + 32 * cc;
-        if (cc >= kBN / 32 || n0p >= shp.n) return;
-        if constexpr (kEpi == kEpiDAct || kEpi == kEpiDGated) {
-          // blocked AUX: this warp's 32 features x 32 tokens, four coalesced 512-byte loads
-          const uint4* gp = aux_block(ep.aux, m_w >> 5, shp.n, n0p) + lane;
+    if constexpr (kFrag) {
+      // ============ fragment epilogue (token-major outputs, training epilogues) ============
+      // tcgen05.ld 16x256b puts each thread on 4 rows (features m_w + 8j + t4, j = 2h + s) x 8
+      // tokens (n0 + 8c + 2p + k, c = 0..3, p = lane % 4, k = 0, 1) of a 32 x 32 chunk: token
+      // pairs pack into one bf16x2 register, stmatrix.trans writes the token-major tile into the
+      // swizzled TMA staging (4 instructions per chunk), and the AUX exchange with the other
+      // GEMM's epilogue is one 16-byte unit per (thread, row pair) -- see aux_frag.
+      const int e = warp - 4, q = e & 3, cw = e >> 2;
+      const int t4 = lane >> 2;
+      uint8_t* stg = smem + C::EPI_OFF + e * 4096;
+      const uint32_t stg_a = smem_u32(stg);
+      // stmatrix row addresses: thread 8j + i addresses row i of matrix j
+      const int mj = lane >> 3, mi = lane & 7;
+      int acc = 0, sbuf = 0, par = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, par ^= 1) {
+        int mb, nb;
+        tile_coords(tile / shp.ksplit, num_m, num_n, shp.group_m, mb, nb);
+        const int m_w = mb * 128 * kCG + 128 * rank + 32 * q;  // first TMEM row of this warp
+        const int n_base = nb * kBN;
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        float bias4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // bias of row m_w + 8j + t4 (forward)
+        float bs1[4] = {0.0f, 0.0f, 0.0f, 0.0f};    // bias-gradient partials (backward), u / plain
+        float bs2[4] = {0.0f, 0.0f, 0.0f, 0.0f};    // v half (kEpiDGated)
+        if constexpr (kEpi == kEpiStore || kEpi == kEpiGeluGrad || kEpi == kEpiGatedGrad) {
+          if (ep.bias != nullptr) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) pre[u] = __ldg(gp + 32 * u);
-          if constexpr (kEpi == kEpiDGated) {
-            const uint4* gp2 = aux_block(ep.aux2, m_w >> 5, shp.n, n0p) + lane;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) pre[4 + u] = __ldg(gp2 + 32 * u);
+            for (int j = 0; j < 4; ++j) {
+              const int row = m_w + 8 * j + t4;
+              bias4[j] = bf16_to_f32(ep.bias[kEpi == kEpiGatedGrad ? gate_row_dev(row, ep.gate_ff) : row]);
+            }
           }
-        } else if constexpr (kEpi == kEpiDw) {
-          if (!decay) return;
+        }
+        // AUX inputs of the backward epilogues, prefetched one chunk ahead (coalesced 512 B)
+        constexpr bool kPre = kEpi == kEpiDAct || kEpi == kEpiDGated;
+        uint4 pre[8];
+        auto prefetch = [&](int cc) {
+          const int n0p = n_base + 32 * cc;
+          if (cc >= kBN / 32 || n0p >= shp.n) return;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint4* gp = aux_frag(ep.aux, (m_w >> 4) + h, shp.n, n0p) + lane;
+            pre[2 * h] = __ldg(gp);
+            pre[2 * h + 1] = __ldg(gp + 32);
+            if constexpr (kEpi == kEpiDGated) {
+              const uint4* gp2 = aux_frag(ep.aux2, (m_w >> 4) + h, shp.n, n0p) + lane;
+              pre[4 + 2 * h] = __ldg(gp2);
+              pre[4 + 2 * h + 1] = __ldg(gp2 + 32);
+            }
+          }
+        };
+        // the two warps of a lane quarter take alternate chunks; the one starting flips per tile
+        const int first = cw ^ par;
+        if constexpr (kPre) prefetch(first);
+#pragma unroll 1
+        for (int cc = first; cc < kBN / 32; cc += 2) {
+          uint4 cur[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cur[u] = pre[u];
+          if constexpr (kPre) prefetch(cc + 2);
+          uint32_t r[32];
+          const uint32_t ta = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + 32 * cc;
+          tmem_ld16x256b_x4(ta, r);
+          tmem_ld16x256b_x4(ta + (16u << 16), r + 16);
+          tmem_ld_wait();
+          const int n0 = n_base + 32 * cc;
+          if (n0 >= shp.n) continue;
+          // v[16 h + 4 c + 2 s + k]: row m_w + 16 h + 8 s + t4, token n0 + 8 c + 2 p + k
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if constexpr (kEpi == kEpiGatedGrad) {
+            // h = 0: u rows, h = 1: the matching v rows of gate features fg + 8 s + t4
+            const int fg = m_w >> 1;
+            uint32_t pa[8], g1[8], g2[8];  // bf16x2 of (c, s): A = act(u) v, AUX = v act'(u), AUX2 = act(u)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+#pragma unroll
+              for (int sl = 0; sl < 2; ++sl) {
+                float a2[2], d2[2], o2[2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                  const float u = v[4 * c + 2 * sl + k] + bias4[sl];
+                  const float w = v[16 + 4 * c + 2 * sl + k] + bias4[2 + sl];
+                  float a, da;
+                  if (shp.exp & 16) { a = u; da = u; }
+                  else if (ep.act == S24_ACT_SWIGLU) gate_act<true>(u, a, da);
+                  else gate_act<false>(u, a, da);
+                  a2[k] = a * w;
+                  d2[k] = w * da;
+                  o2[k] = a;
+                }
+                pa[2 * c + sl] = pack_bf16x2(a2[0], a2[1]);
+                g1[2 * c + sl] = pack_bf16x2(d2[0], d2[1]);
+                g2[2 * c + sl] = pack_bf16x2(o2[0], o2[1]);
+              }
+            }
+            // A: [32 tokens][16 features], 32-byte rows, 32B swizzle; matrices (c, s)
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+#pragma unroll
+            for (int hc = 0; hc < 2; ++hc) {
+              const int tok = 8 * (2 * hc + (mj >> 1)) + mi, sl = mj & 1;
+              stmatrix_x4_trans(stg_a + tok * 32 + ((sl ^ ((tok >> 2) & 1)) << 4), pa[4 * hc], pa[4 * hc + 1],
+                                pa[4 * hc + 2], pa[4 * hc + 3]);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmD, stg, fg, n0);
+              bulk_commit();
+            }
+            uint4* p1 = aux_frag(ep.aux, fg >> 4, shp.n, n0) + lane;
+            uint4* p2 = aux_frag(ep.aux2, fg >> 4, shp.n, n0) + lane;
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+              p1[32 * sl] = make_uint4(g1[sl], g1[2 + sl], g1[4 + sl], g1[6 + sl]);
+              p2[32 * sl] = make_uint4(g2[sl], g2[2 + sl], g2[4 + sl], g2[6 + sl]);
+            }
+          } else if constexpr (kEpi == kEpiDGated) {
+            // dZ_u = dA AUX, dZ_v = dA AUX2 -> interleaved token-major dZ: this warp's 32 gate
+            // features own the 64 columns [2 m_w, 2 m_w + 64): 32 h + 16 (v) + 8 s + row
+            uint32_t pz[2][2][2][4];  // [h][u/v][s][c]
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+              for (int sl = 0; sl < 2; ++sl) {
+                const uint4 x1 = cur[2 * h + sl], x2 = cur[4 + 2 * h + sl];
+                const uint32_t a1[4] = {x1.x, x1.y, x1.z, x1.w}, a2[4] = {x2.x, x2.y, x2.z, x2.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  const float da0 = v[16 * h + 4 * c + 2 * sl], da1 = v[16 * h + 4 * c + 2 * sl + 1];
+                  const float z10 = da0 * __uint_as_float(a1[c] << 16), z11 = da1 * __uint_as_float(a1[c] & 0xFFFF0000u);
+                  const float z20 = da0 * __uint_as_float(a2[c] << 16), z21 = da1 * __uint_as_float(a2[c] & 0xFFFF0000u);
+                  bs1[2 * h + sl] += z10 + z11;
+                  bs2[2 * h + sl] += z20 + z21;
+                  pz[h][0][sl][c] = pack_bf16x2(z10, z11);
+                  pz[h][1][sl][c] = pack_bf16x2(z20, z21);
+                }
+              }
+            }
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            // [32 tokens][64 columns], 128-byte rows, 128B swizzle; one stmatrix per (h, c):
+            // matrices j = (u/v, s) -> 16-byte column chunk 4 h + j
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const int tok = 8 * c + mi;
+                stmatrix_x4_trans(stg_a + tok * 128 + (((4 * h + mj) ^ (tok & 7)) << 4), pz[h][0][0][c],
+                                  pz[h][0][1][c], pz[h][1][0][c], pz[h][1][1][c]);
+              }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmD, stg, 2 * m_w, n0);
+              bulk_commit();
+            }
+          } else {
+            // kEpiStore (+bias), kEpiGeluGrad (GELU(z) out, GELU'(z) to AUX), kEpiDAct (acc * AUX)
+            uint32_t pd[16];  // bf16x2 of (h, c, s) at 8 h + 2 c + s ... stored as [c][j], j = 2 h + s
+            if constexpr (kEpi == kEpiDAct) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint4 x = cur[j];
+                const uint32_t a[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  float& v0 = v[16 * (j >> 1) + 4 * c + 2 * (j & 1)];
+                  float& v1 = v[16 * (j >> 1) + 4 * c + 2 * (j & 1) + 1];
+                  v0 *= __uint_as_float(a[c] << 16);
+                  v1 *= __uint_as_float(a[c] & 0xFFFF0000u);
+                  bs1[j] += v0 + v1;
+                }
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t gq[4];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                float x0 = v[16 * (j >> 1) + 4 * c + 2 * (j & 1)];
+                float x1 = v[16 * (j >> 1) + 4 * c + 2 * (j & 1) + 1];
+                if constexpr (kEpi == kEpiStore || kEpi == kEpiGeluGrad) {
+                  x0 += bias4[j];
+                  x1 += bias4[j];
+                }
+                if constexpr (kEpi == kEpiGeluGrad) {
+                  float g0, g1, d0, d1;
+                  if (shp.exp & 16) { g0 = d0 = x0; g1 = d1 = x1; }
+                  else { gelu_and_grad(x0, g0, d0); gelu_and_grad(x1, g1, d1); }
+                  x0 = g0;
+                  x1 = g1;
+                  gq[c] = pack_bf16x2(d0, d1);
+                }
+                pd[4 * c + j] = pack_bf16x2(x0, x1);
+              }
+              if constexpr (kEpi == kEpiGeluGrad) {
+                // GELU'(z) -> AUX unit (row m_w + 8 j + t4, this chunk)
+                aux_frag(ep.aux, (m_w >> 4) + (j >> 1), shp.n, n0)[32 * (j & 1) + lane] =
+                    make_uint4(gq[0], gq[1], gq[2], gq[3]);
+              }
+            }
+            // [32 tokens][32 features], 64-byte rows, 64B swizzle, double-buffered; one stmatrix per c
+            uint8_t* zb = stg + sbuf * 2048;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+            const uint32_t zb_a = smem_u32(zb);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int tok = 8 * c + mi;
+              stmatrix_x4_trans(zb_a + tok * 64 + ((mj ^ ((tok >> 1) & 3)) << 4), pd[4 * c], pd[4 * c + 1],
+                                pd[4 * c + 2], pd[4 * c + 3]);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmD, zb, m_w, n0);
+              bulk_commit();
+            }
+            sbuf ^= 1;
+          }
+        }
+        if constexpr (kEpi == kEpiDAct || kEpi == kEpiDGated) {
+          // reduce the partials of the 4 threads sharing a row (lanes 4 t4 .. 4 t4 + 3)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            bs1[j] += __shfl_xor_sync(0xffffffffu, bs1[j], 1);
+            bs1[j] += __shfl_xor_sync(0xffffffffu, bs1[j], 2);
+            if constexpr (kEpi == kEpiDGated) {
+              bs2[j] += __shfl_xor_sync(0xffffffffu, bs2[j], 1);
+              bs2[j] += __shfl_xor_sync(0xffffffffu, bs2[j], 2);
+            }
+          }
+          if (ep.dbias != nullptr && (lane & 3) == 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              atomicAdd(ep.dbias + m_w + 8 * j + t4, bs1[j]);  // [b; c] order for gated: u half at j
+              if constexpr (kEpi == kEpiDGated) atomicAdd(ep.dbias + ep.gate_ff + m_w + 8 * j + t4, bs2[j]);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kCG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);
+          else mbar_arrive(&tempty_bar[acc]);
+        }
+        if (++acc == kAcc) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      if (lane == 0) bulk_wait0();
+    } else {
+      // ============ row epilogue (8 warps: lane quarter q, column half h) ============
+      // masked-decay dW (fp32), feature-major plain store, and the API's z / GELU(z) pair:
+      // tcgen05.ld 32x32b (thread = row, 32 consecutive columns) -> registers -> swizzled smem
+      // staging -> TMA store (full-line writes; staging recycled once the bulk store read it).
+      const int q = warp & 3, h = (warp - 4) >> 2;
+      uint8_t* stg = smem + C::EPI_OFF + (warp - 4) * 4096;
+      int acc = 0, sbuf = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        int mb, nb;
+        tile_coords(tile / shp.ksplit, num_m, num_n, shp.group_m, mb, nb);
+        const bool first_chunk = (tile % shp.ksplit) == 0;
+        const int m_w = mb * 128 * kCG + 128 * rank + 32 * q;  // first row of this warp
+        const int m = m_w + lane;
+        const int n_base = nb * kBN;
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        float bias_v = 0.0f;
+        if constexpr (kEpi == kEpiStore || kEpi == kEpiGeluAux) {
+          if (ep.bias != nullptr) bias_v = bf16_to_f32(ep.bias[m]);
+        }
+        // the decay's W row and mask indices are prefetched one chunk ahead so their
+        // latency hides behind the TMEM load and the math of the current chunk
+        constexpr bool kPre = kEpi == kEpiDw;
+        const int w_row = (kEpi == kEpiDw && ep.gate_ff > 0) ? gate_row_dev(m, ep.gate_ff) : m;
+        uint4 pre[8];
+        uint2 pre_idx = make_uint2(0, 0);
+        const bool decay = kEpi == kEpiDw && ep.idx != nullptr && first_chunk;
+        auto prefetch = [&](int cc) {
+          const int n0p = n_base + 32 * cc;
+          if (cc >= kBN / 32 || n0p >= shp.n || !decay) return;
           pre_idx = __ldg(reinterpret_cast<const uint2*>(ep.idx + static_cast<int64_t>(m >> 2) * (shp.n >> 2) +
                                                          (n0p >> 2)));
           if (ep.w_dtype == S24_BF16) {
@@ -354,269 +603,132 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int u = 0; u < 8; ++u) pre[u] = __ldg(wp + u);
           }
-        }
-      };
-      if (kPre && !(shp.exp & 32)) prefetch(h);
+        };
+        if (kPre && !(shp.exp & 32)) prefetch(h);
 #pragma unroll 1
-      for (int cc = h; cc < kBN / 32; cc += 2) {
-        uint4 cur[kPreVec];
-        uint2 cur_idx = pre_idx;
+        for (int cc = h; cc < kBN / 32; cc += 2) {
+          uint4 cur[8];
+          uint2 cur_idx = pre_idx;
 #pragma unroll
-        for (int u = 0; u < kPreVec; ++u) cur[u] = pre[u];
-        if (kPre && !(shp.exp & 32)) prefetch(cc + 2);
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + 32 * cc, r);
-        tmem_ld_wait();
-        const int n0 = n_base + 32 * cc;
-        if (n0 >= shp.n) continue;
-        float v[32];
+          for (int u = 0; u < 8; ++u) cur[u] = pre[u];
+          if (kPre && !(shp.exp & 32)) prefetch(cc + 2);
+          uint32_t r[32];
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + 32 * cc, r);
+          tmem_ld_wait();
+          const int n0 = n_base + 32 * cc;
+          if (n0 >= shp.n) continue;
+          float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if constexpr (kEpi == kEpiDw) {
-          if (decay) {  // the decay term lam (1 - M) W is added by one K chunk only
-            const uint32_t iw[2] = {cur_idx.x, cur_idx.y};
-            float wv[32];
-            if (ep.w_dtype == S24_BF16) {
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if constexpr (kEpi == kEpiDw) {
+            if (decay) {  // the decay term lam (1 - M) W is added by one K chunk only
+              const uint32_t iw[2] = {cur_idx.x, cur_idx.y};
+              float wv[32];
+              if (ep.w_dtype == S24_BF16) {
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const uint32_t xs[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
+                for (int u = 0; u < 4; ++u) {
+                  const uint32_t xs[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  wv[8 * u + 2 * t] = __uint_as_float(xs[t] << 16);
-                  wv[8 * u + 2 * t + 1] = __uint_as_float(xs[t] & 0xFFFF0000u);
+                  for (int t = 0; t < 4; ++t) {
+                    wv[8 * u + 2 * t] = __uint_as_float(xs[t] << 16);
+                    wv[8 * u + 2 * t + 1] = __uint_as_float(xs[t] & 0xFFFF0000u);
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  wv[4 * u] = __uint_as_float(cur[u].x);
+                  wv[4 * u + 1] = __uint_as_float(cur[u].y);
+                  wv[4 * u + 2] = __uint_as_float(cur[u].z);
+                  wv[4 * u + 3] = __uint_as_float(cur[u].w);
                 }
               }
-            } else {
 #pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                wv[4 * u] = __uint_as_float(cur[u].x);
-                wv[4 * u + 1] = __uint_as_float(cur[u].y);
-                wv[4 * u + 2] = __uint_as_float(cur[u].z);
-                wv[4 * u + 3] = __uint_as_float(cur[u].w);
+              for (int blk = 0; blk < 8; ++blk) {
+                const uint32_t pidx = (iw[blk >> 2] >> (8 * (blk & 3))) & 0xFF;
+                const uint32_t rowmask = (c_gemm_pat_bits[min(pidx, 89u)] >> (4 * (m & 3))) & 0xF;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                  if (!((rowmask >> c) & 1)) v[4 * blk + c] += ep.lam * wv[4 * blk + c];
               }
             }
+            // fp32 32x32 tile, 128B swizzle: 16-byte chunk c of row `lane` -> chunk c ^ (lane & 7)
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
 #pragma unroll
-            for (int blk = 0; blk < 8; ++blk) {
-              const uint32_t pidx = (iw[blk >> 2] >> (8 * (blk & 3))) & 0xFF;
-              const uint32_t rowmask = (c_gemm_pat_bits[min(pidx, 89u)] >> (4 * (m & 3))) & 0xF;
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                if (!((rowmask >> c) & 1)) v[4 * blk + c] += ep.lam * wv[4 * blk + c];
-            }
-          }
-          // fp32 32x32 tile, 128B swizzle: 16-byte chunk c of row `lane` -> chunk c ^ (lane & 7)
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
-                make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            // two 16-row boxes: the gated first weight's rows go back to [u; v] order
-            const int y0 = ep.gate_ff > 0 ? gate_row_dev(m_w, ep.gate_ff) : m_w;
-            const int y1 = ep.gate_ff > 0 ? gate_row_dev(m_w + 16, ep.gate_ff) : m_w + 16;
-            if (shp.ksplit > 1) {
-              tma_reduce_add_2d(&tmD, stg, n0, y0);
-              tma_reduce_add_2d(&tmD, stg + 2048, n0, y1);
-            } else {
-              tma_store_2d(&tmD, stg, n0, y0);
-              tma_store_2d(&tmD, stg + 2048, n0, y1);
-            }
-            bulk_commit();
-          }
-        } else if constexpr (kEpi == kEpiGatedGrad) {
-          // rows: lanes 0-15 = u of features 16g+l, lanes 16-31 = the matching v rows.
-          // Swap half the tokens across the pair so every lane holds (u, v) of one
-          // feature for 16 tokens: lanes < 16 tokens 0..15, lanes >= 16 tokens 16..31.
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += bias_v;
-          const bool lo = lane < 16;
-          float uu[16], vv[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float send = lo ? v[16 + i] : v[i];
-            const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-            uu[i] = lo ? v[i] : recv;
-            vv[i] = lo ? recv : v[16 + i];
-          }
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
-          uint16_t* sa = reinterpret_cast<uint16_t*>(stg);  // A: [32 tokens][16 features]
-          const int f = lane & 15, t0 = lo ? 0 : 16;
-          float g1[16], g2[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float a, da;
-            if (shp.exp & 16) { a = uu[i]; da = uu[i]; }
-            else if (ep.act == S24_ACT_SWIGLU) gate_act<true>(uu[i], a, da);
-            else gate_act<false>(uu[i], a, da);
-            sa[(t0 + i) * 16 + f] = f32_to_bf16(a * vv[i]);
-            g1[i] = vv[i] * da;
-            g2[i] = a;
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          const int fg = m_w >> 1;  // first gate feature of this warp: 16 g, g = m_w / 32
-          if (lane == 0) {
-            tma_store_2d(&tmD, stg, fg, n0);
-            bulk_commit();
-          }
-          // AUX = v act'(u), AUX2 = act(u), blocked: this lane's 16 tokens are units t0/8 + j
-          {
-            const int unit = (t0 >> 3) * 32 + (fg & 31) + f;
-            uint4* p1 = aux_block(ep.aux, fg >> 5, shp.n, n0) + unit;
-            uint4* p2 = aux_block(ep.aux2, fg >> 5, shp.n, n0) + unit;
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              p1[32 * j] = make_uint4(pack_bf16x2(g1[8 * j], g1[8 * j + 1]), pack_bf16x2(g1[8 * j + 2], g1[8 * j + 3]),
-                                      pack_bf16x2(g1[8 * j + 4], g1[8 * j + 5]),
-                                      pack_bf16x2(g1[8 * j + 6], g1[8 * j + 7]));
-              p2[32 * j] = make_uint4(pack_bf16x2(g2[8 * j], g2[8 * j + 1]), pack_bf16x2(g2[8 * j + 2], g2[8 * j + 3]),
-                                      pack_bf16x2(g2[8 * j + 4], g2[8 * j + 5]),
-                                      pack_bf16x2(g2[8 * j + 6], g2[8 * j + 7]));
-            }
-          }
-        } else if constexpr (kEpi == kEpiDGated) {
-          // rows: gate features j; dZ_u = dA * v act'(u), dZ_v = dA * act(u) written into the
-          // interleaved token-major dZ: this warp's 32 features own the 64 columns [2 m_w, 2 m_w + 64)
-          float dz1[32], dz2[32];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t x1[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
-            const uint32_t x2[4] = {cur[4 + u].x, cur[4 + u].y, cur[4 + u].z, cur[4 + u].w};
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const int i = 8 * u + 2 * t;
-              dz1[i] = v[i] * __uint_as_float(x1[t] << 16);
-              dz1[i + 1] = v[i + 1] * __uint_as_float(x1[t] & 0xFFFF0000u);
-              dz2[i] = v[i] * __uint_as_float(x2[t] << 16);
-              dz2[i + 1] = v[i + 1] * __uint_as_float(x2[t] & 0xFFFF0000u);
-            }
-          }
-          float r1 = 0.0f, r2 = 0.0f;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            r1 += dz1[i];
-            r2 += dz2[i];
-          }
-          bias_v += r1;
-          bias_v2 += r2;
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
-          uint16_t* sz = reinterpret_cast<uint16_t*>(stg);  // [32 tokens][64 interleaved columns]
-          const int c1 = lane < 16 ? lane : lane + 16;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            sz[i * 64 + c1] = f32_to_bf16(dz1[i]);
-            sz[i * 64 + c1 + 16] = f32_to_bf16(dz2[i]);
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmD, stg, 2 * m_w, n0);
-            bulk_commit();
-          }
-        } else {
-          constexpr bool kTwo = kEpi == kEpiGeluAux;  // two bf16 outputs staged through smem
-          float v2[32];
-          if constexpr (kEpi == kEpiDAct) {
-            // dZ = dA * GELU'(z), GELU'(z) in the output's layout; row sums -> bias gradient
-            // GELU'(z) is stored feature-major (m x n) whatever D's layout: 64 contiguous bytes
-            // per row, prefetched into cur[] one chunk ahead
-            {
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const uint32_t xs[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  v[8 * u + 2 * t] *= __uint_as_float(xs[t] << 16);
-                  v[8 * u + 2 * t + 1] *= __uint_as_float(xs[t] & 0xFFFF0000u);
-                }
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                  make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              // two 16-row boxes: the gated first weight's rows go back to [u; v] order
+              const int y0 = ep.gate_ff > 0 ? gate_row_dev(m_w, ep.gate_ff) : m_w;
+              const int y1 = ep.gate_ff > 0 ? gate_row_dev(m_w + 16, ep.gate_ff) : m_w + 16;
+              if (shp.ksplit > 1) {
+                tma_reduce_add_2d(&tmD, stg, n0, y0);
+                tma_reduce_add_2d(&tmD, stg + 2048, n0, y1);
+              } else {
+                tma_store_2d(&tmD, stg, n0, y0);
+                tma_store_2d(&tmD, stg + 2048, n0, y1);
               }
+              bulk_commit();
             }
-            float rs = 0.0f;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) rs += v[i];
-            bias_v += rs;  // running bias-gradient partial of row m over this tile's chunks
           } else {
+            constexpr bool kTwo = kEpi == kEpiGeluAux;  // z and GELU(z), both in D's layout
+            float v2[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += bias_v;
-          }
-          if (kEpi == kEpiGeluGrad && (shp.exp & 16)) {
+            if constexpr (kTwo) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v2[i] = v[i];
-          } else if constexpr (kEpi == kEpiGeluGrad) {
-            // D = GELU(z), AUX = GELU'(z): one tanh shared by both
-#pragma unroll
-            for (int i = 0; i < 32; ++i) gelu_and_grad(v[i], v[i], v2[i]);
-          } else if constexpr (kEpi == kEpiGeluAux) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v2[i] = gelu_fast(v[i]);
-          }
-          uint8_t* zb = stg + (kTwo ? 0 : sbuf * 2048);
-          if (lane == 0) {
-            if constexpr (kTwo) bulk_wait_read0();
-            else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          }
-          __syncwarp();
-          // stage a 32 x 32 bf16 tile: feature-major -> 64B-swizzled rows of this lane;
-          // token-major (kOutT) -> transposed, row n holds the 32 features of this warp
-          auto stage = [&](uint8_t* buf, const float(&x)[32], bool transposed) {
-            if (transposed) {
-              uint16_t* b16 = reinterpret_cast<uint16_t*>(buf);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) b16[i * 32 + lane] = f32_to_bf16(x[i]);
-            } else {
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                *reinterpret_cast<uint4*>(buf + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
-                    make_uint4(pack_bf16x2(x[8 * c], x[8 * c + 1]), pack_bf16x2(x[8 * c + 2], x[8 * c + 3]),
-                               pack_bf16x2(x[8 * c + 4], x[8 * c + 5]), pack_bf16x2(x[8 * c + 6], x[8 * c + 7]));
+              for (int i = 0; i < 32; ++i) v2[i] = gelu_fast(v[i]);
             }
-          };
-          // API epilogue: AUX follows D's layout; training epilogue: GELU'(z) goes out blocked
-          stage(zb, v, kOutT);
-          if constexpr (kTwo) stage(stg + 2048, v2, kOutT);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmD, zb, kOutT ? m_w : n0, kOutT ? n0 : m_w);
-            if constexpr (kTwo) tma_store_2d(&tmX, stg + 2048, kOutT ? m_w : n0, kOutT ? n0 : m_w);
-            bulk_commit();
-          }
-          if constexpr (kEpi == kEpiGeluGrad) {
-            uint4* gp = aux_block(ep.aux, m_w >> 5, shp.n, n0) + lane;
+            uint8_t* zb = stg + (kTwo ? 0 : sbuf * 2048);
+            if (lane == 0) {
+              if constexpr (kTwo) bulk_wait_read0();
+              else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            }
+            __syncwarp();
+            // stage a 32 x 32 bf16 tile: feature-major -> 64B-swizzled rows of this lane;
+            // token-major (kOutT) -> transposed, row n holds the 32 features of this warp
+            auto stage = [&](uint8_t* buf, const float(&x)[32], bool transposed) {
+              if (transposed) {
+                uint16_t* b16 = reinterpret_cast<uint16_t*>(buf);
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-              gp[32 * c] = make_uint4(pack_bf16x2(v2[8 * c], v2[8 * c + 1]), pack_bf16x2(v2[8 * c + 2], v2[8 * c + 3]),
-                                      pack_bf16x2(v2[8 * c + 4], v2[8 * c + 5]),
-                                      pack_bf16x2(v2[8 * c + 6], v2[8 * c + 7]));
+                for (int i = 0; i < 32; ++i) b16[i * 32 + lane] = f32_to_bf16(x[i]);
+              } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                  *reinterpret_cast<uint4*>(buf + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+                      make_uint4(pack_bf16x2(x[8 * c], x[8 * c + 1]), pack_bf16x2(x[8 * c + 2], x[8 * c + 3]),
+                                 pack_bf16x2(x[8 * c + 4], x[8 * c + 5]), pack_bf16x2(x[8 * c + 6], x[8 * c + 7]));
+              }
+            };
+            stage(zb, v, kOutT);
+            if constexpr (kTwo) stage(stg + 2048, v2, kOutT);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmD, zb, kOutT ? m_w : n0, kOutT ? n0 : m_w);
+              if constexpr (kTwo) tma_store_2d(&tmX, stg + 2048, kOutT ? m_w : n0, kOutT ? n0 : m_w);
+              bulk_commit();
+            }
+            sbuf ^= 1;
           }
-          sbuf ^= 1;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kCG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);
+          else mbar_arrive(&tempty_bar[acc]);
+        }
+        if (++acc == kAcc) {
+          acc = 0;
+          acc_phase ^= 1;
         }
       }
-      if constexpr (kEpi == kEpiDAct) {
-        if (ep.dbias != nullptr) atomicAdd(ep.dbias + m, bias_v);
-      } else if constexpr (kEpi == kEpiDGated) {
-        if (ep.dbias != nullptr) {  // [b; c] order: u half at j, v half at d_ff + j
-          atomicAdd(ep.dbias + m, bias_v);
-          atomicAdd(ep.dbias + ep.gate_ff + m, bias_v2);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (kCG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);
-        else mbar_arrive(&tempty_bar[acc]);
-      }
-      if (++acc == kAcc) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
+      if (lane == 0) bulk_wait0();
     }
-    if (lane == 0) bulk_wait0();
   }
 
   tc_fence_before();
@@ -646,7 +758,7 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-enum MapKind { kMapBf16Sw128 = 0, kMapBf16Sw64 = 1, kMapF32Sw128 = 2, kMapU64 = 3, kMapBf16Plain = 4 };
+enum MapKind { kMapBf16Sw128 = 0, kMapBf16Sw64 = 1, kMapF32Sw128 = 2, kMapU64 = 3, kMapBf16Plain = 4, kMapBf16Sw32 = 5 };
 
 // 2-D tensor map: inner (contiguous) extent, outer extent, row pitch in elements.
 static int make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch_elems,
@@ -665,6 +777,7 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t ou
                                                         : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const CUtensorMapSwizzle sw = (kind == kMapU64 || kind == kMapBf16Plain) ? CU_TENSOR_MAP_SWIZZLE_NONE
                                 : kind == kMapBf16Sw64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : kind == kMapBf16Sw32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                        : CU_TENSOR_MAP_SWIZZLE_128B;
   CUresult r = enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -759,8 +872,9 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   const int64_t d_cols = gated_fwd ? m / 2 : gated_bwd ? 2 * m : m;
   S24_REQUIRE(ldd >= (d_t ? d_cols : n) && ldd % 8 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0,
               S24_ERR_UNSUPPORTED, "output rows must be 16-byte aligned");
+  const bool training = gated_fwd || gated_bwd || epilogue == S24_EPI_GELU_GRAD || epilogue == S24_EPI_DGELU;
+  S24_REQUIRE(d_t == 1 || !training, S24_ERR_ARG, "training epilogues store token-major outputs (d_t = 1)");
   if (gated_fwd || gated_bwd) {
-    S24_REQUIRE(d_t == 1, S24_ERR_ARG, "gated epilogues store token-major outputs (d_t = 1)");
     S24_REQUIRE(gate_ff == (gated_fwd ? m / 2 : m) && gate_ff % 16 == 0, S24_ERR_SHAPE,
                 "gated epilogue: gate_ff must be d_ff (%lld) and a multiple of 16", (long long)gate_ff);
     S24_REQUIRE(aux2 != nullptr && (reinterpret_cast<uintptr_t>(aux2) & 15) == 0, S24_ERR_ARG,
@@ -780,16 +894,20 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, kMapU64)) return rc;
   CUtensorMap md, mx, my;
   if (gated_fwd) {
-    // A: [n tokens][d_ff] boxes of 16 features x 32 tokens; AUX, AUX2 are written blocked
-    if (int rc = make_map(&md, d, m / 2, n, ldd, 16, 32, kMapBf16Plain)) return rc;
+    // A: [n tokens][d_ff] boxes of 16 features x 32 tokens (32B-swizzled stmatrix staging);
+    // AUX, AUX2 go straight to global in the fragment layout (aux_frag)
+    if (int rc = make_map(&md, d, m / 2, n, ldd, 16, 32, kMapBf16Sw32)) return rc;
     mx = my = md;
   } else if (gated_bwd) {
-    if (int rc = make_map(&md, d, 2 * m, n, ldd, 64, 32, kMapBf16Plain)) return rc;  // dZ interleaved
+    // dZ interleaved, token-major: boxes of 64 columns x 32 tokens, 128B-swizzled staging
+    if (int rc = make_map(&md, d, 2 * m, n, ldd, 64, 32, kMapBf16Sw128)) return rc;
     mx = my = md;
   } else {
-    // D[m, n] feature-major (64B-swizzled staging) or D^T[n, m] token-major (d_t, transposed staging)
+    // D[m, n] feature-major (64B-swizzled staging) or D^T[n, m] token-major (d_t: stmatrix.trans into
+    // 64B-swizzled staging; the API's z / GELU(z) epilogue: transposed two-byte staging, no swizzle)
     if (d_t) {
-      if (int rc = make_map(&md, d, m, n, ldd, 32, 32, kMapBf16Plain)) return rc;
+      if (int rc = make_map(&md, d, m, n, ldd, 32, 32, epilogue == S24_EPI_GELU_AUX ? kMapBf16Plain : kMapBf16Sw64))
+        return rc;
     } else {
       if (int rc = make_map(&md, d, n, m, ldd, 32, 32, kMapBf16Sw64)) return rc;
     }
@@ -829,14 +947,17 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
                        EPI, true>(ma, mb, me, md, mx, my, shp, ep, st);                                     \
   return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG,   \
                      EPI, false>(ma, mb, me, md, mx, my, shp, ep, st)
+#define S24_SPT(BMN, BNV, CG, EPI)                                                                           \
+  return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, EPI, \
+                     true>(ma, mb, me, md, mx, my, shp, ep, st)
 #define S24_SP_EPI(BMN, BNV, CG)                                              \
   switch (epilogue) {                                                           \
     case S24_EPI_GELU_AUX: S24_SP(BMN, BNV, CG, kEpiGeluAux);                   \
-    case S24_EPI_GELU_GRAD: S24_SP(BMN, BNV, CG, kEpiGeluGrad);                 \
-    case S24_EPI_DGELU: S24_SP(BMN, BNV, CG, kEpiDAct);                         \
+    case S24_EPI_GELU_GRAD: S24_SPT(BMN, BNV, CG, kEpiGeluGrad);                \
+    case S24_EPI_DGELU: S24_SPT(BMN, BNV, CG, kEpiDAct);                        \
     case S24_EPI_GEGLU_GRAD:                                                    \
-    case S24_EPI_SWIGLU_GRAD: S24_SP(BMN, BNV, CG, kEpiGatedGrad);              \
-    case S24_EPI_DGATED: S24_SP(BMN, BNV, CG, kEpiDGated);                      \
+    case S24_EPI_SWIGLU_GRAD: S24_SPT(BMN, BNV, CG, kEpiGatedGrad);             \
+    case S24_EPI_DGATED: S24_SPT(BMN, BNV, CG, kEpiDGated);                     \
     default: S24_SP(BMN, BNV, CG, kEpiStore);                                   \
   }
   if (pair) {
@@ -846,6 +967,7 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   if (b_mn) S24_SP_EPI(true, BN1, 1);
   S24_SP_EPI(false, BN1, 1);
 #undef S24_SP_EPI
+#undef S24_SPT
 #undef S24_SP
 }
 

@@ -182,23 +182,25 @@ def spmm_dw(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor
 
 
 def aux_empty(f: int, n: int, device) -> torch.Tensor:
-    """Buffer for a blocked AUX matrix (f features x n tokens, see include/sparse24_b200.h)."""
-    return torch.empty((-(-f // 32) * 32, n), dtype=torch.bfloat16, device=device)
+    """Buffer for an AUX matrix (f features x n tokens) in the fragment layout exchanged by the
+    training epilogues (include/sparse24_b200.h, s24_spmm)."""
+    return torch.empty((-(-f // 16) * 16, n), dtype=torch.bfloat16, device=device)
 
 
 def aux_to_feature_major(g: torch.Tensor, f: int, n: int) -> torch.Tensor:
-    """Blocked AUX -> (f, n) feature-major (inspection / tests)."""
-    fb = -(-f // 32)
-    return g.reshape(fb, n // 32, 4, 32, 8).permute(0, 3, 1, 2, 4).reshape(fb * 32, n)[:f]
+    """Fragment-layout AUX -> (f, n) feature-major (inspection / tests).
+    Storage order per 16 x 32 sub-block: [s][r][p][c][k] for feature 8 s + r, token 8 c + 2 p + k."""
+    fb = -(-f // 16)
+    return g.reshape(fb, n // 32, 2, 8, 4, 4, 2).permute(0, 2, 3, 1, 5, 4, 6).reshape(fb * 16, n)[:f]
 
 
 def aux_from_feature_major(x: torch.Tensor) -> torch.Tensor:
-    """(f, n) feature-major -> blocked AUX (tests)."""
+    """(f, n) feature-major -> fragment-layout AUX (tests)."""
     f, n = x.shape
-    fb = -(-f // 32)
-    xp = torch.zeros((fb * 32, n), dtype=x.dtype, device=x.device)
+    fb = -(-f // 16)
+    xp = torch.zeros((fb * 16, n), dtype=x.dtype, device=x.device)
     xp[:f] = x
-    return xp.reshape(fb, 32, n // 32, 4, 8).permute(0, 2, 3, 1, 4).contiguous().reshape(fb * 32, n)
+    return xp.reshape(fb, 2, 8, n // 32, 4, 4, 2).permute(0, 3, 1, 2, 5, 4, 6).contiguous().reshape(fb * 16, n)
 
 
 def _rows(t: torch.Tensor) -> torch.Tensor:
@@ -214,8 +216,8 @@ class FwdState:
     z: torch.Tensor | None  # (N, r_in) pre-activation (None on the fused training path)
     a: torch.Tensor  # (N, d_ff)
     y: torch.Tensor  # (N, d)
-    g: torch.Tensor | None = None  # GELU'(z) / gated v act'(u), blocked (d_ff x N), fused path only
-    g2: torch.Tensor | None = None  # gated act(u), blocked (d_ff x N), fused gated path only
+    g: torch.Tensor | None = None  # GELU'(z) / gated v act'(u), fragment layout (d_ff x N), fused path only
+    g2: torch.Tensor | None = None  # gated act(u), fragment layout (d_ff x N), fused gated path only
 
 
 def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor | None, w2: CompressedOperand,
@@ -239,8 +241,8 @@ def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor 
     if fused and act in GATED:
         if w_in.perm_ff != d_ff:
             raise ShapeError("the fused gated path needs the first weight compressed u/v-interleaved (perm_ff = d_ff)")
-        g = aux_empty(d_ff, n, dev)  # blocked v act'(u)
-        g2 = aux_empty(d_ff, n, dev)  # blocked act(u)
+        g = aux_empty(d_ff, n, dev)  # v act'(u), fragment layout
+        g2 = aux_empty(d_ff, n, dev)  # act(u), fragment layout
         spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, a, bias_in, tag="k3_spmm_fwd_in",
              epi=C.EPI_SWIGLU_GRAD if act == "swiglu" else C.EPI_GEGLU_GRAD, aux=g, aux2=g2, out_t=True,
              gate_ff=d_ff)
@@ -249,7 +251,7 @@ def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor 
     if w_in.perm_ff:
         raise ShapeError("an interleaved gated operand is only valid on the fused path")
     if fused and act == "gelu":
-        g = aux_empty(d_ff, n, dev)  # blocked GELU'(z), read back by GEMM3's epilogue
+        g = aux_empty(d_ff, n, dev)  # GELU'(z), fragment layout, read back by GEMM3's epilogue
         spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, a, bias_in, tag="k3_spmm_fwd_in",
              epi=C.EPI_GELU_GRAD, aux=g, out_t=True)
         spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, a, False, n, y, tag="k3_spmm_fwd_out", out_t=True)
