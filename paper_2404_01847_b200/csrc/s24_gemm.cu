@@ -61,8 +61,10 @@ struct EpiParams {
 
 struct GemmShape {
   int m, n, k;  // k logical
-  int ksplit;   // K chunks per output tile (dW split-K, reduced with TMA add); 1 = no split
+  int streamk;  // 1: stream-K -- every cluster owns an equal run of (tile, k-block) iterations and
+                //    partial tiles are summed with TMA add-reduce stores into the zeroed output
   int group_m;  // M tiles per raster group: each group sweeps all N with its A panels L2-resident
+  int wave_slot;  // >= 0: wave-synchronised schedule on counter slot g_wave_ctr[wave_slot] (see below)
   int exp;      // experiment flags (timing studies only, results invalid): 1 skip B loads, 2 skip metadata cp, 4 every tile loads the B tile of n = 0,
                 //  16 no activation math in the epilogue, 32 no epilogue global loads
 };
@@ -132,6 +134,58 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 232448, "shared memory overflow");
 };
 
+// Work walk shared by the producer, MMA and epilogue roles: static round-robin over whole
+// tiles, or stream-K (cluster c owns linear k-block iterations [c T / C, (c + 1) T / C) of
+// T = tiles x k-blocks, so every cluster does the same work whatever the tile count).
+// Wave synchronisation.  A persistent kernel's CTAs drift apart over many waves (a few percent
+// speed difference per SM accumulates), so CTAs that should share A / B panels in L2 end up
+// a wave apart and every panel streams from HBM several times (measured on B200: dW_in at C3
+// read 15.3 GB with drift, 7.0 GB wave-synchronised, and ran 10% faster at the higher clock
+// the lower HBM power allowed).  Each producer counts the tiles whose loads it has issued and,
+// before the first load of wave w, waits until all CTAs have issued wave w - 1.  Purely a
+// locality hint: the wait is bounded (~20 us), so CTAs that are not co-resident (an SM taken
+// by another kernel) only cost time, never a hang.  The last CTA to exit resets the slot, so
+// every launch (and every CUDA-graph replay) starts from zero; the host spreads streams over
+// slots.
+constexpr int kWaveSlots = 64;
+__device__ unsigned int g_wave_ctr[kWaveSlots][2];  // [slot][0: tiles issued, 1: CTAs exited]
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct WorkIter {
+  long long it, end;
+  int tile, stride;
+  bool sk;
+  __device__ __forceinline__ WorkIter(bool streamk, int num_tiles, int num_kb, int cid, int ncl) : sk(streamk) {
+    const long long t = static_cast<long long>(num_tiles) * num_kb;
+    it = sk ? t * cid / ncl : 0;
+    end = sk ? t * (cid + 1) / ncl : 0;
+    tile = cid;
+    stride = ncl;
+  }
+  // next segment: output tile and its k-block range [kb0, kb1)
+  __device__ __forceinline__ bool next(int num_tiles, int num_kb, int& t, int& kb0, int& kb1) {
+    if (sk) {
+      if (it >= end) return false;
+      t = static_cast<int>(it / num_kb);
+      kb0 = static_cast<int>(it - static_cast<long long>(t) * num_kb);
+      kb1 = static_cast<int>(min(static_cast<long long>(num_kb), kb0 + (end - it)));
+      it += kb1 - kb0;
+      return true;
+    }
+    if (tile >= num_tiles) return false;
+    t = tile;
+    kb0 = 0;
+    kb1 = num_kb;
+    tile += stride;
+    return true;
+  }
+};
+
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group_m, int& mb, int& nb) {
   const int per_group = group_m * num_n;
   const int group = tile / per_group;
@@ -168,8 +222,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t rank = kCG == 2 ? cluster_rank() : 0;
   const int num_m = shp.m / (128 * kCG);
   const int num_n = (shp.n + kBN - 1) / kBN;
-  const int num_tiles = num_m * num_n * shp.ksplit;  // work units: (output tile, K chunk)
-  const int num_kb = shp.k / C::BK / shp.ksplit;        // k-blocks per unit
+  const int num_tiles = num_m * num_n;
+  const int num_kb = shp.k / C::BK;  // k-blocks per output tile
   const int cluster_id = blockIdx.x / kCG, num_clusters = gridDim.x / kCG;
 
   if (warp == 0 && lane == 0) {
@@ -202,14 +256,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      WorkIter wk(shp.streamk, num_tiles, num_kb, cluster_id, num_clusters);
+      int tile, kb0, kb1, wave = 0;
+      unsigned int* wctr = shp.wave_slot >= 0 ? &g_wave_ctr[shp.wave_slot][0] : nullptr;
+      while (wk.next(num_tiles, num_kb, tile, kb0, kb1)) {
+        if (wctr != nullptr && wave > 0) {
+          // every producer has issued the previous wave's loads (bounded wait)
+          const unsigned int target = gridDim.x * wave;
+          const long long t0 = clock64();
+          while (static_cast<int>(ld_acquire_gpu(wctr) - target) < 0 && clock64() - t0 < 40000) __nanosleep(32);
+        }
         int mb, nb;
-        tile_coords(tile / shp.ksplit, num_m, num_n, shp.group_m, mb, nb);
-        const int kb_base = (tile % shp.ksplit) * num_kb;
+        tile_coords(tile, num_m, num_n, shp.group_m, mb, nb);
         const int m0 = mb * 128 * kCG + 128 * rank;      // this CTA's A rows
         const int nb0 = ((shp.exp & 4) ? 0 : nb * kBN) + C::BN_CTA * rank;  // this CTA's B rows (N split)
-        for (int kbi = 0; kbi < num_kb; ++kbi) {
-          const int kb = kb_base + kbi;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + C::A_BYTES;
@@ -240,6 +301,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             phase ^= 1;
           }
         }
+        if (wctr != nullptr) atomicAdd(wctr, 1u);
+        ++wave;
       }
     }
   } else if (warp == 1) {
@@ -249,11 +312,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      WorkIter wk(shp.streamk, num_tiles, num_kb, cluster_id, num_clusters);
+      int tile, kb0, kb1;
+      while (wk.next(num_tiles, num_kb, tile, kb0, kb1)) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * C::STAGE_BYTES);
@@ -277,7 +342,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             } else {
               bdesc = make_sdesc(b_addr + j * 32, 16, 1024, 2);
             }
-            const uint32_t accum = (kb | j) != 0 ? 1u : 0u;
+            const uint32_t accum = (kb != kb0 || j != 0) ? 1u : 0u;
             if constexpr (kSparse) {
               // MMA j's metadata sits in TMEM column E_COL + j; the instruction takes a
               // 2-column-aligned address and selects the column with sparse_id2 (idesc[0:2))
@@ -316,9 +381,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int mj = lane >> 3, mi = lane & 7;
       int acc = 0, sbuf = 0, par = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, par ^= 1) {
+      WorkIter wk(false, num_tiles, num_kb, cluster_id, num_clusters);
+      int tile, kb0, kb1;
+      for (; wk.next(num_tiles, num_kb, tile, kb0, kb1); par ^= 1) {
         int mb, nb;
-        tile_coords(tile / shp.ksplit, num_m, num_n, shp.group_m, mb, nb);
+        tile_coords(tile, num_m, num_n, shp.group_m, mb, nb);
         const int m_w = mb * 128 * kCG + 128 * rank + 32 * q;  // first TMEM row of this warp
         const int n_base = nb * kBN;
         mbar_wait(&tfull_bar[acc], acc_phase);
@@ -567,10 +634,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint8_t* stg = smem + C::EPI_OFF + (warp - 4) * 4096;
       int acc = 0, sbuf = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      WorkIter wk(shp.streamk, num_tiles, num_kb, cluster_id, num_clusters);
+      int tile, kb0, kb1;
+      while (wk.next(num_tiles, num_kb, tile, kb0, kb1)) {
         int mb, nb;
-        tile_coords(tile / shp.ksplit, num_m, num_n, shp.group_m, mb, nb);
-        const bool first_chunk = (tile % shp.ksplit) == 0;
+        tile_coords(tile, num_m, num_n, shp.group_m, mb, nb);
+        const bool first_chunk = kb0 == 0;                  // adds the decay exactly once
+        const bool partial = kb0 != 0 || kb1 != num_kb;     // stream-K piece: add-reduce
         const int m_w = mb * 128 * kCG + 128 * rank + 32 * q;  // first row of this warp
         const int m = m_w + lane;
         const int n_base = nb * kBN;
@@ -665,7 +735,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               // two 16-row boxes: the gated first weight's rows go back to [u; v] order
               const int y0 = ep.gate_ff > 0 ? gate_row_dev(m_w, ep.gate_ff) : m_w;
               const int y1 = ep.gate_ff > 0 ? gate_row_dev(m_w + 16, ep.gate_ff) : m_w + 16;
-              if (shp.ksplit > 1) {
+              if (partial) {
                 tma_reduce_add_2d(&tmD, stg, n0, y0);
                 tma_reduce_add_2d(&tmD, stg + 2048, n0, y1);
               } else {
@@ -736,6 +806,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_cg<kCG>(tmem_base, C::TMEM_COLS);
+  if (shp.wave_slot >= 0 && threadIdx.x == 0) {
+    // the last CTA out resets the slot for the next launch on this stream
+    if (atomicAdd(&g_wave_ctr[shp.wave_slot][1], 1u) == gridDim.x - 1) {
+      atomicExch(&g_wave_ctr[shp.wave_slot][0], 0u);
+      atomicExch(&g_wave_ctr[shp.wave_slot][1], 0u);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -801,6 +878,29 @@ static int num_sms() {
 // Sparse GEMMs (A = compressed weight, 1.125 B per logical K per row incl. metadata)
 // take as many M tiles as fit a ~48 MB L2 budget; dense dW panels (K = tokens) are
 // far larger than L2, so they keep the wave-square default of 8.
+// Stream-K (S24_STREAMK=1; off by default): balances badly filled waves (C2 dW: 64 tiles on
+// 74 CTA pairs), but clusters then sit at different K offsets of the same tiles and stop sharing
+// operand panels in L2 -- measured on B200 it quadrupled the HBM reads of the C2 dW GEMMs
+// (176 -> 748 MB) and made them 20% slower, and C3 dW2 read 17.5 GB instead of 5 GB.
+static int use_streamk(int tiles, int clusters, int num_kb) {
+  static const bool det = getenv("S24_DETERMINISTIC") != nullptr;
+  static const int env = getenv("S24_STREAMK") ? atoi(getenv("S24_STREAMK")) : -1;
+  (void)tiles;
+  (void)clusters;
+  (void)num_kb;
+  return !det && env == 1 ? 1 : 0;
+}
+
+// Wave-synchronised schedule (g_wave_ctr): on for the dW GEMMs (panels of K = tokens, far
+// larger than L2), S24_WAVESYNC=0/1 turns it off / on for every GEMM.  Slot = stream hash.
+static int wave_slot(void* stream, bool dflt) {
+  static const int env = getenv("S24_WAVESYNC") ? atoi(getenv("S24_WAVESYNC")) : -1;
+  const bool on = env < 0 ? dflt : env != 0;
+  if (!on) return -1;
+  const uintptr_t h = reinterpret_cast<uintptr_t>(stream);
+  return static_cast<int>((h ^ (h >> 7) ^ (h >> 17)) % kWaveSlots);
+}
+
 static int exp_flags() {
   static const int v = getenv("S24_EXP") ? atoi(getenv("S24_EXP")) : 0;
   return v;
@@ -827,8 +927,8 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_done = true;
   }
-  const int tiles = (shp.m / (128 * kCG)) * ((shp.n + kBN - 1) / kBN) * shp.ksplit;
-  const int clusters = tiles < num_sms() / kCG ? tiles : num_sms() / kCG;
+  const int tiles = (shp.m / (128 * kCG)) * ((shp.n + kBN - 1) / kBN);
+  const int clusters = (shp.streamk || tiles > num_sms() / kCG) ? num_sms() / kCG : tiles;
   if (clusters <= 0) return S24_OK;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * kCG);
@@ -931,8 +1031,9 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
   const int tile_m = pair ? 256 : 128;
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 1,
-                pick_group_m(static_cast<int>(m / tile_m), 1.125 * tile_m * static_cast<double>(k)), exp_flags()};
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0,
+                pick_group_m(static_cast<int>(m / tile_m), 1.125 * tile_m * static_cast<double>(k)),
+                wave_slot(stream, false), exp_flags()};
   EpiParams ep{d,       ldd,
                bias,    aux,
                ldaux,   dbias,
@@ -1009,36 +1110,21 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   me = mb;  // unused by the dense kernels
   CUtensorMap md;
   if (int rc = make_map(&md, d, n, m, ldd, 32, 16, kMapF32Sw128)) return rc;  // 16-row store boxes
-  // split K so the (tile, K chunk) units fill whole waves of CTA pairs; chunks are
-  // reduced in fp32 with TMA add-reduce stores into the zeroed output
   const int clusters = num_sms() / (pair ? 2 : 1);
   const int tiles = static_cast<int>((m / (pair ? 256 : 128)) * (n / BN));
-  const int num_kb = static_cast<int>(k / 64);
-  int ksplit = 1;
-  if (!getenv("S24_DETERMINISTIC")) {
-    double best = static_cast<double>(tiles) / (((tiles + clusters - 1) / clusters) * clusters);
-    // measured on B200 (C2 dW, 64 tiles on 74 pairs): the fp32 reduce traffic and
-    // memset cost more than the idle 14%, so only split badly under-filled grids
-    for (int s = 2; s <= 8 && best < 0.75; ++s) {
-      if (num_kb % s != 0 || num_kb / s < 32) continue;
-      const int units = tiles * s;
-      const double eff = static_cast<double>(units) / (((units + clusters - 1) / clusters) * clusters);
-      if (eff > best + 0.02) {
-        best = eff;
-        ksplit = s;
-      }
-    }
-  }
+  const int streamk = use_streamk(tiles, clusters, static_cast<int>(k / 64));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (ksplit > 1) {
+  if (streamk) {
     cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   }
   const int tile_m = pair ? 256 : 128;
   static const int env_dw = getenv("S24_GROUP_M_DW") ? atoi(getenv("S24_GROUP_M_DW")) : 8;
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), ksplit,
-                static_cast<int>(m / tile_m) < env_dw ? static_cast<int>(m / tile_m) : env_dw, exp_flags()};
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), streamk,
+                static_cast<int>(m / tile_m) < env_dw ? static_cast<int>(m / tile_m) : env_dw,
+                streamk ? -1 : wave_slot(stream, true), exp_flags()};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
+
 #define S24_DW(AMN, BMN, BNV, CG)                                                                      \
   return launch_gemm<false, AMN, BMN, BNV, stages_for<Cfg<false, AMN, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
                      kEpiDw>(ma, mb, me, md, md, md, shp, ep, st)
@@ -1089,9 +1175,16 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
     if (int rc = make_map(&mb, b, k, n, ldb, 64, bn_cta)) return rc;
   }
   if (int rc = make_map(&md, d, n, m, ldd, 32, 16, kMapF32Sw128)) return rc;
-  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 1, 8, 0};
-  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int sk_tiles = static_cast<int>((m / (pair ? 256 : 128)) * (n / (wide ? 256 : 128)));
+  const int streamk = use_streamk(sk_tiles, num_sms() / (pair ? 2 : 1), static_cast<int>(k / 128));
+  if (streamk) {
+    cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
+    S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+  }
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), streamk, 8,
+                streamk ? -1 : wave_slot(stream, true), 0};
+  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
   // BN = 256 with one TMEM accumulator (256 + 4 metadata columns): K = tokens is long, so the
   // un-overlapped epilogue is a small share; the B half per CTA is exactly two 64-wide chunks
 #define S24_SDW(BMN, BNV, CG, ACC)                                                                            \

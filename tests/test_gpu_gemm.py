@@ -4,6 +4,7 @@ plain fp32 torch reference on the same bf16 operands.
 Tolerance: outputs are bf16 (sparse) or fp32 (dW) from fp32 accumulation;
 normwise relative error <= 1e-2 for bf16 outputs and <= 2e-3 for fp32 dW,
 plus an elementwise bound of 3 bf16 ulps of the row scale."""
+import os
 import numpy as np
 import pytest
 import torch
@@ -145,3 +146,57 @@ def test_sparse_gemm_token_major_output_and_epilogues(m, k, n, epi):
         dz = ref * gin.float()
         assert normwise_rel(out.float().cpu(), dz.cpu()) < 1e-2
         assert normwise_rel(db.cpu(), dz.sum(0).cpu()) < 1e-3
+
+
+@pytest.mark.parametrize("gate_ff", [0, 512])
+def test_dense_dw_gemm_c2_shape(gate_ff):
+    """C2-shaped dW (64 whole tiles on 74 CTA pairs) with the masked decay, plain and gated
+    (u/v-interleaved rows restored to [u; v] order)."""
+    from paper_2404_01847_b200.engine import gemm_dw
+    from paper_2404_01847_b200 import transposable_search_conv
+
+    m, n, k = (1024, 1024, 16384) if gate_ff else (1024, 4096, 16384)
+    w = torch.randn(m, n, device="cuda").bfloat16()
+    mask = transposable_search_conv(w)
+    a = torch.randn(k, m, device="cuda").bfloat16()  # token-major upstream gradient (MN-major A)
+    b = torch.randn(k, n, device="cuda").bfloat16()
+    lam = 0.5
+    out = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+    if gate_ff:
+        # gated first weight: dW rows come out of the u/v interleave back in [u; v] order
+        from paper_2404_01847_b200 import engine as E
+
+        p = torch.arange(m, device="cuda")
+        orig = torch.where(p % 32 < 16, 16 * (p // 32) + p % 32, gate_ff + 16 * (p // 32) + p % 32 - 16)
+        a_perm = torch.empty_like(a)
+        a_perm[:, :] = a[:, orig]
+        op = E.CompressedOperand.empty(m, n, "cuda", perm_ff=gate_ff)
+        E.search_compress(w, op)
+        gemm_dw(a_perm, True, b, True, m, n, k, out, w, op.idx, lam, gate_ff=gate_ff)
+    else:
+        gemm_dw(a, True, b, True, m, n, k, out, w, mask.idx, lam)
+    ref = a.float().t() @ b.float() + lam * (1 - mask.bits.float()) * w.float()
+    assert torch.isfinite(out).all()
+    assert normwise_rel(out.cpu(), ref.cpu()) < 2e-3
+
+
+def test_dense_dw_gemm_streamk_forced_small_shapes():
+    """S24_STREAMK=1 (stream-K schedule: partial tiles add-reduced into the zeroed output) on
+    shapes with fewer k-blocks than clusters, and S24_WAVESYNC=1 on every GEMM."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, sys; sys.path.insert(0, %r)\n"
+        "from paper_2404_01847_b200.engine import gemm_dw\n"
+        "for m, n, k in [(128, 128, 64), (256, 512, 320), (384, 256, 1024), (512, 768, 4096)]:\n"
+        "    a = torch.randn(k, m, device='cuda').bfloat16(); b = torch.randn(k, n, device='cuda').bfloat16()\n"
+        "    out = torch.full((m, n), float('nan'), device='cuda')\n"
+        "    gemm_dw(a, True, b, True, m, n, k, out)\n"
+        "    ref = a.float().t() @ b.float()\n"
+        "    e = float((out - ref).norm() / ref.norm())\n"
+        "    assert e < 2e-3, (m, n, k, e)\n"
+        "print('ok')\n" % os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+    env = dict(os.environ, S24_STREAMK="1", S24_WAVESYNC="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
