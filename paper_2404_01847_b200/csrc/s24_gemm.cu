@@ -66,7 +66,8 @@ struct GemmShape {
   int group_m;  // M tiles per raster group: each group sweeps all N with its A panels L2-resident
   int wave_slot;  // >= 0: wave-synchronised schedule on counter slot g_wave_ctr[wave_slot] (see below)
   int exp;      // experiment flags (timing studies only, results invalid): 1 skip B loads, 2 skip metadata cp, 4 every tile loads the B tile of n = 0,
-                //  16 no activation math in the epilogue, 32 no epilogue global loads
+                //  16 no activation math in the epilogue, 32 no epilogue global loads,
+                //  128 no GELU'(z) AUX stores, 256 no D stores (fragment epilogue)
 };
 
 __constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
@@ -568,13 +569,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
                 pd[4 * c + j] = pack_bf16x2(x0, x1);
               }
-              if constexpr (kEpi == kEpiGeluGrad) {
+              if (kEpi == kEpiGeluGrad && !(shp.exp & 128)) {
                 // GELU'(z) -> AUX unit (row m_w + 8 j + t4, this chunk)
                 aux_frag(ep.aux, (m_w >> 4) + (j >> 1), shp.n, n0)[32 * (j & 1) + lane] =
                     make_uint4(gq[0], gq[1], gq[2], gq[3]);
               }
             }
             // [32 tokens][32 features], 64-byte rows, 64B swizzle, double-buffered; one stmatrix per c
+            if (shp.exp & 256) continue;
             uint8_t* zb = stg + sbuf * 2048;
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             __syncwarp();
