@@ -253,12 +253,19 @@ class SparseStep:
             E.compress_values(self.w_in, self.op_in)
             E.compress_values(self.w2, self.op_out)
         st = E.ffn_forward(x, self.op_in, self.bias, self.op_out, self.act, fused=True)
+        work = []
+
+        def grads_ready():
+            # the one all-reduce of [dW_in | dbias | dW2] starts while dX is still computing
+            if self.world > 1:
+                work.append(self.torch.distributed.all_reduce(self.bucket, group=self.pg, async_op=True))
+
         g = E.ffn_backward(st, dy, self.op_in, self.op_out, self.act, w_in_dense=self.w_in, w2_dense=self.w2,
                            lam=LAMBDA / self.world, dw_in_out=self.dw_in, dw2_out=self.dw2, mvue=bool(self.mvue),
-                           rng_seed=self.t, mvue_exact=self.mvue == "exact")
-        self.dbias.copy_(g.dbias_in)
-        if self.world > 1:
-            self.torch.distributed.all_reduce(self.bucket, group=self.pg)
+                           rng_seed=self.t, mvue_exact=self.mvue == "exact", dbias_out=self.dbias,
+                           grads_ready=grads_ready)
+        for w in work:
+            w.wait()
         self.t += 1
         return st, g
 
@@ -287,6 +294,34 @@ def dense_step_factory(w_in, bias, w2, act):
         y = F.linear(act_fn(F.linear(xg, W1, B1)), W2)
         y.backward(dy)
         W1.grad = B1.grad = W2.grad = None
+
+    return step
+
+
+def dense_gemm_only_factory(w_in, w2, x, dy):
+    """The six bf16 GEMMs of a dense FFN step on cuBLAS with preallocated outputs (Z = X W_in^T,
+    Y = A W2^T, dA = dY W2, dW2 = dY^T A, dX = dZ W_in, dW_in = dZ^T X) and no activation,
+    bias or elementwise work: a floor for any dense implementation on this box."""
+    import torch
+
+    n = x.shape[0]
+    r_in, d_ff = w_in.shape[0], w2.shape[1]
+    z = torch.empty((n, r_in), dtype=torch.bfloat16, device=x.device)
+    act = torch.empty((n, d_ff), dtype=torch.bfloat16, device=x.device).normal_()
+    y = torch.empty_like(dy)
+    da = torch.empty_like(act)
+    dz = torch.empty_like(z).normal_()
+    dx = torch.empty_like(x)
+    dw2 = torch.empty_like(w2)
+    dw1 = torch.empty_like(w_in)
+
+    def step():
+        torch.mm(x, w_in.t(), out=z)
+        torch.mm(act, w2.t(), out=y)
+        torch.mm(dy, w2, out=da)
+        torch.mm(dy.t(), act, out=dw2)
+        torch.mm(dz, w_in, out=dx)
+        torch.mm(dz.t(), x, out=dw1)
 
     return step
 
@@ -387,11 +422,17 @@ def run_ours(a, cfg):
         del mstep
 
     # ---- dense cuBLAS bf16 baseline on the same box ----
-    dense = None
+    dense = dense_gemm_only = None
     if not a.no_dense:
         dstep = dense_step_factory(w_in, bias, w2, cfg["act"])
         dms, _ = time_loop(lambda: dstep(x, dy), max(10, a.steps // 4), a.warmup, dist if world > 1 else None)
         dense = n_tok * world / (dms / max(10, a.steps // 4) / 1000.0)
+        del dstep
+        # lower bound of any dense implementation: the step's six cuBLAS GEMMs alone
+        gstep = dense_gemm_only_factory(w_in, w2, x, dy)
+        gms, _ = time_loop(gstep, max(10, a.steps // 4), a.warmup, dist if world > 1 else None)
+        dense_gemm_only = n_tok * world / (gms / max(10, a.steps // 4) / 1000.0)
+        del gstep
 
     # ---- per-kernel attribution (CUDA events on the launching stream) ----
     timer = EventTimer()
@@ -484,6 +525,8 @@ def run_ours(a, cfg):
                        "tokens_per_rank": n_tok, "mask_refresh_every": REFRESH, "lambda_w": LAMBDA,
                        "parallelism": f"dp{world}", "l2": "per-step working set ~1 GB > 126 MB L2 (no flush)"},
             "dense_tokens_per_s": dense, "speedup_vs_dense": (value / dense) if dense else None,
+            "dense_gemm_only_tokens_per_s": dense_gemm_only,
+            "speedup_vs_dense_gemm_only": (value / dense_gemm_only) if dense_gemm_only else None,
             "variants": {k: dict(v, speedup_vs_dense=(v["tokens_per_s"] / dense) if dense else None)
                          for k, v in variants.items()},
             "mask_search": mask_search,

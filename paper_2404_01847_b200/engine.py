@@ -280,13 +280,19 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
                  w_in_dense: torch.Tensor | None = None, w2_dense: torch.Tensor | None = None,
                  lam: float = 0.0, dw_in_out: torch.Tensor | None = None,
                  dw2_out: torch.Tensor | None = None, mvue: bool = False, rng_seed: int = 0,
-                 mvue_exact: bool = True) -> Grads:
+                 mvue_exact: bool = True, dbias_out: torch.Tensor | None = None,
+                 grads_ready=None) -> Grads:
     """dA = dY W2~ (out_bwd, W2's transposed orientation) -> dZ (activation
     backward, bias gradient) -> dX = dZ W_in~ (in_bwd); dense dW2 = dY^T A and
     dW_in = dZ^T X with the masked decay lam (1 - M) W fused (gated_ffn.py:327-356).
     mvue=True: both weight gradients use the MVUE-sparsified upstream gradients
     (dY^T with salt 1, dZ^T with salt 2, seeds (rng_seed << 2) ^ salt) on the
-    2:4 tensor cores (gated_ffn.py:367-373)."""
+    2:4 tensor cores (gated_ffn.py:367-373).
+
+    Launch order: dA/dZ (+ bias gradient), dW2, dW_in, then dX, so that
+    `grads_ready()` -- called once every weight/bias gradient is enqueued -- can start
+    the data-parallel all-reduce of the gradient bucket while dX is still computing.
+    dbias_out / dw_in_out / dw2_out let the caller hand in views of that bucket."""
     n, d = st.x.shape
     r_in, d_ff = w_in.rows, w2.cols
     if tuple(dy.shape) != (n, d):
@@ -297,23 +303,21 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     gate_ff = w_in.perm_ff
     if st.g2 is not None:
         # gated: dZ_u = dA v act'(u), dZ_v = dA act(u) straight into the interleaved dZ, bias grads fused
-        dbias = torch.zeros(r_in, dtype=torch.float32, device=dev)
+        dbias = dbias_out.zero_() if dbias_out is not None else torch.zeros(r_in, dtype=torch.float32, device=dev)
         spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dy, False, n, dz, tag="k4_spmm_bwd_out", epi=C.EPI_DGATED,
              aux=st.g, aux2=st.g2, dbias=dbias, out_t=True, gate_ff=d_ff)
     elif st.g is not None:
         # dZ = (dY W2~) * GELU'(z) with the bias gradient reduced in the same epilogue
-        dbias = torch.zeros(r_in, dtype=torch.float32, device=dev)
+        dbias = dbias_out.zero_() if dbias_out is not None else torch.zeros(r_in, dtype=torch.float32, device=dev)
         spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dy, False, n, dz, tag="k4_spmm_bwd_out", epi=C.EPI_DGELU,
              aux=st.g, dbias=dbias, out_t=True)
     else:
         da = torch.empty((n, d_ff), dtype=torch.bfloat16, device=dev)
         spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dy, False, n, da, tag="k4_spmm_bwd_out", out_t=True)
-        dbias = torch.empty(r_in, dtype=torch.float32, device=dev)
+        dbias = dbias_out if dbias_out is not None else torch.empty(r_in, dtype=torch.float32, device=dev)
         with TIMER("k7_act_bwd"):
             C.call("s24_act_bwd", st.z.data_ptr(), r_in, da.data_ptr(), d_ff, d_ff, n, ACT_CODES[act],
                    dz.data_ptr(), r_in, dbias.data_ptr(), C.stream_of(dz))
-    dx = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
-    spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dz, False, n, dx, tag="k4_spmm_bwd_in", out_t=True)
     # dW2[d, d_ff] = dY^T A and dW_in[r_in, d] = dZ^T X: K = tokens, both operands token-major (MN-major)
     dw2 = dw2_out if dw2_out is not None else torch.empty((d, d_ff), dtype=torch.float32, device=dev)
     dw_in = dw_in_out if dw_in_out is not None else torch.empty((r_in, d), dtype=torch.float32, device=dev)
@@ -326,4 +330,8 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
         gemm_dw(dy, True, st.a, True, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")
         gemm_dw(dz, True, st.x, True, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam, tag="k5_gemm_dw_in",
                 gate_ff=gate_ff)
+    if grads_ready is not None:
+        grads_ready()
+    dx = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
+    spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dz, False, n, dx, tag="k4_spmm_bwd_in", out_t=True)
     return Grads(dx, dw_in, dbias, dw2)

@@ -298,3 +298,32 @@ def _dz_from(st, dy, op_in, op_out, act):
         E.spmm(op_out.bwd_vals, op_out.bwd_e, d_ff, dy.shape[1], dy, False, n, dz, epi=C.EPI_DGELU, aux=st.g,
                dbias=db, out_t=True)
     return dz.double().cpu().numpy()
+
+
+def test_backward_bucket_views_and_grads_ready_hook():
+    """ffn_backward writes dW_in / dbias / dW2 into caller views (the DP gradient bucket) and
+    calls grads_ready() once all of them are enqueued, before dX (bench.py starts the
+    all-reduce there); results equal the plain call."""
+    from paper_2404_01847_b200 import engine as E
+
+    d, d_ff, n = 128, 256, 128
+    c = _case("gelu", d, d_ff, n, seed=5)
+    w_in, b, w2 = to_dev_bf16(c["w_in"]), to_dev_bf16(c["bias_in"]), to_dev_bf16(c["w2"])
+    op_in, op_out = E.CompressedOperand.empty(d_ff, d, "cuda"), E.CompressedOperand.empty(d, d_ff, "cuda")
+    E.search_compress(w_in, op_in)
+    E.search_compress(w2, op_out)
+    x, dy = to_dev_bf16(c["x"]), to_dev_bf16(c["dy"])
+    st = E.ffn_forward(x, op_in, b, op_out, "gelu", fused=True)
+    ref = E.ffn_backward(st, dy, op_in, op_out, "gelu", w_in_dense=w_in, w2_dense=w2, lam=1e-2)
+    bucket = torch.full((w_in.numel() + d_ff + w2.numel(),), float("nan"), device="cuda")
+    dwi, db, dw2 = (bucket[:w_in.numel()].view(w_in.shape), bucket[w_in.numel():w_in.numel() + d_ff],
+                    bucket[w_in.numel() + d_ff:].view(w2.shape))
+    calls = []
+    g = E.ffn_backward(st, dy, op_in, op_out, "gelu", w_in_dense=w_in, w2_dense=w2, lam=1e-2, dw_in_out=dwi,
+                       dw2_out=dw2, dbias_out=db, grads_ready=lambda: calls.append(1))
+    torch.cuda.synchronize()
+    assert calls == [1]
+    assert g.dw_in.data_ptr() == dwi.data_ptr() and g.dbias_in.data_ptr() == db.data_ptr()
+    assert torch.isfinite(bucket).all()
+    assert torch.equal(dwi, ref.dw_in) and torch.equal(dw2, ref.dw2) and torch.equal(g.dx, ref.dx)
+    assert torch.allclose(db, ref.dbias_in, rtol=1e-5, atol=1e-6)

@@ -8,12 +8,13 @@ keys = [
     ("Kernel Name", "kernel"), ("gpu__time_duration.sum", "us"),
     ("dram__bytes_read.sum", "dram_rd"), ("dram__bytes_write.sum", "dram_wr"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%"),
-    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor%"),
-    ("sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_on.avg.pct_of_peak_sustained_elapsed", "sp_ops%"),
-    ("sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed", "dn_ops%"),
+    ("gpc__cycles_elapsed.avg.per_second", "clk"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor%"),
+    ("sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_on.avg.pct_of_peak_sustained_elapsed", "sp_ops%"),
+    ("sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed", "dn_ops%"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "lsu_smem%"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm%"),
-    ("sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active", "tmem_inst%"),
+    ("lts__t_sector_hit_rate.pct", "l2_hit%"),
     ("launch__registers_per_thread", "regs"),
 ]
 idx = [(hdr.index(k) if k in hdr else -1, n) for k, n in keys]
