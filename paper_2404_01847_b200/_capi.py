@@ -17,7 +17,8 @@ import torch
 from .matrix import FormatError, ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libs24b200.so")
+# S24_LIB_PATH: load a differently-built variant of the same library (build experiments)
+LIB_PATH = os.environ.get("S24_LIB_PATH") or os.path.join(_HERE, "libs24b200.so")
 
 S24_OK, S24_ERR_SHAPE, S24_ERR_FORMAT, S24_ERR_UNSUPPORTED, S24_ERR_CUDA, S24_ERR_ARG = range(6)
 S24_BF16, S24_F32, S24_F64 = 0, 1, 2

@@ -30,20 +30,26 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build the library (default: in-tree LIB).  `out` + `defines` (e.g. ["S24_EPI_WARPS=8"])
+    build a variant elsewhere for experiments; load it with S24_LIB_PATH."""
+    lib = out or LIB
+    if out is None and not defines and not force and not _stale():
         return LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *srcs]
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", lib + ".tmp", *srcs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libs24b200.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    out = args[args.index("-o") + 1] if "-o" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, out=out, defines=defs))
