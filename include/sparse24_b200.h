@@ -198,6 +198,34 @@ int s24_act_fwd(const uint16_t* z, int64_t ldz, int64_t r, int64_t n, int act, u
 int s24_act_bwd(const uint16_t* z, int64_t ldz, const uint16_t* da, int64_t ldda, int64_t r, int64_t n, int act,
                 uint16_t* dz, int64_t lddz, float* dbias, void* stream);
 
+/* ---- optimizer step -----------------------------
+ * One fused pass per parameter: masked decay on the gradient (decay_mode
+ * S24_DECAY_ON_GRADIENTS: g + lambda_w (1 - M) W, optim.py:105-114), Adam
+ * (adam_step, optim.py:128-147: u = b1 u + (1 - b1) g, v = b2 v + (1 - b2) g^2,
+ * W -= lr u / ((sqrt(v / bias_corr2) + eps) bias_corr1)), and the SR-STE decay at
+ * the update site (S24_DECAY_ON_WEIGHTS: W -= lr_lambda (1 - M) W_before,
+ * srste_weight_decay optim.py:117-125, trainer.py:442-447).  W, u, v are updated in
+ * place; state_dtype S24_F64 reproduces the reference bit for bit when the scalars are
+ * passed as Python computes them (one_minus_beta1 = 1.0 - beta1, bias_corr1 =
+ * 1.0 - beta1**t, lr_lambda = lr * lambda_w, ...); S24_F32 is the fp32-master-weight
+ * path.  g: fp32 or the state's dtype.  idx (pattern indices of the rows x cols
+ * weight's mask) is required by the decay modes; without it the parameter is treated
+ * as a flat vector of rows * cols elements (biases). */
+#define S24_DECAY_NONE 0
+#define S24_DECAY_ON_GRADIENTS 1
+#define S24_DECAY_ON_WEIGHTS 2
+int s24_adam_step(void* w, void* u, void* v, int state_dtype, const void* g, int g_dtype, int64_t rows, int64_t cols,
+                  const uint8_t* idx, double lr, double beta1, double beta2, double eps, double one_minus_beta1,
+                  double one_minus_beta2, double bias_corr1, double bias_corr2, double lambda_w, double lr_lambda,
+                  int decay_mode, void* stream);
+
+/* Mask flips of a refresh (flip_rate optim.py:94-102 = changed_bits / (rows cols); the
+ * per-block counts of block_flip_stats optim.py:164-192): adds to *changed_bits (device
+ * uint64, caller zeroes) the number of mask bits that differ between two pattern-index
+ * maps of nblocks 4x4 blocks, and to block_flips[i] (int32, optional) block i's count. */
+int s24_mask_flips(const uint8_t* idx_prev, const uint8_t* idx_curr, int64_t nblocks, unsigned long long* changed_bits,
+                   int32_t* block_flips, void* stream);
+
 /* ---- standalone masked decay on an fp32 gradient (optim.py:105-114) -------- */
 int s24_masked_decay(float* g, const void* w, int w_dtype, const uint8_t* idx, int64_t rows, int64_t cols,
                      float lambda_w, void* stream);

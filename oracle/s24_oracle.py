@@ -395,6 +395,45 @@ def flip_rate(m_prev, m_curr) -> float:  # optim.py:94-102
     return float(np.abs(b - a).sum()) / a.size
 
 
+def adam_step(w, u, v, t: int, g, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
+    """optim.py:128-147 restated in float64 with the reference's evaluation order; returns
+    new (w, u, v) for step number t (1-based, already incremented)."""
+    w, u, v = (np.array(a, dtype=np.float64) for a in (w, u, v))
+    g = np.asarray(g, dtype=np.float64)
+    u *= beta1
+    u += (1.0 - beta1) * g
+    v *= beta2
+    v += (1.0 - beta2) * (g * g)
+    denom = np.sqrt(v / (1.0 - beta2 ** t))
+    denom += eps
+    denom *= 1.0 - beta1 ** t
+    w -= lr * u / denom
+    return w, u, v
+
+
+def srste_weight_decay(w_next_base, w, m, lr: float, lambda_w: float):  # optim.py:117-125
+    return np.asarray(w_next_base, dtype=np.float64) - lr * lambda_w * ((1 - np.asarray(m)) * np.asarray(w, dtype=np.float64))
+
+
+def train_update(w, u, v, t: int, g, m, lambda_w: float, mode: str, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
+    """trainer.py:438-447: masked decay on the gradient (mode 'on_gradients') or at the
+    update site ('on_weights') around one Adam step."""
+    if mode == "on_gradients" and lambda_w > 0:
+        g = masked_decay_gradient(g, w, m, lambda_w)
+    w_before = np.array(w, dtype=np.float64)
+    w1, u1, v1 = adam_step(w, u, v, t, g, lr, beta1, beta2, eps)
+    if mode == "on_weights" and lambda_w > 0:
+        w1 = srste_weight_decay(w1, w_before, m, lr, lambda_w)
+    return w1, u1, v1
+
+
+def block_flips(m_prev, m_curr) -> np.ndarray:
+    """Per-4x4-block count of changed mask bits (the flips of block_flip_stats, optim.py:164-192)."""
+    a = blocks16(np.asarray(m_prev, dtype=np.int64))
+    b = blocks16(np.asarray(m_curr, dtype=np.int64))
+    return np.abs(b - a).sum(axis=1)
+
+
 # ---------------------------------------------------------------------------
 # the reference's own compiled kernels (oracle/_ref), when built
 

@@ -1,4 +1,4 @@
-"""Masked decay and the schedule pieces on the path (optim.py:51-114 of the reference)."""
+"""Masked decay, the fused Adam step and mask-flip statistics (optim.py:51-192 of the reference)."""
 
 from __future__ import annotations
 
@@ -51,3 +51,92 @@ def masked_decay_gradient(g: torch.Tensor, w: torch.Tensor, m, lambda_w: float) 
     if not (g.shape == w.shape == m.shape):
         raise ShapeError("gradient, weights and mask must have equal shapes")
     return g.to(torch.float32) + lambda_w * ((1 - m.to(torch.float32)) * w.to(torch.float32))
+
+
+# ---------------------------------------------------------------------------
+# optimizer step and mask statistics, one fused kernel each
+
+
+@dataclass
+class OptimizerState:
+    """Adam state of one parameter (optim.py:64-86), device tensors.  w, u, v share a
+    dtype: float64 reproduces the reference bit for bit, float32 is the fp32-master-weight
+    training path."""
+
+    w: torch.Tensor
+    u: torch.Tensor
+    v: torch.Tensor
+    t: int = 0
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+    @classmethod
+    def init(cls, w: torch.Tensor, lr: float = 1e-3, beta1: float = 0.9, beta2: float = 0.999,
+             eps: float = 1e-8, dtype: torch.dtype | None = None) -> "OptimizerState":
+        w = w.detach().to(dtype or (w.dtype if w.dtype in (torch.float32, torch.float64) else torch.float32))
+        w = w.contiguous().clone()
+        return cls(w=w, u=torch.zeros_like(w), v=torch.zeros_like(w), t=0, lr=lr, beta1=beta1, beta2=beta2,
+                   eps=eps)
+
+
+_DECAY_CODE = {DecayMode.NONE: 0, DecayMode.ON_GRADIENTS: 1, DecayMode.ON_WEIGHTS: 2}
+
+
+def adam_step(state: OptimizerState, g: torch.Tensor, mask: TransposableMask | None = None,
+              decay: DecayConfig | None = None) -> OptimizerState:
+    """One Adam update in place (optim.py:128-147), fused with the masked decay of the
+    training loop when `decay` asks for it (trainer.py:438-447): ON_GRADIENTS adds
+    lambda_w (1 - m) w to g first (masked_decay_gradient, optim.py:105-114), ON_WEIGHTS
+    subtracts lr lambda_w (1 - m) w_before after the step (srste_weight_decay,
+    optim.py:117-125).  One HBM pass over w, g, u, v (s24_adam_step)."""
+    C.require_cuda(state.w, state.u, state.v, g)
+    if tuple(g.shape) != tuple(state.w.shape):
+        raise ShapeError("gradient shape differs from weights")
+    mode = decay.mode if (decay is not None and decay.lambda_w > 0) else DecayMode.NONE
+    if mode is not DecayMode.NONE and mask is None:
+        raise ValueError("masked decay needs the weight's TransposableMask")
+    if mask is not None and mask.shape != tuple(state.w.shape):
+        raise ShapeError("mask shape differs from weights")
+    for t_ in (state.w, state.u, state.v):
+        if not t_.is_contiguous() or t_.dtype != state.w.dtype:
+            raise ValueError("w, u, v must be contiguous tensors of one dtype")
+    g = g.contiguous()
+    if g.dtype not in (torch.float32, state.w.dtype):
+        g = g.to(state.w.dtype)
+    state.t += 1
+    t = state.t
+    lam = decay.lambda_w if mode is not DecayMode.NONE else 0.0
+    rows, cols = (state.w.shape if state.w.dim() == 2 else (1, state.w.numel()))
+    # the scalars exactly as the reference's Python evaluates them
+    C.call("s24_adam_step", state.w.data_ptr(), state.u.data_ptr(), state.v.data_ptr(), C.dtype_code(state.w),
+           g.data_ptr(), C.dtype_code(g), rows, cols, mask.idx.data_ptr() if mode is not DecayMode.NONE else None,
+           state.lr, state.beta1, state.beta2, state.eps, 1.0 - state.beta1, 1.0 - state.beta2,
+           1.0 - state.beta1 ** t, 1.0 - state.beta2 ** t, lam, state.lr * lam, _DECAY_CODE[mode],
+           C.stream_of(state.w))
+    return state
+
+
+def mask_flips(m_prev: TransposableMask, m_curr: TransposableMask,
+               block_flips: torch.Tensor | None = None) -> torch.Tensor:
+    """Number of mask bits that differ between two transposable masks (device int64
+    scalar); adds each 4x4 block's count to `block_flips` (int32, rows/4 x cols/4) when
+    given -- the cumulative per-block flips of block_flip_stats (optim.py:164-192)."""
+    if m_prev.shape != m_curr.shape:
+        raise ShapeError(f"mask shapes differ: {m_prev.shape} vs {m_curr.shape}")
+    C.require_cuda(m_prev.idx, m_curr.idx)
+    out = torch.zeros(1, dtype=torch.int64, device=m_prev.idx.device)
+    if block_flips is not None and (block_flips.dtype != torch.int32 or block_flips.numel() != m_prev.idx.numel()):
+        raise ShapeError("block_flips must be int32 with one entry per 4x4 block")
+    C.call("s24_mask_flips", m_prev.idx.data_ptr(), m_curr.idx.data_ptr(), m_prev.idx.numel(), out.data_ptr(),
+           C.ptr(block_flips), C.stream_of(out))
+    return out[0]
+
+
+def flip_rate(m_prev: TransposableMask, m_curr: TransposableMask, d: int | None = None) -> float:
+    """Fraction of mask bits that changed, ||m_curr - m_prev||_1 / d (optim.py:94-102)."""
+    n = mask_flips(m_prev, m_curr)
+    if d is None:
+        d = m_prev.shape[0] * m_prev.shape[1]
+    return float(n.item()) / d

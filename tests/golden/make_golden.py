@@ -216,6 +216,42 @@ def main():
     print("wrote", os.listdir(HERE))
 
 
+def optim_golden():
+    """Adam + masked decay in both decay modes (trainer.py:438-447 with the reference's
+    optim.adam_step / masked_decay_gradient / srste_weight_decay) and refresh flip
+    statistics (flip_rate, block_flip_stats) -> optim_golden.npz."""
+    s24 = import_reference()
+    from sparse24.optim import (OptimizerState, adam_step, block_flip_stats, flip_rate, masked_decay_gradient,
+                                srste_weight_decay)
+
+    out = {}
+    w0 = o.det_normal((64, 96), 700) * 0.05
+    m = s24.transposable_search_conv(w0).bits
+    grads = [o.det_normal((64, 96), 710 + t) * 2.0 ** -7 for t in range(3)]
+    out["w0"], out["mask"] = w0, m
+    for t, g in enumerate(grads):
+        out[f"g{t}"] = g
+    for mode, lam in (("none", 0.0), ("on_gradients", 6e-2), ("on_weights", 6e-2)):
+        st = OptimizerState.init(w0.copy(), lr=3e-3)
+        for g in grads:
+            gg = masked_decay_gradient(g, st.w, m, lam) if mode == "on_gradients" else g
+            w_before = st.w.copy()
+            adam_step(st, gg)
+            if mode == "on_weights":
+                st.w[:] = srste_weight_decay(st.w, w_before, m, st.lr, lam)
+        out[f"{mode}.w"], out[f"{mode}.u"], out[f"{mode}.v"] = st.w, st.u, st.v
+        out[f"{mode}.lam"] = np.array(lam)
+    # refresh statistics between two weight snapshots
+    wa = o.det_normal((128, 64), 720)
+    wb = wa + o.det_normal((128, 64), 721) * 0.3
+    ma, mb = s24.transposable_search_conv(wa).bits, s24.transposable_search_conv(wb).bits
+    out["flip.wa"], out["flip.wb"] = wa, wb
+    out["flip.rate"] = np.array(flip_rate(ma, mb))
+    out["flip.block_flips"] = block_flip_stats([wa, wb]).block_flips
+    np.savez_compressed(os.path.join(HERE, "optim_golden.npz"), **out)
+    print("optim golden:", {k: v.shape for k, v in out.items() if hasattr(v, "shape")})
+
+
 def mvue_cases():
     return [((16, 64), 0), ((32, 128), 7), ((8, 256), 2 ** 40 + 3), ((128, 64), (12345 << 2) ^ 2)]
 
@@ -229,4 +265,8 @@ def mvue_input(shape, i):
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["optim"]:
+        optim_golden()
+    else:
+        main()
+        optim_golden()

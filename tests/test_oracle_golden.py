@@ -150,3 +150,25 @@ def test_fst_backward_mvue_matches_reference(act, fst_golden):
         b = o.fst_backward_mvue(layer, f, c["dy"], fg["mask_in"], fg["mask_out"], rng_seed=seed)
         np.testing.assert_allclose(b["dw_in"], g[f"fst_{act}_{seed}.dw_in"], rtol=1e-12, atol=1e-13)
         np.testing.assert_allclose(b["dw2"], g[f"fst_{act}_{seed}.dw2"], rtol=1e-12, atol=1e-13)
+
+
+def _optim_golden():
+    return dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "optim_golden.npz")))
+
+
+@pytest.mark.parametrize("mode", ["none", "on_gradients", "on_weights"])
+def test_train_update_matches_reference_bit_exact(mode):
+    """oracle Adam + masked decay (optim.py:105-147, trainer.py:438-447) == the reference, bitwise."""
+    gd = _optim_golden()
+    w, u, v = gd["w0"], np.zeros_like(gd["w0"]), np.zeros_like(gd["w0"])
+    for t in range(3):
+        w, u, v = o.train_update(w, u, v, t + 1, gd[f"g{t}"], gd["mask"], float(gd[f"{mode}.lam"]), mode, lr=3e-3)
+    for k, a in (("w", w), ("u", u), ("v", v)):
+        assert np.array_equal(a.view(np.uint64), gd[f"{mode}.{k}"].view(np.uint64)), k
+
+
+def test_flip_statistics_match_reference():
+    gd = _optim_golden()
+    ma, mb = o.transposable_search_conv(gd["flip.wa"]), o.transposable_search_conv(gd["flip.wb"])
+    assert o.flip_rate(ma, mb) == float(gd["flip.rate"])
+    assert np.array_equal(o.block_flips(ma, mb), gd["flip.block_flips"])
