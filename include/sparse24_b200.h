@@ -198,6 +198,20 @@ int s24_act_fwd(const uint16_t* z, int64_t ldz, int64_t r, int64_t n, int act, u
 int s24_act_bwd(const uint16_t* z, int64_t ldz, const uint16_t* da, int64_t ldda, int64_t r, int64_t n, int act,
                 uint16_t* dz, int64_t lddz, float* dbias, void* stream);
 
+/* ---- comparators ----------------------------------
+ * Greedy 2-approximate transposable search (transposable_search_greedy, sparsity.py:
+ * 229-238; kernels.greedy_masks, _core.pyx:139-219), bit-exact, emitted as pattern
+ * indices like s24_transposable_search; blocks the greedy scan cannot complete get
+ * idx 255 and are counted into *failures (device int32, caller zeroes; the reference
+ * raises RuntimeError).  rows, cols % 4 == 0. */
+int s24_greedy_search(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* idx, int32_t* failures,
+                      void* stream);
+/* Directional 2:4 pruning (prune_2of4, sparsity.py:274-279; kernels.prune_2of4_keep,
+ * _core.pyx:113-136): bits (uint8 rows x cols) keeps the two largest |w| of each aligned
+ * group of four consecutive columns (colwise = 0) or rows (colwise = 1); ties keep the
+ * lowest indices.  Bit-exact. */
+int s24_prune_2of4(const void* w, int dtype, int64_t rows, int64_t cols, int colwise, uint8_t* bits, void* stream);
+
 /* ---- optimizer step -----------------------------
  * One fused pass per parameter: masked decay on the gradient (decay_mode
  * S24_DECAY_ON_GRADIENTS: g + lambda_w (1 - M) W, optim.py:105-114), Adam

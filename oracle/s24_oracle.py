@@ -395,6 +395,66 @@ def flip_rate(m_prev, m_curr) -> float:  # optim.py:94-102
     return float(np.abs(b - a).sum()) / a.size
 
 
+def greedy_masks(absblocks: np.ndarray) -> np.ndarray:
+    """kernels.greedy_masks (_core.pyx:139-219) restated: (nb, 16) |w| -> (nb, 16) 0/1 masks.
+    Scan cells by descending magnitude (lowest flat index on ties: a stable sort), pick while
+    the block row and column hold < 2 picks; a 7-pick block takes the single swap with the
+    largest (a[rdef,c2] + a[r2,cdef]) - a[r2,c2] (first best on ties)."""
+    a_all = np.asarray(absblocks, dtype=np.float64)
+    out = np.zeros(a_all.shape, dtype=np.uint8)
+    for bi, a in enumerate(a_all):
+        order = np.argsort(-a, kind="stable")
+        rowc, colc, picked = [0] * 4, [0] * 4, np.zeros(16, dtype=np.uint8)
+        for idx in order:
+            r, c = idx >> 2, idx & 3
+            if rowc[r] < 2 and colc[c] < 2:
+                picked[idx] = 1
+                rowc[r] += 1
+                colc[c] += 1
+        if picked.sum() == 7:
+            rdef = max(i for i in range(4) if rowc[i] < 2)
+            cdef = max(i for i in range(4) if colc[i] < 2)
+            best = None
+            for r2 in range(4):
+                for c2 in range(4):
+                    if r2 == rdef or c2 == cdef or not picked[r2 * 4 + c2]:
+                        continue
+                    gain = (a[rdef * 4 + c2] + a[r2 * 4 + cdef]) - a[r2 * 4 + c2]
+                    if best is None or gain > best[0]:
+                        best = (gain, r2, c2)
+            _, br, bc = best
+            picked[br * 4 + bc] = 0
+            picked[rdef * 4 + bc] = 1
+            picked[br * 4 + cdef] = 1
+        if picked.sum() != 8:
+            raise RuntimeError("greedy mask completion failed")
+        out[bi] = picked
+    return out
+
+
+def transposable_search_greedy(w: np.ndarray) -> np.ndarray:  # sparsity.py:229-238
+    arr = np.asarray(w, dtype=np.float64)
+    return unblocks16(greedy_masks(np.abs(blocks16(arr))), arr.shape)
+
+
+def prune_2of4_bits(w: np.ndarray, colwise: bool = False) -> np.ndarray:
+    """prune_2of4 (sparsity.py:274-279; kernels.prune_2of4_keep _core.pyx:113-136): keep the
+    two largest |w| per group of four consecutive columns (or rows); first max wins ties."""
+    a = np.abs(np.asarray(w, dtype=np.float64))
+    if colwise:
+        a = a.T
+    g = a.reshape(-1, 4)
+    i1 = np.argmax(g, axis=1)  # first maximum
+    g2 = g.copy()
+    g2[np.arange(len(g)), i1] = -np.inf
+    i2 = np.argmax(g2, axis=1)
+    keep = np.zeros(g.shape, dtype=np.uint8)
+    keep[np.arange(len(g)), i1] = 1
+    keep[np.arange(len(g)), i2] = 1
+    keep = keep.reshape(a.shape)
+    return np.ascontiguousarray(keep.T) if colwise else keep
+
+
 def adam_step(w, u, v, t: int, g, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
     """optim.py:128-147 restated in float64 with the reference's evaluation order; returns
     new (w, u, v) for step number t (1-based, already incremented)."""

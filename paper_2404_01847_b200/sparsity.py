@@ -151,3 +151,52 @@ def transposable_search_conv(w: torch.Tensor, table: PatternTable | None = None)
     idx = torch.empty((rows // 4, cols // 4), dtype=torch.uint8, device=w.device)
     C.call("s24_transposable_search", w.data_ptr(), C.dtype_code(w), rows, cols, idx.data_ptr(), C.stream_of(w))
     return TransposableMask(idx, (rows, cols))
+
+
+def transposable_search_greedy(w: torch.Tensor) -> TransposableMask:
+    """2-approximation comparator (sparsity.py:229-238 -> kernels.greedy_masks, _core.pyx:139-219)
+    on the GPU, bit-exact: per block, cells by descending |w| (lowest flat index on ties) are
+    picked while their block row and column hold fewer than two picks, and a stranded block
+    is completed by the single best swap.  Raises RuntimeError when a block cannot be
+    completed, like the reference."""
+    if w.dim() != 2:
+        raise ShapeError(f"expected a 2-D operand, got ndim={w.dim()}")
+    C.require_cuda(w)
+    rows, cols = w.shape
+    _check_blocks(rows, cols)
+    w = w.contiguous()
+    idx = torch.empty((rows // 4, cols // 4), dtype=torch.uint8, device=w.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=w.device)
+    C.call("s24_greedy_search", w.data_ptr(), C.dtype_code(w), rows, cols, idx.data_ptr(), bad.data_ptr(),
+           C.stream_of(w))
+    if int(bad.item()):
+        raise RuntimeError("greedy mask completion failed")
+    return TransposableMask(idx, (rows, cols))
+
+
+@dataclass
+class SparseEstimate:
+    """A 2:4-pruned matrix: the kept values in place (zeros elsewhere) and its 0/1 mask with
+    the group direction (the reference's SparseEstimate / Mask24, sparsity.py:82-108)."""
+
+    values: torch.Tensor
+    bits: torch.Tensor
+    direction: "Direction"
+
+
+def prune_2of4(m: torch.Tensor, direction=None) -> SparseEstimate:
+    """Keep the two largest |m| of every aligned group of four along `direction`
+    (sparsity.py:274-279 -> kernels.prune_2of4_keep, _core.pyx:113-136); ties keep the
+    lowest indices.  Bit-exact on the GPU."""
+    from .matrix import Direction
+
+    direction = direction or Direction.ROW_WISE
+    if m.dim() != 2:
+        raise ShapeError(f"expected a 2-D operand, got ndim={m.dim()}")
+    C.require_cuda(m)
+    rows, cols = m.shape
+    m = m.contiguous()
+    bits = torch.empty((rows, cols), dtype=torch.uint8, device=m.device)
+    C.call("s24_prune_2of4", m.data_ptr(), C.dtype_code(m), rows, cols, int(direction is Direction.COL_WISE),
+           bits.data_ptr(), C.stream_of(m))
+    return SparseEstimate(m * bits.to(m.dtype), bits, direction)

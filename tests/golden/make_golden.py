@@ -252,6 +252,29 @@ def optim_golden():
     print("optim golden:", {k: v.shape for k, v in out.items() if hasattr(v, "shape")})
 
 
+def comparator_golden():
+    """Greedy transposable search and directional prune_2of4 of the reference (kernels
+    greedy_masks / prune_2of4_keep) on the small mask corpora -> comparators_golden.npz."""
+    s24 = import_reference()
+    from sparse24.matrix import Direction
+    from sparse24.sparsity import _blocks_16, prune_2of4, transposable_search_greedy
+
+    table = s24.enumerate_patterns()
+    out = {}
+    for name, (w, tag) in mask_corpora().items():
+        if name in ("c1_w1_f32", "c2_w1_bf16"):
+            continue  # large corpora: the search goldens cover them
+        g = transposable_search_greedy(w).bits
+        blocks = _blocks_16(g).reshape(-1, 16)
+        r, c = w.shape
+        out[f"{name}.greedy_idx"] = np.array([table.index_of(b.reshape(4, 4)) for b in blocks],
+                                             dtype=np.uint8).reshape(r // 4, c // 4)
+        out[f"{name}.prune_row"] = prune_2of4(w, Direction.ROW_WISE).mask.bits.astype(np.uint8)
+        out[f"{name}.prune_col"] = prune_2of4(w, Direction.COL_WISE).mask.bits.astype(np.uint8)
+    np.savez_compressed(os.path.join(HERE, "comparators_golden.npz"), **out)
+    print("comparator golden:", sorted(out))
+
+
 def mvue_cases():
     return [((16, 64), 0), ((32, 128), 7), ((8, 256), 2 ** 40 + 3), ((128, 64), (12345 << 2) ^ 2)]
 
@@ -267,6 +290,9 @@ def mvue_input(shape, i):
 if __name__ == "__main__":
     if sys.argv[1:] == ["optim"]:
         optim_golden()
+    elif sys.argv[1:] == ["comparators"]:
+        comparator_golden()
     else:
         main()
         optim_golden()
+        comparator_golden()

@@ -172,3 +172,16 @@ def test_flip_statistics_match_reference():
     ma, mb = o.transposable_search_conv(gd["flip.wa"]), o.transposable_search_conv(gd["flip.wb"])
     assert o.flip_rate(ma, mb) == float(gd["flip.rate"])
     assert np.array_equal(o.block_flips(ma, mb), gd["flip.block_flips"])
+
+
+@pytest.mark.parametrize("name", ["gauss_bf16", "int_ties", "kats"])
+def test_greedy_and_prune2of4_oracle_match_reference(name):
+    """oracle greedy search / prune_2of4 (_core.pyx:113-219) == the reference on the tie-heavy corpora."""
+    gd = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "comparators_golden.npz")))
+    w, _ = mask_corpora()[name]
+    bits = o.transposable_search_greedy(w)
+    o.validate_transposable(bits)
+    pats, _ = o.pattern_table()
+    assert np.array_equal(o.idx_to_bits(gd[f"{name}.greedy_idx"]), bits)
+    assert np.array_equal(o.prune_2of4_bits(w), gd[f"{name}.prune_row"])
+    assert np.array_equal(o.prune_2of4_bits(w, colwise=True), gd[f"{name}.prune_col"])
