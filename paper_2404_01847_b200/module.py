@@ -40,7 +40,8 @@ class _SparseFFNFn(torch.autograd.Function):
         w_in, w2 = ctx.saved_tensors
         mod = ctx.mod
         g = E.ffn_backward(ctx.st, dy.to(torch.bfloat16), mod.op_in, mod.op_out, mod.act, w_in_dense=w_in,
-                           w2_dense=w2, lam=mod.decay_lambda)
+                           w2_dense=w2, lam=mod.decay_lambda, mvue=mod.mvue, rng_seed=mod.mvue_seed,
+                           mvue_exact=mod.mvue_exact)
         ctx.st = None
         return g.dx, g.dw_in, g.dbias_in, g.dw2, None
 
@@ -62,6 +63,11 @@ class SparseFFN(torch.nn.Module):
         self.op_out = E.CompressedOperand.empty(d, d_ff, dev)
         self.steps_since_refresh = None  # None -> search on first use
         self.mask_searches = 0
+        # MVUE-sparsified weight gradients (fst_backward(mvue=True), gated_ffn.py:304-373): the
+        # caller sets the per-step layer seed (trainer.py:245-247) before backward
+        self.mvue = False
+        self.mvue_seed = 0
+        self.mvue_exact = True
 
     @classmethod
     def from_weights(cls, w_in, bias_in, w2, act, refresh_period=40, decay_lambda=0.0) -> "SparseFFN":

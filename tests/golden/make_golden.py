@@ -275,6 +275,37 @@ def comparator_golden():
     print("comparator golden:", sorted(out))
 
 
+TRAIN_CASES = {
+    # name -> reference TrainConfig kwargs (tensor-core friendly dims: d, d_ff % 128, batch % 64)
+    "geglu_ongrad": dict(d=128, d_ff=256, depth=2, batch=128, steps=36, lr=1e-2, mvue=False,
+                         decay=dict(lambda_w=2e-4, mode="on_gradients", refresh_period=8)),
+    "geglu_mvue_onweights": dict(d=128, d_ff=256, depth=2, batch=128, steps=36, lr=1e-2, mvue=True,
+                                 decay=dict(lambda_w=2e-4, mode="on_weights", refresh_period=8)),
+}
+
+
+def train_golden():
+    """Loss / flip-rate curves of the reference's run_training (trainer.py:387-480) ->
+    train_golden.npz; the GPU trainer runs the same configs on the same data."""
+    import_reference()
+    from sparse24.optim import DecayConfig, DecayMode
+    from sparse24.trainer import TrainConfig, run_training
+
+    out = {}
+    for name, kw in TRAIN_CASES.items():
+        kw = dict(kw)
+        dec = kw.pop("decay")
+        cfg = TrainConfig(**kw, decay=DecayConfig(lambda_w=dec["lambda_w"], mode=DecayMode(dec["mode"]),
+                                                  refresh_period=dec["refresh_period"]))
+        art = run_training(cfg)
+        out[f"{name}.losses"] = art.losses
+        out[f"{name}.flips"] = art.flips
+        out[f"{name}.eval"] = np.array(art.final_eval_loss)
+        out[f"{name}.searches"] = np.array(art.mask_search_calls)
+        print(name, art.losses[:3], art.losses[-3:], art.final_eval_loss)
+    np.savez_compressed(os.path.join(HERE, "train_golden.npz"), **out)
+
+
 def mvue_cases():
     return [((16, 64), 0), ((32, 128), 7), ((8, 256), 2 ** 40 + 3), ((128, 64), (12345 << 2) ^ 2)]
 
@@ -292,7 +323,10 @@ if __name__ == "__main__":
         optim_golden()
     elif sys.argv[1:] == ["comparators"]:
         comparator_golden()
+    elif sys.argv[1:] == ["train"]:
+        train_golden()
     else:
         main()
         optim_golden()
         comparator_golden()
+        train_golden()
