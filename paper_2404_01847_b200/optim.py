@@ -140,3 +140,56 @@ def flip_rate(m_prev: TransposableMask, m_curr: TransposableMask, d: int | None 
     if d is None:
         d = m_prev.shape[0] * m_prev.shape[1]
     return float(n.item()) / d
+
+
+# ---------------------------------------------------------------------------
+# decay factor determination (optim.py:195-259): host control logic over GPU warm-up runs
+
+FEASIBLE_MU_BAND = (0.60, 0.95)  # optim.py:38
+DEFAULT_LAMBDA_GRID = (1e-6, 2e-6, 6e-6, 2e-5, 6e-5, 2e-4, 6e-4, 2e-3)  # optim.py:42
+
+
+@dataclass
+class SearchEntry:
+    lambda_w: float
+    mu: float
+    feasible: bool
+    accuracy_risk: bool  # mu >= 1: flips not inhibited below the dense rate
+
+
+@dataclass
+class SearchResult:
+    chosen: float | None
+    entries: list
+    dense_reference: float
+
+    def to_csv(self) -> str:
+        lines = ["lambda,mu,feasible"]
+        for e in self.entries:
+            lines.append(f"{e.lambda_w:g},{e.mu:.6g},{str(e.feasible).lower()}")
+        return "\n".join(lines) + "\n"
+
+
+def decay_factor_search(candidates, warmup_steps: int, run_warmup, window_fraction: float = 0.10) -> SearchResult:
+    """optim.py:220-259: mu = (mean sparse flip rate) / (mean dense-proxy flip rate) over the
+    trailing window of the warm-up; the largest candidate inside FEASIBLE_MU_BAND wins.
+    `run_warmup` is trainer.make_warmup_runner (GPU warm-up runs)."""
+    import numpy as np
+
+    if not candidates:
+        raise ValueError("candidate list is empty")
+    if warmup_steps < 1:
+        raise ValueError("warmup_steps must be >= 1")
+    window = max(1, int(round(window_fraction * warmup_steps)))
+    dense_trace = np.asarray(run_warmup(None), dtype=np.float64)
+    dense_ref = float(dense_trace[-window:].mean())
+    entries = []
+    lo, hi = FEASIBLE_MU_BAND
+    for lam in candidates:
+        trace = np.asarray(run_warmup(float(lam)), dtype=np.float64)
+        sparse_rate = float(trace[-window:].mean())
+        mu = sparse_rate / dense_ref if dense_ref > 0 else float("inf")
+        entries.append(SearchEntry(lambda_w=float(lam), mu=mu, feasible=bool(lo <= mu <= hi),
+                                   accuracy_risk=bool(mu >= 1.0)))
+    feasible = [e.lambda_w for e in entries if e.feasible]
+    return SearchResult(chosen=max(feasible) if feasible else None, entries=entries, dense_reference=dense_ref)

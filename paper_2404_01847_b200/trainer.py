@@ -76,6 +76,7 @@ class TrainConfig:
     sparse: bool = True
     decay: DecayConfig = field(default_factory=DecayConfig)
     mvue: bool = True
+    proxy_flips: bool = False  # per-step mask search on the current weights (dense-run proxy)
     eval_batches: int = 8
     n_classes: int = 4
     schedule_total_steps: int | None = None
@@ -268,10 +269,25 @@ class FFNStack(torch.nn.Module):
 class RunArtifacts:
     config: TrainConfig
     losses: np.ndarray  # length T
-    flips: np.ndarray  # length T; refresh steps carry the flip rate
+    flips: np.ndarray  # length T; refresh steps carry the flip rate (the proxy rates of a dense proxy run)
     final_params: list[dict]
     final_eval_loss: float
     mask_search_calls: int
+    proxy_rates: np.ndarray | None = None
+
+
+def _proxy_masks(stack: "FFNStack") -> list[TransposableMask]:
+    from .sparsity import transposable_search_conv
+
+    out = []
+    for layer in stack.layers:
+        out.append(transposable_search_conv(layer.w_in.detach()))
+        out.append(transposable_search_conv(layer.w2.detach()))
+    return out
+
+
+def _flips_between(a: list[TransposableMask], b: list[TransposableMask], size: int) -> float:
+    return float(sum(mask_flips(x, y) for x, y in zip(a, b))) / size
 
 
 def lr_at(t: int, total: int, peak: float, warmup_fraction: float, floor_fraction: float) -> float:
@@ -308,7 +324,11 @@ def run_training(cfg: TrainConfig, device="cuda") -> RunArtifacts:
     searches = 0
     have_masks = False
     since_refresh = 0
-    prev_idx = None
+    proxy = np.zeros(T) if cfg.proxy_flips else None
+    prev_proxy = None
+    if proxy is not None:
+        prev_proxy = _proxy_masks(stack)
+        searches += 2 * cfg.depth
 
     for t in range(1, T + 1):
         lr = lr_at(t, sched_total, cfg.lr, cfg.warmup_fraction, cfg.lr_floor_fraction)
@@ -353,6 +373,11 @@ def run_training(cfg: TrainConfig, device="cuda") -> RunArtifacts:
             m = masks.get(id(p))
             adam_step(st, p.grad, m, DecayConfig(lambda_w=lam, mode=DecayMode.ON_WEIGHTS) if m is not None else None)
         since_refresh += 1
+        if proxy is not None:
+            pm = _proxy_masks(stack)
+            searches += 2 * cfg.depth
+            proxy[t - 1] = _flips_between(prev_proxy, pm, stack.size)
+            prev_proxy = pm
 
     final_sparse = cfg.sparse and t_pre < T <= t_switch
     stack.set_sparse(final_sparse)
@@ -367,4 +392,24 @@ def run_training(cfg: TrainConfig, device="cuda") -> RunArtifacts:
             ev.append(float(task.loss_and_grad(oe, te.float() if te.is_floating_point() else te)[0]))
     final = [{k: getattr(layer, n).detach().double().cpu().numpy() for k, n in
               (("w_in", "w_in"), ("bias", "bias_in"), ("w2", "w2"))} for layer in stack.layers]
-    return RunArtifacts(cfg, losses.cpu().numpy().astype(np.float64), flips, final, float(np.mean(ev)), searches)
+    rates = proxy if (not cfg.sparse and proxy is not None) else flips
+    return RunArtifacts(cfg, losses.cpu().numpy().astype(np.float64), rates, final, float(np.mean(ev)), searches,
+                        proxy)
+
+
+def make_warmup_runner(base_cfg: TrainConfig, warmup_steps: int, refresh_period: int = 1):
+    """Warm-up handle of the decay-factor search (trainer.py:570-598): None runs the dense
+    proxy (per-step flip instrumentation on a dense run), a float the sparse run with that
+    ON_GRADIENTS decay factor, refreshing masks every `refresh_period` steps."""
+
+    def runner(lam):
+        common = dict(steps=warmup_steps, schedule_total_steps=base_cfg.steps, dense_ft_fraction=0.0,
+                      dense_pretrain_fraction=0.0)
+        if lam is None:
+            cfg = dataclasses.replace(base_cfg, sparse=False, proxy_flips=True, **common)
+        else:
+            cfg = dataclasses.replace(base_cfg, sparse=True, proxy_flips=False,
+                                      decay=DecayConfig(lam, DecayMode.ON_GRADIENTS, refresh_period), **common)
+        return run_training(cfg).flips
+
+    return runner

@@ -284,6 +284,10 @@ TRAIN_CASES = {
 }
 
 
+SEARCH_GRID = (2e-5, 2e-4, 2e-3, 2e-2)
+SEARCH_WARMUP = 20
+
+
 def train_golden():
     """Loss / flip-rate curves of the reference's run_training (trainer.py:387-480) ->
     train_golden.npz; the GPU trainer runs the same configs on the same data."""
@@ -303,6 +307,19 @@ def train_golden():
         out[f"{name}.eval"] = np.array(art.final_eval_loss)
         out[f"{name}.searches"] = np.array(art.mask_search_calls)
         print(name, art.losses[:3], art.losses[-3:], art.final_eval_loss)
+    # decay-factor search on short warm-ups (optim.py:220-259 with trainer.make_warmup_runner)
+    from sparse24.optim import decay_factor_search
+    from sparse24.trainer import make_warmup_runner
+
+    kw = dict(TRAIN_CASES["geglu_ongrad"])
+    kw.pop("decay")
+    kw["steps"] = 200
+    base = TrainConfig(**kw)
+    res = decay_factor_search(list(SEARCH_GRID), SEARCH_WARMUP, make_warmup_runner(base, SEARCH_WARMUP))
+    out["search.mu"] = np.array([e.mu for e in res.entries])
+    out["search.dense_ref"] = np.array(res.dense_reference)
+    out["search.chosen"] = np.array(np.nan if res.chosen is None else res.chosen)
+    print("search", out["search.mu"], res.chosen)
     np.savez_compressed(os.path.join(HERE, "train_golden.npz"), **out)
 
 
