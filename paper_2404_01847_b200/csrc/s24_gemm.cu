@@ -106,23 +106,28 @@ constexpr int stages_for() {
   return budget / kStageBytes > 6 ? 6 : budget / kStageBytes;
 }
 
-template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kAcc = 2>
+// kSlabs = 2 (sparse, plain-store epilogue, long K): every CTA holds TWO 128-row A slabs
+// against one B tile -- a 512 x kBN pair tile in one TMEM accumulator (2 x kBN columns), so
+// each B byte delivered from L2 feeds twice the MACs (operand bytes per MAC -30 %) at the
+// price of an epilogue that no longer overlaps the main loop (a few % at K >= 8192).
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kAcc = 2, int kSlabs = 1>
 struct Cfg {
   static constexpr int BK = kSparse ? 128 : 64;  // logical K per stage
   static constexpr int kMmaK = kSparse ? 32 : 16;
   static constexpr int kMmasPerStage = BK / kMmaK;  // 4
   static constexpr int BN_CTA = kBN / kCG;          // B rows held by one CTA
   static constexpr int B_CHUNKS = (BN_CTA + 63) / 64;  // MN-major 64-wide swizzle chunks
-  static constexpr int A_BYTES = 128 * 64 * 2;         // 16 KB either major
+  static constexpr int A_BYTES = kSlabs * 128 * 64 * 2;  // 16 KB per slab, either major
   static constexpr int B_BOX_BYTES = kBMN ? BK * 128 : BN_CTA * 128;
   static constexpr int B_BOXES = kBMN ? B_CHUNKS : BK / 64;
   static constexpr int B_BYTES = B_BOXES * B_BOX_BYTES;
-  static constexpr int E_BYTES = kSparse ? 2048 : 0;
+  static constexpr int E_BYTES = kSparse ? kSlabs * 2048 : 0;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + E_BYTES;
   static constexpr int TX_BYTES = A_BYTES + (kBMN ? B_BYTES : BN_CTA * BK * 2) + E_BYTES;  // per CTA
-  static constexpr int ACC_COLS = kBN;
-  static constexpr int E_COL = kAcc * kBN;  // kAcc TMEM accumulators (2: epilogue overlaps the next tile)
-  static constexpr int USED_COLS = kAcc * kBN + (kSparse ? 4 : 0);
+  static constexpr int ACC_COLS = kSlabs * kBN;
+  static constexpr int E_COL = kAcc * ACC_COLS;  // kAcc TMEM accumulators (2: epilogue overlaps the next tile)
+  static constexpr int USED_COLS = kAcc * ACC_COLS + (kSparse ? 4 * kSlabs : 0);
+  static constexpr int TILE_M = 128 * kCG * kSlabs;  // output rows per (pair) tile
   static constexpr int TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64 : USED_COLS <= 128 ? 128
                                  : USED_COLS <= 256 ? 256 : 512;
   static constexpr int EPI_OFF = kStages * STAGE_BYTES;          // per-warp 4 KB output staging
@@ -197,19 +202,21 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int 
   nb = in_group / gm;
 }
 
-template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT, int kAcc>
+template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT, int kAcc,
+          int kSlabs>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmD,
                 const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, GemmShape shp,
                 EpiParams ep) {
-  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG, kAcc>;
+  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG, kAcc, kSlabs>;
   // token-major training / plain-store epilogues run on the fragment path (tcgen05.ld 16x256b +
   // stmatrix); the masked-decay dW epilogue and the API's z / GELU(z) epilogue on the row path
   constexpr bool kFrag = kOutT && (kEpi == kEpiStore || kEpi == kEpiGeluGrad || kEpi == kEpiDAct ||
                                    kEpi == kEpiGatedGrad || kEpi == kEpiDGated);
   static_assert(kOutT || !(kEpi == kEpiGeluGrad || kEpi == kEpiDAct || kEpi == kEpiGatedGrad || kEpi == kEpiDGated),
                 "training epilogues store token-major outputs");
+  static_assert(kSlabs == 1 || (kSparse && kFrag && kEpi == kEpiStore && kAcc == 1), "slabs: plain sparse store only");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = kCG == 2 ? cluster_rank() : 0;
-  const int num_m = shp.m / (128 * kCG);
+  const int num_m = shp.m / C::TILE_M;
   const int num_n = (shp.n + kBN - 1) / kBN;
   const int num_tiles = num_m * num_n;
   const int num_kb = shp.k / C::BK;  // k-blocks per output tile
@@ -269,7 +276,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         int mb, nb;
         tile_coords(tile, num_m, num_n, shp.group_m, mb, nb);
-        const int m0 = mb * 128 * kCG + 128 * rank;      // this CTA's A rows
+        const int m0 = mb * C::TILE_M + 128 * rank;      // this CTA's A rows (slab s: + 128 kCG s)
         const int nb0 = ((shp.exp & 4) ? 0 : nb * kBN) + C::BN_CTA * rank;  // this CTA's B rows (N split)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -279,8 +286,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (rank == 0)
             mbar_expect_tx(&full_bar[stage], (C::TX_BYTES - (skip_b ? C::TX_BYTES - C::A_BYTES - C::E_BYTES : 0)) * kCG);
           if constexpr (kSparse) {
-            tma_load<kCG>(sA, &tmA, &full_bar[stage], kb * 64, m0);  // 64 physical = 128 logical
-            tma_load<kCG>(sB + C::B_BYTES, &tmE, &full_bar[stage], 0, (m0 / 128) * (shp.k / 128) + kb);
+#pragma unroll
+            for (int sl = 0; sl < kSlabs; ++sl) {
+              const int ms = m0 + 128 * kCG * sl;
+              tma_load<kCG>(sA + sl * 16384, &tmA, &full_bar[stage], kb * 64, ms);  // 64 physical = 128 logical
+              tma_load<kCG>(sB + C::B_BYTES + sl * 2048, &tmE, &full_bar[stage], 0, (ms / 128) * (shp.k / 128) + kb);
+            }
           } else if constexpr (kAMN) {
             tma_load<kCG>(sA, &tmA, &full_bar[stage], m0, kb * 64);
             tma_load<kCG>(sA + 8192, &tmA, &full_bar[stage], m0 + 64, kb * 64);
@@ -326,7 +337,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t b_addr = a_addr + C::A_BYTES;
           if (kSparse && !(shp.exp & 2)) {
             // metadata: 128 rows x 16 B (no swizzle, 8-row core matrices 128 B apart) -> 4 TMEM columns
-            tmem_cp_128x128b_cg<kCG>(tmem_base + C::E_COL, make_sdesc(b_addr + C::B_BYTES, 2048, 128, 0));
+#pragma unroll
+            for (int sl = 0; sl < kSlabs; ++sl)
+              tmem_cp_128x128b_cg<kCG>(tmem_base + C::E_COL + 4 * sl,
+                                       make_sdesc(b_addr + C::B_BYTES + sl * 2048, 2048, 128, 0));
           }
 #pragma unroll
           for (int j = 0; j < C::kMmasPerStage; ++j) {
@@ -345,10 +359,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
             const uint32_t accum = (kb != kb0 || j != 0) ? 1u : 0u;
             if constexpr (kSparse) {
-              // MMA j's metadata sits in TMEM column E_COL + j; the instruction takes a
+              // MMA j's metadata sits in TMEM column E_COL + 4 slab + j; the instruction takes a
               // 2-column-aligned address and selects the column with sparse_id2 (idesc[0:2))
-              mma_sp_bf16_cg<kCG>(d_tmem, adesc, bdesc, tmem_base + C::E_COL + (j & ~1),
-                                  C::IDESC | static_cast<uint32_t>(j & 1), accum);
+#pragma unroll
+              for (int sl = 0; sl < kSlabs; ++sl)
+                mma_sp_bf16_cg<kCG>(d_tmem + sl * kBN, adesc + static_cast<uint64_t>((sl * 16384) >> 4), bdesc,
+                                    tmem_base + C::E_COL + 4 * sl + (j & ~1), C::IDESC | static_cast<uint32_t>(j & 1),
+                                    accum);
             } else {
               mma_bf16_cg<kCG>(d_tmem, adesc, bdesc, C::IDESC, accum);
             }
@@ -387,10 +404,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (; wk.next(num_tiles, num_kb, tile, kb0, kb1); par ^= 1) {
         int mb, nb;
         tile_coords(tile, num_m, num_n, shp.group_m, mb, nb);
-        const int m_w = mb * 128 * kCG + 128 * rank + 32 * q;  // first TMEM row of this warp
         const int n_base = nb * kBN;
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
+#pragma unroll 1
+        for (int slab = 0; slab < kSlabs; ++slab) {
+        const int m_w = mb * C::TILE_M + 128 * kCG * slab + 128 * rank + 32 * q;  // first TMEM row of this warp
         float bias4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // bias of row m_w + 8j + t4 (forward)
         float bs1[4] = {0.0f, 0.0f, 0.0f, 0.0f};    // bias-gradient partials (backward), u / plain
         float bs2[4] = {0.0f, 0.0f, 0.0f, 0.0f};    // v half (kEpiDGated)
@@ -431,7 +450,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int u = 0; u < 8; ++u) cur[u] = pre[u];
           if constexpr (kPre) prefetch(cc + 2);
           uint32_t r[32];
-          const uint32_t ta = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + 32 * cc;
+          const uint32_t ta =
+              tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + slab * kBN + 32 * cc;
           tmem_ld16x256b_x4(ta, r);
           tmem_ld16x256b_x4(ta + (16u << 16), r + 16);
           tmem_ld_wait();
@@ -550,7 +570,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              uint32_t gq[4];
+              uint32_t gq[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
                 float x0 = v[16 * (j >> 1) + 4 * c + 2 * (j & 1)];
@@ -615,6 +635,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
         }
+        }  // slab
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -643,7 +664,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tile_coords(tile, num_m, num_n, shp.group_m, mb, nb);
         const bool first_chunk = kb0 == 0;                  // adds the decay exactly once
         const bool partial = kb0 != 0 || kb1 != num_kb;     // stream-K piece: add-reduce
-        const int m_w = mb * 128 * kCG + 128 * rank + 32 * q;  // first row of this warp
+        const int m_w = mb * C::TILE_M + 128 * rank + 32 * q;  // first row of this warp
         const int m = m_w + lane;
         const int n_base = nb * kBN;
         mbar_wait(&tfull_bar[acc], acc_phase);
@@ -903,6 +924,15 @@ static int wave_slot(void* stream, bool dflt) {
   return static_cast<int>((h ^ (h >> 7) ^ (h >> 17)) % kWaveSlots);
 }
 
+// Two-slab sparse tiles (Cfg kSlabs) for plain-store GEMMs with a long K, where the main loop
+// per tile dwarfs the then un-overlapped epilogue.  S24_SLABS=0 off, =1 whenever the shape
+// allows (m % 512 == 0), default K >= 8192.
+static bool use_slabs(int64_t m, int64_t k) {
+  static const int env = getenv("S24_SLABS") ? atoi(getenv("S24_SLABS")) : -1;
+  if (m % 512 != 0 || env == 0) return false;
+  return env == 1 || k >= 8192;
+}
+
 static int exp_flags() {
   static const int v = getenv("S24_EXP") ? atoi(getenv("S24_EXP")) : 0;
   return v;
@@ -917,19 +947,19 @@ static int pick_group_m(int num_m, double a_bytes_per_mtile) {
 }
 
 template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT = false,
-          int kAcc = 2>
+          int kAcc = 2, int kSlabs = 1>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& me, const CUtensorMap& md,
                        const CUtensorMap& mx, const CUtensorMap& my, const GemmShape& shp, const EpiParams& ep,
                        cudaStream_t st) {
-  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG, kAcc>;
-  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi, kOutT, kAcc>;
+  using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG, kAcc, kSlabs>;
+  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi, kOutT, kAcc, kSlabs>;
   static bool attr_done = false;  // per template instance
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_done = true;
   }
-  const int tiles = (shp.m / (128 * kCG)) * ((shp.n + kBN - 1) / kBN);
+  const int tiles = (shp.m / C::TILE_M) * ((shp.n + kBN - 1) / kBN);
   const int clusters = (shp.streamk || tiles > num_sms() / kCG) ? num_sms() / kCG : tiles;
   if (clusters <= 0) return S24_OK;
   cudaLaunchConfig_t cfg = {};
@@ -1062,6 +1092,12 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     case S24_EPI_SWIGLU_GRAD: S24_SPT(BMN, BNV, CG, kEpiGatedGrad);             \
     case S24_EPI_DGATED: S24_SPT(BMN, BNV, CG, kEpiDGated);                     \
     default: S24_SP(BMN, BNV, CG, kEpiStore);                                   \
+  }
+  if (pair && !b_mn && d_t && epilogue == S24_EPI_STORE && use_slabs(m, k)) {
+    // two A slabs per CTA, one accumulator: 512 x 224 pair tiles
+    using CS = Cfg<true, false, false, BN2, 1, 2, 1, 2>;
+    return launch_gemm<true, false, false, BN2, stages_for<CS::STAGE_BYTES>(), 2, kEpiStore, true, 1, 2>(
+        ma, mb, me, md, mx, my, shp, ep, st);
   }
   if (pair) {
     if (b_mn) S24_SP_EPI(true, BN2, 2);

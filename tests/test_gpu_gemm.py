@@ -200,3 +200,42 @@ def test_dense_dw_gemm_streamk_forced_small_shapes():
     env = dict(os.environ, S24_STREAMK="1", S24_WAVESYNC="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("m,k,n", [(512, 8192, 480), (1024, 8448, 224)])
+def test_sparse_gemm_two_slab_tiles(m, k, n):
+    """K >= 8192 plain token-major stores run on 512 x 224 two-slab pair tiles (one TMEM
+    accumulator holding both A slabs against one B tile); partial last N tile included."""
+    from paper_2404_01847_b200.engine import spmm
+
+    w, op, bits = _operand(m, k, 77 + m)
+    x = torch.randn(n, k, device="cuda").bfloat16()
+    bias = torch.randn(m, device="cuda").bfloat16()
+    out = torch.full((n, m), float("nan"), dtype=torch.bfloat16, device="cuda")
+    spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, bias, out_t=True)
+    ref = x.float() @ (w.float() * bits.float()).t() + bias.float()
+    assert torch.isfinite(out.float()).all()
+    assert normwise_rel(out.float().cpu(), ref.cpu()) < 1e-2
+
+
+def test_sparse_gemm_two_slab_forced_small_k():
+    """S24_SLABS=1 forces the two-slab tiles on short K (subprocess: the knob is read once)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from test_gpu_gemm import _operand\n"
+        "from paper_2404_01847_b200.engine import spmm\n"
+        "for m, k, n in [(512, 128, 32), (512, 1024, 448), (1536, 2048, 672)]:\n"
+        "    w, op, bits = _operand(m, k, 5 + k)\n"
+        "    x = torch.randn(n, k, device='cuda').bfloat16()\n"
+        "    out = torch.full((n, m), float('nan'), dtype=torch.bfloat16, device='cuda')\n"
+        "    spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, out_t=True)\n"
+        "    ref = x.float() @ (w.float() * bits.float()).t()\n"
+        "    e = float((out.float() - ref).norm() / ref.norm())\n"
+        "    assert e < 1e-2, (m, k, n, e)\n"
+        "print('ok')\n" % (os.path.abspath(os.path.join(os.path.dirname(__file__), "..")), os.path.dirname(__file__)))
+    env = dict(os.environ, S24_SLABS="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
