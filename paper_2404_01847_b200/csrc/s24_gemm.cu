@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                    kEpi == kEpiGatedGrad || kEpi == kEpiDGated);
   static_assert(kOutT || !(kEpi == kEpiGeluGrad || kEpi == kEpiDAct || kEpi == kEpiGatedGrad || kEpi == kEpiDGated),
                 "training epilogues store token-major outputs");
-  static_assert(kSlabs == 1 || (kSparse && kFrag && kEpi == kEpiStore && kAcc == 1), "slabs: plain sparse store only");
+  static_assert(kSlabs == 1 || (kAcc == 1 && ((kSparse && kFrag && kEpi == kEpiStore) || (!kSparse && kEpi == kEpiDw))),
+                "slabs: plain sparse store or dense dW only");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
@@ -292,11 +293,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               tma_load<kCG>(sA + sl * 16384, &tmA, &full_bar[stage], kb * 64, ms);  // 64 physical = 128 logical
               tma_load<kCG>(sB + C::B_BYTES + sl * 2048, &tmE, &full_bar[stage], 0, (ms / 128) * (shp.k / 128) + kb);
             }
-          } else if constexpr (kAMN) {
-            tma_load<kCG>(sA, &tmA, &full_bar[stage], m0, kb * 64);
-            tma_load<kCG>(sA + 8192, &tmA, &full_bar[stage], m0 + 64, kb * 64);
           } else {
-            tma_load<kCG>(sA, &tmA, &full_bar[stage], kb * 64, m0);
+#pragma unroll
+            for (int sl = 0; sl < kSlabs; ++sl) {
+              const int ms = m0 + 128 * kCG * sl;
+              if constexpr (kAMN) {
+                tma_load<kCG>(sA + sl * 16384, &tmA, &full_bar[stage], ms, kb * 64);
+                tma_load<kCG>(sA + sl * 16384 + 8192, &tmA, &full_bar[stage], ms + 64, kb * 64);
+              } else {
+                tma_load<kCG>(sA + sl * 16384, &tmA, &full_bar[stage], kb * 64, ms);
+              }
+            }
           }
           if (skip_b) {
           } else if constexpr (kBMN) {
@@ -367,7 +374,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                     tmem_base + C::E_COL + 4 * sl + (j & ~1), C::IDESC | static_cast<uint32_t>(j & 1),
                                     accum);
             } else {
-              mma_bf16_cg<kCG>(d_tmem, adesc, bdesc, C::IDESC, accum);
+#pragma unroll
+              for (int sl = 0; sl < kSlabs; ++sl)
+                mma_bf16_cg<kCG>(d_tmem + sl * kBN, adesc + static_cast<uint64_t>((sl * 16384) >> 4), bdesc, C::IDESC,
+                                 accum);
             }
           }
           mma_commit_cg<kCG>(&empty_bar[stage]);
@@ -664,11 +674,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tile_coords(tile, num_m, num_n, shp.group_m, mb, nb);
         const bool first_chunk = kb0 == 0;                  // adds the decay exactly once
         const bool partial = kb0 != 0 || kb1 != num_kb;     // stream-K piece: add-reduce
-        const int m_w = mb * C::TILE_M + 128 * rank + 32 * q;  // first row of this warp
-        const int m = m_w + lane;
         const int n_base = nb * kBN;
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
+#pragma unroll 1
+        for (int slab = 0; slab < kSlabs; ++slab) {
+        const int m_w = mb * C::TILE_M + 128 * kCG * slab + 128 * rank + 32 * q;  // first row of this warp
+        const int m = m_w + lane;
         float bias_v = 0.0f;
         if constexpr (kEpi == kEpiStore || kEpi == kEpiGeluAux) {
           if (ep.bias != nullptr) bias_v = bf16_to_f32(ep.bias[m]);
@@ -706,7 +718,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int u = 0; u < 8; ++u) cur[u] = pre[u];
           if (kPre && !(shp.exp & 32)) prefetch(cc + 2);
           uint32_t r[32];
-          tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + 32 * cc, r);
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + slab * kBN + 32 * cc, r);
           tmem_ld_wait();
           const int n0 = n_base + 32 * cc;
           if (n0 >= shp.n) continue;
@@ -809,6 +821,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             sbuf ^= 1;
           }
         }
+        }  // slab
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -927,6 +940,20 @@ static int wave_slot(void* stream, bool dflt) {
 // Two-slab sparse tiles (Cfg kSlabs) for plain-store GEMMs with a long K, where the main loop
 // per tile dwarfs the then un-overlapped epilogue.  S24_SLABS=0 off, =1 whenever the shape
 // allows (m % 512 == 0), default K >= 8192.
+// Two-slab dense dW tiles (512 x 256 per CTA pair, one 512-column accumulator): -25 % operand
+// bytes per MAC, which buys clock under the power cap (measured on B200: C3 dW2 1.98 -> 1.89 ms,
+// C4 dW 12.98 -> 12.62 ms at +7..10 % SM clock) but halves the tile count and exposes the
+// epilogue, so it is used only when the wave fill does not get worse (C3 dW_in 97.9 -> 93 %:
+// 3.87 -> 3.95 ms).  S24_DW_SLABS=0/1 overrides.
+static bool use_dw_slabs(int64_t m, int64_t n, int64_t k) {
+  static const int env = getenv("S24_DW_SLABS") ? atoi(getenv("S24_DW_SLABS")) : -1;
+  if (env >= 0) return env == 1;
+  const int64_t clusters = num_sms() / 2;
+  const int64_t t1 = (m / 256) * (n / 256), t2 = (m / 512) * (n / 256);
+  auto fill = [&](int64_t t) { return static_cast<double>(t) / (((t + clusters - 1) / clusters) * clusters); };
+  return k >= 8192 && t2 >= 2 * clusters && fill(t2) >= fill(t1) - 0.01;
+}
+
 static bool use_slabs(int64_t m, int64_t k) {
   static const int env = getenv("S24_SLABS") ? atoi(getenv("S24_SLABS")) : -1;
   if (m % 512 != 0 || env == 0) return false;
@@ -1166,6 +1193,12 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
 #define S24_DW(AMN, BMN, BNV, CG)                                                                      \
   return launch_gemm<false, AMN, BMN, BNV, stages_for<Cfg<false, AMN, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
                      kEpiDw>(ma, mb, me, md, md, md, shp, ep, st)
+  if (pair && a_mn && b_mn && m % 512 == 0 && use_dw_slabs(m, n, k)) {
+    using CS = Cfg<false, true, true, 256, 1, 2, 1, 2>;
+    shp.wave_slot = streamk ? -1 : wave_slot(stream, true);
+    return launch_gemm<false, true, true, 256, stages_for<CS::STAGE_BYTES>(), 2, kEpiDw, false, 1, 2>(
+        ma, mb, me, md, md, md, shp, ep, st);
+  }
   if (pair) {
     if (a_mn && b_mn) S24_DW(true, true, 256, 2);
     if (a_mn) S24_DW(true, false, 256, 2);

@@ -239,3 +239,34 @@ def test_sparse_gemm_two_slab_forced_small_k():
     env = dict(os.environ, S24_SLABS="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_dense_dw_two_slab_tiles_forced():
+    """S24_DW_SLABS=1: 512 x 256 two-slab dense dW tiles (MN-major operands), with the masked
+    decay and the gated row remap (subprocess: the knob is read once)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, sys; sys.path.insert(0, %r)\n"
+        "from paper_2404_01847_b200.engine import gemm_dw, CompressedOperand, search_compress\n"
+        "from paper_2404_01847_b200 import transposable_search_conv\n"
+        "for m, n, k, gff in [(512, 256, 1024, 0), (1024, 768, 4096, 0), (1024, 512, 2048, 512)]:\n"
+        "    w = torch.randn(m, n, device='cuda').bfloat16()\n"
+        "    mask = transposable_search_conv(w)\n"
+        "    a = torch.randn(k, m, device='cuda').bfloat16(); b = torch.randn(k, n, device='cuda').bfloat16()\n"
+        "    out = torch.full((m, n), float('nan'), device='cuda')\n"
+        "    if gff:\n"
+        "        p = torch.arange(m, device='cuda')\n"
+        "        orig = torch.where(p %% 32 < 16, 16 * (p // 32) + p %% 32, gff + 16 * (p // 32) + p %% 32 - 16)\n"
+        "        op = CompressedOperand.empty(m, n, 'cuda', perm_ff=gff); search_compress(w, op)\n"
+        "        gemm_dw(a[:, orig].contiguous(), True, b, True, m, n, k, out, w, op.idx, 0.5, gate_ff=gff)\n"
+        "    else:\n"
+        "        gemm_dw(a, True, b, True, m, n, k, out, w, mask.idx, 0.5)\n"
+        "    ref = a.float().t() @ b.float() + 0.5 * (1 - mask.bits.float()) * w.float()\n"
+        "    e = float((out - ref).norm() / ref.norm())\n"
+        "    assert torch.isfinite(out).all() and e < 2e-3, (m, n, k, gff, e)\n"
+        "print('ok')\n" % os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+    env = dict(os.environ, S24_DW_SLABS="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
