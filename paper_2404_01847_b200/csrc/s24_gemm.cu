@@ -937,9 +937,6 @@ static int wave_slot(void* stream, bool dflt) {
   return static_cast<int>((h ^ (h >> 7) ^ (h >> 17)) % kWaveSlots);
 }
 
-// Two-slab sparse tiles (Cfg kSlabs) for plain-store GEMMs with a long K, where the main loop
-// per tile dwarfs the then un-overlapped epilogue.  S24_SLABS=0 off, =1 whenever the shape
-// allows (m % 512 == 0), default K >= 8192.
 // Two-slab dense dW tiles (512 x 256 per CTA pair, one 512-column accumulator): -25 % operand
 // bytes per MAC, which buys clock under the power cap (measured on B200: C3 dW2 1.98 -> 1.89 ms,
 // C4 dW 12.98 -> 12.62 ms at +7..10 % SM clock) but halves the tile count and exposes the
@@ -954,10 +951,17 @@ static bool use_dw_slabs(int64_t m, int64_t n, int64_t k) {
   return k >= 8192 && t2 >= 2 * clusters && fill(t2) >= fill(t1) - 0.01;
 }
 
-static bool use_slabs(int64_t m, int64_t k) {
+// Two-slab sparse tiles (Cfg kSlabs) for plain-store GEMMs whose main loop per tile dwarfs the
+// then un-overlapped epilogue: K >= 4096 (measured on B200: C2's K = 4096 plain GEMMs -7 %,
+// C3's K = 11008 / 22016 ones -10..12 %), as long as halving the tile count does not leave a
+// wave worse filled.  S24_SLABS=0 off, =1 whenever the shape allows (m % 512 == 0).
+static bool use_slabs(int64_t m, int64_t n, int64_t k) {
   static const int env = getenv("S24_SLABS") ? atoi(getenv("S24_SLABS")) : -1;
   if (m % 512 != 0 || env == 0) return false;
-  return env == 1 || k >= 8192;
+  if (env == 1) return true;
+  const int64_t clusters = num_sms() / 2, nt = (n + 223) / 224;
+  auto fill = [&](int64_t t) { return static_cast<double>(t) / (((t + clusters - 1) / clusters) * clusters); };
+  return k >= 4096 && fill((m / 512) * nt) >= fill((m / 256) * nt) - 0.02;
 }
 
 static int exp_flags() {
@@ -1120,7 +1124,7 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     case S24_EPI_DGATED: S24_SPT(BMN, BNV, CG, kEpiDGated);                     \
     default: S24_SP(BMN, BNV, CG, kEpiStore);                                   \
   }
-  if (pair && !b_mn && d_t && epilogue == S24_EPI_STORE && use_slabs(m, k)) {
+  if (pair && !b_mn && d_t && epilogue == S24_EPI_STORE && use_slabs(m, n, k)) {
     // two A slabs per CTA, one accumulator: 512 x 224 pair tiles
     using CS = Cfg<true, false, false, BN2, 1, 2, 1, 2>;
     return launch_gemm<true, false, false, BN2, stages_for<CS::STAGE_BYTES>(), 2, kEpiStore, true, 1, 2>(
