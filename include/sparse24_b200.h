@@ -112,6 +112,13 @@ int s24_prune_compress(const void* w, int dtype, int64_t rows, int64_t cols, con
                        uint16_t* fwd_vals, uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e, int64_t perm_ff,
                        void* stream);
 
+/* K2 of two weights in one launch (the per-step prune of W_in and W2; kept values only,
+ * E tiles unchanged): same semantics as two s24_prune_compress calls with NULL E outputs. */
+int s24_prune_compress_pair(const void* w0, const void* w1, int dtype, int64_t rows0, int64_t cols0, int64_t rows1,
+                            int64_t cols1, const uint8_t* idx0, const uint8_t* idx1, uint16_t* fwd_vals0,
+                            uint16_t* bwd_vals0, uint16_t* fwd_vals1, uint16_t* bwd_vals1, int64_t perm_ff0,
+                            int64_t perm_ff1, void* stream);
+
 /* ---- format conversions (parity export / TransposableMask API) ------------ */
 /* idx -> full 0/1 mask, uint8 rows x cols (TransposableMask.bits, sparsity.py:270-271) */
 int s24_idx_to_bits(const uint8_t* idx, int64_t rows, int64_t cols, uint8_t* bits, void* stream);

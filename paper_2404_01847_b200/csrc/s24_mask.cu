@@ -372,11 +372,17 @@ __device__ __forceinline__ uint32_t pair_selector(uint32_t nib) {
   return (2 * i0) | ((2 * i0 + 1) << 4) | ((2 * i1) << 8) | ((2 * i1 + 1) << 12);
 }
 
-__global__ void __launch_bounds__(kPruneThreads, 2) prune_bf16_kernel(MaskArgs p) {
+// one launch prunes one or two weights (the per-step K2 of W_in and W2): CTAs [0, tiles0) take
+// p0's 128 x 128 tiles, the rest p1's
+__global__ void __launch_bounds__(kPruneThreads, 2) prune_bf16_kernel(MaskArgs p0, MaskArgs p1, int tiles0) {
   __shared__ uint32_t s_bv[128 * 32];  // W^T tile: 128 rows x 32 words (64 kept bf16)
   __shared__ uint4 s_sel[90];          // per pattern: row selectors (x, y), column selectors (z, w)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tr = blockIdx.y, tc = blockIdx.x;
+  const bool second = static_cast<int>(blockIdx.x) >= tiles0;
+  const MaskArgs& p = second ? p1 : p0;
+  const int64_t bid = second ? blockIdx.x - tiles0 : blockIdx.x;
+  const int64_t tiles_x = p.cols / kTile;
+  const int64_t tr = bid / tiles_x, tc = bid - tr * tiles_x;
   const int br = 2 * warp + (lane >> 4);  // block row in tile, 0..31
   const int c0 = 8 * (lane & 15);         // first column in tile, 0..120
   const int64_t grow0 = tr * kTile + 4 * br, gcol0 = tc * kTile + c0;
@@ -743,7 +749,8 @@ static int launch_mask(const MaskArgs& a, int dtype, bool search, cudaStream_t s
   } else {
     if (dtype == S24_BF16 && a.fwd_e == nullptr && a.bwd_e == nullptr && a.fwd_vals != nullptr &&
         a.bwd_vals != nullptr && aligned) {
-      prune_bf16_kernel<<<grid, kPruneThreads, 0, st>>>(a);
+      const int tiles = static_cast<int>(grid.x * grid.y);
+      prune_bf16_kernel<<<tiles, kPruneThreads, 0, st>>>(a, a, tiles);
       return s24_check_launch("prune_compress");
     }
     if (narrow) mask_tile_kernel<S24_BF16, false, true><<<grid, kThreads, 0, st>>>(a);
@@ -798,6 +805,28 @@ extern "C" int s24_prune_compress(const void* w, int dtype, int64_t rows, int64_
   if (int rc = check_compress_outputs(rows, cols, fwd_e, bwd_e)) return rc;
   MaskArgs a{w, rows, cols, nullptr, idx, fwd_vals, fwd_e, bwd_vals, bwd_e, perm_ff};
   return launch_mask(a, dtype, false, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int s24_prune_compress_pair(const void* w0, const void* w1, int dtype, int64_t rows0, int64_t cols0,
+                                       int64_t rows1, int64_t cols1, const uint8_t* idx0, const uint8_t* idx1,
+                                       uint16_t* fwd_vals0, uint16_t* bwd_vals0, uint16_t* fwd_vals1,
+                                       uint16_t* bwd_vals1, int64_t perm_ff0, int64_t perm_ff1, void* stream) {
+  if (int rc = check_w(w0, dtype, rows0, cols0)) return rc;
+  if (int rc = check_w(w1, dtype, rows1, cols1)) return rc;
+  S24_REQUIRE(idx0 && idx1 && fwd_vals0 && bwd_vals0 && fwd_vals1 && bwd_vals1, S24_ERR_ARG, "NULL operand");
+  MaskArgs a0{w0, rows0, cols0, nullptr, idx0, fwd_vals0, nullptr, bwd_vals0, nullptr, perm_ff0};
+  MaskArgs a1{w1, rows1, cols1, nullptr, idx1, fwd_vals1, nullptr, bwd_vals1, nullptr, perm_ff1};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool fast = dtype == S24_BF16 && rows0 % kTile == 0 && cols0 % kTile == 0 && rows1 % kTile == 0 &&
+                    cols1 % kTile == 0;
+  if (!fast) {  // general shapes / dtypes: two launches of the tiled kernel
+    if (int rc = launch_mask(a0, dtype, false, st)) return rc;
+    return launch_mask(a1, dtype, false, st);
+  }
+  const int t0 = static_cast<int>((rows0 / kTile) * (cols0 / kTile)), t1 = static_cast<int>((rows1 / kTile) * (cols1 / kTile));
+  if (t0 + t1 == 0) return S24_OK;
+  prune_bf16_kernel<<<t0 + t1, kPruneThreads, 0, st>>>(a0, a1, t0);
+  return s24_check_launch("prune_compress_pair");
 }
 
 extern "C" int s24_idx_to_bits(const uint8_t* idx, int64_t rows, int64_t cols, uint8_t* bits, void* stream) {

@@ -107,6 +107,20 @@ def compress_values(w: torch.Tensor, op: CompressedOperand) -> None:
                op.fwd_vals.data_ptr(), None, op.bwd_vals.data_ptr(), None, op.perm_ff, C.stream_of(w))
 
 
+def compress_values_pair(w0: torch.Tensor, op0: CompressedOperand, w1: torch.Tensor,
+                         op1: CompressedOperand) -> None:
+    """K2 of both weights of a block in one launch (same results as two compress_values calls)."""
+    if w0.dtype != w1.dtype:
+        compress_values(w0, op0)
+        compress_values(w1, op1)
+        return
+    with TIMER("k2_prune_compress"):
+        C.call("s24_prune_compress_pair", w0.data_ptr(), w1.data_ptr(), C.dtype_code(w0), op0.rows, op0.cols,
+               op1.rows, op1.cols, op0.idx.data_ptr(), op1.idx.data_ptr(), op0.fwd_vals.data_ptr(),
+               op0.bwd_vals.data_ptr(), op1.fwd_vals.data_ptr(), op1.bwd_vals.data_ptr(), op0.perm_ff, op1.perm_ff,
+               C.stream_of(w0))
+
+
 def spmm(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b_mn: bool, n: int,
          out: torch.Tensor, bias: torch.Tensor | None = None, gelu_aux: torch.Tensor | None = None,
          tag: str = "k34_spmm", epi: int | None = None, aux: torch.Tensor | None = None,

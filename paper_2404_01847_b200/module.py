@@ -92,8 +92,7 @@ class SparseFFN(torch.nn.Module):
         if self.steps_since_refresh is None or self.steps_since_refresh >= self.refresh_period:
             self.refresh_masks()
         else:
-            E.compress_values(self.w_in.detach(), self.op_in)
-            E.compress_values(self.w2.detach(), self.op_out)
+            E.compress_values_pair(self.w_in.detach(), self.op_in, self.w2.detach(), self.op_out)
         if self.training:
             self.steps_since_refresh += 1
         return _SparseFFNFn.apply(x, self.w_in, self.bias_in, self.w2, self)

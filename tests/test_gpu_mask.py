@@ -226,3 +226,27 @@ def test_k2_fast_prune_matches_oracle(shape, perm_ff):
     compress_values(wd, op)
     assert torch.equal(op.fwd_vals.view(torch.int16), fv1.view(torch.int16))
     assert torch.equal(op.bwd_vals.view(torch.int16), bv1.view(torch.int16))
+
+
+@pytest.mark.parametrize("gated", [False, True])
+def test_k2_pair_launch_equals_two_single_launches(gated):
+    """s24_prune_compress_pair (both weights of a block in one launch) == two s24_prune_compress calls."""
+    from paper_2404_01847_b200 import engine as E
+
+    d, d_ff = 256, 384
+    r_in = 2 * d_ff if gated else d_ff
+    w_in = torch.randn(r_in, d, device="cuda").bfloat16()
+    w2 = torch.randn(d, d_ff, device="cuda").bfloat16()
+    ops = []
+    for _ in range(2):
+        a = E.CompressedOperand.empty(r_in, d, "cuda", perm_ff=d_ff if gated else 0)
+        b = E.CompressedOperand.empty(d, d_ff, "cuda")
+        E.search_compress(w_in, a)
+        E.search_compress(w2, b)
+        ops.append((a, b))
+    w_in2, w22 = w_in * 1.5, w2 - 0.25  # new values under the cached masks
+    E.compress_values(w_in2, ops[0][0])
+    E.compress_values(w22, ops[0][1])
+    E.compress_values_pair(w_in2, ops[1][0], w22, ops[1][1])
+    for x, y in zip(ops[0], ops[1]):
+        assert torch.equal(x.fwd_vals, y.fwd_vals) and torch.equal(x.bwd_vals, y.bwd_vals)
