@@ -186,6 +186,16 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const CUtensorMa
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
       : "memory");
 }
+// CTA-pair TMA load multicast to the CTAs in `mask` (same smem offset in each); each
+// destination's completion bytes land on the same-offset mbarrier of its pair's leader CTA
+__device__ __forceinline__ void tma_load_mc_cg2(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t x,
+                                                int32_t y, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y), "h"(mask)
+      : "memory");
+}
 template <int CG>
 __device__ __forceinline__ void tma_load(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t x,
                                          int32_t y) {
@@ -248,11 +258,10 @@ __device__ __forceinline__ void mma_sp_bf16_cg(uint32_t d_tmem, uint64_t adesc, 
 // commit all prior tcgen05 ops of this thread to the mbarrier at the same smem
 // offset in every CTA of the pair (CG=2) or in this CTA (CG=1)
 template <int CG>
-__device__ __forceinline__ void mma_commit_cg(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_cg(uint64_t* bar, uint16_t mask = 0x3) {
   if constexpr (CG == 1) {
     mma_commit(bar);
   } else {
-    const uint16_t mask = 0x3;
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             smem_u32(bar)),

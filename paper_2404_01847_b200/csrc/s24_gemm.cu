@@ -202,8 +202,13 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int 
   nb = in_group / gm;
 }
 
+// kMC = CTA pairs per cluster.  kMC = 2: the two pairs of a 4-CTA cluster compute vertically
+// adjacent tiles (m-tiles 2 i and 2 i + 1, same n-tile) and share the B (token) tile: each CTA
+// TMA-loads half of its 112-row B half and multicasts it to the CTA at the same position in the
+// other pair, halving the L2 reads of B.  A stage is reused only after both pairs' MMAs have
+// released it (empty barriers count kMC arrivals, MMA commits multicast to all four CTAs).
 template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT, int kAcc,
-          int kSlabs>
+          int kSlabs, int kMC>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmD,
@@ -218,6 +223,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 "training epilogues store token-major outputs");
   static_assert(kSlabs == 1 || (kAcc == 1 && ((kSparse && kFrag && kEpi == kEpiStore) || (!kSparse && kEpi == kEpiDw))),
                 "slabs: plain sparse store or dense dW only");
+  static_assert(kMC == 1 || (kMC == 2 && kSparse && kCG == 2 && !kBMN && kSlabs == 1), "multicast: sparse pairs only");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
@@ -228,12 +234,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = kCG == 2 ? cluster_rank() : 0;
+  const uint32_t crank = kCG == 2 ? cluster_rank() : 0;  // rank in the cluster
+  const uint32_t rank = crank & (kCG - 1);                 // rank in the CTA pair
+  const int pr = static_cast<int>(crank) / kCG;            // pair in the cluster (kMC = 2)
   const int num_m = shp.m / C::TILE_M;
   const int num_n = (shp.n + kBN - 1) / kBN;
   const int num_tiles = num_m * num_n;
   const int num_kb = shp.k / C::BK;  // k-blocks per output tile
-  const int cluster_id = blockIdx.x / kCG, num_clusters = gridDim.x / kCG;
+  const int cluster_id = blockIdx.x / (kCG * kMC), num_clusters = gridDim.x / (kCG * kMC);
+  // work tiles of the cluster: kMC vertically adjacent pair tiles (num_m % kMC == 0)
+  const int num_mc = num_m / kMC;
+  const int num_work = num_mc * num_n;
+  auto coords = [&](int tile, int& mb, int& nb) {
+    tile_coords(tile, num_mc, num_n, shp.group_m, mb, nb);
+    mb = mb * kMC + pr;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -245,7 +260,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], kMC);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -265,10 +280,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      WorkIter wk(shp.streamk, num_tiles, num_kb, cluster_id, num_clusters);
+      WorkIter wk(shp.streamk, num_work, num_kb, cluster_id, num_clusters);
       int tile, kb0, kb1, wave = 0;
       unsigned int* wctr = shp.wave_slot >= 0 ? &g_wave_ctr[shp.wave_slot][0] : nullptr;
-      while (wk.next(num_tiles, num_kb, tile, kb0, kb1)) {
+      while (wk.next(num_work, num_kb, tile, kb0, kb1)) {
         if (wctr != nullptr && wave > 0) {
           // every producer has issued the previous wave's loads (bounded wait)
           const unsigned int target = gridDim.x * wave;
@@ -276,7 +291,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           while (static_cast<int>(ld_acquire_gpu(wctr) - target) < 0 && clock64() - t0 < 40000) __nanosleep(32);
         }
         int mb, nb;
-        tile_coords(tile, num_m, num_n, shp.group_m, mb, nb);
+        coords(tile, mb, nb);
         const int m0 = mb * C::TILE_M + 128 * rank;      // this CTA's A rows (slab s: + 128 kCG s)
         const int nb0 = ((shp.exp & 4) ? 0 : nb * kBN) + C::BN_CTA * rank;  // this CTA's B rows (N split)
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -310,6 +325,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int i = 0; i < C::B_CHUNKS; ++i)
               tma_load<kCG>(sB + i * C::B_BOX_BYTES, &tmB, &full_bar[stage], nb0 + 64 * i, kb * C::BK);
+          } else if constexpr (kMC == 2) {
+            // my half of this CTA's B rows, multicast to the same-position CTA of both pairs
+            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (kCG + rank)));
+#pragma unroll
+            for (int i = 0; i < C::BK / 64; ++i)
+              tma_load_mc_cg2(sB + i * C::B_BOX_BYTES + pr * (C::BN_CTA / 2) * 128, &tmB, &full_bar[stage],
+                              kb * C::BK + 64 * i, nb0 + pr * (C::BN_CTA / 2), mask);
           } else {
 #pragma unroll
             for (int i = 0; i < C::BK / 64; ++i)
@@ -331,9 +353,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      WorkIter wk(shp.streamk, num_tiles, num_kb, cluster_id, num_clusters);
+      WorkIter wk(shp.streamk, num_work, num_kb, cluster_id, num_clusters);
       int tile, kb0, kb1;
-      while (wk.next(num_tiles, num_kb, tile, kb0, kb1)) {
+      while (wk.next(num_work, num_kb, tile, kb0, kb1)) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
@@ -380,13 +402,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                  accum);
             }
           }
-          mma_commit_cg<kCG>(&empty_bar[stage]);
+          // release the stage in every CTA that reads it (both pairs when B is multicast)
+          mma_commit_cg<kCG>(&empty_bar[stage], kMC == 2 ? 0xF : 0x3);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit_cg<kCG>(&tfull_bar[acc]);
+        mma_commit_cg<kCG>(&tfull_bar[acc], static_cast<uint16_t>(0x3u << (kCG * pr)));
         if (++acc == kAcc) {
           acc = 0;
           acc_phase ^= 1;
@@ -409,11 +432,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int mj = lane >> 3, mi = lane & 7;
       int acc = 0, sbuf = 0, par = 0;
       uint32_t acc_phase = 0;
-      WorkIter wk(false, num_tiles, num_kb, cluster_id, num_clusters);
+      WorkIter wk(false, num_work, num_kb, cluster_id, num_clusters);
       int tile, kb0, kb1;
-      for (; wk.next(num_tiles, num_kb, tile, kb0, kb1); par ^= 1) {
+      for (; wk.next(num_work, num_kb, tile, kb0, kb1); par ^= 1) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, shp.group_m, mb, nb);
+        coords(tile, mb, nb);
         const int n_base = nb * kBN;
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
@@ -649,7 +672,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (kCG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);
+          if constexpr (kCG == 2) mbar_arrive_cluster(&tempty_bar[acc], crank & ~1u);  // pair leader
           else mbar_arrive(&tempty_bar[acc]);
         }
         if (++acc == kAcc) {
@@ -667,11 +690,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint8_t* stg = smem + C::EPI_OFF + (warp - 4) * 4096;
       int acc = 0, sbuf = 0;
       uint32_t acc_phase = 0;
-      WorkIter wk(shp.streamk, num_tiles, num_kb, cluster_id, num_clusters);
+      WorkIter wk(shp.streamk, num_work, num_kb, cluster_id, num_clusters);
       int tile, kb0, kb1;
-      while (wk.next(num_tiles, num_kb, tile, kb0, kb1)) {
+      while (wk.next(num_work, num_kb, tile, kb0, kb1)) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, shp.group_m, mb, nb);
+        coords(tile, mb, nb);
         const bool first_chunk = kb0 == 0;                  // adds the decay exactly once
         const bool partial = kb0 != 0 || kb1 != num_kb;     // stream-K piece: add-reduce
         const int n_base = nb * kBN;
@@ -825,7 +848,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (kCG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);
+          if constexpr (kCG == 2) mbar_arrive_cluster(&tempty_bar[acc], crank & ~1u);  // pair leader
           else mbar_arrive(&tempty_bar[acc]);
         }
         if (++acc == kAcc) {
@@ -964,6 +987,14 @@ static bool use_slabs(int64_t m, int64_t n, int64_t k) {
   return k >= 4096 && fill((m / 512) * nt) >= fill((m / 256) * nt) - 0.02;
 }
 
+// B multicast across two CTA pairs (gemm_kernel kMC = 2): halves the L2 reads of the token
+// operand.  S24_MC=0/1 overrides; needs an even number of 256-row pair tiles.
+static bool use_mc(int64_t m) {
+  static const int env = getenv("S24_MC") ? atoi(getenv("S24_MC")) : -1;
+  if (m % 512 != 0 || env == 0) return false;
+  return env == 1;
+}
+
 static int exp_flags() {
   static const int v = getenv("S24_EXP") ? atoi(getenv("S24_EXP")) : 0;
   return v;
@@ -978,29 +1009,52 @@ static int pick_group_m(int num_m, double a_bytes_per_mtile) {
 }
 
 template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int kEpi, bool kOutT = false,
-          int kAcc = 2, int kSlabs = 1>
+          int kAcc = 2, int kSlabs = 1, int kMC = 1>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& me, const CUtensorMap& md,
                        const CUtensorMap& mx, const CUtensorMap& my, const GemmShape& shp, const EpiParams& ep,
                        cudaStream_t st) {
   using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG, kAcc, kSlabs>;
-  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi, kOutT, kAcc, kSlabs>;
+  auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi, kOutT, kAcc, kSlabs, kMC>;
   static bool attr_done = false;  // per template instance
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_done = true;
   }
-  const int tiles = (shp.m / C::TILE_M) * ((shp.n + kBN - 1) / kBN);
-  const int clusters = (shp.streamk || tiles > num_sms() / kCG) ? num_sms() / kCG : tiles;
+  constexpr int kCS = kCG * kMC;  // CTAs per cluster
+  const int tiles = (shp.m / C::TILE_M / kMC) * ((shp.n + kBN - 1) / kBN);
+  // persistent grid: as many clusters as are co-resident (a 4-CTA cluster needs 4 free SMs
+  // in one GPC, so fewer than 148 / 4 may fit), never more than there are work tiles
+  static int max_clusters = 0;  // per template instance
+  if (max_clusters == 0) {
+    max_clusters = num_sms() / kCS;
+    if (kCS > 2) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(kCS * max_clusters);
+      q.blockDim = dim3(kGemmThreads);
+      q.dynamicSmemBytes = C::SMEM_BYTES;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = kCS;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &q) == cudaSuccess && n > 0 && n < max_clusters) max_clusters = n;
+      (void)cudaGetLastError();
+    }
+  }
+  const int clusters = (shp.streamk || tiles > max_clusters) ? max_clusters : tiles;
   if (clusters <= 0) return S24_OK;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(clusters * kCG);
+  cfg.gridDim = dim3(clusters * kCS);
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCG;
+  attr[0].val.clusterDim.x = kCS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -1124,7 +1178,24 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     case S24_EPI_DGATED: S24_SPT(BMN, BNV, CG, kEpiDGated);                     \
     default: S24_SP(BMN, BNV, CG, kEpiStore);                                   \
   }
-  if (pair && !b_mn && d_t && epilogue == S24_EPI_STORE && use_slabs(m, n, k)) {
+  const bool slabs = pair && !b_mn && d_t && epilogue == S24_EPI_STORE && use_slabs(m, n, k);
+  if (!slabs && pair && !b_mn && d_t && epilogue != S24_EPI_GELU_AUX && use_mc(m)) {
+    // 4-CTA clusters, B multicast across the two pairs: B boxes of BN_CTA / 2 rows
+    if (int rc = make_map(&mb, b, k, n, ldb, 64, BN2 / 4)) return rc;
+#define S24_SPMC(EPI)                                                                                             \
+  return launch_gemm<true, false, false, BN2, stages_for<Cfg<true, false, false, BN2, 1, 2>::STAGE_BYTES>(), 2, EPI, \
+                     true, 2, 1, 2>(ma, mb, me, md, mx, my, shp, ep, st)
+    switch (epilogue) {
+      case S24_EPI_GELU_GRAD: S24_SPMC(kEpiGeluGrad);
+      case S24_EPI_DGELU: S24_SPMC(kEpiDAct);
+      case S24_EPI_GEGLU_GRAD:
+      case S24_EPI_SWIGLU_GRAD: S24_SPMC(kEpiGatedGrad);
+      case S24_EPI_DGATED: S24_SPMC(kEpiDGated);
+      default: S24_SPMC(kEpiStore);
+    }
+#undef S24_SPMC
+  }
+  if (slabs) {
     // two A slabs per CTA, one accumulator: 512 x 224 pair tiles
     using CS = Cfg<true, false, false, BN2, 1, 2, 1, 2>;
     return launch_gemm<true, false, false, BN2, stages_for<CS::STAGE_BYTES>(), 2, kEpiStore, true, 1, 2>(
