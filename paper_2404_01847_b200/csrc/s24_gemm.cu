@@ -221,8 +221,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                    kEpi == kEpiGatedGrad || kEpi == kEpiDGated);
   static_assert(kOutT || !(kEpi == kEpiGeluGrad || kEpi == kEpiDAct || kEpi == kEpiGatedGrad || kEpi == kEpiDGated),
                 "training epilogues store token-major outputs");
-  static_assert(kSlabs == 1 || (kAcc == 1 && ((kSparse && kFrag && kEpi == kEpiStore) || (!kSparse && kEpi == kEpiDw))),
-                "slabs: plain sparse store or dense dW only");
+  static_assert(kSlabs == 1 || (kAcc == 1 && ((kSparse && kFrag) || (!kSparse && kEpi == kEpiDw))),
+                "slabs: sparse fragment epilogues or dense dW only");
   static_assert(kMC == 1 || (kMC == 2 && kSparse && kCG == 2 && !kBMN && kSlabs == 1), "multicast: sparse pairs only");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -995,6 +995,18 @@ static bool use_mc(int64_t m) {
   return env == 1;
 }
 
+// Two-slab tiles for the fused training epilogues as well, where K is long enough to carry the
+// un-overlapped epilogue (measured on B200: C3's SwiGLU GEMM1, K = 4096, -4 %; C2's K = 1024
+// GELU / dGELU GEMMs +17..35 %, so not there).  S24_SLABS_EPI=0/1 overrides.
+static bool use_slabs_epi(int64_t m, int64_t n, int64_t k) {
+  static const int env = getenv("S24_SLABS_EPI") ? atoi(getenv("S24_SLABS_EPI")) : -1;
+  if (m % 512 != 0 || env == 0) return false;
+  if (env == 1) return true;
+  const int64_t clusters = num_sms() / 2, nt = (n + 223) / 224;
+  auto fill = [&](int64_t t) { return static_cast<double>(t) / (((t + clusters - 1) / clusters) * clusters); };
+  return k >= 4096 && fill((m / 512) * nt) >= fill((m / 256) * nt) - 0.02;
+}
+
 static int exp_flags() {
   static const int v = getenv("S24_EXP") ? atoi(getenv("S24_EXP")) : 0;
   return v;
@@ -1200,6 +1212,19 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     using CS = Cfg<true, false, false, BN2, 1, 2, 1, 2>;
     return launch_gemm<true, false, false, BN2, stages_for<CS::STAGE_BYTES>(), 2, kEpiStore, true, 1, 2>(
         ma, mb, me, md, mx, my, shp, ep, st);
+  }
+  if (pair && !b_mn && d_t && epilogue != S24_EPI_STORE && epilogue != S24_EPI_GELU_AUX && use_slabs_epi(m, n, k)) {
+    using CS = Cfg<true, false, false, BN2, 1, 2, 1, 2>;
+#define S24_SPSL(EPI) \
+  return launch_gemm<true, false, false, BN2, stages_for<CS::STAGE_BYTES>(), 2, EPI, true, 1, 2>(ma, mb, me, md, mx, my, shp, ep, st)
+    switch (epilogue) {
+      case S24_EPI_GELU_GRAD: S24_SPSL(kEpiGeluGrad);
+      case S24_EPI_DGELU: S24_SPSL(kEpiDAct);
+      case S24_EPI_GEGLU_GRAD:
+      case S24_EPI_SWIGLU_GRAD: S24_SPSL(kEpiGatedGrad);
+      default: S24_SPSL(kEpiDGated);
+    }
+#undef S24_SPSL
   }
   if (pair) {
     if (b_mn) S24_SP_EPI(true, BN2, 2);
