@@ -237,7 +237,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t crank = kCG == 2 ? cluster_rank() : 0;  // rank in the cluster
   const uint32_t rank = crank & (kCG - 1);                 // rank in the CTA pair
   const int pr = static_cast<int>(crank) / kCG;            // pair in the cluster (kMC = 2)
-  const int num_m = shp.m / C::TILE_M;
+  // a two-slab tile may hang half over the last rows (m % 256 == 0): its second slab reads
+  // zero-filled TMA boxes and its epilogue is skipped
+  const int num_m = (shp.m + C::TILE_M - 1) / C::TILE_M;
   const int num_n = (shp.n + kBN - 1) / kBN;
   const int num_tiles = num_m * num_n;
   const int num_kb = shp.k / C::BK;  // k-blocks per output tile
@@ -443,6 +445,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
         for (int slab = 0; slab < kSlabs; ++slab) {
         const int m_w = mb * C::TILE_M + 128 * kCG * slab + 128 * rank + 32 * q;  // first TMEM row of this warp
+        if (kSlabs > 1 && m_w >= shp.m) continue;  // slab beyond the last row
         float bias4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // bias of row m_w + 8j + t4 (forward)
         float bs1[4] = {0.0f, 0.0f, 0.0f, 0.0f};    // bias-gradient partials (backward), u / plain
         float bs2[4] = {0.0f, 0.0f, 0.0f, 0.0f};    // v half (kEpiDGated)
@@ -980,11 +983,13 @@ static bool use_dw_slabs(int64_t m, int64_t n, int64_t k) {
 // wave worse filled.  S24_SLABS=0 off, =1 whenever the shape allows (m % 512 == 0).
 static bool use_slabs(int64_t m, int64_t n, int64_t k) {
   static const int env = getenv("S24_SLABS") ? atoi(getenv("S24_SLABS")) : -1;
-  if (m % 512 != 0 || env == 0) return false;
+  if (m % 256 != 0 || env == 0) return false;
   if (env == 1) return true;
   const int64_t clusters = num_sms() / 2, nt = (n + 223) / 224;
   auto fill = [&](int64_t t) { return static_cast<double>(t) / (((t + clusters - 1) / clusters) * clusters); };
-  return k >= 4096 && fill((m / 512) * nt) >= fill((m / 256) * nt) - 0.02;
+  // work in 256-row units: a ragged last slab tile costs a full tile
+  const double t2 = static_cast<double>((m + 511) / 512 * nt), t1 = static_cast<double>(m / 256 * nt);
+  return k >= 4096 && fill(static_cast<int64_t>(t2)) * t1 / (2.0 * t2) >= fill(static_cast<int64_t>(t1)) - 0.02;
 }
 
 // B multicast across two CTA pairs (gemm_kernel kMC = 2): halves the L2 reads of the token
@@ -1000,11 +1005,12 @@ static bool use_mc(int64_t m) {
 // GELU / dGELU GEMMs +17..35 %, so not there).  S24_SLABS_EPI=0/1 overrides.
 static bool use_slabs_epi(int64_t m, int64_t n, int64_t k) {
   static const int env = getenv("S24_SLABS_EPI") ? atoi(getenv("S24_SLABS_EPI")) : -1;
-  if (m % 512 != 0 || env == 0) return false;
+  if (m % 256 != 0 || env == 0) return false;
   if (env == 1) return true;
   const int64_t clusters = num_sms() / 2, nt = (n + 223) / 224;
   auto fill = [&](int64_t t) { return static_cast<double>(t) / (((t + clusters - 1) / clusters) * clusters); };
-  return k >= 4096 && fill((m / 512) * nt) >= fill((m / 256) * nt) - 0.02;
+  const double t2 = static_cast<double>((m + 511) / 512 * nt), t1 = static_cast<double>(m / 256 * nt);
+  return k >= 4096 && fill(static_cast<int64_t>(t2)) * t1 / (2.0 * t2) >= fill(static_cast<int64_t>(t1)) - 0.02;
 }
 
 static int exp_flags() {
@@ -1034,7 +1040,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
     attr_done = true;
   }
   constexpr int kCS = kCG * kMC;  // CTAs per cluster
-  const int tiles = (shp.m / C::TILE_M / kMC) * ((shp.n + kBN - 1) / kBN);
+  const int tiles = ((shp.m + C::TILE_M - 1) / C::TILE_M / kMC) * ((shp.n + kBN - 1) / kBN);
   // persistent grid: as many clusters as are co-resident (a 4-CTA cluster needs 4 free SMs
   // in one GPC, so fewer than 148 / 4 may fit), never more than there are work tiles
   static int max_clusters = 0;  // per template instance

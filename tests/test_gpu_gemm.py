@@ -227,7 +227,7 @@ def test_sparse_gemm_two_slab_forced_small_k():
         "import torch, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
         "from test_gpu_gemm import _operand\n"
         "from paper_2404_01847_b200.engine import spmm\n"
-        "for m, k, n in [(512, 128, 32), (512, 1024, 448), (1536, 2048, 672)]:\n"
+        "for m, k, n in [(512, 128, 32), (512, 1024, 448), (1536, 2048, 672), (768, 512, 224), (1280, 256, 96)]:\n"
         "    w, op, bits = _operand(m, k, 5 + k)\n"
         "    x = torch.randn(n, k, device='cuda').bfloat16()\n"
         "    out = torch.full((n, m), float('nan'), dtype=torch.bfloat16, device='cuda')\n"
@@ -300,5 +300,36 @@ def test_sparse_gemm_b_multicast_forced():
         "    e = float((out.float() - ref * gd).norm() / (ref * gd).norm()); assert e < 1e-2, ('dgelu', m, k, n, e)\n"
         "print('ok')\n" % (os.path.abspath(os.path.join(os.path.dirname(__file__), "..")), os.path.dirname(__file__)))
     env = dict(os.environ, S24_MC="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_fused_epilogues_two_slab_tiles_forced():
+    """S24_SLABS_EPI=1: GELU/GELU' and dGELU + bias-gradient epilogues on two-slab tiles, including
+    a ragged last tile whose second slab lies beyond m (m = 768)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from test_gpu_gemm import _operand\n"
+        "from paper_2404_01847_b200.engine import spmm, aux_empty, aux_to_feature_major\n"
+        "import paper_2404_01847_b200._capi as C\n"
+        "for m, k, n in [(512, 256, 224), (768, 512, 448), (1280, 1024, 96)]:\n"
+        "    w, op, bits = _operand(m, k, 3 + m + k)\n"
+        "    x = torch.randn(n, k, device='cuda').bfloat16()\n"
+        "    ref = x.float() @ (w.float() * bits.float()).t()\n"
+        "    out = torch.full((n, m), float('nan'), dtype=torch.bfloat16, device='cuda')\n"
+        "    g = aux_empty(m, n, 'cuda')\n"
+        "    spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, None, epi=C.EPI_GELU_GRAD, aux=g, out_t=True)\n"
+        "    zr = ref.double(); cdf = 0.5 * (1 + torch.erf(zr / 2 ** 0.5))\n"
+        "    e = float((out.double() - zr * cdf).norm() / (zr * cdf).norm()); assert e < 1e-2, ('gelu', m, k, n, e)\n"
+        "    db = torch.zeros(m, device='cuda')\n"
+        "    spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, None, epi=C.EPI_DGELU, aux=g, dbias=db, out_t=True)\n"
+        "    gd = aux_to_feature_major(g, m, n).t().float()\n"
+        "    e = float((out.float() - ref * gd).norm() / (ref * gd).norm()); assert e < 1e-2, ('dgelu', m, k, n, e)\n"
+        "    e = float((db - (ref * gd).sum(0)).norm() / (ref * gd).sum(0).norm()); assert e < 1e-2, ('dbias', e)\n"
+        "print('ok')\n" % (os.path.abspath(os.path.join(os.path.dirname(__file__), "..")), os.path.dirname(__file__)))
+    env = dict(os.environ, S24_SLABS_EPI="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
