@@ -45,6 +45,7 @@ CONFIGS = {
                d=12288, d_ff=49152, act="gelu", tokens=16384),
 }
 REFRESH = 40
+DP_RESERVED_SMS = int(os.environ.get("S24_DP_RESERVED_SMS", "16"))  # SMs the dX GEMM leaves to NCCL (N > 1)
 LAMBDA = 6e-5
 METRIC = "2:4 FFN fwd+bwd tokens/s & speedup vs dense bf16; mask-search HBM GB/s"
 
@@ -226,7 +227,9 @@ class SparseStep:
         import torch
         from paper_2404_01847_b200 import engine as E
 
-        self.E, self.torch = E, torch
+        from paper_2404_01847_b200 import _capi
+
+        self.E, self.torch, self.C = E, torch, _capi
         self.w_in, self.bias, self.w2, self.act, self.world, self.pg = w_in, bias, w2, act, world, pg
         dev = w_in.device
         # gated layers: first weight compressed u/v-interleaved for the fused gate epilogues
@@ -256,14 +259,18 @@ class SparseStep:
         work = []
 
         def grads_ready():
-            # the one all-reduce of [dW_in | dbias | dW2] starts while dX is still computing
+            # the one all-reduce of [dW_in | dbias | dW2] starts while dX is still computing; the
+            # dX GEMM leaves DP_RESERVED_SMS SMs to the collective so the two actually overlap
             if self.world > 1:
                 work.append(self.torch.distributed.all_reduce(self.bucket, group=self.pg, async_op=True))
+                self.C.call("s24_set_reserved_sms", DP_RESERVED_SMS)
 
         g = E.ffn_backward(st, dy, self.op_in, self.op_out, self.act, w_in_dense=self.w_in, w2_dense=self.w2,
                            lam=LAMBDA / self.world, dw_in_out=self.dw_in, dw2_out=self.dw2, mvue=bool(self.mvue),
                            rng_seed=self.t, mvue_exact=self.mvue == "exact", dbias_out=self.dbias,
                            grads_ready=grads_ready)
+        if self.world > 1:
+            self.C.call("s24_set_reserved_sms", 0)
         for w in work:
             w.wait()
         self.t += 1

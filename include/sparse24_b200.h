@@ -157,6 +157,11 @@ int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, c
              int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias, int epilogue, uint16_t* aux,
              int64_t ldaux, uint16_t* aux2, float* dbias, int d_t, int64_t gate_ff, void* stream);
 
+/* Process-wide: leave `sms` SMs free in subsequent GEMM launches (0 = use all).  A
+ * data-parallel step sets it around the dX GEMM so the gradient all-reduce's kernels run
+ * concurrently with it (the persistent GEMMs otherwise occupy every SM). */
+int s24_set_reserved_sms(int sms);
+
 /* ---- K5: dense tcgen05 dW GEMM with fused masked decay ---------------------
  * D[m, n] (fp32, ldd) = sum_k A[m, k] B[n, k] + lambda_w * (1 - M[m, n]) * W[m, n]
  * Replaces _grad_weight(mvue=False) (gated_ffn.py:367-371) followed by

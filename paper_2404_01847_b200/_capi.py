@@ -52,6 +52,7 @@ SIGNATURES = {
     "s24_adam_step": [_P, _P, _P, _I, _P, _I, _I64, _I64, _P] + [ctypes.c_double] * 10 + [_I, _P],
     "s24_mask_flips": [_P, _P, _I64, _P, _P, _P],
     "s24_greedy_search": [_P, _I, _I64, _I64, _P, _P, _P],
+    "s24_set_reserved_sms": [_I],
     "s24_prune_compress_pair": [_P, _P, _I, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _I64, _P],
     "s24_prune_2of4": [_P, _I, _I64, _I64, _I, _P, _P],
 }

@@ -22,6 +22,7 @@
 // Pipelines: kStages smem slots (full/empty mbarriers) and two TMEM
 // accumulators (tmem_full/tmem_empty) so the epilogue of tile i overlaps the
 // main loop of tile i+1.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -924,6 +925,11 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t ou
   return S24_OK;
 }
 
+// SMs left free by the persistent GEMMs (s24_set_reserved_sms): a data-parallel step reserves a
+// few while its gradient all-reduce runs so the collective's kernel is co-resident with the
+// dX GEMM instead of queueing behind it.
+static int g_reserved_sms = 0;
+
 static int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -1063,7 +1069,9 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
       (void)cudaGetLastError();
     }
   }
-  const int clusters = (shp.streamk || tiles > max_clusters) ? max_clusters : tiles;
+  int cap = max_clusters;
+  if (g_reserved_sms > 0) cap = std::max(1, std::min(cap, (num_sms() - g_reserved_sms) / kCS));
+  const int clusters = (shp.streamk || tiles > cap) ? cap : tiles;
   if (clusters <= 0) return S24_OK;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * kCS);
@@ -1089,6 +1097,12 @@ using namespace s24;
 static int cg_override() {
   static const int v = getenv("S24_GEMM_CG") ? atoi(getenv("S24_GEMM_CG")) : 0;
   return v;
+}
+
+extern "C" int s24_set_reserved_sms(int sms) {
+  S24_REQUIRE(sms >= 0, S24_ERR_ARG, "reserved SM count must be >= 0");
+  g_reserved_sms = sms;
+  return S24_OK;
 }
 
 extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b,

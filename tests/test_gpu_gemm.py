@@ -333,3 +333,22 @@ def test_fused_epilogues_two_slab_tiles_forced():
     env = dict(os.environ, S24_SLABS_EPI="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_reserved_sms_leave_results_unchanged():
+    """s24_set_reserved_sms shrinks the persistent grids (DP overlap); results are unchanged."""
+    import paper_2404_01847_b200._capi as C
+    from paper_2404_01847_b200.engine import spmm
+
+    m, k, n = 1024, 1024, 2048
+    w, op, bits = _operand(m, k, 21)
+    x = torch.randn(n, k, device="cuda").bfloat16()
+    full = torch.empty((n, m), dtype=torch.bfloat16, device="cuda")
+    spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, full, out_t=True)
+    part = torch.empty_like(full)
+    try:
+        C.call("s24_set_reserved_sms", 100)
+        spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, part, out_t=True)
+    finally:
+        C.call("s24_set_reserved_sms", 0)
+    assert torch.equal(full, part)
