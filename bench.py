@@ -540,6 +540,41 @@ def run_ours(a, cfg):
                       "frac_of_hbm": opt_gbs / peaks["hbm_gbs"]}
     del ost
 
+    # ---- standalone activation kernels (K6/K7: the API's unfused path; the training step fuses
+    # the activation into the GEMM epilogues) at this config's token batch ----
+    r_act = w2.shape[1]
+    r_in_act = w_in.shape[0]
+    zc = torch.randn(n_tok, r_in_act, device=dev).to(torch.bfloat16)
+    ac = torch.empty(n_tok, r_act, dtype=torch.bfloat16, device=dev)
+    dac = torch.randn(n_tok, r_act, device=dev).to(torch.bfloat16)
+    dzc = torch.empty_like(zc)
+    dbc = torch.empty(r_in_act, dtype=torch.float32, device=dev)
+    code = E.ACT_CODES[cfg["act"]]
+
+    def _t(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    f_ms = _t(lambda: C.call("s24_act_fwd", zc.data_ptr(), r_in_act, r_act, n_tok, code, ac.data_ptr(), r_act,
+                             C.stream_of(zc)))
+    b_ms = _t(lambda: C.call("s24_act_bwd", zc.data_ptr(), r_in_act, dac.data_ptr(), r_act, r_act, n_tok, code,
+                             dzc.data_ptr(), r_in_act, dbc.data_ptr(), C.stream_of(zc)))
+    gated = r_in_act == 2 * r_act
+    f_bytes = n_tok * r_act * 2 * (3 if gated else 2)  # K6 fwd
+    b_bytes = n_tok * r_act * 2 * (5 if gated else 3) + r_in_act * 4  # K7 bwd + fp32 bias grads
+    activation = {"kernels": "s24_act_fwd / s24_act_bwd (standalone; fused into the GEMM epilogues on the step)",
+                  "fwd": {"ms": f_ms, "gbs": f_bytes / (f_ms * 1e-3) / 1e9,
+                          "frac_of_hbm": f_bytes / (f_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+                  "bwd": {"ms": b_ms, "gbs": b_bytes / (b_ms * 1e-3) / 1e9,
+                          "frac_of_hbm": b_bytes / (b_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}}
+    del zc, ac, dac, dzc, dbc
+
     # ---- e2e through the public autograd module, host-resident inputs ----
     e2e = run_e2e(a, cfg, w_in, bias, w2, dev, world, dist if world > 1 else None)
 
@@ -572,7 +607,7 @@ def run_ours(a, cfg):
             "speedup_vs_dense_gemm_only": (value / dense_gemm_only) if dense_gemm_only else None,
             "variants": {k: dict(v, speedup_vs_dense=(v["tokens_per_s"] / dense) if dense else None)
                          for k, v in variants.items()},
-            "mask_search": mask_search, "optimizer_step": optimizer_step,
+            "mask_search": mask_search, "optimizer_step": optimizer_step, "activation": activation,
             "roofline": roof,
             "kernels": per_kernel,
             "e2e": e2e,

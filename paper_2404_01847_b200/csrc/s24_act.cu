@@ -15,35 +15,31 @@
 
 namespace s24 {
 
-constexpr float kRsqrt2 = 0.70710678118654752f;
-constexpr float kRsqrt2Pi = 0.39894228040143268f;
-
-// exact-erf GELU and its derivative through erf_fast (|erf error| < 2e-7, far
-// below the bf16 output rounding); erf_fast also returns exp(-x^2/2), reused
-// for the Gaussian density in GELU'.
-__device__ __forceinline__ float gelu_f(float x) { return gelu_fast(x); }
-__device__ __forceinline__ float gelu_grad_f(float x) {
-  float e;
-  const float erf_v = erf_fast(x * kRsqrt2, e);
-  return 0.5f * (1.0f + erf_v) + x * (kRsqrt2Pi * e);
+// GELU / GELU' and SiLU / SiLU' with one MUFU op each (gelu_and_grad, sigmoid_fast in
+// s24_common.cuh -- the same functions as the GEMM epilogues, so the fused and unfused
+// paths agree); the backward of the gated forms needs act and act' of the same z1.
+template <int kAct>
+__device__ __forceinline__ void act_both(float x, float& a, float& da) {
+  if constexpr (kAct == S24_ACT_RELU) {
+    a = fmaxf(x, 0.0f);
+    da = x > 0.0f ? 1.0f : 0.0f;
+  } else if constexpr (kAct == S24_ACT_SWIGLU) {
+    const float sg = sigmoid_fast(x);
+    a = x * sg;
+    da = sg * fmaf(x, 1.0f - sg, 1.0f);
+  } else {
+    gelu_and_grad(x, a, da);
+  }
 }
-__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
-__device__ __forceinline__ float silu_grad_f(float x) {
-  const float s = 1.0f / (1.0f + __expf(-x));
-  return s * (1.0f + x * (1.0f - s));
-}
-
 template <int kAct>
 __device__ __forceinline__ float act_f(float x) {
   if constexpr (kAct == S24_ACT_RELU) return fmaxf(x, 0.0f);
-  else if constexpr (kAct == S24_ACT_SWIGLU) return silu_f(x);
-  else return gelu_f(x);
-}
-template <int kAct>
-__device__ __forceinline__ float act_grad_f(float x) {
-  if constexpr (kAct == S24_ACT_RELU) return x > 0.0f ? 1.0f : 0.0f;
-  else if constexpr (kAct == S24_ACT_SWIGLU) return silu_grad_f(x);
-  else return gelu_grad_f(x);
+  else if constexpr (kAct == S24_ACT_SWIGLU) return x * sigmoid_fast(x);
+  else {
+    float a, da;
+    gelu_and_grad(x, a, da);
+    return a;
+  }
 }
 
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
@@ -82,7 +78,7 @@ __global__ void __launch_bounds__(256) act_fwd_kernel(const uint16_t* __restrict
   }
 }
 
-constexpr int kBwdTokens = 128;  // tokens per CTA in the backward (bias partials per CTA)
+constexpr int kBwdTokens = 64;  // tokens per CTA in the backward (bias partials per CTA)
 
 template <int kAct, bool kGated>
 __global__ void __launch_bounds__(256) act_bwd_kernel(const uint16_t* __restrict__ z, int64_t ldz,
@@ -98,7 +94,7 @@ __global__ void __launch_bounds__(256) act_bwd_kernel(const uint16_t* __restrict
   float s1[8], s2[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) s1[i] = s2[i] = 0.0f;
-#pragma unroll 2
+#pragma unroll 4
   for (int64_t t = t0; t < t1; ++t) {
     float x[8], d[8], o1[8];
     unpack8(__ldg(reinterpret_cast<const uint4*>(z + t * ldz + j)), x);
@@ -108,8 +104,10 @@ __global__ void __launch_bounds__(256) act_bwd_kernel(const uint16_t* __restrict
       unpack8(__ldg(reinterpret_cast<const uint4*>(z + t * ldz + r + j)), g);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        o1[i] = d[i] * g[i] * act_grad_f<kAct>(x[i]);  // dZ1 = dA * z2 * act'(z1)
-        o2[i] = d[i] * act_f<kAct>(x[i]);              // dZ2 = dA * act(z1)
+        float a, da_;
+        act_both<kAct>(x[i], a, da_);
+        o1[i] = d[i] * g[i] * da_;  // dZ1 = dA * z2 * act'(z1)
+        o2[i] = d[i] * a;           // dZ2 = dA * act(z1)
         s1[i] += o1[i];
         s2[i] += o2[i];
       }
@@ -117,7 +115,9 @@ __global__ void __launch_bounds__(256) act_bwd_kernel(const uint16_t* __restrict
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        o1[i] = d[i] * act_grad_f<kAct>(x[i]);
+        float a, da_;
+        act_both<kAct>(x[i], a, da_);
+        o1[i] = d[i] * da_;
         s1[i] += o1[i];
       }
     }
