@@ -1,23 +1,11 @@
-"""K1 (search + compress) timing and ncu target: C3 W_in (22016 x 4096, gated)."""
-import sys, os
+"""K1 (fused search + compress) on the C3 first weight, a few launches (for ncu)."""
+import os, sys
 sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
 import torch
 from paper_2404_01847_b200 import engine as E
-
-rows, cols, ff = 22016, 4096, 11008
-w = torch.randn(rows, cols, device="cuda").bfloat16()
-op = E.CompressedOperand.empty(rows, cols, "cuda", perm_ff=ff)
-E.search_compress(w, op)
+rows, cols = (int(a) for a in (sys.argv[1:3] if len(sys.argv) > 2 else (22016, 4096)))
+w = (torch.randn(rows, cols, device="cuda") / cols ** 0.5).bfloat16()
+op = E.CompressedOperand.empty(rows, cols, "cuda")
 for _ in range(3):
     E.search_compress(w, op)
 torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-algo = rows * cols * (2 * 2 + 0.3125)
-torch.cuda._sleep(1_000_000)
-e0.record()
-for _ in range(20):
-    E.search_compress(w, op)
-e1.record()
-torch.cuda.synchronize()
-ms = e0.elapsed_time(e1) / 20
-print("K1", round(ms, 4), "ms", round(algo / ms / 1e6, 1), "GB/s")
