@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
       const uint32_t k1 = static_cast<uint32_t>(rng.state.lo ^ (rng.state.lo >> 32)),
                      k2 = static_cast<uint32_t>(rng.inc.hi ^ (rng.inc.hi >> 32));
       idx = static_cast<int>(mvue_nibble_f32(gv, counter_uniform(k1, k2, static_cast<uint32_t>(stream0 + j)), f0, f1));
-      packed[j] = static_cast<uint32_t>(f32_to_bf16(f0)) | (static_cast<uint32_t>(f32_to_bf16(f1)) << 16);
+      packed[j] = pack_bf16x2(f0, f1);
     }
     // nibble i0 | i1 << 2 of pair idx = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE}[idx]
     const uint32_t nib = (0xED9C84u >> (4 * idx)) & 0xFu;
