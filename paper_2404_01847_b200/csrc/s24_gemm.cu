@@ -13,15 +13,21 @@
 //                   Replaces _grad_weight(mvue=False) (gated_ffn.py:367-371)
 //                   + masked_decay_gradient (optim.py:105-114).
 //
-// CTA layout (256 threads, one CTA per SM, persistent over output tiles):
-//   warp 0      TMA producer (one elected lane)
-//   warp 1      MMA issuer (one elected lane) + tcgen05.cp of the metadata
-//   warp 2      TMEM allocator
-//   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns -> registers ->
-//               bias / GELU / decay -> global stores
-// Pipelines: kStages smem slots (full/empty mbarriers) and two TMEM
-// accumulators (tmem_full/tmem_empty) so the epilogue of tile i overlaps the
-// main loop of tile i+1.
+// CTA layout (384 threads, one CTA per SM, CTA pairs (cta_group::2) sharing one MMA,
+// persistent over output tiles):
+//   warp 0       TMA producer (one elected lane; wave-synchronised for the dW GEMMs)
+//   warp 1       MMA issuer (one elected lane of the pair's even CTA) + tcgen05.cp of
+//                the sparse metadata
+//   warp 2       TMEM allocator
+//   warps 4..11  epilogue (lane quarter = warp % 4, two warps per quarter alternating
+//                32-column chunks): token-major outputs on the fragment path
+//                (tcgen05.ld 16x256b -> bf16x2 -> stmatrix.trans -> TMA store),
+//                dW / feature-major outputs on the row path (tcgen05.ld 32x32b)
+// Pipelines: kStages smem slots (full/empty mbarriers) and, for one-slab tiles, two
+// TMEM accumulators (tmem_full/tmem_empty) so the epilogue of tile i overlaps the main
+// loop of tile i+1; two-slab tiles (kSlabs = 2) trade that overlap for 512-row tiles.
+// GemmShape::exp holds experiment flags for attribution studies (results invalid when
+// set; 0 in production).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
