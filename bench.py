@@ -43,6 +43,11 @@ CONFIGS = {
     # configs[3] at its N=16384 point
     "c4": dict(workload="large FFN d=12288 d_ff=49152 GELU, 16384 tokens (BASELINE.json configs[3])",
                d=12288, d_ff=49152, act="gelu", tokens=16384),
+    # configs[4]: GPT-2 large 2:4 pre-training step -- the 36-block residual FFN stack
+    # (_FFNStack, trainer.py:159-262), 16k tokens per rank, one dW all-reduce per block
+    "c5": dict(workload="GPT-2 large residual FFN stack: 36 x (d=1280 d_ff=5120 GELU), 16384 tokens/rank "
+                        "(BASELINE.json configs[4])",
+               d=1280, d_ff=5120, act="gelu", tokens=16384, layers=36),
 }
 REFRESH = 40
 DP_RESERVED_SMS = int(os.environ.get("S24_DP_RESERVED_SMS", "16"))  # SMs the dX GEMM leaves to NCCL (N > 1)
@@ -60,6 +65,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-dense", action="store_true")
     p.add_argument("--ref-tokens", type=int, default=64)
+    p.add_argument("--tokens", type=int, default=0, help="override the config's tokens per rank (C4 sweep)")
     return p.parse_args()
 
 
@@ -88,11 +94,14 @@ def run_reference(a, cfg):
         t0 = time.perf_counter()
         res = pool.map(_ref_worker, [(cfg, a.ref_tokens, steps, max(0, min(a.warmup, 1)))] * procs)
         wall = time.perf_counter() - t0
-    value = sum(r[0] for r in res)
+    layers = cfg.get("layers", 1)
+    # a stack of L identical blocks costs L block steps per token batch
+    value = sum(r[0] for r in res) / layers
     kind = res[0][2]["kind"]
     sample = (f"{procs} processes x {a.ref_tokens} tokens x {steps} steps of the {cfg['workload']} step "
               f"(fwd + bwd mvue=False + masked decay; mask search of both weights amortized /{REFRESH}); "
-              f"reference Cython kernels single-threaded per process")
+              f"reference Cython kernels single-threaded per process"
+              + (f"; one block timed, tokens/s divided by the {layers} blocks of the stack" if layers > 1 else ""))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": a.gpus,
         "steps": steps, "warmup": a.warmup, "ms_per_step": 1000.0 * a.ref_tokens * procs / value,
@@ -684,9 +693,17 @@ def run_e2e(a, cfg, w_in, bias, w2, dev, world, dist):
 
 def main():
     a = parse()
-    cfg = CONFIGS[a.config]
+    cfg = dict(CONFIGS[a.config])
+    if a.tokens:
+        cfg["tokens"] = a.tokens
+        cfg["workload"] = cfg["workload"].split(",")[0] + f", {a.tokens} tokens (token-count override)"
     if a.impl == "reference":
         run_reference(a, cfg)
+        return
+    if cfg.get("layers", 1) > 1:
+        from bench_stack import run_stack
+
+        run_stack(a, cfg)
         return
     run_ours(a, cfg)
 

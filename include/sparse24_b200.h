@@ -134,6 +134,26 @@ int s24_meta_flat(const uint8_t* idx, int64_t rows, int64_t cols, uint8_t* fwd_m
 /* E tiles (m x k logical) -> reference-layout nibbles (m x k/4) */
 int s24_e_to_flat(const uint8_t* e, int64_t m, int64_t k, uint8_t* meta, void* stream);
 
+/* ---- packed 2:4 storage of the API's packed route (Compressed24, spmm.py:38-147) ----
+ * Groups of four run along rows (colwise = 0: groups row-major) or down columns
+ * (colwise = 1: groups column-major); values hold the two kept entries of every group in
+ * group order, meta one nibble i0 | i1 << 2 (i0 < i1) per uint8.
+ * s24_pack24: compress (spmm.py:92-106) of w under the 0/1 mask `bits` (both rows x cols
+ * row-major; values copied verbatim in w's dtype, rows*cols/2 of them; meta rows*cols/4).
+ * Groups whose mask is not exactly two ones are counted into *bad (device int32, caller
+ * zeroes; -> FormatError, Mask24.validate sparsity.py:98-105).  w / vals / meta may be NULL
+ * (validation only).
+ * s24_unpack24: decompress / mask_of (spmm.py:109-135) into a dense row-major out (w's
+ * dtype) and / or a 0/1 mask (either may be NULL); groups with i0 >= i1 are counted into
+ * *bad (kept_indices, spmm.py:61-67).
+ * s24_flat_to_e: reference nibbles of a row-wise (m x k) operand -> E tiles (inverse of
+ * s24_e_to_flat), so a bf16 row-wise Compressed24 feeds s24_spmm as (vals, E). */
+int s24_pack24(const void* w, int dtype, const uint8_t* bits, int64_t rows, int64_t cols, int colwise, void* vals,
+               uint8_t* meta, int32_t* bad, void* stream);
+int s24_unpack24(const void* vals, int dtype, const uint8_t* meta, int64_t rows, int64_t cols, int colwise, void* out,
+                 uint8_t* bits, int32_t* bad, void* stream);
+int s24_flat_to_e(const uint8_t* meta, int64_t m, int64_t k, uint8_t* e, void* stream);
+
 /* ---- K3/K4: 2:4-sparse tcgen05 GEMM ----------------------------------------
  * D[m, n] = sum_k A[m, k] * B[n, k] with A 2:4-sparse (vals m x k/2 + E tiles).
  * Replaces kernels.spmm_colwise (_core.pyx:63-80) as driven by
@@ -189,6 +209,14 @@ int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int
 int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int64_t f, uint64_t state_hi, uint64_t state_lo,
                       uint64_t inc_hi, uint64_t inc_lo, int64_t gate_ff, uint16_t* vals, uint8_t* e,
                       uint8_t* pairs, int exact, void* stream);
+
+/* mvue_prune (sparsity.py:379-398) of a whole (rows x cols) matrix (bf16 / f32 / f64), groups
+ * along rows (colwise = 0, groups row-major) or down columns (colwise = 1, groups
+ * column-major): the exact float64 estimator and numpy PCG64 stream of s24_mvue_compress,
+ * stream index = group index.  out: dense float64 estimate (kept g / pi, zeros elsewhere);
+ * bits (optional): its 0/1 mask.  Bit-exact with the reference. */
+int s24_mvue_prune(const void* g, int dtype, int64_t rows, int64_t cols, int colwise, uint64_t state_hi,
+                   uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, double* out, uint8_t* bits, void* stream);
 
 /* sparse-A weight-gradient GEMM: D[m, n] fp32 = sum_k A~[m, k] B[n, k] + decay, with A~ an
  * MVUE-compressed operand (vals m x k/2, E tiles; k = tokens).  Replaces
@@ -251,6 +279,14 @@ int s24_adam_step(void* w, void* u, void* v, int state_dtype, const void* g, int
  * maps of nblocks 4x4 blocks, and to block_flips[i] (int32, optional) block i's count. */
 int s24_mask_flips(const uint8_t* idx_prev, const uint8_t* idx_curr, int64_t nblocks, unsigned long long* changed_bits,
                    int32_t* block_flips, void* stream);
+
+/* Retained-L1 gap of every 4x4 block (the block_gaps of block_flip_stats,
+ * optim.py:164-192): the best minus the second-best of the 90 pattern scores, each score
+ * summed in float64 over the pattern's kept positions in ascending order as
+ * kernels.pattern_scores does (_core.pyx:102-105), so the gaps are bit-exact; ties give 0.
+ * w: (rows, cols) row-major bf16 / f32 / f64, rows, cols % 4 == 0; gaps: (rows/4)(cols/4)
+ * float64 in block order. */
+int s24_block_gaps(const void* w, int dtype, int64_t rows, int64_t cols, double* gaps, void* stream);
 
 /* ---- standalone masked decay on an fp32 gradient (optim.py:105-114) -------- */
 int s24_masked_decay(float* g, const void* w, int w_dtype, const uint8_t* idx, int64_t rows, int64_t cols,

@@ -199,6 +199,41 @@ def decompress_rowwise(kept: np.ndarray, meta: np.ndarray, k: int) -> np.ndarray
     return out.reshape(m, k)
 
 
+def compress_groups(values: np.ndarray, bits: np.ndarray, colwise: bool):
+    """compress (spmm.py:92-106) in either direction: column-wise groups (column-major group
+    order, to_groups sparsity.py:45-54) are the row-wise groups of the transpose.  Returns the
+    flat (values, meta) buffers of Compressed24."""
+    v, b = (np.ascontiguousarray(values.T), np.ascontiguousarray(bits.T)) if colwise else (values, bits)
+    kept, meta = compress_rowwise(v, b)
+    return kept.reshape(-1), meta.reshape(-1)
+
+
+def decompress_groups(values: np.ndarray, meta: np.ndarray, shape, colwise: bool) -> np.ndarray:
+    """decompress (spmm.py:117-129) of flat buffers in either direction."""
+    rows, cols = shape
+    lead, grouped = (cols, rows) if colwise else (rows, cols)
+    out = decompress_rowwise(np.asarray(values).reshape(lead, grouped // 2),
+                             np.asarray(meta).reshape(lead, grouped // 4), grouped)
+    return np.ascontiguousarray(out.T) if colwise else out
+
+
+def mvue_prune(g: np.ndarray, colwise: bool, rng_seed: int):
+    """mvue_prune (sparsity.py:379-398): (dense float64 estimate, 0/1 mask)."""
+    arr = np.asarray(g, dtype=np.float64)
+    src = np.ascontiguousarray(arr.T) if colwise else arr
+    values, kept, _ = mvue_kept(src.reshape(-1, 4), rng_seed)
+    out = np.zeros((src.size // 4, 4))
+    bits = np.zeros((src.size // 4, 4), dtype=np.uint8)
+    rows = np.arange(src.size // 4)
+    for slot in (0, 1):
+        out[rows, kept[:, slot]] = values[:, slot]
+        bits[rows, kept[:, slot]] = 1
+    out, bits = out.reshape(src.shape), bits.reshape(src.shape)
+    if colwise:
+        return np.ascontiguousarray(out.T), np.ascontiguousarray(bits.T)
+    return out, bits
+
+
 # ---------------------------------------------------------------------------
 # gather plan + column-wise sparse product (gated_ffn.py:131-162, _core.pyx:63-80)
 
@@ -492,6 +527,28 @@ def block_flips(m_prev, m_curr) -> np.ndarray:
     a = blocks16(np.asarray(m_prev, dtype=np.int64))
     b = blocks16(np.asarray(m_curr, dtype=np.int64))
     return np.abs(b - a).sum(axis=1)
+
+
+def block_gaps(w) -> np.ndarray:
+    """Retained-L1 gap per 4x4 block of block_flip_stats (optim.py:186-190): best minus
+    second-best pattern score (np.partition's multiset order: ties give 0), scores from
+    pattern_scores on |w| in float64."""
+    _, pos = pattern_table()
+    scores, _ = pattern_scores(np.abs(blocks16(np.asarray(w, dtype=np.float64))), pos)
+    top2 = -np.partition(-scores, 1, axis=1)[:, :2]
+    return top2[:, 0] - top2[:, 1]
+
+
+def block_flip_stats(w_history):
+    """(block_flips int64, block_gaps float64) of block_flip_stats (optim.py:164-192) with
+    the default conv search as the mask function."""
+    if len(w_history) < 2:
+        raise ShapeError("need at least two weight snapshots")
+    masks = [transposable_search_conv(np.asarray(w, dtype=np.float64)) for w in w_history]
+    flips = np.zeros(blocks16(masks[0]).shape[0], dtype=np.int64)
+    for a, b in zip(masks, masks[1:]):
+        flips += block_flips(a, b)
+    return flips, block_gaps(w_history[-1])
 
 
 # ---------------------------------------------------------------------------

@@ -55,6 +55,12 @@ SIGNATURES = {
     "s24_set_reserved_sms": [_I],
     "s24_prune_compress_pair": [_P, _P, _I, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _I64, _P],
     "s24_prune_2of4": [_P, _I, _I64, _I64, _I, _P, _P],
+    "s24_block_gaps": [_P, _I, _I64, _I64, _P, _P],
+    "s24_pack24": [_P, _I, _P, _I64, _I64, _I, _P, _P, _P, _P],
+    "s24_unpack24": [_P, _I, _P, _I64, _I64, _I, _P, _P, _P, _P],
+    "s24_flat_to_e": [_P, _I64, _I64, _P, _P],
+    "s24_mvue_prune": [_P, _I, _I64, _I64, _I, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                       _P, _P, _P],
 }
 
 _lib = None

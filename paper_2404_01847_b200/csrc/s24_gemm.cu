@@ -69,7 +69,8 @@ struct EpiParams {
 struct GemmShape {
   int m, n, k;  // k logical
   int streamk;  // 1: stream-K -- every cluster owns an equal run of (tile, k-block) iterations and
-                //    partial tiles are summed with TMA add-reduce stores into the zeroed output
+                //    partial tiles are summed with TMA add-reduce stores into the zeroed output;
+                // S >= 2: lockstep split-K (WorkIter), partial tiles add-reduced the same way
   int group_m;  // M tiles per raster group: each group sweeps all N with its A panels L2-resident
   int wave_slot;  // >= 0: wave-synchronised schedule on counter slot g_wave_ctr[wave_slot] (see below)
   int exp;      // experiment flags (timing studies only, results invalid): 1 skip B loads, 2 skip metadata cp, 4 every tile loads the B tile of n = 0,
@@ -171,9 +172,13 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
 
 struct WorkIter {
   long long it, end;
-  int tile, stride;
+  int tile, stride, split;
   bool sk;
-  __device__ __forceinline__ WorkIter(bool streamk, int num_tiles, int num_kb, int cid, int ncl) : sk(streamk) {
+  // mode 0: one full-K tile per step; 1: stream-K; S >= 2: lockstep split-K -- every tile is
+  // cut into S equal K ranges, unit u = s * num_tiles + tile, so the clusters of one wave all
+  // sit at the same relative K offset of their range and keep sharing operand panels in L2
+  __device__ __forceinline__ WorkIter(int mode, int num_tiles, int num_kb, int cid, int ncl)
+      : split(mode >= 2 ? mode : 1), sk(mode == 1) {
     const long long t = static_cast<long long>(num_tiles) * num_kb;
     it = sk ? t * cid / ncl : 0;
     end = sk ? t * (cid + 1) / ncl : 0;
@@ -190,10 +195,11 @@ struct WorkIter {
       it += kb1 - kb0;
       return true;
     }
-    if (tile >= num_tiles) return false;
-    t = tile;
-    kb0 = 0;
-    kb1 = num_kb;
+    if (tile >= num_tiles * split) return false;
+    const int s = tile / num_tiles;
+    t = tile - s * num_tiles;
+    kb0 = static_cast<int>(static_cast<long long>(num_kb) * s / split);
+    kb1 = static_cast<int>(static_cast<long long>(num_kb) * (s + 1) / split);
     tile += stride;
     return true;
   }
@@ -965,6 +971,28 @@ static int use_streamk(int tiles, int clusters, int num_kb) {
   return !det && env == 1 ? 1 : 0;
 }
 
+// Lockstep split-K for the weight-gradient GEMMs (WorkIter mode 2): a tile count just above a
+// multiple of the CTA pairs leaves most of the last wave idle (C5 dW: 100 tiles on 74 pairs =
+// 2 tile-times for 1.35 of work); halving K per unit gives 200 units = 1.5 tile-times.  Unlike
+// stream-K every wave stays at one K offset (panels shared in L2), and with two addends onto
+// the zeroed output the fp32 result is order-independent (a + b = b + a), so it stays
+// deterministic.  Taken when it shortens the schedule by >= 10 % and each half keeps K >= 4096.
+// S24_SPLITK=0/2 overrides.
+static int use_splitk(int tiles, int clusters, int num_kb, int kb_min) {
+  static const int env = getenv("S24_SPLITK") ? atoi(getenv("S24_SPLITK")) : -1;
+  if (env == 0 || env == 1) return 0;
+  if (env >= 2) return num_kb >= 2 ? 2 : 0;
+  if (clusters <= 0 || num_kb < 2 * kb_min) return 0;
+  const double t1 = static_cast<double>((tiles + clusters - 1) / clusters);
+  const double t2 = static_cast<double>((2 * tiles + clusters - 1) / clusters) / 2.0;
+  return t2 <= 0.9 * t1 ? 2 : 0;
+}
+
+static int dw_clusters() {
+  const int sms = g_reserved_sms > 0 ? std::max(2, num_sms() - g_reserved_sms) : num_sms();
+  return sms / 2;
+}
+
 // Wave-synchronised schedule (g_wave_ctr): on for the dW GEMMs (panels of K = tokens, far
 // larger than L2), S24_WAVESYNC=0/1 turns it off / on for every GEMM.  Slot = stream hash.
 static int wave_slot(void* stream, bool dflt) {
@@ -1077,7 +1105,8 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
   }
   int cap = max_clusters;
   if (g_reserved_sms > 0) cap = std::max(1, std::min(cap, (num_sms() - g_reserved_sms) / kCS));
-  const int clusters = (shp.streamk || tiles > cap) ? cap : tiles;
+  const int units = shp.streamk >= 2 ? tiles * shp.streamk : tiles;
+  const int clusters = (shp.streamk == 1 || units > cap) ? cap : units;
   if (clusters <= 0) return S24_OK;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * kCS);
@@ -1303,7 +1332,11 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   if (int rc = make_map(&md, d, n, m, ldd, 32, 16, kMapF32Sw128)) return rc;  // 16-row store boxes
   const int clusters = num_sms() / (pair ? 2 : 1);
   const int tiles = static_cast<int>((m / (pair ? 256 : 128)) * (n / BN));
-  const int streamk = use_streamk(tiles, clusters, static_cast<int>(k / 64));
+  const bool slabs = pair && a_mn && b_mn && m % 512 == 0 && use_dw_slabs(m, n, k);
+  int streamk = use_streamk(tiles, clusters, static_cast<int>(k / 64));
+  if (!streamk)
+    streamk = use_splitk(slabs ? static_cast<int>((m / 512) * (n / 256)) : tiles,
+                         pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 64), 64);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (streamk) {
     cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
@@ -1313,15 +1346,14 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   static const int env_dw = getenv("S24_GROUP_M_DW") ? atoi(getenv("S24_GROUP_M_DW")) : 8;
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), streamk,
                 static_cast<int>(m / tile_m) < env_dw ? static_cast<int>(m / tile_m) : env_dw,
-                streamk ? -1 : wave_slot(stream, true), exp_flags()};
+                streamk == 1 ? -1 : wave_slot(stream, true), exp_flags()};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
 
 #define S24_DW(AMN, BMN, BNV, CG)                                                                      \
   return launch_gemm<false, AMN, BMN, BNV, stages_for<Cfg<false, AMN, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
                      kEpiDw>(ma, mb, me, md, md, md, shp, ep, st)
-  if (pair && a_mn && b_mn && m % 512 == 0 && use_dw_slabs(m, n, k)) {
+  if (slabs) {
     using CS = Cfg<false, true, true, 256, 1, 2, 1, 2>;
-    shp.wave_slot = streamk ? -1 : wave_slot(stream, true);
     return launch_gemm<false, true, true, 256, stages_for<CS::STAGE_BYTES>(), 2, kEpiDw, false, 1, 2>(
         ma, mb, me, md, md, md, shp, ep, st);
   }
@@ -1374,13 +1406,14 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
   if (int rc = make_map(&md, d, n, m, ldd, 32, 16, kMapF32Sw128)) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int sk_tiles = static_cast<int>((m / (pair ? 256 : 128)) * (n / (wide ? 256 : 128)));
-  const int streamk = use_streamk(sk_tiles, num_sms() / (pair ? 2 : 1), static_cast<int>(k / 128));
+  int streamk = use_streamk(sk_tiles, num_sms() / (pair ? 2 : 1), static_cast<int>(k / 128));
+  if (!streamk) streamk = use_splitk(sk_tiles, pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 128), 32);
   if (streamk) {
     cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   }
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), streamk, 8,
-                streamk ? -1 : wave_slot(stream, true), 0};
+                streamk == 1 ? -1 : wave_slot(stream, true), 0};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
   // BN = 256 with one TMEM accumulator (256 + 4 metadata columns): K = tokens is long, so the
   // un-overlapped epilogue is a small share; the B half per CTA is exactly two 64-wide chunks

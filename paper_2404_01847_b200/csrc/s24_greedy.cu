@@ -1,4 +1,5 @@
-// the paper's comparators for the transposable mask search --
+// the paper's comparators for the transposable mask search (and, for
+// §8(f) #3, the per-block score gaps of block_flip_stats) --
 //   transposable_search_greedy (sparsity.py:229-238 -> kernels.greedy_masks, _core.pyx:139-219):
 //     per 4x4 block, scan cells by descending |w| (lowest flat index on ties), pick a cell while
 //     its block row and column hold fewer than two picks; a stranded 7-pick block is completed
@@ -135,6 +136,43 @@ __global__ void __launch_bounds__(256) prune2of4_kernel(const T* __restrict__ w,
   }
 }
 
+// retained-L1 gap per block: best - second best of the 90 float64 pattern scores, each the
+// ascending-position sequential sum of kernels.pattern_scores (_core.pyx:102-105); the
+// second best is taken over the multiset of scores (np.partition), so ties give 0
+template <typename T>
+__global__ void __launch_bounds__(256) gaps_kernel(const T* __restrict__ w, int64_t rows, int64_t cols,
+                                                   double* __restrict__ gaps) {
+  const int64_t bc = cols >> 2, nb = (rows >> 2) * bc;
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < nb;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r0 = 4 * (b / bc), c0 = 4 * (b % bc);
+    double a[16];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) a[4 * r + c] = mag<T>(w[(r0 + r) * cols + c0 + c]);
+    double b1 = -INFINITY, b2 = -INFINITY;
+    for (int k = 0; k < 90; ++k) {
+      const uint32_t bits = c_gr_pat_bits[k];
+      double s = 0.0;
+      bool first = true;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if ((bits >> i) & 1) {
+          s = first ? a[i] : __dadd_rn(s, a[i]);
+          first = false;
+        }
+      if (s > b1) {
+        b2 = b1;
+        b1 = s;
+      } else if (s > b2) {
+        b2 = s;
+      }
+    }
+    gaps[b] = __dsub_rn(b1, b2);
+  }
+}
+
 static int grid_for_work(int64_t work) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -179,4 +217,19 @@ extern "C" int s24_prune_2of4(const void* w, int dtype, int64_t rows, int64_t co
   else if (dtype == S24_F64) prune2of4_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(w), rows, cols, colwise, bits);
   else return s24_set_error(S24_ERR_UNSUPPORTED, "unsupported weight dtype %d", dtype);
   return s24_check_launch("prune_2of4");
+}
+
+extern "C" int s24_block_gaps(const void* w, int dtype, int64_t rows, int64_t cols, double* gaps, void* stream) {
+  S24_REQUIRE(w && gaps, S24_ERR_ARG, "NULL operand");
+  S24_REQUIRE(rows >= 0 && cols >= 0 && rows % 4 == 0 && cols % 4 == 0, S24_ERR_SHAPE,
+              "shape (%lld, %lld) not divisible into 4x4 blocks", (long long)rows, (long long)cols);
+  const int64_t nb = (rows / 4) * (cols / 4);
+  if (nb == 0) return S24_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = grid_for_work(nb);
+  if (dtype == S24_BF16) gaps_kernel<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(w), rows, cols, gaps);
+  else if (dtype == S24_F32) gaps_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(w), rows, cols, gaps);
+  else if (dtype == S24_F64) gaps_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(w), rows, cols, gaps);
+  else return s24_set_error(S24_ERR_UNSUPPORTED, "unsupported weight dtype %d", dtype);
+  return s24_check_launch("block_gaps");
 }

@@ -303,9 +303,103 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
   }
 }
 
+// mvue_prune (sparsity.py:379-398) of any (rows x cols) matrix along `colwise`: the same exact
+// float64 estimator and PCG64 stream as the K8 tile kernel, with the reference's group order
+// (to_groups: row-wise groups row-major, column-wise groups column-major) as the stream index.
+// Output: the dense float64 estimate (kept g / pi, zeros elsewhere) and its 0/1 mask.  Each
+// thread jumps ahead once and walks kMvueRun consecutive groups.
+constexpr int kMvueRun = 16;
+
+template <typename T>
+__device__ __forceinline__ double as_f64(T x);
+template <>
+__device__ __forceinline__ double as_f64<uint16_t>(uint16_t x) {
+  return static_cast<double>(bf16_to_f32(x));
+}
+template <>
+__device__ __forceinline__ double as_f64<float>(float x) { return static_cast<double>(x); }
+template <>
+__device__ __forceinline__ double as_f64<double>(double x) { return x; }
+
+template <typename T>
+__global__ void __launch_bounds__(256) mvue_prune_kernel(const T* __restrict__ g, int64_t rows, int64_t cols,
+                                                         int colwise, const __grid_constant__ MvueRng rng,
+                                                         double* __restrict__ out, uint8_t* __restrict__ bits) {
+  const int64_t ng = rows * cols / 4;
+  const int64_t first = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * kMvueRun;
+  if (first >= ng) return;
+  U128 st = pcg_advance(rng, static_cast<uint64_t>(first));
+  const int64_t last = min(first + kMvueRun, ng);
+  for (int64_t gi = first; gi < last; ++gi) {
+    int64_t e[4];
+    if (colwise) {
+      const int64_t c = gi / (rows >> 2), r0 = 4 * (gi % (rows >> 2));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) e[k] = (r0 + k) * cols + c;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) e[k] = 4 * gi + k;
+    }
+    double gv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) gv[k] = as_f64<T>(g[e[k]]);
+    const double u = pcg_uniform(st, rng.inc);
+    double v0, v1;
+    const int idx = mvue_group(gv, u, v0, v1);
+    const int i0 = idx < 3 ? 0 : (idx < 5 ? 1 : 2);
+    const int i1 = idx == 0 ? 1 : (idx == 1 || idx == 3) ? 2 : 3;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      out[e[k]] = k == i0 ? v0 : (k == i1 ? v1 : 0.0);
+      if (bits) bits[e[k]] = (k == i0 || k == i1) ? 1 : 0;
+    }
+  }
+}
+
+static void mvue_rng_tables(MvueRng& rng, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo) {
+  rng.state = U128{state_hi, state_lo};
+  rng.inc = U128{inc_hi, inc_lo};
+  unsigned __int128 m = (static_cast<unsigned __int128>(kPcgMultHi) << 64) | kPcgMultLo;
+  unsigned __int128 pl = (static_cast<unsigned __int128>(inc_hi) << 64) | inc_lo;
+  for (int i = 0; i < 40; ++i) {
+    rng.mult[i] = U128{static_cast<uint64_t>(m >> 64), static_cast<uint64_t>(m)};
+    rng.plus[i] = U128{static_cast<uint64_t>(pl >> 64), static_cast<uint64_t>(pl)};
+    pl = (m + 1) * pl;
+    m = m * m;
+  }
+}
+
 }  // namespace s24
 
 using namespace s24;
+
+extern "C" int s24_mvue_prune(const void* g, int dtype, int64_t rows, int64_t cols, int colwise, uint64_t state_hi,
+                              uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, double* out, uint8_t* bits,
+                              void* stream) {
+  S24_REQUIRE(g && out, S24_ERR_ARG, "NULL pointer");
+  S24_REQUIRE(rows >= 0 && cols >= 0, S24_ERR_SHAPE, "negative shape");
+  if (colwise)
+    S24_REQUIRE(rows % 4 == 0, S24_ERR_SHAPE, "rows=%lld not divisible by 4 for column-wise groups", (long long)rows);
+  else
+    S24_REQUIRE(cols % 4 == 0, S24_ERR_SHAPE, "cols=%lld not divisible by 4 for row-wise groups", (long long)cols);
+  const int64_t ng = rows * cols / 4;
+  if (ng == 0) return S24_OK;
+  S24_REQUIRE(static_cast<double>(ng) < 1099511627776.0, S24_ERR_SHAPE, "MVUE stream index exceeds the 2^40 jump table");
+  MvueRng rng;
+  mvue_rng_tables(rng, state_hi, state_lo, inc_hi, inc_lo);
+  const int64_t threads = (ng + kMvueRun - 1) / kMvueRun;
+  const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == S24_BF16)
+    mvue_prune_kernel<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(g), rows, cols, colwise, rng, out, bits);
+  else if (dtype == S24_F32)
+    mvue_prune_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(g), rows, cols, colwise, rng, out, bits);
+  else if (dtype == S24_F64)
+    mvue_prune_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(g), rows, cols, colwise, rng, out, bits);
+  else
+    return s24_set_error(S24_ERR_UNSUPPORTED, "unsupported dtype %d", dtype);
+  return s24_check_launch("mvue_prune");
+}
 
 extern "C" int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int64_t f, uint64_t state_hi,
                                  uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t gate_ff,
@@ -318,16 +412,7 @@ extern "C" int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int6
               "gradient rows must be 16-byte aligned");
   if (gate_ff > 0) S24_REQUIRE(f == 2 * gate_ff && gate_ff % 16 == 0, S24_ERR_SHAPE, "gated MVUE: f must be 2 d_ff");
   MvueRng rng;
-  rng.state = U128{state_hi, state_lo};
-  rng.inc = U128{inc_hi, inc_lo};
-  unsigned __int128 m = (static_cast<unsigned __int128>(kPcgMultHi) << 64) | kPcgMultLo;
-  unsigned __int128 pl = (static_cast<unsigned __int128>(inc_hi) << 64) | inc_lo;
-  for (int i = 0; i < 40; ++i) {
-    rng.mult[i] = U128{static_cast<uint64_t>(m >> 64), static_cast<uint64_t>(m)};
-    rng.plus[i] = U128{static_cast<uint64_t>(pl >> 64), static_cast<uint64_t>(pl)};
-    pl = (m + 1) * pl;
-    m = m * m;
-  }
+  mvue_rng_tables(rng, state_hi, state_lo, inc_hi, inc_lo);
   S24_REQUIRE(static_cast<double>(f) * static_cast<double>(n / 4) < 1099511627776.0, S24_ERR_SHAPE,
               "MVUE stream index exceeds the 2^40 jump table");
   S24_REQUIRE(exact || static_cast<double>(f) * static_cast<double>(n / 4) < 4294967296.0, S24_ERR_SHAPE,

@@ -53,6 +53,13 @@ def masked_decay_gradient(g: torch.Tensor, w: torch.Tensor, m, lambda_w: float) 
     return g.to(torch.float32) + lambda_w * ((1 - m.to(torch.float32)) * w.to(torch.float32))
 
 
+def srste_weight_decay(w_next_base: torch.Tensor, w: torch.Tensor, m, lr: float, lambda_w: float) -> torch.Tensor:
+    """w_next_base - lr lambda_w (1 - m) w (optim.py:117-125): the decay at the update site.
+    Same kernel as masked_decay_gradient with the coefficient -lr lambda_w (fp32 result);
+    the training step fuses it into the Adam kernel (DecayMode.ON_WEIGHTS)."""
+    return masked_decay_gradient(w_next_base, w, m, -lr * lambda_w)
+
+
 # ---------------------------------------------------------------------------
 # optimizer step and mask statistics (SURVEY.md section 8(f) #2), one fused kernel each
 
@@ -140,6 +147,52 @@ def flip_rate(m_prev: TransposableMask, m_curr: TransposableMask, d: int | None 
     if d is None:
         d = m_prev.shape[0] * m_prev.shape[1]
     return float(n.item()) / d
+
+
+@dataclass
+class FlipTrace:
+    """Per-step flip rates plus per-block oscillation statistics (optim.py:85-91)."""
+
+    rates: torch.Tensor | None = None
+    block_flips: torch.Tensor | None = None  # cumulative flips per 4x4 block, int64, block order
+    block_gaps: torch.Tensor | None = None  # best minus second-best pattern score, float64
+
+
+def block_flip_stats(w_history, table=None, mask_fn=None) -> FlipTrace:
+    """Cumulative mask flips and retained-L1 gap per 4x4 block (optim.py:164-192) on the GPU.
+
+    Flips: K1 search of every snapshot (or `mask_fn(w) -> TransposableMask`) and the
+    per-block changed-bit counts of consecutive masks (s24_mask_flips).  Gaps: best minus
+    second-best of the 90 float64 pattern scores on the final snapshot (s24_block_gaps),
+    bit-exact with the reference.  `table` is accepted for signature compatibility (only
+    the canonical table is supported)."""
+    from .sparsity import transposable_search_conv
+
+    snaps = list(w_history)
+    if len(snaps) < 2:
+        raise ShapeError("need at least two weight snapshots")
+    if mask_fn is None:
+        mask_fn = transposable_search_conv
+    last = snaps[-1]
+    if last.dim() != 2:
+        raise ShapeError(f"expected 2-D snapshots, got ndim={last.dim()}")
+    C.require_cuda(last)
+    rows, cols = last.shape
+    if rows % 4 or cols % 4:
+        raise ShapeError(f"shape {(rows, cols)} not divisible into 4x4 blocks")
+    nb = (rows // 4) * (cols // 4)
+    counts = torch.zeros(nb, dtype=torch.int32, device=last.device)
+    prev = mask_fn(snaps[0])
+    for w in snaps[1:]:
+        if tuple(w.shape) != (rows, cols):
+            raise ShapeError("snapshots differ in shape")
+        curr = mask_fn(w)
+        mask_flips(prev, curr, counts)
+        prev = curr
+    last = last.contiguous()
+    gaps = torch.empty(nb, dtype=torch.float64, device=last.device)
+    C.call("s24_block_gaps", last.data_ptr(), C.dtype_code(last), rows, cols, gaps.data_ptr(), C.stream_of(last))
+    return FlipTrace(rates=torch.zeros(0, dtype=torch.float64), block_flips=counts.to(torch.int64), block_gaps=gaps)
 
 
 # ---------------------------------------------------------------------------

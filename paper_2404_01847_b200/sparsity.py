@@ -122,6 +122,9 @@ class TransposableMask:
         idx_t = lut[self.idx.t().long()].contiguous()
         return TransposableMask(idx_t, (self._shape[1], self._shape[0]))
 
+    def to_mask24(self, direction) -> "Mask24":
+        return Mask24(self.bits, direction)
+
     def retained_l1(self, w: torch.Tensor) -> float:
         return float((w.abs().double() * self.bits.double()).sum().item())
 
@@ -174,14 +177,67 @@ def transposable_search_greedy(w: torch.Tensor) -> TransposableMask:
     return TransposableMask(idx, (rows, cols))
 
 
-@dataclass
-class SparseEstimate:
-    """A 2:4-pruned matrix: the kept values in place (zeros elsewhere) and its 0/1 mask with
-    the group direction (the reference's SparseEstimate / Mask24, sparsity.py:82-108)."""
+class Mask24:
+    """0/1 mask with exactly two ones per aligned group of four along `direction`
+    (sparsity.py:85-108): row-wise groups run along rows, column-wise down columns."""
 
-    values: torch.Tensor
-    bits: torch.Tensor
-    direction: "Direction"
+    def __init__(self, bits: torch.Tensor, direction=None):
+        from .matrix import Direction
+
+        self.bits = bits if bits.dtype == torch.uint8 else bits.to(torch.uint8)
+        self.direction = direction or Direction.ROW_WISE
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return tuple(self.bits.shape)
+
+    def validate(self) -> None:
+        """FormatError unless every group holds exactly two 0/1 ones (sparsity.py:98-105),
+        checked by the pack kernel in validation-only mode."""
+        from .matrix import Direction
+
+        if self.bits.dim() != 2:
+            raise FormatError("mask must be 2-D")
+        rows, cols = self.bits.shape
+        colwise = self.direction is Direction.COL_WISE
+        if colwise and rows % 4:
+            raise ShapeError(f"rows={rows} not divisible by 4 for column-wise groups")
+        if not colwise and cols % 4:
+            raise ShapeError(f"cols={cols} not divisible by 4 for row-wise groups")
+        C.require_cuda(self.bits)
+        b = self.bits.contiguous()
+        bad = torch.zeros(1, dtype=torch.int32, device=b.device)
+        C.call("s24_pack24", None, C.S24_BF16, b.data_ptr(), rows, cols, int(colwise), None, None, bad.data_ptr(),
+               C.stream_of(b))
+        if int(bad.item()):
+            raise FormatError("every group of 4 must contain exactly 2 ones")
+
+
+class SparseEstimate:
+    """A pruned matrix (zeros at dropped positions) with its Mask24 (sparsity.py:148-158).
+    `bits` / `direction` are shorthands for the mask's."""
+
+    def __init__(self, values: torch.Tensor, mask: Mask24):
+        if tuple(values.shape) != tuple(mask.bits.shape):
+            raise ShapeError("values and mask shapes differ")
+        self.values = values
+        self.mask = mask
+
+    @property
+    def bits(self) -> torch.Tensor:
+        return self.mask.bits
+
+    @property
+    def direction(self):
+        return self.mask.direction
+
+
+def apply_mask(w: torch.Tensor, mask) -> torch.Tensor:
+    """Elementwise product of a matrix with a binary mask (sparsity.py:241-251)."""
+    bits = mask.bits if isinstance(mask, (Mask24, TransposableMask)) else mask
+    if tuple(w.shape) != tuple(bits.shape):
+        raise ShapeError(f"mask shape {tuple(bits.shape)} != matrix shape {tuple(w.shape)}")
+    return w * bits.to(w.dtype)
 
 
 def prune_2of4(m: torch.Tensor, direction=None) -> SparseEstimate:
@@ -199,4 +255,35 @@ def prune_2of4(m: torch.Tensor, direction=None) -> SparseEstimate:
     bits = torch.empty((rows, cols), dtype=torch.uint8, device=m.device)
     C.call("s24_prune_2of4", m.data_ptr(), C.dtype_code(m), rows, cols, int(direction is Direction.COL_WISE),
            bits.data_ptr(), C.stream_of(m))
-    return SparseEstimate(m * bits.to(m.dtype), bits, direction)
+    return SparseEstimate(m * bits.to(m.dtype), Mask24(bits, direction))
+
+
+# kept index pairs of a group, lexicographic (sparsity.py:283-285)
+MVUE_PAIRS = np.array([(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)], dtype=np.int64)
+
+
+def mvue_prune(g: torch.Tensor, direction=None, rng_seed: int = 0) -> SparseEstimate:
+    """Unbiased stochastic 2-of-4 sparsifier (sparsity.py:379-398) on the GPU: per group the
+    water-filled inclusion probabilities, the greedy pair distribution, one uniform of numpy's
+    default_rng(rng_seed) stream per group (group order of to_groups) and the kept values
+    g / pi, all in float64 -- bit-exact with the reference.  Values come back float64."""
+    from .engine import pcg64_state
+    from .matrix import Direction
+
+    direction = direction or Direction.ROW_WISE
+    if g.dim() != 2:
+        raise ShapeError(f"expected a 2-D operand, got ndim={g.dim()}")
+    C.require_cuda(g)
+    rows, cols = g.shape
+    colwise = direction is Direction.COL_WISE
+    if colwise and rows % 4:
+        raise ShapeError(f"rows={rows} not divisible by 4 for column-wise groups")
+    if not colwise and cols % 4:
+        raise ShapeError(f"cols={cols} not divisible by 4 for row-wise groups")
+    g = g.contiguous()
+    out = torch.empty((rows, cols), dtype=torch.float64, device=g.device)
+    bits = torch.empty((rows, cols), dtype=torch.uint8, device=g.device)
+    sh, sl, ih, il = pcg64_state(rng_seed)
+    C.call("s24_mvue_prune", g.data_ptr(), C.dtype_code(g), rows, cols, int(colwise), sh, sl, ih, il,
+           out.data_ptr(), bits.data_ptr(), C.stream_of(g))
+    return SparseEstimate(out, Mask24(bits, direction))

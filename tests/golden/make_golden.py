@@ -323,6 +323,64 @@ def train_golden():
     np.savez_compressed(os.path.join(HERE, "train_golden.npz"), **out)
 
 
+PACKED_SHAPES = {"a": (8, 16), "b": (96, 160), "c": (36, 44)}
+
+
+def packed_golden():
+    """The packed route of the reference (spmm.py: compress / decompress / mask_of / spmm /
+    spmm_right), mvue_prune in both directions and block_flip_stats' gaps ->
+    packed_golden.npz."""
+    s24 = import_reference()
+    from sparse24.matrix import Direction
+    from sparse24.optim import block_flip_stats
+    from sparse24.sparsity import mvue_prune, prune_2of4
+    from sparse24.spmm import compress, decompress, mask_of, spmm, spmm_right
+
+    out = {}
+    for name, shape in PACKED_SHAPES.items():
+        w = o.round_bf16(o.det_normal(shape, 800 + len(name) + shape[0]))
+        out[f"{name}.w"] = w
+        for dname, d in (("row", Direction.ROW_WISE), ("col", Direction.COL_WISE)):
+            est = prune_2of4(w, d)
+            c = compress(est)
+            out[f"{name}.{dname}.bits"] = est.mask.bits.astype(np.uint8)
+            out[f"{name}.{dname}.values"] = c.values
+            out[f"{name}.{dname}.meta"] = c.meta
+            out[f"{name}.{dname}.dense"] = decompress(c).data
+            assert np.array_equal(mask_of(c).bits, est.mask.bits)
+    # products through the packed route (A row-wise 96 x 160, B column-wise 160 x 96)
+    w = out["b.w"]
+    a_c = compress(prune_2of4(w, Direction.ROW_WISE))
+    rhs = o.round_bf16(o.det_normal((160, 40), 811))
+    out["spmm.rhs"] = rhs
+    out["spmm.out"] = spmm(a_c, rhs).data
+    lhs = o.round_bf16(o.det_normal((40, 160), 812))
+    b_c = compress(prune_2of4(np.ascontiguousarray(w.T), Direction.COL_WISE))  # 160 x 96 column-wise
+    out["spmm_right.lhs"] = lhs
+    out["spmm_right.out"] = spmm_right(lhs, b_c).data
+    # mvue_prune
+    for i, (shape, seed) in enumerate(mvue_cases()):
+        g = mvue_input(shape, i)
+        out[f"mvue{i}.g"] = g
+        out[f"mvue{i}.seed"] = np.array(seed, dtype=np.uint64)
+        for dname, d in (("row", Direction.ROW_WISE), ("col", Direction.COL_WISE)):
+            est = mvue_prune(g, d, seed)
+            out[f"mvue{i}.{dname}.values"] = est.values
+            out[f"mvue{i}.{dname}.bits"] = est.mask.bits.astype(np.uint8)
+    # block_flip_stats over three snapshots, and the tie corpus' gaps
+    wa = o.det_normal((64, 96), 830)
+    wb = wa + o.det_normal((64, 96), 831) * 0.3
+    wc = wb + o.det_normal((64, 96), 832) * 0.3
+    tr = block_flip_stats([wa, wb, wc])
+    out["flip3.wa"], out["flip3.wb"], out["flip3.wc"] = wa, wb, wc
+    out["flip3.block_flips"], out["flip3.block_gaps"] = tr.block_flips, tr.block_gaps
+    ties = (o._splitmix64(64 * 64, 833) % np.uint64(3)).astype(np.float64).reshape(64, 64)
+    tt = block_flip_stats([ties, ties])
+    out["ties.w"], out["ties.block_gaps"] = ties, tt.block_gaps
+    np.savez_compressed(os.path.join(HERE, "packed_golden.npz"), **out)
+    print("packed golden:", len(out), "arrays")
+
+
 def mvue_cases():
     return [((16, 64), 0), ((32, 128), 7), ((8, 256), 2 ** 40 + 3), ((128, 64), (12345 << 2) ^ 2)]
 
@@ -342,8 +400,11 @@ if __name__ == "__main__":
         comparator_golden()
     elif sys.argv[1:] == ["train"]:
         train_golden()
+    elif sys.argv[1:] == ["packed"]:
+        packed_golden()
     else:
         main()
         optim_golden()
         comparator_golden()
         train_golden()
+        packed_golden()

@@ -352,3 +352,72 @@ def test_reserved_sms_leave_results_unchanged():
     finally:
         C.call("s24_set_reserved_sms", 0)
     assert torch.equal(full, part)
+
+
+@pytest.mark.parametrize("gate_ff", [0, 1280])
+def test_dense_dw_gemm_c5_shape_lockstep_splitk(gate_ff):
+    """C5-shaped dW (100 tiles on 74 CTA pairs): the lockstep split-K schedule (two K halves
+    add-reduced into the zeroed output, the decay added once) against fp32, and bit-identical
+    across repeated launches (two addends onto zero: order-independent)."""
+    from paper_2404_01847_b200 import engine as E
+    from paper_2404_01847_b200.engine import gemm_dw
+    from paper_2404_01847_b200 import transposable_search_conv
+
+    m, n, k = (2560, 1280, 16384) if gate_ff else (1280, 5120, 16384)
+    w = torch.randn(m, n, device="cuda").bfloat16()
+    mask = transposable_search_conv(w)
+    a = torch.randn(k, m, device="cuda").bfloat16()
+    b = torch.randn(k, n, device="cuda").bfloat16()
+    lam = 0.5
+    outs = []
+    for _ in range(2):
+        out = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+        if gate_ff:
+            p = torch.arange(m, device="cuda")
+            orig = torch.where(p % 32 < 16, 16 * (p // 32) + p % 32, gate_ff + 16 * (p // 32) + p % 32 - 16)
+            a_perm = a[:, orig].contiguous()
+            op = E.CompressedOperand.empty(m, n, "cuda", perm_ff=gate_ff)
+            E.search_compress(w, op)
+            gemm_dw(a_perm, True, b, True, m, n, k, out, w, op.idx, lam, gate_ff=gate_ff)
+        else:
+            gemm_dw(a, True, b, True, m, n, k, out, w, mask.idx, lam)
+        outs.append(out)
+    ref = a.float().t() @ b.float() + lam * (1 - mask.bits.float()) * w.float()
+    assert torch.isfinite(outs[0]).all()
+    assert normwise_rel(outs[0].cpu(), ref.cpu()) < 2e-3
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_dw_gemms_splitk_forced_small_shapes():
+    """S24_SPLITK=2 forces the lockstep split-K schedule on every dW GEMM (dense and the MVUE
+    sparse-A one), including odd k-block counts (uneven halves) and the decay."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, sys; sys.path.insert(0, %r)\n"
+        "from paper_2404_01847_b200 import engine as E, transposable_search_conv, _capi as C\n"
+        "for m, n, k in [(128, 128, 128), (256, 512, 320), (384, 256, 1216), (512, 768, 4096)]:\n"
+        "    w = torch.randn(m, n, device='cuda').bfloat16(); mk = transposable_search_conv(w)\n"
+        "    a = torch.randn(k, m, device='cuda').bfloat16(); b = torch.randn(k, n, device='cuda').bfloat16()\n"
+        "    out = torch.full((m, n), float('nan'), device='cuda')\n"
+        "    E.gemm_dw(a, True, b, True, m, n, k, out, w, mk.idx, 0.5)\n"
+        "    ref = a.float().t() @ b.float() + 0.5 * (1 - mk.bits.float()) * w.float()\n"
+        "    e = float((out - ref).norm() / ref.norm())\n"
+        "    assert e < 2e-3, (m, n, k, e)\n"
+        "for f, n, d in [(256, 256, 128), (512, 1024, 256)]:\n"
+        "    g = torch.randn(n, f, device='cuda').bfloat16(); bd = torch.randn(n, d, device='cuda').bfloat16()\n"
+        "    vals, e_, _ = E.mvue_compress(g, 7, exact=False)\n"
+        "    out = torch.full((f, d), float('nan'), device='cuda')\n"
+        "    E.spmm_dw(vals, e_, f, n, bd, True, d, out)\n"
+        "    meta = torch.empty((f, n // 4), dtype=torch.uint8, device='cuda')\n"
+        "    C.call('s24_e_to_flat', e_.data_ptr(), f, n, meta.data_ptr(), C.stream_of(meta))\n"
+        "    sp = torch.empty((f, n), dtype=torch.bfloat16, device='cuda'); bad = torch.zeros(1, dtype=torch.int32, device='cuda')\n"
+        "    C.call('s24_unpack24', vals.data_ptr(), 0, meta.data_ptr(), f, n, 0, sp.data_ptr(), 0, bad.data_ptr(), C.stream_of(meta))\n"
+        "    dense = sp.float() @ bd.float()\n"
+        "    e = float((out - dense).norm() / dense.norm())\n"
+        "    assert e < 2e-3, (f, n, d, e)\n"
+        "print('ok')\n" % os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+    env = dict(os.environ, S24_SPLITK="2")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

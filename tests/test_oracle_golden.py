@@ -185,3 +185,49 @@ def test_greedy_and_prune2of4_oracle_match_reference(name):
     assert np.array_equal(o.idx_to_bits(gd[f"{name}.greedy_idx"]), bits)
     assert np.array_equal(o.prune_2of4_bits(w), gd[f"{name}.prune_row"])
     assert np.array_equal(o.prune_2of4_bits(w, colwise=True), gd[f"{name}.prune_col"])
+
+
+def _packed_golden():
+    return dict(np.load(os.path.join(GOLDEN, "packed_golden.npz")))
+
+
+@pytest.mark.parametrize("name", ["a", "b", "c"])
+@pytest.mark.parametrize("colwise", [False, True])
+def test_packed_format_oracle_matches_reference(name, colwise):
+    """compress / decompress (spmm.py:92-129) restated == the reference in both directions."""
+    gd = _packed_golden()
+    d = "col" if colwise else "row"
+    w, bits = gd[f"{name}.w"], gd[f"{name}.{d}.bits"]
+    assert np.array_equal(o.prune_2of4_bits(w, colwise=colwise), bits)
+    vals, meta = o.compress_groups(w * bits, bits, colwise)
+    assert np.array_equal(vals, gd[f"{name}.{d}.values"]) and np.array_equal(meta, gd[f"{name}.{d}.meta"])
+    assert np.array_equal(o.decompress_groups(vals, meta, w.shape, colwise), gd[f"{name}.{d}.dense"])
+
+
+def test_packed_products_oracle_matches_reference():
+    """spmm / spmm_right (spmm.py:165-190) are the dense products of the decompressed operands."""
+    gd = _packed_golden()
+    w, bits = gd["b.w"], gd["b.row.bits"]
+    dense = o.decompress_groups(*o.compress_groups(w * bits, bits, False), w.shape, False)
+    np.testing.assert_allclose(dense @ gd["spmm.rhs"], gd["spmm.out"], rtol=1e-12, atol=1e-12)
+    bt = o.prune_2of4_bits(np.ascontiguousarray(w.T), colwise=True)
+    np.testing.assert_allclose(gd["spmm_right.lhs"] @ (w.T * bt), gd["spmm_right.out"], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("i", range(4))
+def test_mvue_prune_oracle_bit_exact_vs_reference(i):
+    gd = _packed_golden()
+    for colwise in (False, True):
+        d = "col" if colwise else "row"
+        vals, bits = o.mvue_prune(gd[f"mvue{i}.g"], colwise, int(gd[f"mvue{i}.seed"]))
+        assert np.array_equal(vals.view(np.uint64), gd[f"mvue{i}.{d}.values"].view(np.uint64))
+        assert np.array_equal(bits, gd[f"mvue{i}.{d}.bits"])
+
+
+def test_block_flip_stats_oracle_bit_exact_vs_reference():
+    gd = _packed_golden()
+    flips, gaps = o.block_flip_stats([gd["flip3.wa"], gd["flip3.wb"], gd["flip3.wc"]])
+    assert np.array_equal(flips, gd["flip3.block_flips"])
+    assert np.array_equal(gaps.view(np.uint64), gd["flip3.block_gaps"].view(np.uint64))
+    assert np.array_equal(o.block_gaps(gd["ties.w"]), gd["ties.block_gaps"])
+    assert (gd["ties.block_gaps"] == 0).any()  # the corpus exercises tied top-2 scores
