@@ -3,7 +3,7 @@
 The measured unit is one training step of the residual FFN stack of the reference's
 _FFNStack (trainer.py:159-262): h_{l+1} = h_l + FFN_l(h_l) over 36 blocks of
 d=1280, d_ff=5120, GELU, 16384 tokens per rank, forward then backward through every
-block (dh_l = dh_{l+1} + dX_l).  Each block runs the same kernels as the single-block
+block (dh_l = dh_{l+1} + dX_l, accumulated by the dX GEMM's add-reduce store).  Each block runs the same kernels as the single-block
 bench (K2 prune/compress of both weights, or K1 search every 40th step; fused
 GEMM+GELU, GEMM; dGELU-fused dA, dW2 and dW_in with the masked decay, dX), and each
 block's gradient bucket [dW_in | dbias | dW2] is all-reduced asynchronously as soon as
@@ -37,11 +37,14 @@ class StackStep:
             self.ops.append((op_in, op_out))
             self.buckets.append((bucket, views))
         self.t = 0
+        self.dh = None
         self.launches_per_step = len(layers) * (1 + 2 + 4)
 
     def __call__(self, x, dy):
         E, torch = self.E, self.torch
         refresh = self.t % B.REFRESH == 0
+        if self.dh is None or self.dh.shape != dy.shape:
+            self.dh = torch.empty_like(dy)
         states = []
         h = x
         for (w_in, bias, w2), (op_in, op_out) in zip(self.layers, self.ops):
@@ -54,7 +57,10 @@ class StackStep:
             states.append(st)
             h = h + st.y
         work = []
-        dh = dy
+        # the residual gradient dh_l = dh_{l+1} + dX_l accumulates in one buffer: each block's
+        # dX GEMM add-reduces into it (S24_EPI_STORE_ADD) after the block's dA / dW2 GEMMs read it
+        dh = self.dh
+        dh.copy_(dy)
         for l in reversed(range(len(self.layers))):
             w_in, bias, w2 = self.layers[l]
             op_in, op_out = self.ops[l]
@@ -67,8 +73,7 @@ class StackStep:
 
             g = E.ffn_backward(states[l], dh, op_in, op_out, self.act, w_in_dense=w_in, w2_dense=w2,
                                lam=B.LAMBDA / self.world, dw_in_out=dwi, dw2_out=dw2, dbias_out=db,
-                               grads_ready=grads_ready)
-            dh = dh + g.dx
+                               grads_ready=grads_ready, dx_accumulate=dh)
             states[l] = None
         if self.world > 1:
             self.C.call("s24_set_reserved_sms", 0)

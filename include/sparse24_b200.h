@@ -80,6 +80,10 @@ extern "C" {
 #define S24_EPI_GEGLU_GRAD 4
 #define S24_EPI_SWIGLU_GRAD 5
 #define S24_EPI_DGATED 6
+/* D += acc (+ bias[m]) into an existing token-major bf16 D (d_t = 1): the store is a TMA bf16
+ * add-reduce, so a residual stream's gradient (dh_l = dh_{l+1} + dX_l, the backward of
+ * _FFNStack trainer.py:159-262) is accumulated by the dX GEMM itself. */
+#define S24_EPI_STORE_ADD 7
 
 const char* s24_last_error_string(void);
 int s24_abi_version(void);

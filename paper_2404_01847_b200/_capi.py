@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("S24_LIB_PATH") or os.path.join(_HERE, "libs24b200.so"
 S24_OK, S24_ERR_SHAPE, S24_ERR_FORMAT, S24_ERR_UNSUPPORTED, S24_ERR_CUDA, S24_ERR_ARG = range(6)
 S24_BF16, S24_F32, S24_F64 = 0, 1, 2
 ACT_RELU, ACT_GELU, ACT_GEGLU, ACT_SWIGLU = 0, 1, 2, 3
-EPI_STORE, EPI_GELU_AUX, EPI_GELU_GRAD, EPI_DGELU, EPI_GEGLU_GRAD, EPI_SWIGLU_GRAD, EPI_DGATED = range(7)
+EPI_STORE, EPI_GELU_AUX, EPI_GELU_GRAD, EPI_DGELU, EPI_GEGLU_GRAD, EPI_SWIGLU_GRAD, EPI_DGATED, EPI_STORE_ADD = range(8)
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

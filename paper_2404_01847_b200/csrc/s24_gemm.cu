@@ -64,6 +64,7 @@ struct EpiParams {
   int w_dtype;
   const uint8_t* idx;
   float lam;
+  int accumulate;    // kEpiStore, token-major: D += acc via TMA bf16 add-reduce (S24_EPI_STORE_ADD)
 };
 
 struct GemmShape {
@@ -659,7 +660,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmD, zb, m_w, n0);
+              if (kEpi == kEpiStore && ep.accumulate) tma_reduce_add_2d(&tmD, zb, m_w, n0);
+              else tma_store_2d(&tmD, zb, m_w, n0);
               bulk_commit();
             }
             sbuf ^= 1;
@@ -1148,7 +1150,10 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   S24_REQUIRE(m % 128 == 0 && k % 128 == 0 && n % 32 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
               "sparse GEMM needs m %% 128 == 0, k %% 128 == 0, n %% 32 == 0 (got m=%lld k=%lld n=%lld)",
               (long long)m, (long long)k, (long long)n);
-  S24_REQUIRE(epilogue >= S24_EPI_STORE && epilogue <= S24_EPI_DGATED, S24_ERR_ARG, "bad epilogue");
+  S24_REQUIRE(epilogue >= S24_EPI_STORE && epilogue <= S24_EPI_STORE_ADD, S24_ERR_ARG, "bad epilogue");
+  const bool accumulate = epilogue == S24_EPI_STORE_ADD;
+  S24_REQUIRE(!accumulate || d_t == 1, S24_ERR_ARG, "S24_EPI_STORE_ADD accumulates into a token-major output (d_t = 1)");
+  if (accumulate) epilogue = S24_EPI_STORE;
   const bool gated_fwd = epilogue == S24_EPI_GEGLU_GRAD || epilogue == S24_EPI_SWIGLU_GRAD;
   const bool gated_bwd = epilogue == S24_EPI_DGATED;
   // logical width of the stored output: GEMM1 gated stores d_ff = m/2 gate features, GEMM3 gated
@@ -1224,7 +1229,7 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
                aux2,    epilogue == S24_EPI_SWIGLU_GRAD ? S24_ACT_SWIGLU : S24_ACT_GEGLU,
                gate_ff, nullptr,
                0,       nullptr,
-               0.0f};
+               0.0f,    accumulate ? 1 : 0};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define S24_SP(BMN, BNV, CG, EPI)                                                                          \
   if (d_t)                                                                                                  \

@@ -295,7 +295,7 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
                  lam: float = 0.0, dw_in_out: torch.Tensor | None = None,
                  dw2_out: torch.Tensor | None = None, mvue: bool = False, rng_seed: int = 0,
                  mvue_exact: bool = True, dbias_out: torch.Tensor | None = None,
-                 grads_ready=None) -> Grads:
+                 grads_ready=None, dx_accumulate: torch.Tensor | None = None) -> Grads:
     """dA = dY W2~ (out_bwd, W2's transposed orientation) -> dZ (activation
     backward, bias gradient) -> dX = dZ W_in~ (in_bwd); dense dW2 = dY^T A and
     dW_in = dZ^T X with the masked decay lam (1 - M) W fused (gated_ffn.py:327-356).
@@ -306,7 +306,10 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     Launch order: dA/dZ (+ bias gradient), dW2, dW_in, then dX, so that
     `grads_ready()` -- called once every weight/bias gradient is enqueued -- can start
     the data-parallel all-reduce of the gradient bucket while dX is still computing.
-    dbias_out / dw_in_out / dw2_out let the caller hand in views of that bucket."""
+    dbias_out / dw_in_out / dw2_out let the caller hand in views of that bucket.
+    dx_accumulate: a residual stream's gradient buffer; dX is added into it by the dX GEMM's
+    store (S24_EPI_STORE_ADD) instead of being written to a fresh tensor.  It may be `dy`
+    itself: every reader of dy is enqueued before the dX GEMM on the same stream."""
     n, d = st.x.shape
     r_in, d_ff = w_in.rows, w2.cols
     if tuple(dy.shape) != (n, d):
@@ -346,6 +349,15 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
                 gate_ff=gate_ff)
     if grads_ready is not None:
         grads_ready()
-    dx = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
-    spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dz, False, n, dx, tag="k4_spmm_bwd_in", out_t=True)
+    if dx_accumulate is not None:
+        # residual stream: dX is add-reduced into the caller's (n, d) gradient by the GEMM's store
+        if tuple(dx_accumulate.shape) != (n, d) or dx_accumulate.dtype != torch.bfloat16 \
+                or not dx_accumulate.is_contiguous():
+            raise ShapeError("dx_accumulate must be a contiguous (tokens, d) bf16 tensor")
+        dx = dx_accumulate
+        spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dz, False, n, dx, tag="k4_spmm_bwd_in", out_t=True,
+             epi=C.EPI_STORE_ADD)
+    else:
+        dx = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
+        spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dz, False, n, dx, tag="k4_spmm_bwd_in", out_t=True)
     return Grads(dx, dw_in, dbias, dw2)

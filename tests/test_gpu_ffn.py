@@ -370,3 +370,37 @@ def test_training_step_cuda_graph_capture_and_replay():
         torch.cuda.synchronize()
         for got, want in zip((yg, dxg, dwi, dw2, db), ref):
             assert torch.equal(got, want) or torch.allclose(got, want, rtol=0, atol=1e-6)
+
+
+@pytest.mark.parametrize("d,d_ff,n", [(256, 512, 1024), (1024, 4096, 2048)])
+def test_dx_accumulate_into_residual_gradient(d, d_ff, n):
+    """ffn_backward(dx_accumulate=dh): the dX GEMM add-reduces into the residual gradient
+    (S24_EPI_STORE_ADD, one-slab and two-slab tiles), even when dh is the upstream dy itself:
+    result == rn(dh + dX) of the plain path; the other gradients are unchanged."""
+    from paper_2404_01847_b200 import engine as E
+    from paper_2404_01847_b200 import _capi as C
+
+    g = torch.Generator(device="cpu").manual_seed(d + n)
+    w_in = (torch.randn(d_ff, d, generator=g) / d ** 0.5).to(torch.bfloat16).cuda()
+    w2 = (torch.randn(d, d_ff, generator=g) / d_ff ** 0.5).to(torch.bfloat16).cuda()
+    b = torch.zeros(d_ff, dtype=torch.bfloat16, device="cuda")
+    x = torch.randn(n, d, generator=g).to(torch.bfloat16).cuda()
+    dy = torch.randn(n, d, generator=g).to(torch.bfloat16).cuda()
+    op_in, op_out = E.CompressedOperand.empty(d_ff, d, "cuda"), E.CompressedOperand.empty(d, d_ff, "cuda")
+    E.search_compress(w_in, op_in)
+    E.search_compress(w2, op_out)
+    st = E.ffn_forward(x, op_in, b, op_out, "gelu", fused=True)
+    ref = E.ffn_backward(st, dy, op_in, op_out, "gelu", w_in_dense=w_in, w2_dense=w2, lam=1e-2)
+    want = (dy.float() + ref.dx.float()).to(torch.bfloat16)
+    dh = dy.clone()
+    got = E.ffn_backward(st, dh, op_in, op_out, "gelu", w_in_dense=w_in, w2_dense=w2, lam=1e-2, dx_accumulate=dh)
+    torch.cuda.synchronize()
+    assert got.dx.data_ptr() == dh.data_ptr()
+    assert torch.equal(got.dw_in, ref.dw_in) and torch.equal(got.dw2, ref.dw2)
+    diff = (dh.float() - want.float()).abs()
+    ulp = want.float().abs() * 2.0 ** -7 + 1e-30
+    assert bool((diff <= ulp).all()), float((diff / ulp).max())
+    # the accumulate epilogue needs the token-major store
+    with pytest.raises(RuntimeError):
+        C.call("s24_spmm", op_in.bwd_vals.data_ptr(), op_in.bwd_e.data_ptr(), d, d_ff, st.a.data_ptr(), 0, d_ff,
+               n, dh.data_ptr(), n, None, C.EPI_STORE_ADD, None, 0, None, None, 0, 0, C.stream_of(dh))
