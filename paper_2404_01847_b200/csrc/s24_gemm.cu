@@ -165,6 +165,14 @@ struct Cfg {
 constexpr int kWaveSlots = 64;
 __device__ unsigned int g_wave_ctr[kWaveSlots][2];  // [slot][0: tiles issued, 1: CTAs exited]
 
+// Ordered split-K (WorkIter mode S >= 3): the S partial tiles of one output tile are add-reduced
+// in split order, so the fp32 sums are run-to-run identical.  Every storer (epilogue warp of
+// either CTA of the pair) of split s waits until all storers of split s - 1 have completed their
+// bulk reduce-adds (per-tile counter, bounded spin: the order is a determinism guarantee, the sum
+// is correct either way), and the storer that completes the last split resets the counter.
+constexpr int kSplitTiles = 2048;
+__device__ unsigned int g_split_ctr[kWaveSlots][kSplitTiles];
+
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -187,6 +195,7 @@ struct WorkIter {
     stride = ncl;
   }
   // next segment: output tile and its k-block range [kb0, kb1)
+  int last_split = 0;  // split index of the unit returned by the last next() (0 for other modes)
   __device__ __forceinline__ bool next(int num_tiles, int num_kb, int& t, int& kb0, int& kb1) {
     if (sk) {
       if (it >= end) return false;
@@ -198,6 +207,7 @@ struct WorkIter {
     }
     if (tile >= num_tiles * split) return false;
     const int s = tile / num_tiles;
+    last_split = s;
     t = tile - s * num_tiles;
     kb0 = static_cast<int>(static_cast<long long>(num_kb) * s / split);
     kb1 = static_cast<int>(static_cast<long long>(num_kb) * (s + 1) / split);
@@ -716,8 +726,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const bool first_chunk = kb0 == 0;                  // adds the decay exactly once
         const bool partial = kb0 != 0 || kb1 != num_kb;     // stream-K piece: add-reduce
         const int n_base = nb * kBN;
+        // ordered split-K: this unit's reduce-adds start after split s - 1 of the tile completed
+        constexpr unsigned int kStorers = 8 * kCG;
+        unsigned int* sctr = (kEpi == kEpiDw && shp.streamk >= 3 && shp.wave_slot >= 0 && tile < kSplitTiles)
+                                 ? &g_split_ctr[shp.wave_slot][tile] : nullptr;
+        const int sidx = wk.last_split;
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
+        if (sctr != nullptr && sidx > 0) {
+          if (lane == 0) {
+            const unsigned int target = kStorers * static_cast<unsigned int>(sidx);
+            const long long t0 = clock64();
+            while (ld_acquire_gpu(sctr) < target && clock64() - t0 < 2000000) __nanosleep(64);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+          __syncwarp();
+        }
 #pragma unroll 1
         for (int slab = 0; slab < kSlabs; ++slab) {
         const int m_w = mb * C::TILE_M + 128 * kCG * slab + 128 * rank + 32 * q;  // first row of this warp
@@ -869,6 +893,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if constexpr (kCG == 2) mbar_arrive_cluster(&tempty_bar[acc], crank & ~1u);  // pair leader
           else mbar_arrive(&tempty_bar[acc]);
         }
+        if (sctr != nullptr && lane == 0) {
+          // this storer's reduce-adds of split s are complete -> release split s + 1
+          bulk_wait0();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          const unsigned int old = atomicAdd(sctr, 1u);
+          if (old == kStorers * static_cast<unsigned int>(shp.streamk) - 1u) atomicExch(sctr, 0u);
+        }
         if (++acc == kAcc) {
           acc = 0;
           acc_phase ^= 1;
@@ -973,21 +1005,36 @@ static int use_streamk(int tiles, int clusters, int num_kb) {
   return !det && env == 1 ? 1 : 0;
 }
 
-// Lockstep split-K for the weight-gradient GEMMs (WorkIter mode 2): a tile count just above a
-// multiple of the CTA pairs leaves most of the last wave idle (C5 dW: 100 tiles on 74 pairs =
-// 2 tile-times for 1.35 of work); halving K per unit gives 200 units = 1.5 tile-times.  Unlike
-// stream-K every wave stays at one K offset (panels shared in L2), and with two addends onto
-// the zeroed output the fp32 result is order-independent (a + b = b + a), so it stays
-// deterministic.  Taken when it shortens the schedule by >= 10 % and each half keeps K >= 4096.
-// S24_SPLITK=0/2 overrides.
-static int use_splitk(int tiles, int clusters, int num_kb, int kb_min) {
+// Lockstep split-K for the weight-gradient GEMMs (WorkIter mode S >= 2): a tile count that does
+// not fill the last wave leaves CTA pairs idle (C2 dW: 64 tiles on 74 pairs; C5 dW: 100 tiles =
+// 2 tile-times for 1.35 of work).  Cutting K into S equal ranges makes T S units; S is the
+// smallest split that minimises ceil(T S / P) / S (C5: S = 2 -> 1.5 tile-times; C2: S = 8 ->
+// 0.875).  Unlike stream-K every wave stays at one K offset (panels shared in L2).  Partial tiles
+// TMA-add-reduce into the zeroed output: with two addends (a + b = b + a) the result is
+// order-independent, and for S >= 3 the splits of a tile reduce in split order (g_split_ctr), so
+// every split stays deterministic.  Each unit keeps K >= 64 * kb_min; a split must save >= 3 %,
+// and the fp32 output must fit well inside L2 (<= 32 MB: C2, C5), otherwise every partial tile
+// would round-trip through HBM (C3 dW_in: 360 MB per pass).
+// S24_SPLITK=0 off, =N forces N.
+static int use_splitk(int tiles, int clusters, int num_kb, int kb_min, double out_bytes) {
   static const int env = getenv("S24_SPLITK") ? atoi(getenv("S24_SPLITK")) : -1;
   if (env == 0 || env == 1) return 0;
-  if (env >= 2) return num_kb >= 2 ? 2 : 0;
-  if (clusters <= 0 || num_kb < 2 * kb_min) return 0;
+  const int smax = tiles <= kSplitTiles ? 8 : 2;
+  if (env >= 2) return num_kb >= env && env <= smax ? env : (num_kb >= 2 ? 2 : 0);
+  // the partial tiles of different waves meet in L2 only if the fp32 output stays resident
+  if (clusters <= 0 || out_bytes > 32.0 * 1024 * 1024) return 0;
   const double t1 = static_cast<double>((tiles + clusters - 1) / clusters);
-  const double t2 = static_cast<double>((2 * tiles + clusters - 1) / clusters) / 2.0;
-  return t2 <= 0.9 * t1 ? 2 : 0;
+  int best = 1;
+  double bt = t1;
+  for (int sp = 2; sp <= smax; ++sp) {
+    if (num_kb < sp * kb_min) break;
+    const double t = static_cast<double>((static_cast<int64_t>(tiles) * sp + clusters - 1) / clusters) / sp;
+    if (t < bt - 1e-9) {
+      bt = t;
+      best = sp;
+    }
+  }
+  return bt <= 0.97 * t1 ? best : 0;
 }
 
 static int dw_clusters() {
@@ -1341,7 +1388,7 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   int streamk = use_streamk(tiles, clusters, static_cast<int>(k / 64));
   if (!streamk)
     streamk = use_splitk(slabs ? static_cast<int>((m / 512) * (n / 256)) : tiles,
-                         pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 64), 64);
+                         pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 64), 32, 4.0 * m * n);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (streamk) {
     cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
@@ -1412,7 +1459,8 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int sk_tiles = static_cast<int>((m / (pair ? 256 : 128)) * (n / (wide ? 256 : 128)));
   int streamk = use_streamk(sk_tiles, num_sms() / (pair ? 2 : 1), static_cast<int>(k / 128));
-  if (!streamk) streamk = use_splitk(sk_tiles, pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 128), 32);
+  if (!streamk)
+    streamk = use_splitk(sk_tiles, pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 128), 16, 4.0 * m * n);
   if (streamk) {
     cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));

@@ -388,16 +388,18 @@ def test_dense_dw_gemm_c5_shape_lockstep_splitk(gate_ff):
     assert torch.equal(outs[0], outs[1])
 
 
-def test_dw_gemms_splitk_forced_small_shapes():
-    """S24_SPLITK=2 forces the lockstep split-K schedule on every dW GEMM (dense and the MVUE
-    sparse-A one), including odd k-block counts (uneven halves) and the decay."""
+@pytest.mark.parametrize("splits", ["2", "3", "8"])
+def test_dw_gemms_splitk_forced_small_shapes(splits):
+    """S24_SPLITK=N forces the lockstep split-K schedule on every dW GEMM (dense and the MVUE
+    sparse-A one), including uneven K ranges and the decay; N >= 3 reduces the partial tiles in
+    split order, so repeated launches are bit-identical."""
     import subprocess
     import sys
 
     code = (
         "import torch, sys; sys.path.insert(0, %r)\n"
         "from paper_2404_01847_b200 import engine as E, transposable_search_conv, _capi as C\n"
-        "for m, n, k in [(128, 128, 128), (256, 512, 320), (384, 256, 1216), (512, 768, 4096)]:\n"
+        "for m, n, k in [(128, 128, 512), (256, 512, 640), (384, 256, 1216), (512, 768, 4096)]:\n"
         "    w = torch.randn(m, n, device='cuda').bfloat16(); mk = transposable_search_conv(w)\n"
         "    a = torch.randn(k, m, device='cuda').bfloat16(); b = torch.randn(k, n, device='cuda').bfloat16()\n"
         "    out = torch.full((m, n), float('nan'), device='cuda')\n"
@@ -405,7 +407,11 @@ def test_dw_gemms_splitk_forced_small_shapes():
         "    ref = a.float().t() @ b.float() + 0.5 * (1 - mk.bits.float()) * w.float()\n"
         "    e = float((out - ref).norm() / ref.norm())\n"
         "    assert e < 2e-3, (m, n, k, e)\n"
-        "for f, n, d in [(256, 256, 128), (512, 1024, 256)]:\n"
+        "    for _ in range(3):\n"
+        "        o2 = torch.full((m, n), float('nan'), device='cuda')\n"
+        "        E.gemm_dw(a, True, b, True, m, n, k, o2, w, mk.idx, 0.5)\n"
+        "        assert torch.equal(o2, out), (m, n, k)\n"
+        "for f, n, d in [(256, 1024, 128), (512, 2048, 256)]:\n"
         "    g = torch.randn(n, f, device='cuda').bfloat16(); bd = torch.randn(n, d, device='cuda').bfloat16()\n"
         "    vals, e_, _ = E.mvue_compress(g, 7, exact=False)\n"
         "    out = torch.full((f, d), float('nan'), device='cuda')\n"
@@ -418,6 +424,6 @@ def test_dw_gemms_splitk_forced_small_shapes():
         "    e = float((out - dense).norm() / dense.norm())\n"
         "    assert e < 2e-3, (f, n, d, e)\n"
         "print('ok')\n" % os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
-    env = dict(os.environ, S24_SPLITK="2")
+    env = dict(os.environ, S24_SPLITK=splits)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
