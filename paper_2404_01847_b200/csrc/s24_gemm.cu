@@ -1006,21 +1006,22 @@ static int use_streamk(int tiles, int clusters, int num_kb) {
 }
 
 // Lockstep split-K for the weight-gradient GEMMs (WorkIter mode S >= 2): a tile count that does
-// not fill the last wave leaves CTA pairs idle (C2 dW: 64 tiles on 74 pairs; C5 dW: 100 tiles =
-// 2 tile-times for 1.35 of work).  Cutting K into S equal ranges makes T S units; S is the
-// smallest split that minimises ceil(T S / P) / S (C5: S = 2 -> 1.5 tile-times; C2: S = 8 ->
-// 0.875).  Unlike stream-K every wave stays at one K offset (panels shared in L2).  Partial tiles
-// TMA-add-reduce into the zeroed output: with two addends (a + b = b + a) the result is
-// order-independent, and for S >= 3 the splits of a tile reduce in split order (g_split_ctr), so
-// every split stays deterministic.  Each unit keeps K >= 64 * kb_min; a split must save >= 3 %,
-// and the fp32 output must fit well inside L2 (<= 32 MB: C2, C5), otherwise every partial tile
-// would round-trip through HBM (C3 dW_in: 360 MB per pass).
-// S24_SPLITK=0 off, =N forces N.
+// not fill the last wave leaves CTA pairs idle (C5 dW: 100 tiles on 74 pairs = 2 tile-times for
+// 1.35 of work).  Cutting K into S equal ranges makes T S units (C5, S = 2: 1.5 tile-times,
+// measured 0.221 -> 0.182 ms per launch).  Unlike stream-K every wave stays at one K offset
+// (panels shared in L2).  Partial tiles TMA-add-reduce into the zeroed output: with two addends
+// (a + b = b + a) the result is order-independent, and for S >= 3 the splits of a tile reduce in
+// split order (g_split_ctr), so every split stays deterministic.  The automatic choice stops at
+// S = 2: S = 8 would fill C2's 64-tile dW waves (0.875 tile-times) but measured 25 % slower on
+// B200 (8 reduce passes of the fp32 tile through L2 per output), and C5 got slower too.  A split
+// must save >= 3 %, each unit keeps K >= 64 * kb_min, and the fp32 output must fit well inside L2
+// (<= 32 MB), otherwise every partial tile round-trips through HBM (C3 dW_in: 360 MB per pass).
+// S24_SPLITK=0 off, =N forces N (up to 8).
 static int use_splitk(int tiles, int clusters, int num_kb, int kb_min, double out_bytes) {
   static const int env = getenv("S24_SPLITK") ? atoi(getenv("S24_SPLITK")) : -1;
   if (env == 0 || env == 1) return 0;
-  const int smax = tiles <= kSplitTiles ? 8 : 2;
-  if (env >= 2) return num_kb >= env && env <= smax ? env : (num_kb >= 2 ? 2 : 0);
+  if (env >= 2) return num_kb >= env && env <= (tiles <= kSplitTiles ? 8 : 2) ? env : (num_kb >= 2 ? 2 : 0);
+  const int smax = 2;
   // the partial tiles of different waves meet in L2 only if the fp32 output stays resident
   if (clusters <= 0 || out_bytes > 32.0 * 1024 * 1024) return 0;
   const double t1 = static_cast<double>((tiles + clusters - 1) / clusters);
