@@ -176,3 +176,23 @@ def test_data_parallel_gradient_exchange_gloo(world):
         p.join(60)
     assert all(p.exitcode == 0 for p in ps)
     assert max(errs) < 1e-5, errs
+
+
+def test_bench_reference_arm_line():
+    """`bench.py --impl reference` (the reference's own CPU path on the host cores) prints the
+    contract's JSON line: same metric / unit / workload as our arm, impl, cpu_baseline, e2e."""
+    import json
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                        "--ref-tokens", "8"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    assert line["unit"] == "tokens/s" and line["value"] > 0 and line["higher_is_better"] is True
+    assert line["metric"].startswith("2:4 FFN fwd+bwd tokens/s")
+    assert "BASELINE.json configs[1]" in line["config"]["workload"]
+    cb = line["cpu_baseline"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["sample"] and cb["value"] == line["value"]
+    e2e = line["e2e"]
+    assert e2e["value"] == line["value"] and e2e["h2d_bytes_per_step"] == 0 and e2e["d2h_bytes_per_step"] == 0
