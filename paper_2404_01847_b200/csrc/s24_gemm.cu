@@ -180,34 +180,66 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
 }
 
 struct WorkIter {
-  long long it, end;
-  int tile, stride, split;
+  long long it, end, total;
+  int tile, stride, split, ncl, head_tile = 0, head_kb1 = 0;
   bool sk;
-  // mode 0: one full-K tile per step; 1: stream-K; S >= 2: lockstep split-K -- every tile is
-  // cut into S equal K ranges, unit u = s * num_tiles + tile, so the clusters of one wave all
-  // sit at the same relative K offset of their range and keep sharing operand panels in L2
-  __device__ __forceinline__ WorkIter(int mode, int num_tiles, int num_kb, int cid, int ncl)
-      : split(mode >= 2 ? mode : 1), sk(mode == 1) {
-    const long long t = static_cast<long long>(num_tiles) * num_kb;
-    it = sk ? t * cid / ncl : 0;
-    end = sk ? t * (cid + 1) / ncl : 0;
+  // mode 0: one full-K tile per step; S >= 2: lockstep split-K -- every tile is cut into S equal
+  // K ranges, unit u = s * num_tiles + tile, so the clusters of one wave all sit at the same
+  // relative K offset of their range and keep sharing operand panels in L2.
+  // mode 1: K-aligned stream-K -- cluster c owns the run [T c / ncl, T (c + 1) / ncl) of the
+  // (tile, k-block) space (T = tiles * num_kb) and processes the run's LAST segment first: that
+  // segment starts at k-block 0 of its tile, like every other cluster's first segment, so all
+  // clusters sweep K together; the remaining tail of the previous tile follows, at most
+  // (1 - tiles / ncl) * num_kb k-blocks ahead of the others when the run is shorter than a tile
+  __device__ __forceinline__ WorkIter(int mode, int num_tiles, int num_kb, int cid, int ncl_)
+      : split(mode >= 2 ? mode : 1), ncl(ncl_), sk(mode == 1) {
+    total = static_cast<long long>(num_tiles) * num_kb;
+    it = sk ? total * cid / ncl : 0;
+    end = sk ? total * (cid + 1) / ncl : 0;
+    if (sk) {
+      const long long b = end / num_kb;
+      const int ke = static_cast<int>(end - b * num_kb);
+      if (ke > 0 && b * num_kb > it) {  // the run ends inside tile b and starts before it
+        head_tile = static_cast<int>(b);
+        head_kb1 = ke;
+        end = b * num_kb;
+      }
+    }
     tile = cid;
     stride = ncl;
   }
+  // stream-K: how many runs start at or before linear k-block x (run starts floor(T c / ncl))
+  __device__ __forceinline__ long long runs_upto(long long x) const {
+    const long long c = ((x + 1) * ncl + total - 1) / total;
+    return c < ncl ? c : ncl;
+  }
   // next segment: output tile and its k-block range [kb0, kb1)
-  int last_split = 0;  // split index of the unit returned by the last next() (0 for other modes)
+  int last_split = 0;   // index of the returned segment among its tile's K segments (K order)
+  int last_nsplit = 1;  // number of K segments of that tile
   __device__ __forceinline__ bool next(int num_tiles, int num_kb, int& t, int& kb0, int& kb1) {
     if (sk) {
-      if (it >= end) return false;
-      t = static_cast<int>(it / num_kb);
-      kb0 = static_cast<int>(it - static_cast<long long>(t) * num_kb);
-      kb1 = static_cast<int>(min(static_cast<long long>(num_kb), kb0 + (end - it)));
-      it += kb1 - kb0;
+      if (head_kb1 > 0) {
+        t = head_tile;
+        kb0 = 0;
+        kb1 = head_kb1;
+        head_kb1 = 0;
+      } else {
+        if (it >= end) return false;
+        t = static_cast<int>(it / num_kb);
+        kb0 = static_cast<int>(it - static_cast<long long>(t) * num_kb);
+        kb1 = static_cast<int>(min(static_cast<long long>(num_kb), kb0 + (end - it)));
+        it += kb1 - kb0;
+      }
+      const long long base = static_cast<long long>(t) * num_kb;
+      const long long r0 = runs_upto(base);
+      last_split = static_cast<int>(runs_upto(base + kb0) - r0);
+      last_nsplit = static_cast<int>(runs_upto(base + num_kb - 1) - r0) + 1;
       return true;
     }
     if (tile >= num_tiles * split) return false;
     const int s = tile / num_tiles;
     last_split = s;
+    last_nsplit = split;
     t = tile - s * num_tiles;
     kb0 = static_cast<int>(static_cast<long long>(num_kb) * s / split);
     kb1 = static_cast<int>(static_cast<long long>(num_kb) * (s + 1) / split);
@@ -308,7 +340,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       WorkIter wk(shp.streamk, num_work, num_kb, cluster_id, num_clusters);
       int tile, kb0, kb1, wave = 0;
-      unsigned int* wctr = shp.wave_slot >= 0 ? &g_wave_ctr[shp.wave_slot][0] : nullptr;
+      unsigned int* wctr = (shp.wave_slot >= 0 && shp.streamk != 1) ? &g_wave_ctr[shp.wave_slot][0] : nullptr;
       while (wk.next(num_work, num_kb, tile, kb0, kb1)) {
         if (wctr != nullptr && wave > 0) {
           // every producer has issued the previous wave's loads (bounded wait)
@@ -728,7 +760,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int n_base = nb * kBN;
         // ordered split-K: this unit's reduce-adds start after split s - 1 of the tile completed
         constexpr unsigned int kStorers = 8 * kCG;
-        unsigned int* sctr = (kEpi == kEpiDw && shp.streamk >= 3 && shp.wave_slot >= 0 && tile < kSplitTiles)
+        // (stream-K runs are ordered only when none is empty: T >= clusters)
+        unsigned int* sctr = (kEpi == kEpiDw && (shp.streamk >= 3 || (shp.streamk == 1 && wk.total >= wk.ncl)) &&
+                              shp.wave_slot >= 0 && tile < kSplitTiles)
                                  ? &g_split_ctr[shp.wave_slot][tile] : nullptr;
         const int sidx = wk.last_split;
         mbar_wait(&tfull_bar[acc], acc_phase);
@@ -899,7 +933,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           asm volatile("fence.proxy.async.global;" ::: "memory");
           __threadfence();
           const unsigned int old = atomicAdd(sctr, 1u);
-          if (old == kStorers * static_cast<unsigned int>(shp.streamk) - 1u) atomicExch(sctr, 0u);
+          if (old == kStorers * static_cast<unsigned int>(wk.last_nsplit) - 1u) atomicExch(sctr, 0u);
         }
         if (++acc == kAcc) {
           acc = 0;
@@ -992,17 +1026,25 @@ static int num_sms() {
 // Sparse GEMMs (A = compressed weight, 1.125 B per logical K per row incl. metadata)
 // take as many M tiles as fit a ~48 MB L2 budget; dense dW panels (K = tokens) are
 // far larger than L2, so they keep the wave-square default of 8.
-// Stream-K (S24_STREAMK=1; off by default): balances badly filled waves (C2 dW: 64 tiles on
-// 74 CTA pairs), but clusters then sit at different K offsets of the same tiles and stop sharing
-// operand panels in L2 -- measured on B200 it quadrupled the HBM reads of the C2 dW GEMMs
-// (176 -> 748 MB) and made them 20% slower, and C3 dW2 read 17.5 GB instead of 5 GB.
-static int use_streamk(int tiles, int clusters, int num_kb) {
-  static const bool det = getenv("S24_DETERMINISTIC") != nullptr;
+// Stream-K for a weight-gradient GEMM whose tiles do not fill one wave (C2 dW: 64 tiles on 74
+// CTA pairs, 86 % fill); S24_STREAMK=1 turns it on, off by default.  Plain stream-K (runs
+// processed in linear order) put the clusters at different K offsets of the same tiles, so they
+// stopped sharing operand panels in L2: on B200 it quadrupled the HBM reads of the C2 dW GEMMs
+// (176 -> 748 MB) and made them 20 % slower.  The K-aligned order (WorkIter mode 1: every run
+// starts with the segment at k-block 0 of its last tile) keeps all clusters within
+// (1 - tiles / clusters) of a tile's K range of each other (C2: 35 k-blocks, ~23 MB of panels),
+// and the partial tiles reduce in K order through g_split_ctr (deterministic).  Measured on B200
+// at C2: HBM reads 203 MB (vs 176 MB one-tile-per-pair), kernel 98.7 vs 103.0 us under ncu --
+// but only 4 % of the 13.5 % the fill promises, and with the zeroing memset of the fp32 output
+// the dW step inside full training steps measured 7 % slower, so the automatic choice stays off.
+static int use_streamk(int tiles, int clusters, int num_kb, bool auto_ok = false, double out_bytes = 0.0) {
   static const int env = getenv("S24_STREAMK") ? atoi(getenv("S24_STREAMK")) : -1;
-  (void)tiles;
-  (void)clusters;
-  (void)num_kb;
-  return !det && env == 1 ? 1 : 0;
+  if (env >= 0) return env == 1 ? 1 : 0;
+  static const bool auto_env = getenv("S24_STREAMK_AUTO") != nullptr;  // experiment: the rule below
+  if (!auto_env || !auto_ok || clusters <= 0 || tiles > kSplitTiles || out_bytes > 32.0 * 1024 * 1024) return 0;
+  if (static_cast<double>(tiles) > 0.9 * clusters) return 0;
+  if (static_cast<int64_t>(tiles) * num_kb < 32LL * clusters) return 0;
+  return 1;
 }
 
 // Lockstep split-K for the weight-gradient GEMMs (WorkIter mode S >= 2): a tile count that does
@@ -1386,7 +1428,8 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   const int clusters = num_sms() / (pair ? 2 : 1);
   const int tiles = static_cast<int>((m / (pair ? 256 : 128)) * (n / BN));
   const bool slabs = pair && a_mn && b_mn && m % 512 == 0 && use_dw_slabs(m, n, k);
-  int streamk = use_streamk(tiles, clusters, static_cast<int>(k / 64));
+  int streamk = slabs ? 0 : use_streamk(tiles, pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 64),
+                                         true, 4.0 * m * n);
   if (!streamk)
     streamk = use_splitk(slabs ? static_cast<int>((m / 512) * (n / 256)) : tiles,
                          pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 64), 32, 4.0 * m * n);
@@ -1399,7 +1442,7 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   static const int env_dw = getenv("S24_GROUP_M_DW") ? atoi(getenv("S24_GROUP_M_DW")) : 8;
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), streamk,
                 static_cast<int>(m / tile_m) < env_dw ? static_cast<int>(m / tile_m) : env_dw,
-                streamk == 1 ? -1 : wave_slot(stream, true), exp_flags()};
+                wave_slot(stream, true), exp_flags()};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
 
 #define S24_DW(AMN, BMN, BNV, CG)                                                                      \

@@ -427,3 +427,39 @@ def test_dw_gemms_splitk_forced_small_shapes(splits):
     env = dict(os.environ, S24_SPLITK=splits)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("m,n", [(4096, 1024), (1024, 4096)])
+def test_dense_dw_gemm_c2_shape_aligned_streamk(m, n):
+    """C2-shaped dW (64 tiles on 74 CTA pairs) with S24_STREAMK=1: the K-aligned stream-K
+    schedule (runs start at k-block 0 of their last tile, partial tiles reduced in K order
+    through the split counters, the decay added once) against fp32, and bit-identical across
+    launches (subprocess: the knob is read once)."""
+    import subprocess
+    import sys
+
+    if os.environ.get("S24_STREAMK") != "1":
+        env = dict(os.environ, S24_STREAMK="1")
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", f"{__file__}::test_dense_dw_gemm_c2_shape_aligned_streamk[{m}-{n}]"],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+        return
+    from paper_2404_01847_b200.engine import gemm_dw
+    from paper_2404_01847_b200 import transposable_search_conv
+
+    k = 16384
+    torch.manual_seed(11)
+    w = torch.randn(m, n, device="cuda").bfloat16()
+    mask = transposable_search_conv(w)
+    a = torch.randn(k, m, device="cuda").bfloat16()
+    b = torch.randn(k, n, device="cuda").bfloat16()
+    lam = 0.5
+    outs = []
+    for _ in range(3):
+        out = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+        gemm_dw(a, True, b, True, m, n, k, out, w, mask.idx, lam)
+        outs.append(out)
+    ref = a.float().t() @ b.float() + lam * (1 - mask.bits.float()) * w.float()
+    assert torch.isfinite(outs[0]).all()
+    assert normwise_rel(outs[0].cpu(), ref.cpu()) < 2e-3
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
