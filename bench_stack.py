@@ -49,8 +49,7 @@ class StackStep:
         h = x
         for (w_in, bias, w2), (op_in, op_out) in zip(self.layers, self.ops):
             if refresh:
-                E.search_compress(w_in, op_in)
-                E.search_compress(w2, op_out)
+                E.search_compress_pair(w_in, op_in, w2, op_out)
             else:
                 E.compress_values_pair(w_in, op_in, w2, op_out)
             st = E.ffn_forward(h, op_in, bias, op_out, self.act, fused=True)
@@ -155,8 +154,8 @@ def run_stack(a, cfg):
     ms, clocks = B.time_loop(lambda: step(x, dy), steps, max(3, a.warmup // 4), dist if world > 1 else None,
                              local, True)
     t0 = max(3, a.warmup // 4)
-    refreshes = sum(1 for t in range(t0, t0 + steps) if t % B.REFRESH == 0)
-    launches_timed = steps * step.launches_per_step + refreshes * n_layers
+    # refresh steps: one K1 launch (both weights of a block) in place of the block's K2 launch
+    launches_timed = steps * step.launches_per_step
     ms_step = ms / steps
     value = n_tok * world / (ms_step / 1000.0)
 

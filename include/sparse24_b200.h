@@ -109,6 +109,13 @@ int s24_transposable_search(const void* w, int dtype, int64_t rows, int64_t cols
 int s24_search_compress(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* idx, uint16_t* fwd_vals,
                         uint8_t* fwd_e, uint16_t* bwd_vals, uint8_t* bwd_e, int64_t perm_ff, void* stream);
 
+/* K1 of two weights in one launch (the mask refresh of W_in and W2): same semantics as two
+ * s24_search_compress calls; one grid over both weights' 128 x 128 tiles. */
+int s24_search_compress_pair(const void* w0, const void* w1, int dtype, int64_t rows0, int64_t cols0, int64_t rows1,
+                             int64_t cols1, uint8_t* idx0, uint8_t* idx1, uint16_t* fwd_vals0, uint8_t* fwd_e0,
+                             uint16_t* bwd_vals0, uint8_t* bwd_e0, uint16_t* fwd_vals1, uint8_t* fwd_e1,
+                             uint16_t* bwd_vals1, uint8_t* bwd_e1, int64_t perm_ff0, int64_t perm_ff1, void* stream);
+
 /* ---- K2: per-step prune / compress with a cached mask ----------------------
  * Replaces _GatherPlan.product's gather `w.ravel()[take]` (gated_ffn.py:159-162)
  * for both orientations (in_fwd/in_bwd, out_fwd/out_bwd). */

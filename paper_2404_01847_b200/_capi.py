@@ -36,6 +36,8 @@ SIGNATURES = {
     "s24_device_check": [],
     "s24_transposable_search": [_P, _I, _I64, _I64, _P, _P],
     "s24_search_compress": [_P, _I, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P],
+    "s24_search_compress_pair": [_P, _P, _I, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                 _I64, _I64, _P],
     "s24_prune_compress": [_P, _I, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P],
     "s24_idx_to_bits": [_P, _I64, _I64, _P, _P],
     "s24_bits_to_idx": [_P, _I64, _I64, _P, _P, _P],

@@ -493,14 +493,19 @@ __device__ __forceinline__ int search_block_bf16w(const uint32_t (&wd)[8]) {
   return s24_search_tree(rp);
 }
 
-__global__ void __launch_bounds__(kPruneThreads, 2) search_bf16_kernel(MaskArgs p) {
+// p0's tiles are blocks [0, tiles0), p1's the rest (K1 of a block's two weights in one launch)
+__global__ void __launch_bounds__(kPruneThreads, 2) search_bf16_kernel(MaskArgs p0, MaskArgs p1, int tiles0) {
   __shared__ uint32_t s_bv[128 * 32];
   __shared__ __align__(16) uint32_t s_fe[512];
   __shared__ __align__(16) uint32_t s_be[512];
   __shared__ uint4 s_sel[90];
   __shared__ uint32_t s_nib[90];  // fwd row nibbles (bits 0-15) | bwd column nibbles (bits 16-31)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tr = blockIdx.y, tc = blockIdx.x;
+  const bool second = static_cast<int>(blockIdx.x) >= tiles0;
+  const MaskArgs& p = second ? p1 : p0;
+  const int64_t bid = second ? blockIdx.x - tiles0 : blockIdx.x;
+  const int64_t tiles_x = p.cols / kTile;
+  const int64_t tr = bid / tiles_x, tc = bid - tr * tiles_x;
   const int br = 2 * warp + (lane >> 4);
   const int c0 = 8 * (lane & 15);
   const int64_t grow0 = tr * kTile + 4 * br, gcol0 = tc * kTile + c0;
@@ -739,7 +744,8 @@ static int launch_mask(const MaskArgs& a, int dtype, bool search, cudaStream_t s
   const bool aligned = a.rows % kTile == 0 && a.cols % kTile == 0;
   if (search) {
     if (dtype == S24_BF16 && aligned) {
-      search_bf16_kernel<<<grid, kPruneThreads, 0, st>>>(a);
+      const int tiles = static_cast<int>(grid.x * grid.y);
+      search_bf16_kernel<<<tiles, kPruneThreads, 0, st>>>(a, a, tiles);
       return s24_check_launch("mask_search");
     }
     if (narrow) mask_tile_kernel<S24_BF16, true, true><<<grid, kThreads, 0, st>>>(a);
@@ -827,6 +833,33 @@ extern "C" int s24_prune_compress_pair(const void* w0, const void* w1, int dtype
   if (t0 + t1 == 0) return S24_OK;
   prune_bf16_kernel<<<t0 + t1, kPruneThreads, 0, st>>>(a0, a1, t0);
   return s24_check_launch("prune_compress_pair");
+}
+
+extern "C" int s24_search_compress_pair(const void* w0, const void* w1, int dtype, int64_t rows0, int64_t cols0,
+                                        int64_t rows1, int64_t cols1, uint8_t* idx0, uint8_t* idx1,
+                                        uint16_t* fwd_vals0, uint8_t* fwd_e0, uint16_t* bwd_vals0, uint8_t* bwd_e0,
+                                        uint16_t* fwd_vals1, uint8_t* fwd_e1, uint16_t* bwd_vals1, uint8_t* bwd_e1,
+                                        int64_t perm_ff0, int64_t perm_ff1, void* stream) {
+  if (int rc = check_perm(rows0, perm_ff0)) return rc;
+  if (int rc = check_perm(rows1, perm_ff1)) return rc;
+  if (int rc = check_w(w0, dtype, rows0, cols0)) return rc;
+  if (int rc = check_w(w1, dtype, rows1, cols1)) return rc;
+  S24_REQUIRE(idx0 != nullptr && idx1 != nullptr, S24_ERR_ARG, "idx pointer is NULL");
+  if (int rc = check_compress_outputs(rows0, cols0, fwd_e0, bwd_e0)) return rc;
+  if (int rc = check_compress_outputs(rows1, cols1, fwd_e1, bwd_e1)) return rc;
+  MaskArgs a0{w0, rows0, cols0, idx0, nullptr, fwd_vals0, fwd_e0, bwd_vals0, bwd_e0, perm_ff0};
+  MaskArgs a1{w1, rows1, cols1, idx1, nullptr, fwd_vals1, fwd_e1, bwd_vals1, bwd_e1, perm_ff1};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool fast = dtype == S24_BF16 && rows0 % kTile == 0 && cols0 % kTile == 0 && rows1 % kTile == 0 &&
+                    cols1 % kTile == 0;
+  if (!fast) {  // general shapes / dtypes: two launches of the tiled kernel
+    if (int rc = launch_mask(a0, dtype, true, st)) return rc;
+    return launch_mask(a1, dtype, true, st);
+  }
+  const int t0 = static_cast<int>((rows0 / kTile) * (cols0 / kTile)), t1 = static_cast<int>((rows1 / kTile) * (cols1 / kTile));
+  if (t0 + t1 == 0) return S24_OK;
+  search_bf16_kernel<<<t0 + t1, kPruneThreads, 0, st>>>(a0, a1, t0);
+  return s24_check_launch("search_compress_pair");
 }
 
 extern "C" int s24_idx_to_bits(const uint8_t* idx, int64_t rows, int64_t cols, uint8_t* bits, void* stream) {

@@ -93,6 +93,19 @@ def search_compress(w: torch.Tensor, op: CompressedOperand) -> None:
                op.perm_ff, C.stream_of(w))
 
 
+def search_compress_pair(w0: torch.Tensor, op0: CompressedOperand, w1: torch.Tensor,
+                         op1: CompressedOperand) -> None:
+    """K1 of both weights of a block in one launch (the mask refresh of W_in and W2)."""
+    if w0.dtype != w1.dtype:
+        raise ShapeError("search_compress_pair needs both weights in one dtype")
+    with TIMER("k1_search_compress"):
+        C.call("s24_search_compress_pair", w0.data_ptr(), w1.data_ptr(), C.dtype_code(w0), op0.rows, op0.cols,
+               op1.rows, op1.cols, op0.idx.data_ptr(), op1.idx.data_ptr(), op0.fwd_vals.data_ptr(),
+               op0.fwd_e.data_ptr(), op0.bwd_vals.data_ptr(), op0.bwd_e.data_ptr(), op1.fwd_vals.data_ptr(),
+               op1.fwd_e.data_ptr(), op1.bwd_vals.data_ptr(), op1.bwd_e.data_ptr(), op0.perm_ff, op1.perm_ff,
+               C.stream_of(w0))
+
+
 def compress_with_meta(w: torch.Tensor, op: CompressedOperand) -> None:
     """K2 with metadata: (re)build E tiles and values from a given mask (op.idx)."""
     C.call("s24_prune_compress", w.data_ptr(), C.dtype_code(w), op.rows, op.cols, op.idx.data_ptr(),

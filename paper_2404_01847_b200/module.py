@@ -81,8 +81,7 @@ class SparseFFN(torch.nn.Module):
 
     def refresh_masks(self) -> None:
         """K1: new transposable masks + both compressed orientations."""
-        E.search_compress(self.w_in.detach(), self.op_in)
-        E.search_compress(self.w2.detach(), self.op_out)
+        E.search_compress_pair(self.w_in.detach(), self.op_in, self.w2.detach(), self.op_out)
         self.steps_since_refresh = 0
         self.mask_searches += 2
 

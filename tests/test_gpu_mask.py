@@ -250,3 +250,25 @@ def test_k2_pair_launch_equals_two_single_launches(gated):
     E.compress_values_pair(w_in2, ops[1][0], w22, ops[1][1])
     for x, y in zip(ops[0], ops[1]):
         assert torch.equal(x.fwd_vals, y.fwd_vals) and torch.equal(x.bwd_vals, y.bwd_vals)
+
+
+@pytest.mark.parametrize("gated,dtype", [(False, torch.bfloat16), (True, torch.bfloat16), (False, torch.float32)])
+def test_k1_pair_launch_equals_two_single_launches(gated, dtype):
+    """s24_search_compress_pair (the mask refresh of both weights of a block in one launch) ==
+    two s24_search_compress calls: pattern indices, kept values and E tiles of both orientations."""
+    from paper_2404_01847_b200 import engine as E
+
+    d, d_ff = 256, 384
+    r_in = 2 * d_ff if gated else d_ff
+    torch.manual_seed(5)
+    w_in = torch.randn(r_in, d, device="cuda").to(dtype)
+    w2 = torch.randn(d, d_ff, device="cuda").to(dtype)
+    ops = [(E.CompressedOperand.empty(r_in, d, "cuda", perm_ff=d_ff if gated else 0),
+            E.CompressedOperand.empty(d, d_ff, "cuda")) for _ in range(2)]
+    E.search_compress(w_in, ops[0][0])
+    E.search_compress(w2, ops[0][1])
+    E.search_compress_pair(w_in, ops[1][0], w2, ops[1][1])
+    for x, y in zip(ops[0], ops[1]):
+        assert torch.equal(x.idx, y.idx)
+        assert torch.equal(x.fwd_vals, y.fwd_vals) and torch.equal(x.bwd_vals, y.bwd_vals)
+        assert torch.equal(x.fwd_e, y.fwd_e) and torch.equal(x.bwd_e, y.bwd_e)
