@@ -272,3 +272,37 @@ def test_k1_pair_launch_equals_two_single_launches(gated, dtype):
         assert torch.equal(x.idx, y.idx)
         assert torch.equal(x.fwd_vals, y.fwd_vals) and torch.equal(x.bwd_vals, y.bwd_vals)
         assert torch.equal(x.fwd_e, y.fwd_e) and torch.equal(x.bwd_e, y.bwd_e)
+
+
+@pytest.mark.parametrize("shape", [(256, 512), (132, 136)])
+def test_wide_exponent_span_bf16(shape):
+    """bf16 blocks with exponent spans 10..40 around the integer path's limit (13), with heavy
+    ties, zeros and subnormals: pattern indices equal the reference's float64 search
+    (tile-aligned shape: the fused K1 kernel; ragged shape: the general tiled kernel)."""
+    from paper_2404_01847_b200 import transposable_search_conv
+
+    rng = np.random.default_rng(17)
+    r, c = shape
+    nb = (r // 4) * (c // 4)
+    spans = rng.integers(10, 41, size=nb)
+    blocks = []
+    for s in spans:
+        mant = rng.integers(1, 5, size=16).astype(np.float64)  # small integers: many exact ties
+        ex = rng.integers(0, s + 1, size=16)
+        ex[rng.integers(0, 16)] = 0
+        ex[rng.integers(0, 16)] = s  # the block spans exactly s binades
+        b = mant * 2.0 ** (ex.astype(np.float64) - rng.integers(0, 60))
+        b[rng.random(16) < 0.15] = 0.0
+        if rng.random() < 0.05:
+            b[rng.integers(0, 16)] = 2.0 ** -130  # bf16 subnormal
+        b *= np.where(rng.random(16) < 0.5, -1.0, 1.0)
+        blocks.append(b.reshape(4, 4))
+    w = np.zeros((r, c))
+    k = 0
+    for i in range(r // 4):
+        for j in range(c // 4):
+            w[4 * i:4 * i + 4, 4 * j:4 * j + 4] = blocks[k]
+            k += 1
+    w = o.round_bf16(w)
+    m = transposable_search_conv(to_dev_bf16(w))
+    np.testing.assert_array_equal(m.idx.cpu().numpy(), o.search_pattern_idx(w))
