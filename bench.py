@@ -542,7 +542,7 @@ def run_ours(a, cfg):
     e1.record()
     torch.cuda.synchronize()
     opt_ms = e0.elapsed_time(e1) / reps
-    opt_bytes = el * (4 * 4 + 3 * 4 + 1 / 16)  # read w, g, u, v + write w, u, v (fp32) + mask idx
+    opt_bytes = w_in.numel() * (4 * 4 + 3 * 4 + 1 / 16)  # read w, g, u, v + write w, u, v (fp32) + mask idx
     opt_gbs = opt_bytes / (opt_ms * 1e-3) / 1e9
     optimizer_step = {"kernel": "s24_adam_step (fp32 state, ON_GRADIENTS masked decay)", "weight": list(w_in.shape),
                       "ms": opt_ms, "algorithmic_bytes": opt_bytes, "gbs": opt_gbs,

@@ -10,7 +10,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 for cfg in c2 c3 c5; do
   S24_CFG=$cfg ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 6 -c 6 \
       -o gpurun_out/prof_full_${TAG}_$cfg python tools/prof_one_step.py 2 > gpurun_out/prof_full_$cfg.log 2>&1
-  S24_CFG=$cfg ncu --set full --clock-control none --import-source on -k regex:"prune|search" -s 2 -c 2 \
+  S24_CFG=$cfg ncu --set full --clock-control none --import-source on -k regex:"prune|search" -s 0 -c 2 \
       -o gpurun_out/prof_mask_${TAG}_$cfg python tools/prof_one_step.py 2 > gpurun_out/prof_mask_$cfg.log 2>&1
 done
 ls -la gpurun_out
