@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(kPruneThreads, 2) search_bf16_kernel(MaskArgs 
   __shared__ uint32_t s_nib[90];  // fwd row nibbles (bits 0-15) | bwd column nibbles (bits 16-31)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool second = static_cast<int>(blockIdx.x) >= tiles0;
-  const MaskArgs& p = second ? p1 : p0;
+  const MaskArgs p = second ? p1 : p0;  // fields copied to registers once
   const int64_t bid = second ? blockIdx.x - tiles0 : blockIdx.x;
   const int64_t tiles_x = p.cols / kTile;
   const int64_t tr = bid / tiles_x, tc = bid - tr * tiles_x;
