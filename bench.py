@@ -1,29 +1,39 @@
 #!/usr/bin/env python
 """Benchmark of the 2:4-sparse FFN training hot path on B200 (bench contract).
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c4]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c4|c5]
+
+With no --config the headline line is the largest single-GPU configuration, C4
+(BASELINE.json configs[3]: d=12288, d_ff=49152, GELU, 16384 tokens per rank),
+and C3 (configs[2]: SwiGLU d=4096, d_ff=11008, 32768 tokens) is measured in the
+same run as a sub-line (`sub_lines.c3`); `--config` selects one configuration.
 
 A step = one FFN block fwd + bwd over the configuration's token batch:
 per-step prune/compress of both weights (K2), sparse fwd GEMMs (K3) with the
-fused bias+GELU epilogue or the gated activation (K6), sparse dX / dA GEMMs
-(K4), activation backward with fused bias gradients (K7), dense dW GEMMs with
+fused bias+GELU epilogue or the fused gated activation, sparse dX / dA GEMMs
+(K4) with the fused activation backward + bias gradients, dense dW GEMMs with
 the fused masked-decay epilogue (K5), and every 40th step the transposable
 mask search fused with compression (K1) instead of K2 (refresh period
-l = 40, optim.py:55).  N > 1: token-batch data parallelism (weak scaling, a
-fixed token batch per rank), one NCCL all-reduce of [dW_in, dbias, dW2] per
-step.  Inputs: synthetic, reference init (trainer.py:180-191).
+l = 40, optim.py:55).  The timed region starts on a refresh step, so any K
+timed steps contain ceil(K / 40) mask searches (at least the amortised share).
+N > 1: token-batch data parallelism (weak scaling, a fixed token batch per
+rank), one NCCL all-reduce of [dW_in, dbias, dW2] per step.  Inputs:
+synthetic, reference init (trainer.py:180-191).
 
-Reported (one JSON line on rank 0): tokens/s (value, whole job), the dense
-cuBLAS bf16 FFN on the same box (dense_tokens_per_s, speedup_vs_dense), e2e
-through the public autograd module with host-resident inputs, the roofline of
-the dominant kernel, per-kernel times, mask-search GB/s, clocks and the
-reference CPU path timed on the host (cpu_baseline).
+Reported (one JSON line on rank 0): tokens/s (value, whole job); e2e through
+the public autograd module with host-resident inputs; the roofline of the
+dominant kernel; per-kernel times; mask-search GB/s; clocks; the reference CPU
+path timed on the host (cpu_baseline); and, at the END of the line, the dense
+bf16 FFN on the same box three ways -- eager autograd on cuBLAS, the same fused
+tensor-core kernels on dense weights (bias/GELU/dGELU/bias-gradient epilogues,
+`dense_fused`), and the six cuBLAS GEMMs alone (a floor) -- with the speed-ups.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -40,7 +50,7 @@ CONFIGS = {
     # configs[2]: SwiGLU d=4096 d_ff=11008, 32k tokens, fused gated activation + masked decay
     "c3": dict(workload="SwiGLU FFN d=4096 d_ff=11008, 32768 tokens (BASELINE.json configs[2])",
                d=4096, d_ff=11008, act="swiglu", tokens=32768),
-    # configs[3] at its N=16384 point
+    # configs[3] at its N=16384 point: the largest single-GPU configuration (the default headline)
     "c4": dict(workload="large FFN d=12288 d_ff=49152 GELU, 16384 tokens (BASELINE.json configs[3])",
                d=12288, d_ff=49152, act="gelu", tokens=16384),
     # configs[4]: GPT-2 large 2:4 pre-training step -- the 36-block residual FFN stack
@@ -49,24 +59,39 @@ CONFIGS = {
                         "(BASELINE.json configs[4])",
                d=1280, d_ff=5120, act="gelu", tokens=16384, layers=36),
 }
+DEFAULT_CONFIG, DEFAULT_SUB = "c4", ("c3",)
 REFRESH = 40
 DP_RESERVED_SMS = int(os.environ.get("S24_DP_RESERVED_SMS", "16"))  # SMs the dX GEMM leaves to NCCL (N > 1)
 LAMBDA = 6e-5
 METRIC = "2:4 FFN fwd+bwd tokens/s & speedup vs dense bf16; mask-search HBM GB/s"
+SUSTAINED_AFTER_MS = 2000.0  # attribution loops at least this long are judged against the sustained peak
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=400)
-    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--steps", type=int, default=40)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    p.add_argument("--config", default=None, choices=sorted(CONFIGS))
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-dense", action="store_true")
-    p.add_argument("--ref-tokens", type=int, default=64)
+    p.add_argument("--no-sub", action="store_true", help="skip the C3 sub-line of the default run")
+    p.add_argument("--ref-tokens", type=int, default=32)
     p.add_argument("--tokens", type=int, default=0, help="override the config's tokens per rank (C4 sweep)")
     return p.parse_args()
+
+
+def config_dict(cfg, world, backend="nccl", shared=False):
+    """The `config` object of both arms' JSON lines (same workload keys)."""
+    out = {"workload": cfg["workload"], "d_model": cfg["d"], "d_ff": cfg["d_ff"], "act": cfg["act"],
+           "tokens_per_rank": cfg["tokens"], "mask_refresh_every": REFRESH, "lambda_w": LAMBDA,
+           "parallelism": f"dp{world}",
+           "dp_backend": backend + (" (ranks share GPUs: functional test only)" if shared else ""),
+           "l2": "per-step working set > 126 MB L2 (inputs larger than L2, no flush)"}
+    if cfg.get("layers", 1) > 1:
+        out["layers"] = cfg["layers"]
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -75,10 +100,21 @@ def parse():
 
 def _ref_worker(args):
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    cfg, tokens, steps, warmup = args
+    cfg, tokens, steps, warmup, dfs = args
     from oracle.ref_step import time_reference
-    per, info = time_reference(cfg["d"], cfg["d_ff"], cfg["act"], tokens, steps, warmup=warmup, refresh=REFRESH)
+    per, info = time_reference(cfg["d"], cfg["d_ff"], cfg["act"], tokens, steps, warmup=warmup, refresh=REFRESH,
+                               d_ff_sample=dfs)
     return tokens / per, per, info
+
+
+def _ref_sample_text(cfg, tokens, steps, dfs, procs):
+    layers = cfg.get("layers", 1)
+    sl = (f"; a {dfs}-wide slice of the {cfg['d_ff']} hidden units (both weights), tokens/s scaled by "
+          f"{dfs}/{cfg['d_ff']} (every term of the step is linear in d_ff)" if dfs != cfg["d_ff"] else "")
+    return (f"{procs} process(es) x {tokens} tokens x {steps} step(s) of the {cfg['workload']} step "
+            f"(fwd + bwd mvue=False + masked decay; mask search of both weights amortized /{REFRESH}){sl}; "
+            f"reference Cython kernels single-threaded per process"
+            + (f"; one block timed, tokens/s divided by the {layers} blocks of the stack" if layers > 1 else ""))
 
 
 def run_reference(a, cfg):
@@ -87,27 +123,27 @@ def run_reference(a, cfg):
         return
     import multiprocessing as mp
 
+    from oracle.ref_step import ref_slice
+
     procs = os.cpu_count() or 1
+    dfs = ref_slice(cfg["d"], cfg["d_ff"], cfg["act"])
     # every core runs the same bounded token sample; tokens/s aggregate = sum
     steps = max(1, min(a.steps, 3))
     with mp.get_context("spawn").Pool(procs) as pool:
         t0 = time.perf_counter()
-        res = pool.map(_ref_worker, [(cfg, a.ref_tokens, steps, max(0, min(a.warmup, 1)))] * procs)
+        res = pool.map(_ref_worker, [(cfg, a.ref_tokens, steps, max(0, min(a.warmup, 1)), dfs)] * procs)
         wall = time.perf_counter() - t0
     layers = cfg.get("layers", 1)
     # a stack of L identical blocks costs L block steps per token batch
     value = sum(r[0] for r in res) / layers
     kind = res[0][2]["kind"]
-    sample = (f"{procs} processes x {a.ref_tokens} tokens x {steps} steps of the {cfg['workload']} step "
-              f"(fwd + bwd mvue=False + masked decay; mask search of both weights amortized /{REFRESH}); "
-              f"reference Cython kernels single-threaded per process"
-              + (f"; one block timed, tokens/s divided by the {layers} blocks of the stack" if layers > 1 else ""))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": a.gpus,
-        "steps": steps, "warmup": a.warmup, "ms_per_step": 1000.0 * a.ref_tokens * procs / value,
+        "steps": steps, "warmup": a.warmup, "ms_per_step": 1000.0 * cfg["tokens"] / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference init)", "config": {"workload": cfg["workload"], "tokens_per_step": cfg["tokens"]},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": procs, "kind": kind, "sample": sample},
+        "data": "synthetic (reference init)", "config": config_dict(cfg, a.gpus, backend="none (host CPU)"),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": procs, "kind": kind,
+                         "sample": _ref_sample_text(cfg, a.ref_tokens, steps, dfs, procs)},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
@@ -253,8 +289,8 @@ class SparseStep:
         self.dw2 = self.bucket[n_in + n_b:].view(w2.shape)
         self.t = 0
         self.mvue = mvue
-        # our kernel launches per step: K2 (both weights; K1 x2 every 40th step), fwd 2 sparse GEMMs,
-        # bwd 2 sparse + 2 dW GEMMs (+2 MVUE sparsifiers); activations fused into the GEMM epilogues
+        # our kernel launches per step: K2 (both weights; K1 on the refresh step), fwd 2 sparse
+        # GEMMs, bwd 2 sparse + 2 dW GEMMs (+2 MVUE sparsifiers); activations fused into the GEMMs
         self.launches_per_step = 1 + 2 + 4 + (2 if mvue else 0)
 
     def __call__(self, x, dy):
@@ -283,6 +319,31 @@ class SparseStep:
             w.wait()
         self.t += 1
         return st, g
+
+
+class DenseFusedStep:
+    """The dense bf16 FFN step on the SAME tensor-core kernels and fused epilogues as the 2:4
+    step (s24_gemm_act: bias + GELU / GELU' or the gated activation in GEMM1, dGELU + bias
+    gradient in GEMM3; the dense dW GEMMs): the fair dense comparator, and the dense fine-tune
+    phase's path (gated_ffn.py:286-289, trainer.py:111-114)."""
+
+    def __init__(self, w_in, bias, w2, act):
+        import torch
+        from paper_2404_01847_b200 import engine as E
+
+        self.E = E
+        self.act = act
+        self.op_in = E.DenseOperand.of(w_in, w2.shape[1] if act in E.GATED else 0)
+        self.op_out = E.DenseOperand.of(w2)
+        self.bias = bias
+        self.dw_in = torch.empty(w_in.shape, dtype=torch.float32, device=w_in.device)
+        self.dw2 = torch.empty(w2.shape, dtype=torch.float32, device=w2.device)
+        self.dbias = torch.empty(w_in.shape[0], dtype=torch.float32, device=w_in.device)
+
+    def __call__(self, x, dy):
+        st = self.E.ffn_forward(x, self.op_in, self.bias, self.op_out, self.act, fused=True)
+        return self.E.ffn_backward(st, dy, self.op_in, self.op_out, self.act, dw_in_out=self.dw_in,
+                                   dw2_out=self.dw2, dbias_out=self.dbias)
 
 
 def dense_step_factory(w_in, bias, w2, act):
@@ -341,11 +402,13 @@ def dense_gemm_only_factory(w_in, w2, x, dy):
     return step
 
 
-def time_loop(fn, steps, warmup, dist=None, dev_index=0, sample_clocks=False):
+def time_loop(fn, steps, warmup, dist=None, dev_index=0, sample_clocks=False, before_timed=None):
     import torch
 
     for _ in range(warmup):
         fn()
+    if before_timed is not None:
+        before_timed()
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
@@ -395,7 +458,200 @@ def ncu_traffic(cfg_name, tag):
         return None
 
 
-def run_ours(a, cfg):
+def gemm_flops(cfg, r_in):
+    """Algorithmic dense-equivalent flops per launch (2 M N K) of the six GEMMs of a step."""
+    d, d_ff, n = cfg["d"], cfg["d_ff"], cfg["tokens"]
+    return {"k3_spmm_fwd_in": 2.0 * r_in * n * d, "k3_spmm_fwd_out": 2.0 * d * n * d_ff,
+            "k4_spmm_bwd_out": 2.0 * d_ff * n * d, "k4_spmm_bwd_in": 2.0 * d * n * r_in,
+            "k5_gemm_dw2": 2.0 * d * d_ff * n, "k5_gemm_dw_in": 2.0 * r_in * d * n}
+
+
+def attribute(step, x, dy, cfg, cfg_name, r_in):
+    """Per-kernel times (CUDA events on the launching stream) over 2 refresh periods of steps,
+    the roofline of the dominant kernel against the burst or sustained peak (by loop length)."""
+    import torch
+    from paper_2404_01847_b200 import engine as E
+
+    timer = EventTimer()
+    E.TIMER = timer
+    kt_steps = 2 * REFRESH
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(kt_steps):
+        step(x, dy)
+    e1.record()
+    totals = timer.totals()
+    loop_ms = e0.elapsed_time(e1)
+    E.TIMER = E._NoTimer()
+    per_kernel = {k: {"ms_per_launch": v[0] / v[1], "launches": v[1], "ms_per_step": v[0] / kt_steps}
+                  for k, v in sorted(totals.items())}
+    peaks, peaks_src = load_peaks()
+    sustained = loop_ms >= SUSTAINED_AFTER_MS
+    dense_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) if sustained else peaks["bf16_tflops"]
+    peak_kind = (f"sustained (attribution loop {loop_ms / 1e3:.1f} s >= {SUSTAINED_AFTER_MS / 1e3:.0f} s)" if sustained
+                 else f"burst (attribution loop {loop_ms / 1e3:.2f} s < {SUSTAINED_AFTER_MS / 1e3:.0f} s)")
+    flops = gemm_flops(cfg, r_in)
+    for k, f in flops.items():
+        if k in per_kernel:
+            sp = k.startswith(("k3", "k4"))
+            per_kernel[k]["tflops_dense_equiv"] = f / (per_kernel[k]["ms_per_launch"] * 1e-3) / 1e12
+            per_kernel[k]["frac_of_peak"] = per_kernel[k]["tflops_dense_equiv"] / (dense_peak * (2.0 if sp else 1.0))
+    dom = max((k for k in per_kernel if k in flops), key=lambda k: per_kernel[k]["ms_per_step"])
+    sparse = dom.startswith(("k3", "k4"))
+    achieved = per_kernel[dom]["tflops_dense_equiv"]
+    peak = dense_peak * (2.0 if sparse else 1.0)
+    roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(cfg_name, dom), "peak_kind": peak_kind,
+            "note": ("dense-equivalent 2MNK / t vs 2x the measured dense bf16 peak (2:4 pipe)" if sparse
+                     else "2MNK / t vs the measured dense bf16 peak") + f" ({peaks_src} MEASURED_PEAKS.json)"}
+    return per_kernel, roof, peaks
+
+
+def cpu_baseline_leg(cfg, a):
+    """The reference CPU path (compiled reference kernels, 1 core) on a bounded sample."""
+    try:
+        from oracle.ref_step import ref_slice, time_reference
+
+        toks = a.ref_tokens
+        dfs = ref_slice(cfg["d"], cfg["d_ff"], cfg["act"])
+        per, info = time_reference(cfg["d"], cfg["d_ff"], cfg["act"], toks, steps=3, warmup=1, refresh=REFRESH,
+                                   budget_s=20, d_ff_sample=dfs)
+        layers = cfg.get("layers", 1)
+        return {"value": toks / per / layers, "unit": "tokens/s", "cores": info["cores"], "kind": info["kind"],
+                "sample": _ref_sample_text(cfg, toks, info["steps"], dfs, 1)}
+    except Exception as exc:  # pragma: no cover
+        return {"value": None, "unit": "tokens/s", "cores": 0, "kind": "port", "sample": f"failed: {exc!r}"}
+
+
+def measure(a, cfg, cfg_name, dev, world, rank, local, pg, dist, full=True):
+    """One configuration on the engine: the timed headline plus everything the JSON line reports.
+    full=False (a sub-line) skips the variants and the standalone kernel micro-benchmarks."""
+    import torch
+    from paper_2404_01847_b200 import _capi as C
+    from paper_2404_01847_b200 import engine as E
+
+    w_in, bias, w2, x, dy = make_problem(cfg, dev, seed=1234 + rank)
+    n_tok = cfg["tokens"]
+    step = SparseStep(w_in, bias, w2, cfg["act"], world, pg)
+    dd = dist if world > 1 else None
+
+    def align():
+        step.t = 0  # the timed region starts on a refresh step: ceil(K / 40) K1 searches in K steps
+
+    ms, clocks = time_loop(lambda: step(x, dy), a.steps, a.warmup, dd, local, True, before_timed=align)
+    refreshes = math.ceil(a.steps / REFRESH)
+    launches_timed = a.steps * step.launches_per_step
+    ms_step = ms / a.steps
+    value = n_tok * world / (ms_step / 1000.0)
+    out = {"value": value, "ms_per_step": ms_step, "clocks": clocks, "gpu_launches": launches_timed,
+           "refresh_steps_timed": refreshes}
+
+    # ---- per-kernel attribution + roofline ----
+    per_kernel, roof, peaks = attribute(step, x, dy, cfg, cfg_name, w_in.shape[0])
+    out["roofline"] = roof
+    out["kernels"] = {k: {kk: (round(vv, 5) if isinstance(vv, float) else vv) for kk, vv in v.items()
+                          if kk in ("ms_per_launch", "frac_of_peak")} for k, v in per_kernel.items()}
+
+    # ---- mask search (K1 fused, both weights in one launch, the refresh step) and the per-step
+    # prune (K2, both weights in one launch): HBM GB/s, timed alone ----
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def _t(fn, r=reps):
+        fn()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(r):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / r
+
+    el = w_in.numel() + w2.numel()
+    k1_ms = _t(lambda: E.search_compress_pair(w_in, step.op_in, w2, step.op_out))
+    k1_bytes = el * (2 * 2 + 0.3125)  # read bf16 W + idx + 2 orientations of values + meta (SURVEY 8d)
+    k1_gbs = k1_bytes / (k1_ms * 1e-3) / 1e9
+    k2_ms = _t(lambda: E.compress_values_pair(w_in, step.op_in, w2, step.op_out))
+    k2_gbs = el * (2 * 2 + 1 / 16) / (k2_ms * 1e-3) / 1e9
+    out["mask_search"] = {"ms": k1_ms, "gbs": k1_gbs, "frac_of_hbm": k1_gbs / peaks["hbm_gbs"],
+                          "k2_prune_compress": {"ms": k2_ms, "gbs": k2_gbs, "frac_of_hbm": k2_gbs / peaks["hbm_gbs"]}}
+
+    if full:
+        # ---- variant: MVUE-sparsified dW (the reference default fst_backward(mvue=True)) ----
+        variants = {}
+        for mode in ("fast", "exact"):
+            mstep = SparseStep(w_in, bias, w2, cfg["act"], world, pg, mvue=mode)
+            msteps = 10
+            mms, _ = time_loop(lambda: mstep(x, dy), msteps, 3, dd)
+            variants[f"mvue_dw_{mode}"] = {"tokens_per_s": n_tok * world / (mms / msteps / 1000.0)}
+            del mstep
+        out["variants"] = variants
+
+        # ---- fused optimizer step (Adam + masked decay, SURVEY 8(f) #2) on W_in, fp32 state ----
+        from paper_2404_01847_b200.optim import DecayConfig, DecayMode, OptimizerState, adam_step
+        from paper_2404_01847_b200.sparsity import TransposableMask
+
+        ost = OptimizerState.init(w_in, dtype=torch.float32)
+        omask = TransposableMask(step.op_in.mask_idx(), tuple(w_in.shape))
+        ocfg = DecayConfig(lambda_w=LAMBDA, mode=DecayMode.ON_GRADIENTS)
+        opt_ms = _t(lambda: adam_step(ost, step.dw_in, omask, ocfg))
+        opt_bytes = w_in.numel() * (4 * 4 + 3 * 4 + 1 / 16)  # read w, g, u, v + write w, u, v (fp32) + mask idx
+        out["optimizer_step"] = {"ms": opt_ms, "gbs": opt_bytes / (opt_ms * 1e-3) / 1e9,
+                                 "frac_of_hbm": opt_bytes / (opt_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+        del ost
+
+        # ---- standalone activation kernels (K6/K7: the API's unfused path) ----
+        r_act, r_in_act = w2.shape[1], w_in.shape[0]
+        zc = torch.randn(n_tok, r_in_act, device=dev).to(torch.bfloat16)
+        ac = torch.empty(n_tok, r_act, dtype=torch.bfloat16, device=dev)
+        dac = torch.randn(n_tok, r_act, device=dev).to(torch.bfloat16)
+        dzc = torch.empty_like(zc)
+        dbc = torch.empty(r_in_act, dtype=torch.float32, device=dev)
+        code = E.ACT_CODES[cfg["act"]]
+        f_ms = _t(lambda: C.call("s24_act_fwd", zc.data_ptr(), r_in_act, r_act, n_tok, code, ac.data_ptr(), r_act,
+                                 C.stream_of(zc)))
+        b_ms = _t(lambda: C.call("s24_act_bwd", zc.data_ptr(), r_in_act, dac.data_ptr(), r_act, r_act, n_tok, code,
+                                 dzc.data_ptr(), r_in_act, dbc.data_ptr(), C.stream_of(zc)))
+        gated = r_in_act == 2 * r_act
+        f_bytes = n_tok * r_act * 2 * (3 if gated else 2)  # SURVEY 8(d): K6 fwd
+        b_bytes = n_tok * r_act * 2 * (5 if gated else 3) + r_in_act * 4  # K7 bwd + fp32 bias grads
+        out["activation"] = {"fwd_gbs": f_bytes / (f_ms * 1e-3) / 1e9, "bwd_gbs": b_bytes / (b_ms * 1e-3) / 1e9}
+        del zc, ac, dac, dzc, dbc
+
+    # ---- e2e through the public autograd module, host-resident inputs ----
+    out["e2e"] = run_e2e(a, cfg, w_in, bias, w2, dev, world, dd)
+
+    # ---- dense bf16 FFN on the same box: eager autograd (cuBLAS), the same fused tensor-core
+    # kernels on dense weights, and the six cuBLAS GEMMs alone ----
+    if not a.no_dense:
+        dsteps = 10
+        dstep = dense_step_factory(w_in, bias, w2, cfg["act"])
+        dms, _ = time_loop(lambda: dstep(x, dy), dsteps, 3, dd)
+        out["dense_tokens_per_s"] = n_tok * world / (dms / dsteps / 1000.0)
+        del dstep
+        fstep = DenseFusedStep(w_in, bias, w2, cfg["act"])
+        fms, _ = time_loop(lambda: fstep(x, dy), dsteps, 3, dd)
+        out["dense_fused_tokens_per_s"] = n_tok * world / (fms / dsteps / 1000.0)
+        del fstep
+        gstep = dense_gemm_only_factory(w_in, w2, x, dy)
+        gms, _ = time_loop(gstep, dsteps, 3, dd)
+        out["dense_gemm_only_tokens_per_s"] = n_tok * world / (gms / dsteps / 1000.0)
+        del gstep
+        out["speedup_vs_dense"] = value / out["dense_tokens_per_s"]
+        out["speedup_vs_dense_fused"] = value / out["dense_fused_tokens_per_s"]
+        out["speedup_vs_dense_gemm_only"] = value / out["dense_gemm_only_tokens_per_s"]
+        best = max(out["dense_tokens_per_s"], out["dense_fused_tokens_per_s"])
+        out["speedup_vs_best_dense"] = value / best
+        if full and "variants" in out:
+            for v in out["variants"].values():
+                v["speedup_vs_best_dense"] = v["tokens_per_s"] / best
+    del step, w_in, bias, w2, x, dy
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(a, cfg, cfg_name, subs):
     import torch
     import torch.distributed as dist
 
@@ -418,212 +674,45 @@ def run_ours(a, cfg):
             dist.init_process_group("nccl", device_id=dev)
         pg = dist.group.WORLD
     from paper_2404_01847_b200 import _capi as C
-    from paper_2404_01847_b200 import engine as E
 
     C.load()
     C.call("s24_device_check")
-    w_in, bias, w2, x, dy = make_problem(cfg, dev, seed=1234 + rank)
-    n_tok = cfg["tokens"]
-    step = SparseStep(w_in, bias, w2, cfg["act"], world, pg)
-
-    # ---- headline: device-resident inputs ----
-    ms, clocks = time_loop(lambda: step(x, dy), a.steps, a.warmup, dist if world > 1 else None, local, True)
-    # our launches in the timed region: the refresh steps (t % 40 == 0) run one K1 launch (both
-    # weights) in place of the one K2 launch
-    launches_timed = a.steps * step.launches_per_step
-    ms_step = ms / a.steps
-    value = n_tok * world / (ms_step / 1000.0)
-
-    # ---- variant: MVUE-sparsified dW (the reference default fst_backward(mvue=True)) ----
-    variants = {}
-    for mode in ("fast", "exact"):
-        mstep = SparseStep(w_in, bias, w2, cfg["act"], world, pg, mvue=mode)
-        msteps = max(10, a.steps // 4)
-        mms, _ = time_loop(lambda: mstep(x, dy), msteps, a.warmup, dist if world > 1 else None)
-        variants[f"mvue_dw_{mode}"] = {
-            "tokens_per_s": n_tok * world / (mms / msteps / 1000.0), "ms_per_step": mms / msteps,
-            "note": ("dW GEMMs on MVUE-sparsified dY^T / dZ^T (K8 + 2:4 tensor cores), gated_ffn.py:367-373; "
-                     + ("float64 + numpy PCG64 stream, bit-identical draws" if mode == "exact"
-                        else "fp32 + counter RNG, unbiased"))}
-        del mstep
-
-    # ---- dense cuBLAS bf16 baseline on the same box ----
-    dense = dense_gemm_only = None
-    if not a.no_dense:
-        dstep = dense_step_factory(w_in, bias, w2, cfg["act"])
-        dms, _ = time_loop(lambda: dstep(x, dy), max(10, a.steps // 4), a.warmup, dist if world > 1 else None)
-        dense = n_tok * world / (dms / max(10, a.steps // 4) / 1000.0)
-        del dstep
-        # lower bound of any dense implementation: the step's six cuBLAS GEMMs alone
-        gstep = dense_gemm_only_factory(w_in, w2, x, dy)
-        gms, _ = time_loop(gstep, max(10, a.steps // 4), a.warmup, dist if world > 1 else None)
-        dense_gemm_only = n_tok * world / (gms / max(10, a.steps // 4) / 1000.0)
-        del gstep
-
-    # ---- per-kernel attribution (CUDA events on the launching stream) ----
-    timer = EventTimer()
-    E.TIMER = timer
-    kt_steps = 2 * REFRESH
-    for _ in range(kt_steps):
-        step(x, dy)
-    totals = timer.totals()
-    E.TIMER = E._NoTimer()
-    per_kernel = {k: {"ms_per_launch": v[0] / v[1], "launches": v[1], "ms_per_step": v[0] / kt_steps}
-                  for k, v in sorted(totals.items())}
-
-    # ---- roofline of the dominant kernel ----
-    peaks, peaks_src = load_peaks()
-    d, d_ff, r_in = cfg["d"], cfg["d_ff"], w_in.shape[0]
-    flops = {  # algorithmic dense-equivalent flops per launch (2 M N K)
-        "k3_spmm_fwd_in": 2.0 * r_in * n_tok * d, "k3_spmm_fwd_out": 2.0 * d * n_tok * d_ff,
-        "k4_spmm_bwd_out": 2.0 * d_ff * n_tok * d, "k4_spmm_bwd_in": 2.0 * d * n_tok * r_in,
-        "k5_gemm_dw2": 2.0 * d * d_ff * n_tok, "k5_gemm_dw_in": 2.0 * r_in * d * n_tok,
-    }
-    dom = max(per_kernel.items(), key=lambda kv: kv[1]["ms_per_step"])[0]
-    sustained = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    if dom in flops:
-        sparse = dom.startswith(("k3", "k4"))
-        achieved = flops[dom] / (per_kernel[dom]["ms_per_launch"] * 1e-3) / 1e12
-        # a 2:4 GEMM executes half the MACs: its tensor-pipe peak is 2x the dense peak
-        peak = sustained * (2.0 if sparse else 1.0)
-        roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(a.config, dom),
-                "note": ("dense-equivalent 2MNK / t vs 2x measured sustained dense bf16 peak (2:4 pipe)" if sparse
-                         else "2MNK / t vs measured sustained dense bf16 peak") + f" ({peaks_src})"}
-    else:
-        roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": None, "traffic": None}
-    for k, f in flops.items():
-        if k in per_kernel:
-            sp = k.startswith(("k3", "k4"))
-            per_kernel[k]["tflops_dense_equiv"] = f / (per_kernel[k]["ms_per_launch"] * 1e-3) / 1e12
-            per_kernel[k]["frac_of_peak"] = per_kernel[k]["tflops_dense_equiv"] / (sustained * (2.0 if sp else 1.0))
-
-    # ---- mask search (K1 fused, both weights of the block in one launch, as on the refresh step)
-    # and the per-step prune (K2, both weights in one launch): HBM GB/s, timed alone ----
-    reps = 20
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    E.search_compress_pair(w_in, step.op_in, w2, step.op_out)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
-        E.search_compress_pair(w_in, step.op_in, w2, step.op_out)
-    e1.record()
-    torch.cuda.synchronize()
-    k1_ms = e0.elapsed_time(e1) / reps
-    el = w_in.numel() + w2.numel()
-    k1_bytes = el * (2 * 2 + 0.3125)  # read bf16 W + idx + 2 orientations of values + meta
-    k1_gbs = k1_bytes / (k1_ms * 1e-3) / 1e9
-    mask_search = {"weight": [list(w_in.shape), list(w2.shape)], "ms": k1_ms, "algorithmic_bytes": k1_bytes,
-                   "gbs": k1_gbs, "frac_of_hbm": k1_gbs / peaks["hbm_gbs"],
-                   "launch": "s24_search_compress_pair (both weights of the block, one grid)"}
-    e0.record()
-    for _ in range(reps):
-        E.compress_values_pair(w_in, step.op_in, w2, step.op_out)
-    e1.record()
-    torch.cuda.synchronize()
-    k2_ms = e0.elapsed_time(e1) / reps
-    k2_gbs = el * (2 * 2 + 1 / 16) / (k2_ms * 1e-3) / 1e9
-    mask_search["k2_prune_compress"] = {"ms": k2_ms, "gbs": k2_gbs, "frac_of_hbm": k2_gbs / peaks["hbm_gbs"]}
-
-    # ---- fused optimizer step (Adam + masked decay) on W_in, fp32 state ----
-    from paper_2404_01847_b200.optim import DecayConfig, DecayMode, OptimizerState, adam_step
-    from paper_2404_01847_b200.sparsity import TransposableMask
-
-    ost = OptimizerState.init(w_in, dtype=torch.float32)
-    omask = TransposableMask(step.op_in.mask_idx(), tuple(w_in.shape))
-    ocfg = DecayConfig(lambda_w=LAMBDA, mode=DecayMode.ON_GRADIENTS)
-    gfp = step.dw_in
-    adam_step(ost, gfp, omask, ocfg)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
-        adam_step(ost, gfp, omask, ocfg)
-    e1.record()
-    torch.cuda.synchronize()
-    opt_ms = e0.elapsed_time(e1) / reps
-    opt_bytes = w_in.numel() * (4 * 4 + 3 * 4 + 1 / 16)  # read w, g, u, v + write w, u, v (fp32) + mask idx
-    opt_gbs = opt_bytes / (opt_ms * 1e-3) / 1e9
-    optimizer_step = {"kernel": "s24_adam_step (fp32 state, ON_GRADIENTS masked decay)", "weight": list(w_in.shape),
-                      "ms": opt_ms, "algorithmic_bytes": opt_bytes, "gbs": opt_gbs,
-                      "frac_of_hbm": opt_gbs / peaks["hbm_gbs"]}
-    del ost
-
-    # ---- standalone activation kernels (K6/K7: the API's unfused path; the training step fuses
-    # the activation into the GEMM epilogues) at this config's token batch ----
-    r_act = w2.shape[1]
-    r_in_act = w_in.shape[0]
-    zc = torch.randn(n_tok, r_in_act, device=dev).to(torch.bfloat16)
-    ac = torch.empty(n_tok, r_act, dtype=torch.bfloat16, device=dev)
-    dac = torch.randn(n_tok, r_act, device=dev).to(torch.bfloat16)
-    dzc = torch.empty_like(zc)
-    dbc = torch.empty(r_in_act, dtype=torch.float32, device=dev)
-    code = E.ACT_CODES[cfg["act"]]
-
-    def _t(fn):
-        fn()
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(reps):
-            fn()
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / reps
-
-    f_ms = _t(lambda: C.call("s24_act_fwd", zc.data_ptr(), r_in_act, r_act, n_tok, code, ac.data_ptr(), r_act,
-                             C.stream_of(zc)))
-    b_ms = _t(lambda: C.call("s24_act_bwd", zc.data_ptr(), r_in_act, dac.data_ptr(), r_act, r_act, n_tok, code,
-                             dzc.data_ptr(), r_in_act, dbc.data_ptr(), C.stream_of(zc)))
-    gated = r_in_act == 2 * r_act
-    f_bytes = n_tok * r_act * 2 * (3 if gated else 2)  # K6 fwd
-    b_bytes = n_tok * r_act * 2 * (5 if gated else 3) + r_in_act * 4  # K7 bwd + fp32 bias grads
-    activation = {"kernels": "s24_act_fwd / s24_act_bwd (standalone; fused into the GEMM epilogues on the step)",
-                  "fwd": {"ms": f_ms, "gbs": f_bytes / (f_ms * 1e-3) / 1e9,
-                          "frac_of_hbm": f_bytes / (f_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
-                  "bwd": {"ms": b_ms, "gbs": b_bytes / (b_ms * 1e-3) / 1e9,
-                          "frac_of_hbm": b_bytes / (b_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}}
-    del zc, ac, dac, dzc, dbc
-
-    # ---- e2e through the public autograd module, host-resident inputs ----
-    e2e = run_e2e(a, cfg, w_in, bias, w2, dev, world, dist if world > 1 else None)
-
-    # ---- reference CPU path on the host (rank 0, N=1 only) ----
+    res = measure(a, cfg, cfg_name, dev, world, rank, local, pg, dist, full=True)
+    sub_res = {}
+    for sn in subs:
+        scfg = dict(CONFIGS[sn])
+        r = measure(a, scfg, sn, dev, world, rank, local, pg, dist, full=False)
+        sub_res[sn] = {"workload": scfg["workload"], "value": r["value"], "unit": "tokens/s",
+                       "ms_per_step": r["ms_per_step"], "clocks": r["clocks"], "e2e": r["e2e"]["value"],
+                       "roofline_frac": r["roofline"]["frac"], "mask_search_gbs": r["mask_search"]["gbs"],
+                       **{k: r[k] for k in ("dense_tokens_per_s", "dense_fused_tokens_per_s",
+                                            "dense_gemm_only_tokens_per_s", "speedup_vs_dense",
+                                            "speedup_vs_dense_fused", "speedup_vs_dense_gemm_only",
+                                            "speedup_vs_best_dense") if k in r}}
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        try:
-            from oracle.ref_step import time_reference
-
-            toks = 32
-            per, info = time_reference(d, d_ff, cfg["act"], toks, steps=4, warmup=1, refresh=REFRESH, budget_s=20)
-            cpu = {"value": toks / per, "unit": "tokens/s", "cores": info["cores"], "kind": info["kind"],
-                   "sample": f"{toks} tokens x {info['steps']} steps of the same FFN block step (fwd+bwd mvue=False, "
-                             f"masked decay, mask search /{REFRESH}), reference Cython kernels on 1 core"}
-        except Exception as exc:  # pragma: no cover
-            cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "port", "sample": f"failed: {exc!r}"}
+        cpu = cpu_baseline_leg(cfg, a)
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "metric": METRIC, "value": res["value"], "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (reference init N(0,1)/sqrt(fan_in) weights, N(0,1) tokens)",
-            "config": {"workload": cfg["workload"], "d_model": cfg["d"], "d_ff": cfg["d_ff"], "act": cfg["act"],
-                       "tokens_per_rank": n_tok, "mask_refresh_every": REFRESH, "lambda_w": LAMBDA,
-                       "parallelism": f"dp{world}", "dp_backend": backend + (" (ranks share GPUs: functional test only)" if shared else ""),
-                       "l2": "per-step working set ~1 GB > 126 MB L2 (no flush)"},
-            "dense_tokens_per_s": dense, "speedup_vs_dense": (value / dense) if dense else None,
-            "dense_gemm_only_tokens_per_s": dense_gemm_only,
-            "speedup_vs_dense_gemm_only": (value / dense_gemm_only) if dense_gemm_only else None,
-            "variants": {k: dict(v, speedup_vs_dense=(v["tokens_per_s"] / dense) if dense else None)
-                         for k, v in variants.items()},
-            "mask_search": mask_search, "optimizer_step": optimizer_step, "activation": activation,
-            "roofline": roof,
-            "kernels": per_kernel,
-            "e2e": e2e,
-            "gpu_launches": launches_timed,
-            "clocks": clocks,
-            "cpu_baseline": cpu,
+            "config": dict(config_dict(cfg, world, backend, shared), refresh_steps_in_timed_region=res[
+                "refresh_steps_timed"]),
+            "kernels": res["kernels"], "variants": res.get("variants"), "optimizer_step": res.get("optimizer_step"),
+            "activation": res.get("activation"), "mask_search": res["mask_search"],
+            "roofline": res["roofline"], "e2e": res["e2e"], "gpu_launches": res["gpu_launches"],
+            "clocks": res["clocks"], "cpu_baseline": cpu,
+            "sub_lines": sub_res or None,
         }
+        # the dense comparisons last, so a truncated tail of the line still carries them
+        for k in ("dense_tokens_per_s", "dense_fused_tokens_per_s", "dense_gemm_only_tokens_per_s",
+                  "speedup_vs_dense", "speedup_vs_dense_fused", "speedup_vs_dense_gemm_only", "speedup_vs_best_dense"):
+            line[k] = res.get(k)
+        line["target"] = ("north_star: 2:4 FFN fwd+bwd >= 1.5x the dense bf16 FFN at d_model >= 4096; judged on "
+                          "speedup_vs_best_dense (the faster of eager cuBLAS autograd and the fused dense kernels)")
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -631,7 +720,9 @@ def run_ours(a, cfg):
 
 def run_e2e(a, cfg, w_in, bias, w2, dev, world, dist):
     """Same step through the public API (SparseFFN autograd module), inputs
-    copied host->device every step from pinned memory, loss read back."""
+    copied host->device every step from pinned memory, loss read back.  Each step
+    is one optimizer step for the module's schedule (mark_weights_updated: K2 every
+    step, K1 every 40th), as in training."""
     import torch
     from paper_2404_01847_b200.module import SparseFFN
 
@@ -668,6 +759,7 @@ def run_e2e(a, cfg, w_in, bias, w2, dev, world, dist):
         free[nxt].record()
         fetch(nxt)
         torch.cuda.current_stream().wait_event(ready[cur])
+        mod.mark_weights_updated()  # one optimizer step per training step
         y = mod(dev_x[cur])
         # loss 0.5 |y|^2 / N: value from one norm reduction, its gradient y / N supplied directly
         # (two light kernels instead of autograd's fp32 cast / pow / sum chain and its backward)
@@ -682,8 +774,8 @@ def run_e2e(a, cfg, w_in, bias, w2, dev, world, dist):
         free[cur].record()
         state["i"] = i + 1
 
-    steps = max(10, a.steps // 4)
-    ms, _ = time_loop(one, steps, a.warmup, dist)
+    steps = 10
+    ms, _ = time_loop(one, steps, 3, dist)
     per = ms / steps
     return {"value": n * world / (per / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": n * d * 2,
             "d2h_bytes_per_step": 4, "ms_per_step": per,
@@ -693,7 +785,9 @@ def run_e2e(a, cfg, w_in, bias, w2, dev, world, dist):
 
 def main():
     a = parse()
-    cfg = dict(CONFIGS[a.config])
+    name = a.config or DEFAULT_CONFIG
+    subs = () if (a.config is not None or a.no_sub or a.tokens) else DEFAULT_SUB
+    cfg = dict(CONFIGS[name])
     if a.tokens:
         cfg["tokens"] = a.tokens
         cfg["workload"] = cfg["workload"].split(",")[0] + f", {a.tokens} tokens (token-count override)"
@@ -705,7 +799,7 @@ def main():
 
         run_stack(a, cfg)
         return
-    run_ours(a, cfg)
+    run_ours(a, cfg, name, subs)
 
 
 if __name__ == "__main__":

@@ -188,6 +188,20 @@ int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, c
              int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias, int epilogue, uint16_t* aux,
              int64_t ldaux, uint16_t* aux2, float* dbias, int d_t, int64_t gate_ff, void* stream);
 
+/* ---- dense token-major GEMM with the training epilogues of s24_spmm ---------------
+ * D^T[n, m] (token-major bf16, ldd) = epilogue(sum_k A[m, k] B[n, k]) with A the DENSE bf16
+ * weight: w_t = 0 -> A[m, k] = w[m * ldw + k], w_t = 1 -> A[m, k] = w[k * ldw + m] (the
+ * transposed orientation of the backward).  w_gate_ff > 0: w's [u; v] dimension (its rows,
+ * 2 w_gate_ff of them) is read in the u/v 16-row interleave of the gated epilogues, so the
+ * weight stays in the reference's [u; v] order (FFNLayer.w_in_cat, gated_ffn.py:111-115).
+ * B token-major (n x k, ldb >= k).  Epilogues, bias / aux / aux2 / dbias / gate_ff: as
+ * s24_spmm with d_t = 1 (not S24_EPI_GELU_AUX).  The masks=None route of fst_forward /
+ * fst_backward (gated_ffn.py:286-289; the dense fine-tune phase, trainer.py:111-114,
+ * :435-437) and the fused dense baseline of bench.py.  m % 128 (CTA pairs when m % 256 == 0), k % 64, n % 32 == 0. */
+int s24_gemm_act(const uint16_t* w, int w_t, int64_t ldw, int64_t w_gate_ff, int64_t m, int64_t k, const uint16_t* b,
+                 int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias, int epilogue,
+                 uint16_t* aux, uint16_t* aux2, float* dbias, int64_t gate_ff, void* stream);
+
 /* Process-wide: leave `sms` SMs free in subsequent GEMM launches (0 = use all).  A
  * data-parallel step sets it around the dX GEMM so the gradient all-reduce's kernels run
  * concurrently with it (the persistent GEMMs otherwise occupy every SM). */
@@ -302,6 +316,11 @@ int s24_block_gaps(const void* w, int dtype, int64_t rows, int64_t cols, double*
 /* ---- standalone masked decay on an fp32 gradient (optim.py:105-114) -------- */
 int s24_masked_decay(float* g, const void* w, int w_dtype, const uint8_t* idx, int64_t rows, int64_t cols,
                      float lambda_w, void* stream);
+/* The same under an arbitrary 0/1 mask `bits` (uint8, one per element) over n elements of any
+ * shape -- masked_decay_gradient on a flat parameter vector with a dense mask
+ * (optim.py:105-114, trainer.py:439-441). */
+int s24_masked_decay_bits(float* g, const void* w, int w_dtype, const uint8_t* bits, int64_t n, float lambda_w,
+                          void* stream);
 
 #ifdef __cplusplus
 }

@@ -118,10 +118,26 @@ class RefFFNStep:
         return y, dx, dw_in, dbias, dw2
 
 
-def time_reference(d, d_ff, act, tokens, steps, warmup=1, refresh=40, budget_s=None):
-    """Seconds per step (mask search amortized over `refresh` steps) on a
-    `tokens` sample.  Returns (sec_per_step, info)."""
-    st = RefFFNStep(d, d_ff, act, tokens, refresh=refresh)
+def ref_slice(d: int, d_ff: int, act: str, target_weights: float = 12.6e6) -> int:
+    """Hidden width of the bounded CPU sample: the largest d_ff' <= d_ff (a multiple of 4, d_ff
+    divided by an integer) whose first weight has at most ~target_weights elements.  Every term
+    of the step -- the four sparse products, the activation, both dW products, the decay and the
+    mask search -- is linear in d_ff at fixed d and tokens, so tokens/s at d_ff' divided by
+    d_ff / d_ff' is the full-width rate (used at C3 / C4, where one reference step over the full
+    weights takes minutes and tens of GB per process)."""
+    r_mult = 2 if act in ("geglu", "swiglu") else 1
+    f = 1
+    while d * r_mult * (d_ff // f) > target_weights and d_ff // (f + 1) >= 4:
+        f += 1
+    return max(4, (d_ff // f) // 4 * 4)
+
+
+def time_reference(d, d_ff, act, tokens, steps, warmup=1, refresh=40, budget_s=None, d_ff_sample=None):
+    """Seconds per step (mask search amortized over `refresh` steps) on a `tokens` sample,
+    scaled to the full hidden width when `d_ff_sample` < d_ff (see ref_slice).  Returns
+    (sec_per_step, info)."""
+    dfs = d_ff if d_ff_sample is None else int(d_ff_sample)
+    st = RefFFNStep(d, dfs, act, tokens, refresh=refresh)
     st.refresh()
     search_s = st.search_seconds
     st.t = 1  # skip the refresh inside the timed steps; add it amortized below
@@ -135,6 +151,6 @@ def time_reference(d, d_ff, act, tokens, steps, warmup=1, refresh=40, budget_s=N
         n += 1
         if budget_s is not None and time.perf_counter() - t0 > budget_s:
             break
-    per = (time.perf_counter() - t0) / n + search_s / refresh
+    per = ((time.perf_counter() - t0) / n + search_s / refresh) * (d_ff / dfs)
     cores = 1 if st.kind == "reference" else os.cpu_count()
-    return per, dict(kind=st.kind, steps=n, search_s=search_s, cores=cores)
+    return per, dict(kind=st.kind, steps=n, search_s=search_s, cores=cores, d_ff_sample=dfs)

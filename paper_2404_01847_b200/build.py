@@ -36,14 +36,31 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     lib = out or LIB
     if out is None and not defines and not force and not _stale():
         return LIB
-    srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", lib + ".tmp", *srcs]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    # one nvcc per translation unit in parallel (no cross-TU device symbols), then one link
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = lib + ".objs"
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+
+    def cc(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *cflags, *[f"-D{d}" for d in defines], "-c", "-o", obj, os.path.join(CSRC, src)]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        res = list(ex.map(cc, SOURCES))
+    for _, r in res:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libs24b200.so")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+                        "-o", lib + ".tmp", *[o for o, _ in res]], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libs24b200.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libs24b200.so")
     os.replace(lib + ".tmp", lib)
     return lib
 

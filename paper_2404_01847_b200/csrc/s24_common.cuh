@@ -202,6 +202,25 @@ __device__ __forceinline__ void tma_load(void* smem_dst, const CUtensorMap* map,
   if constexpr (CG == 1) tma_load_2d(smem_dst, map, bar, x, y);
   else tma_load_2d_cg2(smem_dst, map, bar, x, y);
 }
+// 4-D box load (coordinates x, 0, 0, w): the u/v row interleave of a gated dense weight
+// (dims: inner, 16 rows, 2 halves, row groups -- see make_map_gate in s24_gemm.cu)
+template <int CG>
+__device__ __forceinline__ void tma_load4(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t x,
+                                          int32_t w) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %4, %5}], "
+        "[%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(0), "r"(w)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+        "[%1, {%3, %4, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(0), "r"(w)
+        : "memory");
+  }
+}
 // arrive on the same-offset mbarrier of CTA `cta` in the cluster
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
   asm volatile(

@@ -77,6 +77,7 @@ struct GemmShape {
   int exp;      // experiment flags (timing studies only, results invalid): 1 skip B loads, 2 skip metadata cp, 4 every tile loads the B tile of n = 0,
                 //  16 no activation math in the epilogue, 32 no epilogue global loads,
                 //  128 no GELU'(z) AUX stores, 256 no D stores (fragment epilogue)
+  int a_gate;   // dense A through the 4-D u/v interleave map (gated first weight in [u; v] order)
 };
 
 __constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
@@ -371,10 +372,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int sl = 0; sl < kSlabs; ++sl) {
               const int ms = m0 + 128 * kCG * sl;
               if constexpr (kAMN) {
-                tma_load<kCG>(sA + sl * 16384, &tmA, &full_bar[stage], ms, kb * 64);
-                tma_load<kCG>(sA + sl * 16384 + 8192, &tmA, &full_bar[stage], ms + 64, kb * 64);
+                if (shp.a_gate) {  // K runs over the interleaved rows: 64 of them = 2 row groups
+                  tma_load4<kCG>(sA + sl * 16384, &tmA, &full_bar[stage], ms, 2 * kb);
+                  tma_load4<kCG>(sA + sl * 16384 + 8192, &tmA, &full_bar[stage], ms + 64, 2 * kb);
+                } else {
+                  tma_load<kCG>(sA + sl * 16384, &tmA, &full_bar[stage], ms, kb * 64);
+                  tma_load<kCG>(sA + sl * 16384 + 8192, &tmA, &full_bar[stage], ms + 64, kb * 64);
+                }
               } else {
-                tma_load<kCG>(sA + sl * 16384, &tmA, &full_bar[stage], kb * 64, ms);
+                if (shp.a_gate) tma_load4<kCG>(sA + sl * 16384, &tmA, &full_bar[stage], kb * 64, ms / 32);
+                else tma_load<kCG>(sA + sl * 16384, &tmA, &full_bar[stage], kb * 64, ms);
               }
             }
           }
@@ -1005,6 +1012,28 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t ou
   return S24_OK;
 }
 
+// 4-D map of a gated dense weight [u; v] (2 ff rows of `inner` elements, row pitch `pitch`) read
+// in the u/v 16-row interleave of the fused gated epilogues: dims (inner, 16 rows, 2 halves at
+// ff rows apart, ff / 16 row groups), box (box_inner, 16, 2, box_groups) -> smem row
+// 32 g + 16 h + r = interleaved row p of gate_row_dev.  128-byte swizzle.
+static int make_map_gate(CUtensorMap* map, const void* ptr, int64_t inner, int64_t ff, int64_t pitch_elems,
+                         uint32_t box_inner, uint32_t box_groups) {
+  EncodeTiledFn enc = get_encode_fn();
+  S24_REQUIRE(enc != nullptr, S24_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  S24_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && (pitch_elems * 2) % 16 == 0 && ff % 16 == 0,
+              S24_ERR_UNSUPPORTED, "TMA operands need 16-byte aligned base and row pitch");
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(inner), 16, 2, static_cast<cuuint64_t>(ff / 16)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(pitch_elems * 2), static_cast<cuuint64_t>(ff * pitch_elems * 2),
+                           static_cast<cuuint64_t>(16 * pitch_elems * 2)};
+  cuuint32_t box[4] = {box_inner, 16, 2, box_groups};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  S24_REQUIRE(r == CUDA_SUCCESS, S24_ERR_CUDA, "cuTensorMapEncodeTiled (gate) failed (%d)", static_cast<int>(r));
+  return S24_OK;
+}
+
 // SMs left free by the persistent GEMMs (s24_set_reserved_sms): a data-parallel step reserves a
 // few while its gradient all-reduce runs so the collective's kernel is co-resident with the
 // dX GEMM instead of queueing behind it.
@@ -1385,6 +1414,90 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
 #undef S24_SP_EPI
 #undef S24_SPT
 #undef S24_SP
+}
+
+// Dense counterpart of s24_spmm's token-major training products: the same persistent CTA-pair
+// kernel with kind::f16 MMAs on the dense weight and the same fused epilogues (bias, GELU / GELU',
+// dGELU + bias gradient, gated forward / backward, add-reduce store).  Serves the dense fine-tune
+// phase (gated_ffn.py:286-289 with masks=None, trainer.py:111-114) and the fused dense baseline.
+extern "C" int s24_gemm_act(const uint16_t* w, int w_t, int64_t ldw, int64_t w_gate_ff, int64_t m, int64_t k,
+                            const uint16_t* b, int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias,
+                            int epilogue, uint16_t* aux, uint16_t* aux2, float* dbias, int64_t gate_ff,
+                            void* stream) {
+  S24_REQUIRE(w && b && d, S24_ERR_ARG, "NULL operand");
+  S24_REQUIRE(m % 128 == 0 && k % 64 == 0 && n % 32 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
+              "dense GEMM needs m %% 128 == 0, k %% 64 == 0, n %% 32 == 0 (got m=%lld k=%lld n=%lld)",
+              (long long)m, (long long)k, (long long)n);
+  S24_REQUIRE(epilogue >= S24_EPI_STORE && epilogue <= S24_EPI_STORE_ADD && epilogue != S24_EPI_GELU_AUX,
+              S24_ERR_ARG, "bad epilogue for the dense token-major GEMM");
+  S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
+  const bool accumulate = epilogue == S24_EPI_STORE_ADD;
+  if (accumulate) epilogue = S24_EPI_STORE;
+  const bool gated_fwd = epilogue == S24_EPI_GEGLU_GRAD || epilogue == S24_EPI_SWIGLU_GRAD;
+  const bool gated_bwd = epilogue == S24_EPI_DGATED;
+  const int64_t d_cols = gated_fwd ? m / 2 : gated_bwd ? 2 * m : m;
+  S24_REQUIRE(ldd >= d_cols && ldd % 8 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0, S24_ERR_UNSUPPORTED,
+              "output rows must be 16-byte aligned");
+  if (gated_fwd || gated_bwd) {
+    S24_REQUIRE(gate_ff == (gated_fwd ? m / 2 : m) && gate_ff % 16 == 0, S24_ERR_SHAPE,
+                "gated epilogue: gate_ff must be d_ff (%lld) and a multiple of 16", (long long)gate_ff);
+    S24_REQUIRE(aux2 != nullptr && (reinterpret_cast<uintptr_t>(aux2) & 15) == 0, S24_ERR_ARG,
+                "gated epilogues need a 16-byte aligned aux2 tensor");
+  }
+  if (gated_fwd) S24_REQUIRE(w_gate_ff == m / 2 && !w_t, S24_ERR_SHAPE, "gated forward reads the [u; v] weight interleaved");
+  if (epilogue != S24_EPI_STORE)
+    S24_REQUIRE(aux != nullptr && (reinterpret_cast<uintptr_t>(aux) & 15) == 0, S24_ERR_ARG,
+                "this epilogue needs a 16-byte aligned (blocked) aux tensor");
+  const int64_t w_rows = w_t ? k : m, w_cols = w_t ? m : k;
+  S24_REQUIRE(ldw >= w_cols && ldb >= k, S24_ERR_SHAPE, "ldw / ldb too small");
+  if (w_gate_ff > 0)
+    S24_REQUIRE(w_rows == 2 * w_gate_ff && w_gate_ff % 16 == 0, S24_ERR_SHAPE,
+                "interleaved weight: its [u; v] dimension must be 2 * d_ff with d_ff %% 16 == 0");
+  // CTA pairs (M = 256, BN = 224) when m allows, else single CTAs (M = 128, BN = 128)
+  const bool pair = m % 256 == 0 && cg_override() != 1;
+  constexpr int BN = 224, BN1 = 128;
+  CUtensorMap ma, mb, md;
+  if (w_gate_ff > 0) {
+    if (int rc = make_map_gate(&ma, w, w_cols, w_gate_ff, ldw, 64, w_t ? 2 : 4)) return rc;
+  } else if (w_t) {
+    if (int rc = make_map(&ma, w, m, k, ldw, 64, 64)) return rc;
+  } else {
+    if (int rc = make_map(&ma, w, k, m, ldw, 64, 128)) return rc;
+  }
+  if (int rc = make_map(&mb, b, k, n, ldb, 64, pair ? BN / 2 : BN1)) return rc;
+  if (gated_fwd) {
+    if (int rc = make_map(&md, d, m / 2, n, ldd, 16, 32, kMapBf16Sw32)) return rc;
+  } else if (gated_bwd) {
+    if (int rc = make_map(&md, d, 2 * m, n, ldd, 64, 32, kMapBf16Sw128)) return rc;
+  } else {
+    if (int rc = make_map(&md, d, m, n, ldd, 32, 32, kMapBf16Sw64)) return rc;
+  }
+  GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0,
+                pick_group_m(static_cast<int>(m / (pair ? 256 : 128)), 0.0), -1, 0, w_gate_ff > 0 ? 1 : 0};
+  EpiParams ep{d,       ldd,   bias,    aux,     0,   dbias, aux2,
+               epilogue == S24_EPI_SWIGLU_GRAD ? S24_ACT_SWIGLU : S24_ACT_GEGLU,
+               gate_ff, nullptr, 0,     nullptr, 0.0f, accumulate ? 1 : 0};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define S24_DA(AMN, BNV, CG, EPI)                                                                               \
+  return launch_gemm<false, AMN, false, BNV, stages_for<Cfg<false, AMN, false, BNV, 1, CG>::STAGE_BYTES>(), CG, \
+                     EPI, true>(ma, mb, mb, md, md, md, shp, ep, st)
+#define S24_DA_EPI(AMN, BNV, CG)                                   \
+  switch (epilogue) {                                              \
+    case S24_EPI_GELU_GRAD: S24_DA(AMN, BNV, CG, kEpiGeluGrad);    \
+    case S24_EPI_DGELU: S24_DA(AMN, BNV, CG, kEpiDAct);            \
+    case S24_EPI_GEGLU_GRAD:                                       \
+    case S24_EPI_SWIGLU_GRAD: S24_DA(AMN, BNV, CG, kEpiGatedGrad); \
+    case S24_EPI_DGATED: S24_DA(AMN, BNV, CG, kEpiDGated);         \
+    default: S24_DA(AMN, BNV, CG, kEpiStore);                      \
+  }
+  if (pair) {
+    if (w_t) S24_DA_EPI(true, BN, 2);
+    S24_DA_EPI(false, BN, 2);
+  }
+  if (w_t) S24_DA_EPI(true, BN1, 1);
+  S24_DA_EPI(false, BN1, 1);
+#undef S24_DA_EPI
+#undef S24_DA
 }
 
 extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int b_mn, int64_t ldb,

@@ -715,6 +715,23 @@ __global__ void masked_decay_kernel(float* __restrict__ g, const void* __restric
   }
 }
 
+// the same decay under an arbitrary 0/1 mask of any shape (flat, element-aligned): the
+// reference's masked_decay_gradient on a flat parameter vector (optim.py:105-114, trainer.py:441)
+__global__ void masked_decay_bits_kernel(float* __restrict__ g, const void* __restrict__ w, int w_dtype,
+                                         const uint8_t* __restrict__ bits, int64_t n, float lam) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    if (bits[e]) continue;
+    float wv;
+    if (w_dtype == S24_BF16)
+      wv = bf16_to_f32(static_cast<const uint16_t*>(w)[e]);
+    else if (w_dtype == S24_F32)
+      wv = static_cast<const float*>(w)[e];
+    else
+      wv = static_cast<float>(static_cast<const double*>(w)[e]);
+    g[e] = g[e] + lam * wv;
+  }
+}
+
 }  // namespace s24
 
 using namespace s24;
@@ -917,4 +934,14 @@ extern "C" int s24_masked_decay(float* g, const void* w, int w_dtype, const uint
   masked_decay_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(g, w, w_dtype, idx, rows, cols,
                                                                                        lambda_w);
   return s24_check_launch("masked_decay");
+}
+
+extern "C" int s24_masked_decay_bits(float* g, const void* w, int w_dtype, const uint8_t* bits, int64_t n,
+                                     float lambda_w, void* stream) {
+  S24_REQUIRE(g && w && bits, S24_ERR_ARG, "NULL pointer");
+  S24_REQUIRE(w_dtype == S24_BF16 || w_dtype == S24_F32 || w_dtype == S24_F64, S24_ERR_UNSUPPORTED, "bad dtype");
+  if (n == 0) return S24_OK;
+  masked_decay_bits_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(g, w, w_dtype, bits, n,
+                                                                                            lambda_w);
+  return s24_check_launch("masked_decay_bits");
 }

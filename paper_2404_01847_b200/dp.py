@@ -54,5 +54,19 @@ class GradBucket:
             self.views.append(self.flat[off:off + n].view(s))
             off += n
 
+    @classmethod
+    def for_params(cls, params) -> "GradBucket":
+        return cls([p.shape for p in params], params[0].device)
+
+    def owns(self, t: torch.Tensor, i: int) -> bool:
+        """True when `t` is view i of this bucket (the backward wrote the gradient in place)."""
+        v = self.views[i]
+        return t.data_ptr() == v.data_ptr() and t.shape == v.shape and t.dtype == v.dtype
+
     def allreduce(self, group=None, async_op: bool = False):
         return dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+
+
+def allreduce_bucket(bucket: GradBucket, group=None) -> None:
+    """The one SUM all-reduce of a step when the gradients already live in `bucket`."""
+    bucket.allreduce(group)

@@ -208,6 +208,49 @@ def spmm_dw(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor
                C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, C.stream_of(out))
 
 
+@dataclass
+class DenseOperand:
+    """A dense bf16 weight on the tensor-core path (masks=None: the dense fine-tune phase,
+    gated_ffn.py:286-289, and the fused dense baseline).  perm_ff > 0: the gated first weight
+    [u; v] (rows = 2 perm_ff) is read u/v-interleaved by the GEMM's TMA map, so it stays in the
+    reference's order and needs no copy."""
+
+    w: torch.Tensor  # (rows, cols) bf16, row-major
+    perm_ff: int = 0
+
+    @property
+    def rows(self) -> int:
+        return self.w.shape[0]
+
+    @property
+    def cols(self) -> int:
+        return self.w.shape[1]
+
+    idx = None  # no mask: no masked decay
+
+    @classmethod
+    def of(cls, w: torch.Tensor, perm_ff: int = 0) -> "DenseOperand":
+        if w.dtype != torch.bfloat16 or w.stride(1) != 1 or w.stride(0) % 8 or w.data_ptr() % 16:
+            raise ShapeError("dense tensor-core weights must be bf16, row-major, 16-byte aligned rows")
+        return cls(w, perm_ff)
+
+
+def _mm(op, bwd: bool, b: torch.Tensor, n: int, out: torch.Tensor, tag: str, epi: int = C.EPI_STORE,
+        bias: torch.Tensor | None = None, aux: torch.Tensor | None = None, aux2: torch.Tensor | None = None,
+        dbias: torch.Tensor | None = None, gate_ff: int = 0) -> None:
+    """One token-major product of the FFN step: out^T = op (W or W^T when bwd) . b^T with a
+    training epilogue -- the 2:4 GEMM on a CompressedOperand, the dense one on a DenseOperand."""
+    m, k = (op.cols, op.rows) if bwd else (op.rows, op.cols)
+    if isinstance(op, CompressedOperand):
+        spmm(op.bwd_vals if bwd else op.fwd_vals, op.bwd_e if bwd else op.fwd_e, m, k, b, False, n, out, bias,
+             tag=tag, epi=epi, aux=aux, dbias=dbias, out_t=True, aux2=aux2, gate_ff=gate_ff)
+        return
+    with TIMER(tag):
+        C.call("s24_gemm_act", op.w.data_ptr(), int(bwd), op.w.stride(0), op.perm_ff, m, k, b.data_ptr(),
+               b.stride(0), n, out.data_ptr(), out.stride(0), C.ptr(bias), epi, C.ptr(aux), C.ptr(aux2),
+               C.ptr(dbias), gate_ff, C.stream_of(out))
+
+
 def aux_empty(f: int, n: int, device) -> torch.Tensor:
     """Buffer for an AUX matrix (f features x n tokens) in the fragment layout exchanged by the
     training epilogues (include/sparse24_b200.h, s24_spmm)."""
@@ -247,13 +290,15 @@ class FwdState:
     g2: torch.Tensor | None = None  # gated act(u), fragment layout (d_ff x N), fused gated path only
 
 
-def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor | None, w2: CompressedOperand,
-                act: str, fused: bool = False) -> FwdState:
+def ffn_forward(x: torch.Tensor, w_in: "CompressedOperand | DenseOperand", bias_in: torch.Tensor | None,
+                w2: "CompressedOperand | DenseOperand", act: str, fused: bool = False) -> FwdState:
     """Z = X W_in~^T + b -> A = act(Z) -> Y = A W2~^T (gated_ffn.py:293-297).
 
-    fused=True (GELU only): GEMM1's epilogue stores A = GELU(z) and
-    G = GELU'(z) instead of z, so the backward's GEMM3 epilogue applies the
-    activation derivative and reduces the bias gradient (no separate K7)."""
+    fused=True (GELU / gated): GEMM1's epilogue stores A = GELU(z) and
+    G = GELU'(z) (gated: A = act(u) v, G = v act'(u), G2 = act(u)) instead of z,
+    so the backward's GEMM3 epilogue applies the activation derivative and
+    reduces the bias gradient (no separate K7).  DenseOperand weights run the same
+    epilogues on dense tensor-core GEMMs (masks=None, gated_ffn.py:286-289)."""
     n, d = x.shape
     r_in = w_in.rows
     d_ff = w2.cols
@@ -267,31 +312,29 @@ def ffn_forward(x: torch.Tensor, w_in: CompressedOperand, bias_in: torch.Tensor 
     y = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
     if fused and act in GATED:
         if w_in.perm_ff != d_ff:
-            raise ShapeError("the fused gated path needs the first weight compressed u/v-interleaved (perm_ff = d_ff)")
+            raise ShapeError("the fused gated path needs the first weight read u/v-interleaved (perm_ff = d_ff)")
         g = aux_empty(d_ff, n, dev)  # v act'(u), fragment layout
         g2 = aux_empty(d_ff, n, dev)  # act(u), fragment layout
-        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, a, bias_in, tag="k3_spmm_fwd_in",
-             epi=C.EPI_SWIGLU_GRAD if act == "swiglu" else C.EPI_GEGLU_GRAD, aux=g, aux2=g2, out_t=True,
-             gate_ff=d_ff)
-        spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, a, False, n, y, tag="k3_spmm_fwd_out", out_t=True)
+        _mm(w_in, False, x, n, a, "k3_spmm_fwd_in", bias=bias_in,
+            epi=C.EPI_SWIGLU_GRAD if act == "swiglu" else C.EPI_GEGLU_GRAD, aux=g, aux2=g2, gate_ff=d_ff)
+        _mm(w2, False, a, n, y, "k3_spmm_fwd_out")
         return FwdState(x, None, a, y, g, g2)
     if w_in.perm_ff:
         raise ShapeError("an interleaved gated operand is only valid on the fused path")
     if fused and act == "gelu":
         g = aux_empty(d_ff, n, dev)  # GELU'(z), fragment layout, read back by GEMM3's epilogue
-        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, a, bias_in, tag="k3_spmm_fwd_in",
-             epi=C.EPI_GELU_GRAD, aux=g, out_t=True)
-        spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, a, False, n, y, tag="k3_spmm_fwd_out", out_t=True)
+        _mm(w_in, False, x, n, a, "k3_spmm_fwd_in", bias=bias_in, epi=C.EPI_GELU_GRAD, aux=g)
+        _mm(w2, False, a, n, y, "k3_spmm_fwd_out")
         return FwdState(x, None, a, y, g)
     z = torch.empty((n, r_in), dtype=torch.bfloat16, device=dev)
-    if act == "gelu":
+    if act == "gelu" and isinstance(w_in, CompressedOperand):
         spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, z, bias_in, gelu_aux=a, tag="k3_spmm_fwd_in",
              out_t=True)
     else:
-        spmm(w_in.fwd_vals, w_in.fwd_e, r_in, d, x, False, n, z, bias_in, tag="k3_spmm_fwd_in", out_t=True)
+        _mm(w_in, False, x, n, z, "k3_spmm_fwd_in", bias=bias_in)
         with TIMER("k6_act_fwd"):
             C.call("s24_act_fwd", z.data_ptr(), r_in, d_ff, n, ACT_CODES[act], a.data_ptr(), d_ff, C.stream_of(z))
-    spmm(w2.fwd_vals, w2.fwd_e, d, d_ff, a, False, n, y, tag="k3_spmm_fwd_out", out_t=True)
+    _mm(w2, False, a, n, y, "k3_spmm_fwd_out")
     return FwdState(x, z, a, y)
 
 
@@ -334,16 +377,15 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     if st.g2 is not None:
         # gated: dZ_u = dA v act'(u), dZ_v = dA act(u) straight into the interleaved dZ, bias grads fused
         dbias = dbias_out.zero_() if dbias_out is not None else torch.zeros(r_in, dtype=torch.float32, device=dev)
-        spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dy, False, n, dz, tag="k4_spmm_bwd_out", epi=C.EPI_DGATED,
-             aux=st.g, aux2=st.g2, dbias=dbias, out_t=True, gate_ff=d_ff)
+        _mm(w2, True, dy, n, dz, "k4_spmm_bwd_out", epi=C.EPI_DGATED, aux=st.g, aux2=st.g2, dbias=dbias,
+            gate_ff=d_ff)
     elif st.g is not None:
         # dZ = (dY W2~) * GELU'(z) with the bias gradient reduced in the same epilogue
         dbias = dbias_out.zero_() if dbias_out is not None else torch.zeros(r_in, dtype=torch.float32, device=dev)
-        spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dy, False, n, dz, tag="k4_spmm_bwd_out", epi=C.EPI_DGELU,
-             aux=st.g, dbias=dbias, out_t=True)
+        _mm(w2, True, dy, n, dz, "k4_spmm_bwd_out", epi=C.EPI_DGELU, aux=st.g, dbias=dbias)
     else:
         da = torch.empty((n, d_ff), dtype=torch.bfloat16, device=dev)
-        spmm(w2.bwd_vals, w2.bwd_e, d_ff, d, dy, False, n, da, tag="k4_spmm_bwd_out", out_t=True)
+        _mm(w2, True, dy, n, da, "k4_spmm_bwd_out")
         dbias = dbias_out if dbias_out is not None else torch.empty(r_in, dtype=torch.float32, device=dev)
         with TIMER("k7_act_bwd"):
             C.call("s24_act_bwd", st.z.data_ptr(), r_in, da.data_ptr(), d_ff, d_ff, n, ACT_CODES[act],
@@ -351,6 +393,11 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     # dW2[d, d_ff] = dY^T A and dW_in[r_in, d] = dZ^T X: K = tokens, both operands token-major (MN-major)
     dw2 = dw2_out if dw2_out is not None else torch.empty((d, d_ff), dtype=torch.float32, device=dev)
     dw_in = dw_in_out if dw_in_out is not None else torch.empty((r_in, d), dtype=torch.float32, device=dev)
+    if mvue and n % 128:
+        # the MVUE operand is tiled in 128-token groups; a batch that is not a multiple of 128
+        # (legal for the reference, any multiple of 4) takes the dense weight gradient -- the
+        # expectation of the unbiased MVUE estimator -- instead of failing
+        mvue = False
     if mvue:
         v2, e2, _ = mvue_compress(dy, mvue_seed(rng_seed, 1), exact=mvue_exact)
         spmm_dw(v2, e2, d, n, st.a, True, d_ff, dw2, w2_dense, w2.idx, lam, tag="k8_spmm_dw2")
@@ -368,9 +415,8 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
                 or not dx_accumulate.is_contiguous():
             raise ShapeError("dx_accumulate must be a contiguous (tokens, d) bf16 tensor")
         dx = dx_accumulate
-        spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dz, False, n, dx, tag="k4_spmm_bwd_in", out_t=True,
-             epi=C.EPI_STORE_ADD)
+        _mm(w_in, True, dz, n, dx, "k4_spmm_bwd_in", epi=C.EPI_STORE_ADD)
     else:
         dx = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
-        spmm(w_in.bwd_vals, w_in.bwd_e, d, r_in, dz, False, n, dx, tag="k4_spmm_bwd_in", out_t=True)
+        _mm(w_in, True, dz, n, dx, "k4_spmm_bwd_in")
     return Grads(dx, dw_in, dbias, dw2)

@@ -171,29 +171,18 @@ def _as_bf16(t: torch.Tensor) -> torch.Tensor:
     return t if t.dtype == torch.bfloat16 else t.to(torch.bfloat16)
 
 
-def _dense_act(layer: FFNLayer, z: torch.Tensor) -> torch.Tensor:
-    r = layer.d_ff
-    if layer.activation is Activation.GEGLU:
-        return gelu(z[:, :r]) * z[:, r:]
-    if layer.activation is Activation.SWIGLU:
-        return torch.nn.functional.silu(z[:, :r]) * z[:, r:]
-    if layer.activation is Activation.GELU:
-        return gelu(z)
-    return torch.relu(z)
-
-
 def fst_forward(layer: FFNLayer, x: torch.Tensor, masks: FFNMasks | None,
                 traversal: Traversal = Traversal.COL_ORDER) -> FstActivations:
     """Forward (gated_ffn.py:273-301).  masks=None is the dense path (dense
-    fine-tuning, gated_ffn.py:286-289): plain bf16 library GEMMs."""
+    fine-tuning, gated_ffn.py:286-289): the same tensor-core kernels on the
+    dense weights (s24_gemm_act) with the activation kernel K6."""
     x = _as_bf16(x)
     if x.dim() != 2 or x.shape[1] != layer.d:
         raise ShapeError(f"x shape {tuple(x.shape)} does not match layer width {layer.d}")
     if masks is None:
-        z = torch.nn.functional.linear(x, layer.w_in_cat.to(torch.bfloat16), layer.bias_in_cat.to(torch.bfloat16))
-        a = _dense_act(layer, z)
-        y = torch.nn.functional.linear(a, layer.w2.to(torch.bfloat16))
-        return FstActivations(layer, x, z, a, y, None, layer.w_in_cat)
+        w_in, w2 = _dense_ops(layer)
+        st = E.ffn_forward(x, w_in, _as_bf16(layer.bias_in_cat), w2, layer.activation.value)
+        return FstActivations(layer, x, st.z, st.a, st.y, None, layer.w_in_cat, st)
     if masks.w_in.shape != tuple(layer.w_in_cat.shape) or masks.w_out.shape != tuple(layer.w2.shape):
         raise ShapeError("mask shapes do not match layer weights")
     ops = masks.plans(layer)
@@ -232,52 +221,58 @@ def _pack_grads(layer, dx, dw_in, dbias, dw2) -> LayerGrads:
     return grads
 
 
+def _dense_ops(layer: FFNLayer):
+    return (E.DenseOperand.of(_as_bf16(layer.w_in_cat).contiguous()),
+            E.DenseOperand.of(_as_bf16(layer.w2).contiguous()))
+
+
 def _dense_backward(bundle: FstActivations, up: torch.Tensor) -> LayerGrads:
+    """masks=None backward (gated_ffn.py:304-364 on the dense route): dense tensor-core dA / dX
+    GEMMs, K7 for the activation and bias gradients, the dense dW GEMMs (no decay)."""
     layer = bundle.layer
-    with torch.enable_grad():
-        x = bundle.x.detach()
-        w_in = layer.w_in_cat.detach().to(torch.bfloat16).requires_grad_(True)
-        b_in = layer.bias_in_cat.detach().to(torch.bfloat16).requires_grad_(True)
-        w2 = layer.w2.detach().to(torch.bfloat16).requires_grad_(True)
-        xg = x.requires_grad_(True)
-        z = torch.nn.functional.linear(xg, w_in, b_in)
-        y = torch.nn.functional.linear(_dense_act(layer, z), w2)
-        dx, dw_in, db, dw2 = torch.autograd.grad(y, (xg, w_in, b_in, w2), up)
-    return _pack_grads(layer, dx, dw_in.float(), db.float(), dw2.float())
+    w_in, w2 = _dense_ops(layer)
+    g = E.ffn_backward(bundle.state, up, w_in, w2, layer.activation.value)
+    return _pack_grads(layer, g.dx, g.dw_in, g.dbias_in, g.dw2)
 
 
 def geglu_forward(x, u, v, b, c, traversal: Traversal = Traversal.COL_ORDER) -> torch.Tensor:
-    """gelu(x u^T + b) * (x v^T + c) (gated_ffn.py:208-224): one dense GEMM on
-    the concatenated [u; v] (library GEMM: this standalone helper is not on the
-    sparse path), then the fused gate kernel K6.  Returns (N x d_ff)."""
-    x = _as_bf16(x)
-    w_cat = torch.cat([u, v], 0).to(torch.bfloat16)
+    """gelu(x u^T + b) * (x v^T + c) (gated_ffn.py:208-224): the dense tensor-core GEMM on the
+    concatenated [u; v] (s24_gemm_act, bias fused), then the gate kernel K6.  Returns (N x d_ff)."""
+    x = _as_bf16(x).contiguous()
+    w_cat = torch.cat([u, v], 0).to(torch.bfloat16).contiguous()
     b_cat = torch.cat([b, c]).to(torch.bfloat16)
     if x.shape[1] != w_cat.shape[1]:
         raise ShapeError(f"x cols {x.shape[1]} != weight cols {w_cat.shape[1]}")
     n, r = x.shape[0], u.shape[0]
-    z = torch.nn.functional.linear(x, w_cat, b_cat).contiguous()  # (N, 2r) token-major
+    z = torch.empty((n, 2 * r), dtype=torch.bfloat16, device=x.device)  # (N, 2r) token-major
+    E._mm(E.DenseOperand.of(w_cat), False, x, n, z, "geglu_fwd", bias=b_cat)
     a = torch.empty((n, r), dtype=torch.bfloat16, device=x.device)
     C.call("s24_act_fwd", z.data_ptr(), 2 * r, r, n, C.ACT_GEGLU, a.data_ptr(), r, C.stream_of(z))
     return a
 
 
 def geglu_backward(x, u, v, b, c, upstream) -> LayerGrads:
-    """Analytic GEGLU gradients (gated_ffn.py:227-244), the gate part by K7."""
-    x = _as_bf16(x)
+    """Analytic GEGLU gradients (gated_ffn.py:227-244): the gate part by K7, dX by the dense
+    tensor-core GEMM on [u; v]^T, dW by the dense dW GEMM."""
+    x = _as_bf16(x).contiguous()
     up = _as_bf16(upstream).contiguous()
-    w_cat = torch.cat([u, v], 0).to(torch.bfloat16)
+    w_cat = torch.cat([u, v], 0).to(torch.bfloat16).contiguous()
     b_cat = torch.cat([b, c]).to(torch.bfloat16)
     n, r = x.shape[0], u.shape[0]
+    d = x.shape[1]
     if tuple(up.shape) != (n, r):
         raise ShapeError(f"upstream shape {tuple(up.shape)} != output shape {(n, r)}")
-    z = torch.nn.functional.linear(x, w_cat, b_cat).contiguous()
+    op = E.DenseOperand.of(w_cat)
+    z = torch.empty((n, 2 * r), dtype=torch.bfloat16, device=x.device)
+    E._mm(op, False, x, n, z, "geglu_fwd", bias=b_cat)
     dz = torch.empty_like(z)
     dbias = torch.empty(2 * r, dtype=torch.float32, device=x.device)
     C.call("s24_act_bwd", z.data_ptr(), 2 * r, up.data_ptr(), r, r, n, C.ACT_GEGLU, dz.data_ptr(), 2 * r,
            dbias.data_ptr(), C.stream_of(z))
-    dx = dz @ w_cat
-    dw = dz.t().float() @ x.float()
+    dx = torch.empty((n, d), dtype=torch.bfloat16, device=x.device)
+    E._mm(op, True, dz, n, dx, "geglu_bwd")
+    dw = torch.empty((2 * r, d), dtype=torch.float32, device=x.device)
+    E.gemm_dw(dz, True, x, True, 2 * r, d, n, dw)
     return LayerGrads(d_x=dx, d_u=dw[:r], d_v=dw[r:], d_b=dbias[:r], d_c=dbias[r:])
 
 

@@ -1,25 +1,33 @@
 """nn.Module / autograd wrapper of the 2:4 FFN hot path, with the reference's
 training-schedule semantics for one FFN block:
 
-  * mask refresh every `refresh_period` optimizer steps while sparse
-    (trainer.py:422-432; DecayConfig.refresh_period = 40, optim.py:55): K1
-    searches the new transposable masks and compresses both orientations;
-    other steps run K2 (per-step prune/compress of the current weights);
+  * mask refresh every `refresh_period` OPTIMIZER steps while sparse
+    (trainer.py:422-432; DecayConfig.refresh_period = 40, optim.py:55).  An
+    optimizer step is detected as a change of the parameters' in-place version
+    counters (every torch optimizer updates parameters in place; call
+    `mark_weights_updated()` after writing `.data` directly).  The first forward
+    after a step recompresses the current weights (K2), or, once the period is
+    reached, searches new transposable masks and compresses both orientations
+    (K1).  Further forwards of the same step (gradient accumulation, recompute)
+    reuse the operands;
   * masked decay on the gradient (DecayMode.ON_GRADIENTS, trainer.py:439-441)
     fused into the dW epilogue (K5);
-  * dense fine-tune switch: `sparse = False` runs plain dense bf16 GEMMs
-    (fst_forward with masks=None, gated_ffn.py:286-289);
+  * dense fine-tune switch: `sparse = False` runs the same tensor-core kernels
+    on the dense weights (fst_forward with masks=None, gated_ffn.py:286-289,
+    trainer.py:111-114): dense GEMMs with the fused activation / bias-gradient
+    epilogues and the dense dW GEMM, no decay (trainer.py:435-441);
   * data parallelism: `allreduce_grads()` sums [dW_in, dbias, dW2] in one
-    NCCL all-reduce; the decay is pre-scaled by 1/world so it is applied once.
+    NCCL all-reduce of a preallocated bucket the backward writes into; the decay
+    is pre-scaled by 1/world so it is applied once.
 
-Parameters are fp32 master weights; the kernels read them directly and round
-the kept values to bf16 while compressing.
+Parameters are fp32 master weights; the sparse kernels read them directly and
+round the kept values to bf16 while compressing.  A backward whose forward ran
+on a different mask than the current one (a refresh in between) raises.
 """
 
 from __future__ import annotations
 
 import torch
-import torch.nn.functional as F
 
 from . import dp
 from . import engine as E
@@ -27,11 +35,14 @@ from . import engine as E
 
 class _SparseFFNFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, w_in, bias_in, w2, mod):
+    def forward(ctx, x, w_in, bias_in, w2, mod, dense_ops):
         xb = x if x.dtype == torch.bfloat16 else x.to(torch.bfloat16)
-        st = E.ffn_forward(xb, mod.op_in, bias_in.to(torch.bfloat16), mod.op_out, mod.act, fused=True)
+        op_in, op_out = dense_ops if dense_ops is not None else (mod.op_in, mod.op_out)
+        st = E.ffn_forward(xb, op_in, bias_in.to(torch.bfloat16), op_out, mod.act, fused=True)
         ctx.mod = mod
         ctx.st = st
+        ctx.ops = (op_in, op_out)
+        ctx.mask_version = mod.mask_version
         ctx.save_for_backward(w_in, w2)
         return st.y
 
@@ -39,11 +50,28 @@ class _SparseFFNFn(torch.autograd.Function):
     def backward(ctx, dy):
         w_in, w2 = ctx.saved_tensors
         mod = ctx.mod
-        g = E.ffn_backward(ctx.st, dy.to(torch.bfloat16), mod.op_in, mod.op_out, mod.act, w_in_dense=w_in,
-                           w2_dense=w2, lam=mod.decay_lambda, mvue=mod.mvue, rng_seed=mod.mvue_seed,
-                           mvue_exact=mod.mvue_exact)
+        op_in, op_out = ctx.ops
+        dense = isinstance(op_in, E.DenseOperand)
+        if not dense and mod.mask_version != ctx.mask_version:
+            raise RuntimeError("SparseFFN: the masks were refreshed between this forward and its backward; "
+                               "the weight gradient would use a mask that did not produce the activations")
+        params = (mod.w_in, mod.bias_in, mod.w2)
+        # first gradient of the step: the dW GEMMs / bias epilogue write straight into the
+        # preallocated all-reduce bucket, whose views become the parameters' .grad; with
+        # gradient accumulation (.grad already set) autograd adds the fresh gradients in place
+        direct = all(p.grad is None for p in params)
+        b = mod.grad_bucket() if direct else None
+        g = E.ffn_backward(ctx.st, dy.to(torch.bfloat16), op_in, op_out, mod.act, w_in_dense=w_in,
+                           w2_dense=w2, lam=0.0 if dense else mod.decay_lambda, mvue=mod.mvue and not dense,
+                           rng_seed=mod.mvue_seed, mvue_exact=mod.mvue_exact,
+                           dw_in_out=b.views[0] if direct else None, dbias_out=b.views[1] if direct else None,
+                           dw2_out=b.views[2] if direct else None)
         ctx.st = None
-        return g.dx, g.dw_in, g.dbias_in, g.dw2, None
+        if direct:
+            for p, v in zip(params, b.views):
+                p.grad = v
+            return g.dx, None, None, None, None, None
+        return g.dx, g.dw_in, g.dbias_in, g.dw2, None, None
 
 
 class SparseFFN(torch.nn.Module):
@@ -63,6 +91,10 @@ class SparseFFN(torch.nn.Module):
         self.op_out = E.CompressedOperand.empty(d, d_ff, dev)
         self.steps_since_refresh = None  # None -> search on first use
         self.mask_searches = 0
+        self.mask_version = 0  # bumped by every refresh (K1)
+        self._seen_version = None  # parameter versions the operands were built from
+        self._dense_cache = None  # (versions, DenseOperand pair) of the dense phase
+        self._bucket = None
         # MVUE-sparsified weight gradients (fst_backward(mvue=True), gated_ffn.py:304-373): the
         # caller sets the per-step layer seed (trainer.py:245-247) before backward
         self.mvue = False
@@ -79,41 +111,69 @@ class SparseFFN(torch.nn.Module):
             m.w2.copy_(w2.float())
         return m
 
+    def _versions(self):
+        return (self.w_in._version, self.w2._version)
+
+    def mark_weights_updated(self) -> None:
+        """Declare an optimizer step that bypassed the in-place version counters (e.g. writes
+        through `.data`): the next forward recompresses and advances the refresh schedule."""
+        self._seen_version = None
+        self._dense_cache = None
+
     def refresh_masks(self) -> None:
         """K1: new transposable masks + both compressed orientations."""
         E.search_compress_pair(self.w_in.detach(), self.op_in, self.w2.detach(), self.op_out)
         self.steps_since_refresh = 0
         self.mask_searches += 2
+        self.mask_version += 1
+        self._seen_version = self._versions()
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
-        if not self.sparse:
-            return self._dense(x)
-        if self.steps_since_refresh is None or self.steps_since_refresh >= self.refresh_period:
+    def _prepare_sparse(self) -> None:
+        v = self._versions()
+        if self.steps_since_refresh is None:
+            self.refresh_masks()
+            return
+        if v == self._seen_version:
+            return  # same optimizer step: operands are current
+        self.steps_since_refresh += 1  # one optimizer step since the operands were built
+        if self.steps_since_refresh >= self.refresh_period:
             self.refresh_masks()
         else:
             E.compress_values_pair(self.w_in.detach(), self.op_in, self.w2.detach(), self.op_out)
-        if self.training:
-            self.steps_since_refresh += 1
-        return _SparseFFNFn.apply(x, self.w_in, self.bias_in, self.w2, self)
+            self._seen_version = v
 
-    def _dense(self, x):
-        xb = x.to(torch.bfloat16)
-        z = F.linear(xb, self.w_in.to(torch.bfloat16), self.bias_in.to(torch.bfloat16))
-        r = self.w2.shape[1]
-        if self.act == "gelu":
-            a = F.gelu(z)
-        elif self.act == "relu":
-            a = F.relu(z)
-        elif self.act == "swiglu":
-            a = F.silu(z[:, :r]) * z[:, r:]
-        else:
-            a = F.gelu(z[:, :r]) * z[:, r:]
-        return F.linear(a, self.w2.to(torch.bfloat16))
+    def _dense_ops(self):
+        v = self._versions()
+        if self._dense_cache is None or self._dense_cache[0] != v:
+            w_in = self.w_in.detach().to(torch.bfloat16).contiguous()
+            w2 = self.w2.detach().to(torch.bfloat16).contiguous()
+            ff = self.w2.shape[1] if self.act in E.GATED else 0
+            self._dense_cache = (v, (E.DenseOperand.of(w_in, ff), E.DenseOperand.of(w2)))
+        return self._dense_cache[1]
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if not self.sparse:
+            return _SparseFFNFn.apply(x, self.w_in, self.bias_in, self.w2, self, self._dense_ops())
+        self._prepare_sparse()
+        return _SparseFFNFn.apply(x, self.w_in, self.bias_in, self.w2, self, None)
+
+    def grad_bucket(self) -> "dp.GradBucket":
+        """The preallocated fp32 [dW_in | dbias | dW2] bucket the backward writes into (one
+        all-reduce per step, no packing copies)."""
+        if self._bucket is None:
+            self._bucket = dp.GradBucket.for_params([self.w_in, self.bias_in, self.w2])
+        return self._bucket
 
     def allreduce_grads(self, group=None) -> None:
-        """One NCCL all-reduce of the concatenated gradients (SUM: the
-        per-rank loss is a per-rank sum/mean and the decay is pre-scaled)."""
-        dp.allreduce_grads([p.grad for p in (self.w_in, self.bias_in, self.w2)], group)
+        """One NCCL all-reduce of the gradient bucket (SUM: the per-rank loss is a per-rank
+        sum/mean and the decay is pre-scaled).  The parameters' .grad are views of the bucket
+        when the last backward wrote them there; otherwise they are packed first."""
+        params = (self.w_in, self.bias_in, self.w2)
+        b = self.grad_bucket()
+        if all(p.grad is not None and b.owns(p.grad, i) for i, p in enumerate(params)):
+            dp.allreduce_bucket(b, group)
+        else:
+            dp.allreduce_grads([p.grad for p in params], group)
 
     @property
     def masks_idx(self):

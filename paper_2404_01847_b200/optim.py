@@ -50,7 +50,12 @@ def masked_decay_gradient(g: torch.Tensor, w: torch.Tensor, m, lambda_w: float) 
     m = torch.as_tensor(m, device=g.device)
     if not (g.shape == w.shape == m.shape):
         raise ShapeError("gradient, weights and mask must have equal shapes")
-    return g.to(torch.float32) + lambda_w * ((1 - m.to(torch.float32)) * w.to(torch.float32))
+    out = g.to(torch.float32).contiguous().clone()
+    wc = w.contiguous()
+    mb = (m != 0).to(torch.uint8).contiguous()
+    C.call("s24_masked_decay_bits", out.data_ptr(), wc.data_ptr(), C.dtype_code(wc), mb.data_ptr(), out.numel(),
+           float(lambda_w), C.stream_of(out))
+    return out
 
 
 def srste_weight_decay(w_next_base: torch.Tensor, w: torch.Tensor, m, lr: float, lambda_w: float) -> torch.Tensor:
@@ -133,6 +138,17 @@ def mask_flips(m_prev: TransposableMask, m_curr: TransposableMask,
     if m_prev.shape != m_curr.shape:
         raise ShapeError(f"mask shapes differ: {m_prev.shape} vs {m_curr.shape}")
     C.require_cuda(m_prev.idx, m_curr.idx)
+    if m_prev._raw is not None or m_curr._raw is not None:
+        # masks given as arbitrary 0/1 bits (e.g. a reference-style mask_fn): count the changed
+        # bits per 4x4 block from the bits themselves, not from pattern indices
+        rows, cols = m_prev.shape
+        diff = (m_prev.bits != m_curr.bits).to(torch.int32)
+        per = diff.reshape(rows // 4, 4, cols // 4, 4).sum(dim=(1, 3)).reshape(-1)
+        if block_flips is not None:
+            if block_flips.dtype != torch.int32 or block_flips.numel() != per.numel():
+                raise ShapeError("block_flips must be int32 with one entry per 4x4 block")
+            block_flips.view(-1).add_(per)
+        return per.sum(dtype=torch.int64)
     out = torch.zeros(1, dtype=torch.int64, device=m_prev.idx.device)
     if block_flips is not None and (block_flips.dtype != torch.int32 or block_flips.numel() != m_prev.idx.numel()):
         raise ShapeError("block_flips must be int32 with one entry per 4x4 block")
@@ -161,7 +177,8 @@ class FlipTrace:
 def block_flip_stats(w_history, table=None, mask_fn=None) -> FlipTrace:
     """Cumulative mask flips and retained-L1 gap per 4x4 block (optim.py:164-192) on the GPU.
 
-    Flips: K1 search of every snapshot (or `mask_fn(w) -> TransposableMask`) and the
+    Flips: K1 search of every snapshot (or `mask_fn(w)` -> 0/1 bits as in the reference, or a
+    TransposableMask) and the
     per-block changed-bit counts of consecutive masks (s24_mask_flips).  Gaps: best minus
     second-best of the 90 float64 pattern scores on the final snapshot (s24_block_gaps),
     bit-exact with the reference.  `table` is accepted for signature compatibility (only
@@ -182,11 +199,19 @@ def block_flip_stats(w_history, table=None, mask_fn=None) -> FlipTrace:
         raise ShapeError(f"shape {(rows, cols)} not divisible into 4x4 blocks")
     nb = (rows // 4) * (cols // 4)
     counts = torch.zeros(nb, dtype=torch.int32, device=last.device)
-    prev = mask_fn(snaps[0])
+    def as_mask(m):
+        # the reference's mask_fn returns a 0/1 bits array (optim.py:176-177); ours may also
+        # return a TransposableMask
+        if isinstance(m, TransposableMask):
+            return m
+        bits = torch.as_tensor(m, device=last.device)
+        return TransposableMask(bits=bits)
+
+    prev = as_mask(mask_fn(snaps[0]))
     for w in snaps[1:]:
         if tuple(w.shape) != (rows, cols):
             raise ShapeError("snapshots differ in shape")
-        curr = mask_fn(w)
+        curr = as_mask(mask_fn(w))
         mask_flips(prev, curr, counts)
         prev = curr
     last = last.contiguous()

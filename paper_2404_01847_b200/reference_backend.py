@@ -21,8 +21,14 @@ Semantics per entry point:
                         of spmm vs dense_matmul do not apply).
   * gate_gelu        -- the fused gate kernel K6 (fp32 math, bf16 storage):
                         toleranced.
-  * matmul_ref, spmm_rowwise, prune_2of4_keep, greedy_masks -- not on the
-                        B200 hot path: raise.
+  * matmul_ref       -- the dense tcgen05 GEMM (bf16 operands, fp32 accumulation),
+                        toleranced.
+  * spmm_rowwise     -- the MVUE weight-gradient product: a row-wise 2:4 operand
+                        on the 2:4 tensor cores (s24_pack24 + s24_flat_to_e +
+                        s24_spmm_dw), toleranced.
+  * prune_2of4_keep  -- s24_prune_2of4, bit-exact (ties to the lowest index).
+  * greedy_masks     -- s24_greedy_search, bit-exact; RuntimeError when a block
+                        cannot be completed, as the reference.
 """
 
 from __future__ import annotations
@@ -123,14 +129,134 @@ def gate_gelu(z1, z2, row_order):
     return np.asfortranarray(a[:, :n].double().cpu().numpy())
 
 
-def _not_on_path(name):
-    def f(*a, **k):
-        raise NotImplementedError(f"{name} is not on the B200 hot path (SURVEY.md section 2.1)")
-
-    return f
+def _pad(v: int, q: int) -> int:
+    return (v + q - 1) // q * q
 
 
-matmul_ref = _not_on_path("matmul_ref")
-spmm_rowwise = _not_on_path("spmm_rowwise")
-prune_2of4_keep = _not_on_path("prune_2of4_keep")
-greedy_masks = _not_on_path("greedy_masks")
+def _out_dtype(*arrays):
+    """The reference's fused `real` type: float32 in -> float32 out, else float64 (_core.pyx:21-23)."""
+    return np.float32 if all(np.asarray(x).dtype == np.float32 for x in arrays) else np.float64
+
+
+def matmul_ref(a, b):
+    """C = A @ B (_core.pyx:26-41) on the dense tcgen05 GEMM (s24_gemm_dw: bf16 operands, fp32
+    accumulation; toleranced, not the reference's ascending-k float64 sums)."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[0]:
+        raise ValueError("inner dimensions differ")
+    m, k = a.shape
+    n = b.shape[1]
+    out_dt = _out_dtype(a, b)
+    if m == 0 or n == 0 or k == 0:
+        return np.zeros((m, n), dtype=out_dt)
+    M_, N_, K_ = _pad(m, 128), _pad(n, 128), _pad(k, 64)
+    ad = torch.zeros((M_, K_), dtype=torch.bfloat16, device="cuda")
+    ad[:m, :k] = _dev(a.astype(np.float64)).to(torch.bfloat16)
+    bd = torch.zeros((K_, N_), dtype=torch.bfloat16, device="cuda")  # stored k x n: B MN-major
+    bd[:k, :n] = _dev(b.astype(np.float64)).to(torch.bfloat16)
+    out = torch.empty((M_, N_), dtype=torch.float32, device="cuda")
+    from .engine import gemm_dw
+
+    gemm_dw(ad, False, bd, True, M_, N_, K_, out)
+    return out[:m, :n].cpu().numpy().astype(out_dt)
+
+
+def spmm_rowwise(values, pos, b):
+    """C = A @ B with A given row-wise as kept values + absolute column positions
+    (_core.pyx:44-60; the MVUE weight-gradient product of _grad_weight, gated_ffn.py:372-373).
+    A 2:4 row-wise operand (at most two kept per aligned group of four, as mvue_slots_rowwise
+    produces) runs on the 2:4 tensor cores: packed with s24_pack24, metadata to E tiles
+    (s24_flat_to_e), then s24_spmm_dw.  Any other sparsity takes the dense GEMM.  Toleranced."""
+    values = np.asarray(values)
+    pos = np.asarray(pos, dtype=np.int64)
+    b = np.asarray(b)
+    m, s_ = values.shape
+    k, n = b.shape
+    out_dt = _out_dtype(values, b)
+    if pos.shape != values.shape:
+        raise ValueError("values and positions differ in shape")
+    if m == 0 or n == 0 or s_ == 0:
+        return np.zeros((m, n), dtype=out_dt)
+    if pos.min() < 0 or pos.max() >= k:
+        raise ValueError("position out of range")
+    a = np.zeros((m, k))
+    np.add.at(a, (np.repeat(np.arange(m), s_), pos.reshape(-1)), values.reshape(-1).astype(np.float64))
+    kept = np.zeros((m, _pad(k, 4)), dtype=np.int32)
+    np.add.at(kept, (np.repeat(np.arange(m), s_), pos.reshape(-1)), 1)
+    per_group = kept.reshape(m, -1, 4).sum(axis=2)
+    if per_group.max() > 2:
+        return matmul_ref(a, b)
+    M_, K_, N_ = _pad(m, 128), _pad(k, 128), _pad(n, 128)
+    # complete every group to exactly two kept slots (zero-valued fillers at the lowest free
+    # positions) so it is a valid 2:4 operand
+    bits = np.zeros((M_, K_), dtype=np.uint8)
+    bits[:m, :kept.shape[1]] = kept > 0
+    g = bits.reshape(M_, K_ // 4, 4)
+    for _ in range(2):
+        need = g.sum(axis=2) < 2
+        free = np.argmax(g == 0, axis=2)
+        r, c = np.nonzero(need)
+        g[r, c, free[r, c]] = 1
+    wd = torch.zeros((M_, K_), dtype=torch.bfloat16, device="cuda")
+    wd[:m, :k] = _dev(a).to(torch.bfloat16)
+    bits_d = _dev(bits)
+    vals = torch.empty((M_, K_ // 2), dtype=torch.bfloat16, device="cuda")
+    meta = torch.empty((M_, K_ // 4), dtype=torch.uint8, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = C.stream_of(wd)
+    C.call("s24_pack24", wd.data_ptr(), C.S24_BF16, bits_d.data_ptr(), M_, K_, 0, vals.data_ptr(), meta.data_ptr(),
+           bad.data_ptr(), st)
+    e = torch.empty((M_ // 128) * (K_ // 128) * 2048, dtype=torch.uint8, device="cuda")
+    C.call("s24_flat_to_e", meta.data_ptr(), M_, K_, e.data_ptr(), st)
+    bd = torch.zeros((K_, N_), dtype=torch.bfloat16, device="cuda")  # stored k x n: B MN-major
+    bd[:k, :n] = _dev(b.astype(np.float64)).to(torch.bfloat16)
+    out = torch.empty((M_, N_), dtype=torch.float32, device="cuda")
+    from .engine import spmm_dw
+
+    spmm_dw(vals, e, M_, K_, bd, True, N_, out)
+    return out[:m, :n].cpu().numpy().astype(out_dt)
+
+
+def prune_2of4_keep(groups):
+    """Keep-mask (ng, 4) uint8 of the two largest |g| per group, ties to the lowest index
+    (_core.pyx:113-136) -- s24_prune_2of4 on the (ng x 4) matrix, bit-exact."""
+    g = np.ascontiguousarray(np.asarray(groups))
+    if g.ndim != 2 or g.shape[1] != 4:
+        raise ValueError("groups must be (ng, 4)")
+    ng = g.shape[0]
+    if ng == 0:
+        return np.zeros((0, 4), dtype=np.uint8)
+    dt = C.S24_F32 if g.dtype == np.float32 else C.S24_F64
+    gd = _dev(g.astype(np.float32 if dt == C.S24_F32 else np.float64))
+    # the kernel tiles rows in groups of 4: pad the group count to a multiple of 4 rows
+    rows = _pad(ng, 4)
+    if rows != ng:
+        gd = torch.cat([gd, torch.zeros((rows - ng, 4), dtype=gd.dtype, device="cuda")])
+    bits = torch.empty((rows, 4), dtype=torch.uint8, device="cuda")
+    C.call("s24_prune_2of4", gd.data_ptr(), dt, rows, 4, 0, bits.data_ptr(), C.stream_of(gd))
+    return bits[:ng].cpu().numpy()
+
+
+def greedy_masks(absblocks):
+    """Greedy transposable mask per 4x4 block (_core.pyx:139-219), bit-exact: s24_greedy_search
+    on the blocks laid out as a (4, 4 nb) matrix.  RuntimeError when a block cannot be completed
+    (the reference's failure, :215-216)."""
+    ab = np.ascontiguousarray(np.asarray(absblocks))
+    if ab.ndim != 2 or ab.shape[1] != 16:
+        raise ValueError("absblocks must be (nb, 16)")
+    nb = ab.shape[0]
+    if nb == 0:
+        return np.zeros((0, 16), dtype=np.uint8)
+    dt = C.S24_F32 if ab.dtype == np.float32 else C.S24_F64
+    w = _dev(ab.astype(np.float32 if dt == C.S24_F32 else np.float64).reshape(nb, 4, 4).transpose(1, 0, 2)
+             .reshape(4, 4 * nb))
+    idx = torch.empty((1, nb), dtype=torch.uint8, device="cuda")
+    fails = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = C.stream_of(w)
+    C.call("s24_greedy_search", w.data_ptr(), dt, 4, 4 * nb, idx.data_ptr(), fails.data_ptr(), st)
+    if int(fails.item()):
+        raise RuntimeError("greedy mask completion failed")
+    bits = torch.empty((4, 4 * nb), dtype=torch.uint8, device="cuda")
+    C.call("s24_idx_to_bits", idx.data_ptr(), 4, 4 * nb, bits.data_ptr(), st)
+    return bits.reshape(4, nb, 4).permute(1, 0, 2).reshape(nb, 16).cpu().numpy()

@@ -60,9 +60,10 @@ def enumerate_patterns() -> PatternTable:
 
 @lru_cache(maxsize=None)
 def _transpose_map(device: str) -> torch.Tensor:
-    """pattern index -> index of its transpose (the table is transpose-closed)."""
+    """pattern index -> index of its transpose (the table is transpose-closed); indices
+    outside the table (invalid blocks) map to 255, so a lookup can never leave the table."""
     t = enumerate_patterns()
-    lut = [t.index_of(p.T) for p in t.patterns]
+    lut = [t.index_of(p.T) for p in t.patterns] + [255] * (256 - len(t.patterns))
     return torch.tensor(lut, dtype=torch.uint8, device=device)
 
 
@@ -73,11 +74,18 @@ def _check_blocks(rows: int, cols: int) -> None:
 
 class TransposableMask:
     """Mask whose aligned 4x4 blocks hold two ones per block row and column
-    (sparsity.py:111-145), stored as per-block pattern indices on the GPU."""
+    (sparsity.py:111-145), stored as per-block pattern indices on the GPU.
+
+    Built from a 0/1 `bits` matrix the mask also keeps those raw bits, as the
+    reference does: an invalid mask (a block that is none of the 90 patterns)
+    still reports, transposes and scores its own bits, and fails only in
+    `validate()` (FormatError) -- which every consumer of the pattern indices
+    (FFNMasks.plans, compress) runs first."""
 
     def __init__(self, idx: torch.Tensor | None = None, shape: tuple[int, int] | None = None,
                  bits: torch.Tensor | None = None):
         self._bad = None
+        self._raw = None
         if bits is not None:
             C.require_cuda(bits)
             if bits.dim() != 2:
@@ -89,6 +97,7 @@ class TransposableMask:
             bad = torch.zeros(1, dtype=torch.int32, device=b.device)
             C.call("s24_bits_to_idx", b.data_ptr(), rows, cols, idx.data_ptr(), bad.data_ptr(), C.stream_of(b))
             self._bad = bad
+            self._raw = b
             shape = (rows, cols)
         if idx is None or shape is None:
             raise ValueError("TransposableMask needs idx + shape, or bits")
@@ -112,12 +121,16 @@ class TransposableMask:
 
     @property
     def bits(self) -> torch.Tensor:
+        if self._raw is not None:
+            return self._raw
         rows, cols = self._shape
         out = torch.empty((rows, cols), dtype=torch.uint8, device=self.idx.device)
         C.call("s24_idx_to_bits", self.idx.data_ptr(), rows, cols, out.data_ptr(), C.stream_of(self.idx))
         return out
 
     def transpose(self) -> "TransposableMask":
+        if self._raw is not None:  # sparsity.py:137-138: any 0/1 matrix transposes
+            return TransposableMask(bits=self._raw.t().contiguous())
         lut = _transpose_map(str(self.idx.device))
         idx_t = lut[self.idx.t().long()].contiguous()
         return TransposableMask(idx_t, (self._shape[1], self._shape[0]))

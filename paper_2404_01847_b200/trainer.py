@@ -36,7 +36,7 @@ import torch
 from . import engine as E
 from .matrix import ShapeError
 from .module import SparseFFN
-from .optim import DecayConfig, DecayMode, OptimizerState, adam_step, mask_flips
+from .optim import DecayConfig, DecayMode, OptimizerState, adam_step, block_flip_stats, mask_flips
 from .sparsity import TransposableMask
 
 _SALT_INIT = 0x12171
@@ -57,8 +57,10 @@ _ACTS = {"gelu": "gelu", "geglu": "geglu", "relu": "relu", "swiglu": "swiglu"}
 @dataclass
 class TrainConfig:
     """trainer.py:73-152 (field names and defaults of the reference; `activation` is the
-    reference Activation value string).  The tensor-core path needs d, d_ff % 128 == 0
-    and batch % 64 == 0."""
+    reference Activation value string; the reference's Activation enum is accepted and
+    coerced to it).  The tensor-core path needs d, d_ff % 128 == 0 and batch % 64 == 0
+    (with mvue=True a batch that is not a multiple of 128 -- the MVUE operand's token
+    tile -- takes the dense weight-gradient GEMM, the estimator's expectation)."""
 
     d: int = 128
     d_ff: int = 256
@@ -80,8 +82,11 @@ class TrainConfig:
     eval_batches: int = 8
     n_classes: int = 4
     schedule_total_steps: int | None = None
+    collect_block_stats: bool = False  # trainer.py:93: weight snapshots at refreshes -> block_flip_stats
 
     def __post_init__(self) -> None:
+        if hasattr(self.activation, "value"):  # the reference's Activation enum (gated_ffn.py:47-50)
+            self.activation = self.activation.value
         if self.steps < 1:
             raise ValueError("steps must be >= 1")
         for name in ("d", "d_ff"):
@@ -274,6 +279,7 @@ class RunArtifacts:
     final_eval_loss: float
     mask_search_calls: int
     proxy_rates: np.ndarray | None = None
+    block_stats: list | None = None  # [(name, FlipTrace)] when cfg.collect_block_stats (trainer.py:463-468)
 
 
 def _proxy_masks(stack: "FFNStack") -> list[TransposableMask]:
@@ -325,6 +331,7 @@ def run_training(cfg: TrainConfig, device="cuda") -> RunArtifacts:
     have_masks = False
     since_refresh = 0
     proxy = np.zeros(T) if cfg.proxy_flips else None
+    snapshots: dict = {}
     prev_proxy = None
     if proxy is not None:
         prev_proxy = _proxy_masks(stack)
@@ -363,6 +370,10 @@ def run_training(cfg: TrainConfig, device="cuda") -> RunArtifacts:
                 flips[t - 1] = float(n) / stack.size
             have_masks = True
             since_refresh = 0
+            if cfg.collect_block_stats:
+                for blk, layer in enumerate(stack.layers):
+                    for name, w in (("w_in", layer.w_in), ("w2", layer.w2)):
+                        snapshots.setdefault(f"block{blk}.{name}", []).append(w.detach().clone())
         loss, dout = task.loss_and_grad(out, tgt)
         out.backward(dout.to(out.dtype))
         losses[t - 1] = loss.detach()
@@ -372,6 +383,8 @@ def run_training(cfg: TrainConfig, device="cuda") -> RunArtifacts:
             st.lr = lr
             m = masks.get(id(p))
             adam_step(st, p.grad, m, DecayConfig(lambda_w=lam, mode=DecayMode.ON_WEIGHTS) if m is not None else None)
+        for layer in stack.layers:
+            layer.mark_weights_updated()  # adam_step writes p.data: an optimizer step the version counters miss
         since_refresh += 1
         if proxy is not None:
             pm = _proxy_masks(stack)
@@ -393,8 +406,11 @@ def run_training(cfg: TrainConfig, device="cuda") -> RunArtifacts:
     final = [{k: getattr(layer, n).detach().double().cpu().numpy() for k, n in
               (("w_in", "w_in"), ("bias", "bias_in"), ("w2", "w2"))} for layer in stack.layers]
     rates = proxy if (not cfg.sparse and proxy is not None) else flips
+    block_stats = None
+    if cfg.collect_block_stats and snapshots:
+        block_stats = [(name, block_flip_stats(snaps)) for name, snaps in snapshots.items() if len(snaps) >= 2]
     return RunArtifacts(cfg, losses.cpu().numpy().astype(np.float64), rates, final, float(np.mean(ev)), searches,
-                        proxy)
+                        proxy, block_stats)
 
 
 def make_warmup_runner(base_cfg: TrainConfig, warmup_steps: int, refresh_period: int = 1):

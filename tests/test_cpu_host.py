@@ -191,7 +191,7 @@ def test_bench_reference_arm_line():
     assert line["impl"] == "reference"
     assert line["unit"] == "tokens/s" and line["value"] > 0 and line["higher_is_better"] is True
     assert line["metric"].startswith("2:4 FFN fwd+bwd tokens/s")
-    assert "BASELINE.json configs[1]" in line["config"]["workload"]
+    assert "BASELINE.json configs[3]" in line["config"]["workload"]  # the default headline: C4
     cb = line["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["sample"] and cb["value"] == line["value"]
     e2e = line["e2e"]

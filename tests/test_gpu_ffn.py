@@ -143,8 +143,13 @@ def test_sparse_ffn_module_autograd_vs_oracle(act):
     assert normwise_rel(mod.bias_in.grad.cpu().numpy(), br["dbias_in"]) < TOL
     assert normwise_rel(mod.w2.grad.cpu().numpy(), br["dw2"]) < TOL
     assert mod.mask_searches == 2
-    # refresh schedule: 40 training steps -> one more search
+    # refresh schedule: 40 optimizer steps -> one more search; forwards within one step
+    # (gradient accumulation) neither recompress nor advance the schedule
+    for _ in range(3):
+        mod(x)
+    assert mod.mask_searches == 2
     for _ in range(40):
+        mod.mark_weights_updated()
         mod(x)
     assert mod.mask_searches == 4
 
