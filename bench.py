@@ -307,14 +307,13 @@ class SparseStep:
             # dX GEMM leaves DP_RESERVED_SMS SMs to the collective so the two actually overlap
             if self.world > 1:
                 work.append(self.torch.distributed.all_reduce(self.bucket, group=self.pg, async_op=True))
-                self.C.call("s24_set_reserved_sms", DP_RESERVED_SMS)
+                E.RESERVED_SMS = DP_RESERVED_SMS
 
-        g = E.ffn_backward(st, dy, self.op_in, self.op_out, self.act, w_in_dense=self.w_in, w2_dense=self.w2,
-                           lam=LAMBDA / self.world, dw_in_out=self.dw_in, dw2_out=self.dw2, mvue=bool(self.mvue),
-                           rng_seed=self.t, mvue_exact=self.mvue == "exact", dbias_out=self.dbias,
-                           grads_ready=grads_ready)
-        if self.world > 1:
-            self.C.call("s24_set_reserved_sms", 0)
+        with E.reserved_sms(0):  # grads_ready raises it for the dX GEMM while the all-reduce runs
+            g = E.ffn_backward(st, dy, self.op_in, self.op_out, self.act, w_in_dense=self.w_in, w2_dense=self.w2,
+                               lam=LAMBDA / self.world, dw_in_out=self.dw_in, dw2_out=self.dw2, mvue=bool(self.mvue),
+                               rng_seed=self.t, mvue_exact=self.mvue == "exact", dbias_out=self.dbias,
+                               grads_ready=grads_ready)
         for w in work:
             w.wait()
         self.t += 1

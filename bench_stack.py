@@ -9,7 +9,7 @@ GEMM+GELU, GEMM; dGELU-fused dA, dW2 and dW_in with the masked decay, dX), and e
 block's gradient bucket [dW_in | dbias | dW2] is all-reduced asynchronously as soon as
 its dW GEMMs are enqueued, so the collective of block l overlaps the backward of
 blocks l-1 .. 0.  The last few SMs are left to NCCL while any
-all-reduce can be in flight (s24_set_reserved_sms).  Same JSON contract as bench.py."""
+all-reduce can be in flight (the GEMMs' reserved_sms argument, engine.RESERVED_SMS).  Same JSON contract as bench.py."""
 from __future__ import annotations
 
 import os
@@ -68,14 +68,13 @@ class StackStep:
             def grads_ready(bucket=bucket):
                 if self.world > 1:
                     work.append(torch.distributed.all_reduce(bucket, group=self.pg, async_op=True))
-                    self.C.call("s24_set_reserved_sms", B.DP_RESERVED_SMS)
+                    E.RESERVED_SMS = B.DP_RESERVED_SMS
 
             g = E.ffn_backward(states[l], dh, op_in, op_out, self.act, w_in_dense=w_in, w2_dense=w2,
                                lam=B.LAMBDA / self.world, dw_in_out=dwi, dw2_out=dw2, dbias_out=db,
                                grads_ready=grads_ready, dx_accumulate=dh)
             states[l] = None
-        if self.world > 1:
-            self.C.call("s24_set_reserved_sms", 0)
+        E.RESERVED_SMS = 0
         for w in work:
             w.wait()
         self.t += 1

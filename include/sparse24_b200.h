@@ -46,7 +46,22 @@
 extern "C" {
 #endif
 
-#define S24_ABI_VERSION 1
+#define S24_ABI_VERSION 2
+
+/* GEMM workspace (every tensor-core GEMM entry point takes `void* workspace, int reserved_sms`):
+ * the caller allocates S24_GEMM_WORKSPACE_BYTES of device memory per stream, zeroes it once, and
+ * passes it to every GEMM on that stream; the kernels leave it zeroed except for the uint32 at
+ * byte 8, a sticky count of bounded cross-CTA waits that gave up (the persistent dW GEMMs'
+ * wave-synchronised schedule and the ordered split-K reduce wait for CTAs that were not
+ * co-resident, e.g. while another stream's kernels held SMs: the result stays correct, only the
+ * L2-locality / summation-order guarantee of that launch was dropped).  workspace = NULL: no
+ * wave synchronisation and no ordering -- fully stateless.  reserved_sms: leave that many SMs
+ * free (a data-parallel step lets its gradient all-reduce run beside the dX GEMM); 0 = all.
+ * The library keeps no mutable state between calls beyond per-process caches of immutable
+ * facts (SM count, kernel attributes). */
+#define S24_GEMM_WORKSPACE_BYTES 8448
+#define S24_GEMM_WS_TIMEOUTS_WORD 2
+int64_t s24_gemm_workspace_bytes(void);
 
 /* status codes */
 #define S24_OK 0
@@ -186,7 +201,8 @@ int s24_flat_to_e(const uint8_t* meta, int64_t m, int64_t k, uint8_t* e, void* s
  * m % 128 == 0, k % 128 == 0, n % 32 == 0. */
 int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b, int b_mn,
              int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias, int epilogue, uint16_t* aux,
-             int64_t ldaux, uint16_t* aux2, float* dbias, int d_t, int64_t gate_ff, void* stream);
+             int64_t ldaux, uint16_t* aux2, float* dbias, int d_t, int64_t gate_ff, void* workspace, int reserved_sms,
+             void* stream);
 
 /* ---- dense token-major GEMM with the training epilogues of s24_spmm ---------------
  * D^T[n, m] (token-major bf16, ldd) = epilogue(sum_k A[m, k] B[n, k]) with A the DENSE bf16
@@ -200,12 +216,10 @@ int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, c
  * :435-437) and the fused dense baseline of bench.py.  m % 128 (CTA pairs when m % 256 == 0), k % 64, n % 32 == 0. */
 int s24_gemm_act(const uint16_t* w, int w_t, int64_t ldw, int64_t w_gate_ff, int64_t m, int64_t k, const uint16_t* b,
                  int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias, int epilogue,
-                 uint16_t* aux, uint16_t* aux2, float* dbias, int64_t gate_ff, void* stream);
+                 uint16_t* aux, uint16_t* aux2, float* dbias, int64_t gate_ff, void* workspace, int reserved_sms,
+                 void* stream);
 
-/* Process-wide: leave `sms` SMs free in subsequent GEMM launches (0 = use all).  A
- * data-parallel step sets it around the dX GEMM so the gradient all-reduce's kernels run
- * concurrently with it (the persistent GEMMs otherwise occupy every SM). */
-int s24_set_reserved_sms(int sms);
+
 
 /* ---- K5: dense tcgen05 dW GEMM with fused masked decay ---------------------
  * D[m, n] (fp32, ldd) = sum_k A[m, k] B[n, k] + lambda_w * (1 - M[m, n]) * W[m, n]
@@ -217,7 +231,7 @@ int s24_set_reserved_sms(int sms);
  * order.  m % 128 == 0, n % 256 == 0 (or % 128), k % 64 == 0. */
 int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int b_mn, int64_t ldb, int64_t m,
                 int64_t n, int64_t k, float* d, int64_t ldd, const void* w, int w_dtype, const uint8_t* idx,
-                float lambda_w, int64_t gate_ff, void* stream);
+                float lambda_w, int64_t gate_ff, void* workspace, int reserved_sms, void* stream);
 
 /* ---- K8: MVUE sparsification of an upstream gradient (next row 1 of SURVEY 8f) ----
  * G is n tokens x f features (token-major, ldg); the sparsified matrix is G^T with
@@ -249,7 +263,7 @@ int s24_mvue_prune(const void* g, int dtype, int64_t rows, int64_t cols, int col
  * w / idx / lambda_w / gate_ff as s24_gemm_dw.  m % 128, k % 128, n % 128 == 0. */
 int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b, int b_mn,
                 int64_t ldb, int64_t n, float* d, int64_t ldd, const void* w, int w_dtype, const uint8_t* idx,
-                float lambda_w, int64_t gate_ff, void* stream);
+                float lambda_w, int64_t gate_ff, void* workspace, int reserved_sms, void* stream);
 
 /* ---- K6/K7: fused (gated) activation, token-major ----------------------------
  * Z is n tokens x r_in (r_in = 2r gated, = r plain), row pitch ldz; A is n x r.

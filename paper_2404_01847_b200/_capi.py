@@ -23,6 +23,7 @@ LIB_PATH = os.environ.get("S24_LIB_PATH") or os.path.join(_HERE, "libs24b200.so"
 S24_OK, S24_ERR_SHAPE, S24_ERR_FORMAT, S24_ERR_UNSUPPORTED, S24_ERR_CUDA, S24_ERR_ARG = range(6)
 S24_BF16, S24_F32, S24_F64 = 0, 1, 2
 ACT_RELU, ACT_GELU, ACT_GEGLU, ACT_SWIGLU = 0, 1, 2, 3
+GEMM_WORKSPACE_BYTES, GEMM_WS_TIMEOUTS_WORD = 8448, 2  # S24_GEMM_WORKSPACE_BYTES (header)
 EPI_STORE, EPI_GELU_AUX, EPI_GELU_GRAD, EPI_DGELU, EPI_GEGLU_GRAD, EPI_SWIGLU_GRAD, EPI_DGATED, EPI_STORE_ADD = range(8)
 
 _P = ctypes.c_void_p
@@ -43,12 +44,13 @@ SIGNATURES = {
     "s24_bits_to_idx": [_P, _I64, _I64, _P, _P, _P],
     "s24_meta_flat": [_P, _I64, _I64, _P, _P, _P],
     "s24_e_to_flat": [_P, _I64, _I64, _P, _P],
-    "s24_spmm": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _I64, _P, _P, _I, _I64, _P],
-    "s24_gemm_dw": [_P, _I, _I64, _P, _I, _I64, _I64, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _P],
-    "s24_gemm_act": [_P, _I, _I64, _I64, _I64, _I64, _P, _I64, _I64, _P, _I64, _P, _I, _P, _P, _P, _I64, _P],
+    "s24_spmm": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _I64, _P, _P, _I, _I64, _P, _I, _P],
+    "s24_gemm_dw": [_P, _I, _I64, _P, _I, _I64, _I64, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _P, _I, _P],
+    "s24_gemm_act": [_P, _I, _I64, _I64, _I64, _I64, _P, _I64, _I64, _P, _I64, _P, _I, _P, _P, _P, _I64, _P, _I,
+                     _P],
     "s24_mvue_compress": [_P, _I64, _I64, _I64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                           ctypes.c_uint64, _I64, _P, _P, _P, _I, _P],
-    "s24_spmm_dw": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _P],
+    "s24_spmm_dw": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _P, _I, _P],
     "s24_act_fwd": [_P, _I64, _I64, _I64, _I, _P, _I64, _P],
     "s24_act_bwd": [_P, _I64, _P, _I64, _I64, _I64, _I, _P, _I64, _P, _P],
     "s24_masked_decay": [_P, _P, _I, _P, _I64, _I64, _F, _P],
@@ -56,7 +58,6 @@ SIGNATURES = {
     "s24_adam_step": [_P, _P, _P, _I, _P, _I, _I64, _I64, _P] + [ctypes.c_double] * 10 + [_I, _P],
     "s24_mask_flips": [_P, _P, _I64, _P, _P, _P],
     "s24_greedy_search": [_P, _I, _I64, _I64, _P, _P, _P],
-    "s24_set_reserved_sms": [_I],
     "s24_prune_compress_pair": [_P, _P, _I, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _I64, _P],
     "s24_prune_2of4": [_P, _I, _I64, _I64, _I, _P, _P],
     "s24_block_gaps": [_P, _I, _I64, _I64, _P, _P],
@@ -89,6 +90,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             fn.restype = ctypes.c_int
         lib.s24_last_error_string.argtypes = []
         lib.s24_last_error_string.restype = ctypes.c_char_p
+        lib.s24_gemm_workspace_bytes.argtypes = []
+        lib.s24_gemm_workspace_bytes.restype = ctypes.c_int64
         _lib = lib
         return lib
 

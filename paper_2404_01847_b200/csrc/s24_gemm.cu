@@ -73,12 +73,21 @@ struct GemmShape {
                 //    partial tiles are summed with TMA add-reduce stores into the zeroed output;
                 // S >= 2: lockstep split-K (WorkIter), partial tiles add-reduced the same way
   int group_m;  // M tiles per raster group: each group sweeps all N with its A panels L2-resident
-  int wave_slot;  // >= 0: wave-synchronised schedule on counter slot g_wave_ctr[wave_slot] (see below)
+  unsigned int* ws;  // caller's GEMM workspace (S24 ABI: zeroed once, left zeroed by every launch), or NULL
+  int wave_sync;     // wave-synchronised schedule on ws[kWsWave] (see below; needs ws)
   int exp;      // experiment flags (timing studies only, results invalid): 1 skip B loads, 2 skip metadata cp, 4 every tile loads the B tile of n = 0,
                 //  16 no activation math in the epilogue, 32 no epilogue global loads,
                 //  128 no GELU'(z) AUX stores, 256 no D stores (fragment epilogue)
   int a_gate;   // dense A through the 4-D u/v interleave map (gated first weight in [u; v] order)
 };
+
+// Experiment flags exist only in builds with -DS24_EXPERIMENTS (attribution studies); in the
+// production library every S24_EXP(f) is a compile-time false and the flag code is gone.
+#ifdef S24_EXPERIMENTS
+#define S24_EXP(f) ((shp.exp & (f)) != 0)
+#else
+#define S24_EXP(f) (false)
+#endif
 
 __constant__ uint16_t c_gemm_pat_bits[90] = S24_PATTERN_BITS;
 
@@ -160,11 +169,12 @@ struct Cfg {
 // the lower HBM power allowed).  Each producer counts the tiles whose loads it has issued and,
 // before the first load of wave w, waits until all CTAs have issued wave w - 1.  Purely a
 // locality hint: the wait is bounded (~20 us), so CTAs that are not co-resident (an SM taken
-// by another kernel) only cost time, never a hang.  The last CTA to exit resets the slot, so
-// every launch (and every CUDA-graph replay) starts from zero; the host spreads streams over
-// slots.
-constexpr int kWaveSlots = 64;
-__device__ unsigned int g_wave_ctr[kWaveSlots][2];  // [slot][0: tiles issued, 1: CTAs exited]
+// by another kernel) only cost time, never a hang -- and a wait that gives up is counted in
+// ws[kWsTimeouts], so the caller can see that the locality (or, below, ordering) guarantee was
+// dropped.  The last CTA to exit resets the counters, so every launch (and every CUDA-graph
+// replay) starts from zero.  The counters live in the CALLER's workspace (one per stream), not
+// in library globals: concurrent launches on different streams never share them.
+constexpr int kWsWave = 0, kWsExit = 1, kWsTimeouts = 2, kWsSplit = 16;
 
 // Ordered split-K (WorkIter mode S >= 3): the S partial tiles of one output tile are add-reduced
 // in split order, so the fp32 sums are run-to-run identical.  Every storer (epilogue warp of
@@ -172,7 +182,7 @@ __device__ unsigned int g_wave_ctr[kWaveSlots][2];  // [slot][0: tiles issued, 1
 // bulk reduce-adds (per-tile counter, bounded spin: the order is a determinism guarantee, the sum
 // is correct either way), and the storer that completes the last split resets the counter.
 constexpr int kSplitTiles = 2048;
-__device__ unsigned int g_split_ctr[kWaveSlots][kSplitTiles];
+static_assert((kWsSplit + kSplitTiles) * 4 <= S24_GEMM_WORKSPACE_BYTES, "GEMM workspace too small");
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
   unsigned int v;
@@ -341,23 +351,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       WorkIter wk(shp.streamk, num_work, num_kb, cluster_id, num_clusters);
       int tile, kb0, kb1, wave = 0;
-      unsigned int* wctr = (shp.wave_slot >= 0 && shp.streamk != 1) ? &g_wave_ctr[shp.wave_slot][0] : nullptr;
+      unsigned int* wctr = (shp.ws != nullptr && shp.wave_sync && shp.streamk != 1) ? shp.ws + kWsWave : nullptr;
       while (wk.next(num_work, num_kb, tile, kb0, kb1)) {
         if (wctr != nullptr && wave > 0) {
           // every producer has issued the previous wave's loads (bounded wait)
           const unsigned int target = gridDim.x * wave;
           const long long t0 = clock64();
-          while (static_cast<int>(ld_acquire_gpu(wctr) - target) < 0 && clock64() - t0 < 40000) __nanosleep(32);
+          bool late = false;
+          while (static_cast<int>(ld_acquire_gpu(wctr) - target) < 0) {
+            if (clock64() - t0 >= 40000) {
+              late = true;
+              break;
+            }
+            __nanosleep(32);
+          }
+          if (late) atomicAdd(shp.ws + kWsTimeouts, 1u);
         }
         int mb, nb;
         coords(tile, mb, nb);
         const int m0 = mb * C::TILE_M + 128 * rank;      // this CTA's A rows (slab s: + 128 kCG s)
-        const int nb0 = ((shp.exp & 4) ? 0 : nb * kBN) + C::BN_CTA * rank;  // this CTA's B rows (N split)
+        const int nb0 = (S24_EXP(4) ? 0 : nb * kBN) + C::BN_CTA * rank;  // this CTA's B rows (N split)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + C::A_BYTES;
-          const bool skip_b = shp.exp & 1;
+          const bool skip_b = S24_EXP(1);
           if (rank == 0)
             mbar_expect_tx(&full_bar[stage], (C::TX_BYTES - (skip_b ? C::TX_BYTES - C::A_BYTES - C::E_BYTES : 0)) * kCG);
           if constexpr (kSparse) {
@@ -429,7 +447,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t b_addr = a_addr + C::A_BYTES;
-          if (kSparse && !(shp.exp & 2)) {
+          if (kSparse && !S24_EXP(2)) {
             // metadata: 128 rows x 16 B (no swizzle, 8-row core matrices 128 B apart) -> 4 TMEM columns
 #pragma unroll
             for (int sl = 0; sl < kSlabs; ++sl)
@@ -492,7 +510,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int e = warp - 4, q = e & 3, cw = e >> 2;
       const int t4 = lane >> 2;
       uint8_t* stg = smem + C::EPI_OFF + e * 4096;
-      const uint32_t stg_a = smem_u32(stg);
       // stmatrix row addresses: thread 8j + i addresses row i of matrix j
       const int mj = lane >> 3, mi = lane & 7;
       int acc = 0, sbuf = 0, par = 0;
@@ -574,7 +591,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   const float u = v[4 * c + 2 * sl + k] + bias4[sl];
                   const float w = v[16 + 4 * c + 2 * sl + k] + bias4[2 + sl];
                   float a, da;
-                  if (shp.exp & 16) { a = u; da = u; }
+                  if S24_EXP(16) { a = u; da = u; }
                   else if (ep.act == S24_ACT_SWIGLU) gate_act<true>(u, a, da);
                   else gate_act<false>(u, a, da);
                   a2[k] = a * w;
@@ -586,21 +603,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 g2[2 * c + sl] = pack_bf16x2(o2[0], o2[1]);
               }
             }
-            // A: [32 tokens][16 features], 32-byte rows, 32B swizzle; matrices (c, s)
-            if (lane == 0) bulk_wait_read0();
+            // A: [32 tokens][16 features], 32-byte rows, 32B swizzle; matrices (c, s); two 1 KB
+            // staging buffers, so the stmatrix of this chunk overlaps the previous chunk's store
+            uint8_t* ab = stg + sbuf * 1024;
+            const uint32_t ab_a = smem_u32(ab);
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             __syncwarp();
 #pragma unroll
             for (int hc = 0; hc < 2; ++hc) {
               const int tok = 8 * (2 * hc + (mj >> 1)) + mi, sl = mj & 1;
-              stmatrix_x4_trans(stg_a + tok * 32 + ((sl ^ ((tok >> 2) & 1)) << 4), pa[4 * hc], pa[4 * hc + 1],
+              stmatrix_x4_trans(ab_a + tok * 32 + ((sl ^ ((tok >> 2) & 1)) << 4), pa[4 * hc], pa[4 * hc + 1],
                                 pa[4 * hc + 2], pa[4 * hc + 3]);
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmD, stg, fg, n0);
+              tma_store_2d(&tmD, ab, fg, n0);
               bulk_commit();
             }
+            sbuf ^= 1;
             uint4* p1 = aux_frag(ep.aux, fg >> 4, shp.n, n0) + lane;
             uint4* p2 = aux_frag(ep.aux2, fg >> 4, shp.n, n0) + lane;
 #pragma unroll
@@ -630,24 +651,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
               }
             }
-            if (lane == 0) bulk_wait_read0();
-            __syncwarp();
-            // [32 tokens][64 columns], 128-byte rows, 128B swizzle; one stmatrix per (h, c):
-            // matrices j = (u/v, s) -> 16-byte column chunk 4 h + j
+            // [32 tokens][64 columns] as two [32 tokens][32 columns] halves h (64-byte rows, 64B
+            // swizzle, double-buffered 2 KB staging, one TMA store each); one stmatrix per c:
+            // matrices j = (u/v, s) -> 16-byte column chunk j of half h
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
+              uint8_t* zb = stg + sbuf * 2048;
+              const uint32_t zb_a = smem_u32(zb);
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              __syncwarp();
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
                 const int tok = 8 * c + mi;
-                stmatrix_x4_trans(stg_a + tok * 128 + (((4 * h + mj) ^ (tok & 7)) << 4), pz[h][0][0][c],
-                                  pz[h][0][1][c], pz[h][1][0][c], pz[h][1][1][c]);
+                stmatrix_x4_trans(zb_a + tok * 64 + ((mj ^ ((tok >> 1) & 3)) << 4), pz[h][0][0][c], pz[h][0][1][c],
+                                  pz[h][1][0][c], pz[h][1][1][c]);
               }
-            }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmD, stg, 2 * m_w, n0);
-              bulk_commit();
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&tmD, zb, 2 * m_w + 32 * h, n0);
+                bulk_commit();
+              }
+              sbuf ^= 1;
             }
           } else {
             // kEpiStore (+bias), kEpiGeluGrad (GELU(z) out, GELU'(z) to AUX), kEpiDAct (acc * AUX)
@@ -680,7 +705,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
                 if constexpr (kEpi == kEpiGeluGrad) {
                   float g0, g1, d0, d1;
-                  if (shp.exp & 16) { g0 = d0 = x0; g1 = d1 = x1; }
+                  if S24_EXP(16) { g0 = d0 = x0; g1 = d1 = x1; }
                   else { gelu_and_grad(x0, g0, d0); gelu_and_grad(x1, g1, d1); }
                   x0 = g0;
                   x1 = g1;
@@ -688,14 +713,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
                 pd[4 * c + j] = pack_bf16x2(x0, x1);
               }
-              if (kEpi == kEpiGeluGrad && !(shp.exp & 128)) {
+              if (kEpi == kEpiGeluGrad && !S24_EXP(128)) {
                 // GELU'(z) -> AUX unit (row m_w + 8 j + t4, this chunk)
                 aux_frag(ep.aux, (m_w >> 4) + (j >> 1), shp.n, n0)[32 * (j & 1) + lane] =
                     make_uint4(gq[0], gq[1], gq[2], gq[3]);
               }
             }
             // [32 tokens][32 features], 64-byte rows, 64B swizzle, double-buffered; one stmatrix per c
-            if (shp.exp & 256) continue;
+            if S24_EXP(256) continue;
             uint8_t* zb = stg + sbuf * 2048;
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             __syncwarp();
@@ -769,8 +794,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         constexpr unsigned int kStorers = 8 * kCG;
         // (stream-K runs are ordered only when none is empty: T >= clusters)
         unsigned int* sctr = (kEpi == kEpiDw && (shp.streamk >= 3 || (shp.streamk == 1 && wk.total >= wk.ncl)) &&
-                              shp.wave_slot >= 0 && tile < kSplitTiles)
-                                 ? &g_split_ctr[shp.wave_slot][tile] : nullptr;
+                              shp.ws != nullptr && tile < kSplitTiles)
+                                 ? shp.ws + kWsSplit + tile : nullptr;
         const int sidx = wk.last_split;
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
@@ -778,7 +803,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (lane == 0) {
             const unsigned int target = kStorers * static_cast<unsigned int>(sidx);
             const long long t0 = clock64();
-            while (ld_acquire_gpu(sctr) < target && clock64() - t0 < 2000000) __nanosleep(64);
+            while (ld_acquire_gpu(sctr) < target) {
+              if (clock64() - t0 >= 2000000) {  // order (determinism) dropped, sum still correct
+                atomicAdd(shp.ws + kWsTimeouts, 1u);
+                break;
+              }
+              __nanosleep(64);
+            }
             asm volatile("fence.proxy.async.global;" ::: "memory");
           }
           __syncwarp();
@@ -815,14 +846,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int u = 0; u < 8; ++u) pre[u] = __ldg(wp + u);
           }
         };
-        if (kPre && !(shp.exp & 32)) prefetch(h);
+        if (kPre && !S24_EXP(32)) prefetch(h);
 #pragma unroll 1
         for (int cc = h; cc < kBN / 32; cc += 2) {
           uint4 cur[8];
           uint2 cur_idx = pre_idx;
 #pragma unroll
           for (int u = 0; u < 8; ++u) cur[u] = pre[u];
-          if (kPre && !(shp.exp & 32)) prefetch(cc + 2);
+          if (kPre && !S24_EXP(32)) prefetch(cc + 2);
           uint32_t r[32];
           tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + slab * kBN + 32 * cc, r);
           tmem_ld_wait();
@@ -956,11 +987,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_cg<kCG>(tmem_base, C::TMEM_COLS);
-  if (shp.wave_slot >= 0 && threadIdx.x == 0) {
-    // the last CTA out resets the slot for the next launch on this stream
-    if (atomicAdd(&g_wave_ctr[shp.wave_slot][1], 1u) == gridDim.x - 1) {
-      atomicExch(&g_wave_ctr[shp.wave_slot][0], 0u);
-      atomicExch(&g_wave_ctr[shp.wave_slot][1], 0u);
+  if (shp.ws != nullptr && shp.wave_sync && threadIdx.x == 0) {
+    // the last CTA out resets the wave counter for the next launch on this stream
+    if (atomicAdd(shp.ws + kWsExit, 1u) == gridDim.x - 1) {
+      atomicExch(shp.ws + kWsWave, 0u);
+      atomicExch(shp.ws + kWsExit, 0u);
     }
   }
 }
@@ -1034,10 +1065,9 @@ static int make_map_gate(CUtensorMap* map, const void* ptr, int64_t inner, int64
   return S24_OK;
 }
 
-// SMs left free by the persistent GEMMs (s24_set_reserved_sms): a data-parallel step reserves a
-// few while its gradient all-reduce runs so the collective's kernel is co-resident with the
-// dX GEMM instead of queueing behind it.
-static int g_reserved_sms = 0;
+// SMs left free by the persistent GEMMs (the `reserved_sms` argument of every GEMM entry point):
+// a data-parallel step reserves a few while its gradient all-reduce runs so the collective's
+// kernel is co-resident with the dX GEMM instead of queueing behind it.
 
 static int num_sms() {
   static int n = 0;
@@ -1062,11 +1092,15 @@ static int num_sms() {
 // (176 -> 748 MB) and made them 20 % slower.  The K-aligned order (WorkIter mode 1: every run
 // starts with the segment at k-block 0 of its last tile) keeps all clusters within
 // (1 - tiles / clusters) of a tile's K range of each other (C2: 35 k-blocks, ~23 MB of panels),
-// and the partial tiles reduce in K order through g_split_ctr (deterministic).  Measured on B200
+// and the partial tiles reduce in K order through the workspace's split counters (deterministic).  Measured on B200
 // at C2: HBM reads 203 MB (vs 176 MB one-tile-per-pair), kernel 98.7 vs 103.0 us under ncu --
 // but only 4 % of the 13.5 % the fill promises, and with the zeroing memset of the fp32 output
 // the dW step inside full training steps measured 7 % slower, so the automatic choice stays off.
 static int use_streamk(int tiles, int clusters, int num_kb, bool auto_ok = false, double out_bytes = 0.0) {
+#ifndef S24_EXPERIMENTS
+  (void)tiles, (void)clusters, (void)num_kb, (void)auto_ok, (void)out_bytes;
+  return 0;  // measured slower (see above): experiment builds only
+#endif
   static const int env = getenv("S24_STREAMK") ? atoi(getenv("S24_STREAMK")) : -1;
   if (env >= 0) return env == 1 ? 1 : 0;
   static const bool auto_env = getenv("S24_STREAMK_AUTO") != nullptr;  // experiment: the rule below
@@ -1082,7 +1116,7 @@ static int use_streamk(int tiles, int clusters, int num_kb, bool auto_ok = false
 // measured 0.221 -> 0.182 ms per launch).  Unlike stream-K every wave stays at one K offset
 // (panels shared in L2).  Partial tiles TMA-add-reduce into the zeroed output: with two addends
 // (a + b = b + a) the result is order-independent, and for S >= 3 the splits of a tile reduce in
-// split order (g_split_ctr), so every split stays deterministic.  The automatic choice stops at
+// split order (the workspace's split counters), so every split stays deterministic.  The automatic choice stops at
 // S = 2: S = 8 would fill C2's 64-tile dW waves (0.875 tile-times) but measured 25 % slower on
 // B200 (8 reduce passes of the fp32 tile through L2 per output), and C5 got slower too.  A split
 // must save >= 3 %, each unit keeps K >= 64 * kb_min, and the fp32 output must fit well inside L2
@@ -1109,19 +1143,16 @@ static int use_splitk(int tiles, int clusters, int num_kb, int kb_min, double ou
   return bt <= 0.97 * t1 ? best : 0;
 }
 
-static int dw_clusters() {
-  const int sms = g_reserved_sms > 0 ? std::max(2, num_sms() - g_reserved_sms) : num_sms();
+static int dw_clusters(int reserved) {
+  const int sms = reserved > 0 ? std::max(2, num_sms() - reserved) : num_sms();
   return sms / 2;
 }
 
-// Wave-synchronised schedule (g_wave_ctr): on for the dW GEMMs (panels of K = tokens, far
-// larger than L2), S24_WAVESYNC=0/1 turns it off / on for every GEMM.  Slot = stream hash.
-static int wave_slot(void* stream, bool dflt) {
+// Wave-synchronised schedule (workspace wave counter): on for the dW GEMMs (panels of K = tokens,
+// far larger than L2); S24_WAVESYNC=0/1 turns it off / on for every GEMM.
+static int wave_on(bool dflt) {
   static const int env = getenv("S24_WAVESYNC") ? atoi(getenv("S24_WAVESYNC")) : -1;
-  const bool on = env < 0 ? dflt : env != 0;
-  if (!on) return -1;
-  const uintptr_t h = reinterpret_cast<uintptr_t>(stream);
-  return static_cast<int>((h ^ (h >> 7) ^ (h >> 17)) % kWaveSlots);
+  return (env < 0 ? dflt : env != 0) ? 1 : 0;
 }
 
 // Two-slab dense dW tiles (512 x 256 per CTA pair, one 512-column accumulator): -25 % operand
@@ -1155,7 +1186,7 @@ static bool use_slabs(int64_t m, int64_t n, int64_t k) {
 
 // B multicast across two CTA pairs (gemm_kernel kMC = 2): halves the L2 reads of the token
 // operand.  S24_MC=0/1 overrides; needs an even number of 256-row pair tiles.
-static bool use_mc(int64_t m) {
+[[maybe_unused]] static bool use_mc(int64_t m) {
   static const int env = getenv("S24_MC") ? atoi(getenv("S24_MC")) : -1;
   if (m % 512 != 0 || env == 0) return false;
   return env == 1;
@@ -1175,8 +1206,12 @@ static bool use_slabs_epi(int64_t m, int64_t n, int64_t k) {
 }
 
 static int exp_flags() {
+#ifdef S24_EXPERIMENTS
   static const int v = getenv("S24_EXP") ? atoi(getenv("S24_EXP")) : 0;
   return v;
+#else
+  return 0;
+#endif
 }
 
 static int pick_group_m(int num_m, double a_bytes_per_mtile) {
@@ -1191,7 +1226,7 @@ template <bool kSparse, bool kAMN, bool kBMN, int kBN, int kStages, int kCG, int
           int kAcc = 2, int kSlabs = 1, int kMC = 1>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& me, const CUtensorMap& md,
                        const CUtensorMap& mx, const CUtensorMap& my, const GemmShape& shp, const EpiParams& ep,
-                       cudaStream_t st) {
+                       int reserved, cudaStream_t st) {
   using C = Cfg<kSparse, kAMN, kBMN, kBN, kStages, kCG, kAcc, kSlabs>;
   auto kern = gemm_kernel<kSparse, kAMN, kBMN, kBN, kStages, kCG, kEpi, kOutT, kAcc, kSlabs, kMC>;
   static bool attr_done = false;  // per template instance
@@ -1225,7 +1260,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
     }
   }
   int cap = max_clusters;
-  if (g_reserved_sms > 0) cap = std::max(1, std::min(cap, (num_sms() - g_reserved_sms) / kCS));
+  if (reserved > 0) cap = std::max(1, std::min(cap, (num_sms() - reserved) / kCS));
   const int units = shp.streamk >= 2 ? tiles * shp.streamk : tiles;
   const int clusters = (shp.streamk == 1 || units > cap) ? cap : units;
   if (clusters <= 0) return S24_OK;
@@ -1255,17 +1290,16 @@ static int cg_override() {
   return v;
 }
 
-extern "C" int s24_set_reserved_sms(int sms) {
-  S24_REQUIRE(sms >= 0, S24_ERR_ARG, "reserved SM count must be >= 0");
-  g_reserved_sms = sms;
-  return S24_OK;
-}
+extern "C" int64_t s24_gemm_workspace_bytes(void) { return S24_GEMM_WORKSPACE_BYTES; }
+
 
 extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b,
                         int b_mn, int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias,
                         int epilogue, uint16_t* aux, int64_t ldaux, uint16_t* aux2, float* dbias, int d_t,
-                        int64_t gate_ff, void* stream) {
+                        int64_t gate_ff, void* workspace, int reserved, void* stream) {
   S24_REQUIRE(a_vals && a_e && b && d, S24_ERR_ARG, "NULL operand");
+  S24_REQUIRE(reserved >= 0 && (reinterpret_cast<uintptr_t>(workspace) & 3) == 0, S24_ERR_ARG,
+              "reserved_sms must be >= 0 and the workspace 4-byte aligned");
   S24_REQUIRE(m % 128 == 0 && k % 128 == 0 && n % 32 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
               "sparse GEMM needs m %% 128 == 0, k %% 128 == 0, n %% 32 == 0 (got m=%lld k=%lld n=%lld)",
               (long long)m, (long long)k, (long long)n);
@@ -1307,8 +1341,8 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     if (int rc = make_map(&md, d, m / 2, n, ldd, 16, 32, kMapBf16Sw32)) return rc;
     mx = my = md;
   } else if (gated_bwd) {
-    // dZ interleaved, token-major: boxes of 64 columns x 32 tokens, 128B-swizzled staging
-    if (int rc = make_map(&md, d, 2 * m, n, ldd, 64, 32, kMapBf16Sw128)) return rc;
+    // dZ interleaved, token-major: boxes of 32 columns x 32 tokens, 64B-swizzled staging
+    if (int rc = make_map(&md, d, 2 * m, n, ldd, 32, 32, kMapBf16Sw64)) return rc;
     mx = my = md;
   } else {
     // D[m, n] feature-major (64B-swizzled staging) or D^T[n, m] token-major (d_t: stmatrix.trans into
@@ -1341,7 +1375,7 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   const int tile_m = pair ? 256 : 128;
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0,
                 pick_group_m(static_cast<int>(m / tile_m), 1.125 * tile_m * static_cast<double>(k)),
-                wave_slot(stream, false), exp_flags()};
+                static_cast<unsigned int*>(workspace), wave_on(false), exp_flags()};
   EpiParams ep{d,       ldd,
                bias,    aux,
                ldaux,   dbias,
@@ -1353,12 +1387,12 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
 #define S24_SP(BMN, BNV, CG, EPI)                                                                          \
   if (d_t)                                                                                                  \
     return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
-                       EPI, true>(ma, mb, me, md, mx, my, shp, ep, st);                                     \
+                       EPI, true>(ma, mb, me, md, mx, my, shp, ep, reserved, st);                                     \
   return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG,   \
-                     EPI, false>(ma, mb, me, md, mx, my, shp, ep, st)
+                     EPI, false>(ma, mb, me, md, mx, my, shp, ep, reserved, st)
 #define S24_SPT(BMN, BNV, CG, EPI)                                                                           \
   return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, EPI, \
-                     true>(ma, mb, me, md, mx, my, shp, ep, st)
+                     true>(ma, mb, me, md, mx, my, shp, ep, reserved, st)
 #define S24_SP_EPI(BMN, BNV, CG)                                              \
   switch (epilogue) {                                                           \
     case S24_EPI_GELU_AUX: S24_SP(BMN, BNV, CG, kEpiGeluAux);                   \
@@ -1370,12 +1404,13 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     default: S24_SP(BMN, BNV, CG, kEpiStore);                                   \
   }
   const bool slabs = pair && !b_mn && d_t && epilogue == S24_EPI_STORE && use_slabs(m, n, k);
+#ifdef S24_EXPERIMENTS
   if (!slabs && pair && !b_mn && d_t && epilogue != S24_EPI_GELU_AUX && use_mc(m)) {
     // 4-CTA clusters, B multicast across the two pairs: B boxes of BN_CTA / 2 rows
     if (int rc = make_map(&mb, b, k, n, ldb, 64, BN2 / 4)) return rc;
 #define S24_SPMC(EPI)                                                                                             \
   return launch_gemm<true, false, false, BN2, stages_for<Cfg<true, false, false, BN2, 1, 2>::STAGE_BYTES>(), 2, EPI, \
-                     true, 2, 1, 2>(ma, mb, me, md, mx, my, shp, ep, st)
+                     true, 2, 1, 2>(ma, mb, me, md, mx, my, shp, ep, reserved, st)
     switch (epilogue) {
       case S24_EPI_GELU_GRAD: S24_SPMC(kEpiGeluGrad);
       case S24_EPI_DGELU: S24_SPMC(kEpiDAct);
@@ -1386,16 +1421,17 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
     }
 #undef S24_SPMC
   }
+#endif
   if (slabs) {
     // two A slabs per CTA, one accumulator: 512 x 224 pair tiles
     using CS = Cfg<true, false, false, BN2, 1, 2, 1, 2>;
     return launch_gemm<true, false, false, BN2, stages_for<CS::STAGE_BYTES>(), 2, kEpiStore, true, 1, 2>(
-        ma, mb, me, md, mx, my, shp, ep, st);
+        ma, mb, me, md, mx, my, shp, ep, reserved, st);
   }
   if (pair && !b_mn && d_t && epilogue != S24_EPI_STORE && epilogue != S24_EPI_GELU_AUX && use_slabs_epi(m, n, k)) {
     using CS = Cfg<true, false, false, BN2, 1, 2, 1, 2>;
 #define S24_SPSL(EPI) \
-  return launch_gemm<true, false, false, BN2, stages_for<CS::STAGE_BYTES>(), 2, EPI, true, 1, 2>(ma, mb, me, md, mx, my, shp, ep, st)
+  return launch_gemm<true, false, false, BN2, stages_for<CS::STAGE_BYTES>(), 2, EPI, true, 1, 2>(ma, mb, me, md, mx, my, shp, ep, reserved, st)
     switch (epilogue) {
       case S24_EPI_GELU_GRAD: S24_SPSL(kEpiGeluGrad);
       case S24_EPI_DGELU: S24_SPSL(kEpiDAct);
@@ -1423,8 +1459,10 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
 extern "C" int s24_gemm_act(const uint16_t* w, int w_t, int64_t ldw, int64_t w_gate_ff, int64_t m, int64_t k,
                             const uint16_t* b, int64_t ldb, int64_t n, uint16_t* d, int64_t ldd, const uint16_t* bias,
                             int epilogue, uint16_t* aux, uint16_t* aux2, float* dbias, int64_t gate_ff,
-                            void* stream) {
+                            void* workspace, int reserved, void* stream) {
   S24_REQUIRE(w && b && d, S24_ERR_ARG, "NULL operand");
+  S24_REQUIRE(reserved >= 0 && (reinterpret_cast<uintptr_t>(workspace) & 3) == 0, S24_ERR_ARG,
+              "reserved_sms must be >= 0 and the workspace 4-byte aligned");
   S24_REQUIRE(m % 128 == 0 && k % 64 == 0 && n % 32 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
               "dense GEMM needs m %% 128 == 0, k %% 64 == 0, n %% 32 == 0 (got m=%lld k=%lld n=%lld)",
               (long long)m, (long long)k, (long long)n);
@@ -1468,19 +1506,20 @@ extern "C" int s24_gemm_act(const uint16_t* w, int w_t, int64_t ldw, int64_t w_g
   if (gated_fwd) {
     if (int rc = make_map(&md, d, m / 2, n, ldd, 16, 32, kMapBf16Sw32)) return rc;
   } else if (gated_bwd) {
-    if (int rc = make_map(&md, d, 2 * m, n, ldd, 64, 32, kMapBf16Sw128)) return rc;
+    if (int rc = make_map(&md, d, 2 * m, n, ldd, 32, 32, kMapBf16Sw64)) return rc;
   } else {
     if (int rc = make_map(&md, d, m, n, ldd, 32, 32, kMapBf16Sw64)) return rc;
   }
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0,
-                pick_group_m(static_cast<int>(m / (pair ? 256 : 128)), 0.0), -1, 0, w_gate_ff > 0 ? 1 : 0};
+                pick_group_m(static_cast<int>(m / (pair ? 256 : 128)), 0.0), static_cast<unsigned int*>(workspace),
+                wave_on(false), 0, w_gate_ff > 0 ? 1 : 0};
   EpiParams ep{d,       ldd,   bias,    aux,     0,   dbias, aux2,
                epilogue == S24_EPI_SWIGLU_GRAD ? S24_ACT_SWIGLU : S24_ACT_GEGLU,
                gate_ff, nullptr, 0,     nullptr, 0.0f, accumulate ? 1 : 0};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define S24_DA(AMN, BNV, CG, EPI)                                                                               \
   return launch_gemm<false, AMN, false, BNV, stages_for<Cfg<false, AMN, false, BNV, 1, CG>::STAGE_BYTES>(), CG, \
-                     EPI, true>(ma, mb, mb, md, md, md, shp, ep, st)
+                     EPI, true>(ma, mb, mb, md, md, md, shp, ep, reserved, st)
 #define S24_DA_EPI(AMN, BNV, CG)                                   \
   switch (epilogue) {                                              \
     case S24_EPI_GELU_GRAD: S24_DA(AMN, BNV, CG, kEpiGeluGrad);    \
@@ -1502,10 +1541,13 @@ extern "C" int s24_gemm_act(const uint16_t* w, int w_t, int64_t ldw, int64_t w_g
 
 extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int b_mn, int64_t ldb,
                            int64_t m, int64_t n, int64_t k, float* d, int64_t ldd, const void* w, int w_dtype,
-                           const uint8_t* idx, float lambda_w, int64_t gate_ff, void* stream) {
+                           const uint8_t* idx, float lambda_w, int64_t gate_ff, void* workspace, int reserved,
+                           void* stream) {
   if (gate_ff > 0)
     S24_REQUIRE(m == 2 * gate_ff && gate_ff % 16 == 0, S24_ERR_SHAPE, "gated dW: m must be 2 * d_ff");
   S24_REQUIRE(a && b && d, S24_ERR_ARG, "NULL operand");
+  S24_REQUIRE(reserved >= 0 && (reinterpret_cast<uintptr_t>(workspace) & 3) == 0, S24_ERR_ARG,
+              "reserved_sms must be >= 0 and the workspace 4-byte aligned");
   S24_REQUIRE(m % 128 == 0 && n % 128 == 0 && k % 64 == 0 && m > 0 && n > 0 && k > 0, S24_ERR_SHAPE,
               "dW GEMM needs m %% 128 == 0, n %% 128 == 0, k %% 64 == 0 (got m=%lld n=%lld k=%lld)", (long long)m,
               (long long)n, (long long)k);
@@ -1541,11 +1583,11 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   const int clusters = num_sms() / (pair ? 2 : 1);
   const int tiles = static_cast<int>((m / (pair ? 256 : 128)) * (n / BN));
   const bool slabs = pair && a_mn && b_mn && m % 512 == 0 && use_dw_slabs(m, n, k);
-  int streamk = slabs ? 0 : use_streamk(tiles, pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 64),
+  int streamk = slabs ? 0 : use_streamk(tiles, pair ? dw_clusters(reserved) : 2 * dw_clusters(reserved), static_cast<int>(k / 64),
                                          true, 4.0 * m * n);
   if (!streamk)
     streamk = use_splitk(slabs ? static_cast<int>((m / 512) * (n / 256)) : tiles,
-                         pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 64), 32, 4.0 * m * n);
+                         pair ? dw_clusters(reserved) : 2 * dw_clusters(reserved), static_cast<int>(k / 64), 32, 4.0 * m * n);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (streamk) {
     cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
@@ -1555,16 +1597,16 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   static const int env_dw = getenv("S24_GROUP_M_DW") ? atoi(getenv("S24_GROUP_M_DW")) : 8;
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), streamk,
                 static_cast<int>(m / tile_m) < env_dw ? static_cast<int>(m / tile_m) : env_dw,
-                wave_slot(stream, true), exp_flags()};
+                static_cast<unsigned int*>(workspace), wave_on(true), exp_flags()};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
 
 #define S24_DW(AMN, BMN, BNV, CG)                                                                      \
   return launch_gemm<false, AMN, BMN, BNV, stages_for<Cfg<false, AMN, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
-                     kEpiDw>(ma, mb, me, md, md, md, shp, ep, st)
+                     kEpiDw>(ma, mb, me, md, md, md, shp, ep, reserved, st)
   if (slabs) {
     using CS = Cfg<false, true, true, 256, 1, 2, 1, 2>;
     return launch_gemm<false, true, true, 256, stages_for<CS::STAGE_BYTES>(), 2, kEpiDw, false, 1, 2>(
-        ma, mb, me, md, md, md, shp, ep, st);
+        ma, mb, me, md, md, md, shp, ep, reserved, st);
   }
   if (pair) {
     if (a_mn && b_mn) S24_DW(true, true, 256, 2);
@@ -1587,8 +1629,11 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
 
 extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b,
                            int b_mn, int64_t ldb, int64_t n, float* d, int64_t ldd, const void* w, int w_dtype,
-                           const uint8_t* idx, float lambda_w, int64_t gate_ff, void* stream) {
+                           const uint8_t* idx, float lambda_w, int64_t gate_ff, void* workspace, int reserved,
+                           void* stream) {
   S24_REQUIRE(a_vals && a_e && b && d, S24_ERR_ARG, "NULL operand");
+  S24_REQUIRE(reserved >= 0 && (reinterpret_cast<uintptr_t>(workspace) & 3) == 0, S24_ERR_ARG,
+              "reserved_sms must be >= 0 and the workspace 4-byte aligned");
   S24_REQUIRE(m % 128 == 0 && k % 128 == 0 && n % 128 == 0 && m > 0 && k > 0 && n > 0, S24_ERR_SHAPE,
               "sparse dW GEMM needs m %% 128 == 0, k %% 128 == 0, n %% 128 == 0 (got m=%lld k=%lld n=%lld)",
               (long long)m, (long long)k, (long long)n);
@@ -1617,19 +1662,19 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
   const int sk_tiles = static_cast<int>((m / (pair ? 256 : 128)) * (n / (wide ? 256 : 128)));
   int streamk = use_streamk(sk_tiles, num_sms() / (pair ? 2 : 1), static_cast<int>(k / 128));
   if (!streamk)
-    streamk = use_splitk(sk_tiles, pair ? dw_clusters() : 2 * dw_clusters(), static_cast<int>(k / 128), 16, 4.0 * m * n);
+    streamk = use_splitk(sk_tiles, pair ? dw_clusters(reserved) : 2 * dw_clusters(reserved), static_cast<int>(k / 128), 16, 4.0 * m * n);
   if (streamk) {
     cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   }
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), streamk, 8,
-                streamk == 1 ? -1 : wave_slot(stream, true), 0};
+                static_cast<unsigned int*>(workspace), streamk == 1 ? 0 : wave_on(true), 0};
   EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
   // BN = 256 with one TMEM accumulator (256 + 4 metadata columns): K = tokens is long, so the
   // un-overlapped epilogue is a small share; the B half per CTA is exactly two 64-wide chunks
 #define S24_SDW(BMN, BNV, CG, ACC)                                                                            \
   return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG, ACC>::STAGE_BYTES>(), \
-                     CG, kEpiDw, false, ACC>(ma, mb, me, md, md, md, shp, ep, st)
+                     CG, kEpiDw, false, ACC>(ma, mb, me, md, md, md, shp, ep, reserved, st)
   if (wide) {
     if (pair) {
       if (b_mn) S24_SDW(true, 256, 2, 1);

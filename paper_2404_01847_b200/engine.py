@@ -42,6 +42,49 @@ class _NoTimer:
 # attribute step time to kernels); the default is a no-op.
 TIMER = _NoTimer()
 
+# Per-(device, stream) GEMM workspace (include/sparse24_b200.h, S24_GEMM_WORKSPACE_BYTES): the
+# counters of the dW GEMMs' wave-synchronised schedule and ordered split-K live here, owned by the
+# caller, so launches on different streams never share them and the library keeps no state.
+_WORKSPACES: dict = {}
+# SMs every GEMM leaves free (the data-parallel step sets it while its all-reduce is in flight)
+RESERVED_SMS = 0
+
+
+def gemm_workspace(t: torch.Tensor) -> torch.Tensor:
+    dev = t.device
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    ws = _WORKSPACES.get(key)
+    if ws is None:
+        ws = torch.zeros(C.GEMM_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+        _WORKSPACES[key] = ws
+    return ws
+
+
+def gemm_timeouts(device=None) -> int:
+    """Bounded cross-CTA waits that gave up on the current stream's GEMMs so far (their L2-locality
+    or summation-order guarantee was dropped; the results are correct either way)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    ws = _WORKSPACES.get((dev.index, torch.cuda.current_stream(dev).cuda_stream))
+    return 0 if ws is None else int(ws[C.GEMM_WS_TIMEOUTS_WORD].item())
+
+
+class reserved_sms:
+    """Context: every GEMM launched inside leaves `n` SMs free (per-call argument of the ABI)."""
+
+    def __init__(self, n: int):
+        self.n = int(n)
+
+    def __enter__(self):
+        global RESERVED_SMS
+        self.prev, RESERVED_SMS = RESERVED_SMS, self.n
+        return self
+
+    def __exit__(self, *a):
+        global RESERVED_SMS
+        RESERVED_SMS = self.prev
+        return False
+
+
 ACT_CODES = {"relu": C.ACT_RELU, "gelu": C.ACT_GELU, "geglu": C.ACT_GEGLU, "swiglu": C.ACT_SWIGLU}
 GATED = {"geglu", "swiglu"}
 
@@ -150,7 +193,8 @@ def spmm(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b
     with TIMER(tag):
         C.call("s24_spmm", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), b.stride(0), n,
                out.data_ptr(), out.stride(0), C.ptr(bias), epi, C.ptr(aux), aux.stride(0) if aux is not None else 0,
-               C.ptr(aux2), C.ptr(dbias), int(out_t), gate_ff, C.stream_of(out))
+               C.ptr(aux2), C.ptr(dbias), int(out_t), gate_ff, gemm_workspace(out).data_ptr(),
+               RESERVED_SMS, C.stream_of(out))
 
 
 def gemm_dw(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, m: int, n: int, k: int,
@@ -161,7 +205,8 @@ def gemm_dw(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, m: int, n:
     with TIMER(tag):
         C.call("s24_gemm_dw", a.data_ptr(), int(a_mn), a.stride(0), b.data_ptr(), int(b_mn), b.stride(0), m, n,
                k, out.data_ptr(), out.stride(0), C.ptr(w) if decay else None, C.dtype_code(w) if decay else 0,
-               C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, C.stream_of(out))
+               C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, gemm_workspace(out).data_ptr(),
+               RESERVED_SMS, C.stream_of(out))
 
 
 def mvue_seed(rng_seed: int, salt: int) -> int:
@@ -205,7 +250,8 @@ def spmm_dw(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor
     with TIMER(tag):
         C.call("s24_spmm_dw", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), b.stride(0), n,
                out.data_ptr(), out.stride(0), C.ptr(w) if decay else None, C.dtype_code(w) if decay else 0,
-               C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, C.stream_of(out))
+               C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, gemm_workspace(out).data_ptr(),
+               RESERVED_SMS, C.stream_of(out))
 
 
 @dataclass
@@ -248,7 +294,8 @@ def _mm(op, bwd: bool, b: torch.Tensor, n: int, out: torch.Tensor, tag: str, epi
     with TIMER(tag):
         C.call("s24_gemm_act", op.w.data_ptr(), int(bwd), op.w.stride(0), op.perm_ff, m, k, b.data_ptr(),
                b.stride(0), n, out.data_ptr(), out.stride(0), C.ptr(bias), epi, C.ptr(aux), C.ptr(aux2),
-               C.ptr(dbias), gate_ff, C.stream_of(out))
+               C.ptr(dbias), gate_ff, gemm_workspace(out).data_ptr(),
+               RESERVED_SMS, C.stream_of(out))
 
 
 def aux_empty(f: int, n: int, device) -> torch.Tensor:

@@ -170,7 +170,7 @@ def _sparse_product(vals: torch.Tensor, meta: torch.Tensor, m: int, k: int, b_nk
     else:
         d = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
     C.call("s24_spmm", v.data_ptr(), e.data_ptr(), M, K, b.data_ptr(), 0, K, N, d.data_ptr(), d.stride(0), None,
-           C.EPI_STORE, None, 0, None, None, int(out_nm), 0, C.stream_of(d))
+           C.EPI_STORE, None, 0, None, None, int(out_nm), 0, None, 0, C.stream_of(d))
     return d[:n, :m] if out_nm else d[:m, :n]
 
 
@@ -214,7 +214,7 @@ def dense_matmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     bp[:k, :n] = b
     d = torch.empty((M, N), dtype=torch.float32, device=a.device)
     C.call("s24_gemm_dw", ap.data_ptr(), 0, K, bp.data_ptr(), 1, N, M, N, K, d.data_ptr(), N, None, 0, None, 0.0,
-           0, C.stream_of(d))
+           0, None, 0, C.stream_of(d))
     return d[:m, :n]
 
 

@@ -33,9 +33,10 @@ def test_library_builds_and_exports_every_header_symbol():
     # the ctypes binding types exactly the declared compute entry points
     from paper_2404_01847_b200 import _capi
 
-    assert set(_capi.SIGNATURES) | {"s24_last_error_string"} == set(syms)
+    assert set(_capi.SIGNATURES) | {"s24_last_error_string", "s24_gemm_workspace_bytes"} == set(syms)
     lib_h = _capi.load()
-    assert lib_h.s24_abi_version() == 1
+    assert lib_h.s24_abi_version() == 2
+    assert lib_h.s24_gemm_workspace_bytes() == _capi.GEMM_WORKSPACE_BYTES
 
 
 def test_cuda_calls_fail_loudly_without_gpu():

@@ -408,4 +408,4 @@ def test_dx_accumulate_into_residual_gradient(d, d_ff, n):
     # the accumulate epilogue needs the token-major store
     with pytest.raises(RuntimeError):
         C.call("s24_spmm", op_in.bwd_vals.data_ptr(), op_in.bwd_e.data_ptr(), d, d_ff, st.a.data_ptr(), 0, d_ff,
-               n, dh.data_ptr(), n, None, C.EPI_STORE_ADD, None, 0, None, None, 0, 0, C.stream_of(dh))
+               n, dh.data_ptr(), n, None, C.EPI_STORE_ADD, None, 0, None, None, 0, 0, None, 0, C.stream_of(dh))

@@ -1,0 +1,25 @@
+"""One training step of the 2:4 FFN block (K1 refresh, fwd, bwd with the fused decay), one K2
+step, and one fused dense step, for compute-sanitizer (memcheck / racecheck / synccheck).
+python tools/sanitize_step.py <c2|c5|c3-small>"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench as B  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+cfg = dict(B.CONFIGS["c5" if name == "c5" else "c2"])
+if name == "c5":
+    cfg["layers"] = 1  # one block of the GPT-2 large stack
+if name == "c3-small":  # the gated (SwiGLU) epilogues at a sanitizer-friendly size
+    cfg = dict(d=1024, d_ff=2816, act="swiglu", tokens=4096, workload="c3-shaped small")
+dev = torch.device("cuda", 0)
+w_in, bias, w2, x, dy = B.make_problem(cfg, dev, 1)
+st = B.SparseStep(w_in, bias, w2, cfg["act"], 1)
+st(x, dy)  # refresh step: K1 + fwd + bwd
+st(x, dy)  # K2 step
+B.DenseFusedStep(w_in, bias, w2, cfg["act"])(x, dy)
+torch.cuda.synchronize()
+print("sanitize step ok", name)
