@@ -228,10 +228,12 @@ int s24_gemm_act(const uint16_t* w, int w_t, int64_t ldw, int64_t w_gate_ff, int
  * a_mn = 0 -> A stored m x k, 1 -> k x m; b_mn likewise (n x k / k x n).
  * idx/w may be NULL (no decay).  gate_ff > 0: A's rows (m = 2 gate_ff) are in the gated
  * u/v-interleaved order (idx too); D rows and the W rows read for the decay are in [u; v]
- * order.  m % 128 == 0, n % 256 == 0 (or % 128), k % 64 == 0. */
+ * order.  accumulate = 1: D += the product (TMA fp32 add-reduce into D's current values; the
+ * decay, if given, is added once) -- the split-bf16 products of the fp32 mode.
+ * m % 128 == 0, n % 256 == 0 (or % 128), k % 64 == 0. */
 int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int b_mn, int64_t ldb, int64_t m,
                 int64_t n, int64_t k, float* d, int64_t ldd, const void* w, int w_dtype, const uint8_t* idx,
-                float lambda_w, int64_t gate_ff, void* workspace, int reserved_sms, void* stream);
+                float lambda_w, int64_t gate_ff, int accumulate, void* workspace, int reserved_sms, void* stream);
 
 /* ---- K8: MVUE sparsification of an upstream gradient (next row 1 of SURVEY 8f) ----
  * G is n tokens x f features (token-major, ldg); the sparsified matrix is G^T with
@@ -263,7 +265,7 @@ int s24_mvue_prune(const void* g, int dtype, int64_t rows, int64_t cols, int col
  * w / idx / lambda_w / gate_ff as s24_gemm_dw.  m % 128, k % 128, n % 128 == 0. */
 int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b, int b_mn,
                 int64_t ldb, int64_t n, float* d, int64_t ldd, const void* w, int w_dtype, const uint8_t* idx,
-                float lambda_w, int64_t gate_ff, void* workspace, int reserved_sms, void* stream);
+                float lambda_w, int64_t gate_ff, int accumulate, void* workspace, int reserved_sms, void* stream);
 
 /* ---- K6/K7: fused (gated) activation, token-major ----------------------------
  * Z is n tokens x r_in (r_in = 2r gated, = r plain), row pitch ldz; A is n x r.
@@ -276,6 +278,25 @@ int s24_act_fwd(const uint16_t* z, int64_t ldz, int64_t r, int64_t n, int act, u
                 void* stream);
 int s24_act_bwd(const uint16_t* z, int64_t ldz, const uint16_t* da, int64_t ldda, int64_t r, int64_t n, int act,
                 uint16_t* dz, int64_t lddz, float* dbias, void* stream);
+
+/* ---- fp32 mode (the reference's float32 fused type, _core.pyx:21-23; C1 is fp32) ----------
+ * tf32 structured sparsity is 1:2 per 32-bit pair and cannot hold a transposable 2:4 mask, so
+ * the fp32 mode runs every product as three bf16 2:4 products on split operands
+ * (x = x_hi + x_lo, A B ~= A_hi B_hi + A_hi B_lo + A_lo B_hi, fp32 accumulation through the
+ * accumulate flag of s24_spmm_dw / s24_gemm_dw).  Activations are FEATURE-major fp32
+ * (features x tokens, ld >= n), the storage order of the reference's column-major outputs.
+ * s24_split_bf16: hi = bf16(x), lo = bf16(x - hi) over n elements.
+ * s24_act_fwd_f32: Z (r_in x n; r_in = 2r gated with rows [u; v], else r) += bias (fp32, may
+ *   be NULL) in place, then A = act(z) or act(z_u) z_v (exact erf GELU, exp SiLU) into A
+ *   (r x n fp32) and its split A_hi / A_lo (bf16, pitch lda) -- gated_ffn.py:264-270, 293-297.
+ * s24_act_bwd_f32: dZ (fp32, may be NULL) and its split dZ_hi / dZ_lo (pitch lddz) from the
+ *   pre-activation Z and dA (r x n), and dbias[r_in] = sum over tokens (fixed-order reduction,
+ *   written not accumulated) -- gated_ffn.py:336-348. */
+int s24_split_bf16(const float* x, int64_t n, uint16_t* hi, uint16_t* lo, void* stream);
+int s24_act_fwd_f32(float* z, int64_t ldz, const float* bias, int64_t r, int64_t n, int act, float* a, int64_t lda,
+                    uint16_t* a_hi, uint16_t* a_lo, void* stream);
+int s24_act_bwd_f32(const float* z, int64_t ldz, const float* da, int64_t ldda, int64_t r, int64_t n, int act,
+                    float* dz, int64_t lddz, uint16_t* dz_hi, uint16_t* dz_lo, float* dbias, void* stream);
 
 /* ---- comparators ----------------------------------
  * Greedy 2-approximate transposable search (transposable_search_greedy, sparsity.py:

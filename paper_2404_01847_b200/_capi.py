@@ -45,16 +45,19 @@ SIGNATURES = {
     "s24_meta_flat": [_P, _I64, _I64, _P, _P, _P],
     "s24_e_to_flat": [_P, _I64, _I64, _P, _P],
     "s24_spmm": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _I64, _P, _P, _I, _I64, _P, _I, _P],
-    "s24_gemm_dw": [_P, _I, _I64, _P, _I, _I64, _I64, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _P, _I, _P],
+    "s24_gemm_dw": [_P, _I, _I64, _P, _I, _I64, _I64, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _I, _P, _I, _P],
     "s24_gemm_act": [_P, _I, _I64, _I64, _I64, _I64, _P, _I64, _I64, _P, _I64, _P, _I, _P, _P, _P, _I64, _P, _I,
                      _P],
     "s24_mvue_compress": [_P, _I64, _I64, _I64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                           ctypes.c_uint64, _I64, _P, _P, _P, _I, _P],
-    "s24_spmm_dw": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _P, _I, _P],
+    "s24_spmm_dw": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _I, _P, _I, _P],
     "s24_act_fwd": [_P, _I64, _I64, _I64, _I, _P, _I64, _P],
     "s24_act_bwd": [_P, _I64, _P, _I64, _I64, _I64, _I, _P, _I64, _P, _P],
     "s24_masked_decay": [_P, _P, _I, _P, _I64, _I64, _F, _P],
     "s24_masked_decay_bits": [_P, _P, _I, _P, _I64, _F, _P],
+    "s24_split_bf16": [_P, _I64, _P, _P, _P],
+    "s24_act_fwd_f32": [_P, _I64, _P, _I64, _I64, _I, _P, _I64, _P, _P, _P],
+    "s24_act_bwd_f32": [_P, _I64, _P, _I64, _I64, _I64, _I, _P, _I64, _P, _P, _P, _P],
     "s24_adam_step": [_P, _P, _P, _I, _P, _I, _I64, _I64, _P] + [ctypes.c_double] * 10 + [_I, _P],
     "s24_mask_flips": [_P, _P, _I64, _P, _P, _P],
     "s24_greedy_search": [_P, _I, _I64, _I64, _P, _P, _P],

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libs24b200.so")
-SOURCES = ["s24_capi.cu", "s24_mask.cu", "s24_act.cu", "s24_gemm.cu", "s24_mvue.cu", "s24_optim.cu", "s24_greedy.cu", "s24_pack.cu"]
+SOURCES = ["s24_capi.cu", "s24_mask.cu", "s24_act.cu", "s24_gemm.cu", "s24_mvue.cu", "s24_optim.cu", "s24_greedy.cu", "s24_pack.cu", "s24_fp32.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -788,7 +788,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         int mb, nb;
         coords(tile, mb, nb);
         const bool first_chunk = kb0 == 0;                  // adds the decay exactly once
-        const bool partial = kb0 != 0 || kb1 != num_kb;     // stream-K piece: add-reduce
+        // stream-K / split-K piece, or a launch that accumulates into D (fp32 mode): add-reduce
+        const bool partial = kb0 != 0 || kb1 != num_kb || ep.accumulate;
         const int n_base = nb * kBN;
         // ordered split-K: this unit's reduce-adds start after split s - 1 of the tile completed
         constexpr unsigned int kStorers = 8 * kCG;
@@ -1541,8 +1542,8 @@ extern "C" int s24_gemm_act(const uint16_t* w, int w_t, int64_t ldw, int64_t w_g
 
 extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int b_mn, int64_t ldb,
                            int64_t m, int64_t n, int64_t k, float* d, int64_t ldd, const void* w, int w_dtype,
-                           const uint8_t* idx, float lambda_w, int64_t gate_ff, void* workspace, int reserved,
-                           void* stream) {
+                           const uint8_t* idx, float lambda_w, int64_t gate_ff, int accumulate, void* workspace,
+                           int reserved, void* stream) {
   if (gate_ff > 0)
     S24_REQUIRE(m == 2 * gate_ff && gate_ff % 16 == 0, S24_ERR_SHAPE, "gated dW: m must be 2 * d_ff");
   S24_REQUIRE(a && b && d, S24_ERR_ARG, "NULL operand");
@@ -1589,7 +1590,7 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
     streamk = use_splitk(slabs ? static_cast<int>((m / 512) * (n / 256)) : tiles,
                          pair ? dw_clusters(reserved) : 2 * dw_clusters(reserved), static_cast<int>(k / 64), 32, 4.0 * m * n);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (streamk) {
+  if (streamk && !accumulate) {  // accumulate: the partial tiles add onto D's current values
     cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   }
@@ -1598,7 +1599,7 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), streamk,
                 static_cast<int>(m / tile_m) < env_dw ? static_cast<int>(m / tile_m) : env_dw,
                 static_cast<unsigned int*>(workspace), wave_on(true), exp_flags()};
-  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
+  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w, accumulate ? 1 : 0};
 
 #define S24_DW(AMN, BMN, BNV, CG)                                                                      \
   return launch_gemm<false, AMN, BMN, BNV, stages_for<Cfg<false, AMN, BMN, BNV, 1, CG>::STAGE_BYTES>(), CG, \
@@ -1629,8 +1630,8 @@ extern "C" int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint1
 
 extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, int64_t k, const uint16_t* b,
                            int b_mn, int64_t ldb, int64_t n, float* d, int64_t ldd, const void* w, int w_dtype,
-                           const uint8_t* idx, float lambda_w, int64_t gate_ff, void* workspace, int reserved,
-                           void* stream) {
+                           const uint8_t* idx, float lambda_w, int64_t gate_ff, int accumulate, void* workspace,
+                           int reserved, void* stream) {
   S24_REQUIRE(a_vals && a_e && b && d, S24_ERR_ARG, "NULL operand");
   S24_REQUIRE(reserved >= 0 && (reinterpret_cast<uintptr_t>(workspace) & 3) == 0, S24_ERR_ARG,
               "reserved_sms must be >= 0 and the workspace 4-byte aligned");
@@ -1663,13 +1664,13 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
   int streamk = use_streamk(sk_tiles, num_sms() / (pair ? 2 : 1), static_cast<int>(k / 128));
   if (!streamk)
     streamk = use_splitk(sk_tiles, pair ? dw_clusters(reserved) : 2 * dw_clusters(reserved), static_cast<int>(k / 128), 16, 4.0 * m * n);
-  if (streamk) {
+  if (streamk && !accumulate) {  // accumulate: the partial tiles add onto D's current values
     cudaError_t e = cudaMemset2DAsync(d, ldd * sizeof(float), 0, n * sizeof(float), m, st);
     S24_REQUIRE(e == cudaSuccess, S24_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   }
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), streamk, 8,
                 static_cast<unsigned int*>(workspace), streamk == 1 ? 0 : wave_on(true), 0};
-  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w};
+  EpiParams ep{d, ldd, nullptr, nullptr, 0, nullptr, nullptr, 0, gate_ff, w, w_dtype, idx, lambda_w, accumulate ? 1 : 0};
   // BN = 256 with one TMEM accumulator (256 + 4 metadata columns): K = tokens is long, so the
   // un-overlapped epilogue is a small share; the B half per CTA is exactly two 64-wide chunks
 #define S24_SDW(BMN, BNV, CG, ACC)                                                                            \

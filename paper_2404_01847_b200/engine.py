@@ -199,13 +199,14 @@ def spmm(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b
 
 def gemm_dw(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, m: int, n: int, k: int,
             out: torch.Tensor, w: torch.Tensor | None = None, idx: torch.Tensor | None = None,
-            lam: float = 0.0, tag: str = "k5_gemm_dw", gate_ff: int = 0) -> None:
-    """out[m, n] fp32 = sum_k A[m, k] B[n, k] + lam (1 - M) W  (dense tcgen05)."""
+            lam: float = 0.0, tag: str = "k5_gemm_dw", gate_ff: int = 0, accumulate: bool = False) -> None:
+    """out[m, n] fp32 (+)= sum_k A[m, k] B[n, k] + lam (1 - M) W  (dense tcgen05)."""
     decay = idx is not None and lam != 0.0
     with TIMER(tag):
         C.call("s24_gemm_dw", a.data_ptr(), int(a_mn), a.stride(0), b.data_ptr(), int(b_mn), b.stride(0), m, n,
                k, out.data_ptr(), out.stride(0), C.ptr(w) if decay else None, C.dtype_code(w) if decay else 0,
-               C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, gemm_workspace(out).data_ptr(),
+               C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, int(accumulate),
+               gemm_workspace(out).data_ptr(),
                RESERVED_SMS, C.stream_of(out))
 
 
@@ -244,13 +245,15 @@ def mvue_compress(g: torch.Tensor, seed: int, gate_ff: int = 0, want_pairs: bool
 
 def spmm_dw(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b_mn: bool, n: int,
             out: torch.Tensor, w: torch.Tensor | None = None, idx: torch.Tensor | None = None, lam: float = 0.0,
-            gate_ff: int = 0, tag: str = "k8_spmm_dw") -> None:
-    """out[m, n] fp32 = MVUE-sparse A~[m, k] . B[n, k]^T + lam (1 - M) W (2:4 tensor cores)."""
+            gate_ff: int = 0, tag: str = "k8_spmm_dw", accumulate: bool = False) -> None:
+    """out[m, n] fp32 (+)= 2:4 A~[m, k] . B[n, k]^T + lam (1 - M) W (2:4 tensor cores); A~ an MVUE
+    operand or a compressed weight (the fp32 mode's split-bf16 products)."""
     decay = idx is not None and lam != 0.0
     with TIMER(tag):
         C.call("s24_spmm_dw", vals.data_ptr(), e.data_ptr(), m, k, b.data_ptr(), int(b_mn), b.stride(0), n,
                out.data_ptr(), out.stride(0), C.ptr(w) if decay else None, C.dtype_code(w) if decay else 0,
-               C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, gemm_workspace(out).data_ptr(),
+               C.ptr(idx) if decay else None, float(lam if decay else 0.0), gate_ff, int(accumulate),
+               gemm_workspace(out).data_ptr(),
                RESERVED_SMS, C.stream_of(out))
 
 
@@ -467,3 +470,166 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
         dx = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
         _mm(w_in, True, dz, n, dx, "k4_spmm_bwd_in")
     return Grads(dx, dw_in, dbias, dw2)
+
+
+# ---------------------------------------------------------------------------
+# fp32 mode: split-bf16 products on the 2:4 tensor cores (include/sparse24_b200.h, s24_fp32.cu)
+
+
+def split_bf16(x: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """x (fp32, contiguous) -> (hi, lo) bf16 with hi = bf16(x), lo = bf16(x - hi)."""
+    x = x.contiguous()
+    hi = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
+    lo = torch.empty_like(hi)
+    C.call("s24_split_bf16", x.data_ptr(), x.numel(), hi.data_ptr(), lo.data_ptr(), C.stream_of(x))
+    return hi, lo
+
+
+@dataclass
+class SplitOperand:
+    """An fp32 weight under one transposable mask as two 2:4 operands: hi = bf16(W) and
+    lo = bf16(W - hi), sharing the pattern indices and E tiles (both orientations)."""
+
+    hi: CompressedOperand
+    lo: CompressedOperand
+
+    @property
+    def rows(self) -> int:
+        return self.hi.rows
+
+    @property
+    def cols(self) -> int:
+        return self.hi.cols
+
+    @property
+    def idx(self) -> torch.Tensor:
+        return self.hi.idx
+
+    @classmethod
+    def empty(cls, rows: int, cols: int, device) -> "SplitOperand":
+        hi = CompressedOperand.empty(rows, cols, device)
+        lo = CompressedOperand(rows, cols, hi.idx, torch.empty_like(hi.fwd_vals), hi.fwd_e,
+                               torch.empty_like(hi.bwd_vals), hi.bwd_e)
+        return cls(hi, lo)
+
+    def compress(self, w: torch.Tensor, with_meta: bool = False) -> None:
+        """Kept values of both halves (K2) from the current fp32 weight; with_meta also (re)builds
+        the E tiles from the pattern indices."""
+        w_hi, w_lo = split_bf16(w.float())
+        (compress_with_meta if with_meta else compress_values)(w_hi, self.hi)
+        compress_values(w_lo, self.lo)
+
+
+@dataclass
+class DenseSplitOperand:
+    """A dense fp32 weight as hi = bf16(W) and lo = bf16(W - hi) (the fp32 mode's masks=None
+    route): products on the dense tcgen05 GEMM with fp32 output."""
+
+    hi: torch.Tensor
+    lo: torch.Tensor
+    idx = None
+
+    @property
+    def rows(self) -> int:
+        return self.hi.shape[0]
+
+    @property
+    def cols(self) -> int:
+        return self.hi.shape[1]
+
+    @classmethod
+    def of(cls, w: torch.Tensor) -> "DenseSplitOperand":
+        return cls(*split_bf16(w.float()))
+
+
+def _split_spmm(op, bwd: bool, b_hi: torch.Tensor, b_lo: torch.Tensor, b_mn: bool, n: int,
+                out: torch.Tensor, tag: str) -> None:
+    """out[m, n] fp32 = W~ (or W~^T) . B^T as hi.hi + hi.lo + lo.hi (fixed order): the 2:4 GEMM
+    on a SplitOperand, the dense one on a DenseSplitOperand."""
+    m, k = (op.cols, op.rows) if bwd else (op.rows, op.cols)
+    for i, (a_op, b) in enumerate(((op.hi, b_hi), (op.hi, b_lo), (op.lo, b_hi))):
+        if isinstance(op, DenseSplitOperand):
+            gemm_dw(a_op, bwd, b, b_mn, m, n, k, out, tag=tag, accumulate=i > 0)
+        else:
+            spmm_dw(a_op.bwd_vals if bwd else a_op.fwd_vals, a_op.bwd_e if bwd else a_op.fwd_e, m, k, b, b_mn, n,
+                    out, tag=tag, accumulate=i > 0)
+
+
+def _split_dw(a_hi, a_lo, a_mn, b_hi, b_lo, b_mn, m, n, k, out, w=None, idx=None, lam=0.0, tag="k5_gemm_dw"):
+    for i, (a, b) in enumerate(((a_hi, b_hi), (a_hi, b_lo), (a_lo, b_hi))):
+        gemm_dw(a, a_mn, b, b_mn, m, n, k, out, w if i == 0 else None, idx if i == 0 else None,
+                lam if i == 0 else 0.0, tag=tag, accumulate=i > 0)
+
+
+@dataclass
+class FwdStateF32:
+    x_hi: torch.Tensor  # (N, d) bf16, token-major
+    x_lo: torch.Tensor
+    zt: torch.Tensor  # (r_in, N) fp32 feature-major pre-activation (bias added)
+    at: torch.Tensor  # (d_ff, N) fp32
+    a_hi: torch.Tensor  # (d_ff, N) bf16
+    a_lo: torch.Tensor
+    yt: torch.Tensor  # (d, N) fp32
+
+
+def ffn_forward_f32(x: torch.Tensor, w_in: SplitOperand, bias_in: torch.Tensor | None, w2: SplitOperand,
+                    act: str) -> FwdStateF32:
+    """fp32 mode forward (gated_ffn.py:293-297 on the float32 type): every product is three bf16
+    2:4 products with fp32 accumulation; activations feature-major fp32."""
+    n, d = x.shape
+    r_in, d_ff = w_in.rows, w2.cols
+    if w_in.cols != d or w2.rows != d or (r_in != (2 * d_ff if act in GATED else d_ff)):
+        raise ShapeError("layer weight shapes are inconsistent with the activation / input width")
+    if n % 128:
+        raise ShapeError(f"the fp32 mode needs a token count divisible by 128, got {n}")
+    dev = x.device
+    x_hi, x_lo = split_bf16(x.float())
+    zt = torch.empty((r_in, n), dtype=torch.float32, device=dev)
+    _split_spmm(w_in, False, x_hi, x_lo, False, n, zt, "k3_spmm_fwd_in")
+    at = torch.empty((d_ff, n), dtype=torch.float32, device=dev)
+    a_hi = torch.empty((d_ff, n), dtype=torch.bfloat16, device=dev)
+    a_lo = torch.empty_like(a_hi)
+    b = None if bias_in is None else bias_in.float().contiguous()
+    with TIMER("k6_act_fwd"):
+        C.call("s24_act_fwd_f32", zt.data_ptr(), n, C.ptr(b), d_ff, n, ACT_CODES[act], at.data_ptr(), n,
+               a_hi.data_ptr(), a_lo.data_ptr(), C.stream_of(zt))
+    yt = torch.empty((d, n), dtype=torch.float32, device=dev)
+    _split_spmm(w2, False, a_hi, a_lo, True, n, yt, "k3_spmm_fwd_out")
+    return FwdStateF32(x_hi, x_lo, zt, at, a_hi, a_lo, yt)
+
+
+@dataclass
+class GradsF32:
+    dxt: torch.Tensor  # (d, N) fp32 feature-major
+    dw_in: torch.Tensor  # (r_in, d) fp32
+    dbias_in: torch.Tensor  # (r_in,) fp32
+    dw2: torch.Tensor  # (d, d_ff) fp32
+
+
+def ffn_backward_f32(st: FwdStateF32, dy: torch.Tensor, w_in: SplitOperand, w2: SplitOperand, act: str,
+                     w_in_dense: torch.Tensor | None = None, w2_dense: torch.Tensor | None = None,
+                     lam: float = 0.0) -> GradsF32:
+    """fp32 mode backward (gated_ffn.py:327-356, mvue=False): dA, the activation backward with
+    the bias gradient, dX, and the dense dW GEMMs with the masked decay, all as split products."""
+    d, n = st.yt.shape
+    r_in, d_ff = w_in.rows, w2.cols
+    if tuple(dy.shape) != (n, d):
+        raise ShapeError(f"upstream shape {tuple(dy.shape)} != output shape {(n, d)}")
+    dev = dy.device
+    dy_hi, dy_lo = split_bf16(dy.float())
+    dat = torch.empty((d_ff, n), dtype=torch.float32, device=dev)
+    _split_spmm(w2, True, dy_hi, dy_lo, False, n, dat, "k4_spmm_bwd_out")
+    dz_hi = torch.empty((r_in, n), dtype=torch.bfloat16, device=dev)
+    dz_lo = torch.empty_like(dz_hi)
+    dbias = torch.empty(r_in, dtype=torch.float32, device=dev)
+    with TIMER("k7_act_bwd"):
+        C.call("s24_act_bwd_f32", st.zt.data_ptr(), n, dat.data_ptr(), n, d_ff, n, ACT_CODES[act], None, n,
+               dz_hi.data_ptr(), dz_lo.data_ptr(), dbias.data_ptr(), C.stream_of(dat))
+    dw2 = torch.empty((d, d_ff), dtype=torch.float32, device=dev)
+    _split_dw(dy_hi, dy_lo, True, st.a_hi, st.a_lo, False, d, d_ff, n, dw2, w2_dense, w2.idx, lam, "k5_gemm_dw2")
+    dw_in = torch.empty((r_in, d), dtype=torch.float32, device=dev)
+    _split_dw(dz_hi, dz_lo, False, st.x_hi, st.x_lo, True, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam,
+              "k5_gemm_dw_in")
+    dxt = torch.empty((d, n), dtype=torch.float32, device=dev)
+    _split_spmm(w_in, True, dz_hi, dz_lo, True, n, dxt, "k4_spmm_bwd_in")
+    return GradsF32(dxt, dw_in, dbias, dw2)

@@ -126,6 +126,20 @@ class FFNMasks:
     w_in: TransposableMask
     w_out: TransposableMask
     _ops: dict = field(default_factory=dict, repr=False, compare=False)
+    _ops_f32: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def plans_f32(self, layer: FFNLayer) -> dict:
+        """The fp32 mode's operands: both weights as SplitOperands (hi / lo values of both
+        orientations sharing the E tiles), validated once."""
+        if not self._ops_f32:
+            self.w_in.validate()
+            self.w_out.validate()
+            for name, mask, w in (("in", self.w_in, layer.w_in_cat), ("out", self.w_out, layer.w2)):
+                op = E.SplitOperand.empty(mask.shape[0], mask.shape[1], w.device)
+                op.hi.idx.copy_(mask.idx)
+                op.compress(w, with_meta=True)
+                self._ops_f32[name] = op
+        return self._ops_f32
 
     def plans(self, layer: FFNLayer | None = None) -> dict:
         if not self._ops:
@@ -163,7 +177,7 @@ class FstActivations:
     y: torch.Tensor  # (N, d)
     masks: FFNMasks | None
     w_in_cat: torch.Tensor
-    state: E.FwdState | None = None
+    state: "E.FwdState | E.FwdStateF32 | None" = None
 
 
 def _as_bf16(t: torch.Tensor) -> torch.Tensor:
@@ -171,11 +185,43 @@ def _as_bf16(t: torch.Tensor) -> torch.Tensor:
     return t if t.dtype == torch.bfloat16 else t.to(torch.bfloat16)
 
 
+def _fp32_mode(x: torch.Tensor, precision: str | None) -> bool:
+    if precision is None:  # the reference computes in its input's float type (_core.pyx:21-23)
+        return x.dtype in (torch.float32, torch.float64)
+    if precision not in ("bf16", "fp32"):
+        raise ValueError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
+    return precision == "fp32"
+
+
+def _fst_forward_f32(layer: FFNLayer, x: torch.Tensor, masks: FFNMasks | None) -> FstActivations:
+    """fp32 mode: split-bf16 products on the tensor cores, fp32 accumulation and activations
+    (include/sparse24_b200.h, s24_fp32.cu); outputs are the feature-major fp32 results viewed as
+    (tokens x features), i.e. the reference's column-major layout."""
+    C.require_cuda(x)
+    if masks is None:
+        w_in, w2 = E.DenseSplitOperand.of(layer.w_in_cat), E.DenseSplitOperand.of(layer.w2)
+    else:
+        ops = masks.plans_f32(layer)
+        ops["in"].compress(layer.w_in_cat)
+        ops["out"].compress(layer.w2)
+        w_in, w2 = ops["in"], ops["out"]
+    st = E.ffn_forward_f32(x.float(), w_in, layer.bias_in_cat, w2, layer.activation.value)
+    return FstActivations(layer, x, st.zt.t(), st.at.t(), st.yt.t(), masks, layer.w_in_cat, st)
+
+
 def fst_forward(layer: FFNLayer, x: torch.Tensor, masks: FFNMasks | None,
-                traversal: Traversal = Traversal.COL_ORDER) -> FstActivations:
+                traversal: Traversal = Traversal.COL_ORDER, precision: str | None = None) -> FstActivations:
     """Forward (gated_ffn.py:273-301).  masks=None is the dense path (dense
     fine-tuning, gated_ffn.py:286-289): the same tensor-core kernels on the
-    dense weights (s24_gemm_act) with the activation kernel K6."""
+    dense weights (s24_gemm_act) with the activation kernel K6.
+
+    precision: None follows the input like the reference's fused float type -- bf16 input runs
+    the bf16 path, float32 / float64 input the fp32 mode (split-bf16 products with fp32
+    accumulation, fp32 activations); 'bf16' / 'fp32' force one."""
+    if x.dim() != 2 or x.shape[1] != layer.d:
+        raise ShapeError(f"x shape {tuple(x.shape)} does not match layer width {layer.d}")
+    if _fp32_mode(x, precision):
+        return _fst_forward_f32(layer, x, masks)
     x = _as_bf16(x)
     if x.dim() != 2 or x.shape[1] != layer.d:
         raise ShapeError(f"x shape {tuple(x.shape)} does not match layer width {layer.d}")
@@ -198,6 +244,20 @@ def fst_backward(bundle: FstActivations, upstream: torch.Tensor, rng_seed: int =
     gradients reported against the dense weights.  `decay_lambda` (extension)
     fuses masked_decay_gradient (optim.py:105-114) into the dW epilogue."""
     layer = bundle.layer
+    if isinstance(bundle.state, E.FwdStateF32):
+        # fp32 mode: dense weight gradients (with mvue=True: the MVUE estimator's expectation)
+        C.require_cuda(upstream)
+        if tuple(upstream.shape) != tuple(bundle.y.shape):
+            raise ShapeError(f"upstream shape {tuple(upstream.shape)} != output shape {tuple(bundle.y.shape)}")
+        if bundle.masks is None:
+            w_in, w2 = E.DenseSplitOperand.of(layer.w_in_cat), E.DenseSplitOperand.of(layer.w2)
+            lam = 0.0
+        else:
+            ops = bundle.masks.plans_f32(layer)
+            w_in, w2, lam = ops["in"], ops["out"], decay_lambda
+        g = E.ffn_backward_f32(bundle.state, upstream.float(), w_in, w2, layer.activation.value,
+                               w_in_dense=layer.w_in_cat.float(), w2_dense=layer.w2.float(), lam=lam)
+        return _pack_grads(layer, g.dxt.t(), g.dw_in, g.dbias_in, g.dw2)
     up = _as_bf16(upstream)
     if tuple(up.shape) != tuple(bundle.y.shape):
         raise ShapeError(f"upstream shape {tuple(up.shape)} != output shape {tuple(bundle.y.shape)}")

@@ -214,7 +214,7 @@ def dense_matmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     bp[:k, :n] = b
     d = torch.empty((M, N), dtype=torch.float32, device=a.device)
     C.call("s24_gemm_dw", ap.data_ptr(), 0, K, bp.data_ptr(), 1, N, M, N, K, d.data_ptr(), N, None, 0, None, 0.0,
-           0, None, 0, C.stream_of(d))
+           0, 0, None, 0, C.stream_of(d))
     return d[:m, :n]
 
 
