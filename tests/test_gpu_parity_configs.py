@@ -133,8 +133,11 @@ def _oracle_step(c, act, mi, mo, lam):
     lo = o.Layer(_f64(c["w_in"]), _f64(c["b"]), _f64(c["w2"]), act)
     fr = o.fst_forward(lo, _f64(c["x"]), mi, mo, exact=False)
     br = o.fst_backward(lo, fr, _f64(c["dy"]), mi, mo, exact=False)
-    br["dw_in_decayed"] = o.masked_decay_gradient(br["dw_in"], lo.w_in, mi, lam)
-    br["dw2_decayed"] = o.masked_decay_gradient(br["dw2"], lo.w2, mo, lam)
+    if mi is None:  # the dense route has no decay
+        br["dw_in_decayed"], br["dw2_decayed"] = br["dw_in"], br["dw2"]
+    else:
+        br["dw_in_decayed"] = o.masked_decay_gradient(br["dw_in"], lo.w_in, mi, lam)
+        br["dw2_decayed"] = o.masked_decay_gradient(br["dw2"], lo.w2, mo, lam)
     return fr, br
 
 
@@ -252,8 +255,6 @@ def _fp32_case(act, d, d_ff, n, seed, sparse=True, lam=LAM):
         np.testing.assert_array_equal(mi, o.transposable_search_conv(_f64(c["w_in"])))
         np.testing.assert_array_equal(mo, o.transposable_search_conv(_f64(c["w2"])))
     fr, br = _oracle_step(c, act, mi, mo, lam if sparse else 0.0)
-    if not sparse:
-        br["dw_in_decayed"], br["dw2_decayed"] = br["dw_in"], br["dw2"]
     dw_in = torch.cat([g.d_u, g.d_v]) if layer.is_gated else g.d_w1
     db = torch.cat([g.d_b, g.d_c]) if layer.is_gated else g.d_b
     errs = {k: normwise_rel(_f64(v), r) for k, v, r in (
