@@ -559,24 +559,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // the two warps of a lane quarter take alternate chunks; the one starting flips per tile
         const int first = cw ^ par;
         if constexpr (kPre) prefetch(first);
+        // TMEM loads run one chunk ahead: chunk cc + 2's tcgen05.ld is issued right after chunk
+        // cc's data arrived, so its latency hides behind chunk cc's math and stores (the wait at
+        // the top of the next iteration then finds it complete)
+        uint32_t r[32];
+        auto tmem_chunk = [&](int cc) {
+          const uint32_t ta =
+              tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + slab * kBN + 32 * cc;
+          tmem_ld16x256b_x4(ta, r);
+          tmem_ld16x256b_x4(ta + (16u << 16), r + 16);
+        };
+        if (first < kBN / 32) tmem_chunk(first);
 #pragma unroll 1
         for (int cc = first; cc < kBN / 32; cc += 2) {
           uint4 cur[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) cur[u] = pre[u];
-          if constexpr (kPre) prefetch(cc + 2);
-          uint32_t r[32];
-          const uint32_t ta =
-              tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * C::ACC_COLS + slab * kBN + 32 * cc;
-          tmem_ld16x256b_x4(ta, r);
-          tmem_ld16x256b_x4(ta + (16u << 16), r + 16);
           tmem_ld_wait();
-          const int n0 = n_base + 32 * cc;
-          if (n0 >= shp.n) continue;
           // v[16 h + 4 c + 2 s + k]: row m_w + 16 h + 8 s + t4, token n0 + 8 c + 2 p + k
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if (cc + 2 < kBN / 32) tmem_chunk(cc + 2);
+          const int n0 = n_base + 32 * cc;
+          if (n0 >= shp.n) continue;
           if constexpr (kEpi == kEpiGatedGrad) {
             // h = 0: u rows, h = 1: the matching v rows of gate features fg + 8 s + t4
             const int fg = m_w >> 1;
@@ -692,6 +698,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
               }
             }
+            uint4 gaux[4];  // GELU'(z) units, stored after the TMA store is issued (see below)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               uint32_t gq[4] = {0u, 0u, 0u, 0u};
@@ -713,11 +720,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
                 pd[4 * c + j] = pack_bf16x2(x0, x1);
               }
-              if (kEpi == kEpiGeluGrad && !S24_EXP(128)) {
-                // GELU'(z) -> AUX unit (row m_w + 8 j + t4, this chunk)
-                aux_frag(ep.aux, (m_w >> 4) + (j >> 1), shp.n, n0)[32 * (j & 1) + lane] =
-                    make_uint4(gq[0], gq[1], gq[2], gq[3]);
-              }
+              gaux[j] = make_uint4(gq[0], gq[1], gq[2], gq[3]);
             }
             // [32 tokens][32 features], 64-byte rows, 64B swizzle, double-buffered; one stmatrix per c
             if S24_EXP(256) continue;
@@ -739,7 +742,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               bulk_commit();
             }
             sbuf ^= 1;
+            if (kEpi == kEpiGeluGrad && !S24_EXP(128)) {
+              // GELU'(z) -> AUX units (rows m_w + 8 j + t4, this chunk).  Issued after the proxy
+              // fence: the fence (MEMBAR + FENCE.VIEW.ASYNC) waits for every outstanding global
+              // access of the thread, so stores issued before it stalled each chunk ~1 round trip
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                aux_frag(ep.aux, (m_w >> 4) + (j >> 1), shp.n, n0)[32 * (j & 1) + lane] = gaux[j];
+            }
           }
+          // next-but-one chunk's AUX inputs, likewise issued after this chunk's fence
+          if constexpr (kPre) prefetch(cc + 2);
         }
         if constexpr (kEpi == kEpiDAct || kEpi == kEpiDGated) {
           // reduce the partials of the 4 threads sharing a row (lanes 4 t4 .. 4 t4 + 3)
