@@ -333,6 +333,19 @@ int s24_adam_step(void* w, void* u, void* v, int state_dtype, const void* g, int
                   double one_minus_beta2, double bias_corr1, double bias_corr2, double lambda_w, double lr_lambda,
                   int decay_mode, void* stream);
 
+/* The fp32 optimizer step of a 2:4 weight fused with the next step's per-step compression:
+ * s24_adam_step (state S24_F32, g fp32) on w, u, v in place, and the updated weight's kept
+ * values written into both orientations (fwd_vals rows x cols/2, bwd_vals cols x rows/2,
+ * either may be NULL) under the cached mask idx -- the same outputs as s24_prune_compress
+ * on the updated weight, so the next forward needs no K2 launch (trainer.py:438-447
+ * followed by gated_ffn.py:159-162).  idx and the outputs are in the operand's row order:
+ * perm_ff > 0 is the gated u/v interleave of s24_search_compress (w, u, v, g stay in [u; v]
+ * order).  The masked decay reads its mask from idx.  rows, cols % 128 == 0. */
+int s24_adam_compress(float* w, float* u, float* v, const float* g, int64_t rows, int64_t cols, const uint8_t* idx,
+                      double lr, double beta1, double beta2, double eps, double one_minus_beta1,
+                      double one_minus_beta2, double bias_corr1, double bias_corr2, double lambda_w, double lr_lambda,
+                      int decay_mode, uint16_t* fwd_vals, uint16_t* bwd_vals, int64_t perm_ff, void* stream);
+
 /* Mask flips of a refresh (flip_rate optim.py:94-102 = changed_bits / (rows cols); the
  * per-block counts of block_flip_stats optim.py:164-192): adds to *changed_bits (device
  * uint64, caller zeroes) the number of mask bits that differ between two pattern-index

@@ -59,6 +59,7 @@ SIGNATURES = {
     "s24_act_fwd_f32": [_P, _I64, _P, _I64, _I64, _I, _P, _I64, _P, _P, _P],
     "s24_act_bwd_f32": [_P, _I64, _P, _I64, _I64, _I64, _I, _P, _I64, _P, _P, _P, _P],
     "s24_adam_step": [_P, _P, _P, _I, _P, _I, _I64, _I64, _P] + [ctypes.c_double] * 10 + [_I, _P],
+    "s24_adam_compress": [_P, _P, _P, _P, _I64, _I64, _P] + [ctypes.c_double] * 10 + [_I, _P, _P, _I64, _P],
     "s24_mask_flips": [_P, _P, _I64, _P, _P, _P],
     "s24_greedy_search": [_P, _I, _I64, _I64, _P, _P, _P],
     "s24_prune_compress_pair": [_P, _P, _I, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _I64, _P],

@@ -25,6 +25,7 @@
 #include "s24_common.cuh"
 #include "s24_patterns.h"
 #include "s24_search_tree.h"
+#include "s24_adam.cuh"
 
 namespace s24 {
 
@@ -354,6 +355,123 @@ __global__ void __launch_bounds__(kThreads, 2) mask_tile_kernel(MaskArgs p) {
         *reinterpret_cast<uint32_t*>(p.bwd_vals + grow_t * (p.rows / 2) + kcol) = val;
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K9+K2 fused: the fp32 optimizer step (Adam + masked decay, optim.py:105-147) of a sparse
+// weight with the NEXT step's per-step prune / compress (gated_ffn.py:159-162) in the same
+// pass: each thread updates 4 rows x 16 columns (w, u, v in place, 16-byte streaming
+// accesses) and compresses the updated values into both orientations exactly as
+// mask_tile_kernel does with a cached mask (the E tiles only change at a refresh).  The
+// step's K2 launch then disappears from the forward.  Mask / compressed outputs follow the
+// operand's row order (perm_ff: the gated u/v interleave); w, u, v, g stay in [u; v] order.
+struct AdamCompressArgs {
+  float* w;
+  float* u;
+  float* v;
+  const float* g;
+  int64_t rows, cols;
+  const uint8_t* idx;  // operand order
+  uint16_t* fwd_vals;
+  uint16_t* bwd_vals;
+  int64_t perm_ff;
+  AdamScalars s;
+};
+
+__global__ void __launch_bounds__(kThreads, 2) adam_compress_kernel(AdamCompressArgs p) {
+  __shared__ __align__(16) uint32_t s_bv[128 * 32];  // bwd kept values, 128 x 64 bf16 (swizzled)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tr = blockIdx.y, tc = blockIdx.x;
+  const int br = 4 * warp + (lane >> 3);
+  const int c0 = 16 * (lane & 7);
+  const int64_t grow0 = tr * kTile + 4 * br;  // operand row
+  const int64_t gcol0 = tc * kTile + c0;
+  const bool ok = grow0 < p.rows && gcol0 < p.cols;  // rows, cols % 128 == 0 (host check)
+  int pat[4] = {0, 0, 0, 0};
+  if (ok) {
+    const uint32_t word = *reinterpret_cast<const uint32_t*>(p.idx + (grow0 / 4) * (p.cols / 4) + gcol0 / 4);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int t = (word >> (8 * b)) & 0xFF;
+      pat[b] = t > 89 ? 0 : t;
+    }
+  }
+  float val[4][16];
+  const int64_t in_row0 = p.perm_ff > 0 ? gate_row(grow0, p.perm_ff) : grow0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (!ok) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) val[i][4 * b + j] = 0.0f;
+        continue;
+      }
+      const int64_t e = (in_row0 + i) * p.cols + gcol0 + 4 * b;
+      const float4 w4 = __ldcs(reinterpret_cast<const float4*>(p.w + e));
+      const float4 g4 = __ldcs(reinterpret_cast<const float4*>(p.g + e));
+      const float4 u4 = __ldcs(reinterpret_cast<const float4*>(p.u + e));
+      const float4 v4 = __ldcs(reinterpret_cast<const float4*>(p.v + e));
+      float wv[4] = {w4.x, w4.y, w4.z, w4.w}, gv[4] = {g4.x, g4.y, g4.z, g4.w};
+      float uv[4] = {u4.x, u4.y, u4.z, u4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+      const uint32_t keep = (c_pat_bits[pat[b]] >> (4 * i)) & 0xFu;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) adam_elem<float>(wv[j], uv[j], vv[j], gv[j], !((keep >> j) & 1), p.s);
+      __stcs(reinterpret_cast<float4*>(p.w + e), make_float4(wv[0], wv[1], wv[2], wv[3]));
+      __stcs(reinterpret_cast<float4*>(p.u + e), make_float4(uv[0], uv[1], uv[2], uv[3]));
+      __stcs(reinterpret_cast<float4*>(p.v + e), make_float4(vv[0], vv[1], vv[2], vv[3]));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) val[i][4 * b + j] = wv[j];
+    }
+  }
+  // fwd orientation: kept values along rows
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t packed[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t nib = nib_of_mask((c_pat_bits[pat[b]] >> (4 * i)) & 0xFu);
+      const int i0 = nib & 3, i1 = nib >> 2;
+      uint16_t lo = 0, hi = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint16_t bits = f32_to_bf16(val[i][4 * b + j]);
+        lo = (j == i0) ? bits : lo;
+        hi = (j == i1) ? bits : hi;
+      }
+      packed[b] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+    }
+    if (ok && p.fwd_vals != nullptr)
+      *reinterpret_cast<uint4*>(p.fwd_vals + (grow0 + i) * (p.cols / 2) + gcol0 / 2) =
+          make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  }
+  if (p.bwd_vals == nullptr) return;
+  // bwd orientation (W^T): kept values along columns, transposed through shared memory
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const uint32_t bits16 = c_pat_bits[pat[b]];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t nib = nib_of_mask(col_mask(bits16, j));
+      const int i0 = nib & 3, i1 = nib >> 2;
+      uint16_t lo = 0, hi = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint16_t bits = f32_to_bf16(val[i][4 * b + j]);
+        lo = (i == i0) ? bits : lo;
+        hi = (i == i1) ? bits : hi;
+      }
+      const int mp = c0 + 4 * b + j;
+      s_bv[mp * 32 + ((br + 4 * (mp >> 4)) & 31)] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+    }
+  }
+  __syncthreads();
+  const int64_t kcol = tr * (kTile / 2) + 2 * lane;
+  for (int rr = warp; rr < kTile; rr += kThreads / 32) {
+    const int64_t grow_t = tc * kTile + rr;
+    *reinterpret_cast<uint32_t*>(p.bwd_vals + grow_t * (p.rows / 2) + kcol) =
+        s_bv[rr * 32 + ((lane + 4 * (rr >> 4)) & 31)];
   }
 }
 
@@ -944,4 +1062,26 @@ extern "C" int s24_masked_decay_bits(float* g, const void* w, int w_dtype, const
   masked_decay_bits_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(g, w, w_dtype, bits, n,
                                                                                             lambda_w);
   return s24_check_launch("masked_decay_bits");
+}
+
+extern "C" int s24_adam_compress(float* w, float* u, float* v, const float* g, int64_t rows, int64_t cols,
+                                 const uint8_t* idx, double lr, double beta1, double beta2, double eps,
+                                 double one_minus_beta1, double one_minus_beta2, double bias_corr1, double bias_corr2,
+                                 double lambda_w, double lr_lambda, int decay_mode, uint16_t* fwd_vals,
+                                 uint16_t* bwd_vals, int64_t perm_ff, void* stream) {
+  S24_REQUIRE(w && u && v && g && idx, S24_ERR_ARG, "NULL operand");
+  S24_REQUIRE(rows % 128 == 0 && cols % 128 == 0 && rows > 0 && cols > 0, S24_ERR_SHAPE,
+              "the fused optimizer + compression needs rows, cols %% 128 == 0 (got %lld, %lld)", (long long)rows,
+              (long long)cols);
+  S24_REQUIRE(decay_mode >= S24_DECAY_NONE && decay_mode <= S24_DECAY_ON_WEIGHTS, S24_ERR_ARG, "bad decay mode");
+  S24_REQUIRE(((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v) |
+                reinterpret_cast<uintptr_t>(g)) & 15) == 0,
+              S24_ERR_UNSUPPORTED, "w, u, v, g need 16-byte aligned base addresses");
+  if (int rc = check_perm(rows, perm_ff)) return rc;
+  AdamCompressArgs a{w, u, v, g, rows, cols, idx, fwd_vals, bwd_vals, perm_ff,
+                     AdamScalars{lr, beta1, beta2, eps, one_minus_beta1, one_minus_beta2, bias_corr1, bias_corr2,
+                                 lambda_w, lr_lambda, decay_mode}};
+  const dim3 grid(static_cast<unsigned>(cols / kTile), static_cast<unsigned>(rows / kTile));
+  adam_compress_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return s24_check_launch("adam_compress");
 }

@@ -93,6 +93,8 @@ class SparseFFN(torch.nn.Module):
         self.mask_searches = 0
         self.mask_version = 0  # bumped by every refresh (K1)
         self._seen_version = None  # parameter versions the operands were built from
+        self._dirty_steps = 0  # declared optimizer steps not yet seen by a forward
+        self._fresh = False  # the last declared step left the operands current (fused compression)
         self._dense_cache = None  # (versions, DenseOperand pair) of the dense phase
         self._bucket = None
         # MVUE-sparsified weight gradients (fst_backward(mvue=True), gated_ffn.py:304-373): the
@@ -114,16 +116,21 @@ class SparseFFN(torch.nn.Module):
     def _versions(self):
         return (self.w_in._version, self.w2._version)
 
-    def mark_weights_updated(self) -> None:
+    def mark_weights_updated(self, compressed: bool = False) -> None:
         """Declare an optimizer step that bypassed the in-place version counters (e.g. writes
-        through `.data`): the next forward recompresses and advances the refresh schedule."""
-        self._seen_version = None
+        through `.data`): the next forward advances the refresh schedule and recompresses --
+        unless `compressed`, i.e. the step ran the fused optimizer + compression
+        (optim.adam_step(compress_into=op_in / op_out)), which already left the current kept
+        values in both operands (no K2 launch)."""
+        self._dirty_steps += 1
+        self._fresh = compressed
         self._dense_cache = None
 
     def refresh_masks(self) -> None:
         """K1: new transposable masks + both compressed orientations."""
         E.search_compress_pair(self.w_in.detach(), self.op_in, self.w2.detach(), self.op_out)
         self.steps_since_refresh = 0
+        self._dirty_steps, self._fresh = 0, False
         self.mask_searches += 2
         self.mask_version += 1
         self._seen_version = self._versions()
@@ -133,13 +140,18 @@ class SparseFFN(torch.nn.Module):
         if self.steps_since_refresh is None:
             self.refresh_masks()
             return
-        if v == self._seen_version:
-            return  # same optimizer step: operands are current
-        self.steps_since_refresh += 1  # one optimizer step since the operands were built
+        # optimizer steps since the operands were built: declared ones, or one detected through
+        # the parameters' version counters (an in-place torch optimizer step)
+        steps = self._dirty_steps or (1 if v != self._seen_version else 0)
+        if steps == 0:
+            return  # same optimizer step (gradient accumulation, recompute): operands are current
+        fresh, self._dirty_steps, self._fresh = self._fresh, 0, False
+        self.steps_since_refresh += steps
         if self.steps_since_refresh >= self.refresh_period:
             self.refresh_masks()
         else:
-            E.compress_values_pair(self.w_in.detach(), self.op_in, self.w2.detach(), self.op_out)
+            if not fresh:
+                E.compress_values_pair(self.w_in.detach(), self.op_in, self.w2.detach(), self.op_out)
             self._seen_version = v
 
     def _dense_ops(self):
@@ -150,6 +162,11 @@ class SparseFFN(torch.nn.Module):
             ff = self.w2.shape[1] if self.act in E.GATED else 0
             self._dense_cache = (v, (E.DenseOperand.of(w_in, ff), E.DenseOperand.of(w2)))
         return self._dense_cache[1]
+
+    def next_forward_refreshes(self) -> bool:
+        """Whether the next sparse forward searches new masks (after one more optimizer step)."""
+        return self.steps_since_refresh is None or self.steps_since_refresh + self._dirty_steps + 1 \
+            >= self.refresh_period
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         if not self.sparse:

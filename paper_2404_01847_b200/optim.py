@@ -97,13 +97,20 @@ _DECAY_CODE = {DecayMode.NONE: 0, DecayMode.ON_GRADIENTS: 1, DecayMode.ON_WEIGHT
 
 
 def adam_step(state: OptimizerState, g: torch.Tensor, mask: TransposableMask | None = None,
-              decay: DecayConfig | None = None) -> OptimizerState:
+              decay: DecayConfig | None = None, compress_into=None) -> OptimizerState:
     """One Adam update in place (optim.py:128-147), fused with the masked decay of the
     training loop when `decay` asks for it (trainer.py:438-447): ON_GRADIENTS adds
     lambda_w (1 - m) w to g first (masked_decay_gradient, optim.py:105-114), ON_WEIGHTS
     subtracts lr lambda_w (1 - m) w_before after the step (srste_weight_decay,
-    optim.py:117-125).  One HBM pass over w, g, u, v (s24_adam_step)."""
+    optim.py:117-125).  One HBM pass over w, g, u, v (s24_adam_step).
+
+    compress_into (an engine.CompressedOperand of this weight, fp32 state): the same update
+    fused with the next forward's per-step compression (s24_adam_compress) -- the updated
+    weight's kept values land in both orientations of the operand under its cached mask, which
+    also supplies the decay mask, so the next step needs no K2 launch."""
     C.require_cuda(state.w, state.u, state.v, g)
+    if compress_into is not None:
+        return _adam_compress(state, g, decay, compress_into)
     if tuple(g.shape) != tuple(state.w.shape):
         raise ShapeError("gradient shape differs from weights")
     mode = decay.mode if (decay is not None and decay.lambda_w > 0) else DecayMode.NONE
@@ -127,6 +134,26 @@ def adam_step(state: OptimizerState, g: torch.Tensor, mask: TransposableMask | N
            state.lr, state.beta1, state.beta2, state.eps, 1.0 - state.beta1, 1.0 - state.beta2,
            1.0 - state.beta1 ** t, 1.0 - state.beta2 ** t, lam, state.lr * lam, _DECAY_CODE[mode],
            C.stream_of(state.w))
+    return state
+
+
+def _adam_compress(state: OptimizerState, g: torch.Tensor, decay: DecayConfig | None, op) -> OptimizerState:
+    if state.w.dtype != torch.float32 or state.w.dim() != 2 or tuple(state.w.shape) != (op.rows, op.cols):
+        raise ShapeError("the fused optimizer + compression takes the fp32 2-D weight of its operand")
+    for t_ in (state.w, state.u, state.v):
+        if not t_.is_contiguous() or t_.dtype != torch.float32:
+            raise ValueError("w, u, v must be contiguous fp32 tensors")
+    g = g.contiguous()
+    if g.dtype != torch.float32 or tuple(g.shape) != tuple(state.w.shape):
+        raise ShapeError("the fused path takes an fp32 gradient of the weight's shape")
+    mode = decay.mode if (decay is not None and decay.lambda_w > 0) else DecayMode.NONE
+    lam = decay.lambda_w if mode is not DecayMode.NONE else 0.0
+    state.t += 1
+    t = state.t
+    C.call("s24_adam_compress", state.w.data_ptr(), state.u.data_ptr(), state.v.data_ptr(), g.data_ptr(), op.rows,
+           op.cols, op.idx.data_ptr(), state.lr, state.beta1, state.beta2, state.eps, 1.0 - state.beta1,
+           1.0 - state.beta2, 1.0 - state.beta1 ** t, 1.0 - state.beta2 ** t, lam, state.lr * lam, _DECAY_CODE[mode],
+           op.fwd_vals.data_ptr(), op.bwd_vals.data_ptr(), op.perm_ff, C.stream_of(state.w))
     return state
 
 

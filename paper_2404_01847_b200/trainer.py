@@ -379,12 +379,21 @@ def run_training(cfg: TrainConfig, device="cuda") -> RunArtifacts:
         losses[t - 1] = loss.detach()
         mode = cfg.decay.mode if (sparse_now and lam > 0 and cfg.decay.mode is DecayMode.ON_WEIGHTS) else None
         masks = dict((id(w), m) for w, m in stack.masks()) if mode is not None else {}
+        # when the next step is sparse and keeps its masks, the sparse weights' Adam updates also
+        # write the next forward's compressed operands (s24_adam_compress): no K2 launch there
+        fuse = (sparse_now and cfg.sparse and t_pre < t + 1 <= t_switch
+                and since_refresh + 1 < cfg.decay.refresh_period)
+        ops = {}
+        if fuse:
+            for layer in stack.layers:
+                ops[id(layer.w_in)], ops[id(layer.w2)] = layer.op_in, layer.op_out
         for st, p in zip(states, stack.parameters()):
             st.lr = lr
             m = masks.get(id(p))
-            adam_step(st, p.grad, m, DecayConfig(lambda_w=lam, mode=DecayMode.ON_WEIGHTS) if m is not None else None)
+            dec = DecayConfig(lambda_w=lam, mode=DecayMode.ON_WEIGHTS) if m is not None else None
+            adam_step(st, p.grad, m, dec, compress_into=ops.get(id(p)))
         for layer in stack.layers:
-            layer.mark_weights_updated()  # adam_step writes p.data: an optimizer step the version counters miss
+            layer.mark_weights_updated(compressed=fuse)  # adam_step writes p.data: version counters miss it
         since_refresh += 1
         if proxy is not None:
             pm = _proxy_masks(stack)

@@ -79,3 +79,38 @@ def test_flip_rate_and_block_flips_bit_exact():
     mask_flips(ma, mb, blk)  # accumulates
     assert int(n) == int(round(float(GD["flip.rate"]) * GD["flip.wa"].size))
     assert np.array_equal(blk.cpu().numpy(), 2 * GD["flip.block_flips"])
+
+
+@pytest.mark.parametrize("mode", ["none", "on_gradients", "on_weights"])
+@pytest.mark.parametrize("gated", [False, True])
+def test_adam_fused_with_next_step_compression_bit_exact(mode, gated):
+    """s24_adam_compress (the fp32 optimizer step fused with the next forward's prune/compress)
+    equals s24_adam_step followed by K2 on the updated weight, bit for bit: w, u, v and the kept
+    values of both orientations (gated: the u/v-interleaved operand of W_in)."""
+    import paper_2404_01847_b200 as P
+    from paper_2404_01847_b200 import engine as E
+    from paper_2404_01847_b200.optim import DecayConfig, DecayMode, OptimizerState, adam_step
+
+    rows, cols = (768, 256) if gated else (512, 384)
+    ff = rows // 2 if gated else 0
+    g0 = torch.Generator(device="cuda").manual_seed(rows + cols + len(mode))
+    w = torch.randn(rows, cols, generator=g0, device="cuda") * 0.05
+    op_a = E.CompressedOperand.empty(rows, cols, "cuda", perm_ff=ff)
+    E.search_compress(w, op_a)
+    op_b = E.CompressedOperand.empty(rows, cols, "cuda", perm_ff=ff)
+    op_b.idx.copy_(op_a.idx)
+    mask = P.TransposableMask(op_a.mask_idx(), (rows, cols))
+    cfg = DecayConfig(lambda_w=0.02, mode={"none": DecayMode.NONE, "on_gradients": DecayMode.ON_GRADIENTS,
+                                           "on_weights": DecayMode.ON_WEIGHTS}[mode])
+    sa = OptimizerState.init(w, lr=3e-3, dtype=torch.float32)
+    sb = OptimizerState.init(w, lr=3e-3, dtype=torch.float32)
+    for t in range(3):
+        g = torch.randn(rows, cols, generator=g0, device="cuda")
+        adam_step(sa, g, mask, cfg)
+        E.compress_values(sa.w, op_a)
+        adam_step(sb, g, None, cfg, compress_into=op_b)
+        torch.cuda.synchronize()
+        for k in ("w", "u", "v"):
+            assert torch.equal(getattr(sa, k), getattr(sb, k)), (t, k)
+        assert torch.equal(op_a.fwd_vals.view(torch.int16), op_b.fwd_vals.view(torch.int16)), t
+        assert torch.equal(op_a.bwd_vals.view(torch.int16), op_b.bwd_vals.view(torch.int16)), t
