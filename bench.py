@@ -293,11 +293,11 @@ class SparseStep:
         # GEMMs, bwd 2 sparse + 2 dW GEMMs (+2 MVUE sparsifiers); activations fused into the GEMMs
         self.launches_per_step = 1 + 2 + 4 + (2 if mvue else 0)
 
-    def __call__(self, x, dy):
+    def __call__(self, x, dy, fused_optimizer=False):
         E = self.E
         if self.t % REFRESH == 0:
             E.search_compress_pair(self.w_in, self.op_in, self.w2, self.op_out)
-        else:
+        elif not fused_optimizer:  # else the previous step's fused optimizer left the operands current
             E.compress_values_pair(self.w_in, self.op_in, self.w2, self.op_out)
         st = E.ffn_forward(x, self.op_in, self.bias, self.op_out, self.act, fused=True)
         work = []
@@ -600,6 +600,12 @@ def measure(a, cfg, cfg_name, dev, world, rank, local, pg, dist, full=True):
                                  "frac_of_hbm": opt_bytes / (opt_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}
         del ost
 
+        # ---- training step incl. the optimizer: the 2:4 step whose operands come from the fused
+        # Adam + next-step compression (s24_adam_compress, no K2 in the step) against the dense
+        # step + Adam with the bf16 cast of its fp32 master weights (the dense counterpart of the
+        # compression); fp32 master weights and moments on both sides ----
+        out["training_step"] = training_step_compare(step, w_in, bias, w2, x, dy, cfg, world, dd)
+
         # ---- standalone activation kernels (K6/K7: the API's unfused path) ----
         r_act, r_in_act = w2.shape[1], w_in.shape[0]
         zc = torch.randn(n_tok, r_in_act, device=dev).to(torch.bfloat16)
@@ -648,6 +654,66 @@ def measure(a, cfg, cfg_name, dev, world, rank, local, pg, dist, full=True):
     del step, w_in, bias, w2, x, dy
     torch.cuda.empty_cache()
     return out
+
+
+def training_step_compare(step, w_in, bias, w2, x, dy, cfg, world, dist):
+    import torch
+    from paper_2404_01847_b200.optim import DecayConfig, DecayMode, OptimizerState, adam_step
+
+    n_tok = cfg["tokens"]
+    sw_in = OptimizerState.init(w_in.float(), dtype=torch.float32)
+    sw2 = OptimizerState.init(w2.float(), dtype=torch.float32)
+    sb = OptimizerState.init(bias.float(), dtype=torch.float32)
+    nodecay = DecayConfig(lambda_w=0.0, mode=DecayMode.NONE)  # the decay is fused in the dW epilogue
+
+    def sparse():
+        step.t = max(step.t, 1)
+        if step.t % REFRESH == 0:
+            step.t += 1  # refreshes are amortised in the headline; this loop times the steady state
+        step(x, dy, fused_optimizer=True)
+        adam_step(sw_in, step.dw_in, None, nodecay, compress_into=step.op_in)
+        adam_step(sw2, step.dw2, None, nodecay, compress_into=step.op_out)
+        adam_step(sb, step.dbias)
+
+    fstep = DenseFusedStep(w_in.clone(), bias, w2.clone(), cfg["act"])  # its own bf16 copies, updated in place
+
+    def dense_fused():
+        g = fstep(x, dy)
+        adam_step(sw_in, g.dw_in)
+        adam_step(sw2, g.dw2)
+        adam_step(sb, g.dbias_in)
+        fstep.op_in.w.copy_(sw_in.w)  # bf16 copies of the fp32 masters for the next step's GEMMs
+        fstep.op_out.w.copy_(sw2.w)
+
+    import torch.nn.functional as F
+
+    W1, B1, W2 = (t.clone().requires_grad_(True) for t in (w_in, bias, w2))
+    d_ff = w2.shape[1]
+    act = {"gelu": F.gelu, "relu": F.relu, "swiglu": lambda z: F.silu(z[:, :d_ff]) * z[:, d_ff:],
+           "geglu": lambda z: F.gelu(z[:, :d_ff]) * z[:, d_ff:]}[cfg["act"]]
+
+    def dense_eager():
+        xg = x.detach().requires_grad_(True)
+        F.linear(act(F.linear(xg, W1, B1)), W2).backward(dy)
+        adam_step(sw_in, W1.grad.float())
+        adam_step(sw2, W2.grad.float())
+        adam_step(sb, B1.grad.float())
+        W1.grad = B1.grad = W2.grad = None
+        with torch.no_grad():
+            W1.copy_(sw_in.w)
+            W2.copy_(sw2.w)
+
+    steps = 10
+    sms, _ = time_loop(sparse, steps, 3, dist)
+    fms, _ = time_loop(dense_fused, steps, 3, dist)
+    ems, _ = time_loop(dense_eager, steps, 3, dist)
+    tps = lambda ms: n_tok * world / (ms / steps / 1e3)  # noqa: E731
+    sp, dn = tps(sms), max(tps(fms), tps(ems))
+    return {"sparse_tokens_per_s": sp, "dense_fused_tokens_per_s": tps(fms), "dense_eager_tokens_per_s": tps(ems),
+            "speedup_vs_best_dense": sp / dn,
+            "what": "fwd + bwd + fp32 Adam on W_in, bias, W2; 2:4: operands from the fused Adam + compression "
+                    "(no K2 launch); dense: the fused dense kernels, or eager cuBLAS autograd, + Adam + bf16 cast "
+                    "of the fp32 masters"}
 
 
 def run_ours(a, cfg, cfg_name, subs):
@@ -705,6 +771,7 @@ def run_ours(a, cfg, cfg_name, subs):
             "roofline": res["roofline"], "e2e": res["e2e"], "gpu_launches": res["gpu_launches"],
             "clocks": res["clocks"], "cpu_baseline": cpu,
             "sub_lines": sub_res or None,
+            "training_step": res.get("training_step"),
         }
         # the dense comparisons last, so a truncated tail of the line still carries them
         for k in ("dense_tokens_per_s", "dense_fused_tokens_per_s", "dense_gemm_only_tokens_per_s",
