@@ -611,29 +611,73 @@ __device__ __forceinline__ int search_block_bf16w(const uint32_t (&wd)[8]) {
   return s24_search_tree(rp);
 }
 
-// p0's tiles are blocks [0, tiles0), p1's the rest (K1 of a block's two weights in one launch)
-__global__ void __launch_bounds__(kPruneThreads, 2) search_bf16_kernel(MaskArgs p0, MaskArgs p1, int tiles0) {
-  __shared__ uint32_t s_bv[128 * 32];
-  __shared__ __align__(16) uint32_t s_fe[512];
-  __shared__ __align__(16) uint32_t s_be[512];
-  __shared__ uint4 s_sel[90];
-  __shared__ uint32_t s_nib[90];  // fwd row nibbles (bits 0-15) | bwd column nibbles (bits 16-31)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool second = static_cast<int>(blockIdx.x) >= tiles0;
-  const MaskArgs p = second ? p1 : p0;  // fields copied to registers once
-  const int64_t bid = second ? blockIdx.x - tiles0 : blockIdx.x;
-  const int64_t tiles_x = p.cols / kTile;
-  const int64_t tr = bid / tiles_x, tc = bid - tr * tiles_x;
-  const int br = 2 * warp + (lane >> 4);
-  const int c0 = 8 * (lane & 15);
-  const int64_t grow0 = tr * kTile + 4 * br, gcol0 = tc * kTile + c0;
-  const int64_t in_row0 = p.perm_ff > 0 ? gate_row(grow0, p.perm_ff) : grow0;
-  const uint16_t* w = static_cast<const uint16_t*>(p.w);
-  uint4 v[4];
+// Persistent K1: one CTA per (SM, slot), each walking tiles g = blockIdx.x, + gridDim.x, ...
+// over p0's tiles [0, tiles0) then p1's.  Every thread streams the 4 x 16 bytes it will search
+// for its NEXT tile into its own shared-memory slot with cp.async while it searches the current
+// one, so HBM reads run under the integer search instead of behind it (the one-tile-per-CTA
+// version left the load latency exposed at every tile: 64 % issue activity); the slots are
+// thread-private, so the input pipeline needs no barrier.  The transposed-value and E-tile
+// staging is double-buffered: one __syncthreads per tile.  Every byte of both E tiles is
+// written by exactly one thread, so the staging needs no clearing.
+struct K1Smem {
+  uint4 in[2][4][kPruneThreads];  // 64 KB: slot (buffer, row i, thread)
+  uint32_t bv[2][128 * 32];       // 32 KB: W^T tile, 128 rows x 32 words (64 kept bf16)
+  uint32_t fe[2][512];            // fwd E tile (2048 B)
+  uint32_t be[2][512];            // bwd E tile
+  uint4 sel[90];                  // per pattern: row selectors (x, y), column selectors (z, w)
+  uint32_t nib[90];               // fwd row nibbles (bits 0-15) | bwd column nibbles (bits 16-31)
+};
+constexpr int kK1SmemBytes = static_cast<int>(sizeof(K1Smem));
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+struct K1Tile {
+  int which;       // 0: p0, 1: p1, -1: none
+  int64_t tr, tc;  // tile row / col of that weight
+};
+
+__device__ __forceinline__ K1Tile k1_tile(int g, int tiles0, int total, const MaskArgs& p0, const MaskArgs& p1) {
+  K1Tile t{-1, 0, 0};
+  if (g >= total) return t;
+  const bool second = g >= tiles0;
+  const int b = second ? g - tiles0 : g;
+  const int tiles_x = static_cast<int>((second ? p1.cols : p0.cols) / kTile);
+  const int r = b / tiles_x;
+  t.which = second ? 1 : 0;
+  t.tr = r;
+  t.tc = b - r * tiles_x;
+  return t;
+}
+
+__global__ void __launch_bounds__(kPruneThreads, 2) search_bf16_kernel(MaskArgs p0, MaskArgs p1, int tiles0,
+                                                                        int total) {
+  extern __shared__ __align__(16) uint8_t k1_raw[];
+  K1Smem& S = *reinterpret_cast<K1Smem*>(k1_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int br = 2 * warp + (lane >> 4);  // block row in the tile, 0..31
+  const int c0 = 8 * (lane & 15);         // first column in the tile, 0..120
+
+  auto prefetch = [&](const K1Tile& t, int buf) {
+    if (t.which >= 0) {
+      const MaskArgs& q = t.which ? p1 : p0;
+      const int64_t grow0 = t.tr * kTile + 4 * br;
+      const int64_t in_row0 = q.perm_ff > 0 ? gate_row(grow0, q.perm_ff) : grow0;
+      const uint16_t* src = static_cast<const uint16_t*>(q.w) + in_row0 * q.cols + t.tc * kTile + c0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const uint4*>(w + (in_row0 + i) * p.cols + gcol0));
-  if (threadIdx.x < 90) {
-    const uint32_t bits16 = c_pat_bits[threadIdx.x];
+      for (int i = 0; i < 4; ++i) cp_async16(&S.in[buf][i][tid], src + i * q.cols);
+    }
+    cp_async_commit();  // (possibly empty) group: wait_group 1 below always means "the previous tile"
+  };
+
+  int g = blockIdx.x;
+  K1Tile cur = k1_tile(g, tiles0, total, p0, p1);
+  prefetch(cur, 0);
+  if (tid < 90) {
+    const uint32_t bits16 = c_pat_bits[tid];
     uint32_t r[4], c[4], nf = 0, nb = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -643,103 +687,129 @@ __global__ void __launch_bounds__(kPruneThreads, 2) search_bf16_kernel(MaskArgs 
       nf |= rn << (4 * k);
       nb |= cn << (4 * k);
     }
-    s_sel[threadIdx.x] = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), c[0] | (c[1] << 16), c[2] | (c[3] << 16));
-    s_nib[threadIdx.x] = nf | (nb << 16);
+    S.sel[tid] = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+    S.nib[tid] = nf | (nb << 16);
   }
-  for (int i = threadIdx.x; i < 512; i += kPruneThreads) {
-    s_fe[i] = 0;
-    s_be[i] = 0;
-  }
-  int pat[2];
-#pragma unroll
-  for (int b = 0; b < 2; ++b) {
-    uint32_t wd[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      wd[2 * i] = (&v[i].x)[2 * b];
-      wd[2 * i + 1] = (&v[i].x)[2 * b + 1];
-    }
-    pat[b] = search_block_bf16w(wd);
-  }
-  *reinterpret_cast<uint16_t*>(p.idx_out + (grow0 / 4) * (p.cols / 4) + gcol0 / 4) =
-      static_cast<uint16_t>(pat[0] | (pat[1] << 8));
   __syncthreads();  // tables ready
-  const uint32_t n0 = s_nib[pat[0]], n1 = s_nib[pat[1]];
-  // fwd E: row m = 4 br + i holds groups c0/4, c0/4 + 1 -> one byte of its halfword
-  if (p.fwd_e) {
-    uint8_t* fe = reinterpret_cast<uint8_t*>(s_fe);
+
+  for (int buf = 0; cur.which >= 0; buf ^= 1) {
+    const K1Tile nxt = k1_tile(g + gridDim.x, tiles0, total, p0, p1);
+    prefetch(nxt, buf ^ 1);
+    cp_async_wait1();  // this thread's slot of the current tile has landed
+    const MaskArgs& p = cur.which ? p1 : p0;
+    const int64_t tr = cur.tr, tc = cur.tc;
+    const int64_t grow0 = tr * kTile + 4 * br, gcol0 = tc * kTile + c0;
+    uint4 v[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int m = 4 * br + i;
-      const int L = (m & 7) + 8 * ((c0 & 31) >> 4) + 16 * (m >> 4);
-      const int c = c0 >> 5, h = (m >> 3) & 1;
-      fe[2 * (L * 8 + c * 2 + h) + ((c0 >> 3) & 1)] =
-          static_cast<uint8_t>(((n0 >> (4 * i)) & 0xFu) | (((n1 >> (4 * i)) & 0xFu) << 4));
+    for (int i = 0; i < 4; ++i) v[i] = S.in[buf][i][tid];
+
+    int pat[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      uint32_t wd[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        wd[2 * i] = (&v[i].x)[2 * b];
+        wd[2 * i + 1] = (&v[i].x)[2 * b + 1];
+      }
+      pat[b] = search_block_bf16w(wd);
     }
-  }
-  // bwd E: W^T row mp = c0 + 4b + j, group br; block rows 2w (lane < 16) and 2w + 1
-  // (lane + 16) share one byte -> exchange the eight column nibbles once
-  if (p.bwd_e) {
-    const uint32_t mine = (n0 >> 16) | (n1 & 0xFFFF0000u);  // nibble 4b + j
-    const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, 16);
-    const uint32_t lo = lane < 16 ? mine : other, hi = lane < 16 ? other : mine;
-    uint8_t* be = reinterpret_cast<uint8_t*>(s_be);
-    const int brp = br & ~1;  // even block row of the pair
-    const int c = brp >> 3, byte_in_half = (brp >> 1) & 1;
+    *reinterpret_cast<uint16_t*>(p.idx_out + (grow0 / 4) * (p.cols / 4) + gcol0 / 4) =
+        static_cast<uint16_t>(pat[0] | (pat[1] << 8));
+    const uint32_t n0 = S.nib[pat[0]], n1 = S.nib[pat[1]];
+    // fwd E: row m = 4 br + i holds groups c0/4, c0/4 + 1 -> one byte of its halfword
+    if (p.fwd_e) {
+      uint8_t* fe = reinterpret_cast<uint8_t*>(S.fe[buf]);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = 4 * (lane >> 4) + q;  // lanes < 16: columns 0-3, lanes >= 16: columns 4-7
-      const int mp = c0 + k;
-      const int L = (mp & 7) + 16 * (mp >> 4) + 8 * ((brp >> 2) & 1);
-      const int h = (mp >> 3) & 1;
-      be[4 * (L * 4 + c) + 2 * h + byte_in_half] =
-          static_cast<uint8_t>(((lo >> (4 * k)) & 0xFu) | (((hi >> (4 * k)) & 0xFu) << 4));
-    }
-  }
-  uint32_t fw[4][2];
-#pragma unroll
-  for (int b = 0; b < 2; ++b) {
-    const uint4 sel = s_sel[pat[b]];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t si = ((i < 2 ? sel.x : sel.y) >> (16 * (i & 1))) & 0xFFFFu;
-      fw[i][b] = __byte_perm((&v[i].x)[2 * b], (&v[i].x)[2 * b + 1], si);
-    }
-    if (p.bwd_vals) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int wj = 2 * b + (j >> 1);
-        const uint32_t hsel = (j & 1) ? 0x7632u : 0x5410u;
-        const uint32_t col01 = __byte_perm((&v[0].x)[wj], (&v[1].x)[wj], hsel);
-        const uint32_t col23 = __byte_perm((&v[2].x)[wj], (&v[3].x)[wj], hsel);
-        const uint32_t sj = ((j < 2 ? sel.z : sel.w) >> (16 * (j & 1))) & 0xFFFFu;
-        const int mp = c0 + 4 * b + j;
-        s_bv[mp * 32 + ((br + 2 * (mp >> 3)) & 31)] = __byte_perm(col01, col23, sj);
+      for (int i = 0; i < 4; ++i) {
+        const int m = 4 * br + i;
+        const int L = (m & 7) + 8 * ((c0 & 31) >> 4) + 16 * (m >> 4);
+        const int c = c0 >> 5, h = (m >> 3) & 1;
+        fe[2 * (L * 8 + c * 2 + h) + ((c0 >> 3) & 1)] =
+            static_cast<uint8_t>(((n0 >> (4 * i)) & 0xFu) | (((n1 >> (4 * i)) & 0xFu) << 4));
       }
     }
-  }
-  if (p.fwd_vals) {
+    // bwd E: W^T row mp = c0 + 4b + j, group br; block rows 2w (lane < 16) and 2w + 1
+    // (lane + 16) share one byte -> exchange the eight column nibbles once
+    if (p.bwd_e) {
+      const uint32_t mine = (n0 >> 16) | (n1 & 0xFFFF0000u);  // nibble 4b + j
+      const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, 16);
+      const uint32_t lo = lane < 16 ? mine : other, hi = lane < 16 ? other : mine;
+      uint8_t* be = reinterpret_cast<uint8_t*>(S.be[buf]);
+      const int brp = br & ~1;  // even block row of the pair
+      const int c = brp >> 3, byte_in_half = (brp >> 1) & 1;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      *reinterpret_cast<uint2*>(p.fwd_vals + (grow0 + i) * (p.cols / 2) + gcol0 / 2) = make_uint2(fw[i][0], fw[i][1]);
-  }
-  __syncthreads();
-  if (p.fwd_e && threadIdx.x < 128) {
-    uint4* dst = reinterpret_cast<uint4*>(p.fwd_e + (tr * (p.cols / kTile) + tc) * 2048);
-    dst[threadIdx.x] = reinterpret_cast<const uint4*>(s_fe)[threadIdx.x];
-  }
-  if (p.bwd_e && threadIdx.x >= 128 && threadIdx.x < 256) {
-    uint4* dst = reinterpret_cast<uint4*>(p.bwd_e + (tc * (p.rows / kTile) + tr) * 2048);
-    dst[threadIdx.x - 128] = reinterpret_cast<const uint4*>(s_be)[threadIdx.x - 128];
-  }
-  if (p.bwd_vals) {
-    const int64_t kcol = tr * (kTile / 2) + 2 * lane;
-#pragma unroll 4
-    for (int rr = warp; rr < kTile; rr += kPruneThreads / 32) {
-      const uint32_t val = s_bv[rr * 32 + ((lane + 2 * (rr >> 3)) & 31)];
-      *reinterpret_cast<uint32_t*>(p.bwd_vals + (tc * kTile + rr) * (p.rows / 2) + kcol) = val;
+      for (int q = 0; q < 4; ++q) {
+        const int k = 4 * (lane >> 4) + q;  // lanes < 16: columns 0-3, lanes >= 16: columns 4-7
+        const int mp = c0 + k;
+        const int L = (mp & 7) + 16 * (mp >> 4) + 8 * ((brp >> 2) & 1);
+        const int h = (mp >> 3) & 1;
+        be[4 * (L * 4 + c) + 2 * h + byte_in_half] =
+            static_cast<uint8_t>(((lo >> (4 * k)) & 0xFu) | (((hi >> (4 * k)) & 0xFu) << 4));
+      }
     }
+    uint32_t fw[4][2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const uint4 sel = S.sel[pat[b]];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t si = ((i < 2 ? sel.x : sel.y) >> (16 * (i & 1))) & 0xFFFFu;
+        fw[i][b] = __byte_perm((&v[i].x)[2 * b], (&v[i].x)[2 * b + 1], si);
+      }
+      if (p.bwd_vals) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int wj = 2 * b + (j >> 1);
+          const uint32_t hsel = (j & 1) ? 0x7632u : 0x5410u;
+          const uint32_t col01 = __byte_perm((&v[0].x)[wj], (&v[1].x)[wj], hsel);
+          const uint32_t col23 = __byte_perm((&v[2].x)[wj], (&v[3].x)[wj], hsel);
+          const uint32_t sj = ((j < 2 ? sel.z : sel.w) >> (16 * (j & 1))) & 0xFFFFu;
+          const int mp = c0 + 4 * b + j;
+          S.bv[buf][mp * 32 + ((br + 2 * (mp >> 3)) & 31)] = __byte_perm(col01, col23, sj);
+        }
+      }
+    }
+    if (p.fwd_vals) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        *reinterpret_cast<uint2*>(p.fwd_vals + (grow0 + i) * (p.cols / 2) + gcol0 / 2) = make_uint2(fw[i][0], fw[i][1]);
+    }
+    __syncthreads();  // staging[buf] complete (and staging[buf ^ 1]'s copy-out of the previous tile done)
+    if (p.fwd_e && tid < 128) {
+      uint4* dst = reinterpret_cast<uint4*>(p.fwd_e + (tr * (p.cols / kTile) + tc) * 2048);
+      dst[tid] = reinterpret_cast<const uint4*>(S.fe[buf])[tid];
+    }
+    if (p.bwd_e && tid >= 128 && tid < 256) {
+      uint4* dst = reinterpret_cast<uint4*>(p.bwd_e + (tc * (p.rows / kTile) + tr) * 2048);
+      dst[tid - 128] = reinterpret_cast<const uint4*>(S.be[buf])[tid - 128];
+    }
+    if (p.bwd_vals) {
+      const int64_t kcol = tr * (kTile / 2) + 2 * lane;
+#pragma unroll 4
+      for (int rr = warp; rr < kTile; rr += kPruneThreads / 32) {
+        const uint32_t val = S.bv[buf][rr * 32 + ((lane + 2 * (rr >> 3)) & 31)];
+        *reinterpret_cast<uint32_t*>(p.bwd_vals + (tc * kTile + rr) * (p.rows / 2) + kcol) = val;
+      }
+    }
+    g += gridDim.x;
+    cur = nxt;
   }
+}
+
+// persistent grid: two CTAs per SM (the kernel's register and shared-memory footprint)
+static int k1_grid(int total) {
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (sms[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(search_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kK1SmemBytes);
+    sms[dev] = n > 0 ? n : 148;
+  }
+  return total < 2 * sms[dev] ? total : 2 * sms[dev];
 }
 
 // ---------------------------------------------------------------------------
@@ -880,7 +950,7 @@ static int launch_mask(const MaskArgs& a, int dtype, bool search, cudaStream_t s
   if (search) {
     if (dtype == S24_BF16 && aligned) {
       const int tiles = static_cast<int>(grid.x * grid.y);
-      search_bf16_kernel<<<tiles, kPruneThreads, 0, st>>>(a, a, tiles);
+      search_bf16_kernel<<<k1_grid(tiles), kPruneThreads, kK1SmemBytes, st>>>(a, a, tiles, tiles);
       return s24_check_launch("mask_search");
     }
     if (narrow) mask_tile_kernel<S24_BF16, true, true><<<grid, kThreads, 0, st>>>(a);
@@ -993,7 +1063,7 @@ extern "C" int s24_search_compress_pair(const void* w0, const void* w1, int dtyp
   }
   const int t0 = static_cast<int>((rows0 / kTile) * (cols0 / kTile)), t1 = static_cast<int>((rows1 / kTile) * (cols1 / kTile));
   if (t0 + t1 == 0) return S24_OK;
-  search_bf16_kernel<<<t0 + t1, kPruneThreads, 0, st>>>(a0, a1, t0);
+  search_bf16_kernel<<<k1_grid(t0 + t1), kPruneThreads, kK1SmemBytes, st>>>(a0, a1, t0, t0 + t1);
   return s24_check_launch("search_compress_pair");
 }
 
