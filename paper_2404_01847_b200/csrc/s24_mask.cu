@@ -564,9 +564,10 @@ __global__ void __launch_bounds__(kPruneThreads, 2) prune_bf16_kernel(MaskArgs p
 // thread); kept values via byte permutes, metadata nibbles from a per-pattern
 // table, E-tile bytes assembled without shared-memory atomics.
 
-// integer search on one block given as 4 rows x 2 words (bf16 pairs); falls back
-// to the float64 reference-order path for exponent spans > 13
-__device__ __forceinline__ int search_block_bf16w(const uint32_t (&wd)[8]) {
+// integer search on one block given as 4 rows x 2 words (bf16 pairs).  Returns the pattern, or
+// -1 when the block needs the float64 reference-order path (exponent span > 13, tiny values) and
+// -2 when it holds inf / nan (the owner lane then runs the sequential reference loop itself)
+__device__ __forceinline__ int search_block_fast(const uint32_t (&wd)[8]) {
   uint32_t h[16];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
@@ -585,14 +586,9 @@ __device__ __forceinline__ int search_block_bf16w(const uint32_t (&wd)[8]) {
   }
   if (bmax == 0) return 0;  // all-zero block: every score ties -> pattern 0
   const int emax = static_cast<int>(bmax >> 23), emin = static_cast<int>((bmin1 + 1u) >> 23);
-  // span > 13 (sums need > 24 bits), inf/nan, or tiny values (scale not representable):
-  // the float64 reference-order path
-  if (emax - emin > 13 || emax == 0xFF || emin < 8) {
-    double a[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) a[i] = static_cast<double>(f[i]);
-    return search_block_f64(a);
-  }
+  if (emax == 0xFF) return -2;
+  // span > 13 (sums need > 24 bits) or tiny values (scale not representable): float64 path
+  if (emax - emin > 13 || emin < 8) return -1;
   // |w| * 2^(134 - emin) is an integer < 2^21 (8-bit significand, span <= 13);
   // adding 1.5 * 2^23 puts it in the low mantissa bits exactly, and the integer
   // is pre-scaled by 128 for the tie-break bits: v = (bits - 0x4B400000) << 7
@@ -611,21 +607,80 @@ __device__ __forceinline__ int search_block_bf16w(const uint32_t (&wd)[8]) {
   return s24_search_tree(rp);
 }
 
-// Persistent K1: one CTA per (SM, slot), each walking tiles g = blockIdx.x, + gridDim.x, ...
-// over p0's tiles [0, tiles0) then p1's.  Every thread streams the 4 x 16 bytes it will search
-// for its NEXT tile into its own shared-memory slot with cp.async while it searches the current
-// one, so HBM reads run under the integer search instead of behind it (the one-tile-per-CTA
-// version left the load latency exposed at every tile: 64 % issue activity); the slots are
-// thread-private, so the input pipeline needs no barrier.  The transposed-value and E-tile
-// staging is double-buffered: one __syncthreads per tile.  Every byte of both E tiles is
-// written by exactly one thread, so the staging needs no clearing.
+__device__ __forceinline__ void block_abs_f64(const uint32_t (&wd)[8], double (&a)[16]) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      a[4 * r + k] = static_cast<double>(__uint_as_float(((wd[2 * r + (k >> 1)] >> (16 * (k & 1))) & 0x7FFFu) << 16));
+}
+
+__constant__ uint16_t c_pat_rows[90] = S24_PATTERN_ROWS;
+
+// The float64 reference-order search of one block with finite values, warp-cooperatively (the
+// north-star's warp-shuffle argmax): lane l scores patterns l, l + 32, l + 64 with the
+// reference's sequential adds over the 8 kept positions (_core.pyx:98-109), then a butterfly
+// reduction keeps the largest score and, on equal scores, the lowest pattern index -- for
+// finite scores exactly the reference's first strict maximum.  wd is warp-uniform.
+__device__ __noinline__ int search_block_f64_warp(const uint32_t (&wd)[8], int lane) {
+  double a[16];
+  block_abs_f64(wd, a);
+  double best = 0.0;
+  int bt = 127;  // none
+#pragma unroll
+  for (int rr = 0; rr < 3; ++rr) {
+    const int t = lane + 32 * rr;
+    if (t < 90) {
+      const uint32_t rows = c_pat_rows[t];
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t q = (rows >> (4 * r)) & 15u;
+        const int lo = static_cast<int>((0x000112u >> (4 * q)) & 15u), hi = static_cast<int>((0x123233u >> (4 * q)) & 15u);
+        s = r == 0 ? __dadd_rn(a[lo], a[hi]) : __dadd_rn(__dadd_rn(s, a[4 * r + lo]), a[4 * r + hi]);
+      }
+      if (bt == 127 || s > best) {
+        best = s;
+        bt = t;
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, off);
+    const int ot = __shfl_xor_sync(0xFFFFFFFFu, bt, off);
+    if (ot != 127 && (bt == 127 || ob > best || (ob == best && ot < bt))) {
+      best = ob;
+      bt = ot;
+    }
+  }
+  return bt;
+}
+
+// Persistent K1 with warp-owned strips.  A CTA of 4 warps owns one 128 x 128 tile at a time
+// (tiles blockIdx.x, + gridDim.x, ... over p0's tiles, then p1's); warp a owns the tile's rows
+// 32 a .. 32 a + 31 and sweeps them in four PASSES of 32 columns (lane = (block row lane / 4,
+// column group lane % 4) holds two 4x4 blocks of a pass, 4 rows x 16 bytes).  Every lane streams
+// its 4 x 16 bytes of the pass two ahead into its own shared-memory slots with cp.async while it
+// searches the current one.  Every output leaves in whole 32-byte sectors (a partial-sector
+// write that misses L2 costs a DRAM read to fill the sector):
+//   fwd_vals  4 rows x 8 bytes per lane and pass (4 lanes = one row's 32-byte segment);
+//   bwd_vals  8 W^T rows x 4 bytes per lane and pass (8 lanes = one W^T row's 32-byte segment);
+//   fwd E     the warp's 32 rows are 32 whole metadata lines: lane (m & 7, kpar, m >> 4) gathers
+//             one 4-byte word of its line per pass (4 shuffles) and stores the 16-byte line once;
+//   idx       8 bytes per lane per tile after a 4-lane exchange;
+//   bwd E     a W^T metadata line spans all 128 rows (all four warps): the words are staged in
+//             shared memory (double-buffered per tile) and written as 16-byte lines after the
+//             tile's one 4-warp barrier.
+// Blocks whose exponent span needs the float64 reference-order path are searched after the fast
+// path by the whole warp together (search_block_f64_warp, the north-star's warp-shuffle argmax).
+constexpr int kK1Threads = 128;  // 4 warps; 6 CTAs per SM (80 registers per thread)
+constexpr int kK1Depth = 3;      // input slots per lane: the current pass + two in flight
 struct K1Smem {
-  uint4 in[2][4][kPruneThreads];  // 64 KB: slot (buffer, row i, thread)
-  uint32_t bv[2][128 * 32];       // 32 KB: W^T tile, 128 rows x 32 words (64 kept bf16)
-  uint32_t fe[2][512];            // fwd E tile (2048 B)
-  uint32_t be[2][512];            // bwd E tile
-  uint4 sel[90];                  // per pattern: row selectors (x, y), column selectors (z, w)
-  uint32_t nib[90];               // fwd row nibbles (bits 0-15) | bwd column nibbles (bits 16-31)
+  uint4 in[kK1Depth][4][kK1Threads];  // 24 KB: slot (buffer, row i, thread)
+  uint32_t be[2][512];                // bwd E tile staging, double-buffered over tiles
+  uint4 sel[90];                      // per pattern: row selectors (x, y), column selectors (z, w)
+  uint32_t nib[90];                   // fwd row nibbles (bits 0-15) | bwd column nibbles (bits 16-31)
 };
 constexpr int kK1SmemBytes = static_cast<int>(sizeof(K1Smem));
 
@@ -633,49 +688,31 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait2() { asm volatile("cp.async.wait_group 2;" ::: "memory"); }
 
-struct K1Tile {
-  int which;       // 0: p0, 1: p1, -1: none
-  int64_t tr, tc;  // tile row / col of that weight
+struct K1Pos {
+  int which;         // 0: p0, 1: p1, -1: past the end
+  uint32_t tr, tc;   // tile of that weight
 };
 
-__device__ __forceinline__ K1Tile k1_tile(int g, int tiles0, int total, const MaskArgs& p0, const MaskArgs& p1) {
-  K1Tile t{-1, 0, 0};
-  if (g >= total) return t;
-  const bool second = g >= tiles0;
-  const int b = second ? g - tiles0 : g;
-  const int tiles_x = static_cast<int>((second ? p1.cols : p0.cols) / kTile);
-  const int r = b / tiles_x;
-  t.which = second ? 1 : 0;
-  t.tr = r;
-  t.tc = b - r * tiles_x;
-  return t;
+__device__ __forceinline__ K1Pos k1_pos(uint32_t t, uint32_t tiles0, uint32_t total, uint32_t tx0, uint32_t tx1) {
+  K1Pos q{-1, 0, 0};
+  if (t >= total) return q;
+  const bool second = t >= tiles0;
+  const uint32_t b = second ? t - tiles0 : t, tx = second ? tx1 : tx0;
+  q.which = second ? 1 : 0;
+  q.tr = b / tx;
+  q.tc = b - q.tr * tx;
+  return q;
 }
 
-__global__ void __launch_bounds__(kPruneThreads, 2) search_bf16_kernel(MaskArgs p0, MaskArgs p1, int tiles0,
-                                                                        int total) {
+__global__ void __launch_bounds__(kK1Threads, 6) search_bf16_kernel(MaskArgs p0, MaskArgs p1, uint32_t tiles0,
+                                                                     uint32_t total) {
   extern __shared__ __align__(16) uint8_t k1_raw[];
   K1Smem& S = *reinterpret_cast<K1Smem*>(k1_raw);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int br = 2 * warp + (lane >> 4);  // block row in the tile, 0..31
-  const int c0 = 8 * (lane & 15);         // first column in the tile, 0..120
-
-  auto prefetch = [&](const K1Tile& t, int buf) {
-    if (t.which >= 0) {
-      const MaskArgs& q = t.which ? p1 : p0;
-      const int64_t grow0 = t.tr * kTile + 4 * br;
-      const int64_t in_row0 = q.perm_ff > 0 ? gate_row(grow0, q.perm_ff) : grow0;
-      const uint16_t* src = static_cast<const uint16_t*>(q.w) + in_row0 * q.cols + t.tc * kTile + c0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) cp_async16(&S.in[buf][i][tid], src + i * q.cols);
-    }
-    cp_async_commit();  // (possibly empty) group: wait_group 1 below always means "the previous tile"
-  };
-
-  int g = blockIdx.x;
-  K1Tile cur = k1_tile(g, tiles0, total, p0, p1);
-  prefetch(cur, 0);
+  const int tid = threadIdx.x, lane = tid & 31, wa = tid >> 5;  // warp = row strip of the tile
+  const int br = lane >> 2;  // block row in the strip, 0..7
+  const int g = lane & 3;    // column group (8 columns = two blocks), 0..3
   if (tid < 90) {
     const uint32_t bits16 = c_pat_bits[tid];
     uint32_t r[4], c[4], nf = 0, nb = 0;
@@ -690,115 +727,183 @@ __global__ void __launch_bounds__(kPruneThreads, 2) search_bf16_kernel(MaskArgs 
     S.sel[tid] = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), c[0] | (c[1] << 16), c[2] | (c[3] << 16));
     S.nib[tid] = nf | (nb << 16);
   }
+  const uint32_t tx0 = static_cast<uint32_t>(p0.cols >> 7), tx1 = static_cast<uint32_t>(p1.cols >> 7);
+
+  // (tile, pass) sequence of this CTA: s -> tile blockIdx.x + (s / 4) gridDim.x, pass s % 4
+  auto src_of = [&](const K1Pos& q, int pass) {
+    const MaskArgs& a = q.which ? p1 : p0;
+    const uint32_t cols = static_cast<uint32_t>(a.cols);
+    const uint32_t grow0 = 128 * q.tr + 32 * wa + 4 * br;
+    const uint32_t in_row0 = a.perm_ff > 0 ? static_cast<uint32_t>(gate_row(grow0, a.perm_ff)) : grow0;
+    return static_cast<const uint16_t*>(a.w) + (static_cast<uint64_t>(in_row0) * cols + 128 * q.tc + 32 * pass + 8 * g);
+  };
+  auto prefetch = [&](const K1Pos& q, int pass, int buf) {
+    if (q.which >= 0) {
+      const uint16_t* src = src_of(q, pass);
+      const uint64_t cols = static_cast<uint64_t>((q.which ? p1 : p0).cols);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cp_async16(&S.in[buf][i][tid], src + i * cols);
+    }
+    cp_async_commit();  // (possibly empty) group: wait_group 2 below always means "the current pass"
+  };
+
+  uint32_t t = blockIdx.x;
+  K1Pos cur = k1_pos(t, tiles0, total, tx0, tx1);
+  K1Pos nxt = k1_pos(t + gridDim.x, tiles0, total, tx0, tx1);  // tile after cur
+  prefetch(cur, 0, 0);
+  prefetch(cur, 1, 1);
   __syncthreads();  // tables ready
-
-  for (int buf = 0; cur.which >= 0; buf ^= 1) {
-    const K1Tile nxt = k1_tile(g + gridDim.x, tiles0, total, p0, p1);
-    prefetch(nxt, buf ^ 1);
-    cp_async_wait1();  // this thread's slot of the current tile has landed
+  int buf = 0, tslot = 0;
+  uint32_t f0 = 0, f1 = 0, f2 = 0, f3 = 0;  // fwd E line words of passes 0..3
+  uint64_t idx_acc = 0;                      // the lane's 2-byte idx chunk of passes 0..3
+  while (cur.which >= 0) {
     const MaskArgs& p = cur.which ? p1 : p0;
-    const int64_t tr = cur.tr, tc = cur.tc;
-    const int64_t grow0 = tr * kTile + 4 * br, gcol0 = tc * kTile + c0;
-    uint4 v[4];
+    const uint32_t rows = static_cast<uint32_t>(p.rows), cols = static_cast<uint32_t>(p.cols);
+#pragma unroll 1
+    for (int pass = 0; pass < 4; ++pass) {
+      // prefetch pass + 2 (this tile's, or the next tile's first two)
+      if (pass < 2) prefetch(cur, pass + 2, buf == 0 ? 2 : buf - 1);
+      else prefetch(nxt, pass - 2, buf == 0 ? 2 : buf - 1);
+      cp_async_wait2();  // this lane's slot of the current pass has landed
+      uint4 v[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = S.in[buf][i][tid];
+      for (int i = 0; i < 4; ++i) v[i] = S.in[buf][i][tid];
 
-    int pat[2];
+      // ---- search: integer fast path per lane, then the float64 blocks warp-cooperatively ----
+      int pat[2];
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      uint32_t wd[8];
+      for (int b = 0; b < 2; ++b) {
+        uint32_t wd[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        wd[2 * i] = (&v[i].x)[2 * b];
-        wd[2 * i + 1] = (&v[i].x)[2 * b + 1];
-      }
-      pat[b] = search_block_bf16w(wd);
-    }
-    *reinterpret_cast<uint16_t*>(p.idx_out + (grow0 / 4) * (p.cols / 4) + gcol0 / 4) =
-        static_cast<uint16_t>(pat[0] | (pat[1] << 8));
-    const uint32_t n0 = S.nib[pat[0]], n1 = S.nib[pat[1]];
-    // fwd E: row m = 4 br + i holds groups c0/4, c0/4 + 1 -> one byte of its halfword
-    if (p.fwd_e) {
-      uint8_t* fe = reinterpret_cast<uint8_t*>(S.fe[buf]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int m = 4 * br + i;
-        const int L = (m & 7) + 8 * ((c0 & 31) >> 4) + 16 * (m >> 4);
-        const int c = c0 >> 5, h = (m >> 3) & 1;
-        fe[2 * (L * 8 + c * 2 + h) + ((c0 >> 3) & 1)] =
-            static_cast<uint8_t>(((n0 >> (4 * i)) & 0xFu) | (((n1 >> (4 * i)) & 0xFu) << 4));
-      }
-    }
-    // bwd E: W^T row mp = c0 + 4b + j, group br; block rows 2w (lane < 16) and 2w + 1
-    // (lane + 16) share one byte -> exchange the eight column nibbles once
-    if (p.bwd_e) {
-      const uint32_t mine = (n0 >> 16) | (n1 & 0xFFFF0000u);  // nibble 4b + j
-      const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, 16);
-      const uint32_t lo = lane < 16 ? mine : other, hi = lane < 16 ? other : mine;
-      uint8_t* be = reinterpret_cast<uint8_t*>(S.be[buf]);
-      const int brp = br & ~1;  // even block row of the pair
-      const int c = brp >> 3, byte_in_half = (brp >> 1) & 1;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int k = 4 * (lane >> 4) + q;  // lanes < 16: columns 0-3, lanes >= 16: columns 4-7
-        const int mp = c0 + k;
-        const int L = (mp & 7) + 16 * (mp >> 4) + 8 * ((brp >> 2) & 1);
-        const int h = (mp >> 3) & 1;
-        be[4 * (L * 4 + c) + 2 * h + byte_in_half] =
-            static_cast<uint8_t>(((lo >> (4 * k)) & 0xFu) | (((hi >> (4 * k)) & 0xFu) << 4));
-      }
-    }
-    uint32_t fw[4][2];
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      const uint4 sel = S.sel[pat[b]];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t si = ((i < 2 ? sel.x : sel.y) >> (16 * (i & 1))) & 0xFFFFu;
-        fw[i][b] = __byte_perm((&v[i].x)[2 * b], (&v[i].x)[2 * b + 1], si);
-      }
-      if (p.bwd_vals) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int wj = 2 * b + (j >> 1);
-          const uint32_t hsel = (j & 1) ? 0x7632u : 0x5410u;
-          const uint32_t col01 = __byte_perm((&v[0].x)[wj], (&v[1].x)[wj], hsel);
-          const uint32_t col23 = __byte_perm((&v[2].x)[wj], (&v[3].x)[wj], hsel);
-          const uint32_t sj = ((j < 2 ? sel.z : sel.w) >> (16 * (j & 1))) & 0xFFFFu;
-          const int mp = c0 + 4 * b + j;
-          S.bv[buf][mp * 32 + ((br + 2 * (mp >> 3)) & 31)] = __byte_perm(col01, col23, sj);
+        for (int i = 0; i < 4; ++i) {
+          wd[2 * i] = (&v[i].x)[2 * b];
+          wd[2 * i + 1] = (&v[i].x)[2 * b + 1];
+        }
+        pat[b] = search_block_fast(wd);
+        if (pat[b] == -2) {  // inf / nan: the sequential reference loop (its own comparison semantics)
+          double a[16];
+          block_abs_f64(wd, a);
+          pat[b] = search_block_f64(a);
         }
       }
-    }
-    if (p.fwd_vals) {
+      unsigned slow0 = __ballot_sync(0xFFFFFFFFu, pat[0] < 0), slow1 = __ballot_sync(0xFFFFFFFFu, pat[1] < 0);
+      while (slow0 | slow1) {  // warp-uniform
+        const int b = slow0 ? 0 : 1;
+        const int owner = __ffs(b ? slow1 : slow0) - 1;
+        if (b) slow1 &= slow1 - 1;
+        else slow0 &= slow0 - 1;
+        uint32_t wd[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        *reinterpret_cast<uint2*>(p.fwd_vals + (grow0 + i) * (p.cols / 2) + gcol0 / 2) = make_uint2(fw[i][0], fw[i][1]);
-    }
-    __syncthreads();  // staging[buf] complete (and staging[buf ^ 1]'s copy-out of the previous tile done)
-    if (p.fwd_e && tid < 128) {
-      uint4* dst = reinterpret_cast<uint4*>(p.fwd_e + (tr * (p.cols / kTile) + tc) * 2048);
-      dst[tid] = reinterpret_cast<const uint4*>(S.fe[buf])[tid];
-    }
-    if (p.bwd_e && tid >= 128 && tid < 256) {
-      uint4* dst = reinterpret_cast<uint4*>(p.bwd_e + (tc * (p.rows / kTile) + tr) * 2048);
-      dst[tid - 128] = reinterpret_cast<const uint4*>(S.be[buf])[tid - 128];
-    }
-    if (p.bwd_vals) {
-      const int64_t kcol = tr * (kTile / 2) + 2 * lane;
-#pragma unroll 4
-      for (int rr = warp; rr < kTile; rr += kPruneThreads / 32) {
-        const uint32_t val = S.bv[buf][rr * 32 + ((lane + 2 * (rr >> 3)) & 31)];
-        *reinterpret_cast<uint32_t*>(p.bwd_vals + (tc * kTile + rr) * (p.rows / 2) + kcol) = val;
+        for (int i = 0; i < 4; ++i) {
+          wd[2 * i] = __shfl_sync(0xFFFFFFFFu, b ? v[i].z : v[i].x, owner);
+          wd[2 * i + 1] = __shfl_sync(0xFFFFFFFFu, b ? v[i].w : v[i].y, owner);
+        }
+        const int tt = search_block_f64_warp(wd, lane);
+        if (lane == owner) {
+          if (b) pat[1] = tt;
+          else pat[0] = tt;
+        }
       }
+
+      const uint32_t grow0 = 128 * cur.tr + 32 * wa + 4 * br, gcol0 = 128 * cur.tc + 32 * pass + 8 * g;
+      idx_acc = (idx_acc >> 16) | (static_cast<uint64_t>(pat[0] | (pat[1] << 8)) << 48);
+      const uint32_t n0 = S.nib[pat[0]], n1 = S.nib[pat[1]];
+      {  // fwd E: byte i of fb = row 4 br + i of the lane's 8 columns (block 0 | block 1 << 4)
+        uint32_t fb = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) fb |= (((n0 >> (4 * i)) & 0xFu) | (((n1 >> (4 * i)) & 0xFu) << 4)) << (8 * i);
+        // lane -> line (m & 7, kpar, m >> 4): rows m, m + 8 x column groups 2 kpar, 2 kpar + 1
+        const int m7 = lane & 7, kp = (lane >> 3) & 1, mhi = lane >> 4;
+        const int br0 = 4 * mhi + (m7 >> 2), i = m7 & 3;
+        const int la = 4 * br0 + 2 * kp, lb = la + 8;  // block rows br0 and br0 + 2
+        const uint32_t a0 = __shfl_sync(0xFFFFFFFFu, fb, la), a1 = __shfl_sync(0xFFFFFFFFu, fb, la + 1);
+        const uint32_t b0 = __shfl_sync(0xFFFFFFFFu, fb, lb), b1 = __shfl_sync(0xFFFFFFFFu, fb, lb + 1);
+        const uint32_t lo = __byte_perm(a0, a1, i | ((i + 4) << 4)), hi = __byte_perm(b0, b1, i | ((i + 4) << 4));
+        f0 = f1;
+        f1 = f2;
+        f2 = f3;
+        f3 = (lo & 0xFFFFu) | (hi << 16);
+      }
+      if (p.bwd_e) {
+        // column nibble k of the lane's 8 columns (block b = k / 4)
+        const uint32_t mine = (n0 >> 16) | (n1 & 0xFFFF0000u);
+        // lane -> W^T rows mp = 32 pass + 16 mhi + k (h = 0) and mp + 8 (h = 1); block-row pairs
+        // (4 q2, 4 q2 + 1) -> byte 0 and (4 q2 + 2, 4 q2 + 3) -> byte 1 of each halfword
+        const int k = lane & 7, mhi = (lane >> 3) & 1, q2 = lane >> 4;
+        uint32_t word = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            const uint32_t x = __shfl_sync(0xFFFFFFFFu, mine, 4 * (4 * q2 + bb) + 2 * mhi + h);
+            word |= ((x >> (4 * k)) & 0xFu) << (16 * h + 4 * bb);
+          }
+        S.be[tslot][(k + 16 * (2 * pass + mhi) + 8 * q2) * 4 + wa] = word;
+      }
+      uint32_t fw[4][2];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const uint4 sel = S.sel[pat[b]];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t si = ((i < 2 ? sel.x : sel.y) >> (16 * (i & 1))) & 0xFFFFu;
+          fw[i][b] = __byte_perm((&v[i].x)[2 * b], (&v[i].x)[2 * b + 1], si);
+        }
+        if (p.bwd_vals) {
+          // W^T row = column gcol0 + 4 b + jj, the block row's two kept values at element grow0 / 2
+          uint16_t* bv = p.bwd_vals + (static_cast<uint64_t>(gcol0 + 4 * b) * (rows >> 1) + (grow0 >> 1));
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int wj = 2 * b + (jj >> 1);
+            const uint32_t hsel = (jj & 1) ? 0x7632u : 0x5410u;
+            const uint32_t col01 = __byte_perm((&v[0].x)[wj], (&v[1].x)[wj], hsel);
+            const uint32_t col23 = __byte_perm((&v[2].x)[wj], (&v[3].x)[wj], hsel);
+            const uint32_t sj = ((jj < 2 ? sel.z : sel.w) >> (16 * (jj & 1))) & 0xFFFFu;
+            *reinterpret_cast<uint32_t*>(bv + static_cast<uint64_t>(jj) * (rows >> 1)) = __byte_perm(col01, col23, sj);
+          }
+        }
+      }
+      if (p.fwd_vals) {
+        uint16_t* fv = p.fwd_vals + (static_cast<uint64_t>(grow0) * (cols >> 1) + (gcol0 >> 1));
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          *reinterpret_cast<uint2*>(fv + static_cast<uint64_t>(i) * (cols >> 1)) = make_uint2(fw[i][0], fw[i][1]);
+      }
+      buf = buf == kK1Depth - 1 ? 0 : buf + 1;
     }
-    g += gridDim.x;
+    // ---- per tile: fwd E lines, idx, bwd E tile ----
+    const uint32_t tr = cur.tr, tc = cur.tc;
+    if (p.fwd_e) {
+      const int L = (lane & 7) + 8 * ((lane >> 3) & 1) + 16 * (2 * wa + (lane >> 4));
+      *reinterpret_cast<uint4*>(p.fwd_e + (static_cast<uint64_t>(tr) * (cols >> 7) + tc) * 2048 + L * 16) =
+          make_uint4(f0, f1, f2, f3);
+    }
+    if (p.idx_out) {
+      // lane (br, g) stores block columns 8 g .. 8 g + 7 of its block row: pass g's chunks of lanes (br, 0..3)
+      uint32_t part[4];
+#pragma unroll
+      for (int gg = 0; gg < 4; ++gg) {
+        const uint64_t x = __shfl_sync(0xFFFFFFFFu, idx_acc, 4 * br + gg);
+        part[gg] = static_cast<uint32_t>(x >> (16 * g)) & 0xFFFFu;
+      }
+      const uint32_t brow = 32 * tr + 8 * wa + br;
+      *reinterpret_cast<uint2*>(p.idx_out + static_cast<uint64_t>(brow) * (cols >> 2) + 32 * tc + 8 * g) =
+          make_uint2(part[0] | (part[1] << 16), part[2] | (part[3] << 16));
+    }
+    __syncthreads();  // the tile's bwd E words from all four warps are in S.be[tslot]
+    if (p.bwd_e)
+      reinterpret_cast<uint4*>(p.bwd_e + (static_cast<uint64_t>(tc) * (rows >> 7) + tr) * 2048)[tid] =
+          reinterpret_cast<const uint4*>(S.be[tslot])[tid];
+    tslot ^= 1;
+    t += gridDim.x;
     cur = nxt;
+    nxt = k1_pos(t + gridDim.x, tiles0, total, tx0, tx1);
   }
 }
 
-// persistent grid: two CTAs per SM (the kernel's register and shared-memory footprint)
-static int k1_grid(int total) {
+// persistent grid: six 4-warp CTAs per SM (the kernel's register footprint)
+static int k1_grid(long long tiles) {
+  const long long total = tiles;  // one tile per CTA at a time
   static int sms[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -809,7 +914,7 @@ static int k1_grid(int total) {
     cudaFuncSetAttribute(search_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kK1SmemBytes);
     sms[dev] = n > 0 ? n : 148;
   }
-  return total < 2 * sms[dev] ? total : 2 * sms[dev];
+  return static_cast<int>(total < 6 * sms[dev] ? total : 6 * sms[dev]);
 }
 
 // ---------------------------------------------------------------------------
@@ -949,8 +1054,12 @@ static int launch_mask(const MaskArgs& a, int dtype, bool search, cudaStream_t s
   const bool aligned = a.rows % kTile == 0 && a.cols % kTile == 0;
   if (search) {
     if (dtype == S24_BF16 && aligned) {
-      const int tiles = static_cast<int>(grid.x * grid.y);
-      search_bf16_kernel<<<k1_grid(tiles), kPruneThreads, kK1SmemBytes, st>>>(a, a, tiles, tiles);
+      if (a.rows * a.cols < (int64_t(1) << 32)) {
+        const uint32_t tiles = static_cast<uint32_t>(grid.x * grid.y);
+        search_bf16_kernel<<<k1_grid(tiles), kK1Threads, kK1SmemBytes, st>>>(a, a, tiles, tiles);
+        return s24_check_launch("mask_search");
+      }
+      mask_tile_kernel<S24_BF16, true, false><<<grid, kThreads, 0, st>>>(a);
       return s24_check_launch("mask_search");
     }
     if (narrow) mask_tile_kernel<S24_BF16, true, true><<<grid, kThreads, 0, st>>>(a);
@@ -1063,7 +1172,12 @@ extern "C" int s24_search_compress_pair(const void* w0, const void* w1, int dtyp
   }
   const int t0 = static_cast<int>((rows0 / kTile) * (cols0 / kTile)), t1 = static_cast<int>((rows1 / kTile) * (cols1 / kTile));
   if (t0 + t1 == 0) return S24_OK;
-  search_bf16_kernel<<<k1_grid(t0 + t1), kPruneThreads, kK1SmemBytes, st>>>(a0, a1, t0, t0 + t1);
+  if (rows0 * cols0 >= (int64_t(1) << 32) || rows1 * cols1 >= (int64_t(1) << 32)) {  // 32-bit strip indexing
+    if (int rc = launch_mask(a0, dtype, true, st)) return rc;
+    return launch_mask(a1, dtype, true, st);
+  }
+  search_bf16_kernel<<<k1_grid(t0 + t1), kK1Threads, kK1SmemBytes, st>>>(a0, a1, static_cast<uint32_t>(t0),
+                                                                         static_cast<uint32_t>(t0 + t1));
   return s24_check_launch("search_compress_pair");
 }
 
