@@ -657,30 +657,35 @@ __device__ __noinline__ int search_block_f64_warp(const uint32_t (&wd)[8], int l
   return bt;
 }
 
-// Persistent K1 with warp-owned strips.  A CTA of 4 warps owns one 128 x 128 tile at a time
-// (tiles blockIdx.x, + gridDim.x, ... over p0's tiles, then p1's); warp a owns the tile's rows
-// 32 a .. 32 a + 31 and sweeps them in four PASSES of 32 columns (lane = (block row lane / 4,
-// column group lane % 4) holds two 4x4 blocks of a pass, 4 rows x 16 bytes).  Every lane streams
-// its 4 x 16 bytes of the pass two ahead into its own shared-memory slots with cp.async while it
+// Persistent K1 with warp-owned strips.  A CTA of 4 warps owns one SUPER-TILE at a time: two
+// horizontally adjacent 128 x 128 tiles (one when the weight has an odd number of tile columns),
+// super-tiles blockIdx.x, + gridDim.x, ... over p0's, then p1's.  Warp a owns rows 32 a .. 32 a
+// + 31 and sweeps them in PASSES of 32 columns (4 per tile; lane = (block row lane / 4, column
+// group lane % 4) holds two 4x4 blocks of a pass, 4 rows x 16 bytes).  Every lane streams its
+// 4 x 16 bytes of the pass two ahead into its own shared-memory slots with cp.async while it
 // searches the current one.  Every output leaves in whole 32-byte sectors (a partial-sector
 // write that misses L2 costs a DRAM read to fill the sector):
 //   fwd_vals  4 rows x 8 bytes per lane and pass (4 lanes = one row's 32-byte segment);
 //   bwd_vals  8 W^T rows x 4 bytes per lane and pass (8 lanes = one W^T row's 32-byte segment);
-//   fwd E     the warp's 32 rows are 32 whole metadata lines: lane (m & 7, kpar, m >> 4) gathers
-//             one 4-byte word of its line per pass (4 shuffles) and stores the 16-byte line once;
+//   fwd E     the warp's 32 rows are 32 whole metadata lines per tile: lane (m & 7, kpar, m >> 4)
+//             gathers one 4-byte word of its line per pass (4 shuffles), stores the line once;
 //   idx       8 bytes per lane per tile after a 4-lane exchange;
-//   bwd E     a W^T metadata line spans all 128 rows (all four warps): the words are staged in
-//             shared memory (double-buffered per tile) and written as 16-byte lines after the
-//             tile's one 4-warp barrier.
+//   bwd E     a W^T metadata line spans all 128 rows (all four warps): per pass each lane's word
+//             comes out of an 8 x 8 nibble transpose (one gather shuffle + three butterfly
+//             stages), is staged in shared memory, and the tiles leave as 16-byte lines after the
+//             super-tile's one 4-warp barrier (one barrier per 8 passes).
 // Blocks whose exponent span needs the float64 reference-order path are searched after the fast
 // path by the whole warp together (search_block_f64_warp, the north-star's warp-shuffle argmax).
-constexpr int kK1Threads = 128;  // 4 warps; 6 CTAs per SM (80 registers per thread)
+constexpr int kK1Threads = 128;  // 4 warps per CTA
+#ifndef S24_K1_MINB
+#define S24_K1_MINB 6  // CTAs per SM (6: 80 registers per thread, no spills)
+#endif
 constexpr int kK1Depth = 3;      // input slots per lane: the current pass + two in flight
 struct K1Smem {
   uint4 in[kK1Depth][4][kK1Threads];  // 24 KB: slot (buffer, row i, thread)
-  uint32_t be[2][512];                // bwd E tile staging, double-buffered over tiles
+  uint32_t be[2][2][512];             // bwd E staging: [super-tile parity][tile of the pair]
   uint4 sel[90];                      // per pattern: row selectors (x, y), column selectors (z, w)
-  uint32_t nib[90];                   // fwd row nibbles (bits 0-15) | bwd column nibbles (bits 16-31)
+  uint2 nib[90];                      // per pattern: x = fwd row nibble i at bits 8 i, y = bwd column nibbles
 };
 constexpr int kK1SmemBytes = static_cast<int>(sizeof(K1Smem));
 
@@ -692,22 +697,40 @@ __device__ __forceinline__ void cp_async_wait2() { asm volatile("cp.async.wait_g
 
 struct K1Pos {
   int which;         // 0: p0, 1: p1, -1: past the end
-  uint32_t tr, tc;   // tile of that weight
+  int ntile;         // tiles in this super-tile (1 or 2)
+  uint32_t tr, tc0;  // first tile of the super-tile
 };
 
-__device__ __forceinline__ K1Pos k1_pos(uint32_t t, uint32_t tiles0, uint32_t total, uint32_t tx0, uint32_t tx1) {
-  K1Pos q{-1, 0, 0};
+// super-tile t of the concatenated list; sx = super-tiles per tile row, pair = 2-tile super-tiles
+__device__ __forceinline__ K1Pos k1_pos(uint32_t t, uint32_t st0, uint32_t total, uint32_t sx0, uint32_t sx1,
+                                        int pair0, int pair1) {
+  K1Pos q{-1, 1, 0, 0};
   if (t >= total) return q;
-  const bool second = t >= tiles0;
-  const uint32_t b = second ? t - tiles0 : t, tx = second ? tx1 : tx0;
+  const bool second = t >= st0;
+  const uint32_t b = second ? t - st0 : t, sx = second ? sx1 : sx0;
+  const int pr = second ? pair1 : pair0;
   q.which = second ? 1 : 0;
-  q.tr = b / tx;
-  q.tc = b - q.tr * tx;
+  q.ntile = pr ? 2 : 1;
+  q.tr = b / sx;
+  q.tc0 = (b - q.tr * sx) * (pr ? 2 : 1);
   return q;
 }
 
-__global__ void __launch_bounds__(kK1Threads, 6) search_bf16_kernel(MaskArgs p0, MaskArgs p1, uint32_t tiles0,
-                                                                     uint32_t total) {
+// lane j of an 8-lane group holds row j of an 8 x 8 nibble matrix (nibble c at bits 4 c); after
+// the three butterfly stages it holds column j (nibble c = row c's nibble j)
+__device__ __forceinline__ uint32_t nibble_transpose8(uint32_t x, int j) {
+#pragma unroll
+  for (int sdist = 4; sdist >= 1; sdist >>= 1) {
+    const uint32_t keep = sdist == 4 ? 0x0000FFFFu : sdist == 2 ? 0x00FF00FFu : 0x0F0F0F0Fu;
+    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, sdist);
+    x = (j & sdist) ? ((x & ~keep) | ((y & ~keep) >> (4 * sdist))) : ((x & keep) | ((y & keep) << (4 * sdist)));
+  }
+  return x;
+}
+
+__global__ void __launch_bounds__(kK1Threads, S24_K1_MINB) search_bf16_kernel(MaskArgs p0, MaskArgs p1,
+                                                                               uint32_t st0, uint32_t total,
+                                                                               int pairs) {
   extern __shared__ __align__(16) uint8_t k1_raw[];
   K1Smem& S = *reinterpret_cast<K1Smem*>(k1_raw);
   const int tid = threadIdx.x, lane = tid & 31, wa = tid >> 5;  // warp = row strip of the tile
@@ -721,26 +744,24 @@ __global__ void __launch_bounds__(kK1Threads, 6) search_bf16_kernel(MaskArgs p0,
       const uint32_t rn = nib_of_mask((bits16 >> (4 * k)) & 0xFu), cn = nib_of_mask(col_mask(bits16, k));
       r[k] = pair_selector(rn);
       c[k] = pair_selector(cn);
-      nf |= rn << (4 * k);
+      nf |= rn << (8 * k);
       nb |= cn << (4 * k);
     }
     S.sel[tid] = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), c[0] | (c[1] << 16), c[2] | (c[3] << 16));
-    S.nib[tid] = nf | (nb << 16);
+    S.nib[tid] = make_uint2(nf, nb);
   }
-  const uint32_t tx0 = static_cast<uint32_t>(p0.cols >> 7), tx1 = static_cast<uint32_t>(p1.cols >> 7);
+  const int pair0 = pairs & 1, pair1 = (pairs >> 1) & 1;
+  const uint32_t sx0 = static_cast<uint32_t>(p0.cols >> 7) / (pair0 ? 2 : 1);
+  const uint32_t sx1 = static_cast<uint32_t>(p1.cols >> 7) / (pair1 ? 2 : 1);
 
-  // (tile, pass) sequence of this CTA: s -> tile blockIdx.x + (s / 4) gridDim.x, pass s % 4
-  auto src_of = [&](const K1Pos& q, int pass) {
-    const MaskArgs& a = q.which ? p1 : p0;
-    const uint32_t cols = static_cast<uint32_t>(a.cols);
-    const uint32_t grow0 = 128 * q.tr + 32 * wa + 4 * br;
-    const uint32_t in_row0 = a.perm_ff > 0 ? static_cast<uint32_t>(gate_row(grow0, a.perm_ff)) : grow0;
-    return static_cast<const uint16_t*>(a.w) + (static_cast<uint64_t>(in_row0) * cols + 128 * q.tc + 32 * pass + 8 * g);
-  };
-  auto prefetch = [&](const K1Pos& q, int pass, int buf) {
+  // pass sequence of this CTA: super-tile blockIdx.x + k gridDim.x, passes 0 .. 4 ntile - 1
+  auto prefetch = [&](const K1Pos& q, int pp, int buf) {
     if (q.which >= 0) {
-      const uint16_t* src = src_of(q, pass);
-      const uint64_t cols = static_cast<uint64_t>((q.which ? p1 : p0).cols);
+      const MaskArgs& a = q.which ? p1 : p0;
+      const uint64_t cols = static_cast<uint64_t>(a.cols);
+      const uint32_t grow0 = 128 * q.tr + 32 * wa + 4 * br;
+      const uint32_t in_row0 = a.perm_ff > 0 ? static_cast<uint32_t>(gate_row(grow0, a.perm_ff)) : grow0;
+      const uint16_t* src = static_cast<const uint16_t*>(a.w) + (in_row0 * cols + 128 * q.tc0 + 32 * pp + 8 * g);
 #pragma unroll
       for (int i = 0; i < 4; ++i) cp_async16(&S.in[buf][i][tid], src + i * cols);
     }
@@ -748,22 +769,26 @@ __global__ void __launch_bounds__(kK1Threads, 6) search_bf16_kernel(MaskArgs p0,
   };
 
   uint32_t t = blockIdx.x;
-  K1Pos cur = k1_pos(t, tiles0, total, tx0, tx1);
-  K1Pos nxt = k1_pos(t + gridDim.x, tiles0, total, tx0, tx1);  // tile after cur
+  K1Pos cur = k1_pos(t, st0, total, sx0, sx1, pair0, pair1);
+  K1Pos nxt = k1_pos(t + gridDim.x, st0, total, sx0, sx1, pair0, pair1);
   prefetch(cur, 0, 0);
-  prefetch(cur, 1, 1);
+  prefetch(cur.ntile * 4 > 1 ? cur : nxt, 1, 1);
   __syncthreads();  // tables ready
-  int buf = 0, tslot = 0;
-  uint32_t f0 = 0, f1 = 0, f2 = 0, f3 = 0;  // fwd E line words of passes 0..3
-  uint64_t idx_acc = 0;                      // the lane's 2-byte idx chunk of passes 0..3
+  int buf = 0, sslot = 0;
+  uint32_t f0 = 0, f1 = 0, f2 = 0, f3 = 0;  // fwd E line words of the tile's passes 0..3
+  uint64_t idx_acc = 0;                      // the lane's 2-byte idx chunk of the tile's passes 0..3
+  // bwd E transpose roles: lane = (q2, mhi, k) of its line word, gather source row k
+  const int tk = lane & 7, tmhi = (lane >> 3) & 1, tq2 = lane >> 4;
+  const int tsrc = 4 * (4 * tq2 + (tk & 3)) + 2 * tmhi + (tk >> 2);
   while (cur.which >= 0) {
     const MaskArgs& p = cur.which ? p1 : p0;
     const uint32_t rows = static_cast<uint32_t>(p.rows), cols = static_cast<uint32_t>(p.cols);
+    const int npass = 4 * cur.ntile;
 #pragma unroll 1
-    for (int pass = 0; pass < 4; ++pass) {
-      // prefetch pass + 2 (this tile's, or the next tile's first two)
-      if (pass < 2) prefetch(cur, pass + 2, buf == 0 ? 2 : buf - 1);
-      else prefetch(nxt, pass - 2, buf == 0 ? 2 : buf - 1);
+    for (int pp = 0; pp < npass; ++pp) {
+      // prefetch pass pp + 2 (this super-tile's, or the next one's first passes)
+      if (pp + 2 < npass) prefetch(cur, pp + 2, buf == 0 ? 2 : buf - 1);
+      else prefetch(nxt, pp + 2 - npass, buf == 0 ? 2 : buf - 1);
       cp_async_wait2();  // this lane's slot of the current pass has landed
       uint4 v[4];
 #pragma unroll
@@ -805,13 +830,12 @@ __global__ void __launch_bounds__(kK1Threads, 6) search_bf16_kernel(MaskArgs p0,
         }
       }
 
-      const uint32_t grow0 = 128 * cur.tr + 32 * wa + 4 * br, gcol0 = 128 * cur.tc + 32 * pass + 8 * g;
+      const int tile = pp >> 2, pass = pp & 3;
+      const uint32_t grow0 = 128 * cur.tr + 32 * wa + 4 * br, gcol0 = 128 * cur.tc0 + 32 * pp + 8 * g;
       idx_acc = (idx_acc >> 16) | (static_cast<uint64_t>(pat[0] | (pat[1] << 8)) << 48);
-      const uint32_t n0 = S.nib[pat[0]], n1 = S.nib[pat[1]];
+      const uint2 n0 = S.nib[pat[0]], n1 = S.nib[pat[1]];
       {  // fwd E: byte i of fb = row 4 br + i of the lane's 8 columns (block 0 | block 1 << 4)
-        uint32_t fb = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) fb |= (((n0 >> (4 * i)) & 0xFu) | (((n1 >> (4 * i)) & 0xFu) << 4)) << (8 * i);
+        const uint32_t fb = n0.x | (n1.x << 4);
         // lane -> line (m & 7, kpar, m >> 4): rows m, m + 8 x column groups 2 kpar, 2 kpar + 1
         const int m7 = lane & 7, kp = (lane >> 3) & 1, mhi = lane >> 4;
         const int br0 = 4 * mhi + (m7 >> 2), i = m7 & 3;
@@ -825,20 +849,13 @@ __global__ void __launch_bounds__(kK1Threads, 6) search_bf16_kernel(MaskArgs p0,
         f3 = (lo & 0xFFFFu) | (hi << 16);
       }
       if (p.bwd_e) {
-        // column nibble k of the lane's 8 columns (block b = k / 4)
-        const uint32_t mine = (n0 >> 16) | (n1 & 0xFFFF0000u);
-        // lane -> W^T rows mp = 32 pass + 16 mhi + k (h = 0) and mp + 8 (h = 1); block-row pairs
-        // (4 q2, 4 q2 + 1) -> byte 0 and (4 q2 + 2, 4 q2 + 3) -> byte 1 of each halfword
-        const int k = lane & 7, mhi = (lane >> 3) & 1, q2 = lane >> 4;
-        uint32_t word = 0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int bb = 0; bb < 4; ++bb) {
-            const uint32_t x = __shfl_sync(0xFFFFFFFFu, mine, 4 * (4 * q2 + bb) + 2 * mhi + h);
-            word |= ((x >> (4 * k)) & 0xFu) << (16 * h + 4 * bb);
-          }
-        S.be[tslot][(k + 16 * (2 * pass + mhi) + 8 * q2) * 4 + wa] = word;
+        // the lane's 8 column nibbles (block 0: columns 0-3, block 1: 4-7) are one row of an 8 x 8
+        // nibble matrix per (q2, mhi) group; lane (q2, mhi, k) needs column k: nibble 4 h + bb =
+        // column nibble k of block row 4 q2 + bb, column group 2 mhi + h
+        const uint32_t mine = n0.y | (n1.y << 16);
+        const uint32_t word = nibble_transpose8(__shfl_sync(0xFFFFFFFFu, mine, tsrc), tk);
+        // nibble j of word = source row j = (bb = j & 3, h = j >> 2) -> bits 16 h + 4 bb: as stored
+        S.be[sslot][tile][(tk + 16 * (2 * pass + tmhi) + 8 * tq2) * 4 + wa] = word;
       }
       uint32_t fw[4][2];
 #pragma unroll
@@ -869,41 +886,56 @@ __global__ void __launch_bounds__(kK1Threads, 6) search_bf16_kernel(MaskArgs p0,
         for (int i = 0; i < 4; ++i)
           *reinterpret_cast<uint2*>(fv + static_cast<uint64_t>(i) * (cols >> 1)) = make_uint2(fw[i][0], fw[i][1]);
       }
+      if (pass == 3) {  // ---- per tile: fwd E lines, idx ----
+        const uint32_t tr = cur.tr, tc = cur.tc0 + tile;
+        if (p.fwd_e) {
+          const int L = (lane & 7) + 8 * ((lane >> 3) & 1) + 16 * (2 * wa + (lane >> 4));
+          *reinterpret_cast<uint4*>(p.fwd_e + (static_cast<uint64_t>(tr) * (cols >> 7) + tc) * 2048 + L * 16) =
+              make_uint4(f0, f1, f2, f3);
+        }
+        if (p.idx_out) {
+          // lane (br, g) stores block columns 8 g .. 8 g + 7 of its block row: pass g's chunks of lanes (br, 0..3)
+          uint32_t part[4];
+#pragma unroll
+          for (int gg = 0; gg < 4; ++gg) {
+            const uint64_t x = __shfl_sync(0xFFFFFFFFu, idx_acc, 4 * br + gg);
+            part[gg] = static_cast<uint32_t>(x >> (16 * g)) & 0xFFFFu;
+          }
+          const uint32_t brow = 32 * tr + 8 * wa + br;
+          *reinterpret_cast<uint2*>(p.idx_out + static_cast<uint64_t>(brow) * (cols >> 2) + 32 * tc + 8 * g) =
+              make_uint2(part[0] | (part[1] << 16), part[2] | (part[3] << 16));
+        }
+      }
       buf = buf == kK1Depth - 1 ? 0 : buf + 1;
     }
-    // ---- per tile: fwd E lines, idx, bwd E tile ----
-    const uint32_t tr = cur.tr, tc = cur.tc;
-    if (p.fwd_e) {
-      const int L = (lane & 7) + 8 * ((lane >> 3) & 1) + 16 * (2 * wa + (lane >> 4));
-      *reinterpret_cast<uint4*>(p.fwd_e + (static_cast<uint64_t>(tr) * (cols >> 7) + tc) * 2048 + L * 16) =
-          make_uint4(f0, f1, f2, f3);
+    // ---- per super-tile: the bwd E tiles ----
+    __syncthreads();  // the super-tile's bwd E words from all four warps are staged
+    if (p.bwd_e) {
+      for (int tl = 0; tl < cur.ntile; ++tl)
+        reinterpret_cast<uint4*>(p.bwd_e + (static_cast<uint64_t>(cur.tc0 + tl) * (rows >> 7) + cur.tr) * 2048)[tid] =
+            reinterpret_cast<const uint4*>(S.be[sslot][tl])[tid];
     }
-    if (p.idx_out) {
-      // lane (br, g) stores block columns 8 g .. 8 g + 7 of its block row: pass g's chunks of lanes (br, 0..3)
-      uint32_t part[4];
-#pragma unroll
-      for (int gg = 0; gg < 4; ++gg) {
-        const uint64_t x = __shfl_sync(0xFFFFFFFFu, idx_acc, 4 * br + gg);
-        part[gg] = static_cast<uint32_t>(x >> (16 * g)) & 0xFFFFu;
-      }
-      const uint32_t brow = 32 * tr + 8 * wa + br;
-      *reinterpret_cast<uint2*>(p.idx_out + static_cast<uint64_t>(brow) * (cols >> 2) + 32 * tc + 8 * g) =
-          make_uint2(part[0] | (part[1] << 16), part[2] | (part[3] << 16));
-    }
-    __syncthreads();  // the tile's bwd E words from all four warps are in S.be[tslot]
-    if (p.bwd_e)
-      reinterpret_cast<uint4*>(p.bwd_e + (static_cast<uint64_t>(tc) * (rows >> 7) + tr) * 2048)[tid] =
-          reinterpret_cast<const uint4*>(S.be[tslot])[tid];
-    tslot ^= 1;
+    sslot ^= 1;
     t += gridDim.x;
     cur = nxt;
-    nxt = k1_pos(t + gridDim.x, tiles0, total, tx0, tx1);
+    nxt = k1_pos(t + gridDim.x, st0, total, sx0, sx1, pair0, pair1);
   }
 }
 
-// persistent grid: six 4-warp CTAs per SM (the kernel's register footprint)
+// persistent grid: S24_K1_MINB 4-warp CTAs per SM (the kernel's register footprint)
+// super-tiles: pairs of horizontally adjacent 128 x 128 tiles (one barrier per 8 passes) when the
+// launch has many tiles per CTA and the weight an even number of tile columns, else single tiles
+// (small weights need every CTA: C2's 512 tiles run as 512 CTAs)
+static int64_t k1_super_tiles(int64_t rows, int64_t cols, bool pair) {
+  const int64_t tx = cols / kTile;
+  return (rows / kTile) * (pair ? tx / 2 : tx);
+}
+static bool k1_pairable(int64_t cols, int64_t tiles_total) {
+  return (cols / kTile) % 2 == 0 && tiles_total >= 4LL * S24_K1_MINB * 148;
+}
+
 static int k1_grid(long long tiles) {
-  const long long total = tiles;  // one tile per CTA at a time
+  const long long total = tiles;  // one super-tile per CTA at a time
   static int sms[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -914,7 +946,7 @@ static int k1_grid(long long tiles) {
     cudaFuncSetAttribute(search_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kK1SmemBytes);
     sms[dev] = n > 0 ? n : 148;
   }
-  return static_cast<int>(total < 6 * sms[dev] ? total : 6 * sms[dev]);
+  return static_cast<int>(total < S24_K1_MINB * sms[dev] ? total : S24_K1_MINB * sms[dev]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1055,8 +1087,9 @@ static int launch_mask(const MaskArgs& a, int dtype, bool search, cudaStream_t s
   if (search) {
     if (dtype == S24_BF16 && aligned) {
       if (a.rows * a.cols < (int64_t(1) << 32)) {
-        const uint32_t tiles = static_cast<uint32_t>(grid.x * grid.y);
-        search_bf16_kernel<<<k1_grid(tiles), kK1Threads, kK1SmemBytes, st>>>(a, a, tiles, tiles);
+        const bool pr = k1_pairable(a.cols, (a.rows / kTile) * (a.cols / kTile));
+        const uint32_t nst = static_cast<uint32_t>(k1_super_tiles(a.rows, a.cols, pr));
+        search_bf16_kernel<<<k1_grid(nst), kK1Threads, kK1SmemBytes, st>>>(a, a, nst, nst, pr ? 3 : 0);
         return s24_check_launch("mask_search");
       }
       mask_tile_kernel<S24_BF16, true, false><<<grid, kThreads, 0, st>>>(a);
@@ -1176,8 +1209,11 @@ extern "C" int s24_search_compress_pair(const void* w0, const void* w1, int dtyp
     if (int rc = launch_mask(a0, dtype, true, st)) return rc;
     return launch_mask(a1, dtype, true, st);
   }
-  search_bf16_kernel<<<k1_grid(t0 + t1), kK1Threads, kK1SmemBytes, st>>>(a0, a1, static_cast<uint32_t>(t0),
-                                                                         static_cast<uint32_t>(t0 + t1));
+  const bool pr0 = k1_pairable(cols0, t0 + t1), pr1 = k1_pairable(cols1, t0 + t1);
+  const uint32_t s0 = static_cast<uint32_t>(k1_super_tiles(rows0, cols0, pr0));
+  const uint32_t s1 = static_cast<uint32_t>(k1_super_tiles(rows1, cols1, pr1));
+  search_bf16_kernel<<<k1_grid(s0 + s1), kK1Threads, kK1SmemBytes, st>>>(a0, a1, s0, s0 + s1,
+                                                                         (pr0 ? 1 : 0) | (pr1 ? 2 : 0));
   return s24_check_launch("search_compress_pair");
 }
 
