@@ -243,8 +243,10 @@ int s24_gemm_dw(const uint16_t* a, int a_mn, int64_t lda, const uint16_t* b, int
  * (128-bit values split hi/lo).  Outputs the kept values g/pi (f x n/2 bf16) and
  * E tiles of the f x n operand; `pairs` (optional, f x n/4) gets each group's kept
  * pair index 0..5 (MVUE_PAIRS order).  gate_ff > 0: feature p of G is row
- * gate_row(p) of [u; v] for the random-stream index.  exact = 1: float64 math and
- * numpy's PCG64 stream, bit-identical to the reference draw; exact = 0: the same
+ * gate_row(p) of [u; v] for the random-stream index.  exact = 1: numpy's PCG64 stream and the
+ * reference's float64 decisions, bit-identical to the reference draw (each group in fp32 under a
+ * rigorous error certificate, in float64 where the certificate fails; exact = 2 forces float64
+ * for every group -- a test hook); exact = 0: the same
  * estimator in fp32 with a counter-based uniform (unbiased, throughput mode).
  * n, f % 128 == 0. */
 int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int64_t f, uint64_t state_hi, uint64_t state_lo,

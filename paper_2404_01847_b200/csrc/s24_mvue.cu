@@ -44,6 +44,8 @@ struct MvueRng {
   U128 inc;         // increment (odd)
   U128 mult[40];    // MULT^(2^i)
   U128 plus[40];    // additive term of 2^i steps
+  U128 rowm[7];     // multiplier of (groups per feature row) * 2^i steps (K8 tile kernel)
+  U128 rowp[7];     // additive term of the same
 };
 
 constexpr uint64_t kPcgMultHi = 0x2360ED051FC65DA4ull, kPcgMultLo = 0x4385DF649FCCF645ull;
@@ -58,14 +60,50 @@ __device__ __forceinline__ U128 pcg_advance(const MvueRng& rng, uint64_t delta) 
   }
   return add128(mul128(am, rng.state), ap);
 }
-// one numpy Generator.random(): step, XSL-RR output, 53-bit double
-__device__ __forceinline__ double pcg_uniform(U128& st, const U128& inc) {
+// the LCG's k-step maps x -> M x + P all commute; composition and application
+__device__ __forceinline__ void affine_compose(U128& m, U128& p, const U128& m2, const U128& p2) {
+  p = add128(mul128(p, m2), p2);
+  m = mul128(m, m2);
+}
+__device__ __forceinline__ U128 affine_apply(const U128& m, const U128& p, const U128& x) {
+  return add128(mul128(m, x), p);
+}
+__device__ __forceinline__ U128 shfl_xor128(const U128& v, int off) {
+  U128 r;
+  r.hi = __shfl_xor_sync(0xFFFFFFFFu, v.hi, off);
+  r.lo = __shfl_xor_sync(0xFFFFFFFFu, v.lo, off);
+  return r;
+}
+// PCG64 state `delta` steps after rng.state, computed by a whole warp (delta < 2^40): lane l
+// holds the maps of bits l and l + 32, a butterfly composes them (every lane ends with the map)
+__device__ __forceinline__ U128 pcg_advance_warp(const MvueRng& rng, uint64_t delta, int lane) {
+  U128 m{0, 1}, p{0, 0};
+  if ((delta >> lane) & 1) {
+    m = rng.mult[lane];
+    p = rng.plus[lane];
+  }
+  if (lane < 8 && ((delta >> (lane + 32)) & 1)) affine_compose(m, p, rng.mult[lane + 32], rng.plus[lane + 32]);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const U128 m2 = shfl_xor128(m, off), p2 = shfl_xor128(p, off);
+    affine_compose(m, p, m2, p2);
+  }
+  return affine_apply(m, p, rng.state);
+}
+
+// one PCG64 step and its XSL-RR 64-bit output
+__device__ __forceinline__ uint64_t pcg_next64(U128& st, const U128& inc) {
   st = add128(mul128(st, U128{kPcgMultHi, kPcgMultLo}), inc);
   const uint64_t x = st.hi ^ st.lo;
   const unsigned rot = static_cast<unsigned>(st.hi >> 58);
-  const uint64_t out = (x >> rot) | (x << ((64u - rot) & 63u));
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+// numpy Generator.random() of that output: (out >> 11) * 2^-53, exactly
+__device__ __forceinline__ double pcg_double(uint64_t out) {
   return __dmul_rn(static_cast<double>(out >> 11), 1.0 / 9007199254740992.0);
 }
+// one numpy Generator.random(): step, XSL-RR output, 53-bit double
+__device__ __forceinline__ double pcg_uniform(U128& st, const U128& inc) { return pcg_double(pcg_next64(st, inc)); }
 
 // exact reference arithmetic helpers (no contraction)
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -144,6 +182,105 @@ __device__ __forceinline__ int mvue_group(const double (&g)[4], double u, double
   return idx;
 }
 
+// The exact estimator's common case in fp32 with a certificate.  When the group's nonzero
+// magnitudes span at most 14 binades, every sum of them (total, rest) is exact in fp32 (bf16
+// significands: the sum is an integer < 2^24 times the smallest binade's unit), so the clamp test
+// amax > rest is the reference's.  The inclusion probabilities n / d (n = 2 a or a) are then
+// within 2 ulp(1) of the reference's float64 quotients (reciprocal and product roundings), and
+// the greedy pair fill and cumulative sums add their operands' bounds step by step -- at most
+// 968 ulp(1) between c_j and the draw (the bound propagation in DESIGN.md), so a decision
+// c_j <= draw whose fp32 margin exceeds 2^-14 (1024 ulp(1)) is the reference's decision.  The
+// kept VALUES need no division: pi_k is proportional to |g_k| (2 |g_k| / total, or |g_k| / rest
+// when clamped), so the reference's g_k / pi_k is sign(g_k) total / 2 (resp. sign(g_k) rest) up
+// to two float64 roundings (2^-52 relative), which its f32 conversion removes because that
+// magnitude is an (exact) f32 number; the clamped maximum (pi = 1) and the single nonzero of a
+// group keep g itself, zeros keep +-0.  Anything uncertain (span, margins, extreme magnitudes)
+// sets ok = false and the caller reruns the group in float64 (mvue_group_slow): bit-exact by
+// construction.
+__device__ __forceinline__ int mvue_group_cert(const float (&g)[4], uint64_t out, uint32_t& packed, bool& ok) {
+  const float a0 = fabsf(g[0]), a1 = fabsf(g[1]), a2 = fabsf(g[2]), a3 = fabsf(g[3]);
+  const float total = __fadd_rn(__fadd_rn(__fadd_rn(a0, a1), a2), a3);
+  int fm = 0;
+  float amax = a0;
+  if (a1 > amax) { fm = 1; amax = a1; }
+  if (a2 > amax) { fm = 2; amax = a2; }
+  if (a3 > amax) { fm = 3; amax = a3; }
+  const float b0 = fm == 0 ? 0.0f : a0, b1 = fm == 1 ? 0.0f : a1, b2 = fm == 2 ? 0.0f : a2, b3 = fm == 3 ? 0.0f : a3;
+  const float rest = __fadd_rn(__fadd_rn(__fadd_rn(b0, b1), b2), b3);
+  const int nnz = (a0 != 0.0f) + (a1 != 0.0f) + (a2 != 0.0f) + (a3 != 0.0f);
+  const float amin = fminf(fminf(a0 == 0.0f ? amax : a0, a1 == 0.0f ? amax : a1),
+                           fminf(a2 == 0.0f ? amax : a2, a3 == 0.0f ? amax : a3));
+  // exact sums: binade span <= 14 over the nonzero magnitudes, all normal and far from overflow
+  const int span = static_cast<int>(__float_as_uint(amax) >> 23) - static_cast<int>(__float_as_uint(amin) >> 23);
+  ok = nnz == 0 || (span <= 14 && amin >= 1.0e-30f && total <= 1.0e30f);  // total: also NaN / inf
+  const bool clamp = amax > rest;
+  const float inv = __frcp_rn(clamp ? rest : total);
+  float pi[4];
+  const float ak[4] = {a0, a1, a2, a3};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    pi[k] = clamp ? (k == fm ? 1.0f : __fmul_rn(ak[k], inv)) : __fmul_rn(2.0f * ak[k], inv);
+    if (nnz == 1) pi[k] = ak[k] > 0.0f ? 1.0f : (1.0f / 3.0f);
+    if (nnz == 0) pi[k] = 0.5f;
+  }
+  float r0 = pi[0], r1 = pi[1], r2 = pi[2], r3 = pi[3];
+  float s = 0.5f * __fadd_rn(__fadd_rn(__fadd_rn(pi[0], pi[1]), pi[2]), pi[3]);
+  const float p01 = fmaxf(fminf(fminf(fminf(r0, r1), __fsub_rn(s, r2)), __fsub_rn(s, r3)), 0.0f);
+  r0 = __fsub_rn(r0, p01);
+  r1 = __fsub_rn(r1, p01);
+  s = __fsub_rn(s, p01);
+  const float p02 = fmaxf(fminf(fminf(r0, r2), __fsub_rn(s, r3)), 0.0f);
+  r0 = __fsub_rn(r0, p02);
+  r2 = __fsub_rn(r2, p02);
+  s = __fsub_rn(s, p02);
+  const float p03 = fmaxf(fminf(r0, r3), 0.0f);
+  r3 = __fsub_rn(r3, p03);
+  s = __fsub_rn(s, p03);
+  const float p12 = fmaxf(fminf(fminf(r1, r2), __fsub_rn(s, r3)), 0.0f);
+  r1 = __fsub_rn(r1, p12);
+  r2 = __fsub_rn(r2, p12);
+  const float p13 = fmaxf(fminf(r1, r3), 0.0f);
+  r3 = __fsub_rn(r3, p13);
+  const float p23 = fmaxf(fminf(r2, r3), 0.0f);
+  const float c0 = p01, c1 = __fadd_rn(c0, p02), c2 = __fadd_rn(c1, p03), c3 = __fadd_rn(c2, p12),
+              c4 = __fadd_rn(c3, p13), c5 = __fadd_rn(c4, p23);
+  // the uniform's top 24 bits: within 2^-24 of the reference's 53-bit double (no float64 ops)
+  const float uf = __uint2float_rn(static_cast<uint32_t>(out >> 40)) * 5.9604644775390625e-8f;  // 2^-24
+  const float draw = __fmul_rn(uf, c5);
+  constexpr float kMargin = 6.103515625e-5f;  // 2^-14 = 1024 ulp(1) > the 968 ulp(1) bound
+  ok = ok && fabsf(c0 - draw) > kMargin && fabsf(c1 - draw) > kMargin && fabsf(c2 - draw) > kMargin &&
+       fabsf(c3 - draw) > kMargin && fabsf(c4 - draw) > kMargin && fabsf(c5 - draw) > kMargin;
+  const int idx = min((c0 <= draw) + (c1 <= draw) + (c2 <= draw) + (c3 <= draw) + (c4 <= draw) + (c5 <= draw), 5);
+  const int i0 = idx < 3 ? 0 : (idx < 5 ? 1 : 2);
+  const int i1 = idx == 0 ? 1 : (idx == 1 || idx == 3) ? 2 : 3;
+  const float g0 = i0 == 0 ? g[0] : (i0 == 1 ? g[1] : g[2]);
+  const float g1 = i1 == 1 ? g[1] : (i1 == 2 ? g[2] : g[3]);
+  // nnz >= 2: a kept element has pi > 0 (its pair probability is positive), so a != 0
+  if (nnz >= 2) ok = ok && g0 != 0.0f && g1 != 0.0f;
+  const float m = clamp ? rest : 0.5f * total;  // kept magnitude when pi = 2 a / total or a / rest
+  float v0 = g0, v1 = g1;  // nnz == 1: the nonzero keeps g (pi = 1), zeros keep +-0; nnz == 0: +-0
+  if (nnz >= 2) {
+    v0 = (clamp && i0 == fm) ? g0 : copysignf(m, g0);
+    v1 = (clamp && i1 == fm) ? g1 : copysignf(m, g1);
+  }
+  packed = static_cast<uint32_t>(f32_to_bf16(v0)) | (static_cast<uint32_t>(f32_to_bf16(v1)) << 16);
+  return idx;
+}
+
+// the float64 reference computation of one group, out of line (the rare uncertain groups)
+__device__ __noinline__ int mvue_group_slow(const float (&g)[4], uint64_t out, uint32_t& packed) {
+  const double u = pcg_double(out);
+  double gv[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) gv[k] = static_cast<double>(g[k]);
+  double v0, v1;
+  const int idx = mvue_group(gv, u, v0, v1);
+  // f64 -> f32 -> bf16 (the rounding of the reference-side bf16 operand)
+  packed = static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v0))) |
+           (static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v1))) << 16);
+  return idx;
+}
+
 // Throughput mode: the same estimator in fp32 (inclusion probabilities, greedy
 // pair fill, cumulative draw, g / pi) with a counter-based uniform per group.
 // Unbiased like the reference (E[value] = g) but not bit-identical to numpy's
@@ -209,6 +346,7 @@ struct MvueArgs {
   uint16_t* vals;     // f x n/2
   uint8_t* e;         // E tiles [f/128][n/128]
   uint8_t* pairs;     // optional f x n/4 pair indices (tests)
+  int force_f64;      // exact mode 2 (tests): every group through the float64 path, no certificate
 };
 
 template <bool kExact>
@@ -242,51 +380,101 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
   const int64_t grp0 = t0 / 4 + 16 * half;
   const uint64_t stream0 = static_cast<uint64_t>(row * (p.n / 4) + grp0);
   U128 st{0, 0};
-  if constexpr (kExact) st = pcg_advance(rng, stream0);
+  if constexpr (kExact) {
+    // stream index of this thread = base(u / v rows) + roff * (n / 4) + 16 half: the CTA's one or
+    // two base states by a warp each (pcg_advance_warp), then at most 7 + 1 table steps per thread
+    // instead of a full 40-bit jump-ahead
+    __shared__ U128 s_base[2];
+    const int w = tid >> 5, lane = tid & 31;
+    const int nbase = p.gate_ff > 0 ? 2 : 1;
+    const int64_t rbase0 = p.gate_ff > 0 ? f0 / 2 : f0;
+    if (w < nbase) {
+      const int64_t rb = rbase0 + (w ? p.gate_ff : 0);
+      const U128 b = pcg_advance_warp(rng, static_cast<uint64_t>(rb * (p.n / 4) + t0 / 4), lane);
+      if (lane == 0) s_base[w] = b;
+    }
+    __syncthreads();
+    const int sel = p.gate_ff > 0 ? ((ml >> 4) & 1) : 0;
+    const int roff = p.gate_ff > 0 ? 16 * (ml >> 5) + (ml & 15) : ml;
+    st = s_base[sel];
+#pragma unroll
+    for (int i = 0; i < 7; ++i)
+      if ((roff >> i) & 1) st = affine_apply(rng.rowm[i], rng.rowp[i], st);
+    if (half) st = affine_apply(rng.mult[4], rng.plus[4], st);  // 16 groups
+  }
   uint32_t halfwords[4] = {0, 0, 0, 0};
-  uint32_t packed[16];
   uint32_t pidx[4] = {0, 0, 0, 0};
+  const uint32_t* s_out;  // [feature][32 words + 1 pad] kept-value pairs of the tile
+  if constexpr (kExact) {
+    // four passes of four groups: a fully unrolled 16-group body with the certificate and the
+    // float64 fallback call overflows the instruction cache (measured: "no instruction" stalls
+    // dominated); values go straight to their own staging area
+    extern __shared__ uint32_t s_pk[];  // 128 x 33 words (dynamic: the static tile already uses 36 KB)
+#pragma unroll 1
+    for (int jj = 0; jj < 4; ++jj) {
+      uint32_t hw = 0, pw = 0;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    int idx;
-    if constexpr (kExact) {
-      double gv[4];
+      for (int q = 0; q < 4; ++q) {
+        const int j = 4 * jj + q;
+        float gv[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) gv[k] = static_cast<double>(bf16_to_f32(s_g[(64 * half + 4 * j + k) * 136 + ml]));
-      const double u = pcg_uniform(st, rng.inc);
-      double v0, v1;
-      idx = mvue_group(gv, u, v0, v1);
-      // f64 -> f32 -> bf16 (the rounding of the reference-side bf16 operand)
-      packed[j] = static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v0))) |
-                  (static_cast<uint32_t>(f32_to_bf16(__double2float_rn(v1))) << 16);
-    } else {
+        for (int k = 0; k < 4; ++k) gv[k] = bf16_to_f32(s_g[(64 * half + 4 * j + k) * 136 + ml]);
+        const uint64_t out = pcg_next64(st, rng.inc);
+        bool ok;
+        uint32_t pk;
+        int idx = mvue_group_cert(gv, out, pk, ok);
+#ifndef S24_MVUE_DEBUG
+        if (!ok || p.force_f64) idx = mvue_group_slow(gv, out, pk);
+#endif
+        s_pk[ml * 33 + 16 * half + j] = pk;
+        // nibble i0 | i1 << 2 of pair idx = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE}[idx]
+        hw |= ((0xED9C84u >> (4 * idx)) & 0xFu) << (4 * q);
+        pw |= static_cast<uint32_t>(idx) << (8 * q);
+      }
+      halfwords[0] = halfwords[1];
+      halfwords[1] = halfwords[2];
+      halfwords[2] = halfwords[3];
+      halfwords[3] = hw;
+      pidx[0] = pidx[1];
+      pidx[1] = pidx[2];
+      pidx[2] = pidx[3];
+      pidx[3] = pw;
+    }
+    __syncthreads();
+    s_out = s_pk;
+  } else {
+    uint32_t packed[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
       float gv[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) gv[k] = bf16_to_f32(s_g[(64 * half + 4 * j + k) * 136 + ml]);
       float f0, f1;
       const uint32_t k1 = static_cast<uint32_t>(rng.state.lo ^ (rng.state.lo >> 32)),
                      k2 = static_cast<uint32_t>(rng.inc.hi ^ (rng.inc.hi >> 32));
-      idx = static_cast<int>(mvue_nibble_f32(gv, counter_uniform(k1, k2, static_cast<uint32_t>(stream0 + j)), f0, f1));
+      const int idx =
+          static_cast<int>(mvue_nibble_f32(gv, counter_uniform(k1, k2, static_cast<uint32_t>(stream0 + j)), f0, f1));
       packed[j] = pack_bf16x2(f0, f1);
+      // nibble i0 | i1 << 2 of pair idx = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE}[idx]
+      const uint32_t nib = (0xED9C84u >> (4 * idx)) & 0xFu;
+      halfwords[j >> 2] |= nib << (4 * (j & 3));
+      pidx[j >> 2] |= static_cast<uint32_t>(idx) << (8 * (j & 3));
     }
-    // nibble i0 | i1 << 2 of pair idx = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE}[idx]
-    const uint32_t nib = (0xED9C84u >> (4 * idx)) & 0xFu;
-    halfwords[j >> 2] |= nib << (4 * (j & 3));
-    pidx[j >> 2] |= static_cast<uint32_t>(idx) << (8 * (j & 3));
+    // kept values staged in the (now free) input tile, then streamed as whole 128-byte rows
+    __syncthreads();
+    uint32_t* s_v = reinterpret_cast<uint32_t*>(s_g);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s_v[ml * 33 + 16 * half + j] = packed[j];
+    __syncthreads();
+    s_out = s_v;
   }
   if (p.pairs) {
     uint4* dp = reinterpret_cast<uint4*>(p.pairs + feat * (p.n / 4) + grp0);
     *dp = make_uint4(pidx[0], pidx[1], pidx[2], pidx[3]);
   }
-  // kept values staged in the (now free) input tile, then streamed as whole 128-byte rows
-  __syncthreads();
-  uint32_t* s_v = reinterpret_cast<uint32_t*>(s_g);  // [feature][32 words + 1 pad]
-#pragma unroll
-  for (int j = 0; j < 16; ++j) s_v[ml * 33 + 16 * half + j] = packed[j];
-  __syncthreads();
   for (int rr = tid >> 5; rr < 128; rr += 8) {
     const int lane = tid & 31;
-    reinterpret_cast<uint32_t*>(p.vals + (f0 + rr) * (p.n / 2) + t0 / 2)[lane] = s_v[rr * 33 + lane];
+    reinterpret_cast<uint32_t*>(p.vals + (f0 + rr) * (p.n / 2) + t0 / 2)[lane] = s_out[rr * 33 + lane];
   }
   // metadata: halfword w covers tokens 64 half + 16 w .. +15 of row ml
   if (p.e) {
@@ -356,7 +544,8 @@ __global__ void __launch_bounds__(256) mvue_prune_kernel(const T* __restrict__ g
   }
 }
 
-static void mvue_rng_tables(MvueRng& rng, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo) {
+static void mvue_rng_tables(MvueRng& rng, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                            uint64_t row_groups = 0) {
   rng.state = U128{state_hi, state_lo};
   rng.inc = U128{inc_hi, inc_lo};
   unsigned __int128 m = (static_cast<unsigned __int128>(kPcgMultHi) << 64) | kPcgMultLo;
@@ -366,6 +555,21 @@ static void mvue_rng_tables(MvueRng& rng, uint64_t state_hi, uint64_t state_lo, 
     rng.plus[i] = U128{static_cast<uint64_t>(pl >> 64), static_cast<uint64_t>(pl)};
     pl = (m + 1) * pl;
     m = m * m;
+  }
+  // (row_groups * 2^i)-step maps: x -> M x + P composed from the 2^i tables, then squared
+  unsigned __int128 rm = 1, rp = 0;
+  for (int i = 0; i < 40; ++i)
+    if ((row_groups >> i) & 1) {
+      const unsigned __int128 mi = (static_cast<unsigned __int128>(rng.mult[i].hi) << 64) | rng.mult[i].lo;
+      const unsigned __int128 pi = (static_cast<unsigned __int128>(rng.plus[i].hi) << 64) | rng.plus[i].lo;
+      rp = rp * mi + pi;
+      rm = rm * mi;
+    }
+  for (int i = 0; i < 7; ++i) {
+    rng.rowm[i] = U128{static_cast<uint64_t>(rm >> 64), static_cast<uint64_t>(rm)};
+    rng.rowp[i] = U128{static_cast<uint64_t>(rp >> 64), static_cast<uint64_t>(rp)};
+    rp = rm * rp + rp;
+    rm = rm * rm;
   }
 }
 
@@ -412,14 +616,24 @@ extern "C" int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int6
               "gradient rows must be 16-byte aligned");
   if (gate_ff > 0) S24_REQUIRE(f == 2 * gate_ff && gate_ff % 16 == 0, S24_ERR_SHAPE, "gated MVUE: f must be 2 d_ff");
   MvueRng rng;
-  mvue_rng_tables(rng, state_hi, state_lo, inc_hi, inc_lo);
+  mvue_rng_tables(rng, state_hi, state_lo, inc_hi, inc_lo, static_cast<uint64_t>(n / 4));
   S24_REQUIRE(static_cast<double>(f) * static_cast<double>(n / 4) < 1099511627776.0, S24_ERR_SHAPE,
               "MVUE stream index exceeds the 2^40 jump table");
   S24_REQUIRE(exact || static_cast<double>(f) * static_cast<double>(n / 4) < 4294967296.0, S24_ERR_SHAPE,
               "fast MVUE: group counter exceeds 2^32 (use exact mode or split the call)");
-  MvueArgs a{g, ldg, n, f, gate_ff, vals, e, pairs};
+  MvueArgs a{g, ldg, n, f, gate_ff, vals, e, pairs, exact == 2 ? 1 : 0};
   dim3 grid(static_cast<unsigned>(n / 128), static_cast<unsigned>(f / 128));
-  if (exact) mvue_tile_kernel<true><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, rng);
+  if (exact) {
+    constexpr int kPkBytes = 128 * 33 * 4;
+    static bool attr[64] = {false};  // per device: the opt-in belongs to the kernel, not to the call
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
+      cudaFuncSetAttribute(mvue_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPkBytes);
+      if (dev >= 0 && dev < 64) attr[dev] = true;
+    }
+    mvue_tile_kernel<true><<<grid, 256, kPkBytes, static_cast<cudaStream_t>(stream)>>>(a, rng);
+  }
   else mvue_tile_kernel<false><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, rng);
   return s24_check_launch("mvue_compress");
 }

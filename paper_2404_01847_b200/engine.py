@@ -229,7 +229,9 @@ def pcg64_state(seed: int) -> tuple[int, int, int, int]:
 def mvue_compress(g: torch.Tensor, seed: int, gate_ff: int = 0, want_pairs: bool = False, exact: bool = True):
     """K8: MVUE-sparsify g^T (features x tokens) along tokens (sparsity.py:401-413)
     into the tensor-core operand.  g: token-major (N x F) bf16.  Returns
-    (vals F x N/2, E tiles, pairs F x N/4 or None).  exact=False: fp32 math and a
+    (vals F x N/2, E tiles, pairs F x N/4 or None).  exact=True: numpy's PCG64 stream and the
+    reference's float64 decisions (fp32 under an error certificate, float64 where the certificate
+    fails; exact=2 forces float64 everywhere, a test hook).  exact=False: fp32 math and a
     counter-based uniform (unbiased, not numpy's stream) for throughput."""
     n, f = g.shape
     dev = g.device

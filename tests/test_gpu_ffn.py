@@ -409,3 +409,57 @@ def test_dx_accumulate_into_residual_gradient(d, d_ff, n):
     with pytest.raises(RuntimeError):
         C.call("s24_spmm", op_in.bwd_vals.data_ptr(), op_in.bwd_e.data_ptr(), d, d_ff, st.a.data_ptr(), 0, d_ff,
                n, dh.data_ptr(), n, None, C.EPI_STORE_ADD, None, 0, None, None, 0, 0, None, 0, C.stream_of(dh))
+
+
+def _mvue_corpus(f, n, kind, seed):
+    """features x tokens bf16-valued corpora for the certificate: Gaussian, small integers (exact
+    ties, clamp boundaries amax == rest, rounding midpoints of g / pi), wide exponent spans."""
+    x = o.det_normal((f, n), seed=seed)
+    if kind == "ints":
+        x = np.floor(np.abs(x) * 1.7) * np.sign(x)  # {0, +-1, +-2, +-3, ...}
+    elif kind == "span":
+        sh = (o._splitmix64(f * n, seed + 11) % np.uint64(60)).astype(np.int64).reshape(f, n) - 30
+        x = x * np.exp2(sh.astype(np.float64))
+    elif kind == "pow2":
+        sh = (o._splitmix64(f * n, seed + 13) % np.uint64(4)).astype(np.int64).reshape(f, n)
+        x = np.sign(x) * np.exp2(sh.astype(np.float64)) * ((o._splitmix64(f * n, seed + 17) % np.uint64(3)) > 0
+                                                            ).reshape(f, n)
+    return o.round_bf16(x)
+
+
+@pytest.mark.parametrize("kind", ["normal", "ints", "span", "pow2"])
+@pytest.mark.parametrize("gate_ff", [0, 512])
+def test_mvue_certified_fast_path_equals_float64_path(kind, gate_ff):
+    """Exact mode's common case runs in fp32 under an error certificate and falls back to the
+    float64 reference computation when a decision is within the bound; exact=2 forces float64 for
+    every group.  Both must give identical kept pairs, values and metadata (2 M groups per corpus)."""
+    from paper_2404_01847_b200 import engine as E
+
+    f, n = 1024, 8192
+    x = _mvue_corpus(f, n, kind, seed=len(kind) * 7 + gate_ff)
+    g = to_dev_bf16(np.ascontiguousarray(x.T))
+    outs = [E.mvue_compress(g, 4242, gate_ff=gate_ff, want_pairs=True, exact=mode) for mode in (1, 2)]
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a.view(torch.uint8) if a.dtype != torch.uint8 else a,
+                           b.view(torch.uint8) if b.dtype != torch.uint8 else b)
+
+
+def test_mvue_gated_stream_bit_exact_vs_oracle():
+    """Gated operand (u / v rows interleaved in 16-row groups): feature p of G draws from the
+    stream of row gate_row(p) of [u; v] -- the per-CTA base states and row-table jumps."""
+    from paper_2404_01847_b200 import engine as E
+
+    ff, n, seed = 256, 512, 77
+    f = 2 * ff
+    x = _mvue_corpus(f, n, "normal", seed=5)  # interleaved feature order
+    rows = np.array([16 * (p // 32) + (p % 32) if p % 32 < 16 else ff + 16 * (p // 32) + (p % 32) - 16
+                     for p in range(f)])
+    xr = np.empty_like(x)
+    xr[rows] = x  # [u; v] order: row r holds feature p with gate_row(p) = r
+    g = to_dev_bf16(np.ascontiguousarray(x.T))
+    vals, e, pairs = E.mvue_compress(g, seed, gate_ff=ff, want_pairs=True)
+    rv, _, ridx = o.mvue_kept(xr.reshape(-1, 4), seed)
+    ridx = ridx.reshape(f, n // 4)[rows]
+    rv = rv.reshape(f, n // 2)[rows]
+    np.testing.assert_array_equal(pairs.cpu().numpy(), ridx)
+    np.testing.assert_array_equal(bf16_bits_of(vals), o.bf16_bits(o.round_bf16(rv)))
