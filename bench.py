@@ -825,7 +825,7 @@ def run_e2e(a, cfg, w_in, bias, w2, dev, world, dist):
 
     def fetch(slot):
         # 4 chunks: one 32 MB pinned copy reaches ~45 GB/s on the box's PCIe 5 x16 link, several
-        # back-to-back chunks ~52 GB/s (tools/exp_e2e.py)
+        # back-to-back chunks ~52 GB/s (tools/experiments/exp_e2e.py)
         with torch.cuda.stream(copy_stream):
             copy_stream.wait_event(free[slot])
             for c in range(4):

@@ -1,6 +1,6 @@
 """dW GEMM (dZ^T X, MN-major operands) at C3-like shapes for ncu DRAM/drift studies."""
 import os, sys
-sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..", "..")))
 import torch
 from paper_2404_01847_b200 import engine as E
 n = 32768

@@ -1,6 +1,6 @@
 """Diagnose the e2e loop: CPU time per step vs GPU time per step, and raw H2D copy rates."""
 import os, sys, time
-sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..", "..")))
 import torch
 import bench
 from paper_2404_01847_b200.module import SparseFFN

@@ -1,7 +1,7 @@
 """Isolated sparse / dense GEMMs at C3 shapes (for ncu per-clock efficiency studies).
-python tools/exp_gemm_iso.py [reps]"""
+python tools/experiments/exp_gemm_iso.py [reps]"""
 import os, sys
-sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..", "..")))
 import torch
 from paper_2404_01847_b200 import engine as E
 

@@ -1,10 +1,10 @@
 """Eager vs CUDA-graph step time and host enqueue time of the bench's sparse step.
-python tools/exp_graph.py [cfg]"""
+python tools/experiments/exp_graph.py [cfg]"""
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..", "..")))
 import torch
 
 import bench

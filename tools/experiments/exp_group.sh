@@ -6,7 +6,7 @@ for cfg in c3 c2; do
     for gd in 8 4 16; do
       if [ "$g" = "0" ]; then unset S24_GROUP_M; else export S24_GROUP_M=$g; fi
       export S24_GROUP_M_DW=$gd
-      timeout 300 python tools/exp_kernels.py $cfg 20
+      timeout 300 python tools/experiments/exp_kernels.py $cfg 20
     done
   done
 done > gpurun_out/exp_group.jsonl 2> gpurun_out/exp_group.err

@@ -1,7 +1,7 @@
 """Per-kernel times inside full steps (CUDA events on the launching stream).
-python tools/exp_kernels.py <cfg> [steps]  -- env knobs (S24_GROUP_M, ...) are read by the library."""
+python tools/experiments/exp_kernels.py <cfg> [steps]  -- env knobs (S24_GROUP_M, ...) are read by the library."""
 import json, os, sys
-sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..", "..")))
 import torch
 import bench
 from paper_2404_01847_b200 import engine as E

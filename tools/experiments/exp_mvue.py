@@ -1,6 +1,6 @@
 """Per-kernel times of the MVUE-dW step (fast / exact) at a config."""
 import json, os, sys
-sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..", "..")))
 import torch
 import bench
 from paper_2404_01847_b200 import engine as E
