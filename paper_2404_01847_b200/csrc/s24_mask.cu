@@ -567,7 +567,10 @@ __global__ void __launch_bounds__(kPruneThreads, 2) prune_bf16_kernel(MaskArgs p
 // integer search on one block given as 4 rows x 2 words (bf16 pairs).  Returns the pattern, or
 // -1 when the block needs the float64 reference-order path (exponent span > 13, tiny values) and
 // -2 when it holds inf / nan (the owner lane then runs the sequential reference loop itself)
-__device__ __forceinline__ int search_block_fast(const uint32_t (&wd)[8]) {
+// one = 1 from a kernel argument (opaque to the compiler): the products by `one` / `128 one` below
+// compile to IMAD, which issues on the FMA pipe, instead of IADD3 / LEA on the integer ALU pipe --
+// the search is ALU-pipe bound and the FMA pipe is mostly idle
+__device__ __forceinline__ int search_block_fast(const uint32_t (&wd)[8], int one) {
   uint32_t h[16];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
@@ -594,16 +597,18 @@ __device__ __forceinline__ int search_block_fast(const uint32_t (&wd)[8]) {
   // is pre-scaled by 128 for the tie-break bits: v = (bits - 0x4B400000) << 7
   const float scale = __uint_as_float(static_cast<uint32_t>(261 - emin) << 23);
   int v[16];
+  const int k128 = one << 7;
 #pragma unroll
   for (int i = 0; i < 16; ++i)
-    v[i] = static_cast<int>(__float_as_uint(__fmaf_rn(f[i], scale, 12582912.0f)) * 128u - (0x4B400000u << 7));
+    v[i] = static_cast<int>(__float_as_uint(__fmaf_rn(f[i], scale, 12582912.0f))) * k128 -
+           static_cast<int>(0x4B400000u << 7);
   constexpr int kLo[6] = S24_PAIR_LO;
   constexpr int kHi[6] = S24_PAIR_HI;
   int rp[4][6];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int q = 0; q < 6; ++q) rp[r][q] = v[4 * r + kLo[q]] + v[4 * r + kHi[q]];
+    for (int q = 0; q < 6; ++q) rp[r][q] = v[4 * r + kLo[q]] * one + v[4 * r + kHi[q]];
   return s24_search_tree(rp);
 }
 
@@ -730,7 +735,7 @@ __device__ __forceinline__ uint32_t nibble_transpose8(uint32_t x, int j) {
 
 __global__ void __launch_bounds__(kK1Threads, S24_K1_MINB) search_bf16_kernel(MaskArgs p0, MaskArgs p1,
                                                                                uint32_t st0, uint32_t total,
-                                                                               int pairs) {
+                                                                               int pairs, int one) {
   extern __shared__ __align__(16) uint8_t k1_raw[];
   K1Smem& S = *reinterpret_cast<K1Smem*>(k1_raw);
   const int tid = threadIdx.x, lane = tid & 31, wa = tid >> 5;  // warp = row strip of the tile
@@ -804,7 +809,7 @@ __global__ void __launch_bounds__(kK1Threads, S24_K1_MINB) search_bf16_kernel(Ma
           wd[2 * i] = (&v[i].x)[2 * b];
           wd[2 * i + 1] = (&v[i].x)[2 * b + 1];
         }
-        pat[b] = search_block_fast(wd);
+        pat[b] = search_block_fast(wd, one);
         if (pat[b] == -2) {  // inf / nan: the sequential reference loop (its own comparison semantics)
           double a[16];
           block_abs_f64(wd, a);
@@ -1089,7 +1094,7 @@ static int launch_mask(const MaskArgs& a, int dtype, bool search, cudaStream_t s
       if (a.rows * a.cols < (int64_t(1) << 32)) {
         const bool pr = k1_pairable(a.cols, (a.rows / kTile) * (a.cols / kTile));
         const uint32_t nst = static_cast<uint32_t>(k1_super_tiles(a.rows, a.cols, pr));
-        search_bf16_kernel<<<k1_grid(nst), kK1Threads, kK1SmemBytes, st>>>(a, a, nst, nst, pr ? 3 : 0);
+        search_bf16_kernel<<<k1_grid(nst), kK1Threads, kK1SmemBytes, st>>>(a, a, nst, nst, pr ? 3 : 0, 1);
         return s24_check_launch("mask_search");
       }
       mask_tile_kernel<S24_BF16, true, false><<<grid, kThreads, 0, st>>>(a);
@@ -1213,7 +1218,7 @@ extern "C" int s24_search_compress_pair(const void* w0, const void* w1, int dtyp
   const uint32_t s0 = static_cast<uint32_t>(k1_super_tiles(rows0, cols0, pr0));
   const uint32_t s1 = static_cast<uint32_t>(k1_super_tiles(rows1, cols1, pr1));
   search_bf16_kernel<<<k1_grid(s0 + s1), kK1Threads, kK1SmemBytes, st>>>(a0, a1, s0, s0 + s1,
-                                                                         (pr0 ? 1 : 0) | (pr1 ? 2 : 0));
+                                                                         (pr0 ? 1 : 0) | (pr1 ? 2 : 0), 1);
   return s24_check_launch("search_compress_pair");
 }
 
