@@ -610,17 +610,18 @@ def measure(a, cfg, cfg_name, dev, world, rank, local, pg, dist, full=True):
                           "k2_prune_compress": {"ms": k2_ms, "gbs": k2_bytes / (k2_ms * 1e-3) / 1e9,
                                                 "frac_of_hbm": k2_bytes / (k2_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}}
 
-    if full:
-        # ---- variant: MVUE-sparsified dW (the reference default fst_backward(mvue=True)) ----
-        variants = {}
-        for mode in ("fast", "exact"):
-            mstep = SparseStep(w_in, bias, w2, cfg["act"], world, pg, mvue=mode)
-            msteps = a.steps
-            mms, _ = time_loop(lambda: mstep(x, dy), msteps, a.warmup, dd)
-            variants[f"mvue_dw_{mode}"] = {"tokens_per_s": n_tok * world / (mms / msteps / 1000.0)}
-            del mstep
-        out["variants"] = variants
+    # ---- variant: MVUE-sparsified dW (the reference default fst_backward(mvue=True)), also on
+    # sub-lines ----
+    variants = {}
+    for mode in ("fast", "exact"):
+        mstep = SparseStep(w_in, bias, w2, cfg["act"], world, pg, mvue=mode)
+        msteps = a.steps
+        mms, _ = time_loop(lambda: mstep(x, dy), msteps, a.warmup, dd)
+        variants[f"mvue_dw_{mode}"] = {"tokens_per_s": n_tok * world / (mms / msteps / 1000.0)}
+        del mstep
+    out["variants"] = variants
 
+    if full:
         # ---- fused optimizer step (Adam + masked decay) on W_in, fp32 state ----
         from paper_2404_01847_b200.optim import DecayConfig, DecayMode, OptimizerState, adam_step
         from paper_2404_01847_b200.sparsity import TransposableMask
@@ -661,7 +662,7 @@ def measure(a, cfg, cfg_name, dev, world, rank, local, pg, dist, full=True):
     # ---- e2e through the public autograd module, host-resident inputs ----
     out["e2e"] = run_e2e(a, cfg, w_in, bias, w2, dev, world, dd)
 
-    if not a.no_dense and full and "variants" in out:
+    if not a.no_dense and "variants" in out:
         for v in out["variants"].values():
             v["speedup_vs_best_dense"] = v["tokens_per_s"] / dense_best
     del step, w_in, bias, w2, x, dy
@@ -766,7 +767,9 @@ def run_ours(a, cfg, cfg_name, subs):
                        **{k: r[k] for k in ("dense_tokens_per_s", "dense_fused_tokens_per_s",
                                             "dense_gemm_only_tokens_per_s", "speedup_vs_dense",
                                             "speedup_vs_dense_fused", "speedup_vs_dense_gemm_only",
-                                            "speedup_vs_best_dense") if k in r}}
+                                            "speedup_vs_best_dense") if k in r},
+                       "mvue_exact_tokens_per_s": r["variants"]["mvue_dw_exact"]["tokens_per_s"],
+                       "mvue_exact_speedup_vs_best_dense": r["variants"]["mvue_dw_exact"].get("speedup_vs_best_dense")}
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cpu = cpu_baseline_leg(cfg, a)
