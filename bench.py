@@ -290,8 +290,9 @@ class SparseStep:
         self.t = 0
         self.mvue = mvue
         # our kernel launches per step: K2 (both weights; K1 on the refresh step), fwd 2 sparse
-        # GEMMs, bwd 2 sparse + 2 dW GEMMs (+2 MVUE sparsifiers); activations fused into the GEMMs
-        self.launches_per_step = 1 + 2 + 4 + (2 if mvue else 0)
+        # GEMMs, bwd 2 sparse + 2 dW GEMMs (+2 MVUE sparsifiers and, on large shapes, the 2
+        # transposes of the token operands for the two-slab MVUE GEMMs); activations fused
+        self.launches_per_step = 1 + 2 + 4 + (4 if mvue else 0)
 
     def __call__(self, x, dy, fused_optimizer=False):
         E = self.E

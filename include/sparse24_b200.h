@@ -281,6 +281,12 @@ int s24_act_fwd(const uint16_t* z, int64_t ldz, int64_t r, int64_t n, int act, u
 int s24_act_bwd(const uint16_t* z, int64_t ldz, const uint16_t* da, int64_t ldda, int64_t r, int64_t n, int act,
                 uint16_t* dz, int64_t lddz, float* dbias, void* stream);
 
+/* dst (cols x rows, ld ldd) = src^T (rows x cols, ld lds), bf16: the K-major (token-contiguous)
+ * B operand of the two-slab MVUE weight-gradient GEMM (s24_spmm_dw with b_mn = 0).  rows, cols,
+ * lds, ldd divisible by 8, 16-byte aligned base pointers. */
+int s24_transpose_bf16(const uint16_t* src, int64_t rows, int64_t cols, int64_t lds, uint16_t* dst, int64_t ldd,
+                       void* stream);
+
 /* ---- fp32 mode (the reference's float32 fused type, _core.pyx:21-23; C1 is fp32) ----------
  * tf32 structured sparsity is 1:2 per 32-bit pair and cannot hold a transposable 2:4 mask, so
  * the fp32 mode runs every product as three bf16 2:4 products on split operands

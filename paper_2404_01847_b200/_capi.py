@@ -53,6 +53,7 @@ SIGNATURES = {
     "s24_spmm_dw": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _I, _P, _I, _P],
     "s24_act_fwd": [_P, _I64, _I64, _I64, _I, _P, _I64, _P],
     "s24_act_bwd": [_P, _I64, _P, _I64, _I64, _I64, _I, _P, _I64, _P, _P],
+    "s24_transpose_bf16": [_P, _I64, _I64, _I64, _P, _I64, _P],
     "s24_masked_decay": [_P, _P, _I, _P, _I64, _I64, _F, _P],
     "s24_masked_decay_bits": [_P, _P, _I, _P, _I64, _F, _P],
     "s24_split_bf16": [_P, _I64, _P, _P, _P],

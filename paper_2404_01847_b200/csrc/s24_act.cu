@@ -197,3 +197,56 @@ extern "C" int s24_act_bwd(const uint16_t* z, int64_t ldz, const uint16_t* da, i
   }
   return s24_check_launch("act_bwd");
 }
+
+// ---------------------------------------------------------------------------
+// bf16 transpose (dst = src^T): the K-major token operand of the two-slab MVUE weight-gradient
+// GEMM (X^T for dW_in, A^T for dW2).  64 x 64 tiles through shared memory, 16-byte loads and
+// stores on both sides; HBM-bound (2 bytes read + 2 written per element).
+namespace s24 {
+__global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __restrict__ src, int64_t rows,
+                                                             int64_t cols, int64_t lds, uint16_t* __restrict__ dst,
+                                                             int64_t ldd) {
+  // 64 x 64 tile as 32-bit words (bf16 pairs along a row), pitch 33 words: thread (v, c) of the
+  // write-out takes word c of rows 8 v .. 8 v + 7 (banks (row + c) % 32: conflict-free across a
+  // warp) and emits 8 elements of BOTH output rows 2 c and 2 c + 1 (low / high halves).  (A
+  // 128 x 64 tile with whole-sector 32-byte stores per thread measured slower: 3.4 vs 3.7 TB/s.)
+  __shared__ uint32_t t[64][33];
+  const int tid = threadIdx.x;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 64;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int i = tid + 256 * q, rr = i >> 3, v = i & 7;  // 64 rows x 8 vectors of 8
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (r0 + rr < rows && c0 + 8 * v < cols) x = __ldg(reinterpret_cast<const uint4*>(src + (r0 + rr) * lds + c0 + 8 * v));
+    t[rr][4 * v] = x.x;
+    t[rr][4 * v + 1] = x.y;
+    t[rr][4 * v + 2] = x.z;
+    t[rr][4 * v + 3] = x.w;
+  }
+  __syncthreads();
+  const int c = tid & 31, v = tid >> 5;
+  uint32_t w[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w[j] = t[8 * v + j][c];
+  const uint4 lo = make_uint4(__byte_perm(w[0], w[1], 0x5410), __byte_perm(w[2], w[3], 0x5410),
+                              __byte_perm(w[4], w[5], 0x5410), __byte_perm(w[6], w[7], 0x5410));
+  const uint4 hi = make_uint4(__byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632),
+                              __byte_perm(w[4], w[5], 0x7632), __byte_perm(w[6], w[7], 0x7632));
+  if (r0 + 8 * v < rows) {
+    if (c0 + 2 * c < cols) *reinterpret_cast<uint4*>(dst + (c0 + 2 * c) * ldd + r0 + 8 * v) = lo;
+    if (c0 + 2 * c + 1 < cols) *reinterpret_cast<uint4*>(dst + (c0 + 2 * c + 1) * ldd + r0 + 8 * v) = hi;
+  }
+}
+}  // namespace s24
+
+extern "C" int s24_transpose_bf16(const uint16_t* src, int64_t rows, int64_t cols, int64_t lds, uint16_t* dst,
+                                  int64_t ldd, void* stream) {
+  S24_REQUIRE(src != nullptr && dst != nullptr, S24_ERR_ARG, "NULL pointer");
+  S24_REQUIRE(rows % 8 == 0 && cols % 8 == 0 && lds >= cols && ldd >= rows && lds % 8 == 0 && ldd % 8 == 0 &&
+                  (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0,
+              S24_ERR_UNSUPPORTED, "transpose needs 16-byte aligned rows and dims divisible by 8");
+  if (rows == 0 || cols == 0) return S24_OK;
+  const dim3 grid(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>((rows + 63) / 64));
+  s24::transpose_bf16_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, rows, cols, lds, dst, ldd);
+  return s24_check_launch("transpose_bf16");
+}

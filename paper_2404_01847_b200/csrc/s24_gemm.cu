@@ -288,8 +288,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                    kEpi == kEpiGatedGrad || kEpi == kEpiDGated);
   static_assert(kOutT || !(kEpi == kEpiGeluGrad || kEpi == kEpiDAct || kEpi == kEpiGatedGrad || kEpi == kEpiDGated),
                 "training epilogues store token-major outputs");
-  static_assert(kSlabs == 1 || (kAcc == 1 && ((kSparse && kFrag) || (!kSparse && kEpi == kEpiDw))),
-                "slabs: sparse fragment epilogues or dense dW only");
+  static_assert(kSlabs == 1 || (kAcc == 1 && ((kSparse && kFrag) || kEpi == kEpiDw)),
+                "slabs: sparse fragment epilogues or the dW epilogue only");
   static_assert(kMC == 1 || (kMC == 2 && kSparse && kCG == 2 && !kBMN && kSlabs == 1), "multicast: sparse pairs only");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -1183,6 +1183,20 @@ static bool use_dw_slabs(int64_t m, int64_t n, int64_t k) {
   return k >= 8192 && t2 >= 2 * clusters && fill(t2) >= fill(t1) - 0.01;
 }
 
+// Two-slab tiles for the 2:4 weight-gradient GEMM (MVUE operand, K = tokens) with a K-major B:
+// when K is long enough for the un-overlapped epilogue not to matter and the wave fill holds.
+// S24_SDW_SLABS=0/1 overrides.
+static bool use_sdw_slabs(int64_t m, int64_t n, int64_t k) {
+  static const int env = getenv("S24_SDW_SLABS") ? atoi(getenv("S24_SDW_SLABS")) : -1;
+  if (env >= 0) return env == 1;
+  const int64_t clusters = num_sms() / 2;
+  const int64_t t1 = (m / 256) * ((n + 255) / 256), t2 = (m / 512) * ((n + 223) / 224);
+  auto fill = [&](int64_t t) { return static_cast<double>(t) / (((t + clusters - 1) / clusters) * clusters); };
+  (void)fill;
+  (void)t1;
+  return k >= 4096 && t2 >= 2 * clusters;
+}
+
 // Two-slab sparse tiles (Cfg kSlabs) for plain-store GEMMs whose main loop per tile dwarfs the
 // then un-overlapped epilogue: K >= 4096 (measured on B200: C2's K = 4096 plain GEMMs -7 %,
 // C3's K = 11008 / 22016 ones -10..12 %), as long as halving the tile count does not leave a
@@ -1660,7 +1674,12 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
   S24_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX, S24_ERR_SHAPE, "dims exceed int32");
   const bool pair = m % 256 == 0 && cg_override() != 1;
   const bool wide = n % 256 == 0;
-  const int bn_cta = (wide ? 256 : 128) / (pair ? 2 : 1);
+  // two-slab tiles (512 x 224 per CTA pair, one 448-column accumulator + 8 metadata columns) for
+  // a K-major (token-contiguous) B: -22 % operand bytes per MAC against 256 x 256 tiles on this
+  // L2-bound GEMM; the B operand must be K-major (an MN-major 112-row half needs two 64-wide
+  // swizzle boxes, and the 68 KB stage leaves room for only two stages)
+  const bool sdw_slabs = pair && !b_mn && m % 512 == 0 && use_sdw_slabs(m, n, k);
+  const int bn_cta = sdw_slabs ? 112 : (wide ? 256 : 128) / (pair ? 2 : 1);
   CUtensorMap ma, mb, me, md;
   if (int rc = make_map(&ma, a_vals, k / 2, m, k / 2, 64, 128)) return rc;
   if (int rc = make_map(&me, a_e, 256, (m / 128) * (k / 128), 256, 256, 1, kMapU64)) return rc;
@@ -1673,7 +1692,8 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
   }
   if (int rc = make_map(&md, d, n, m, ldd, 32, 16, kMapF32Sw128)) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int sk_tiles = static_cast<int>((m / (pair ? 256 : 128)) * (n / (wide ? 256 : 128)));
+  const int sk_tiles = sdw_slabs ? static_cast<int>((m / 512) * ((n + 223) / 224))
+                                  : static_cast<int>((m / (pair ? 256 : 128)) * (n / (wide ? 256 : 128)));
   int streamk = use_streamk(sk_tiles, num_sms() / (pair ? 2 : 1), static_cast<int>(k / 128));
   if (!streamk)
     streamk = use_splitk(sk_tiles, pair ? dw_clusters(reserved) : 2 * dw_clusters(reserved), static_cast<int>(k / 128), 16, 4.0 * m * n);
@@ -1689,6 +1709,9 @@ extern "C" int s24_spmm_dw(const uint16_t* a_vals, const uint8_t* a_e, int64_t m
 #define S24_SDW(BMN, BNV, CG, ACC)                                                                            \
   return launch_gemm<true, false, BMN, BNV, stages_for<Cfg<true, false, BMN, BNV, 1, CG, ACC>::STAGE_BYTES>(), \
                      CG, kEpiDw, false, ACC>(ma, mb, me, md, md, md, shp, ep, reserved, st)
+  if (sdw_slabs)
+    return launch_gemm<true, false, false, 224, stages_for<Cfg<true, false, false, 224, 1, 2, 1, 2>::STAGE_BYTES>(), 2,
+                       kEpiDw, false, 1, 2>(ma, mb, me, md, md, md, shp, ep, reserved, st);
   if (wide) {
     if (pair) {
       if (b_mn) S24_SDW(true, 256, 2, 1);

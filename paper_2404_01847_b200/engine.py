@@ -22,6 +22,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import torch
 
 from . import _capi as C
@@ -245,6 +247,36 @@ def mvue_compress(g: torch.Tensor, seed: int, gate_ff: int = 0, want_pairs: bool
     return vals, e, pairs
 
 
+def transpose_bf16(x: torch.Tensor) -> torch.Tensor:
+    """x^T (bf16, contiguous) by the repo's tiled transpose kernel."""
+    rows, cols = x.shape
+    out = torch.empty((cols, rows), dtype=torch.bfloat16, device=x.device)
+    with TIMER("k14_transpose"):
+        C.call("s24_transpose_bf16", x.data_ptr(), rows, cols, x.stride(0), out.data_ptr(), rows, C.stream_of(x))
+    return out
+
+
+def _sdw_slabs(m: int, n: int, k: int, dev) -> bool:
+    """Mirror of the library's choice of two-slab tiles for the 2:4 weight-gradient GEMM
+    (s24_gemm.cu use_sdw_slabs): worth a K-major copy of the token operand."""
+    env = os.environ.get("S24_SDW_SLABS")
+    if env is not None:
+        return env == "1" and m % 512 == 0
+    clusters = torch.cuda.get_device_properties(dev).multi_processor_count // 2
+    return m % 512 == 0 and k >= 4096 and (m // 512) * ((n + 223) // 224) >= 2 * clusters
+
+
+def spmm_dw_tokens(vals, e, m: int, k: int, b_tok: torch.Tensor, n: int, out: torch.Tensor, w, idx, lam: float,
+                   gate_ff: int, tag: str) -> None:
+    """The MVUE weight gradient out[m, n] = A~[m, k] . B_tok[k, n] with B_tok token-major (k = tokens):
+    large shapes transpose B_tok once (k14, HBM-bound) so the GEMM runs two-slab 512 x 224 tiles on a
+    K-major B (-22 % operand bytes per MAC on this L2-bound GEMM); small ones read B_tok MN-major."""
+    if _sdw_slabs(m, n, k, b_tok.device):
+        spmm_dw(vals, e, m, k, transpose_bf16(b_tok), False, n, out, w, idx, lam, gate_ff, tag=tag)
+    else:
+        spmm_dw(vals, e, m, k, b_tok, True, n, out, w, idx, lam, gate_ff, tag=tag)
+
+
 def spmm_dw(vals: torch.Tensor, e: torch.Tensor, m: int, k: int, b: torch.Tensor, b_mn: bool, n: int,
             out: torch.Tensor, w: torch.Tensor | None = None, idx: torch.Tensor | None = None, lam: float = 0.0,
             gate_ff: int = 0, tag: str = "k8_spmm_dw", accumulate: bool = False) -> None:
@@ -452,9 +484,9 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
         mvue = False
     if mvue:
         v2, e2, _ = mvue_compress(dy, mvue_seed(rng_seed, 1), exact=mvue_exact)
-        spmm_dw(v2, e2, d, n, st.a, True, d_ff, dw2, w2_dense, w2.idx, lam, tag="k8_spmm_dw2")
+        spmm_dw_tokens(v2, e2, d, n, st.a, d_ff, dw2, w2_dense, w2.idx, lam, 0, "k8_spmm_dw2")
         v1, e1, _ = mvue_compress(dz, mvue_seed(rng_seed, 2), gate_ff, exact=mvue_exact)
-        spmm_dw(v1, e1, r_in, n, st.x, True, d, dw_in, w_in_dense, w_in.idx, lam, gate_ff, tag="k8_spmm_dw_in")
+        spmm_dw_tokens(v1, e1, r_in, n, st.x, d, dw_in, w_in_dense, w_in.idx, lam, gate_ff, "k8_spmm_dw_in")
     else:
         gemm_dw(dy, True, st.a, True, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")
         gemm_dw(dz, True, st.x, True, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam, tag="k5_gemm_dw_in",

@@ -410,3 +410,35 @@ def test_ordered_splitk_under_sm_contention_is_deterministic_or_reported():
     env = dict(os.environ, S24_SPLITK="4")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_sparse_dw_two_slab_tiles_forced():
+    """S24_SDW_SLABS=1: the 2:4 weight-gradient GEMM (MVUE operand, K = tokens) on 512 x 224
+    two-slab tiles with a K-major B (the repo's transpose of the token-major operand) equals the
+    256 x 256 single-slab GEMM on the MN-major operand, with the masked decay and the gated row
+    remap, ragged last N tile included (subprocess: the knob is read once)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, sys; sys.path.insert(0, %r)\n"
+        "from paper_2404_01847_b200 import engine as E\n"
+        "for m, n, k, ff in [(1024, 384, 4096, 0), (1536, 640, 2048, 0), (1024, 896, 1024, 512)]:\n"
+        "    g = (torch.randn(k, m, device='cuda') * 0.1).bfloat16()\n"
+        "    b = torch.randn(k, n, device='cuda').bfloat16()\n"
+        "    w = (torch.randn(m, n, device='cuda') * 0.05).bfloat16()\n"
+        "    op = E.CompressedOperand.empty(m, n, 'cuda')\n"
+        "    E.search_compress(w, op)\n"
+        "    vals, e, _ = E.mvue_compress(g, 5, gate_ff=ff)\n"
+        "    ref = torch.empty(m, n, device='cuda')\n"
+        "    out = torch.full((m, n), float('nan'), device='cuda')\n"
+        "    E.spmm_dw(vals, e, m, k, b, True, n, ref, w, op.idx, 0.01, ff)\n"
+        "    E.spmm_dw(vals, e, m, k, E.transpose_bf16(b), False, n, out, w, op.idx, 0.01, ff)\n"
+        "    err = float((out - ref).norm() / ref.norm())\n"
+        "    assert err < 1e-5, (m, n, k, ff, err)\n"
+        "x = torch.randn(328, 200, device='cuda').bfloat16()\n"
+        "assert torch.equal(E.transpose_bf16(x), x.t().contiguous())\n"
+        "print('ok')\n" % os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+    env = dict(os.environ, S24_SDW_SLABS="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
