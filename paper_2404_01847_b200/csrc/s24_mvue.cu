@@ -188,7 +188,7 @@ __device__ __forceinline__ int mvue_group(const double (&g)[4], double u, double
 // amax > rest is the reference's.  The inclusion probabilities n / d (n = 2 a or a) are then
 // within 2 ulp(1) of the reference's float64 quotients (reciprocal and product roundings), and
 // the greedy pair fill and cumulative sums add their operands' bounds step by step -- at most
-// 968 ulp(1) between c_j and the draw (the bound propagation in DESIGN.md), so a decision
+// 968 ulp(1) between c_j and the draw (tools/mvue_bound.py), so a decision
 // c_j <= draw whose fp32 margin exceeds 2^-14 (1024 ulp(1)) is the reference's decision.  The
 // kept VALUES need no division: pi_k is proportional to |g_k| (2 |g_k| / total, or |g_k| / rest
 // when clamped), so the reference's g_k / pi_k is sign(g_k) total / 2 (resp. sign(g_k) rest) up
@@ -423,9 +423,7 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
         bool ok;
         uint32_t pk;
         int idx = mvue_group_cert(gv, out, pk, ok);
-#ifndef S24_MVUE_DEBUG
         if (!ok || p.force_f64) idx = mvue_group_slow(gv, out, pk);
-#endif
         s_pk[ml * 33 + 16 * half + j] = pk;
         // nibble i0 | i1 << 2 of pair idx = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE}[idx]
         hw |= ((0xED9C84u >> (4 * idx)) & 0xFu) << (4 * q);

@@ -197,3 +197,18 @@ def test_bench_reference_arm_line():
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["sample"] and cb["value"] == line["value"]
     e2e = line["e2e"]
     assert e2e["value"] == line["value"] and e2e["h2d_bytes_per_step"] == 0 and e2e["d2h_bytes_per_step"] == 0
+
+
+def test_mvue_certificate_bound_below_margin():
+    """The certified exact-MVUE kernel decides c_j <= draw in fp32 only with a 2^-14 (1024 ulp(1))
+    margin; the worst-case error propagated through the reference's greedy pair fill must stay
+    below it (tools/mvue_bound.py, the kernel's constant kMargin)."""
+    import importlib.util
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("mvue_bound", os.path.join(root, "tools", "mvue_bound.py"))
+    mb = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mb)
+    assert mb.bound(2.0) < 1024
+    src = open(os.path.join(root, "paper_2404_01847_b200", "csrc", "s24_mvue.cu")).read()
+    assert "kMargin = 6.103515625e-5f" in src  # 2^-14
