@@ -17,7 +17,8 @@ mask search fused with compression (K1) instead of K2 (refresh period
 l = 40, optim.py:55).  The timed region starts on a refresh step, so any K
 timed steps contain ceil(K / 40) mask searches (at least the amortised share).
 N > 1: token-batch data parallelism (weak scaling, a fixed token batch per
-rank), one NCCL all-reduce of [dW_in, dbias, dW2] per step.  Inputs:
+rank), one flat fp32 bucket [dW_in, dbias, dW2] per step, SUM-reduced over NCCL in two chunks each
+launched right after its dW GEMM ([dbias, dW2] under the dW_in GEMM, [dW_in] under dX).  Inputs:
 synthetic, reference init (trainer.py:180-191).
 
 Reported (one JSON line on rank 0): tokens/s (value, whole job); e2e through
@@ -281,7 +282,7 @@ class SparseStep:
         self.op_in = E.CompressedOperand.empty(w_in.shape[0], w_in.shape[1], dev,
                                                perm_ff=w2.shape[1] if act in E.GATED else 0)
         self.op_out = E.CompressedOperand.empty(w2.shape[0], w2.shape[1], dev)
-        # one flat fp32 gradient bucket [dW_in | dbias_in | dW2] -> one all-reduce per step
+        # one flat fp32 gradient bucket [dW_in | dbias_in | dW2], reduced in two chunks (see __call__)
         n_in, n_b, n_2 = w_in.numel(), w_in.shape[0], w2.numel()
         self.bucket = torch.empty(n_in + n_b + n_2, dtype=torch.float32, device=dev)
         self.dw_in = self.bucket[:n_in].view(w_in.shape)
@@ -303,18 +304,26 @@ class SparseStep:
         st = E.ffn_forward(x, self.op_in, self.bias, self.op_out, self.act, fused=True)
         work = []
 
-        def grads_ready():
-            # the one all-reduce of [dW_in | dbias | dW2] starts while dX is still computing; the
-            # dX GEMM leaves DP_RESERVED_SMS SMs to the collective so the two actually overlap
+        # the bucket [dW_in | dbias | dW2] is reduced in two SUM all-reduces: [dbias | dW2] as soon as
+        # the dW2 GEMM is enqueued (it overlaps the dW_in GEMM), [dW_in] once that one is (it overlaps
+        # the dX GEMM); the GEMMs running under a collective leave DP_RESERVED_SMS SMs to it
+        n_in = self.w_in.numel()
+
+        def dw2_ready():
             if self.world > 1:
-                work.append(self.torch.distributed.all_reduce(self.bucket, group=self.pg, async_op=True))
+                work.append(self.torch.distributed.all_reduce(self.bucket[n_in:], group=self.pg, async_op=True))
                 E.RESERVED_SMS = DP_RESERVED_SMS
 
-        with E.reserved_sms(0):  # grads_ready raises it for the dX GEMM while the all-reduce runs
+        def grads_ready():
+            if self.world > 1:
+                work.append(self.torch.distributed.all_reduce(self.bucket[:n_in], group=self.pg, async_op=True))
+                E.RESERVED_SMS = DP_RESERVED_SMS
+
+        with E.reserved_sms(0):  # the hooks raise it while a collective is in flight
             g = E.ffn_backward(st, dy, self.op_in, self.op_out, self.act, w_in_dense=self.w_in, w2_dense=self.w2,
                                lam=LAMBDA / self.world, dw_in_out=self.dw_in, dw2_out=self.dw2, mvue=bool(self.mvue),
                                rng_seed=self.t, mvue_exact=self.mvue == "exact", dbias_out=self.dbias,
-                               grads_ready=grads_ready)
+                               grads_ready=grads_ready, dw2_ready=dw2_ready)
         for w in work:
             w.wait()
         self.t += 1

@@ -435,7 +435,7 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
                  lam: float = 0.0, dw_in_out: torch.Tensor | None = None,
                  dw2_out: torch.Tensor | None = None, mvue: bool = False, rng_seed: int = 0,
                  mvue_exact: bool = True, dbias_out: torch.Tensor | None = None,
-                 grads_ready=None, dx_accumulate: torch.Tensor | None = None) -> Grads:
+                 grads_ready=None, dx_accumulate: torch.Tensor | None = None, dw2_ready=None) -> Grads:
     """dA = dY W2~ (out_bwd, W2's transposed orientation) -> dZ (activation
     backward, bias gradient) -> dX = dZ W_in~ (in_bwd); dense dW2 = dY^T A and
     dW_in = dZ^T X with the masked decay lam (1 - M) W fused (gated_ffn.py:327-356).
@@ -444,6 +444,7 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     2:4 tensor cores (gated_ffn.py:367-373).
 
     Launch order: dA/dZ (+ bias gradient), dW2, dW_in, then dX, so that
+    `dw2_ready()` -- called once dW2 and the bias gradient are enqueued (before the dW_in GEMM) -- and
     `grads_ready()` -- called once every weight/bias gradient is enqueued -- can start
     the data-parallel all-reduce of the gradient bucket while dX is still computing.
     dbias_out / dw_in_out / dw2_out let the caller hand in views of that bucket.
@@ -485,10 +486,14 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     if mvue:
         v2, e2, _ = mvue_compress(dy, mvue_seed(rng_seed, 1), exact=mvue_exact)
         spmm_dw_tokens(v2, e2, d, n, st.a, d_ff, dw2, w2_dense, w2.idx, lam, 0, "k8_spmm_dw2")
+        if dw2_ready is not None:
+            dw2_ready()
         v1, e1, _ = mvue_compress(dz, mvue_seed(rng_seed, 2), gate_ff, exact=mvue_exact)
         spmm_dw_tokens(v1, e1, r_in, n, st.x, d, dw_in, w_in_dense, w_in.idx, lam, gate_ff, "k8_spmm_dw_in")
     else:
         gemm_dw(dy, True, st.a, True, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")
+        if dw2_ready is not None:
+            dw2_ready()
         gemm_dw(dz, True, st.x, True, r_in, d, n, dw_in, w_in_dense, w_in.idx, lam, tag="k5_gemm_dw_in",
                 gate_ff=gate_ff)
     if grads_ready is not None:
