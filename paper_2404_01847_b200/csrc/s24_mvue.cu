@@ -198,13 +198,20 @@ __device__ __forceinline__ int mvue_group(const double (&g)[4], double u, double
 // sets ok = false and the caller reruns the group in float64 (mvue_group_slow): bit-exact by
 // construction.
 __device__ __forceinline__ int mvue_group_cert(const float (&g)[4], uint64_t out, uint32_t& packed, bool& ok) {
+  // written as selects throughout: `if` forms compiled to branches with reconvergence
+  // bookkeeping (BSSY / BSYNC) in every group
   const float a0 = fabsf(g[0]), a1 = fabsf(g[1]), a2 = fabsf(g[2]), a3 = fabsf(g[3]);
   const float total = __fadd_rn(__fadd_rn(__fadd_rn(a0, a1), a2), a3);
-  int fm = 0;
-  float amax = a0;
-  if (a1 > amax) { fm = 1; amax = a1; }
-  if (a2 > amax) { fm = 2; amax = a2; }
-  if (a3 > amax) { fm = 3; amax = a3; }
+  // first maximum (strict >, the reference's scan)
+  const bool s1 = a1 > a0;
+  float amax = s1 ? a1 : a0;
+  int fm = s1 ? 1 : 0;
+  const bool s2 = a2 > amax;
+  amax = s2 ? a2 : amax;
+  fm = s2 ? 2 : fm;
+  const bool s3 = a3 > amax;
+  amax = s3 ? a3 : amax;
+  fm = s3 ? 3 : fm;
   const float b0 = fm == 0 ? 0.0f : a0, b1 = fm == 1 ? 0.0f : a1, b2 = fm == 2 ? 0.0f : a2, b3 = fm == 3 ? 0.0f : a3;
   const float rest = __fadd_rn(__fadd_rn(__fadd_rn(b0, b1), b2), b3);
   const int nnz = (a0 != 0.0f) + (a1 != 0.0f) + (a2 != 0.0f) + (a3 != 0.0f);
@@ -212,16 +219,16 @@ __device__ __forceinline__ int mvue_group_cert(const float (&g)[4], uint64_t out
                            fminf(a2 == 0.0f ? amax : a2, a3 == 0.0f ? amax : a3));
   // exact sums: binade span <= 14 over the nonzero magnitudes, all normal and far from overflow
   const int span = static_cast<int>(__float_as_uint(amax) >> 23) - static_cast<int>(__float_as_uint(amin) >> 23);
-  ok = nnz == 0 || (span <= 14 && amin >= 1.0e-30f && total <= 1.0e30f);  // total: also NaN / inf
+  bool good = nnz == 0 || (span <= 14 && amin >= 1.0e-30f && total <= 1.0e30f);  // total: also NaN / inf
   const bool clamp = amax > rest;
   const float inv = __frcp_rn(clamp ? rest : total);
-  float pi[4];
   const float ak[4] = {a0, a1, a2, a3};
+  float pi[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    pi[k] = clamp ? (k == fm ? 1.0f : __fmul_rn(ak[k], inv)) : __fmul_rn(2.0f * ak[k], inv);
-    if (nnz == 1) pi[k] = ak[k] > 0.0f ? 1.0f : (1.0f / 3.0f);
-    if (nnz == 0) pi[k] = 0.5f;
+    const float pg = clamp ? (k == fm ? 1.0f : __fmul_rn(ak[k], inv)) : __fmul_rn(2.0f * ak[k], inv);
+    const float p1 = ak[k] > 0.0f ? 1.0f : (1.0f / 3.0f);
+    pi[k] = nnz >= 2 ? pg : (nnz == 1 ? p1 : 0.5f);
   }
   float r0 = pi[0], r1 = pi[1], r2 = pi[2], r3 = pi[3];
   float s = 0.5f * __fadd_rn(__fadd_rn(__fadd_rn(pi[0], pi[1]), pi[2]), pi[3]);
@@ -248,21 +255,21 @@ __device__ __forceinline__ int mvue_group_cert(const float (&g)[4], uint64_t out
   const float uf = __uint2float_rn(static_cast<uint32_t>(out >> 40)) * 5.9604644775390625e-8f;  // 2^-24
   const float draw = __fmul_rn(uf, c5);
   constexpr float kMargin = 6.103515625e-5f;  // 2^-14 = 1024 ulp(1) > the 968 ulp(1) bound
-  ok = ok && fabsf(c0 - draw) > kMargin && fabsf(c1 - draw) > kMargin && fabsf(c2 - draw) > kMargin &&
-       fabsf(c3 - draw) > kMargin && fabsf(c4 - draw) > kMargin && fabsf(c5 - draw) > kMargin;
+  const float dmin = fminf(fminf(fminf(fabsf(c0 - draw), fabsf(c1 - draw)), fminf(fabsf(c2 - draw), fabsf(c3 - draw))),
+                           fminf(fabsf(c4 - draw), fabsf(c5 - draw)));
+  good = good && dmin > kMargin;
   const int idx = min((c0 <= draw) + (c1 <= draw) + (c2 <= draw) + (c3 <= draw) + (c4 <= draw) + (c5 <= draw), 5);
   const int i0 = idx < 3 ? 0 : (idx < 5 ? 1 : 2);
   const int i1 = idx == 0 ? 1 : (idx == 1 || idx == 3) ? 2 : 3;
   const float g0 = i0 == 0 ? g[0] : (i0 == 1 ? g[1] : g[2]);
   const float g1 = i1 == 1 ? g[1] : (i1 == 2 ? g[2] : g[3]);
   // nnz >= 2: a kept element has pi > 0 (its pair probability is positive), so a != 0
-  if (nnz >= 2) ok = ok && g0 != 0.0f && g1 != 0.0f;
+  good = good && (nnz < 2 || (g0 != 0.0f && g1 != 0.0f));
+  ok = good;
   const float m = clamp ? rest : 0.5f * total;  // kept magnitude when pi = 2 a / total or a / rest
-  float v0 = g0, v1 = g1;  // nnz == 1: the nonzero keeps g (pi = 1), zeros keep +-0; nnz == 0: +-0
-  if (nnz >= 2) {
-    v0 = (clamp && i0 == fm) ? g0 : copysignf(m, g0);
-    v1 = (clamp && i1 == fm) ? g1 : copysignf(m, g1);
-  }
+  // nnz == 1: the nonzero keeps g (pi = 1), zeros keep +-0; nnz == 0: +-0
+  const float v0 = (nnz < 2 || (clamp && i0 == fm)) ? g0 : copysignf(m, g0);
+  const float v1 = (nnz < 2 || (clamp && i1 == fm)) ? g1 : copysignf(m, g1);
   packed = static_cast<uint32_t>(f32_to_bf16(v0)) | (static_cast<uint32_t>(f32_to_bf16(v1)) << 16);
   return idx;
 }
