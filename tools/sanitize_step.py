@@ -1,6 +1,9 @@
 """One training step of the 2:4 FFN block (K1 refresh, fwd, bwd with the fused decay), one K2
 step, and one fused dense step, for compute-sanitizer (memcheck / racecheck / synccheck).
-python tools/sanitize_step.py <c2|c5|c3-small>"""
+mvue: the same block with the MVUE weight gradient (K8 exact: certified fp32 + float64 fallback,
+then the forced float64 path), the token-operand transpose and the two-slab 2:4 dW GEMM (run with
+S24_SDW_SLABS=1 so the small shape takes it).
+python tools/sanitize_step.py <c2|c5|c3-small|mvue>"""
 import os
 import sys
 
@@ -17,9 +20,17 @@ if name == "c3-small":  # the gated (SwiGLU) epilogues at a sanitizer-friendly s
     cfg = dict(d=1024, d_ff=2816, act="swiglu", tokens=4096, workload="c3-shaped small")
 dev = torch.device("cuda", 0)
 w_in, bias, w2, x, dy = B.make_problem(cfg, dev, 1)
-st = B.SparseStep(w_in, bias, w2, cfg["act"], 1)
-st(x, dy)  # refresh step: K1 + fwd + bwd
-st(x, dy)  # K2 step
-B.DenseFusedStep(w_in, bias, w2, cfg["act"])(x, dy)
+if name == "mvue":
+    from paper_2404_01847_b200 import engine as E
+
+    st = B.SparseStep(w_in, bias, w2, cfg["act"], 1, mvue="exact")
+    st(x, dy)  # refresh step: K1 + fwd + bwd with K8 exact, transposes, two-slab 2:4 dW GEMMs
+    st(x, dy)
+    E.mvue_compress(dy, 3, exact=2)  # the float64 path for every group
+else:
+    st = B.SparseStep(w_in, bias, w2, cfg["act"], 1)
+    st(x, dy)  # refresh step: K1 + fwd + bwd
+    st(x, dy)  # K2 step
+    B.DenseFusedStep(w_in, bias, w2, cfg["act"])(x, dy)
 torch.cuda.synchronize()
 print("sanitize step ok", name)
