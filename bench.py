@@ -83,12 +83,13 @@ def parse():
     return p.parse_args()
 
 
-def config_dict(cfg, world, backend="nccl", shared=False):
-    """The `config` object of both arms' JSON lines (same workload keys)."""
+def config_dict(cfg, world):
+    """The `config` object of both arms' JSON lines: the workload only, identical in both arms
+    (the arm-specific facts -- collective backend, refreshes in the timed region -- are top-level
+    keys of the line)."""
     out = {"workload": cfg["workload"], "d_model": cfg["d"], "d_ff": cfg["d_ff"], "act": cfg["act"],
            "tokens_per_rank": cfg["tokens"], "mask_refresh_every": REFRESH, "lambda_w": LAMBDA,
            "parallelism": f"dp{world}",
-           "dp_backend": backend + (" (ranks share GPUs: functional test only)" if shared else ""),
            "l2": "per-step working set > 126 MB L2 (inputs larger than L2, no flush)"}
     if cfg.get("layers", 1) > 1:
         out["layers"] = cfg["layers"]
@@ -142,7 +143,7 @@ def run_reference(a, cfg):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": a.gpus,
         "steps": steps, "warmup": a.warmup, "ms_per_step": 1000.0 * cfg["tokens"] / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference init)", "config": config_dict(cfg, a.gpus, backend="none (host CPU)"),
+        "data": "synthetic (reference init)", "config": config_dict(cfg, a.gpus), "dp_backend": "none (host CPU)",
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": procs, "kind": kind,
                          "sample": _ref_sample_text(cfg, a.ref_tokens, steps, dfs, procs)},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -790,8 +791,9 @@ def run_ours(a, cfg, cfg_name, subs):
             "warmup": a.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (reference init N(0,1)/sqrt(fan_in) weights, N(0,1) tokens)",
-            "config": dict(config_dict(cfg, world, backend, shared), refresh_steps_in_timed_region=res[
-                "refresh_steps_timed"]),
+            "config": config_dict(cfg, world),
+            "dp_backend": backend + (" (ranks share GPUs: functional test only)" if shared else ""),
+            "refresh_steps_in_timed_region": res["refresh_steps_timed"],
             "kernels": res["kernels"], "variants": res.get("variants"), "optimizer_step": res.get("optimizer_step"),
             "activation": res.get("activation"), "mask_search": res["mask_search"],
             "roofline": res["roofline"], "e2e": res["e2e"], "gpu_launches": res["gpu_launches"],
