@@ -224,13 +224,11 @@ def run_stack(a, cfg):
             "warmup": t0, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (reference init N(0,1)/sqrt(fan_in) weights, N(0,1) tokens)",
-            "config": {"workload": cfg["workload"], "layers": n_layers, "d_model": d, "d_ff": d_ff,
-                       "act": cfg["act"], "tokens_per_rank": n_tok, "mask_refresh_every": B.REFRESH,
-                       "lambda_w": B.LAMBDA, "parallelism": f"dp{world}",
-                       "dp_backend": backend + (" (ranks share GPUs: functional test only)" if shared else ""),
-                       "allreduce": "one fp32 bucket [dW_in|dbias|dW2] per block, async, overlapped with the "
-                                    "backward of the blocks below",
-                       "l2": "per-step working set ~15 GB > 126 MB L2 (no flush)"},
+            "config": B.config_dict(dict(cfg, tokens=n_tok, layers=n_layers), world),
+            "dp_backend": backend + (" (ranks share GPUs: functional test only)" if shared else ""),
+            "allreduce": "one fp32 bucket [dW_in|dbias|dW2] per block, async, overlapped with the backward of the "
+                         "blocks below",
+            "working_set": "~15 GB per step > 126 MB L2 (no flush)",
             "dense_tokens_per_s": dense, "speedup_vs_dense": (value / dense) if dense else None,
             "roofline": roof, "kernels": per_kernel, "e2e": e2e, "gpu_launches": launches_timed,
             "clocks": clocks, "cpu_baseline": cpu,
