@@ -206,10 +206,11 @@ namespace s24 {
 __global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __restrict__ src, int64_t rows,
                                                              int64_t cols, int64_t lds, uint16_t* __restrict__ dst,
                                                              int64_t ldd) {
-  // 64 x 64 tile as 32-bit words (bf16 pairs along a row), pitch 33 words: thread (v, c) of the
-  // write-out takes word c of rows 8 v .. 8 v + 7 (banks (row + c) % 32: conflict-free across a
-  // warp) and emits 8 elements of BOTH output rows 2 c and 2 c + 1 (low / high halves).  (A
-  // 128 x 64 tile with whole-sector 32-byte stores per thread measured slower: 3.4 vs 3.7 TB/s.)
+  // 64 x 64 tile as 32-bit words (bf16 pairs along a row), pitch 33 words.  Write-out: warp wp
+  // owns word columns 4 wp .. 4 wp + 3 (output rows 8 wp .. 8 wp + 7); lane (wq, j) reads word
+  // 4 wp + wq of rows 8 j .. 8 j + 7 and emits elements r0 + 8 j .. + 7 of output rows 2 w and
+  // 2 w + 1 (low / high halves), so 8 lanes write one output row's 128 contiguous bytes: a store
+  // instruction touches 4 cache lines, not 32 (the L1 store wavefronts were the limit)
   __shared__ uint32_t t[64][33];
   const int tid = threadIdx.x;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 64;
@@ -224,17 +225,18 @@ __global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __r
     t[rr][4 * v + 3] = x.w;
   }
   __syncthreads();
-  const int c = tid & 31, v = tid >> 5;
-  uint32_t w[8];
+  const int lane = tid & 31, wp = tid >> 5;
+  const int w = 4 * wp + (lane >> 3), j = lane & 7;  // word column, 8-row group
+  uint32_t x[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) w[j] = t[8 * v + j][c];
-  const uint4 lo = make_uint4(__byte_perm(w[0], w[1], 0x5410), __byte_perm(w[2], w[3], 0x5410),
-                              __byte_perm(w[4], w[5], 0x5410), __byte_perm(w[6], w[7], 0x5410));
-  const uint4 hi = make_uint4(__byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632),
-                              __byte_perm(w[4], w[5], 0x7632), __byte_perm(w[6], w[7], 0x7632));
-  if (r0 + 8 * v < rows) {
-    if (c0 + 2 * c < cols) *reinterpret_cast<uint4*>(dst + (c0 + 2 * c) * ldd + r0 + 8 * v) = lo;
-    if (c0 + 2 * c + 1 < cols) *reinterpret_cast<uint4*>(dst + (c0 + 2 * c + 1) * ldd + r0 + 8 * v) = hi;
+  for (int k = 0; k < 8; ++k) x[k] = t[8 * j + k][w];
+  const uint4 lo = make_uint4(__byte_perm(x[0], x[1], 0x5410), __byte_perm(x[2], x[3], 0x5410),
+                              __byte_perm(x[4], x[5], 0x5410), __byte_perm(x[6], x[7], 0x5410));
+  const uint4 hi = make_uint4(__byte_perm(x[0], x[1], 0x7632), __byte_perm(x[2], x[3], 0x7632),
+                              __byte_perm(x[4], x[5], 0x7632), __byte_perm(x[6], x[7], 0x7632));
+  if (r0 + 8 * j < rows) {
+    if (c0 + 2 * w < cols) *reinterpret_cast<uint4*>(dst + (c0 + 2 * w) * ldd + r0 + 8 * j) = lo;
+    if (c0 + 2 * w + 1 < cols) *reinterpret_cast<uint4*>(dst + (c0 + 2 * w + 1) * ldd + r0 + 8 * j) = hi;
   }
 }
 }  // namespace s24
