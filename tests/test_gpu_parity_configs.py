@@ -276,3 +276,25 @@ def test_c1_fp32_mode():
 @pytest.mark.parametrize("sparse", [True, False])
 def test_fp32_mode_small(act, sparse):
     _fp32_case(act, 256, 384, 256, seed=606 + len(act), sparse=sparse)
+
+
+def test_pair_launch_mixed_super_tiles_equals_single_launches():
+    """K1 of a block's two weights in one launch with two-tile super-tiles for the weight whose tile
+    columns are even and single tiles for the odd one (12288 x 3968: 31 tile columns), against two
+    single-weight launches (below the pairing threshold: single tiles) -- every output bit-equal --
+    and oracle bands of both weights."""
+    from paper_2404_01847_b200.engine import CompressedOperand, search_compress, search_compress_pair
+
+    w0 = _bf16((12288, 3968), seed=11, scale=1.0 / np.sqrt(3968))
+    w1 = _bf16((3968, 12288), seed=12, scale=1.0 / np.sqrt(12288))
+    ops = [CompressedOperand.empty(*w.shape, w.device) for w in (w0, w1)]
+    search_compress_pair(w0, ops[0], w1, ops[1])
+    for w, op in zip((w0, w1), ops):
+        ref = CompressedOperand.empty(*w.shape, w.device)
+        search_compress(w, ref)
+        for a in ("idx", "fwd_vals", "bwd_vals", "fwd_e", "bwd_e"):
+            assert torch.equal(getattr(op, a), getattr(ref, a)), a
+    op, w = ops[1], w1
+    for r0 in (0, 1984, 3904):
+        idx = o.search_pattern_idx(_f64(w[r0:r0 + 64]))
+        np.testing.assert_array_equal(op.idx[r0 // 4:(r0 + 64) // 4].cpu().numpy(), idx)
