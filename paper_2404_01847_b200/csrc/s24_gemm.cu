@@ -1163,7 +1163,10 @@ static int dw_clusters(int reserved) {
 }
 
 // Wave-synchronised schedule (workspace wave counter): on for the dW GEMMs (panels of K = tokens,
-// far larger than L2); S24_WAVESYNC=0/1 turns it off / on for every GEMM.
+// far larger than L2) and for the forward / dX GEMMs with K >= 8192, whose tiles run long enough
+// for the CTAs to drift apart (measured on B200, alternating A/B: C4 step -1.7 %, every sparse
+// GEMM faster; C3's K = 4096 fused-epilogue GEMMs +2 % with it, its K = 11008 / 22016 ones
+// unchanged).  S24_WAVESYNC=0/1 turns it off / on for every GEMM.
 static int wave_on(bool dflt) {
   static const int env = getenv("S24_WAVESYNC") ? atoi(getenv("S24_WAVESYNC")) : -1;
   return (env < 0 ? dflt : env != 0) ? 1 : 0;
@@ -1403,7 +1406,7 @@ extern "C" int s24_spmm(const uint16_t* a_vals, const uint8_t* a_e, int64_t m, i
   const int tile_m = pair ? 256 : 128;
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0,
                 pick_group_m(static_cast<int>(m / tile_m), 1.125 * tile_m * static_cast<double>(k)),
-                static_cast<unsigned int*>(workspace), wave_on(false), exp_flags()};
+                static_cast<unsigned int*>(workspace), wave_on(k >= 8192), exp_flags()};
   EpiParams ep{d,       ldd,
                bias,    aux,
                ldaux,   dbias,
@@ -1540,7 +1543,7 @@ extern "C" int s24_gemm_act(const uint16_t* w, int w_t, int64_t ldw, int64_t w_g
   }
   GemmShape shp{static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), 0,
                 pick_group_m(static_cast<int>(m / (pair ? 256 : 128)), 0.0), static_cast<unsigned int*>(workspace),
-                wave_on(false), 0, w_gate_ff > 0 ? 1 : 0};
+                wave_on(k >= 8192), 0, w_gate_ff > 0 ? 1 : 0};
   EpiParams ep{d,       ldd,   bias,    aux,     0,   dbias, aux2,
                epilogue == S24_EPI_SWIGLU_GRAD ? S24_ACT_SWIGLU : S24_ACT_GEGLU,
                gate_ff, nullptr, 0,     nullptr, 0.0f, accumulate ? 1 : 0};
