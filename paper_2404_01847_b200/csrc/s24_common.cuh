@@ -356,6 +356,32 @@ __device__ __forceinline__ void gelu_and_grad(float x, float& g, float& dg) {
   const float hdp = fmaf(fmaf(2.5f * kC, x2, 1.5f * kB), x2, 0.5f * kA);  // half the derivative of the tanh argument
   dg = fmaf(xc * fmaf(-t, t, 1.0f), hdp, cdf);
 }
+// Two elements of gelu_and_grad with the packed f32x2 FFMA2 / FMUL2 of sm_100 (half the FP
+// instructions: the two-slab GEMM epilogue is not overlapped with the main loop, so its drain is
+// issue-bound).  The clamp moves to x^2 <= 81: for |x| > 9 the tanh argument x * p(81) (p(81) > 1.5)
+// saturates tanh to +-1 exactly as the clamped argument does, so g = x Phi and the derivative term
+// x (1 - t^2) = 0 come out the same.
+__device__ __forceinline__ void gelu_and_grad2(float x0, float x1, float& g0, float& g1, float& d0, float& d1) {
+  constexpr float kA = 0.797422874f, kB = 0.0370039386f, kC = -3.47603262e-4f;
+  const float2 x = make_float2(x0, x1);
+  float2 x2 = __fmul2_rn(x, x);
+  x2 = make_float2(fminf(x2.x, 81.0f), fminf(x2.y, 81.0f));
+  const float2 p = __ffma2_rn(__ffma2_rn(make_float2(kC, kC), x2, make_float2(kB, kB)), x2, make_float2(kA, kA));
+  const float2 u = __fmul2_rn(x, p);
+  const float2 t = make_float2(tanh_approx(u.x), tanh_approx(u.y));
+  const float2 cdf = __ffma2_rn(make_float2(0.5f, 0.5f), t, make_float2(0.5f, 0.5f));
+  const float2 g = __fmul2_rn(x, cdf);
+  // x (1 - t^2) = 4 g (1 - Phi): the factor 4 goes into the derivative polynomial, and 1 - Phi
+  // needs no negated operand (a negated register costs an extra FADD per element)
+  const float2 hdp4 = __ffma2_rn(__ffma2_rn(make_float2(10.0f * kC, 10.0f * kC), x2, make_float2(6.0f * kB, 6.0f * kB)),
+                                 x2, make_float2(2.0f * kA, 2.0f * kA));
+  const float2 omc = __ffma2_rn(make_float2(-0.5f, -0.5f), t, make_float2(0.5f, 0.5f));
+  const float2 d = __ffma2_rn(__fmul2_rn(g, omc), hdp4, cdf);
+  g0 = g.x;
+  g1 = g.y;
+  d0 = d.x;
+  d1 = d.y;
+}
 // sigmoid(u) = 0.5 + 0.5 tanh(u / 2): one MUFU op
 __device__ __forceinline__ float sigmoid_fast(float u) { return fmaf(0.5f, tanh_approx(0.5f * u), 0.5f); }
 

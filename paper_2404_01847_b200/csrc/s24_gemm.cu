@@ -706,14 +706,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               for (int c = 0; c < 4; ++c) {
                 float x0 = v[16 * (j >> 1) + 4 * c + 2 * (j & 1)];
                 float x1 = v[16 * (j >> 1) + 4 * c + 2 * (j & 1) + 1];
-                if constexpr (kEpi == kEpiStore || kEpi == kEpiGeluGrad) {
+                if constexpr (kEpi == kEpiStore) {
                   x0 += bias4[j];
                   x1 += bias4[j];
+                } else if constexpr (kEpi == kEpiGeluGrad) {
+                  const float2 xb = __fadd2_rn(make_float2(x0, x1), make_float2(bias4[j], bias4[j]));
+                  x0 = xb.x;
+                  x1 = xb.y;
                 }
                 if constexpr (kEpi == kEpiGeluGrad) {
                   float g0, g1, d0, d1;
                   if S24_EXP(16) { g0 = d0 = x0; g1 = d1 = x1; }
-                  else { gelu_and_grad(x0, g0, d0); gelu_and_grad(x1, g1, d1); }
+                  else gelu_and_grad2(x0, x1, g0, g1, d0, d1);
                   x0 = g0;
                   x1 = g1;
                   gq[c] = pack_bf16x2(d0, d1);
