@@ -67,6 +67,54 @@ def test_sparse_gemm_bwd_orientation_and_gelu_epilogue(m, k, n):
     assert normwise_rel(a.float().cpu(), ar.cpu()) < 1e-2
 
 
+@pytest.mark.parametrize("m,k,n,slabs", [(256, 256, 384, "0"), (512, 4096, 448, "1")])
+def test_gelu_epilogue_wide_range_and_saturation(m, k, n, slabs):
+    """The packed f32x2 GELU / GELU' epilogue (clamp on z^2) over pre-activations spanning
+    |z| up to ~40: elementwise against the float64 exact-erf GELU, and exact saturation
+    (GELU' = 1 / 0, GELU = z / 0) beyond |z| = 9.5; single- and two-slab tiles."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, sys\n"
+        "sys.path[:0] = [%r, %r]\n"
+        "import paper_2404_01847_b200._capi as C\n"
+        "from paper_2404_01847_b200.engine import spmm, aux_empty, aux_to_feature_major, CompressedOperand, search_compress\n"
+        "from paper_2404_01847_b200 import TransposableMask\n"
+        "m, k, n = %d, %d, %d\n"
+        "g = torch.Generator(device='cuda').manual_seed(5)\n"
+        "w = (torch.randn(m, k, generator=g, device='cuda') / k ** 0.5).bfloat16()\n"
+        "op = CompressedOperand.empty(m, k, 'cuda'); search_compress(w, op)\n"
+        "bits = TransposableMask(op.idx, (m, k)).bits\n"
+        "x = (torch.randn(n, k, generator=g, device='cuda') * 14).bfloat16()\n"
+        "out = torch.empty((n, m), dtype=torch.bfloat16, device='cuda')\n"
+        "ga = aux_empty(m, n, 'cuda')\n"
+        "spmm(op.fwd_vals, op.fwd_e, m, k, x, False, n, out, None, epi=C.EPI_GELU_GRAD, aux=ga, out_t=True)\n"
+        "gd = aux_to_feature_major(ga, m, n).t().double().cpu()\n"
+        "z = (x.double() @ (w.double() * bits.double()).t()).cpu()\n"
+        "cdf = 0.5 * (1 + torch.erf(z / 2 ** 0.5))\n"
+        "ref = z * cdf\n"
+        "dref = cdf + z * torch.exp(-0.5 * z * z) / (2 * torch.pi) ** 0.5\n"
+        "o = out.double().cpu()\n"
+        "assert z.abs().max() > 20, float(z.abs().max())\n"
+        # bf16 rounding of the stored value + tanh.approx (<= 2^-11 relative in t, i.e.
+        # <= 2.5e-4 |z| in GELU and ~1e-3 |z| in GELU' where t is not saturated)
+        "tol = 2 ** -8 * ref.abs() + 3e-4 * z.abs() + 1e-4\n"
+        "assert torch.all((o - ref).abs() <= tol), float(((o - ref).abs() / tol).max())\n"
+        "dtol = 2 ** -8 * dref.abs() + 1.2e-3 * z.abs().clamp(max=10) + 5e-4\n"
+        "assert torch.all((gd - dref).abs() <= dtol), float(((gd - dref).abs() / dtol).max())\n"
+        "hi, lo = z > 9.5, z < -9.5\n"
+        "assert hi.sum() > 100 and lo.sum() > 100\n"
+        "assert torch.all(gd[hi] == 1.0) and torch.all(gd[lo] == 0.0)\n"
+        "assert torch.all(o[lo] == 0.0)\n"
+        "assert ((o[hi] - z[hi]).abs() / z[hi].abs()).max() < 2 ** -7\n"
+        "print('ok')\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)), m, k, n)
+    env = dict(os.environ, S24_SLABS_EPI=slabs)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
 @pytest.mark.parametrize("m,n,k", [(128, 128, 64), (256, 512, 320), (384, 256, 1024)])
