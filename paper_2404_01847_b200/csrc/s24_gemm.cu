@@ -308,7 +308,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // zero-filled TMA boxes and its epilogue is skipped
   const int num_m = (shp.m + C::TILE_M - 1) / C::TILE_M;
   const int num_n = (shp.n + kBN - 1) / kBN;
-  const int num_tiles = num_m * num_n;
   const int num_kb = shp.k / C::BK;  // k-blocks per output tile
   const int cluster_id = blockIdx.x / (kCG * kMC), num_clusters = gridDim.x / (kCG * kMC);
   // work tiles of the cluster: kMC vertically adjacent pair tiles (num_m % kMC == 0)
@@ -1197,10 +1196,7 @@ static bool use_sdw_slabs(int64_t m, int64_t n, int64_t k) {
   static const int env = getenv("S24_SDW_SLABS") ? atoi(getenv("S24_SDW_SLABS")) : -1;
   if (env >= 0) return env == 1;
   const int64_t clusters = num_sms() / 2;
-  const int64_t t1 = (m / 256) * ((n + 255) / 256), t2 = (m / 512) * ((n + 223) / 224);
-  auto fill = [&](int64_t t) { return static_cast<double>(t) / (((t + clusters - 1) / clusters) * clusters); };
-  (void)fill;
-  (void)t1;
+  const int64_t t2 = (m / 512) * ((n + 223) / 224);
   return k >= 4096 && t2 >= 2 * clusters;
 }
 
