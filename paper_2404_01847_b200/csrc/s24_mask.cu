@@ -492,6 +492,10 @@ __device__ __forceinline__ uint32_t pair_selector(uint32_t nib) {
 
 // one launch prunes one or two weights (the per-step K2 of W_in and W2): CTAs [0, tiles0) take
 // p0's 128 x 128 tiles, the rest p1's
+// T = uint16_t: bf16 weights; T = float: fp32 master weights, kept values rounded to bf16 on the
+// way in (cvt.rn.bf16x2.f32, the rounding of f32_to_bf16) -- the module's per-step K2 on fp32
+// parameters (module.py _prepare_sparse), one pass instead of the general tiled kernel
+template <typename T>
 __global__ void __launch_bounds__(kPruneThreads, 2) prune_bf16_kernel(MaskArgs p0, MaskArgs p1, int tiles0) {
   __shared__ uint32_t s_bv[128 * 32];  // W^T tile: 128 rows x 32 words (64 kept bf16)
   __shared__ uint4 s_sel[90];          // per pattern: row selectors (x, y), column selectors (z, w)
@@ -505,10 +509,24 @@ __global__ void __launch_bounds__(kPruneThreads, 2) prune_bf16_kernel(MaskArgs p
   const int c0 = 8 * (lane & 15);         // first column in tile, 0..120
   const int64_t grow0 = tr * kTile + 4 * br, gcol0 = tc * kTile + c0;
   const int64_t in_row0 = p.perm_ff > 0 ? gate_row(grow0, p.perm_ff) : grow0;
-  const uint16_t* w = static_cast<const uint16_t*>(p.w);
+  const T* w = static_cast<const T*>(p.w);
   uint4 v[4];
+  if constexpr (sizeof(T) == 2) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const uint4*>(w + (in_row0 + i) * p.cols + gcol0));
+    for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const uint4*>(w + (in_row0 + i) * p.cols + gcol0));
+  } else {
+    float4 f[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4* src = reinterpret_cast<const float4*>(w + (in_row0 + i) * p.cols + gcol0);
+      f[i][0] = __ldg(src);
+      f[i][1] = __ldg(src + 1);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      v[i] = make_uint4(pack_bf16x2(f[i][0].x, f[i][0].y), pack_bf16x2(f[i][0].z, f[i][0].w),
+                        pack_bf16x2(f[i][1].x, f[i][1].y), pack_bf16x2(f[i][1].z, f[i][1].w));
+  }
   const uint32_t t2 = *reinterpret_cast<const uint16_t*>(p.idx_in + (grow0 / 4) * (p.cols / 4) + gcol0 / 4);
   if (threadIdx.x < 90) {
     const uint32_t bits16 = c_pat_bits[threadIdx.x];
@@ -1105,10 +1123,11 @@ static int launch_mask(const MaskArgs& a, int dtype, bool search, cudaStream_t s
     else if (dtype == S24_F32) mask_tile_kernel<S24_F32, true, false><<<grid, kThreads, 0, st>>>(a);
     else mask_tile_kernel<S24_F64, true, false><<<grid, kThreads, 0, st>>>(a);
   } else {
-    if (dtype == S24_BF16 && a.fwd_e == nullptr && a.bwd_e == nullptr && a.fwd_vals != nullptr &&
-        a.bwd_vals != nullptr && aligned) {
+    if ((dtype == S24_BF16 || dtype == S24_F32) && a.fwd_e == nullptr && a.bwd_e == nullptr &&
+        a.fwd_vals != nullptr && a.bwd_vals != nullptr && aligned) {
       const int tiles = static_cast<int>(grid.x * grid.y);
-      prune_bf16_kernel<<<tiles, kPruneThreads, 0, st>>>(a, a, tiles);
+      if (dtype == S24_BF16) prune_bf16_kernel<uint16_t><<<tiles, kPruneThreads, 0, st>>>(a, a, tiles);
+      else prune_bf16_kernel<float><<<tiles, kPruneThreads, 0, st>>>(a, a, tiles);
       return s24_check_launch("prune_compress");
     }
     if (narrow) mask_tile_kernel<S24_BF16, false, true><<<grid, kThreads, 0, st>>>(a);
@@ -1175,15 +1194,16 @@ extern "C" int s24_prune_compress_pair(const void* w0, const void* w1, int dtype
   MaskArgs a0{w0, rows0, cols0, nullptr, idx0, fwd_vals0, nullptr, bwd_vals0, nullptr, perm_ff0};
   MaskArgs a1{w1, rows1, cols1, nullptr, idx1, fwd_vals1, nullptr, bwd_vals1, nullptr, perm_ff1};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool fast = dtype == S24_BF16 && rows0 % kTile == 0 && cols0 % kTile == 0 && rows1 % kTile == 0 &&
-                    cols1 % kTile == 0;
+  const bool fast = (dtype == S24_BF16 || dtype == S24_F32) && rows0 % kTile == 0 && cols0 % kTile == 0 &&
+                    rows1 % kTile == 0 && cols1 % kTile == 0;
   if (!fast) {  // general shapes / dtypes: two launches of the tiled kernel
     if (int rc = launch_mask(a0, dtype, false, st)) return rc;
     return launch_mask(a1, dtype, false, st);
   }
   const int t0 = static_cast<int>((rows0 / kTile) * (cols0 / kTile)), t1 = static_cast<int>((rows1 / kTile) * (cols1 / kTile));
   if (t0 + t1 == 0) return S24_OK;
-  prune_bf16_kernel<<<t0 + t1, kPruneThreads, 0, st>>>(a0, a1, t0);
+  if (dtype == S24_BF16) prune_bf16_kernel<uint16_t><<<t0 + t1, kPruneThreads, 0, st>>>(a0, a1, t0);
+  else prune_bf16_kernel<float><<<t0 + t1, kPruneThreads, 0, st>>>(a0, a1, t0);
   return s24_check_launch("prune_compress_pair");
 }
 

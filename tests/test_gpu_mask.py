@@ -228,6 +228,41 @@ def test_k2_fast_prune_matches_oracle(shape, perm_ff):
     assert torch.equal(op.bwd_vals.view(torch.int16), bv1.view(torch.int16))
 
 
+@pytest.mark.parametrize("shape,perm_ff", [((256, 384), 0), ((512, 128), 256)])
+def test_k2_fp32_masters_fast_prune_matches_oracle(shape, perm_ff):
+    """K2 on fp32 master weights (the module's per-step recompression): kept values rounded to
+    bf16 (round-to-nearest-even, incl. exact ties and values beyond bf16 range) equal the
+    oracle's compress of the bf16-rounded weights, and equal K1's fused compress of the same
+    fp32 weights (the general tiled kernel's conversion)."""
+    from paper_2404_01847_b200.engine import CompressedOperand, compress_values, search_compress
+
+    rows, cols = shape
+    w = o.det_normal(shape, seed=rows + 3 * cols).astype(np.float32)
+    # bf16 rounding ties (exactly halfway, both parities) and huge / tiny magnitudes
+    flat = w.reshape(-1)
+    flat[::97] = np.float32(1.0 + 2.0 ** -8)           # tie -> round down to even
+    flat[5::97] = np.float32(1.0 + 3 * 2.0 ** -8)      # tie -> round up to even
+    flat[11::193] = np.float32(3.0e38)
+    flat[17::193] = np.float32(-1.0e-40)
+    wd = torch.from_numpy(w).cuda()
+    op = CompressedOperand.empty(rows, cols, "cuda", perm_ff=perm_ff)
+    search_compress(wd, op)
+    fv1, bv1 = op.fwd_vals.clone(), op.bwd_vals.clone()
+    op.fwd_vals.zero_()
+    op.bwd_vals.zero_()
+    compress_values(wd, op)
+    assert torch.equal(op.fwd_vals.view(torch.int16), fv1.view(torch.int16))
+    assert torch.equal(op.bwd_vals.view(torch.int16), bv1.view(torch.int16))
+    bits = o.idx_to_bits(op.mask_idx().cpu().numpy())
+    p = np.arange(rows)
+    order = p if perm_ff == 0 else np.where(p % 32 < 16, 16 * (p // 32) + p % 32, perm_ff + 16 * (p // 32) + p % 32 - 16)
+    wr = o.round_bf16(w)
+    kv, _ = o.compress_rowwise(wr[order], bits[order])
+    np.testing.assert_array_equal(bf16_bits_of(op.fwd_vals), o.bf16_bits(kv))
+    kb, _ = o.compress_rowwise(np.ascontiguousarray(wr[order].T), np.ascontiguousarray(bits[order].T))
+    np.testing.assert_array_equal(bf16_bits_of(op.bwd_vals), o.bf16_bits(kb))
+
+
 @pytest.mark.parametrize("gated", [False, True])
 def test_k2_pair_launch_equals_two_single_launches(gated):
     """s24_prune_compress_pair (both weights of a block in one launch) == two s24_prune_compress calls."""
