@@ -20,3 +20,10 @@ print('$f', d.get('config',{}).get('workload','')[:30], round(d['value']), d.get
 timeout 1500 tools/gpu_c4_evidence.sh $TAG > /dev/null 2>&1
 cat gpurun_out/c4_$TAG/ncu_full_c4.txt | cut -c1-200
 du -sh gpurun_out
+# C4 token sweep (BASELINE configs[3]) on the final code
+timeout 2400 tools/c4_sweep.sh $OUT/sweep > /dev/null 2>&1
+for f in $OUT/sweep/c4_sweep_*.json; do python -c "
+import json
+d=json.loads(open('$f').read().splitlines()[-1])
+print('$f', round(d['value']), d.get('speedup_vs_best_dense'), d.get('mvue_exact_speedup_vs_best_dense'), d.get('clocks',{}).get('sm_mhz'))
+"; done
