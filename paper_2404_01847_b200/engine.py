@@ -23,11 +23,15 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import os
+import warnings
 
 import torch
 
 from . import _capi as C
 from .matrix import ShapeError
+
+_MVUE_FALLBACK_WARNED = False
+
 
 class _NoTimer:
     def __call__(self, name):
@@ -481,7 +485,14 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     if mvue and n % 128:
         # the MVUE operand is tiled in 128-token groups; a batch that is not a multiple of 128
         # (legal for the reference, any multiple of 4) takes the dense weight gradient -- the
-        # expectation of the unbiased MVUE estimator -- instead of failing
+        # expectation of the unbiased MVUE estimator -- instead of failing; said once per process,
+        # since the result then differs from the reference's draws
+        global _MVUE_FALLBACK_WARNED
+        if not _MVUE_FALLBACK_WARNED:
+            _MVUE_FALLBACK_WARNED = True
+            warnings.warn(f"fst_backward(mvue=True) with {n} tokens (not a multiple of 128): using the dense "
+                          "weight gradient (the MVUE estimator's expectation) instead of MVUE draws", RuntimeWarning,
+                          stacklevel=3)
         mvue = False
     if mvue:
         v2, e2, _ = mvue_compress(dy, mvue_seed(rng_seed, 1), exact=mvue_exact)

@@ -149,15 +149,18 @@ def test_module_gradient_accumulation_and_refresh_guard():
 
 def test_mvue_batch_not_multiple_of_128():
     """ADVICE: mvue=True with a batch that is a multiple of 64 but not of 128 (legal for the
-    reference) takes the dense weight gradient instead of failing."""
+    reference) takes the dense weight gradient instead of failing, and says so once."""
     import paper_2404_01847_b200 as P
+    from paper_2404_01847_b200 import engine as E
 
     d, d_ff, n = 128, 256, 64
     c = _case("gelu", d, d_ff, n, seed=13)
     layer = P.FFNLayer(to_dev_bf16(c["w_in"]), to_dev_bf16(c["bias_in"]), to_dev_bf16(c["w2"]), P.Activation.GELU)
     masks = P.search_layer_masks(layer)
     f = P.fst_forward(layer, to_dev_bf16(c["x"]), masks)
-    g = P.fst_backward(f, to_dev_bf16(c["dy"]), mvue=True)
+    E._MVUE_FALLBACK_WARNED = False
+    with pytest.warns(RuntimeWarning, match="not a multiple of 128"):
+        g = P.fst_backward(f, to_dev_bf16(c["dy"]), mvue=True)
     lo = o.Layer(c["w_in"], c["bias_in"], c["w2"], "gelu")
     mi, mo = o.transposable_search_conv(c["w_in"]), o.transposable_search_conv(c["w2"])
     fr = o.fst_forward(lo, c["x"], mi, mo, exact=False)
