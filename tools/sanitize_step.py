@@ -3,7 +3,9 @@ step, and one fused dense step, for compute-sanitizer (memcheck / racecheck / sy
 mvue: the same block with the MVUE weight gradient (K8 exact: certified fp32 + float64 fallback,
 then the forced float64 path), the token-operand transpose and the two-slab 2:4 dW GEMM (run with
 S24_SDW_SLABS=1 so the small shape takes it).
-python tools/sanitize_step.py <c2|c5|c3-small|mvue>"""
+python tools/sanitize_step.py <c2|c5|c3-small|mvue|train>
+train: run_training (gated epilogues, K1, MVUE exact, fused Adam + compression) and the autograd
+module on fp32 parameters (the fp32 K2 path)."""
 import os
 import sys
 
@@ -20,7 +22,23 @@ if name == "c3-small":  # the gated (SwiGLU) epilogues at a sanitizer-friendly s
     cfg = dict(d=1024, d_ff=2816, act="swiglu", tokens=4096, workload="c3-shaped small")
 dev = torch.device("cuda", 0)
 w_in, bias, w2, x, dy = B.make_problem(cfg, dev, 1)
-if name == "mvue":
+if name == "train":
+    # the training-loop kernels: run_training (GEGLU, K1 refreshes, MVUE exact, the fused fp32
+    # Adam + next-step compression) and the autograd module on fp32 parameters (K2 fp32 path)
+    import paper_2404_01847_b200 as P
+    from paper_2404_01847_b200.module import SparseFFN
+
+    P.run_training(P.TrainConfig(d=256, d_ff=512, depth=1, batch=256, steps=4))
+    mod = SparseFFN(256, 512, act="gelu", decay_lambda=1e-4, device=dev)
+    xin = torch.randn(512, 256, device=dev).bfloat16()
+    for _ in range(2):
+        y = mod(xin)
+        y.float().square().sum().backward()
+        with torch.no_grad():
+            for prm in mod.parameters():
+                prm -= 1e-3 * prm.grad
+                prm.grad = None
+elif name == "mvue":
     from paper_2404_01847_b200 import engine as E
 
     st = B.SparseStep(w_in, bias, w2, cfg["act"], 1, mvue="exact")
