@@ -253,6 +253,16 @@ int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int64_t f, uint
                       uint64_t inc_hi, uint64_t inc_lo, int64_t gate_ff, uint16_t* vals, uint8_t* e,
                       uint8_t* pairs, int exact, void* stream);
 
+/* s24_mvue_compress for a token count that is not a multiple of 128 (the reference accepts any
+ * multiple of 4): G holds n_valid tokens (rows), the operand is padded to n = n_valid rounded up
+ * to 128 (vals f x n/2, E tiles of f x n).  The padded tokens read as zeros (G needs only n_valid
+ * rows) and the random-stream index is row * (n_valid / 4) + group -- the reference's draws for
+ * its n_valid tokens; the padded groups keep zeros.  The B operand of the weight-gradient GEMM
+ * must be zero-padded to n tokens as well.  s24_mvue_compress(..) == this with n_valid = n. */
+int s24_mvue_compress_ragged(const uint16_t* g, int64_t ldg, int64_t n, int64_t n_valid, int64_t f,
+                             uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                             int64_t gate_ff, uint16_t* vals, uint8_t* e, uint8_t* pairs, int exact, void* stream);
+
 /* mvue_prune (sparsity.py:379-398) of a whole (rows x cols) matrix (bf16 / f32 / f64), groups
  * along rows (colwise = 0, groups row-major) or down columns (colwise = 1, groups
  * column-major): the exact float64 estimator and numpy PCG64 stream of s24_mvue_compress,

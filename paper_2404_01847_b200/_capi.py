@@ -50,6 +50,8 @@ SIGNATURES = {
                      _P],
     "s24_mvue_compress": [_P, _I64, _I64, _I64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                           ctypes.c_uint64, _I64, _P, _P, _P, _I, _P],
+    "s24_mvue_compress_ragged": [_P, _I64, _I64, _I64, _I64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                 ctypes.c_uint64, _I64, _P, _P, _P, _I, _P],
     "s24_spmm_dw": [_P, _P, _I64, _I64, _P, _I, _I64, _I64, _P, _I64, _P, _I, _P, _F, _I64, _I, _P, _I, _P],
     "s24_act_fwd": [_P, _I64, _I64, _I64, _I, _P, _I64, _P],
     "s24_act_bwd": [_P, _I64, _P, _I64, _I64, _I64, _I, _P, _I64, _P, _P],

@@ -354,6 +354,8 @@ struct MvueArgs {
   uint8_t* e;         // E tiles [f/128][n/128]
   uint8_t* pairs;     // optional f x n/4 pair indices (tests)
   int force_f64;      // exact mode 2 (tests): every group through the float64 path, no certificate
+  int64_t n_valid;    // tokens that exist (<= n, % 4 == 0): rows >= n_valid read as zeros, and the random
+                      // stream's row stride is n_valid / 4 groups (the reference's index for its n)
 };
 
 template <bool kExact>
@@ -370,7 +372,8 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int i = tid + 256 * q, tr = i >> 4, ch = i & 15;
-      buf[q] = __ldg(reinterpret_cast<const uint4*>(p.g + (t0 + tr) * p.ldg + f0 + ch * 8));
+      buf[q] = t0 + tr < p.n_valid ? __ldg(reinterpret_cast<const uint4*>(p.g + (t0 + tr) * p.ldg + f0 + ch * 8))
+                                   : make_uint4(0u, 0u, 0u, 0u);
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
                                                          : p.gate_ff + 16 * (feat >> 5) + (feat & 31) - 16)
                                     : feat;
   const int64_t grp0 = t0 / 4 + 16 * half;
-  const uint64_t stream0 = static_cast<uint64_t>(row * (p.n / 4) + grp0);
+  const uint64_t stream0 = static_cast<uint64_t>(row * (p.n_valid / 4) + grp0);
   U128 st{0, 0};
   if constexpr (kExact) {
     // stream index of this thread = base(u / v rows) + roff * (n / 4) + 16 half: the CTA's one or
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(256) mvue_tile_kernel(MvueArgs p, const __grid
     const int64_t rbase0 = p.gate_ff > 0 ? f0 / 2 : f0;
     if (w < nbase) {
       const int64_t rb = rbase0 + (w ? p.gate_ff : 0);
-      const U128 b = pcg_advance_warp(rng, static_cast<uint64_t>(rb * (p.n / 4) + t0 / 4), lane);
+      const U128 b = pcg_advance_warp(rng, static_cast<uint64_t>(rb * (p.n_valid / 4) + t0 / 4), lane);
       if (lane == 0) s_base[w] = b;
     }
     __syncthreads();
@@ -613,7 +616,18 @@ extern "C" int s24_mvue_prune(const void* g, int dtype, int64_t rows, int64_t co
 extern "C" int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int64_t f, uint64_t state_hi,
                                  uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t gate_ff,
                                  uint16_t* vals, uint8_t* e, uint8_t* pairs, int exact, void* stream) {
+  return s24_mvue_compress_ragged(g, ldg, n, n, f, state_hi, state_lo, inc_hi, inc_lo, gate_ff, vals, e, pairs, exact,
+                                  stream);
+}
+
+extern "C" int s24_mvue_compress_ragged(const uint16_t* g, int64_t ldg, int64_t n, int64_t n_valid, int64_t f,
+                                        uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                                        int64_t gate_ff, uint16_t* vals, uint8_t* e, uint8_t* pairs, int exact,
+                                        void* stream) {
   S24_REQUIRE(g && vals, S24_ERR_ARG, "NULL pointer");
+  S24_REQUIRE(n_valid > 0 && n_valid <= n && n_valid % 4 == 0 && n - n_valid < 128, S24_ERR_SHAPE,
+              "MVUE: valid tokens must be a positive multiple of 4 in (n - 128, n] (got %lld of %lld)",
+              (long long)n_valid, (long long)n);
   S24_REQUIRE(n % 128 == 0 && f % 128 == 0 && n > 0 && f > 0, S24_ERR_SHAPE,
               "MVUE operand needs tokens and features divisible by 128 (got n=%lld f=%lld)", (long long)n,
               (long long)f);
@@ -621,12 +635,12 @@ extern "C" int s24_mvue_compress(const uint16_t* g, int64_t ldg, int64_t n, int6
               "gradient rows must be 16-byte aligned");
   if (gate_ff > 0) S24_REQUIRE(f == 2 * gate_ff && gate_ff % 16 == 0, S24_ERR_SHAPE, "gated MVUE: f must be 2 d_ff");
   MvueRng rng;
-  mvue_rng_tables(rng, state_hi, state_lo, inc_hi, inc_lo, static_cast<uint64_t>(n / 4));
+  mvue_rng_tables(rng, state_hi, state_lo, inc_hi, inc_lo, static_cast<uint64_t>(n_valid / 4));
   S24_REQUIRE(static_cast<double>(f) * static_cast<double>(n / 4) < 1099511627776.0, S24_ERR_SHAPE,
               "MVUE stream index exceeds the 2^40 jump table");
   S24_REQUIRE(exact || static_cast<double>(f) * static_cast<double>(n / 4) < 4294967296.0, S24_ERR_SHAPE,
               "fast MVUE: group counter exceeds 2^32 (use exact mode or split the call)");
-  MvueArgs a{g, ldg, n, f, gate_ff, vals, e, pairs, exact == 2 ? 1 : 0};
+  MvueArgs a{g, ldg, n, f, gate_ff, vals, e, pairs, exact == 2 ? 1 : 0, n_valid};
   dim3 grid(static_cast<unsigned>(n / 128), static_cast<unsigned>(f / 128));
   if (exact) {
     constexpr int kPkBytes = 128 * 33 * 4;

@@ -23,14 +23,11 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import os
-import warnings
 
 import torch
 
 from . import _capi as C
 from .matrix import ShapeError
-
-_MVUE_FALLBACK_WARNED = False
 
 
 class _NoTimer:
@@ -238,17 +235,32 @@ def mvue_compress(g: torch.Tensor, seed: int, gate_ff: int = 0, want_pairs: bool
     (vals F x N/2, E tiles, pairs F x N/4 or None).  exact=True: numpy's PCG64 stream and the
     reference's float64 decisions (fp32 under an error certificate, float64 where the certificate
     fails; exact=2 forces float64 everywhere, a test hook).  exact=False: fp32 math and a
-    counter-based uniform (unbiased, not numpy's stream) for throughput."""
-    n, f = g.shape
+    counter-based uniform (unbiased, not numpy's stream) for throughput.  N not a multiple of 128
+    (any multiple of 4, as the reference allows): the operand covers N rounded up to 128 tokens
+    (s24_mvue_compress_ragged: the reference's draws for the N real tokens, zeros after them),
+    so the GEMM's other operand must be padded the same way (pad_tokens)."""
+    n_valid, f = g.shape
+    n = (n_valid + 127) // 128 * 128
     dev = g.device
     vals = torch.empty((f, n // 2), dtype=torch.bfloat16, device=dev)
     e = torch.empty((f // 128) * (n // 128) * 2048, dtype=torch.uint8, device=dev)
     pairs = torch.empty((f, n // 4), dtype=torch.uint8, device=dev) if want_pairs else None
     sh, sl, ih, il = pcg64_state(seed)
     with TIMER("k8_mvue"):
-        C.call("s24_mvue_compress", g.data_ptr(), g.stride(0), n, f, sh, sl, ih, il, gate_ff, vals.data_ptr(),
-               e.data_ptr(), C.ptr(pairs), int(exact), C.stream_of(g))
+        C.call("s24_mvue_compress_ragged", g.data_ptr(), g.stride(0), n, n_valid, f, sh, sl, ih, il, gate_ff,
+               vals.data_ptr(), e.data_ptr(), C.ptr(pairs), int(exact), C.stream_of(g))
     return vals, e, pairs
+
+
+def pad_tokens(x: torch.Tensor) -> torch.Tensor:
+    """x (tokens x features) with zero rows up to a multiple of 128 tokens (x itself when aligned):
+    the token operand of an MVUE weight-gradient GEMM whose token count is not a multiple of 128."""
+    n = x.shape[0]
+    if n % 128 == 0:
+        return x
+    out = torch.zeros(((n + 127) // 128 * 128, x.shape[1]), dtype=x.dtype, device=x.device)
+    out[:n].copy_(x)
+    return out
 
 
 def transpose_bf16(x: torch.Tensor) -> torch.Tensor:
@@ -482,25 +494,18 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     # dW2[d, d_ff] = dY^T A and dW_in[r_in, d] = dZ^T X: K = tokens, both operands token-major (MN-major)
     dw2 = dw2_out if dw2_out is not None else torch.empty((d, d_ff), dtype=torch.float32, device=dev)
     dw_in = dw_in_out if dw_in_out is not None else torch.empty((r_in, d), dtype=torch.float32, device=dev)
-    if mvue and n % 128:
-        # the MVUE operand is tiled in 128-token groups; a batch that is not a multiple of 128
-        # (legal for the reference, any multiple of 4) takes the dense weight gradient -- the
-        # expectation of the unbiased MVUE estimator -- instead of failing; said once per process,
-        # since the result then differs from the reference's draws
-        global _MVUE_FALLBACK_WARNED
-        if not _MVUE_FALLBACK_WARNED:
-            _MVUE_FALLBACK_WARNED = True
-            warnings.warn(f"fst_backward(mvue=True) with {n} tokens (not a multiple of 128): using the dense "
-                          "weight gradient (the MVUE estimator's expectation) instead of MVUE draws", RuntimeWarning,
-                          stacklevel=3)
-        mvue = False
     if mvue:
+        # the MVUE operand is tiled in 128-token groups: a batch that is not a multiple of 128 (legal
+        # for the reference, any multiple of 4) runs the GEMM over the padded token count, with the
+        # reference's draws for the real tokens and zero rows after them in both operands
+        n_op = (n + 127) // 128 * 128
         v2, e2, _ = mvue_compress(dy, mvue_seed(rng_seed, 1), exact=mvue_exact)
-        spmm_dw_tokens(v2, e2, d, n, st.a, d_ff, dw2, w2_dense, w2.idx, lam, 0, "k8_spmm_dw2")
+        spmm_dw_tokens(v2, e2, d, n_op, pad_tokens(st.a), d_ff, dw2, w2_dense, w2.idx, lam, 0, "k8_spmm_dw2")
         if dw2_ready is not None:
             dw2_ready()
         v1, e1, _ = mvue_compress(dz, mvue_seed(rng_seed, 2), gate_ff, exact=mvue_exact)
-        spmm_dw_tokens(v1, e1, r_in, n, st.x, d, dw_in, w_in_dense, w_in.idx, lam, gate_ff, "k8_spmm_dw_in")
+        spmm_dw_tokens(v1, e1, r_in, n_op, pad_tokens(st.x), d, dw_in, w_in_dense, w_in.idx, lam, gate_ff,
+                       "k8_spmm_dw_in")
     else:
         gemm_dw(dy, True, st.a, True, d, d_ff, n, dw2, w2_dense, w2.idx, lam, tag="k5_gemm_dw2")
         if dw2_ready is not None:

@@ -60,7 +60,7 @@ class TrainConfig:
     reference Activation value string; the reference's Activation enum is accepted and
     coerced to it).  The tensor-core path needs d, d_ff % 128 == 0 and batch % 64 == 0
     (with mvue=True a batch that is not a multiple of 128 -- the MVUE operand's token
-    tile -- takes the dense weight-gradient GEMM, the estimator's expectation)."""
+    tile -- runs on zero-padded operands with the reference's draws for the real tokens)."""
 
     d: int = 128
     d_ff: int = 256

@@ -149,24 +149,27 @@ def test_module_gradient_accumulation_and_refresh_guard():
 
 def test_mvue_batch_not_multiple_of_128():
     """ADVICE: mvue=True with a batch that is a multiple of 64 but not of 128 (legal for the
-    reference) takes the dense weight gradient instead of failing, and says so once."""
+    reference) runs the MVUE weight gradient on padded operands -- no fallback, no warning -- and
+    stays an unbiased estimate of the dense gradient (exact draws: test_gpu_ffn)."""
+    import warnings
+
     import paper_2404_01847_b200 as P
-    from paper_2404_01847_b200 import engine as E
 
     d, d_ff, n = 128, 256, 64
     c = _case("gelu", d, d_ff, n, seed=13)
     layer = P.FFNLayer(to_dev_bf16(c["w_in"]), to_dev_bf16(c["bias_in"]), to_dev_bf16(c["w2"]), P.Activation.GELU)
     masks = P.search_layer_masks(layer)
     f = P.fst_forward(layer, to_dev_bf16(c["x"]), masks)
-    E._MVUE_FALLBACK_WARNED = False
-    with pytest.warns(RuntimeWarning, match="not a multiple of 128"):
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
         g = P.fst_backward(f, to_dev_bf16(c["dy"]), mvue=True)
-    lo = o.Layer(c["w_in"], c["bias_in"], c["w2"], "gelu")
-    mi, mo = o.transposable_search_conv(c["w_in"]), o.transposable_search_conv(c["w2"])
-    fr = o.fst_forward(lo, c["x"], mi, mo, exact=False)
-    br = o.fst_backward(lo, fr, c["dy"], mi, mo, exact=False)
-    assert normwise_rel(g.d_w1.cpu().numpy(), br["dw_in"]) < TOL
-    assert normwise_rel(g.d_w2.cpu().numpy(), br["dw2"]) < TOL
+        gd = P.fst_backward(f, to_dev_bf16(c["dy"]), mvue=False)
+    w1, w2 = g.d_w1.cpu().numpy(), g.d_w2.cpu().numpy()
+    assert np.isfinite(w1).all() and np.isfinite(w2).all()
+    assert not np.array_equal(w2, gd.d_w2.cpu().numpy())  # MVUE draws, not the dense gradient
+    # half the entries of every 4-token group kept: the estimate's 2:4 structure along tokens
+    # shows as a visible but bounded deviation from the dense gradient
+    assert normwise_rel(w2, gd.d_w2.cpu().numpy()) < 4.0
 
 
 # ---------------------------------------------------------------------------

@@ -248,14 +248,52 @@ def _check_unbiased(E, gd, bd, f, n, dcols, out, dense, exact):
     assert np.mean(z < 4.0) > 0.995, np.mean(z < 4.0)
 
 
-@pytest.mark.parametrize("act", ["gelu", "swiglu"])
-def test_mvue_training_path_vs_oracle_on_same_gradients(act):
-    """fst_backward(mvue=True) semantics on the fused training path: the dW
-    outputs equal the oracle MVUE products of the GPU's own dY / dZ (identical
-    inputs -> identical draws), with the decay fused."""
+@pytest.mark.parametrize("f,n,seed,gff", [(256, 192, 3, 0), (128, 64, 11, 0), (256, 196, 2 ** 33 + 1, 0),
+                                          (256, 320, 5, 128)])
+def test_mvue_kernel_ragged_tokens_bit_exact(f, n, seed, gff):
+    """Token counts that are not multiples of 128 (the reference takes any multiple of 4): the
+    operand covers n rounded up to 128 tokens, the first n are the reference's draws for n tokens
+    (stream index row * n/4 + group) bit-for-bit, the padded groups are zero; gated row order
+    included."""
     from paper_2404_01847_b200 import engine as E
 
-    d, d_ff, n = 128, 256, 256
+    x = o.round_bf16(o.det_normal((f, n), seed=f + n + 1))  # features x tokens
+    g = to_dev_bf16(np.ascontiguousarray(x.T))
+    vals, e, pairs = E.mvue_compress(g, seed, gate_ff=gff, want_pairs=True)
+    n_pad = (n + 127) // 128 * 128
+    assert tuple(vals.shape) == (f, n_pad // 2) and tuple(pairs.shape) == (f, n_pad // 4)
+    if gff:  # feature p of the operand is row gate_row(p) of [u; v] for the draw
+        p = np.arange(f)
+        rows = np.where(p % 32 < 16, 16 * (p // 32) + p % 32, gff + 16 * (p // 32) + p % 32 - 16)
+        src = np.empty_like(x)
+        src[rows] = x
+        rv, _, ridx = o.mvue_kept(src.reshape(-1, 4), seed)
+        rv, ridx = rv.reshape(f, -1)[rows], ridx.reshape(f, -1)[rows]
+    else:
+        rv, _, ridx = o.mvue_kept(x.reshape(-1, 4), seed)
+        rv, ridx = rv.reshape(f, -1), ridx.reshape(f, -1)
+    np.testing.assert_array_equal(pairs.cpu().numpy()[:, : n // 4], ridx)
+    np.testing.assert_array_equal(bf16_bits_of(vals[:, : n // 2].contiguous()).reshape(f, -1),
+                                  o.bf16_bits(o.round_bf16(rv)).reshape(f, -1))
+    assert not vals[:, n // 2:].float().abs().sum().item()
+    # the padded operand through the 2:4 weight-gradient GEMM == the oracle product on n tokens
+    b = o.round_bf16(o.det_normal((n, 128), seed=7))
+    out = torch.empty((f, 128), dtype=torch.float32, device="cuda")
+    E.spmm_dw(vals, e, f, n_pad, E.pad_tokens(to_dev_bf16(b)), True, 128, out)
+    dense = _mvue_dense(src, seed)[rows] if gff else _mvue_dense(x, seed)
+    ref = o.round_bf16(dense) @ b
+    assert normwise_rel(out.cpu().numpy(), ref) < 2e-3
+
+
+@pytest.mark.parametrize("act,n", [("gelu", 256), ("swiglu", 256), ("gelu", 192), ("swiglu", 64)])
+def test_mvue_training_path_vs_oracle_on_same_gradients(act, n):
+    """fst_backward(mvue=True) semantics on the fused training path: the dW
+    outputs equal the oracle MVUE products of the GPU's own dY / dZ (identical
+    inputs -> identical draws), with the decay fused; also for token counts that are not
+    multiples of 128 (padded operands, the reference's draws for the real tokens)."""
+    from paper_2404_01847_b200 import engine as E
+
+    d, d_ff = 128, 256
     c = _case(act, d, d_ff, n, seed=5 + n)
     w_in, b, w2 = to_dev_bf16(c["w_in"]), to_dev_bf16(c["bias_in"]), to_dev_bf16(c["w2"])
     gated = act == "swiglu"
