@@ -451,7 +451,8 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
                  lam: float = 0.0, dw_in_out: torch.Tensor | None = None,
                  dw2_out: torch.Tensor | None = None, mvue: bool = False, rng_seed: int = 0,
                  mvue_exact: bool = True, dbias_out: torch.Tensor | None = None,
-                 grads_ready=None, dx_accumulate: torch.Tensor | None = None, dw2_ready=None) -> Grads:
+                 grads_ready=None, dx_accumulate: torch.Tensor | None = None, dw2_ready=None,
+                 n_valid: int | None = None) -> Grads:
     """dA = dY W2~ (out_bwd, W2's transposed orientation) -> dZ (activation
     backward, bias gradient) -> dX = dZ W_in~ (in_bwd); dense dW2 = dY^T A and
     dW_in = dZ^T X with the masked decay lam (1 - M) W fused (gated_ffn.py:327-356).
@@ -466,7 +467,9 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
     dbias_out / dw_in_out / dw2_out let the caller hand in views of that bucket.
     dx_accumulate: a residual stream's gradient buffer; dX is added into it by the dX GEMM's
     store (S24_EPI_STORE_ADD) instead of being written to a fresh tensor.  It may be `dy`
-    itself: every reader of dy is enqueued before the dX GEMM on the same stream."""
+    itself: every reader of dy is enqueued before the dX GEMM on the same stream.
+    n_valid: the caller padded the token batch with zero rows to a multiple of 64 (gated_ffn);
+    the MVUE draws then cover the first n_valid tokens, as the reference's do for its batch."""
     n, d = st.x.shape
     r_in, d_ff = w_in.rows, w2.cols
     if tuple(dy.shape) != (n, d):
@@ -499,11 +502,12 @@ def ffn_backward(st: FwdState, dy: torch.Tensor, w_in: CompressedOperand, w2: Co
         # for the reference, any multiple of 4) runs the GEMM over the padded token count, with the
         # reference's draws for the real tokens and zero rows after them in both operands
         n_op = (n + 127) // 128 * 128
-        v2, e2, _ = mvue_compress(dy, mvue_seed(rng_seed, 1), exact=mvue_exact)
+        nv = n if n_valid is None else n_valid
+        v2, e2, _ = mvue_compress(dy[:nv], mvue_seed(rng_seed, 1), exact=mvue_exact)
         spmm_dw_tokens(v2, e2, d, n_op, pad_tokens(st.a), d_ff, dw2, w2_dense, w2.idx, lam, 0, "k8_spmm_dw2")
         if dw2_ready is not None:
             dw2_ready()
-        v1, e1, _ = mvue_compress(dz, mvue_seed(rng_seed, 2), gate_ff, exact=mvue_exact)
+        v1, e1, _ = mvue_compress(dz[:nv], mvue_seed(rng_seed, 2), gate_ff, exact=mvue_exact)
         spmm_dw_tokens(v1, e1, r_in, n_op, pad_tokens(st.x), d, dw_in, w_in_dense, w_in.idx, lam, gate_ff,
                        "k8_spmm_dw_in")
     else:

@@ -180,6 +180,22 @@ class FstActivations:
     state: "E.FwdState | E.FwdStateF32 | None" = None
 
 
+def _pad_tokens64(t: torch.Tensor) -> torch.Tensor:
+    """t (tokens x features) with zero rows up to a multiple of 64 tokens (the tensor-core path's
+    token granule; the reference takes any batch).  Zero tokens leave every real output and, with a
+    zero upstream gradient, every gradient sum unchanged; their own outputs are dropped."""
+    n = t.shape[0]
+    if n % 64 == 0:
+        return t
+    out = torch.zeros(((n + 63) // 64 * 64, t.shape[1]), dtype=t.dtype, device=t.device)
+    out[:n].copy_(t)
+    return out
+
+
+def _head(t, n: int):
+    return None if t is None or t.shape[0] == n else t[:n]
+
+
 def _as_bf16(t: torch.Tensor) -> torch.Tensor:
     C.require_cuda(t)
     return t if t.dtype == torch.bfloat16 else t.to(torch.bfloat16)
@@ -225,17 +241,24 @@ def fst_forward(layer: FFNLayer, x: torch.Tensor, masks: FFNMasks | None,
     x = _as_bf16(x)
     if x.dim() != 2 or x.shape[1] != layer.d:
         raise ShapeError(f"x shape {tuple(x.shape)} does not match layer width {layer.d}")
+    n = x.shape[0]
+    xp = _pad_tokens64(x)
+
+    def bundle(st, m):
+        if xp is x:
+            return FstActivations(layer, x, st.z, st.a, st.y, m, layer.w_in_cat, st)
+        return FstActivations(layer, x, _head(st.z, n), _head(st.a, n), _head(st.y, n), m, layer.w_in_cat, st)
+
     if masks is None:
         w_in, w2 = _dense_ops(layer)
-        st = E.ffn_forward(x, w_in, _as_bf16(layer.bias_in_cat), w2, layer.activation.value)
-        return FstActivations(layer, x, st.z, st.a, st.y, None, layer.w_in_cat, st)
+        return bundle(E.ffn_forward(xp, w_in, _as_bf16(layer.bias_in_cat), w2, layer.activation.value), None)
     if masks.w_in.shape != tuple(layer.w_in_cat.shape) or masks.w_out.shape != tuple(layer.w2.shape):
         raise ShapeError("mask shapes do not match layer weights")
     ops = masks.plans(layer)
     E.compress_values(layer.w_in_cat, ops["in"])
     E.compress_values(layer.w2, ops["out"])
-    st = E.ffn_forward(x, ops["in"], _as_bf16(layer.bias_in_cat), ops["out"], layer.activation.value)
-    return FstActivations(layer, x, st.z, st.a, st.y, masks, layer.w_in_cat, st)
+    return bundle(E.ffn_forward(xp, ops["in"], _as_bf16(layer.bias_in_cat), ops["out"], layer.activation.value),
+                  masks)
 
 
 def fst_backward(bundle: FstActivations, upstream: torch.Tensor, rng_seed: int = 0, mvue: bool = True,
@@ -261,13 +284,15 @@ def fst_backward(bundle: FstActivations, upstream: torch.Tensor, rng_seed: int =
     up = _as_bf16(upstream)
     if tuple(up.shape) != tuple(bundle.y.shape):
         raise ShapeError(f"upstream shape {tuple(up.shape)} != output shape {tuple(bundle.y.shape)}")
+    n = up.shape[0]
+    up = _pad_tokens64(up)  # zero upstream rows for the padded tokens (fst_forward)
     if bundle.masks is None:
-        return _dense_backward(bundle, up)
+        return _dense_backward(bundle, up, n)
     ops = bundle.masks.plans(layer)
     g = E.ffn_backward(bundle.state, up, ops["in"], ops["out"], layer.activation.value,
                        w_in_dense=layer.w_in_cat, w2_dense=layer.w2, lam=decay_lambda, mvue=mvue,
-                       rng_seed=rng_seed)
-    return _pack_grads(layer, g.dx, g.dw_in, g.dbias_in, g.dw2)
+                       rng_seed=rng_seed, n_valid=n)
+    return _pack_grads(layer, g.dx[:n] if g.dx.shape[0] != n else g.dx, g.dw_in, g.dbias_in, g.dw2)
 
 
 def _pack_grads(layer, dx, dw_in, dbias, dw2) -> LayerGrads:
@@ -286,13 +311,13 @@ def _dense_ops(layer: FFNLayer):
             E.DenseOperand.of(_as_bf16(layer.w2).contiguous()))
 
 
-def _dense_backward(bundle: FstActivations, up: torch.Tensor) -> LayerGrads:
+def _dense_backward(bundle: FstActivations, up: torch.Tensor, n: int) -> LayerGrads:
     """masks=None backward (gated_ffn.py:304-364 on the dense route): dense tensor-core dA / dX
     GEMMs, K7 for the activation and bias gradients, the dense dW GEMMs (no decay)."""
     layer = bundle.layer
     w_in, w2 = _dense_ops(layer)
     g = E.ffn_backward(bundle.state, up, w_in, w2, layer.activation.value)
-    return _pack_grads(layer, g.dx, g.dw_in, g.dbias_in, g.dw2)
+    return _pack_grads(layer, g.dx[:n] if g.dx.shape[0] != n else g.dx, g.dw_in, g.dbias_in, g.dw2)
 
 
 def geglu_forward(x, u, v, b, c, traversal: Traversal = Traversal.COL_ORDER) -> torch.Tensor:

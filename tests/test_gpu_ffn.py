@@ -32,8 +32,10 @@ def _case(act, d, d_ff, n, seed):
 
 
 @pytest.mark.parametrize("act", ["gelu", "geglu", "relu", "swiglu"])
-@pytest.mark.parametrize("d,d_ff,n", [(128, 256, 128), (256, 512, 192)])
+@pytest.mark.parametrize("d,d_ff,n", [(128, 256, 128), (256, 512, 192), (128, 256, 100), (128, 128, 4)])
 def test_fst_fwd_bwd_vs_oracle(act, d, d_ff, n):
+    """fst_forward / fst_backward vs the float64 oracle; token counts that are not multiples of 64
+    (the reference takes any batch) run on zero-padded tokens."""
     import paper_2404_01847_b200 as P
 
     c = _case(act, d, d_ff, n, seed=d + d_ff + n)
@@ -57,6 +59,25 @@ def test_fst_fwd_bwd_vs_oracle(act, d, d_ff, n):
     db = torch.cat([g.d_b, g.d_c]) if layer.is_gated else g.d_b
     assert normwise_rel(dw_in.cpu().numpy(), br["dw_in"]) < TOL
     assert normwise_rel(db.cpu().numpy(), br["dbias_in"]) < TOL
+
+
+@pytest.mark.parametrize("act,n", [("gelu", 100), ("geglu", 36)])
+def test_fst_backward_mvue_ragged_batch_reference_draws(act, n):
+    """fst_backward(mvue=True) (the reference default) at a batch that is not a multiple of 64:
+    dW2 = MVUE(dY^T, the reference's draws for n tokens) A, on the zero-padded tensor-core path."""
+    import paper_2404_01847_b200 as P
+
+    d, d_ff = 128, 256
+    c = _case(act, d, d_ff, n, seed=77 + n)
+    layer = P.FFNLayer(to_dev_bf16(c["w_in"]), to_dev_bf16(c["bias_in"]), to_dev_bf16(c["w2"]), P.Activation(act))
+    masks = P.search_layer_masks(layer)
+    f = P.fst_forward(layer, to_dev_bf16(c["x"]), masks)
+    assert f.y.shape == (n, d) and f.a.shape == (n, d_ff)
+    g = P.fst_backward(f, to_dev_bf16(c["dy"]), rng_seed=9, mvue=True)
+    assert g.d_x.shape == (n, d)
+    a = f.a.double().cpu().numpy()
+    ref2 = o.round_bf16(_mvue_dense(np.ascontiguousarray(c["dy"].T), o.mvue_seed(9, 1))) @ a
+    assert normwise_rel(g.d_w2.cpu().numpy(), ref2) < 5e-3
 
 
 def test_fused_masked_decay_matches_oracle():
