@@ -252,13 +252,15 @@ def mvue_compress(g: torch.Tensor, seed: int, gate_ff: int = 0, want_pairs: bool
     return vals, e, pairs
 
 
-def pad_tokens(x: torch.Tensor) -> torch.Tensor:
-    """x (tokens x features) with zero rows up to a multiple of 128 tokens (x itself when aligned):
-    the token operand of an MVUE weight-gradient GEMM whose token count is not a multiple of 128."""
+def pad_tokens(x: torch.Tensor, granule: int = 128) -> torch.Tensor:
+    """x (tokens x features) with zero rows up to a multiple of `granule` tokens (x itself when
+    aligned): 128 for the token operand of an MVUE weight-gradient GEMM, 64 for a batch entering
+    the tensor-core path (the reference takes any batch; zero tokens change no real output and,
+    with a zero upstream gradient, no gradient sum)."""
     n = x.shape[0]
-    if n % 128 == 0:
+    if n % granule == 0:
         return x
-    out = torch.zeros(((n + 127) // 128 * 128, x.shape[1]), dtype=x.dtype, device=x.device)
+    out = torch.zeros(((n + granule - 1) // granule * granule, x.shape[1]), dtype=x.dtype, device=x.device)
     out[:n].copy_(x)
     return out
 

@@ -181,15 +181,8 @@ class FstActivations:
 
 
 def _pad_tokens64(t: torch.Tensor) -> torch.Tensor:
-    """t (tokens x features) with zero rows up to a multiple of 64 tokens (the tensor-core path's
-    token granule; the reference takes any batch).  Zero tokens leave every real output and, with a
-    zero upstream gradient, every gradient sum unchanged; their own outputs are dropped."""
-    n = t.shape[0]
-    if n % 64 == 0:
-        return t
-    out = torch.zeros(((n + 63) // 64 * 64, t.shape[1]), dtype=t.dtype, device=t.device)
-    out[:n].copy_(t)
-    return out
+    """Zero token rows up to the tensor-core path's 64-token granule (E.pad_tokens)."""
+    return E.pad_tokens(t, 64)
 
 
 def _head(t, n: int):

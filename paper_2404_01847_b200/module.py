@@ -38,13 +38,15 @@ class _SparseFFNFn(torch.autograd.Function):
     def forward(ctx, x, w_in, bias_in, w2, mod, dense_ops):
         xb = x if x.dtype == torch.bfloat16 else x.to(torch.bfloat16)
         op_in, op_out = dense_ops if dense_ops is not None else (mod.op_in, mod.op_out)
-        st = E.ffn_forward(xb, op_in, bias_in.to(torch.bfloat16), op_out, mod.act, fused=True)
+        n = xb.shape[0]  # any token count: zero-padded to the 64-token granule, outputs sliced
+        st = E.ffn_forward(E.pad_tokens(xb, 64), op_in, bias_in.to(torch.bfloat16), op_out, mod.act, fused=True)
+        ctx.n = n
         ctx.mod = mod
         ctx.st = st
         ctx.ops = (op_in, op_out)
         ctx.mask_version = mod.mask_version
         ctx.save_for_backward(w_in, w2)
-        return st.y
+        return st.y if st.y.shape[0] == n else st.y[:n]
 
     @staticmethod
     def backward(ctx, dy):
@@ -61,17 +63,19 @@ class _SparseFFNFn(torch.autograd.Function):
         # gradient accumulation (.grad already set) autograd adds the fresh gradients in place
         direct = all(p.grad is None for p in params)
         b = mod.grad_bucket() if direct else None
-        g = E.ffn_backward(ctx.st, dy.to(torch.bfloat16), op_in, op_out, mod.act, w_in_dense=w_in,
+        n = ctx.n
+        g = E.ffn_backward(ctx.st, E.pad_tokens(dy.to(torch.bfloat16), 64), op_in, op_out, mod.act, w_in_dense=w_in,
                            w2_dense=w2, lam=0.0 if dense else mod.decay_lambda, mvue=mod.mvue and not dense,
                            rng_seed=mod.mvue_seed, mvue_exact=mod.mvue_exact,
                            dw_in_out=b.views[0] if direct else None, dbias_out=b.views[1] if direct else None,
-                           dw2_out=b.views[2] if direct else None)
+                           dw2_out=b.views[2] if direct else None, n_valid=n)
         ctx.st = None
+        dx = g.dx if g.dx.shape[0] == n else g.dx[:n]
         if direct:
             for p, v in zip(params, b.views):
                 p.grad = v
-            return g.dx, None, None, None, None, None
-        return g.dx, g.dw_in, g.dbias_in, g.dw2, None, None
+            return dx, None, None, None, None, None
+        return dx, g.dw_in, g.dbias_in, g.dw2, None, None
 
 
 class SparseFFN(torch.nn.Module):

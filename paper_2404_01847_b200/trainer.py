@@ -58,9 +58,9 @@ _ACTS = {"gelu": "gelu", "geglu": "geglu", "relu": "relu", "swiglu": "swiglu"}
 class TrainConfig:
     """trainer.py:73-152 (field names and defaults of the reference; `activation` is the
     reference Activation value string; the reference's Activation enum is accepted and
-    coerced to it).  The tensor-core path needs d, d_ff % 128 == 0 and batch % 64 == 0
-    (with mvue=True a batch that is not a multiple of 128 -- the MVUE operand's token
-    tile -- runs on zero-padded operands with the reference's draws for the real tokens)."""
+    coerced to it).  The tensor-core path needs d, d_ff % 128 == 0; the batch is any multiple
+    of 4 like the reference's (MVUE groups 4 tokens): it is zero-padded to the 64-token granule
+    of the GEMMs (and to 128 for the MVUE operand, the reference's draws for the real tokens)."""
 
     d: int = 128
     d_ff: int = 256
@@ -92,8 +92,8 @@ class TrainConfig:
         for name in ("d", "d_ff"):
             if getattr(self, name) % 128 != 0:
                 raise ShapeError(f"{name} must be divisible by 128 on the tensor-core path")
-        if self.batch % 64 != 0:
-            raise ShapeError("batch must be divisible by 64 on the tensor-core path")
+        if self.batch < 4 or self.batch % 4 != 0:
+            raise ShapeError("batch must be a positive multiple of 4 (MVUE groups of 4 tokens)")
         for name in ("dense_ft_fraction", "dense_pretrain_fraction", "warmup_fraction"):
             frac = getattr(self, name)
             if not (0.0 <= frac < 1.0):

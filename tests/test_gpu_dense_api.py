@@ -305,3 +305,17 @@ def test_train_config_accepts_activation_enum_and_block_stats():
     assert art.block_stats is not None and len(art.block_stats) == 2
     name, tr = art.block_stats[0]
     assert name == "block0.w_in" and tr.block_flips.numel() == (128 // 4) * (128 // 4)
+
+
+def test_run_training_small_batch_like_the_reference():
+    """TrainConfig takes any batch that is a multiple of 4 (the reference's tests use 4 .. 16):
+    the tokens are zero-padded to the tensor-core granule, MVUE (the default) draws over the real
+    batch; the loop runs and its losses stay finite."""
+    import paper_2404_01847_b200 as P
+
+    with pytest.raises(P.ShapeError):
+        P.TrainConfig(d=128, d_ff=128, batch=6)
+    cfg = P.TrainConfig(d=128, d_ff=128, depth=2, batch=12, steps=8, activation=P.Activation.GEGLU,
+                        decay=P.DecayConfig(lambda_w=6e-5, refresh_period=3))
+    art = P.run_training(cfg)
+    assert art.losses.shape == (8,) and np.isfinite(art.losses).all() and np.isfinite(art.final_eval_loss)
