@@ -186,7 +186,8 @@ def _pad_tokens64(t: torch.Tensor) -> torch.Tensor:
 
 
 def _head(t, n: int):
-    return None if t is None or t.shape[0] == n else t[:n]
+    """The first n token rows of a (possibly padded) activation, or t itself (None included)."""
+    return t if t is None or t.shape[0] == n else t[:n]
 
 
 def _as_bf16(t: torch.Tensor) -> torch.Tensor:
@@ -238,8 +239,6 @@ def fst_forward(layer: FFNLayer, x: torch.Tensor, masks: FFNMasks | None,
     xp = _pad_tokens64(x)
 
     def bundle(st, m):
-        if xp is x:
-            return FstActivations(layer, x, st.z, st.a, st.y, m, layer.w_in_cat, st)
         return FstActivations(layer, x, _head(st.z, n), _head(st.a, n), _head(st.y, n), m, layer.w_in_cat, st)
 
     if masks is None:
@@ -285,7 +284,7 @@ def fst_backward(bundle: FstActivations, upstream: torch.Tensor, rng_seed: int =
     g = E.ffn_backward(bundle.state, up, ops["in"], ops["out"], layer.activation.value,
                        w_in_dense=layer.w_in_cat, w2_dense=layer.w2, lam=decay_lambda, mvue=mvue,
                        rng_seed=rng_seed, n_valid=n)
-    return _pack_grads(layer, g.dx[:n] if g.dx.shape[0] != n else g.dx, g.dw_in, g.dbias_in, g.dw2)
+    return _pack_grads(layer, _head(g.dx, n), g.dw_in, g.dbias_in, g.dw2)
 
 
 def _pack_grads(layer, dx, dw_in, dbias, dw2) -> LayerGrads:
@@ -310,7 +309,7 @@ def _dense_backward(bundle: FstActivations, up: torch.Tensor, n: int) -> LayerGr
     layer = bundle.layer
     w_in, w2 = _dense_ops(layer)
     g = E.ffn_backward(bundle.state, up, w_in, w2, layer.activation.value)
-    return _pack_grads(layer, g.dx[:n] if g.dx.shape[0] != n else g.dx, g.dw_in, g.dbias_in, g.dw2)
+    return _pack_grads(layer, _head(g.dx, n), g.dw_in, g.dbias_in, g.dw2)
 
 
 def geglu_forward(x, u, v, b, c, traversal: Traversal = Traversal.COL_ORDER) -> torch.Tensor:
